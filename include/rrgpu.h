@@ -1,0 +1,202 @@
+/*
+ * rrgpu.h -- C ABI of the B200-native IMM hot path (librrgpu.so).
+ *
+ * Drop-in boundary for the reference rrflow 0.1.0 (/root/reference/proj/include/rrflow).
+ * The reference has no FFI; its operator API is a set of free C++ functions.
+ * Each entry point below replaces one of them (file:line cited per symbol) with the
+ * same argument meaning, slot/stream semantics, side effects and error classes:
+ *   RRG_EINVAL <-> std::invalid_argument, RRG_ENOMEM <-> BatchOutOfMemory /
+ *   std::bad_alloc, RRG_ECUDA <-> std::runtime_error. Messages via rrg_last_error().
+ * The C++17 adapter include/rrgpu/rrgpu.hpp maps these back onto exceptions and
+ * reference-shaped types; INTEGRATION.md shows the caller-side switch.
+ *
+ * All calls are synchronous at return (the reference's WorkPool barrier semantics,
+ * work_pool.hpp:14-19). Host arrays are borrowed for the duration of a call.
+ * A graph and the stores created on it are NOT thread-safe (one orchestrator
+ * thread, as SPEC.md:420 states for the reference driver).
+ */
+#ifndef RRGPU_H
+#define RRGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { RRG_OK = 0, RRG_EINVAL = 1, RRG_ENOMEM = 2, RRG_ECUDA = 3 } rrg_status;
+
+/* rrflow::DiffusionModel (graph.hpp:19) */
+typedef enum { RRG_IC = 0, RRG_LT = 1 } rrg_model;
+
+typedef struct rrg_graph rrg_graph; /* device-resident transpose CSR (rrflow::Graph, graph.hpp:34-59) */
+typedef struct rrg_store rrg_store; /* RRRStore + fused Counter (rrr_store.hpp:20-120, counter.hpp:15-62) */
+
+/* ---- graph ---------------------------------------------------------------
+ * Replaces the transpose view of rrflow::Graph (graph.hpp:45-47): reverse_offsets
+ * u64[n+1], reverse_sources u32[m], reverse_weights f32[m], in the reference's
+ * in-list order (graph.hpp:96-113), which is the draw order. m must be < 2^32.
+ * n == 0 is accepted here; sampling on it fails like generate_batch (sampling.hpp:165). */
+rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* rev_offsets,
+                            const uint32_t* rev_sources, const float* rev_weights,
+                            rrg_graph** out);
+void rrg_graph_destroy(rrg_graph* g);
+/* Builds the per-model device layout up front (otherwise done on first use):
+ * IC -> interleaved {source, weight} records; LT -> sequential fp64 CDF (K0). */
+rrg_status rrg_graph_prepare(rrg_graph* g, rrg_model model);
+/* Runs every subsequent call of this graph and its stores on `cuda_stream`
+ * (a cudaStream_t; NULL restores the graph's private stream). */
+rrg_status rrg_graph_set_stream(rrg_graph* g, void* cuda_stream);
+uint32_t rrg_graph_num_vertices(const rrg_graph* g);
+uint64_t rrg_graph_num_edges(const rrg_graph* g);
+
+/* Tuning knobs; none changes any output bit. */
+typedef enum {
+  RRG_OPT_LT_SCAN = 0,  /* 0 = linear CDF scan (reference trip count), 1 = binary search */
+  RRG_OPT_LT_COOP_MIN = 1, /* in-list length from which LT scans go warp-cooperative */
+  RRG_OPT_IC_INNER = 2  /* IC edge steps per scheduling round (1..64) */
+} rrg_option;
+rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value);
+
+/* ---- store -------------------------------------------------------------- */
+rrg_status rrg_store_create(rrg_graph* g, rrg_store** out);
+void rrg_store_destroy(rrg_store* s);
+/* Drops every set and zeroes the fused counter. */
+rrg_status rrg_store_clear(rrg_store* s);
+/* RRRStore::size / total_member_count / max_set_size (rrr_store.hpp:29, :100-110) */
+rrg_status rrg_store_info(const rrg_store* s, uint64_t* sets, uint64_t* members,
+                          uint32_t* max_set_size);
+
+/* ---- sampling: generate_batch (sampling.hpp:159-199) --------------------
+ * Appends exactly `count` sets at slots [size, size+count); set j is sampled from
+ * stream derive_stream_seed(run_seed, j) (sampling.hpp:179, prng.hpp:17-20), so the
+ * sets are bit-identical to the reference's. fused != 0 adds every member to the
+ * store's occurrence counter (sampling.hpp:184-186). density_divisor only selects
+ * the reference's in-memory representation (rrr_set.hpp:73-90) and changes no
+ * output; it is accepted for signature parity. On RRG_ENOMEM, *sets_generated holds
+ * the number of sets that were appended (BatchOutOfMemory, sampling.hpp:148-154). */
+rrg_status rrg_generate_batch(rrg_graph* g, rrg_model model, uint64_t run_seed, uint64_t count,
+                              rrg_store* s, int fused, uint32_t density_divisor,
+                              uint64_t* sets_generated);
+
+/* Per-call counters of the last rrg_generate_batch on this graph. */
+typedef struct {
+  uint64_t sets;               /* sets appended */
+  uint64_t members;            /* members appended */
+  uint64_t edges_inspected;    /* reference-equivalent in-edges inspected */
+  uint64_t entries_read;       /* adjacency entries the kernels actually loaded */
+  uint64_t deferred;           /* sets routed to the big-set path */
+  float sample_ms;             /* device time of the sampler kernels (CUDA events) */
+  float total_ms;              /* device time of the whole call incl. compaction */
+} rrg_batch_stats;
+rrg_status rrg_last_batch_stats(const rrg_graph* g, rrg_batch_stats* out);
+
+/* ---- selection: select_seeds (selection.hpp:209-243) ---------------------
+ * k in [1, n] else RRG_EINVAL (:213-214). Revives every set first (:215). With
+ * use_prebuilt the fused counter is the starting tally (:217-218), else it is
+ * recounted (build_counter, :79-95). k greedy rounds run on the device with no host
+ * round-trip: argmax with ties to the lowest id (:100-125), exhaustion fill with the
+ * lowest unselected ids at zero gain (:61-72), decrement through an on-device
+ * inverted index (:130-156). adaptive_threshold picks decrement vs rebuild in the
+ * reference (:228-231); both are observationally identical (test_selection.cpp:116-137)
+ * and the device always decrements, so it changes no output.
+ * seeds u32[k], marginals u64[k]; round_counters (nullable) u64[k*n] receives the
+ * per-round counter snapshots (SelectionStats::capture_round_counters, :237-239).
+ * *rounds_done (nullable) = rounds that produced a snapshot. The store stays
+ * tombstoned: *covered_total (nullable) = size - live_count (imm.hpp:194-195). */
+rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double adaptive_threshold, int use_prebuilt,
+                            uint32_t* seeds, uint64_t* marginals, uint64_t* round_counters,
+                            uint32_t* rounds_done, uint64_t* covered_total);
+
+/* fraction_covered (selection.hpp:340-358) */
+rrg_status rrg_fraction_covered(rrg_store* s, const uint32_t* seeds, uint32_t nseeds,
+                                double* out);
+
+/* ---- IMM driver: run_imm (imm.hpp:214-251) -------------------------------- */
+typedef struct {
+  uint32_t k;                 /* ImmConfig defaults (imm.hpp:27-36): 50 */
+  double epsilon;             /* 0.5 */
+  int model;                  /* RRG_IC */
+  uint32_t workers;           /* 1; validated (>= 1) but the device ignores it */
+  uint64_t rng_seed;          /* 1 */
+  double ell;                 /* 1.0 */
+  double adaptive_threshold;  /* 0.25 */
+} rrg_imm_config;
+
+typedef struct {
+  uint64_t theta;
+  uint64_t theta_prime;
+  double lower_bound;
+  uint64_t sets_generated;
+  double mean_set_size;
+  uint32_t max_set_size;
+  double mean_coverage_fraction;
+  double t_generate;          /* ImmTimings (imm.hpp:38-42), seconds */
+  double t_select;
+  double t_total;
+} rrg_imm_result;
+
+void rrg_imm_config_default(rrg_imm_config* cfg);
+/* seeds u32[k], marginals u64[k] */
+rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
+                       uint64_t* marginals, rrg_imm_result* out);
+
+/* ---- parity / interop --------------------------------------------------- */
+/* Copies sets [first, first+count) to the host: offsets u64[count+1] (relative to
+ * the first set), members in visit order (root first, sampling.hpp:93-94). */
+rrg_status rrg_store_export(const rrg_store* s, uint64_t first, uint64_t count, uint64_t* offsets,
+                            uint32_t* members);
+/* Appends literal sets (e.g. the oracle's), updating the fused counter. */
+rrg_status rrg_store_import(rrg_store* s, uint64_t count, const uint64_t* offsets,
+                            const uint32_t* members);
+/* Fused occurrence counter as u64[n] (Counter::get, counter.hpp:29). */
+rrg_status rrg_store_counter(const rrg_store* s, uint64_t* counts);
+
+/* ---- host-side graph preparation (plumbing that feeds both sides) ---------- */
+/* detail::build_graph (graph.hpp:69-115): transpose of an edge list in the
+ * reference's in-list order. roff u64[n+1], rsrc u32[m], rw f32[m]. */
+rrg_status rrg_build_transpose(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                               const float* w, uint64_t* roff, uint32_t* rsrc, float* rw);
+/* normalize_lt_weights (graph.hpp:207-235) on transpose weights, in place. */
+rrg_status rrg_normalize_lt_weights(uint32_t n, const uint64_t* roff, float* rw);
+
+/* Synthetic BASELINE graphs (pinned generators). Fills the
+ * transpose arrays; call with roff == NULL first to learn n and m. */
+typedef enum {
+  RRG_GEN_RMAT = 0,           /* p0=scale, p1..p3 = a,b,c, edges = m (unique, no loops) */
+  RRG_GEN_CHUNG_LU = 1,       /* directed; p0=gamma; flags bit0: correlated in/out */
+  RRG_GEN_CHUNG_LU_UNDIR = 2  /* undirected, m unique pairs -> 2m arcs */
+} rrg_gen_kind;
+typedef enum {
+  RRG_W_WC = 0,               /* f32(1/indeg(v)) */
+  RRG_W_UNIFORM = 1,          /* U(0, scale) f32 */
+  RRG_W_LT_UNIFORM = 2        /* U(0,1) / per-vertex double sum, then normalize_lt_weights */
+} rrg_weight_kind;
+typedef struct {
+  int kind;
+  uint32_t n;
+  uint64_t m;                 /* edges (directed) or unique pairs (undirected) */
+  double p0, p1, p2, p3;
+  uint32_t flags;
+  uint64_t graph_seed;
+  int weights;
+  double weight_scale;
+  uint64_t weight_seed;
+  uint32_t threads;           /* 0 = hardware concurrency */
+} rrg_gen_spec;
+rrg_status rrg_generate_graph(const rrg_gen_spec* spec, uint32_t* n, uint64_t* m, uint64_t* roff,
+                              uint32_t* rsrc, float* rw);
+
+/* ---- misc ------------------------------------------------------------------ */
+const char* rrg_last_error(void);
+const char* rrg_version(void);
+/* Test hook: the integer Bernoulli threshold used by the IC kernel
+ * (uniform01() < (double)w  <=>  (next_u64() >> 11) < threshold(w)). */
+uint64_t rrg_debug_bernoulli_threshold(uint32_t weight_bits);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RRGPU_H */

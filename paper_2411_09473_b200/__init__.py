@@ -1,0 +1,321 @@
+"""paper_2411_09473_b200 -- B200-native IMM hot path (RRR sampling + greedy seed selection).
+
+Python mirror of the reference's operator API (rrflow 0.1.0, proj/include/rrflow),
+same names, argument meaning and error classes, over the C ABI of librrgpu.so:
+
+  Graph            rrflow::Graph transpose view (graph.hpp:34-59), device-resident
+  RRRStore         RRRStore + fused Counter (rrr_store.hpp:20-120, counter.hpp:15-62)
+  generate_batch   sampling.hpp:159-199
+  select_seeds     selection.hpp:209-243
+  fraction_covered selection.hpp:340-358
+  run_imm          imm.hpp:214-251 (driver in C++17, csrc/imm.cpp)
+  build_graph      detail::build_graph (graph.hpp:69-115), host
+  normalize_lt_weights graph.hpp:207-235, host
+
+Every compute call runs the sm_100a kernels in csrc/; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import RRGError, RRGOutOfMemory, check, lib, ptr
+
+__all__ = [
+    "DiffusionModel", "Graph", "RRRStore", "SeedSet", "ImmConfig", "ImmResult",
+    "generate_batch", "generate_batch_fused", "select_seeds", "fraction_covered",
+    "run_imm", "build_graph", "normalize_lt_weights", "RRGError", "RRGOutOfMemory",
+    "version", "BatchStats",
+]
+
+kDefaultDensityDivisor = 64  # rrr_set.hpp:13
+
+
+class DiffusionModel(enum.IntEnum):
+    IC = 0
+    LT = 1
+
+
+def version() -> str:
+    return lib.rrg_version().decode()
+
+
+def _model(m) -> int:
+    if isinstance(m, str):
+        s = m.lower()
+        if s not in ("ic", "lt"):
+            raise ValueError(f"unknown diffusion model: {m}")  # graph.hpp:24-28
+        return 0 if s == "ic" else 1
+    return int(DiffusionModel(m))
+
+
+def build_graph(n: int, src, dst, w):
+    """Transpose arrays of detail::build_graph (graph.hpp:69-115) for an edge list."""
+    src = np.ascontiguousarray(src, dtype=np.uint32)
+    dst = np.ascontiguousarray(dst, dtype=np.uint32)
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    m = src.size
+    roff = np.zeros(n + 1, dtype=np.uint64)
+    rsrc = np.zeros(m, dtype=np.uint32)
+    rw = np.zeros(m, dtype=np.float32)
+    check(lib.rrg_build_transpose(n, m, ptr(src, C.c_uint32), ptr(dst, C.c_uint32),
+                                  ptr(w, C.c_float), ptr(roff, C.c_uint64),
+                                  ptr(rsrc, C.c_uint32), ptr(rw, C.c_float)))
+    return roff, rsrc, rw
+
+
+def normalize_lt_weights(roff, rw):
+    """normalize_lt_weights (graph.hpp:207-235), in place on transpose weights."""
+    n = roff.size - 1
+    check(lib.rrg_normalize_lt_weights(n, ptr(roff, C.c_uint64), ptr(rw, C.c_float)))
+    return rw
+
+
+class Graph:
+    """Device-resident transpose CSR (the reverse arrays of rrflow::Graph)."""
+
+    def __init__(self, rev_offsets, rev_sources, rev_weights):
+        self.reverse_offsets = np.ascontiguousarray(rev_offsets, dtype=np.uint64)
+        self.reverse_sources = np.ascontiguousarray(rev_sources, dtype=np.uint32)
+        self.reverse_weights = np.ascontiguousarray(rev_weights, dtype=np.float32)
+        self.num_vertices = int(self.reverse_offsets.size - 1)
+        self.num_edges = int(self.reverse_sources.size)
+        h = C.c_void_p()
+        check(lib.rrg_graph_create(
+            self.num_vertices, self.num_edges, ptr(self.reverse_offsets, C.c_uint64),
+            ptr(self.reverse_sources, C.c_uint32), ptr(self.reverse_weights, C.c_float),
+            C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def from_edges(cls, n: int, edges):
+        """Like proj/tests/test_util.hpp:46-52 graph_from_edges: [(src, dst, w), ...]."""
+        if len(edges):
+            arr = np.array(edges, dtype=np.float64)
+            src, dst, w = arr[:, 0].astype(np.uint32), arr[:, 1].astype(np.uint32), arr[:, 2]
+        else:
+            src = dst = np.zeros(0, np.uint32)
+            w = np.zeros(0, np.float32)
+        return cls(*build_graph(n, src, dst, w))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def in_degree(self, v: int) -> int:
+        return int(self.reverse_offsets[v + 1] - self.reverse_offsets[v])
+
+    def prepare(self, model) -> None:
+        check(lib.rrg_graph_prepare(self._h, _model(model)))
+
+    def set_stream(self, cuda_stream_handle: int) -> None:
+        check(lib.rrg_graph_set_stream(self._h, C.c_void_p(cuda_stream_handle or None)))
+
+    def set_option(self, opt: str, value: int) -> None:
+        code = {"lt_scan": 0, "lt_coop_min": 1, "ic_inner": 2}[opt]
+        check(lib.rrg_graph_set_option(self._h, code, int(value)))
+
+    def last_batch_stats(self) -> "BatchStats":
+        st = _lib.BatchStats()
+        check(lib.rrg_last_batch_stats(self._h, C.byref(st)))
+        return BatchStats(st.sets, st.members, st.edges_inspected, st.entries_read,
+                          st.deferred, st.sample_ms, st.total_ms)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.rrg_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class BatchStats:
+    sets: int
+    members: int
+    edges_inspected: int
+    entries_read: int
+    deferred: int
+    sample_ms: float
+    total_ms: float
+
+
+class RRRStore:
+    """Slot-ordered device store of RRR sets plus the fused occurrence counter."""
+
+    def __init__(self, graph: Graph):
+        self.graph = graph
+        h = C.c_void_p()
+        check(lib.rrg_store_create(graph.handle, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def size(self) -> int:
+        s = C.c_uint64()
+        check(lib.rrg_store_info(self._h, C.byref(s), None, None))
+        return s.value
+
+    def total_member_count(self) -> int:
+        m = C.c_uint64()
+        check(lib.rrg_store_info(self._h, None, C.byref(m), None))
+        return m.value
+
+    def max_set_size(self) -> int:
+        x = C.c_uint32()
+        check(lib.rrg_store_info(self._h, None, None, C.byref(x)))
+        return x.value
+
+    def clear(self) -> None:
+        check(lib.rrg_store_clear(self._h))
+
+    def export(self, first: int = 0, count: Optional[int] = None):
+        """(offsets u64[count+1], members u32[...]) in slot order, visit order per set."""
+        if count is None:
+            count = self.size() - first
+        off = np.zeros(count + 1, dtype=np.uint64)
+        check(lib.rrg_store_export(self._h, first, count, ptr(off, C.c_uint64), None))
+        mem = np.zeros(int(off[-1]), dtype=np.uint32)
+        check(lib.rrg_store_export(self._h, first, count, ptr(off, C.c_uint64),
+                                   ptr(mem, C.c_uint32)))
+        return off, mem
+
+    def sets(self, first: int = 0, count: Optional[int] = None, sort: bool = True):
+        off, mem = self.export(first, count)
+        out = [mem[off[i]:off[i + 1]] for i in range(off.size - 1)]
+        return [np.sort(s) for s in out] if sort else out
+
+    def import_sets(self, offsets, members) -> None:
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        members = np.ascontiguousarray(members, dtype=np.uint32)
+        check(lib.rrg_store_import(self._h, offsets.size - 1, ptr(offsets, C.c_uint64),
+                                   ptr(members, C.c_uint32)))
+
+    def counter(self) -> np.ndarray:
+        out = np.zeros(self.graph.num_vertices, dtype=np.uint64)
+        check(lib.rrg_store_counter(self._h, ptr(out, C.c_uint64)))
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.rrg_store_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def generate_batch(g: Graph, model, run_seed: int, count: int, store: RRRStore,
+                   fused: bool = True, density_divisor: int = kDefaultDensityDivisor) -> int:
+    """sampling.hpp:159-199: appends `count` sets at slots [size, size+count)."""
+    made = C.c_uint64()
+    st = lib.rrg_generate_batch(g.handle, _model(model), int(run_seed) & (2**64 - 1), int(count),
+                                store.handle, 1 if fused else 0, int(density_divisor),
+                                C.byref(made))
+    check(st, made.value)
+    return made.value
+
+
+def generate_batch_fused(g: Graph, model, run_seed: int, count: int, store: RRRStore,
+                         density_divisor: int = kDefaultDensityDivisor) -> int:
+    """sampling.hpp:201-206."""
+    return generate_batch(g, model, run_seed, count, store, True, density_divisor)
+
+
+@dataclass
+class SeedSet:
+    """selection.hpp:19-22."""
+    seeds: List[int] = field(default_factory=list)
+    marginal_counts: List[int] = field(default_factory=list)
+    round_counters: Optional[np.ndarray] = None
+    covered: int = 0
+
+
+def select_seeds(store: RRRStore, n: int, k: int, adaptive_threshold: float = 0.25,
+                 prebuilt: bool = True, capture_round_counters: bool = False) -> SeedSet:
+    """selection.hpp:209-243 (k rounds resident on the GPU)."""
+    if n != store.graph.num_vertices:
+        raise ValueError("select_seeds: n does not match the store's graph")
+    if k < 1:
+        raise ValueError("select_seeds: k must be >= 1")
+    if k > n:
+        raise ValueError("select_seeds: k exceeds vertex count")
+    seeds = np.zeros(k, dtype=np.uint32)
+    marg = np.zeros(k, dtype=np.uint64)
+    snap = np.zeros(k * n, dtype=np.uint64) if capture_round_counters else None
+    rounds = C.c_uint32()
+    covered = C.c_uint64()
+    check(lib.rrg_select_seeds(store.handle, k, float(adaptive_threshold), 1 if prebuilt else 0,
+                               ptr(seeds, C.c_uint32), ptr(marg, C.c_uint64),
+                               ptr(snap, C.c_uint64), C.byref(rounds), C.byref(covered)))
+    rc = snap.reshape(k, n)[: rounds.value] if snap is not None else None
+    return SeedSet([int(x) for x in seeds], [int(x) for x in marg], rc, covered.value)
+
+
+def fraction_covered(store: RRRStore, seeds) -> float:
+    """selection.hpp:340-358."""
+    s = np.ascontiguousarray(list(seeds.seeds if isinstance(seeds, SeedSet) else seeds),
+                             dtype=np.uint32)
+    out = C.c_double()
+    check(lib.rrg_fraction_covered(store.handle, ptr(s, C.c_uint32), s.size, C.byref(out)))
+    return out.value
+
+
+@dataclass
+class ImmConfig:
+    """imm.hpp:27-36 defaults."""
+    k: int = 50
+    epsilon: float = 0.5
+    model: int = DiffusionModel.IC
+    workers: int = 1
+    rng_seed: int = 1
+    ell: float = 1.0
+    adaptive_threshold: float = 0.25
+
+
+@dataclass
+class ImmResult:
+    """imm.hpp:44-54."""
+    seeds: SeedSet
+    theta: int
+    theta_prime: int
+    lower_bound: float
+    timings: dict
+    sets_generated: int
+    mean_set_size: float
+    max_set_size: int
+    mean_coverage_fraction: float
+
+
+def run_imm(g: Graph, cfg: ImmConfig) -> ImmResult:
+    """imm.hpp:214-251, driven by the C++17 driver in csrc/imm.cpp."""
+    c = _lib.ImmConfigC(int(cfg.k), float(cfg.epsilon), _model(cfg.model), int(cfg.workers),
+                        int(cfg.rng_seed) & (2**64 - 1), float(cfg.ell),
+                        float(cfg.adaptive_threshold))
+    k = max(int(cfg.k), 1)
+    seeds = np.zeros(k, dtype=np.uint32)
+    marg = np.zeros(k, dtype=np.uint64)
+    r = _lib.ImmResultC()
+    check(lib.rrg_run_imm(g.handle, C.byref(c), ptr(seeds, C.c_uint32), ptr(marg, C.c_uint64),
+                          C.byref(r)))
+    return ImmResult(
+        seeds=SeedSet([int(x) for x in seeds], [int(x) for x in marg]),
+        theta=r.theta, theta_prime=r.theta_prime, lower_bound=r.lower_bound,
+        timings={"generate_rrrsets": r.t_generate, "find_most_influential": r.t_select,
+                 "total": r.t_total},
+        sets_generated=r.sets_generated, mean_set_size=r.mean_set_size,
+        max_set_size=r.max_set_size, mean_coverage_fraction=r.mean_coverage_fraction)

@@ -1,0 +1,594 @@
+// capi.cu -- the extern "C" boundary (include/rrgpu.h): device graph, store,
+// generate_batch, select_seeds, export/import. Every call is synchronous at
+// return, mirroring the reference's fork-join barriers (work_pool.hpp:14-19).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace rrgpu {
+
+namespace {
+thread_local std::string t_err;
+}
+
+void set_error(const std::string& msg) { t_err = msg; }
+
+// Converts exceptions at the C boundary into status codes.
+template <typename Fn>
+rrg_status guarded(Fn&& fn) {
+  try {
+    return fn();
+  } catch (const CudaError& e) {
+    set_error(std::string(e.where) + ": " + cudaGetErrorString(e.err));
+    if (e.err == cudaErrorMemoryAllocation) {
+      cudaGetLastError();  // clear the sticky-free allocation error
+      return RRG_ENOMEM;
+    }
+    return RRG_ECUDA;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return RRG_ENOMEM;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return RRG_ECUDA;
+  }
+}
+
+rrg_status invalid(const char* msg) {
+  set_error(msg);
+  return RRG_EINVAL;
+}
+
+}  // namespace rrgpu
+
+using namespace rrgpu;
+
+namespace {
+
+constexpr int kMaxBlocksPerSm = 4;
+constexpr uint32_t kBigWorkersMax = 256;
+
+void ensure_lane_scratch(rrg_graph* g, uint64_t lanes) {
+  LaneScratch& sc = g->scratch;
+  if (sc.lanes >= lanes) return;
+  sc.lists.release();
+  sc.tabs.release();
+  sc.tags.release();
+  sc.lists.reserve_discard(lanes * kMemCap);
+  sc.tabs.reserve_discard(lanes * kTabCap);
+  sc.tags.reserve_discard(lanes);
+  RRG_CUDA(cudaMemsetAsync(sc.tabs.ptr, 0, lanes * kTabCap * sizeof(uint64_t), g->stream));
+  RRG_CUDA(cudaMemsetAsync(sc.tags.ptr, 0, lanes * sizeof(uint32_t), g->stream));
+  sc.lanes = lanes;
+}
+
+void ensure_big_scratch(rrg_graph* g, uint32_t workers) {
+  BigScratch& b = g->big;
+  if (b.workers >= workers) return;
+  const uint64_t words = (static_cast<uint64_t>(g->n) + 31) / 32;
+  b.bitmaps.release();
+  b.lists.release();
+  b.bitmaps.reserve_discard(words * workers);
+  b.lists.reserve_discard(static_cast<uint64_t>(g->n) * workers);
+  RRG_CUDA(cudaMemsetAsync(b.bitmaps.ptr, 0, words * workers * 4, g->stream));
+  b.workers = workers;
+}
+
+template <typename T>
+void d2h(T* dst, const T* src, size_t count, cudaStream_t s) {
+  if (!count) return;
+  RRG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+
+void sync(rrg_graph* g) { RRG_CUDA(cudaStreamSynchronize(g->stream)); }
+
+// Appends `count` already-staged sets (slot_len/slot_start in the store's staging
+// arrays) to the slot-ordered buffer: K3 scan + compaction.
+void commit_staged(rrg_store* s, uint64_t count) {
+  rrg_graph* g = s->g;
+  s->scan.reserve_discard(count + 1);
+  exclusive_scan_u32(s->slot_len.ptr, s->scan.ptr, count, s->scan_tmp, g->stream);
+  uint64_t added = 0;
+  d2h(&added, s->scan.ptr + count, 1, g->stream);
+  sync(g);
+  const uint64_t need_mem = s->total + added;
+  if (need_mem > s->mem.cap)
+    s->mem.reserve_keep(std::max<uint64_t>(need_mem, s->mem.cap + s->mem.cap / 2), s->total,
+                        g->stream);
+  const uint64_t need_off = s->nsets + count + 1;
+  if (need_off > s->off.cap)
+    s->off.reserve_keep(std::max<uint64_t>(need_off, s->off.cap + s->off.cap / 2), s->nsets + 1,
+                        g->stream);
+  launch_compact(s->stage.ptr, s->slot_start.ptr, s->slot_len.ptr, s->scan.ptr, s->total, count,
+                 s->mem.ptr, s->off.ptr + s->nsets, s->maxlen_dev.ptr, g->stream);
+  uint32_t mx = 0;
+  d2h(&mx, s->maxlen_dev.ptr, 1, g->stream);
+  sync(g);
+  s->nsets += count;
+  s->total += added;
+  s->max_len = mx;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rrg_last_error(void) { return rrgpu::t_err.c_str(); }
+const char* rrg_version(void) { return "rrgpu 0.1.0 (sm_100a; reference rrflow 0.1.0)"; }
+uint64_t rrg_debug_bernoulli_threshold(uint32_t bits) { return bernoulli_threshold(bits); }
+
+rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* roff, const uint32_t* rsrc,
+                            const float* rw, rrg_graph** out) {
+  if (!out) return invalid("rrg_graph_create: null output");
+  *out = nullptr;
+  if (m >= (1ull << 32)) return invalid("rrg_graph_create: m must be < 2^32");
+  if (n && !roff) return invalid("rrg_graph_create: null offsets");
+  if (m && (!rsrc || !rw)) return invalid("rrg_graph_create: null edge arrays");
+  if (n == UINT32_MAX) return invalid("rrg_graph_create: n must be < 2^32 - 1");
+  if (n && (roff[0] != 0 || roff[n] != m))
+    return invalid("rrg_graph_create: offsets must start at 0 and end at m");
+  for (uint32_t v = 0; n && v < n; ++v)
+    if (roff[v + 1] < roff[v]) return invalid("rrg_graph_create: offsets must be non-decreasing");
+  for (uint64_t j = 0; j < m; ++j)
+    if (rsrc[j] >= n) return invalid("rrg_graph_create: source id out of range");
+  auto* g = new (std::nothrow) rrg_graph;
+  if (!g) return RRG_ENOMEM;
+  const rrg_status st = guarded([&]() -> rrg_status {
+    RRG_CUDA(cudaGetDevice(&g->device));
+    RRG_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device));
+    RRG_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    g->own_stream = true;
+    RRG_CUDA(cudaEventCreate(&g->ev0));
+    RRG_CUDA(cudaEventCreate(&g->ev1));
+    g->n = n;
+    g->m = m;
+    std::vector<uint32_t> off32(static_cast<size_t>(n) + 1);
+    for (uint64_t v = 0; v <= n; ++v) off32[v] = n ? static_cast<uint32_t>(roff[v]) : 0;
+    g->off.reserve_discard(off32.size());
+    g->src.reserve_discard(m ? m : 1);
+    g->w.reserve_discard(m ? m : 1);
+    g->ctl.reserve_discard(1);
+    RRG_CUDA(cudaMemcpyAsync(g->off.ptr, off32.data(), off32.size() * 4, cudaMemcpyHostToDevice,
+                             g->stream));
+    if (m) {
+      RRG_CUDA(cudaMemcpyAsync(g->src.ptr, rsrc, m * 4, cudaMemcpyHostToDevice, g->stream));
+      RRG_CUDA(cudaMemcpyAsync(g->w.ptr, rw, m * 4, cudaMemcpyHostToDevice, g->stream));
+    }
+    RRG_CUDA(cudaStreamSynchronize(g->stream));
+    return RRG_OK;
+  });
+  if (st != RRG_OK) {
+    rrg_graph_destroy(g);
+    return st;
+  }
+  *out = g;
+  return RRG_OK;
+}
+
+void rrg_graph_destroy(rrg_graph* g) {
+  if (!g) return;
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  if (g->ev0) cudaEventDestroy(g->ev0);
+  if (g->ev1) cudaEventDestroy(g->ev1);
+  if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+rrg_status rrg_graph_prepare(rrg_graph* g, rrg_model model) {
+  if (!g) return invalid("null graph");
+  if (model != RRG_IC && model != RRG_LT) return invalid("unknown diffusion model");
+  return guarded([&]() -> rrg_status {
+    if (model == RRG_IC) prepare_ic(g);
+    else prepare_lt(g);
+    return RRG_OK;
+  });
+}
+
+rrg_status rrg_graph_set_stream(rrg_graph* g, void* stream) {
+  if (!g) return invalid("null graph");
+  return guarded([&]() -> rrg_status {
+    RRG_CUDA(cudaStreamSynchronize(g->stream));
+    if (g->own_stream) {
+      RRG_CUDA(cudaStreamDestroy(g->stream));
+      g->own_stream = false;
+    }
+    if (stream) {
+      g->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      RRG_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+      g->own_stream = true;
+    }
+    return RRG_OK;
+  });
+}
+
+uint32_t rrg_graph_num_vertices(const rrg_graph* g) { return g ? g->n : 0; }
+uint64_t rrg_graph_num_edges(const rrg_graph* g) { return g ? g->m : 0; }
+
+rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value) {
+  if (!g) return invalid("null graph");
+  switch (opt) {
+    case RRG_OPT_LT_SCAN:
+      if (value != kLtLinear && value != kLtBsearch) return invalid("LT scan must be 0 or 1");
+      g->lt_scan = static_cast<int>(value);
+      return RRG_OK;
+    case RRG_OPT_LT_COOP_MIN:
+      if (value < 2) return invalid("coop_min must be >= 2");
+      g->coop_min = static_cast<uint32_t>(std::min<int64_t>(value, UINT32_MAX));
+      return RRG_OK;
+    case RRG_OPT_IC_INNER:
+      if (value < 1 || value > 64) return invalid("ic_inner must be in [1, 64]");
+      g->ic_inner = static_cast<uint32_t>(value);
+      return RRG_OK;
+  }
+  return invalid("unknown option");
+}
+
+rrg_status rrg_store_create(rrg_graph* g, rrg_store** out) {
+  if (!g || !out) return invalid("rrg_store_create: null argument");
+  *out = nullptr;
+  auto* s = new (std::nothrow) rrg_store;
+  if (!s) return RRG_ENOMEM;
+  s->g = g;
+  const rrg_status st = guarded([&]() -> rrg_status {
+    s->off.reserve_discard(1024);
+    s->mem.reserve_discard(1 << 16);
+    s->counter.reserve_discard(g->n ? g->n : 1);
+    s->maxlen_dev.reserve_discard(1);
+    s->status.reserve_discard(2);
+    RRG_CUDA(cudaMemsetAsync(s->off.ptr, 0, 8, g->stream));
+    RRG_CUDA(cudaMemsetAsync(s->counter.ptr, 0, 4ull * (g->n ? g->n : 1), g->stream));
+    RRG_CUDA(cudaMemsetAsync(s->maxlen_dev.ptr, 0, 4, g->stream));
+    sync(g);
+    return RRG_OK;
+  });
+  if (st != RRG_OK) {
+    delete s;
+    return st;
+  }
+  *out = s;
+  return RRG_OK;
+}
+
+void rrg_store_destroy(rrg_store* s) {
+  if (!s) return;
+  cudaStreamSynchronize(s->g->stream);
+  delete s;
+}
+
+rrg_status rrg_store_clear(rrg_store* s) {
+  if (!s) return invalid("null store");
+  return guarded([&]() -> rrg_status {
+    rrg_graph* g = s->g;
+    RRG_CUDA(cudaMemsetAsync(s->counter.ptr, 0, 4ull * (g->n ? g->n : 1), g->stream));
+    RRG_CUDA(cudaMemsetAsync(s->maxlen_dev.ptr, 0, 4, g->stream));
+    sync(g);
+    s->nsets = s->total = 0;
+    s->max_len = 0;
+    s->counter_complete = true;
+    return RRG_OK;
+  });
+}
+
+rrg_status rrg_store_info(const rrg_store* s, uint64_t* sets, uint64_t* members,
+                          uint32_t* max_set_size) {
+  if (!s) return invalid("null store");
+  if (sets) *sets = s->nsets;
+  if (members) *members = s->total;
+  if (max_set_size) *max_set_size = s->max_len;
+  return RRG_OK;
+}
+
+rrg_status rrg_generate_batch(rrg_graph* g, rrg_model model, uint64_t run_seed, uint64_t count,
+                              rrg_store* s, int fused, uint32_t /*density_divisor*/,
+                              uint64_t* sets_generated) {
+  if (sets_generated) *sets_generated = 0;
+  if (!g || !s || s->g != g) return invalid("generate_batch: graph/store mismatch");
+  if (model != RRG_IC && model != RRG_LT) return invalid("unknown diffusion model");
+  if (g->n == 0) return invalid("generate_batch: empty graph");
+  g->last = rrg_batch_stats{};
+  if (count == 0) return RRG_OK;
+  return guarded([&]() -> rrg_status {
+    if (model == RRG_IC) prepare_ic(g);
+    else prepare_lt(g);
+    if (!fused) s->counter_complete = false;
+    const cudaStream_t st = g->stream;
+    const int block = sampler_block();
+    const int per_sm = std::min(kMaxBlocksPerSm, sampler_blocks_per_sm(model, g->ic_inner));
+    const uint64_t full_grid = static_cast<uint64_t>(g->num_sms) * per_sm;
+    ensure_lane_scratch(g, full_grid * block);
+    const uint64_t kChunk = 1ull << 30;  // batch-local indices are u32
+    float sample_ms = 0.0f;
+    const auto t0 = std::chrono::steady_clock::now();
+    rrg_batch_stats acc{};
+    for (uint64_t done = 0; done < count;) {
+      const uint64_t c = std::min(kChunk, count - done);
+      // staging sized from the running mean set size
+      const double mean = s->nsets ? static_cast<double>(s->total) / s->nsets : 16.0;
+      const uint64_t want = static_cast<uint64_t>(c * (mean * 1.25 + 4)) + (1u << 16);
+      if (want > s->stage.cap) s->stage.reserve_discard(want);
+      s->slot_start.reserve_discard(c);
+      s->slot_len.reserve_discard(c);
+      s->deferred.reserve_discard(c);
+      s->deferred2.reserve_discard(c);
+      RRG_CUDA(cudaMemsetAsync(g->ctl.ptr, 0, sizeof(SampleCtl), st));
+      SampleParams p{};
+      p.n = g->n;
+      p.off = g->off.ptr;
+      p.rec = g->rec.ptr;
+      p.src = g->src.ptr;
+      p.cdf = g->cdf.ptr;
+      p.run_seed = run_seed;
+      p.base_slot = s->nsets;
+      p.count = c;
+      p.lists = g->scratch.lists.ptr;
+      p.tabs = g->scratch.tabs.ptr;
+      p.tags = g->scratch.tags.ptr;
+      p.stage = s->stage.ptr;
+      p.stage_cap = s->stage.cap;
+      p.slot_start = s->slot_start.ptr;
+      p.slot_len = s->slot_len.ptr;
+      p.counter = fused ? s->counter.ptr : nullptr;
+      p.deferred = s->deferred.ptr;
+      p.ctl = g->ctl.ptr;
+      p.lt_scan = (g->lt_scan == kLtBsearch && g->cdf_monotone) ? kLtBsearch : kLtLinear;
+      p.coop_min = g->coop_min;
+      const uint64_t grid_need = (c + block - 1) / block;
+      const int grid = static_cast<int>(std::min<uint64_t>(full_grid, grid_need));
+      RRG_CUDA(cudaEventRecord(g->ev0, st));
+      launch_sampler(model, p, grid, g->ic_inner, st);
+      RRG_CUDA(cudaEventRecord(g->ev1, st));
+      SampleCtl ctl{};
+      d2h(&ctl, g->ctl.ptr, 1, st);
+      sync(g);
+      float ms = 0.0f;
+      RRG_CUDA(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+      sample_ms += ms;
+      acc.deferred += ctl.ndeferred;
+      // big-set path for deferred slots; grows staging when it ran out
+      uint32_t* list = s->deferred.ptr;
+      uint32_t* relist = s->deferred2.ptr;
+      uint32_t nlist = ctl.ndeferred;
+      int guard = 0;
+      while (nlist > 0) {
+        if (++guard > 64) throw std::runtime_error("big-set path did not converge");
+        if (ctl.cursor + ctl.deferred_members + 1024 > s->stage.cap) {
+          const uint64_t ncap = std::max<uint64_t>(
+              s->stage.cap * 2, ctl.cursor + 2 * ctl.deferred_members + (1u << 20));
+          s->stage.reserve_keep(ncap, s->stage.cap, st);
+          p.stage = s->stage.ptr;
+          p.stage_cap = s->stage.cap;
+        }
+        const uint32_t workers = std::min<uint32_t>(nlist, kBigWorkersMax);
+        ensure_big_scratch(g, workers);
+        // reset deferral counters, keep cursor/inspected
+        const unsigned zero = 0;
+        const unsigned long long zero64 = 0;
+        RRG_CUDA(cudaMemcpyAsync(&g->ctl.ptr->ndeferred, &zero, 4, cudaMemcpyHostToDevice, st));
+        RRG_CUDA(cudaMemcpyAsync(&g->ctl.ptr->deferred_members, &zero64, 8,
+                                 cudaMemcpyHostToDevice, st));
+        RRG_CUDA(cudaEventRecord(g->ev0, st));
+        launch_big(model, p, list, nlist, g->big.bitmaps.ptr, g->big.lists.ptr, workers, relist,
+                   st);
+        RRG_CUDA(cudaEventRecord(g->ev1, st));
+        d2h(&ctl, g->ctl.ptr, 1, st);
+        sync(g);
+        RRG_CUDA(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+        sample_ms += ms;
+        std::swap(list, relist);
+        nlist = ctl.ndeferred;
+      }
+      acc.edges_inspected += ctl.inspected;
+      acc.entries_read += ctl.entries;
+      const uint64_t before = s->total;
+      commit_staged(s, c);
+      acc.members += s->total - before;
+      acc.sets += c;
+      done += c;
+      if (sets_generated) *sets_generated = done;
+    }
+    acc.sample_ms = sample_ms;
+    acc.total_ms = static_cast<float>(
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    g->last = acc;
+    return RRG_OK;
+  });
+}
+
+rrg_status rrg_last_batch_stats(const rrg_graph* g, rrg_batch_stats* out) {
+  if (!g || !out) return invalid("null argument");
+  *out = g->last;
+  return RRG_OK;
+}
+
+rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double /*adaptive_threshold*/,
+                            int use_prebuilt, uint32_t* seeds, uint64_t* marginals,
+                            uint64_t* round_counters, uint32_t* rounds_done,
+                            uint64_t* covered_total) {
+  if (!s) return invalid("null store");
+  rrg_graph* g = s->g;
+  if (k < 1) return invalid("select_seeds: k must be >= 1");
+  if (k > g->n) return invalid("select_seeds: k exceeds vertex count");
+  if (!seeds || !marginals) return invalid("select_seeds: null output");
+  return guarded([&]() -> rrg_status {
+    const cudaStream_t st = g->stream;
+    const uint32_t n = g->n;
+    s->wcnt.reserve_discard(n);
+    if (use_prebuilt) {
+      RRG_CUDA(cudaMemcpyAsync(s->wcnt.ptr, s->counter.ptr, 4ull * n, cudaMemcpyDeviceToDevice,
+                               st));
+    } else {
+      RRG_CUDA(cudaMemsetAsync(s->wcnt.ptr, 0, 4ull * n, st));
+      launch_recount(s->off.ptr, s->mem.ptr, s->nsets, s->wcnt.ptr, st);
+    }
+    // K5: inverted index from the starting tally (all sets live: revive_all, :215)
+    s->ioff.reserve_discard(static_cast<uint64_t>(n) + 1);
+    exclusive_scan_u32(s->wcnt.ptr, s->ioff.ptr, n, s->scan_tmp, st);
+    s->icur.reserve_discard(n);
+    RRG_CUDA(cudaMemcpyAsync(s->icur.ptr, s->ioff.ptr, 8ull * n, cudaMemcpyDeviceToDevice, st));
+    s->inv.reserve_discard(s->total ? s->total : 1);
+    RRG_CUDA(cudaMemsetAsync(s->status.ptr, 0, 8, st));
+    launch_invert(s->off.ptr, s->mem.ptr, s->nsets, s->icur.ptr, s->ioff.ptr, s->inv.ptr,
+                  s->status.ptr, st);
+    s->covered.reserve_discard(s->nsets ? s->nsets : 1);
+    RRG_CUDA(cudaMemsetAsync(s->covered.ptr, 0, 4ull * (s->nsets ? s->nsets : 1), st));
+    s->keys.reserve_discard(k);
+    s->marg.reserve_discard(k);
+    s->seeds.reserve_discard(k);
+    s->selected.reserve_discard(n);
+    RRG_CUDA(cudaMemsetAsync(s->keys.ptr, 0, 8ull * k, st));
+    RRG_CUDA(cudaMemsetAsync(s->marg.ptr, 0, 8ull * k, st));
+    RRG_CUDA(cudaMemsetAsync(s->selected.ptr, 0, n, st));
+    if (round_counters) s->snap.reserve_discard(static_cast<uint64_t>(k) * n);
+    SelectParams p{};
+    p.n = n;
+    p.k = k;
+    p.cnt = s->wcnt.ptr;
+    p.ioff = s->ioff.ptr;
+    p.inv = s->inv.ptr;
+    p.off = s->off.ptr;
+    p.mem = s->mem.ptr;
+    p.covered = s->covered.ptr;
+    p.keys = s->keys.ptr;
+    p.marg = s->marg.ptr;
+    p.seeds = s->seeds.ptr;
+    p.selected = s->selected.ptr;
+    p.snap = round_counters ? s->snap.ptr : nullptr;
+    p.status = s->status.ptr;
+    launch_select(p, g->num_sms, st);
+    uint32_t status[2] = {0, 0};
+    std::vector<unsigned long long> marg(k);
+    d2h(status, s->status.ptr, 2, st);
+    d2h(seeds, s->seeds.ptr, k, st);
+    d2h(marg.data(), s->marg.ptr, k, st);
+    sync(g);
+    if (status[1]) {
+      set_error("select_seeds: prebuilt counter does not match the stored sets");
+      return RRG_EINVAL;
+    }
+    uint64_t covered = 0;
+    for (uint32_t r = 0; r < k; ++r) {
+      marginals[r] = marg[r];
+      covered += marg[r];
+    }
+    if (covered_total) *covered_total = covered;
+    if (rounds_done) *rounds_done = status[0];
+    if (round_counters && status[0]) {
+      std::vector<uint32_t> snap(static_cast<uint64_t>(status[0]) * n);
+      d2h(snap.data(), s->snap.ptr, snap.size(), st);
+      sync(g);
+      for (size_t i = 0; i < snap.size(); ++i) round_counters[i] = snap[i];
+    }
+    return RRG_OK;
+  });
+}
+
+rrg_status rrg_fraction_covered(rrg_store* s, const uint32_t* seeds, uint32_t nseeds,
+                                double* out) {
+  if (!s || !out) return invalid("null argument");
+  if (nseeds && !seeds) return invalid("null seeds");
+  rrg_graph* g = s->g;
+  for (uint32_t i = 0; i < nseeds; ++i)
+    if (seeds[i] >= g->n) return invalid("fraction_covered: seed out of range");
+  if (s->nsets == 0) {
+    *out = 0.0;
+    return RRG_OK;
+  }
+  return guarded([&]() -> rrg_status {
+    std::vector<uint8_t> flag(g->n, 0);
+    for (uint32_t i = 0; i < nseeds; ++i) flag[seeds[i]] = 1;
+    s->selected.reserve_discard(g->n);
+    s->marg.reserve_discard(1);
+    RRG_CUDA(cudaMemcpyAsync(s->selected.ptr, flag.data(), g->n, cudaMemcpyHostToDevice,
+                             g->stream));
+    RRG_CUDA(cudaMemsetAsync(s->marg.ptr, 0, 8, g->stream));
+    launch_fraction(s->off.ptr, s->mem.ptr, s->nsets, s->selected.ptr, s->marg.ptr, g->stream);
+    unsigned long long hits = 0;
+    d2h(&hits, s->marg.ptr, 1, g->stream);
+    sync(g);
+    *out = static_cast<double>(hits) / static_cast<double>(s->nsets);
+    return RRG_OK;
+  });
+}
+
+rrg_status rrg_store_export(const rrg_store* s, uint64_t first, uint64_t count, uint64_t* offsets,
+                            uint32_t* members) {
+  if (!s || !offsets) return invalid("null argument");
+  if (first + count > s->nsets) return invalid("export range out of bounds");
+  return guarded([&]() -> rrg_status {
+    rrg_graph* g = s->g;
+    std::vector<uint64_t> off(count + 1);
+    d2h(off.data(), s->off.ptr + first, count + 1, g->stream);
+    sync(g);
+    const uint64_t base = off[0];
+    for (uint64_t i = 0; i <= count; ++i) offsets[i] = off[i] - base;
+    if (members && off[count] > base) {
+      d2h(members, s->mem.ptr + base, off[count] - base, g->stream);
+      sync(g);
+    }
+    return RRG_OK;
+  });
+}
+
+rrg_status rrg_store_import(rrg_store* s, uint64_t count, const uint64_t* offsets,
+                            const uint32_t* members) {
+  if (!s) return invalid("null store");
+  if (count == 0) return RRG_OK;
+  if (!offsets) return invalid("null offsets");
+  rrg_graph* g = s->g;
+  const uint64_t total = offsets[count] - offsets[0];
+  if (total && !members) return invalid("null members");
+  for (uint64_t i = 0; i < count; ++i) {
+    if (offsets[i + 1] < offsets[i]) return invalid("offsets must be non-decreasing");
+    if (offsets[i + 1] - offsets[i] >= (1ull << 32)) return invalid("set too large");
+  }
+  for (uint64_t t = 0; t < total; ++t)
+    if (members[offsets[0] + t] >= g->n) return invalid("member out of range");
+  return guarded([&]() -> rrg_status {
+    const cudaStream_t st = g->stream;
+    std::vector<uint64_t> start(count);
+    std::vector<uint32_t> len(count);
+    for (uint64_t i = 0; i < count; ++i) {
+      start[i] = offsets[i] - offsets[0];
+      len[i] = static_cast<uint32_t>(offsets[i + 1] - offsets[i]);
+    }
+    s->stage.reserve_discard(total ? total : 1);
+    s->slot_start.reserve_discard(count);
+    s->slot_len.reserve_discard(count);
+    if (total)
+      RRG_CUDA(cudaMemcpyAsync(s->stage.ptr, members + offsets[0], total * 4,
+                               cudaMemcpyHostToDevice, st));
+    RRG_CUDA(cudaMemcpyAsync(s->slot_start.ptr, start.data(), count * 8, cudaMemcpyHostToDevice,
+                             st));
+    RRG_CUDA(cudaMemcpyAsync(s->slot_len.ptr, len.data(), count * 4, cudaMemcpyHostToDevice, st));
+    const uint64_t nsets0 = s->nsets;
+    commit_staged(s, count);
+    // fused counter over the imported sets only
+    s->scan.reserve_discard(1);
+    launch_recount(s->off.ptr + nsets0, s->mem.ptr, count, s->counter.ptr, st);
+    sync(g);
+    return RRG_OK;
+  });
+}
+
+rrg_status rrg_store_counter(const rrg_store* s, uint64_t* counts) {
+  if (!s || !counts) return invalid("null argument");
+  return guarded([&]() -> rrg_status {
+    rrg_graph* g = s->g;
+    std::vector<uint32_t> c(g->n);
+    d2h(c.data(), s->counter.ptr, g->n, g->stream);
+    sync(g);
+    for (uint32_t v = 0; v < g->n; ++v) counts[v] = c[v];
+    return RRG_OK;
+  });
+}
+
+}  // extern "C"

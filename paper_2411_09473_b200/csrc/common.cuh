@@ -1,0 +1,167 @@
+// common.cuh -- device-side building blocks shared by the rrgpu kernels.
+//
+//   * the per-slot xoshiro256** stream of the reference (prng.hpp:8-70),
+//     reproduced bit-exactly so RRR sets match the CPU path slot for slot;
+//   * the exact Bernoulli test of prng.hpp:62 rewritten as one integer compare;
+//   * per-lane open-addressing visited sets (tagged, never cleared);
+//   * the control block shared by the sampler launches.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rrgpu {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// RNG: prng.hpp:8-13 (splitmix64), :17-20 (derive_stream_seed), :28-31
+// (reseed), :33-43 (next_u64), :46 (uniform01), :49-60 (uniform_below).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t splitmix_next(uint64_t& s) {
+  s += 0x9e3779b97f4a7c15ULL;
+  uint64_t z = s;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t stream_seed(uint64_t run_seed, uint64_t slot) {
+  uint64_t s = run_seed ^ (0x9e3779b97f4a7c15ULL * (slot + 1));
+  return splitmix_next(s);
+}
+
+struct Xoshiro {
+  uint64_t a, b, c, d;
+
+  __device__ __forceinline__ void seed(uint64_t v) {
+    a = splitmix_next(v);
+    b = splitmix_next(v);
+    c = splitmix_next(v);
+    d = splitmix_next(v);
+  }
+  __device__ __forceinline__ static uint64_t rol(uint64_t x, int k) {
+    return (x << k) | (x >> (64 - k));
+  }
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t out = rol(b * 5, 7) * 9;
+    const uint64_t t = b << 17;
+    c ^= a;
+    d ^= b;
+    b ^= c;
+    a ^= d;
+    c ^= t;
+    d = rol(d, 45);
+    return out;
+  }
+  // 53-bit integer behind uniform01(): uniform01() == u53() * 2^-53 exactly.
+  __device__ __forceinline__ uint64_t u53() { return next() >> 11; }
+  __device__ __forceinline__ double u01() {
+    return __ull2double_rn(next() >> 11) * 0x1.0p-53;
+  }
+  // Lemire multiply-shift with the reference's rejection rule.
+  __device__ __forceinline__ uint64_t below(uint64_t bound) {
+    uint64_t x = next();
+    uint64_t lo = x * bound;
+    uint64_t hi = __umul64hi(x, bound);
+    if (lo < bound) {
+      const uint64_t thr = (0 - bound) % bound;
+      while (lo < thr) {
+        x = next();
+        lo = x * bound;
+        hi = __umul64hi(x, bound);
+      }
+    }
+    return hi;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Exact Bernoulli: uniform01() < (double)w  (prng.hpp:46, :62; sampling.hpp:102)
+// uniform01() = k * 2^-53 with integer k < 2^53, and (double)w * 2^53 is exact,
+// so the test is k < ceil(w * 2^53).  The threshold is derived from the f32
+// bits with integer ops only; NaN and negatives never fire, >= 1 always fires.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t bernoulli_threshold(uint32_t bits) {
+  if (bits & 0x80000000u) return 0;                    // negative or -0
+  const uint32_t e = bits >> 23;
+  const uint32_t f = bits & 0x7fffffu;
+  if (e == 0xff) return f ? 0 : (1ull << 53);          // NaN never, +inf always
+  if (e == 0) return f ? 1 : 0;                        // subnormal: k < tiny  <=> k == 0
+  const uint64_t mant = f | 0x800000u;                 // w = mant * 2^(e-150)
+  const int sh = static_cast<int>(e) - 97;             // w*2^53 = mant * 2^(e-97)
+  if (sh >= 30) return 1ull << 53;                     // w >= 1: every k fires
+  if (sh >= 0) return mant << sh;
+  const int rs = -sh;
+  if (rs >= 24) return 1;                              // 0 < w*2^53 < 1
+  return ((mant - 1) >> rs) + 1;                       // ceil(mant / 2^rs)
+}
+
+// ---------------------------------------------------------------------------
+// Per-lane visited set: open addressing over u64 entries (tag << 32 | vertex).
+// An entry is live only while its tag equals the lane's current tag, so a new
+// sample (or a rehash into a larger table) just bumps the tag -- tables are
+// never swept. Capacity grows 64 -> kTabCap keeping load <= 1/2.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kMemCap = 1024;  // members per lane before deferring to the big path
+constexpr uint32_t kTabCap = 2048;  // max table entries per lane (2 x kMemCap)
+constexpr uint32_t kTabLog0 = 6;    // initial table log2 capacity
+
+__device__ __forceinline__ uint32_t vhash(uint32_t v) { return v * 0x9E3779B1u; }
+
+__device__ __forceinline__ bool tab_contains(const uint64_t* tab, uint32_t tag, uint32_t lg,
+                                             uint32_t v) {
+  const uint32_t mask = (1u << lg) - 1;
+  uint32_t h = vhash(v) >> (32 - lg);
+  while (true) {
+    const uint64_t e = tab[h];
+    if (static_cast<uint32_t>(e >> 32) != tag) return false;
+    if (static_cast<uint32_t>(e) == v) return true;
+    h = (h + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ void tab_insert(uint64_t* tab, uint32_t tag, uint32_t lg, uint32_t v) {
+  const uint32_t mask = (1u << lg) - 1;
+  uint32_t h = vhash(v) >> (32 - lg);
+  while (static_cast<uint32_t>(tab[h] >> 32) == tag) h = (h + 1) & mask;
+  tab[h] = (static_cast<uint64_t>(tag) << 32) | v;
+}
+
+// 128-bit register filter in front of the table: a clear bit proves absence.
+struct Filter {
+  uint64_t lo, hi;
+  __device__ __forceinline__ void clear() { lo = hi = 0; }
+  __device__ __forceinline__ static uint32_t bit(uint32_t v) { return (v * 0x2545F491u) >> 25; }
+  __device__ __forceinline__ void add(uint32_t v) {
+    const uint32_t b = bit(v);
+    if (b & 64) hi |= 1ull << (b & 63);
+    else lo |= 1ull << (b & 63);
+  }
+  __device__ __forceinline__ bool maybe(uint32_t v) const {
+    const uint32_t b = bit(v);
+    const uint64_t w = (b & 64) ? hi : lo;
+    return (w >> (b & 63)) & 1;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Sampler control block (one per launch sequence of a generate_batch call).
+// ---------------------------------------------------------------------------
+struct SampleCtl {
+  unsigned long long next;        // batch-local slot dispenser
+  unsigned long long cursor;      // staging bump allocator (u32 units)
+  unsigned long long inspected;   // reference-equivalent in-edges inspected
+  unsigned long long entries;     // adjacency entries actually read by the kernel
+  unsigned long long deferred_members;  // members of sets refused for lack of staging
+  unsigned int ndeferred;         // slots handed to the big-set path
+  unsigned int pad;
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace rrgpu

@@ -1,0 +1,207 @@
+// internal.hpp -- host-side context objects and kernel launchers (not exported).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/rrgpu.h"
+#include "common.cuh"
+
+namespace rrgpu {
+
+void set_error(const std::string& msg);
+
+struct CudaError {
+  cudaError_t err;
+  std::string where;
+};
+
+#define RRG_CUDA(call)                                                   \
+  do {                                                                   \
+    cudaError_t e_ = (call);                                             \
+    if (e_ != cudaSuccess) throw ::rrgpu::CudaError{e_, #call};          \
+  } while (0)
+
+// Owning device buffer, grow-only.
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+  // Ensures capacity >= n elements; contents are NOT preserved.
+  void reserve_discard(size_t n) {
+    if (n <= cap) return;
+    release();
+    RRG_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+    cap = n;
+  }
+  // Ensures capacity >= n elements, preserving the first `keep` elements.
+  void reserve_keep(size_t n, size_t keep, cudaStream_t s) {
+    if (n <= cap) return;
+    T* np = nullptr;
+    RRG_CUDA(cudaMalloc(&np, n * sizeof(T)));
+    if (keep) RRG_CUDA(cudaMemcpyAsync(np, ptr, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    RRG_CUDA(cudaStreamSynchronize(s));
+    release();
+    ptr = np;
+    cap = n;
+  }
+};
+
+enum LtScan : int { kLtLinear = 0, kLtBsearch = 1 };
+
+// Per-lane sampler scratch: visit-order list + tagged hash table + tag.
+struct LaneScratch {
+  uint64_t lanes = 0;
+  DevBuf<uint32_t> lists;
+  DevBuf<uint64_t> tabs;
+  DevBuf<uint32_t> tags;
+};
+
+// Big-set path scratch: one n-bit map and one n-entry list per worker warp.
+struct BigScratch {
+  uint32_t workers = 0;
+  DevBuf<uint32_t> bitmaps;
+  DevBuf<uint32_t> lists;
+};
+
+}  // namespace rrgpu
+
+struct rrg_graph {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint32_t n = 0;
+  uint64_t m = 0;
+  rrgpu::DevBuf<uint32_t> off;   // u32[n+1] transpose offsets
+  rrgpu::DevBuf<uint32_t> src;   // u32[m]   transpose sources (CSR order = draw order)
+  rrgpu::DevBuf<float> w;        // f32[m]   transpose weights
+  rrgpu::DevBuf<uint2> rec;      // IC: {source, weight bits} per in-edge (lazy)
+  rrgpu::DevBuf<double> cdf;     // LT: sequential fp64 prefix per in-list (lazy, +2 pad)
+  bool rec_ready = false;
+  bool cdf_ready = false;
+  bool cdf_monotone = true;
+  int lt_scan = rrgpu::kLtLinear;
+  uint32_t coop_min = 64;        // LT: in-lists at least this long are scanned warp-cooperatively
+  uint32_t ic_inner = 8;         // IC: edge steps per flat-loop iteration
+  rrgpu::LaneScratch scratch;
+  rrgpu::BigScratch big;
+  rrgpu::DevBuf<rrgpu::SampleCtl> ctl;
+  rrg_batch_stats last{};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+struct rrg_store {
+  rrg_graph* g = nullptr;
+  uint64_t nsets = 0;
+  uint64_t total = 0;            // members stored
+  uint32_t max_len = 0;
+  bool counter_complete = true;  // every batch so far was fused
+  rrgpu::DevBuf<uint64_t> off;   // u64[nsets+1], slot order
+  rrgpu::DevBuf<uint32_t> mem;   // u32[total], visit order within a set (root first)
+  rrgpu::DevBuf<uint32_t> counter;  // fused occurrence histogram u32[n]
+  rrgpu::DevBuf<uint32_t> maxlen_dev;
+  // staging for one batch
+  rrgpu::DevBuf<uint32_t> stage;
+  rrgpu::DevBuf<uint64_t> slot_start;
+  rrgpu::DevBuf<uint32_t> slot_len;
+  rrgpu::DevBuf<uint32_t> deferred;
+  rrgpu::DevBuf<uint32_t> deferred2;
+  rrgpu::DevBuf<uint64_t> scan;
+  rrgpu::DevBuf<uint64_t> scan_tmp;
+  // selection scratch
+  rrgpu::DevBuf<uint32_t> wcnt;
+  rrgpu::DevBuf<uint64_t> ioff;
+  rrgpu::DevBuf<unsigned long long> icur;
+  rrgpu::DevBuf<uint32_t> inv;
+  rrgpu::DevBuf<uint32_t> covered;
+  rrgpu::DevBuf<unsigned long long> keys;
+  rrgpu::DevBuf<unsigned long long> marg;
+  rrgpu::DevBuf<uint32_t> seeds;
+  rrgpu::DevBuf<uint8_t> selected;
+  rrgpu::DevBuf<uint32_t> snap;
+  rrgpu::DevBuf<uint32_t> status;
+};
+
+namespace rrgpu {
+
+// ---- launchers (sample.cu) ------------------------------------------------
+struct SampleParams {
+  uint32_t n;
+  const uint32_t* off;
+  const uint2* rec;
+  const uint32_t* src;
+  const double* cdf;
+  uint64_t run_seed;
+  uint64_t base_slot;
+  uint64_t count;
+  uint32_t* lists;
+  uint64_t* tabs;
+  uint32_t* tags;
+  uint32_t* stage;
+  uint64_t stage_cap;
+  uint64_t* slot_start;
+  uint32_t* slot_len;
+  uint32_t* counter;
+  uint32_t* deferred;
+  SampleCtl* ctl;
+  int lt_scan;
+  uint32_t coop_min;
+};
+
+void prepare_ic(rrg_graph* g);
+void prepare_lt(rrg_graph* g);
+int sampler_block();
+int sampler_blocks_per_sm(int model, uint32_t ic_inner);
+void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, cudaStream_t s);
+void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t nlist,
+                uint32_t* bitmaps, uint32_t* lists, uint32_t workers, uint32_t* redefer,
+                cudaStream_t s);
+
+// ---- store.cu ---------------------------------------------------------------
+// out[i] = sum_{t<i} in[t] for i in [0, count]; tmp grows as needed.
+void exclusive_scan_u32(const uint32_t* in, uint64_t* out, uint64_t count, DevBuf<uint64_t>& tmp,
+                        cudaStream_t s);
+void launch_compact(const uint32_t* stage, const uint64_t* slot_start, const uint32_t* slot_len,
+                    const uint64_t* scan, uint64_t base_total, uint64_t count, uint32_t* mem_out,
+                    uint64_t* off_out, uint32_t* maxlen, cudaStream_t s);
+void launch_recount(const uint64_t* off, const uint32_t* mem, uint64_t nsets, uint32_t* counter,
+                    cudaStream_t s);
+void launch_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
+                   unsigned long long* icur, const uint64_t* ioff, uint32_t* inv,
+                   uint32_t* status, cudaStream_t s);
+void launch_fraction(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
+                     const uint8_t* in_seed_set, unsigned long long* hits, cudaStream_t s);
+
+// ---- select.cu --------------------------------------------------------------
+struct SelectParams {
+  uint32_t n;
+  uint32_t k;
+  uint32_t* cnt;
+  const uint64_t* ioff;
+  const uint32_t* inv;
+  const uint64_t* off;
+  const uint32_t* mem;
+  uint32_t* covered;
+  unsigned long long* keys;
+  unsigned long long* marg;
+  uint32_t* seeds;
+  uint8_t* selected;
+  uint32_t* snap;      // k*n or null
+  uint32_t* status;    // [0] = rounds completed
+};
+void launch_select(const SelectParams& p, int num_sms, cudaStream_t s);
+
+}  // namespace rrgpu

@@ -1,0 +1,462 @@
+// sample.cu -- K0 graph layouts and K1/K2 RRR samplers (IC / LT).
+//
+// Replaces generate_batch + generate_rrr_ic / generate_rrr_lt + fused
+// Counter::add of the reference (proj/include/rrflow/sampling.hpp:90-199).
+//
+// Execution model: a persistent grid where every LANE owns one sample at a time
+// and pulls the next batch-local slot from a warp-aggregated dispenser. The
+// lane replays the slot's xoshiro256** stream exactly (common.cuh), so each
+// set is bit-identical to the reference's whatever the schedule.
+//   IC (K1): reverse BFS; the lane walks in-lists in CSR order, drawing only for
+//            unvisited sources (sampling.hpp:102). Visited = 128-bit register
+//            filter + per-lane tagged hash table.
+//   LT (K2): reverse walk; one draw per step (sampling.hpp:127); "first j with
+//            draw < acc_j" is found on a precomputed sequential fp64 CDF, so the
+//            chosen index is bit-identical. Long in-lists are scanned by the
+//            whole warp with 16-byte loads (coalesced), short ones per lane; an
+//            optional binary-search mode picks the identical index.
+// Sets that outgrow the per-lane budget (kMemCap) -- or find the staging buffer
+// full -- are deferred to k_big (warp per set, n-bit visited map), which
+// replays the same stream from the start.
+#include <cooperative_groups.h>
+
+#include "internal.hpp"
+
+namespace rrgpu {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ void defer_slot(const SampleParams& p, uint32_t idx) {
+  const unsigned q = atomicAdd(&p.ctl->ndeferred, 1u);
+  p.deferred[q] = idx;  // at most one deferral per slot per launch: q < count
+}
+
+// Writes a finished set to staging, bumps the fused counter, records the slot.
+__device__ __forceinline__ void emit_set(const SampleParams& p, uint32_t idx, const uint32_t* mem,
+                                         uint32_t nmem) {
+  const unsigned long long pos = atomicAdd(&p.ctl->cursor, (unsigned long long)nmem);
+  if (pos + nmem > p.stage_cap) {
+    atomicAdd(&p.ctl->deferred_members, (unsigned long long)nmem);
+    defer_slot(p, idx);
+    return;
+  }
+  uint32_t* out = p.stage + pos;
+  for (uint32_t t = 0; t < nmem; ++t) {
+    const uint32_t v = mem[t];
+    out[t] = v;
+    if (p.counter) atomicAdd(p.counter + v, 1u);
+  }
+  p.slot_start[idx] = pos;
+  p.slot_len[idx] = nmem;
+}
+
+__device__ __forceinline__ void flush_counters(const SampleParams& p, uint64_t insp,
+                                               uint64_t ent) {
+  for (int o = 16; o; o >>= 1) {
+    insp += __shfl_xor_sync(kFull, insp, o);
+    ent += __shfl_xor_sync(kFull, ent, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&p.ctl->inspected, (unsigned long long)insp);
+    atomicAdd(&p.ctl->entries, (unsigned long long)ent);
+  }
+}
+
+// Warp-aggregated slot dispenser. Lanes with `need` get a batch-local index or
+// are marked exhausted.
+__device__ __forceinline__ bool fetch_slot(const SampleParams& p, bool need, bool& exhausted,
+                                           uint32_t& idx) {
+  const unsigned nm = __ballot_sync(kFull, need);
+  if (!nm) return false;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(nm) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(&p.ctl->next, (unsigned long long)__popc(nm));
+  base = __shfl_sync(kFull, base, leader);
+  if (!need) return false;
+  const uint64_t k = base + __popc(nm & lanemask_lt());
+  if (k >= p.count) {
+    exhausted = true;
+    return false;
+  }
+  idx = static_cast<uint32_t>(k);
+  return true;
+}
+
+// Inserts v into the lane's visited set (member list + table), growing the
+// table by rehash when the load would exceed 1/2.
+__device__ __forceinline__ void lane_insert(uint32_t* mem, uint64_t* tab, uint32_t& tag,
+                                            uint32_t& lg, uint32_t& nmem, uint32_t v) {
+  mem[nmem++] = v;
+  if (2 * nmem > (1u << lg)) {
+    ++lg;
+    ++tag;
+    for (uint32_t t = 0; t < nmem; ++t) tab_insert(tab, tag, lg, mem[t]);
+  } else {
+    tab_insert(tab, tag, lg, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: IC sampler (sampling.hpp:90-111 per slot, :177-189 per batch)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_sample_ic(const SampleParams p, const uint32_t inner) {
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t* mem = p.lists + gid * kMemCap;
+  uint64_t* tab = p.tabs + gid * kTabCap;
+  uint32_t tag = p.tags[gid];
+  Xoshiro rng{0, 0, 0, 0};
+  Filter flt;
+  flt.clear();
+  bool active = false, exhausted = false;
+  uint32_t idx = 0, nmem = 0, head = 0, lg = kTabLog0, j = 0, jend = 0;
+  uint64_t insp = 0;
+
+  for (;;) {
+    if (fetch_slot(p, !active && !exhausted, exhausted, idx)) {
+      rng.seed(stream_seed(p.run_seed, p.base_slot + idx));      // sampling.hpp:179
+      const uint32_t root = static_cast<uint32_t>(rng.below(p.n));  // :180
+      ++tag;
+      lg = kTabLog0;
+      flt.clear();
+      mem[0] = root;
+      nmem = 1;
+      head = 0;
+      j = jend = 0;
+      tab_insert(tab, tag, lg, root);
+      flt.add(root);
+      active = true;
+    }
+    if (__all_sync(kFull, !active)) break;
+    if (!active) continue;
+
+    if (j < jend) {
+      // in-edges of the current vertex, CSR order (sampling.hpp:100-106)
+      const uint32_t stop = min(jend, j + inner);
+      for (; j < stop; ++j) {
+        const uint2 r = p.rec[j];
+        const uint32_t v = r.x;
+        if (flt.maybe(v) && tab_contains(tab, tag, lg, v)) continue;  // visited: no draw
+        if (rng.u53() < bernoulli_threshold(r.y)) {
+          if (nmem == kMemCap) {
+            defer_slot(p, idx);
+            active = false;
+            break;
+          }
+          lane_insert(mem, tab, tag, lg, nmem, v);
+          flt.add(v);
+        }
+      }
+    } else if (head < nmem) {
+      const uint32_t u = mem[head++];  // FIFO dequeue (sampling.hpp:96-97)
+      j = p.off[u];
+      jend = p.off[u + 1];
+      insp += jend - j;
+    } else {
+      emit_set(p, idx, mem, nmem);
+      active = false;
+    }
+  }
+  p.tags[gid] = tag;
+  flush_counters(p, insp, insp);
+}
+
+// ---------------------------------------------------------------------------
+// K2: LT sampler (sampling.hpp:117-145 per slot)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t* mem = p.lists + gid * kMemCap;
+  uint64_t* tab = p.tabs + gid * kTabCap;
+  uint32_t tag = p.tags[gid];
+  Xoshiro rng{0, 0, 0, 0};
+  bool active = false, exhausted = false;
+  uint32_t idx = 0, nmem = 0, lg = kTabLog0, u = 0;
+  uint64_t insp = 0, ent = 0;
+  const bool linear = p.lt_scan == kLtLinear;
+
+  for (;;) {
+    if (fetch_slot(p, !active && !exhausted, exhausted, idx)) {
+      rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
+      u = static_cast<uint32_t>(rng.below(p.n));
+      ++tag;
+      lg = kTabLog0;
+      mem[0] = u;
+      nmem = 1;
+      tab_insert(tab, tag, lg, u);
+      active = true;
+    }
+    if (__all_sync(kFull, !active)) break;
+
+    // one walk step for every active lane
+    uint32_t b = 0, e = 0;
+    double d = 0.0;
+    if (active) {
+      d = rng.u01();  // sampling.hpp:127 -- always consumed
+      b = p.off[u];
+      e = p.off[u + 1];
+    }
+    uint32_t pick = e;  // index of the first cdf entry > d, or e for "none"
+    const bool coop = active && linear && (e - b) >= p.coop_min;
+    unsigned cm = __ballot_sync(kFull, coop);
+    while (cm) {
+      // warp-cooperative linear scan of one lane's long in-list: 64 entries per
+      // iteration, one 16-byte load per lane, first hit by ballot
+      const int L = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const uint32_t bL = __shfl_sync(kFull, b, L);
+      const uint32_t eL = __shfl_sync(kFull, e, L);
+      const double dL = __shfl_sync(kFull, d, L);
+      uint32_t found = eL;
+      uint32_t chunks = 0;
+      for (uint32_t base = bL & ~1u; base < eL; base += 64) {
+        const uint32_t i0 = base + 2 * lane;
+        bool h0 = false, h1 = false;
+        if (i0 < eL) {
+          const double2 c = __ldg(reinterpret_cast<const double2*>(p.cdf + i0));
+          h0 = i0 >= bL && dL < c.x;
+          h1 = i0 + 1 < eL && dL < c.y;
+        }
+        ++chunks;
+        const unsigned hm = __ballot_sync(kFull, h0 || h1);
+        if (hm) {
+          const int f = __ffs(hm) - 1;
+          const unsigned first0 = __ballot_sync(kFull, h0);
+          found = base + 2 * f + (((first0 >> f) & 1u) ? 0 : 1);
+          break;
+        }
+      }
+      if (lane == L) {
+        pick = found;
+        const uint64_t span = static_cast<uint64_t>(chunks) * 64;
+        ent += (span < (uint64_t)(eL - (bL & ~1u))) ? span : (uint64_t)(eL - (bL & ~1u));
+      }
+    }
+    if (active && !coop) {
+      if (linear) {
+        for (uint32_t t = b; t < e; ++t) {
+          if (d < p.cdf[t]) {
+            pick = t;
+            break;
+          }
+        }
+        ent += (pick < e ? pick + 1 : e) - b;
+      } else {
+        // upper_bound: first cdf[t] > d (cdf is non-decreasing)
+        uint32_t lo = b, hi = e;
+        while (lo < hi) {
+          const uint32_t mid = lo + ((hi - lo) >> 1);
+          ++ent;
+          if (p.cdf[mid] > d) hi = mid;
+          else lo = mid + 1;
+        }
+        pick = lo;
+      }
+    }
+    if (!active) continue;
+    insp += (pick < e ? pick + 1 : e) - b;  // reference trip count (sampling.hpp:130-136)
+    bool stop = pick >= e;
+    uint32_t v = 0;
+    if (!stop) {
+      v = p.src[pick];
+      stop = tab_contains(tab, tag, lg, v);  // chosen already visited (:137)
+    }
+    if (stop) {
+      emit_set(p, idx, mem, nmem);
+      active = false;
+    } else if (nmem == kMemCap) {
+      defer_slot(p, idx);
+      active = false;
+    } else {
+      lane_insert(mem, tab, tag, lg, nmem, v);
+      u = v;
+    }
+  }
+  p.tags[gid] = tag;
+  flush_counters(p, insp, ent);
+}
+
+// ---------------------------------------------------------------------------
+// Big-set path: warp per deferred slot, n-bit visited map, lane 0 replays the
+// reference loop serially; the warp writes out and clears the map.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, const int model,
+                                                       const uint32_t* list, const uint32_t nlist,
+                                                       uint32_t* bitmaps, uint32_t* lists,
+                                                       const uint32_t workers, uint32_t* redefer) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= workers) return;
+  const uint64_t words = (static_cast<uint64_t>(p.n) + 31) / 32;
+  uint32_t* vis = bitmaps + w * words;
+  uint32_t* mem = lists + static_cast<uint64_t>(w) * p.n;
+  uint64_t insp = 0;
+  for (uint32_t t = w; t < nlist; t += workers) {
+    const uint32_t idx = list[t];
+    uint32_t nmem = 0;
+    if (lane == 0) {
+      Xoshiro rng;
+      rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
+      const uint32_t root = static_cast<uint32_t>(rng.below(p.n));
+      mem[0] = root;
+      nmem = 1;
+      vis[root >> 5] |= 1u << (root & 31);
+      if (model == RRG_IC) {
+        for (uint32_t head = 0; head < nmem; ++head) {
+          const uint32_t uu = mem[head];
+          const uint32_t jb = p.off[uu], je = p.off[uu + 1];
+          insp += je - jb;
+          for (uint32_t j = jb; j < je; ++j) {
+            const uint2 r = p.rec[j];
+            if ((vis[r.x >> 5] >> (r.x & 31)) & 1u) continue;
+            if (rng.u53() < bernoulli_threshold(r.y)) {
+              vis[r.x >> 5] |= 1u << (r.x & 31);
+              mem[nmem++] = r.x;
+            }
+          }
+        }
+      } else {
+        uint32_t uu = root;
+        for (;;) {
+          const double d = rng.u01();
+          const uint32_t jb = p.off[uu], je = p.off[uu + 1];
+          uint32_t pick = je;
+          for (uint32_t j = jb; j < je; ++j) {
+            if (d < p.cdf[j]) {
+              pick = j;
+              break;
+            }
+          }
+          insp += (pick < je ? pick + 1 : je) - jb;
+          if (pick >= je) break;
+          const uint32_t v = p.src[pick];
+          if ((vis[v >> 5] >> (v & 31)) & 1u) break;
+          vis[v >> 5] |= 1u << (v & 31);
+          mem[nmem++] = v;
+          uu = v;
+        }
+      }
+    }
+    nmem = __shfl_sync(kFull, nmem, 0);
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(&p.ctl->cursor, (unsigned long long)nmem);
+    pos = __shfl_sync(kFull, pos, 0);
+    __syncwarp();
+    if (pos + nmem > p.stage_cap) {
+      if (lane == 0) {
+        atomicAdd(&p.ctl->deferred_members, (unsigned long long)nmem);
+        redefer[atomicAdd(&p.ctl->ndeferred, 1u)] = idx;
+      }
+    } else {
+      for (uint32_t i = lane; i < nmem; i += 32) {
+        const uint32_t v = mem[i];
+        p.stage[pos + i] = v;
+        if (p.counter) atomicAdd(p.counter + v, 1u);
+      }
+      if (lane == 0) {
+        p.slot_start[idx] = pos;
+        p.slot_len[idx] = nmem;
+      }
+    }
+    for (uint32_t i = lane; i < nmem; i += 32) {
+      const uint32_t v = mem[i];
+      atomicAnd(vis + (v >> 5), ~(1u << (v & 31)));
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    atomicAdd(&p.ctl->inspected, (unsigned long long)insp);
+    atomicAdd(&p.ctl->entries, (unsigned long long)insp);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K0: per-model layouts
+// ---------------------------------------------------------------------------
+__global__ void k_build_rec(const uint32_t* src, const float* w, uint2* rec, uint64_t m) {
+  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    rec[j] = make_uint2(src[j], __float_as_uint(w[j]));
+  }
+}
+
+// Sequential fp64 prefix per in-list, the exact add order of sampling.hpp:128-131.
+// One thread per vertex; `bad` flags a non-monotone prefix (NaN / negative weight).
+__global__ void k_build_cdf(const uint32_t* off, const float* w, double* cdf, uint32_t n,
+                            uint32_t* bad) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    const uint32_t e = off[v + 1];
+    for (uint32_t j = off[v]; j < e; ++j) {
+      const float x = w[j];
+      if (!(x >= 0.0f)) *bad = 1;
+      acc = __dadd_rn(acc, static_cast<double>(x));
+      cdf[j] = acc;
+    }
+  }
+}
+
+}  // namespace
+
+int sampler_block() { return kBlock; }
+
+int sampler_blocks_per_sm(int model, uint32_t) {
+  int b = 0;
+  if (model == RRG_IC)
+    RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_ic, kBlock, 0));
+  else
+    RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_lt, kBlock, 0));
+  return b < 1 ? 1 : b;
+}
+
+void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner,
+                    cudaStream_t s) {
+  if (model == RRG_IC)
+    k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
+  else
+    k_sample_lt<<<grid, kBlock, 0, s>>>(p);
+  RRG_CUDA(cudaGetLastError());
+}
+
+void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t nlist,
+                uint32_t* bitmaps, uint32_t* lists, uint32_t workers, uint32_t* redefer,
+                cudaStream_t s) {
+  const int grid = static_cast<int>((workers * 32 + kBlock - 1) / kBlock);
+  k_sample_big<<<grid, kBlock, 0, s>>>(p, model, list, nlist, bitmaps, lists, workers, redefer);
+  RRG_CUDA(cudaGetLastError());
+}
+
+void prepare_ic(rrg_graph* g) {
+  if (g->rec_ready) return;
+  g->rec.reserve_discard(g->m ? g->m : 1);
+  if (g->m) {
+    k_build_rec<<<g->num_sms * 8, 256, 0, g->stream>>>(g->src.ptr, g->w.ptr, g->rec.ptr, g->m);
+    RRG_CUDA(cudaGetLastError());
+  }
+  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  g->rec_ready = true;
+}
+
+void prepare_lt(rrg_graph* g) {
+  if (g->cdf_ready) return;
+  g->cdf.reserve_discard(g->m + 2);  // +2: the paired 16-byte loads may touch cdf[m]
+  RRG_CUDA(cudaMemsetAsync(g->cdf.ptr, 0, (g->m + 2) * sizeof(double), g->stream));
+  DevBuf<uint32_t> bad;
+  bad.reserve_discard(1);
+  RRG_CUDA(cudaMemsetAsync(bad.ptr, 0, 4, g->stream));
+  if (g->m) {
+    const int blocks = (g->n + 127) / 128;
+    k_build_cdf<<<blocks, 128, 0, g->stream>>>(g->off.ptr, g->w.ptr, g->cdf.ptr, g->n, bad.ptr);
+    RRG_CUDA(cudaGetLastError());
+  }
+  uint32_t hbad = 0;
+  RRG_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
+  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  g->cdf_monotone = hbad == 0;
+  g->cdf_ready = true;
+}
+
+}  // namespace rrgpu

@@ -1,0 +1,232 @@
+// store.cu -- K3 stream compaction into the slot-ordered flat RRR buffer, the
+// hand-written exclusive scan it uses, K4 standalone recount, K5 inverted index.
+//
+// Replaces RRRStore::place / finalize (rrr_store.hpp:41-60), build_counter
+// (selection.hpp:79-95) and the membership probes of decrement_update
+// (selection.hpp:137-149), which become a vertex -> set-id index.
+#include "internal.hpp"
+
+namespace rrgpu {
+
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr uint64_t kTile = static_cast<uint64_t>(kScanThreads) * kScanItems;
+
+// Block-wide exclusive scan of one value per thread; returns the block total.
+__device__ __forceinline__ uint64_t block_exclusive(uint64_t v, uint64_t& excl) {
+  __shared__ uint64_t warp_tot[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t incl = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t t = lane < kScanThreads / 32 ? warp_tot[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(kFull, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < kScanThreads / 32) warp_tot[lane] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const uint64_t warp_base = wid ? warp_tot[wid - 1] : 0;
+  const uint64_t total = warp_tot[kScanThreads / 32 - 1];
+  excl = warp_base + incl - v;
+  __syncthreads();
+  return total;
+}
+
+// Tile-local exclusive scan; tile totals to `sums`.
+template <typename TIn>
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_tiles(const TIn* in, uint64_t* out, uint64_t count, uint64_t* sums) {
+  const uint64_t base = blockIdx.x * kTile + static_cast<uint64_t>(threadIdx.x) * kScanItems;
+  uint64_t vals[kScanItems];
+  uint64_t local = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const uint64_t idx = base + i;
+    vals[i] = idx < count ? static_cast<uint64_t>(in[idx]) : 0;
+    local += vals[i];
+  }
+  uint64_t excl;
+  const uint64_t total = block_exclusive(local, excl);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const uint64_t idx = base + i;
+    if (idx < count) out[idx] = excl;
+    excl += vals[i];
+  }
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void k_scan_add(uint64_t* out, uint64_t count, const uint64_t* tile_prefix) {
+  const uint64_t idx = blockIdx.x * kTile + threadIdx.x;
+  const uint64_t add = tile_prefix[blockIdx.x];
+  for (int i = 0; i < kScanItems; ++i) {
+    const uint64_t t = idx + static_cast<uint64_t>(i) * kScanThreads;
+    if (t < count) out[t] += add;
+  }
+}
+
+__global__ void k_set_total(uint64_t* out, uint64_t count, const uint64_t* sums_scan,
+                            const uint64_t* sums, uint64_t ntiles) {
+  out[count] = sums_scan[ntiles - 1] + sums[ntiles - 1];
+}
+
+// exclusive scan of u64 values (tile sums) -- recursion helper
+void scan_u64_rec(const uint64_t* in, uint64_t* out, uint64_t count, DevBuf<uint64_t>& tmp,
+                  uint64_t tmp_off, cudaStream_t s);
+
+template <typename TIn>
+void scan_impl(const TIn* in, uint64_t* out, uint64_t count, DevBuf<uint64_t>& tmp,
+               uint64_t tmp_off, cudaStream_t s) {
+  const uint64_t ntiles = (count + kTile - 1) / kTile;
+  uint64_t* sums = tmp.ptr + tmp_off;
+  uint64_t* sums_scan = sums + ntiles;
+  k_scan_tiles<TIn><<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(in, out, count, sums);
+  RRG_CUDA(cudaGetLastError());
+  if (ntiles > 1) {
+    scan_u64_rec(sums, sums_scan, ntiles, tmp, tmp_off + 2 * ntiles + 1, s);
+    k_scan_add<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(out, count, sums_scan);
+    RRG_CUDA(cudaGetLastError());
+  } else {
+    RRG_CUDA(cudaMemsetAsync(sums_scan, 0, sizeof(uint64_t), s));
+  }
+  k_set_total<<<1, 1, 0, s>>>(out, count, sums_scan, sums, ntiles);
+  RRG_CUDA(cudaGetLastError());
+}
+
+void scan_u64_rec(const uint64_t* in, uint64_t* out, uint64_t count, DevBuf<uint64_t>& tmp,
+                  uint64_t tmp_off, cudaStream_t s) {
+  scan_impl<uint64_t>(in, out, count, tmp, tmp_off, s);
+}
+
+uint64_t scan_tmp_words(uint64_t count) {
+  uint64_t words = 0;
+  while (true) {
+    const uint64_t ntiles = (count + kTile - 1) / kTile;
+    words += 2 * ntiles + 2;
+    if (ntiles <= 1) break;
+    count = ntiles;
+  }
+  return words;
+}
+
+// K3: warp per set, copies staging -> slot-ordered buffer, writes offsets.
+__global__ void k_compact(const uint32_t* stage, const uint64_t* slot_start,
+                          const uint32_t* slot_len, const uint64_t* scan, uint64_t base_total,
+                          uint64_t count, uint32_t* mem_out, uint64_t* off_out,
+                          uint32_t* maxlen) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * blockDim.x / 32;
+  uint32_t mx = 0;
+  for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; i < count;
+       i += warps) {
+    const uint32_t len = slot_len[i];
+    const uint32_t* from = stage + slot_start[i];
+    const uint64_t dst = base_total + scan[i];
+    for (uint32_t t = lane; t < len; t += 32) mem_out[dst + t] = from[t];
+    if (lane == 0) off_out[i + 1] = dst + len;
+    mx = max(mx, len);
+  }
+  if (lane == 0 && mx) atomicMax(maxlen, mx);
+}
+
+// K4: occurrence histogram over stored sets (build_counter, selection.hpp:79-95).
+__global__ void k_recount(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
+                          uint32_t* counter) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * blockDim.x / 32;
+  for (uint64_t s = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; s < nsets;
+       s += warps) {
+    for (uint64_t t = off[s] + lane; t < off[s + 1]; t += 32) atomicAdd(counter + mem[t], 1u);
+  }
+}
+
+// K5: vertex -> ids of the sets containing it. icur starts at ioff[v].
+__global__ void k_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
+                         unsigned long long* icur, const uint64_t* ioff, uint32_t* inv,
+                         uint32_t* status) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * blockDim.x / 32;
+  for (uint64_t s = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; s < nsets;
+       s += warps) {
+    for (uint64_t t = off[s] + lane; t < off[s + 1]; t += 32) {
+      const uint32_t v = mem[t];
+      const unsigned long long pos = atomicAdd(icur + v, 1ull);
+      if (pos < ioff[v + 1]) inv[pos] = static_cast<uint32_t>(s);
+      else status[1] = 1;  // prebuilt counter disagrees with the stored sets
+    }
+  }
+}
+
+// fraction_covered helper: sets with a member flagged in `in_seed_set`.
+__global__ void k_fraction(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
+                           const uint8_t* flag, unsigned long long* hits) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * blockDim.x / 32;
+  unsigned long long local = 0;
+  for (uint64_t s = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; s < nsets;
+       s += warps) {
+    bool hit = false;
+    for (uint64_t t = off[s] + lane; t < off[s + 1] && !hit; t += 32) hit = flag[mem[t]] != 0;
+    if (__any_sync(kFull, hit) && lane == 0) ++local;
+  }
+  if (lane == 0 && local) atomicAdd(hits, local);
+}
+
+int grid_for(uint64_t warps_needed) {
+  const uint64_t blocks = (warps_needed * 32 + 255) / 256;
+  return static_cast<int>(blocks < 1 ? 1 : (blocks > 65535 ? 65535 : blocks));
+}
+
+}  // namespace
+
+void exclusive_scan_u32(const uint32_t* in, uint64_t* out, uint64_t count, DevBuf<uint64_t>& tmp,
+                        cudaStream_t s) {
+  if (count == 0) {
+    RRG_CUDA(cudaMemsetAsync(out, 0, sizeof(uint64_t), s));
+    return;
+  }
+  tmp.reserve_discard(scan_tmp_words(count));
+  scan_impl<uint32_t>(in, out, count, tmp, 0, s);
+}
+
+void launch_compact(const uint32_t* stage, const uint64_t* slot_start, const uint32_t* slot_len,
+                    const uint64_t* scan, uint64_t base_total, uint64_t count, uint32_t* mem_out,
+                    uint64_t* off_out, uint32_t* maxlen, cudaStream_t s) {
+  if (!count) return;
+  k_compact<<<grid_for(count), 256, 0, s>>>(stage, slot_start, slot_len, scan, base_total, count,
+                                            mem_out, off_out, maxlen);
+  RRG_CUDA(cudaGetLastError());
+}
+
+void launch_recount(const uint64_t* off, const uint32_t* mem, uint64_t nsets, uint32_t* counter,
+                    cudaStream_t s) {
+  if (!nsets) return;
+  k_recount<<<grid_for(nsets), 256, 0, s>>>(off, mem, nsets, counter);
+  RRG_CUDA(cudaGetLastError());
+}
+
+void launch_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
+                   unsigned long long* icur, const uint64_t* ioff, uint32_t* inv,
+                   uint32_t* status, cudaStream_t s) {
+  if (!nsets) return;
+  k_invert<<<grid_for(nsets), 256, 0, s>>>(off, mem, nsets, icur, ioff, inv, status);
+  RRG_CUDA(cudaGetLastError());
+}
+
+void launch_fraction(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
+                     const uint8_t* in_seed_set, unsigned long long* hits, cudaStream_t s) {
+  if (!nsets) return;
+  k_fraction<<<grid_for(nsets), 256, 0, s>>>(off, mem, nsets, in_seed_set, hits);
+  RRG_CUDA(cudaGetLastError());
+}
+
+}  // namespace rrgpu

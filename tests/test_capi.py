@@ -1,0 +1,100 @@
+"""The C-ABI library (CPU only): loads, exports every symbol include/rrgpu.h
+declares, and its host-side pieces behave (no device compute calls here)."""
+import ctypes
+import os
+import re
+import struct
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "rrgpu.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(rrg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2411_09473_b200._lib as L
+    lib = ctypes.CDLL(L.LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 25
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    bound = {name for name, _, _ in L.SIGNATURES}
+    assert set(syms) == bound, set(syms) ^ bound
+
+
+def test_library_is_sm100a():
+    import paper_2411_09473_b200._lib as L
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {L.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out, out
+
+
+def test_version_and_errors():
+    import paper_2411_09473_b200 as P
+    assert "sm_100a" in P.version()
+    with pytest.raises(ValueError):
+        P.build_graph(3, [0, 5], [1, 1], [0.5, 0.5])  # id out of range
+
+
+def f32_bits(x):
+    return struct.unpack("<I", struct.pack("<f", x))[0]
+
+
+def test_bernoulli_threshold_equals_double_compare():
+    """uniform01() < (double)w  <=>  (x >> 11) < threshold(w)   (prng.hpp:46, :62)."""
+    from paper_2411_09473_b200._lib import lib
+    rng = np.random.default_rng(1)
+    weights = list(rng.random(300).astype(np.float32)) + [
+        0.0, -0.0, 1.0, 1.5, 1e-45, 1e-40, 1e-30, 2.0 ** -24, 2.0 ** -53, 2.0 ** -54,
+        np.float32(0.1), np.float32(1 / 3), float("inf"), -1.0, float("nan"),
+        np.nextafter(np.float32(1.0), np.float32(0.0))]
+    for w in weights:
+        w32 = np.float32(w)
+        t = lib.rrg_debug_bernoulli_threshold(f32_bits(float(w32)))
+        ks = [0, 1, 2, 2**52, 2**53 - 1, int(rng.integers(0, 2**53))]
+        if 0 < t < 2**53:
+            ks += [t - 1, t, t + 1]
+        for k in ks:
+            if k < 0 or k >= 2**53:
+                continue
+            expect = (k * 2.0 ** -53) < float(w32)
+            assert (k < t) == expect, (w, k, t)
+
+
+def test_generators_are_deterministic_and_simple():
+    from paper_2411_09473_b200 import graphs
+    for name, n, m in [("cfg1", 1 << 10, 1 << 13), ("cfg3", 5000, 40000), ("cfg4", 5000, 40000),
+                       ("cfg5", 3000, 20000)]:
+        cfg = graphs.scaled(graphs.CONFIGS[name], n, m)
+        a = graphs.generate(cfg, threads=1)
+        b = graphs.generate(cfg, threads=5)
+        for x, y in zip(a, b):
+            assert (x == y).all()
+        roff, rsrc, rw = a
+        deg = np.diff(roff.astype(np.int64))
+        dst = np.repeat(np.arange(deg.size), deg)
+        key = dst * (1 << 32) + rsrc.astype(np.int64)
+        assert (np.diff(key) > 0).all()  # in-lists by source ascending, no duplicates
+        assert not (rsrc == dst).any()  # no self-loops
+        expect_arcs = 2 * cfg.m if cfg.kind == graphs.CHUNG_LU_UNDIR else cfg.m
+        assert rsrc.size == expect_arcs
+        if cfg.weights == graphs.W_LT:
+            sums = np.add.reduceat(rw.astype(np.float64), roff[:-1].astype(np.int64))[deg > 0]
+            assert (sums <= 1.0).all() and (rw >= 0).all()
+        if cfg.weights == graphs.W_WC:
+            assert np.allclose(rw, np.repeat(1.0 / np.maximum(deg, 1), deg).astype(np.float32))
+
+
+def test_undirected_generator_is_symmetric():
+    from paper_2411_09473_b200 import graphs
+    cfg = graphs.scaled(graphs.CONFIGS["cfg5"], 3000, 20000)
+    roff, rsrc, _ = graphs.generate(cfg)
+    deg = np.diff(roff.astype(np.int64))
+    dst = np.repeat(np.arange(deg.size), deg)
+    fwd = set(zip(rsrc.tolist(), dst.tolist()))
+    assert all((d, s) in fwd for s, d in fwd)

@@ -1,0 +1,189 @@
+"""GPU sampling parity: every RRR set bit-identical to the reference's, slot by slot.
+
+Re-expresses proj/tests/test_sampling.cpp and the per-slot parity contract of
+SURVEY.md section 8(c) against the CUDA path (librrgpu.so through the C ABI).
+"""
+import numpy as np
+import pytest
+
+import paper_2411_09473_b200 as P
+from paper_2411_09473_b200 import graphs
+from helpers import assert_sets_equal
+
+pytestmark = pytest.mark.gpu
+
+IC, LT = 0, 1
+
+
+def gpu_sample(arrays, model, run_seed, count, fused=True, chunks=1, **opts):
+    g = P.Graph(*arrays)
+    for k, v in opts.items():
+        g.set_option(k, v)
+    st = P.RRRStore(g)
+    per = [count // chunks] * chunks
+    per[-1] += count - sum(per)
+    for c in per:
+        P.generate_batch(g, model, run_seed, c, st, fused=fused)
+    off, mem = st.export()
+    return g, st, off, mem
+
+
+SMALL = [
+    ("cfg1", IC, 1 << 11, 1 << 15),
+    ("cfg2", LT, 1 << 11, 1 << 15),
+    ("cfg3", IC, 30000, 500000),
+    ("cfg4", LT, 40000, 600000),
+    ("cfg5", IC, 20000, 300000),
+]
+
+
+@pytest.mark.parametrize("name,model,n,m", SMALL)
+def test_sets_match_reference_per_slot(cuda, oracle, name, model, n, m):
+    cfg = graphs.scaled(graphs.CONFIGS[name], n, m)
+    arrays = graphs.generate(cfg)
+    count = 3000
+    g, st, off, mem = gpu_sample(arrays, model, 1, count)
+    ref = oracle.graph(*arrays).sample(model, 1, 0, count, workers=4)
+    assert_sets_equal(off, mem, ref, msg=name)
+    assert (st.counter() == ref.counter).all(), "fused counter differs"
+    stats = g.last_batch_stats()
+    assert stats.sets == count
+    assert stats.members == ref.members.size
+
+
+@pytest.mark.parametrize("model", [IC, LT])
+def test_top_ups_continue_the_slot_stream(cuda, oracle, model):
+    """Slots continue across generate_batch calls (rrr_store.hpp:34-39)."""
+    cfg = graphs.scaled(graphs.CONFIGS["cfg1" if model == IC else "cfg2"], 1 << 10, 1 << 14)
+    arrays = graphs.generate(cfg)
+    _, st, off, mem = gpu_sample(arrays, model, 7, 2500, chunks=3)
+    ref = oracle.graph(*arrays).sample(model, 7, 0, 2500, workers=4)
+    assert_sets_equal(off, mem, ref)
+    assert (st.counter() == ref.counter).all()
+
+
+def test_lt_binary_search_mode_is_identical(cuda, oracle):
+    cfg = graphs.scaled(graphs.CONFIGS["cfg4"], 40000, 600000)
+    arrays = graphs.generate(cfg)
+    _, st_a, off_a, mem_a = gpu_sample(arrays, LT, 3, 4000, lt_scan=0)
+    _, st_b, off_b, mem_b = gpu_sample(arrays, LT, 3, 4000, lt_scan=1)
+    assert (off_a == off_b).all() and (mem_a == mem_b).all()
+    ref = oracle.graph(*arrays).sample(LT, 3, 0, 4000, workers=4)
+    assert_sets_equal(off_b, mem_b, ref)
+
+
+@pytest.mark.parametrize("coop_min", [2, 7, 64, 1 << 30])
+def test_lt_cooperative_scan_threshold_changes_nothing(cuda, oracle, coop_min):
+    cfg = graphs.scaled(graphs.CONFIGS["cfg2"], 1 << 10, 1 << 14)
+    arrays = graphs.generate(cfg)
+    _, _, off, mem = gpu_sample(arrays, LT, 11, 1500, lt_coop_min=coop_min)
+    ref = oracle.graph(*arrays).sample(LT, 11, 0, 1500)
+    assert_sets_equal(off, mem, ref)
+
+
+@pytest.mark.parametrize("inner", [1, 3, 32])
+def test_ic_inner_steps_change_nothing(cuda, oracle, inner):
+    cfg = graphs.scaled(graphs.CONFIGS["cfg1"], 1 << 10, 1 << 14)
+    arrays = graphs.generate(cfg)
+    _, _, off, mem = gpu_sample(arrays, IC, 5, 1500, ic_inner=inner)
+    ref = oracle.graph(*arrays).sample(IC, 5, 0, 1500)
+    assert_sets_equal(off, mem, ref)
+
+
+def test_reference_synth_graphs(cuda, ref):
+    """The reference's own fixtures (test_sampling.cpp:132-164) through the GPU."""
+    for (kind, n, frac, gseed, wseed, model, rseed, count) in [
+        (1, 300, 0.25, 13, 5, IC, 99, 500),
+        (1, 120, 0.3, 3, 21, LT, 7, 400),
+        (1, 200, 0.2, 17, 11, IC, 31, 200),
+        (1, 200, 0.2, 17, 11, LT, 31, 200),
+        (0, 64, 0.03, 77, 1, IC, 5, 300),
+    ]:
+        arrays = ref.synth_graph(kind, n, frac, gseed, wseed)
+        _, st, off, mem = gpu_sample(arrays, model, rseed, count)
+        orc = ref.graph(*arrays).sample(model, rseed, 0, count, workers=3)
+        assert_sets_equal(off, mem, orc, msg=f"synth {kind} {n}")
+        assert (st.counter() == orc.counter).all()
+
+
+def test_big_set_path(cuda, oracle):
+    """Dense IC (weights near 1) makes sets exceed the per-lane budget (1024),
+    exercising the deferred warp-per-set path."""
+    rng = np.random.default_rng(5)
+    n, m = 6000, 60000
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    w = rng.uniform(0.2, 0.6, src.size).astype(np.float32)
+    arrays = P.build_graph(n, src, dst, w)
+    g, st, off, mem = gpu_sample(arrays, IC, 9, 600)
+    assert g.last_batch_stats().deferred > 0
+    ref = oracle.graph(*arrays).sample(IC, 9, 0, 600, workers=4)
+    assert_sets_equal(off, mem, ref)
+    assert (st.counter() == ref.counter).all()
+
+
+def test_duplicate_edges_and_weights_edge_cases(cuda, oracle):
+    """Parallel edges (kept by load_edge_list, graph.hpp:163-165), zero, one,
+    subnormal and >1 weights, isolated vertices."""
+    edges = [(0, 1, 0.5), (0, 1, 0.5), (2, 1, 1.0), (3, 1, 0.0), (4, 1, 1e-40),
+             (1, 2, 2.0), (5, 2, 0.25), (5, 2, 0.25), (6, 0, 0.999999)]
+    n = 8
+    src = np.array([e[0] for e in edges], np.uint32)
+    dst = np.array([e[1] for e in edges], np.uint32)
+    w = np.array([e[2] for e in edges], np.float32)
+    arrays = P.build_graph(n, src, dst, w)
+    for model in (IC, LT):
+        if model == LT:
+            arrays = (arrays[0], arrays[1], P.normalize_lt_weights(arrays[0], arrays[2].copy()))
+        _, st, off, mem = gpu_sample(arrays, model, 3, 2000)
+        ref = oracle.graph(*arrays).sample(model, 3, 0, 2000)
+        assert_sets_equal(off, mem, ref)
+
+
+def test_single_vertex_and_count_zero(cuda):
+    """test_sampling.cpp:111-130."""
+    g = P.Graph.from_edges(1, [])
+    st = P.RRRStore(g)
+    assert P.generate_batch(g, IC, 1, 0, st) == 0
+    assert st.size() == 0
+    P.generate_batch_fused(g, IC, 1, 7, st)
+    assert st.size() == 7
+    assert st.counter().tolist() == [7]
+    assert all(len(s) == 1 for s in st.sets())
+
+
+def test_deterministic_sketches(cuda):
+    """Isolated root; forced reverse edge (test_sampling.cpp:44-59, :80-87)."""
+    g = P.Graph.from_edges(2, [(0, 1, 1.0)])
+    for model in (IC, LT):
+        st = P.RRRStore(g)
+        P.generate_batch(g, model, 123, 200, st)
+        for s in st.sets(sort=False):
+            assert (s.tolist() == [0]) or (s.tolist() == [1, 0])
+
+
+def test_bernoulli_and_categorical_rates(cuda):
+    """test_sampling.cpp:61-72 (0.5 +- 0.01) and :89-109 (0.3/0.3/0.4 +- 0.01)."""
+    g = P.Graph.from_edges(2, [(0, 1, 0.5)])
+    st = P.RRRStore(g)
+    P.generate_batch(g, IC, 4242, 100000, st)
+    sets = st.sets()
+    with_root1 = [s for s in sets if 1 in s]
+    rate = np.mean([0 in s for s in with_root1])
+    assert abs(rate - 0.5) < 0.01
+    g = P.Graph.from_edges(3, [(0, 2, 0.3), (1, 2, 0.3)])
+    st = P.RRRStore(g)
+    P.generate_batch(g, LT, 777, 300000, st)
+    rooted = [s for s in st.sets(sort=False) if s[0] == 2]
+    a1 = np.mean([0 in s for s in rooted])
+    a2 = np.mean([1 in s for s in rooted])
+    assert abs(a1 - 0.3) < 0.01 and abs(a2 - 0.3) < 0.01 and abs(1 - a1 - a2 - 0.4) < 0.01
+
+
+def test_empty_graph_is_rejected(cuda):
+    g = P.Graph(np.zeros(1, np.uint64), np.zeros(0, np.uint32), np.zeros(0, np.float32))
+    st = P.RRRStore(g)
+    with pytest.raises(ValueError):
+        P.generate_batch(g, IC, 1, 5, st)

@@ -1,0 +1,130 @@
+"""GPU selection parity: given the identical RRR-set collection, the coverage
+counts, seeds and marginals are bit-exact with the reference's select_seeds.
+
+Re-expresses proj/tests/test_selection.cpp and acceptance.cpp criteria 01-03.
+"""
+import numpy as np
+import pytest
+
+import paper_2411_09473_b200 as P
+from helpers import random_store
+
+pytestmark = pytest.mark.gpu
+
+
+def store_from_lists(n, lists):
+    g = P.Graph(np.zeros(n + 1, np.uint64), np.zeros(0, np.uint32), np.zeros(0, np.float32))
+    st = P.RRRStore(g)
+    off = np.zeros(len(lists) + 1, np.uint64)
+    for i, l in enumerate(lists):
+        off[i + 1] = off[i] + len(l)
+    mem = np.array([v for l in lists for v in l], np.uint32)
+    if len(lists):
+        st.import_sets(off, mem)
+    return g, st
+
+
+def test_hand_greedy(cuda):
+    """test_selection.cpp:139-153."""
+    g, st = store_from_lists(3, [[0, 1], [0], [2]])
+    s = P.select_seeds(st, 3, 2)
+    assert s.seeds == [0, 2] and s.marginal_counts == [2, 1]
+    g, st = store_from_lists(4, [[1, 2], [1], [3]])
+    s = P.select_seeds(st, 4, 1)
+    assert s.seeds == [1] and s.marginal_counts == [2]
+
+
+def test_k_bounds_and_empty_store_fill(cuda):
+    """test_selection.cpp:155-164."""
+    g, st = store_from_lists(3, [[0]])
+    with pytest.raises(ValueError):
+        P.select_seeds(st, 3, 4)
+    with pytest.raises(ValueError):
+        P.select_seeds(st, 3, 0)
+    g, st = store_from_lists(5, [])
+    s = P.select_seeds(st, 5, 3)
+    assert s.seeds == [0, 1, 2] and s.marginal_counts == [0, 0, 0]
+
+
+def test_ties_go_to_lowest_id(cuda):
+    """test_selection.cpp:43-55 via one-round selection."""
+    g, st = store_from_lists(3, [[0], [0], [0], [1], [2]])
+    assert P.select_seeds(st, 3, 1).seeds == [0]
+    g, st = store_from_lists(3, [[0], [0], [1], [1], [2]])
+    assert P.select_seeds(st, 3, 1).seeds == [0]
+    g, st = store_from_lists(5, [[4], [3], [3], [4]])
+    assert P.select_seeds(st, 5, 1).seeds == [3]
+
+
+def test_exhaustion_fill_skips_selected(cuda):
+    g, st = store_from_lists(6, [[3], [3, 4], [5]])
+    s = P.select_seeds(st, 6, 5)
+    assert s.seeds == [3, 5, 0, 1, 2] and s.marginal_counts == [2, 1, 0, 0, 0]
+
+
+@pytest.mark.parametrize("trial", range(12))
+def test_random_stores_match_reference_with_round_counters(cuda, oracle, trial):
+    """acceptance.cpp:128-155 (criterion 02) + :111-126 (criterion 01)."""
+    rng = np.random.default_rng(202 + trial)
+    n = int(2 + rng.integers(0, 400))
+    nsets = int(1 + rng.integers(0, 800))
+    off, mem = random_store(n, nsets, rng, 0.15)
+    k = int(1 + rng.integers(0, min(n, 10)))
+    g, st = store_from_lists(n, [mem[off[i]:off[i + 1]].tolist() for i in range(nsets)])
+    ref_counts = np.bincount(mem, minlength=n).astype(np.uint64)
+    assert (st.counter() == ref_counts).all()
+    seeds, marg, rc = oracle.select(n, off, np.concatenate(
+        [np.sort(mem[off[i]:off[i + 1]]) for i in range(nsets)]).astype(np.uint32), k,
+        capture=True)
+    for prebuilt in (True, False):
+        for thr in (0.0, 0.25, 1.0):
+            s = P.select_seeds(st, n, k, thr, prebuilt=prebuilt, capture_round_counters=True)
+            assert s.seeds == seeds
+            assert s.marginal_counts == marg
+            assert s.round_counters.shape == rc.shape
+            assert (s.round_counters == rc).all()
+
+
+def test_sampled_store_selection_matches_reference(cuda, oracle):
+    """Selection over the GPU's own sampled store vs the reference's select_seeds
+    over the reference's store (identical collections by the sampling parity)."""
+    from paper_2411_09473_b200 import graphs
+    cfg = graphs.scaled(graphs.CONFIGS["cfg1"], 1 << 12, 1 << 16)
+    arrays = graphs.generate(cfg)
+    g = P.Graph(*arrays)
+    st = P.RRRStore(g)
+    P.generate_batch(g, 0, 1, 20000, st)
+    orc = oracle.graph(*arrays).sample(0, 1, 0, 20000, workers=4)
+    seeds, marg = oracle.select(g.num_vertices, orc.offsets, orc.members, 50)
+    s = P.select_seeds(st, g.num_vertices, 50)
+    assert s.seeds == seeds and s.marginal_counts == marg
+    # the store is left tombstoned; a second call revives everything (selection.hpp:215)
+    s2 = P.select_seeds(st, g.num_vertices, 50)
+    assert s2.seeds == seeds
+    assert P.fraction_covered(st, s) == pytest.approx(sum(marg) / 20000, abs=0)
+
+
+def test_fraction_covered(cuda):
+    """test_selection.cpp:219-238."""
+    g, st = store_from_lists(4, [[0], [1], [2]])
+    assert P.fraction_covered(st, [0, 1, 2]) == 1.0
+    assert P.fraction_covered(st, []) == 0.0
+    rng = np.random.default_rng(53)
+    off, mem = random_store(60, 80, rng)
+    g, st = store_from_lists(60, [mem[off[i]:off[i + 1]].tolist() for i in range(80)])
+    seeds = [1, 5, 17, 33]
+    hit = sum(any(v in seeds for v in mem[off[i]:off[i + 1]]) for i in range(80))
+    assert P.fraction_covered(st, seeds) == hit / 80
+
+
+def test_coverage_of_prefixes_nondecreasing(cuda):
+    """test_selection.cpp:240-253."""
+    rng = np.random.default_rng(59)
+    off, mem = random_store(80, 100, rng)
+    g, st = store_from_lists(80, [mem[off[i]:off[i + 1]].tolist() for i in range(100)])
+    s = P.select_seeds(st, 80, 10)
+    prev = 0.0
+    for L in range(1, 11):
+        f = P.fraction_covered(st, s.seeds[:L])
+        assert f >= prev
+        prev = f
