@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""bench.py -- RRR-set sampling throughput of the IMM hot path on B200.
+
+Workload (default): BASELINE config 4, the north-star LT config -- directed
+Chung-Lu graph, 4,847,571 vertices / 68,993,773 edges, gamma 2.2, correlated
+in/out degrees, U(0,1) in-weights normalized per vertex.
+A step = one generate_batch of N RRR sets (fused occurrence counter + slot-
+ordered flat buffer) with the graph resident in HBM. Sets are bit-identical to
+the reference's (tests/test_gpu_sampling.py); the first step's sets are also
+hashed against the CPU reference in the cpu_baseline leg.
+
+  value  sets/s over all ranks, device-timed (CUDA events on the graph's stream)
+  e2e    sets/s through the public API with HOST buffers: graph upload from
+         pinned memory + K0 layout + sampling + export of sets and counter
+
+Multi-GPU (torchrun): rank r samples its own slot range, no data-path
+collective (slot j depends only on (run_seed, j)); scaling "weak".
+`--impl reference` times the reference CPU implementation (oracle/_ref, the
+unmodified rrflow headers) on this box's host cores for the same metric.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4")
+    ap.add_argument("--sets", type=int, default=1 << 16)
+    ap.add_argument("--lt-scan", default="linear", choices=["linear", "bsearch"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-imm", action="store_true")
+    ap.add_argument("--ref-sets", type=int, default=1 << 14,
+                    help="sets per step of the reference arm (bounded CPU sample)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def graph_arrays(name):
+    from paper_2411_09473_b200 import graphs
+    cfg = graphs.CONFIGS[name]
+    return cfg, graphs.generate(cfg)
+
+
+def workload_desc(cfg, n, m):
+    return f"{cfg.name}: {cfg.description} (n={n}, arcs={m}, k={cfg.k})"
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank):
+    """The reference's own CPU path (oracle/_ref = unmodified rrflow headers)."""
+    if rank != 0:
+        return
+    from oracle import Oracle, available
+    kind = "reference" if available("reference") else "port"
+    orc = Oracle(kind)
+    cfg, (roff, rsrc, rw) = graph_arrays(args.workload)
+    g = orc.graph(roff, rsrc, rw)
+    cores = cpu_cores()
+    n_sets = args.ref_sets
+    for _ in range(args.warmup):
+        g.sample(cfg.model, 1, 0, n_sets, workers=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        g.sample(cfg.model, 1, 0, n_sets, workers=cores)
+    dt = time.perf_counter() - t0
+    value = n_sets * args.steps / dt
+    line = {
+        "impl": "reference", "metric": "rrr_sets_per_sec", "value": value, "unit": "sets/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 cdf / u32 ids", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg, roff.size - 1, rsrc.size),
+                   "sets_per_step": n_sets, "run_seed": 1},
+        "cpu_baseline": {"value": value, "unit": "sets/s", "cores": cores, "kind": orc.kind,
+                         "sample": f"generate_batch_fused of slots [0,{n_sets}) per step "
+                                   f"on WorkPool({cores})"},
+        "e2e": {"value": value, "unit": "sets/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_2411_09473_b200 as P
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    cfg, (roff, rsrc, rw) = graph_arrays(args.workload)
+    n, m = roff.size - 1, rsrc.size
+    model = cfg.model
+    N = args.sets
+
+    # ---- device-resident throughput ------------------------------------------
+    stream = torch.cuda.current_stream()
+    g = P.Graph(roff, rsrc, rw)
+    g.set_stream(stream.cuda_stream)
+    g.prepare(model)
+    g.set_option("lt_scan", 1 if args.lt_scan == "bsearch" else 0)
+    store = P.RRRStore(g)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step(i):
+        store.clear()
+        first = (i * world + rank) * N
+        P.generate_slots(g, model, 1, first, N, store)
+        return g.last_batch_stats()
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    clocks = Clocks(local)
+    launches0 = P.launch_count()
+    total_ms, sample_ms, insp, ent, members, deferred = 0.0, 0.0, 0, 0, 0, 0
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps, outside the events
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st = step(args.warmup + i)
+        e1.record(stream)
+        e1.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        sample_ms += st.sample_ms
+        insp += st.edges_inspected
+        ent += st.entries_read
+        members += st.members
+        deferred += st.deferred
+    barrier()
+    launches = P.launch_count() - launches0
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = world * N * args.steps / (max_ms / 1e3)
+
+    # ---- end to end through the public API with host buffers -----------------
+    pin = [torch.from_numpy(a).pin_memory() for a in (roff, rsrc, rw)]
+    host = [p.numpy() for p in pin]
+    e2e_times, h2d, d2h = [], 0, 0
+    for i in range(args.e2e_steps + 1):
+        barrier()
+        t0 = time.perf_counter()
+        ge = P.Graph(*host)
+        ge.set_option("lt_scan", 1 if args.lt_scan == "bsearch" else 0)
+        se = P.RRRStore(ge)
+        P.generate_slots(ge, model, 1, rank * N, N, se)
+        off, mem = se.export()
+        cnt = se.counter()
+        se.close()
+        ge.close()
+        dt = time.perf_counter() - t0
+        if i > 0:  # first one warms the allocator
+            e2e_times.append(dt)
+        h2d = roff.nbytes + rsrc.nbytes + rw.nbytes
+        d2h = off.nbytes + mem.nbytes + n * 4
+    e2e_s = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = world * N / float(e2e_s.item())
+
+    peak, peak_src = measured_peak()
+    per_launch_ms = sample_ms / args.steps
+    if args.lt_scan == "linear" or model == 0:
+        alg_bytes = 8 * insp / args.steps  # one 8-byte CDF entry (LT) / edge record (IC)
+    else:
+        alg_bytes = 8 * ent / args.steps  # bytes the binary search actually reads
+    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("traffic_bytes_per_launch", {}).get(
+                    f"{args.workload}:{args.lt_scan}")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": "rrr_sets_per_sec", "value": value, "unit": "sets/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 cdf / u32 ids" if model == 1 else "u64 rng / u32 ids",
+        "data": "synthetic",
+        "config": {"workload": workload_desc(cfg, n, m), "sets_per_step": N, "run_seed": 1,
+                   "slots": "rank r, step i: [(i*world+r)*N, +N)",
+                   "lt_scan": args.lt_scan if model == 1 else None,
+                   "l2": "graph > L2 (arrays 0.9+ GB) and 256 MiB L2 flush between steps",
+                   "generator": "pinned Chung-Lu/R-MAT, DESIGN.md Inputs",
+                   "parallelism": f"slot-range shards x{world}"},
+        "edges_inspected_per_sec": world * insp / (max_ms / 1e3),
+        "edges_inspected_per_set": insp / (N * args.steps),
+        "members_per_set": members / (N * args.steps),
+        "deferred_sets": deferred,
+        "sampler_ms_per_step": per_launch_ms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_sample_lt" if model == 1 else "k_sample_ic",
+                     "bytes": "8 B x reference-equivalent inspected entries"
+                              if (args.lt_scan == "linear" or model == 0)
+                              else "8 B x CDF probes actually read",
+                     "peak_source": peak_src},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": {"value": e2e_value, "unit": "sets/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": len(e2e_times),
+                "includes": "pinned H2D graph upload, K0 layout, sampling, D2H sets+counter"},
+    }
+
+    # ---- CPU reference beside it (rank 0, N=1 only) --------------------------
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import Oracle, available
+        orc = Oracle("reference" if available("reference") else "port")
+        og = orc.graph(roff, rsrc, rw)
+        cores = cpu_cores()
+        ncpu = N
+        t0 = time.perf_counter()
+        sk = og.sample(model, 1, 0, ncpu, workers=cores)
+        dt = time.perf_counter() - t0
+        # parity spot check of the same slots on the GPU
+        store.clear()
+        P.generate_slots(g, model, 1, 0, ncpu, store)
+        o2, m2 = store.export()
+        same = bool((np.diff(o2.astype(np.int64)) == np.diff(sk.offsets.astype(np.int64))).all())
+        if same:
+            for i in range(0, ncpu, max(1, ncpu // 2048)):
+                a = np.sort(m2[o2[i]:o2[i + 1]])
+                if not np.array_equal(a, sk.members[sk.offsets[i]:sk.offsets[i + 1]]):
+                    same = False
+                    break
+        same = same and bool((store.counter() == sk.counter).all())
+        line["cpu_baseline"] = {
+            "value": ncpu / dt, "unit": "sets/s", "cores": cores, "kind": orc.kind,
+            "sample": f"generate_batch_fused of slots [0,{ncpu}) on WorkPool({cores})",
+            "seconds": dt, "gpu_sets_match_reference": same}
+        if not args.no_imm:
+            store.close()
+            ti = time.perf_counter()
+            r = P.run_imm(g, P.ImmConfig(k=cfg.k, epsilon=cfg.epsilon, model=model))
+            gpu_imm = time.perf_counter() - ti
+            ti = time.perf_counter()
+            rr = og.imm(k=cfg.k, epsilon=cfg.epsilon, model=model, workers=cores)
+            cpu_imm = time.perf_counter() - ti
+            line["imm"] = {
+                "k": cfg.k, "epsilon": cfg.epsilon, "gpu_wall_s": gpu_imm,
+                "gpu_timings": r.timings, "cpu_reference_wall_s": cpu_imm, "cpu_cores": cores,
+                "theta": r.theta, "theta_prime": r.theta_prime,
+                "seeds_match": r.seeds.seeds == rr["seeds"],
+                "marginals_match": r.seeds.marginal_counts == rr["marginals"],
+                "theta_match": (r.theta, r.theta_prime, r.lower_bound) ==
+                               (rr["theta"], rr["theta_prime"], rr["lower_bound"]),
+                "influence_estimate": n * sum(r.seeds.marginal_counts) / r.sets_generated}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -80,6 +80,13 @@ rrg_status rrg_generate_batch(rrg_graph* g, rrg_model model, uint64_t run_seed, 
                               rrg_store* s, int fused, uint32_t density_divisor,
                               uint64_t* sets_generated);
 
+/* Same, but the appended sets come from streams [first_slot, first_slot+count)
+ * instead of [size, size+count): one shard of a slot range split across GPUs
+ * (slot j depends only on (run_seed, j), sampling.hpp:179). */
+rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
+                              uint64_t first_slot, uint64_t count, rrg_store* s, int fused,
+                              uint32_t density_divisor, uint64_t* sets_generated);
+
 /* Per-call counters of the last rrg_generate_batch on this graph. */
 typedef struct {
   uint64_t sets;               /* sets appended */
@@ -191,6 +198,8 @@ rrg_status rrg_generate_graph(const rrg_gen_spec* spec, uint32_t* n, uint64_t* m
 /* ---- misc ------------------------------------------------------------------ */
 const char* rrg_last_error(void);
 const char* rrg_version(void);
+/* Kernels this library has launched in the process so far (all graphs). */
+uint64_t rrg_launch_count(void);
 /* Test hook: the integer Bernoulli threshold used by the IC kernel
  * (uniform01() < (double)w  <=>  (next_u64() >> 11) < threshold(w)). */
 uint64_t rrg_debug_bernoulli_threshold(uint32_t weight_bits);

@@ -230,6 +230,24 @@ def generate_batch(g: Graph, model, run_seed: int, count: int, store: RRRStore,
     return made.value
 
 
+def generate_slots(g: Graph, model, run_seed: int, first_slot: int, count: int,
+                   store: RRRStore, fused: bool = True,
+                   density_divisor: int = kDefaultDensityDivisor) -> int:
+    """Appends the sets of slots [first_slot, first_slot+count) (one shard of a
+    slot range split across GPUs; slot j depends only on (run_seed, j))."""
+    made = C.c_uint64()
+    st = lib.rrg_generate_slots(g.handle, _model(model), int(run_seed) & (2**64 - 1),
+                                int(first_slot), int(count), store.handle, 1 if fused else 0,
+                                int(density_divisor), C.byref(made))
+    check(st, made.value)
+    return made.value
+
+
+def launch_count() -> int:
+    """Kernels librrgpu.so has launched in this process."""
+    return int(lib.rrg_launch_count())
+
+
 def generate_batch_fused(g: Graph, model, run_seed: int, count: int, store: RRRStore,
                          density_divisor: int = kDefaultDensityDivisor) -> int:
     """sampling.hpp:201-206."""

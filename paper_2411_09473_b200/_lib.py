@@ -93,7 +93,10 @@ SIGNATURES = [
     ("rrg_store_info", C.c_int, [vp, u64p, u64p, u32p]),
     ("rrg_generate_batch", C.c_int,
      [vp, C.c_int, C.c_uint64, C.c_uint64, vp, C.c_int, C.c_uint32, u64p]),
+    ("rrg_generate_slots", C.c_int,
+     [vp, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_int, C.c_uint32, u64p]),
     ("rrg_last_batch_stats", C.c_int, [vp, C.POINTER(BatchStats)]),
+    ("rrg_launch_count", C.c_uint64, []),
     ("rrg_select_seeds", C.c_int,
      [vp, C.c_uint32, C.c_double, C.c_int, u32p, u64p, u64p, u32p, u64p]),
     ("rrg_fraction_covered", C.c_int, [vp, u32p, C.c_uint32, C.POINTER(C.c_double)]),

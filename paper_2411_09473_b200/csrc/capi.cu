@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
 #include <new>
@@ -20,6 +21,12 @@ thread_local std::string t_err;
 }
 
 void set_error(const std::string& msg) { t_err = msg; }
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+uint64_t launches() { return g_launches.load(); }
+void count_launch(uint64_t k) { g_launches += k; }
 
 // Converts exceptions at the C boundary into status codes.
 template <typename Fn>
@@ -122,6 +129,7 @@ void commit_staged(rrg_store* s, uint64_t count) {
 extern "C" {
 
 const char* rrg_last_error(void) { return rrgpu::t_err.c_str(); }
+uint64_t rrg_launch_count(void) { return rrgpu::launches(); }
 const char* rrg_version(void) { return "rrgpu 0.1.0 (sm_100a; reference rrflow 0.1.0)"; }
 uint64_t rrg_debug_bernoulli_threshold(uint32_t bits) { return bernoulli_threshold(bits); }
 
@@ -133,12 +141,7 @@ rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* roff, const 
   if (n && !roff) return invalid("rrg_graph_create: null offsets");
   if (m && (!rsrc || !rw)) return invalid("rrg_graph_create: null edge arrays");
   if (n == UINT32_MAX) return invalid("rrg_graph_create: n must be < 2^32 - 1");
-  if (n && (roff[0] != 0 || roff[n] != m))
-    return invalid("rrg_graph_create: offsets must start at 0 and end at m");
-  for (uint32_t v = 0; n && v < n; ++v)
-    if (roff[v + 1] < roff[v]) return invalid("rrg_graph_create: offsets must be non-decreasing");
-  for (uint64_t j = 0; j < m; ++j)
-    if (rsrc[j] >= n) return invalid("rrg_graph_create: source id out of range");
+  if (n == 0 && m != 0) return invalid("rrg_graph_create: edges without vertices");
   auto* g = new (std::nothrow) rrg_graph;
   if (!g) return RRG_ENOMEM;
   const rrg_status st = guarded([&]() -> rrg_status {
@@ -150,19 +153,27 @@ rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* roff, const 
     RRG_CUDA(cudaEventCreate(&g->ev1));
     g->n = n;
     g->m = m;
-    std::vector<uint32_t> off32(static_cast<size_t>(n) + 1);
-    for (uint64_t v = 0; v <= n; ++v) off32[v] = n ? static_cast<uint32_t>(roff[v]) : 0;
-    g->off.reserve_discard(off32.size());
+    g->off.reserve_discard(static_cast<size_t>(n) + 1);
     g->src.reserve_discard(m ? m : 1);
     g->w.reserve_discard(m ? m : 1);
     g->ctl.reserve_discard(1);
-    RRG_CUDA(cudaMemcpyAsync(g->off.ptr, off32.data(), off32.size() * 4, cudaMemcpyHostToDevice,
-                             g->stream));
+    if (n == 0) {
+      RRG_CUDA(cudaMemsetAsync(g->off.ptr, 0, 4, g->stream));
+      RRG_CUDA(cudaStreamSynchronize(g->stream));
+      return RRG_OK;
+    }
+    // offsets travel as u64 and are narrowed + validated on the device
+    DevBuf<uint64_t> off64;
+    off64.reserve_discard(static_cast<size_t>(n) + 1);
+    RRG_CUDA(cudaMemcpyAsync(off64.ptr, roff, (static_cast<size_t>(n) + 1) * 8,
+                             cudaMemcpyHostToDevice, g->stream));
     if (m) {
       RRG_CUDA(cudaMemcpyAsync(g->src.ptr, rsrc, m * 4, cudaMemcpyHostToDevice, g->stream));
       RRG_CUDA(cudaMemcpyAsync(g->w.ptr, rw, m * 4, cudaMemcpyHostToDevice, g->stream));
     }
-    RRG_CUDA(cudaStreamSynchronize(g->stream));
+    const uint32_t bad = upload_checks(g, off64.ptr);
+    if (bad & 1u) return invalid("rrg_graph_create: offsets must run 0..m, non-decreasing");
+    if (bad & 2u) return invalid("rrg_graph_create: source id out of range");
     return RRG_OK;
   });
   if (st != RRG_OK) {
@@ -288,8 +299,16 @@ rrg_status rrg_store_info(const rrg_store* s, uint64_t* sets, uint64_t* members,
 }
 
 rrg_status rrg_generate_batch(rrg_graph* g, rrg_model model, uint64_t run_seed, uint64_t count,
-                              rrg_store* s, int fused, uint32_t /*density_divisor*/,
+                              rrg_store* s, int fused, uint32_t density_divisor,
                               uint64_t* sets_generated) {
+  if (!s) return invalid("generate_batch: null store");
+  return rrg_generate_slots(g, model, run_seed, s->nsets, count, s, fused, density_divisor,
+                            sets_generated);
+}
+
+rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
+                              uint64_t first_slot, uint64_t count, rrg_store* s, int fused,
+                              uint32_t /*density_divisor*/, uint64_t* sets_generated) {
   if (sets_generated) *sets_generated = 0;
   if (!g || !s || s->g != g) return invalid("generate_batch: graph/store mismatch");
   if (model != RRG_IC && model != RRG_LT) return invalid("unknown diffusion model");
@@ -311,15 +330,20 @@ rrg_status rrg_generate_batch(rrg_graph* g, rrg_model model, uint64_t run_seed, 
     rrg_batch_stats acc{};
     for (uint64_t done = 0; done < count;) {
       const uint64_t c = std::min(kChunk, count - done);
-      // staging sized from the running mean set size
-      const double mean = s->nsets ? static_cast<double>(s->total) / s->nsets : 16.0;
-      const uint64_t want = static_cast<uint64_t>(c * (mean * 1.25 + 4)) + (1u << 16);
+      // staging sized from the running mean set size (first batch: a guess;
+      // sets that do not fit are re-run once staging has grown)
+      const double per_set = s->nsets ? static_cast<double>(s->total) / s->nsets * 1.5 + 8 : 96.0;
+      const uint64_t want = std::min<uint64_t>(static_cast<uint64_t>(c * per_set) + (1u << 20),
+                                               1ull << 31);
       if (want > s->stage.cap) s->stage.reserve_discard(want);
       s->slot_start.reserve_discard(c);
       s->slot_len.reserve_discard(c);
       s->deferred.reserve_discard(c);
       s->deferred2.reserve_discard(c);
-      RRG_CUDA(cudaMemsetAsync(g->ctl.ptr, 0, sizeof(SampleCtl), st));
+      s->restage.reserve_discard(c);
+      s->restage2.reserve_discard(c);
+      s->bigre.reserve_discard(c);
+      SampleCtl ctl{};
       SampleParams p{};
       p.n = g->n;
       p.off = g->off.ptr;
@@ -327,7 +351,7 @@ rrg_status rrg_generate_batch(rrg_graph* g, rrg_model model, uint64_t run_seed, 
       p.src = g->src.ptr;
       p.cdf = g->cdf.ptr;
       p.run_seed = run_seed;
-      p.base_slot = s->nsets;
+      p.base_slot = first_slot + done;
       p.count = c;
       p.lists = g->scratch.lists.ptr;
       p.tabs = g->scratch.tabs.ptr;
@@ -337,54 +361,76 @@ rrg_status rrg_generate_batch(rrg_graph* g, rrg_model model, uint64_t run_seed, 
       p.slot_start = s->slot_start.ptr;
       p.slot_len = s->slot_len.ptr;
       p.counter = fused ? s->counter.ptr : nullptr;
-      p.deferred = s->deferred.ptr;
       p.ctl = g->ctl.ptr;
       p.lt_scan = (g->lt_scan == kLtBsearch && g->cdf_monotone) ? kLtBsearch : kLtLinear;
       p.coop_min = g->coop_min;
-      const uint64_t grid_need = (c + block - 1) / block;
-      const int grid = static_cast<int>(std::min<uint64_t>(full_grid, grid_need));
-      RRG_CUDA(cudaEventRecord(g->ev0, st));
-      launch_sampler(model, p, grid, g->ic_inner, st);
-      RRG_CUDA(cudaEventRecord(g->ev1, st));
-      SampleCtl ctl{};
-      d2h(&ctl, g->ctl.ptr, 1, st);
-      sync(g);
-      float ms = 0.0f;
-      RRG_CUDA(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
-      sample_ms += ms;
-      acc.deferred += ctl.ndeferred;
-      // big-set path for deferred slots; grows staging when it ran out
-      uint32_t* list = s->deferred.ptr;
-      uint32_t* relist = s->deferred2.ptr;
-      uint32_t nlist = ctl.ndeferred;
-      int guard = 0;
-      while (nlist > 0) {
-        if (++guard > 64) throw std::runtime_error("big-set path did not converge");
-        if (ctl.cursor + ctl.deferred_members + 1024 > s->stage.cap) {
-          const uint64_t ncap = std::max<uint64_t>(
-              s->stage.cap * 2, ctl.cursor + 2 * ctl.deferred_members + (1u << 20));
-          s->stage.reserve_keep(ncap, s->stage.cap, st);
-          p.stage = s->stage.ptr;
-          p.stage_cap = s->stage.cap;
-        }
-        const uint32_t workers = std::min<uint32_t>(nlist, kBigWorkersMax);
-        ensure_big_scratch(g, workers);
-        // reset deferral counters, keep cursor/inspected
-        const unsigned zero = 0;
-        const unsigned long long zero64 = 0;
-        RRG_CUDA(cudaMemcpyAsync(&g->ctl.ptr->ndeferred, &zero, 4, cudaMemcpyHostToDevice, st));
-        RRG_CUDA(cudaMemcpyAsync(&g->ctl.ptr->deferred_members, &zero64, 8,
-                                 cudaMemcpyHostToDevice, st));
+
+      // One launch: reset the per-launch counters (keep cursor and tallies),
+      // run, read the control block back.
+      auto run = [&](bool big, const uint32_t* list, uint64_t n_items, uint32_t* restage_out) {
+        ctl.next = 0;
+        ctl.restage_members = 0;
+        ctl.ndeferred = 0;
+        ctl.nrestage = 0;
+        RRG_CUDA(cudaMemcpyAsync(g->ctl.ptr, &ctl, sizeof(SampleCtl), cudaMemcpyHostToDevice, st));
+        p.restage = restage_out;
         RRG_CUDA(cudaEventRecord(g->ev0, st));
-        launch_big(model, p, list, nlist, g->big.bitmaps.ptr, g->big.lists.ptr, workers, relist,
-                   st);
+        if (big) {
+          const uint32_t workers =
+              static_cast<uint32_t>(std::min<uint64_t>(n_items, kBigWorkersMax));
+          ensure_big_scratch(g, workers);
+          launch_big(model, p, list, static_cast<uint32_t>(n_items), g->big.bitmaps.ptr,
+                     g->big.lists.ptr, workers, st);
+        } else {
+          p.list = list;
+          p.count = n_items;
+          const uint64_t grid_need = (n_items + block - 1) / block;
+          launch_sampler(model, p, static_cast<int>(std::min<uint64_t>(full_grid, grid_need)),
+                         g->ic_inner, st);
+        }
         RRG_CUDA(cudaEventRecord(g->ev1, st));
         d2h(&ctl, g->ctl.ptr, 1, st);
         sync(g);
+        float ms = 0.0f;
         RRG_CUDA(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
         sample_ms += ms;
-        std::swap(list, relist);
-        nlist = ctl.ndeferred;
+      };
+      auto grow_staging = [&]() {
+        const uint64_t ncap = std::max<uint64_t>(
+            s->stage.cap + s->stage.cap / 2, ctl.cursor + 2 * ctl.restage_members + (1u << 20));
+        s->stage.reserve_keep(ncap, s->stage.cap, st);
+        p.stage = s->stage.ptr;
+        p.stage_cap = s->stage.cap;
+      };
+      // Big-set path over `list`; its staging refusals are re-run on it.
+      auto run_big = [&](const uint32_t* list, uint64_t n_items) {
+        uint32_t* bufs[2] = {s->deferred2.ptr, s->bigre.ptr};
+        for (int it = 0; n_items > 0; ++it) {
+          if (it > 64) throw std::runtime_error("big-set path did not converge");
+          run(true, list, n_items, bufs[it & 1]);
+          acc.deferred += (it == 0) ? n_items : 0;
+          n_items = ctl.nrestage;
+          list = bufs[it & 1];
+          if (n_items) grow_staging();
+        }
+      };
+      // main sampler over the batch, then over staging refusals until none remain
+      p.deferred = s->deferred.ptr;
+      const uint32_t* list = nullptr;
+      uint64_t n_items = c;
+      uint32_t* rbufs[2] = {s->restage.ptr, s->restage2.ptr};
+      for (int it = 0; n_items > 0; ++it) {
+        if (it > 64) throw std::runtime_error("staging did not converge");
+        uint32_t* out = rbufs[it & 1];
+        run(false, list, n_items, out);
+        const uint64_t ndef = ctl.ndeferred, nre = ctl.nrestage, rmem = ctl.restage_members;
+        if (ndef) run_big(s->deferred.ptr, ndef);  // may overwrite ctl.nrestage
+        n_items = nre;
+        list = out;
+        if (nre) {
+          ctl.restage_members = rmem;
+          grow_staging();
+        }
       }
       acc.edges_inspected += ctl.inspected;
       acc.entries_read += ctl.entries;

@@ -153,9 +153,9 @@ struct SampleCtl {
   unsigned long long cursor;      // staging bump allocator (u32 units)
   unsigned long long inspected;   // reference-equivalent in-edges inspected
   unsigned long long entries;     // adjacency entries actually read by the kernel
-  unsigned long long deferred_members;  // members of sets refused for lack of staging
-  unsigned int ndeferred;         // slots handed to the big-set path
-  unsigned int pad;
+  unsigned long long restage_members;  // members of sets refused for lack of staging
+  unsigned int ndeferred;         // slots handed to the big-set path (set > kMemCap)
+  unsigned int nrestage;          // slots to re-run once staging has grown
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {

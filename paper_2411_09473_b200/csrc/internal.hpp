@@ -119,6 +119,9 @@ struct rrg_store {
   rrgpu::DevBuf<uint32_t> slot_len;
   rrgpu::DevBuf<uint32_t> deferred;
   rrgpu::DevBuf<uint32_t> deferred2;
+  rrgpu::DevBuf<uint32_t> restage;
+  rrgpu::DevBuf<uint32_t> restage2;
+  rrgpu::DevBuf<uint32_t> bigre;
   rrgpu::DevBuf<uint64_t> scan;
   rrgpu::DevBuf<uint64_t> scan_tmp;
   // selection scratch
@@ -155,7 +158,9 @@ struct SampleParams {
   uint64_t* slot_start;
   uint32_t* slot_len;
   uint32_t* counter;
-  uint32_t* deferred;
+  const uint32_t* list;  // optional batch-local slot list (reruns); count = its length
+  uint32_t* deferred;    // out: slots for the big-set path
+  uint32_t* restage;     // out: slots refused for lack of staging
   SampleCtl* ctl;
   int lt_scan;
   uint32_t coop_min;
@@ -163,12 +168,16 @@ struct SampleParams {
 
 void prepare_ic(rrg_graph* g);
 void prepare_lt(rrg_graph* g);
+// converts d_off64 into g->off and validates offsets/sources on the device;
+// returns a bit mask of violations (1 offsets, 2 sources), 0 if clean
+uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64);
 int sampler_block();
 int sampler_blocks_per_sm(int model, uint32_t ic_inner);
 void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, cudaStream_t s);
 void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t nlist,
-                uint32_t* bitmaps, uint32_t* lists, uint32_t workers, uint32_t* redefer,
-                cudaStream_t s);
+                uint32_t* bitmaps, uint32_t* lists, uint32_t workers, cudaStream_t s);
+uint64_t launches();  // kernels launched by this library so far (bench evidence)
+void count_launch(uint64_t k = 1);
 
 // ---- store.cu ---------------------------------------------------------------
 // out[i] = sum_{t<i} in[t] for i in [0, count]; tmp grows as needed.

@@ -33,13 +33,17 @@ __device__ __forceinline__ void defer_slot(const SampleParams& p, uint32_t idx) 
   p.deferred[q] = idx;  // at most one deferral per slot per launch: q < count
 }
 
+__device__ __forceinline__ void restage_slot(const SampleParams& p, uint32_t idx, uint32_t nmem) {
+  atomicAdd(&p.ctl->restage_members, (unsigned long long)nmem);
+  p.restage[atomicAdd(&p.ctl->nrestage, 1u)] = idx;
+}
+
 // Writes a finished set to staging, bumps the fused counter, records the slot.
 __device__ __forceinline__ void emit_set(const SampleParams& p, uint32_t idx, const uint32_t* mem,
                                          uint32_t nmem) {
   const unsigned long long pos = atomicAdd(&p.ctl->cursor, (unsigned long long)nmem);
   if (pos + nmem > p.stage_cap) {
-    atomicAdd(&p.ctl->deferred_members, (unsigned long long)nmem);
-    defer_slot(p, idx);
+    restage_slot(p, idx, nmem);
     return;
   }
   uint32_t* out = p.stage + pos;
@@ -81,7 +85,7 @@ __device__ __forceinline__ bool fetch_slot(const SampleParams& p, bool need, boo
     exhausted = true;
     return false;
   }
-  idx = static_cast<uint32_t>(k);
+  idx = p.list ? p.list[k] : static_cast<uint32_t>(k);
   return true;
 }
 
@@ -286,7 +290,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
 __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, const int model,
                                                        const uint32_t* list, const uint32_t nlist,
                                                        uint32_t* bitmaps, uint32_t* lists,
-                                                       const uint32_t workers, uint32_t* redefer) {
+                                                       const uint32_t workers) {
   const int lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= workers) return;
@@ -346,10 +350,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
     pos = __shfl_sync(kFull, pos, 0);
     __syncwarp();
     if (pos + nmem > p.stage_cap) {
-      if (lane == 0) {
-        atomicAdd(&p.ctl->deferred_members, (unsigned long long)nmem);
-        redefer[atomicAdd(&p.ctl->ndeferred, 1u)] = idx;
-      }
+      if (lane == 0) restage_slot(p, idx, nmem);
     } else {
       for (uint32_t i = lane; i < nmem; i += 32) {
         const uint32_t v = mem[i];
@@ -399,7 +400,47 @@ __global__ void k_build_cdf(const uint32_t* off, const float* w, double* cdf, ui
   }
 }
 
+// Upload checks done on the device: offsets u64 -> u32 with monotonicity and
+// range checks, sources < n. bad[0] |= 1 offsets, 2 sources.
+__global__ void k_offsets_u32(const uint64_t* off64, uint32_t* off32, uint32_t n, uint64_t m,
+                              uint32_t* bad) {
+  for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v <= n;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t x = off64[v];
+    off32[v] = static_cast<uint32_t>(x);
+    const bool ok = x <= m && (v == 0 ? x == 0 : off64[v - 1] <= x) && (v < n || x == m);
+    if (!ok) atomicOr(bad, 1u);
+  }
+}
+
+__global__ void k_check_sources(const uint32_t* src, uint64_t m, uint32_t n, uint32_t* bad) {
+  bool ok = true;
+  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    ok &= src[j] < n;
+  if (!__all_sync(kFull, ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 2u);
+}
+
 }  // namespace
+
+uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64) {
+  DevBuf<uint32_t> bad;
+  bad.reserve_discard(1);
+  RRG_CUDA(cudaMemsetAsync(bad.ptr, 0, 4, g->stream));
+  const int grid = g->num_sms * 8;
+  k_offsets_u32<<<grid, 256, 0, g->stream>>>(d_off64, g->off.ptr, g->n, g->m, bad.ptr);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+  if (g->m) {
+    k_check_sources<<<grid, 256, 0, g->stream>>>(g->src.ptr, g->m, g->n, bad.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+  }
+  uint32_t h = 0;
+  RRG_CUDA(cudaMemcpyAsync(&h, bad.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
+  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  return h;
+}
 
 int sampler_block() { return kBlock; }
 
@@ -419,14 +460,15 @@ void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inne
   else
     k_sample_lt<<<grid, kBlock, 0, s>>>(p);
   RRG_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t nlist,
-                uint32_t* bitmaps, uint32_t* lists, uint32_t workers, uint32_t* redefer,
-                cudaStream_t s) {
+                uint32_t* bitmaps, uint32_t* lists, uint32_t workers, cudaStream_t s) {
   const int grid = static_cast<int>((workers * 32 + kBlock - 1) / kBlock);
-  k_sample_big<<<grid, kBlock, 0, s>>>(p, model, list, nlist, bitmaps, lists, workers, redefer);
+  k_sample_big<<<grid, kBlock, 0, s>>>(p, model, list, nlist, bitmaps, lists, workers);
   RRG_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void prepare_ic(rrg_graph* g) {
@@ -435,6 +477,7 @@ void prepare_ic(rrg_graph* g) {
   if (g->m) {
     k_build_rec<<<g->num_sms * 8, 256, 0, g->stream>>>(g->src.ptr, g->w.ptr, g->rec.ptr, g->m);
     RRG_CUDA(cudaGetLastError());
+    count_launch();
   }
   RRG_CUDA(cudaStreamSynchronize(g->stream));
   g->rec_ready = true;
@@ -451,6 +494,7 @@ void prepare_lt(rrg_graph* g) {
     const int blocks = (g->n + 127) / 128;
     k_build_cdf<<<blocks, 128, 0, g->stream>>>(g->off.ptr, g->w.ptr, g->cdf.ptr, g->n, bad.ptr);
     RRG_CUDA(cudaGetLastError());
+    count_launch();
   }
   uint32_t hbad = 0;
   RRG_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, 4, cudaMemcpyDeviceToHost, g->stream));

@@ -118,6 +118,7 @@ void launch_select(const SelectParams& p, int num_sms, cudaStream_t s) {
   void* kargs[] = {&args};
   RRG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_select), dim3(grid),
                                        dim3(kSelBlock), kargs, 0, s));
+  count_launch();
 }
 
 }  // namespace rrgpu

@@ -91,15 +91,18 @@ void scan_impl(const TIn* in, uint64_t* out, uint64_t count, DevBuf<uint64_t>& t
   uint64_t* sums_scan = sums + ntiles;
   k_scan_tiles<TIn><<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(in, out, count, sums);
   RRG_CUDA(cudaGetLastError());
+  count_launch();
   if (ntiles > 1) {
     scan_u64_rec(sums, sums_scan, ntiles, tmp, tmp_off + 2 * ntiles + 1, s);
     k_scan_add<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(out, count, sums_scan);
     RRG_CUDA(cudaGetLastError());
+    count_launch();
   } else {
     RRG_CUDA(cudaMemsetAsync(sums_scan, 0, sizeof(uint64_t), s));
   }
   k_set_total<<<1, 1, 0, s>>>(out, count, sums_scan, sums, ntiles);
   RRG_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void scan_u64_rec(const uint64_t* in, uint64_t* out, uint64_t count, DevBuf<uint64_t>& tmp,
@@ -205,6 +208,7 @@ void launch_compact(const uint32_t* stage, const uint64_t* slot_start, const uin
   k_compact<<<grid_for(count), 256, 0, s>>>(stage, slot_start, slot_len, scan, base_total, count,
                                             mem_out, off_out, maxlen);
   RRG_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void launch_recount(const uint64_t* off, const uint32_t* mem, uint64_t nsets, uint32_t* counter,
@@ -212,6 +216,7 @@ void launch_recount(const uint64_t* off, const uint32_t* mem, uint64_t nsets, ui
   if (!nsets) return;
   k_recount<<<grid_for(nsets), 256, 0, s>>>(off, mem, nsets, counter);
   RRG_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void launch_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
@@ -220,6 +225,7 @@ void launch_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
   if (!nsets) return;
   k_invert<<<grid_for(nsets), 256, 0, s>>>(off, mem, nsets, icur, ioff, inv, status);
   RRG_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void launch_fraction(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
@@ -227,6 +233,7 @@ void launch_fraction(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
   if (!nsets) return;
   k_fraction<<<grid_for(nsets), 256, 0, s>>>(off, mem, nsets, in_seed_set, hits);
   RRG_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 }  // namespace rrgpu

@@ -1,0 +1,34 @@
+"""One warm-up batch + one measured batch of the sampler on a BASELINE config
+(the command profiled by ncu: `ncu -k regex:k_sample -s 1 -c 1 ...`)."""
+import argparse
+import sys
+import time
+
+sys.path.insert(0, ".")
+import paper_2411_09473_b200 as P  # noqa: E402
+from paper_2411_09473_b200 import graphs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("workload")
+ap.add_argument("--sets", type=int, default=1 << 16)
+ap.add_argument("--lt-scan", type=int, default=0)
+ap.add_argument("--n", type=int, default=0, help="scaled-down vertex count (0 = full size)")
+ap.add_argument("--m", type=int, default=0)
+a = ap.parse_args()
+cfg = graphs.CONFIGS[a.workload]
+if a.n:
+    cfg = graphs.scaled(cfg, a.n, a.m)
+arrays = graphs.generate(cfg)
+g = P.Graph(*arrays)
+g.prepare(cfg.model)
+g.set_option("lt_scan", a.lt_scan)
+st = P.RRRStore(g)
+P.generate_batch(g, cfg.model, 99, a.sets, st)
+st.clear()
+t = time.time()
+P.generate_batch(g, cfg.model, 1, a.sets, st)
+s = g.last_batch_stats()
+print(f"{cfg.name} sets {s.sets} insp/set {s.edges_inspected / s.sets:.0f} members/set "
+      f"{s.members / s.sets:.1f} deferred {s.deferred} sample {s.sample_ms:.2f} ms "
+      f"{s.sets / s.sample_ms * 1e3:.3e} sets/s {s.edges_inspected / s.sample_ms * 1e3:.3e} edges/s "
+      f"wall {1e3 * (time.time() - t):.1f} ms")
