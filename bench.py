@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--sets", type=int, default=1 << 16)
-    ap.add_argument("--lt-scan", default="linear", choices=["linear", "bsearch"])
+    ap.add_argument("--lt-scan", default="bsearch", choices=["linear", "bsearch"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-imm", action="store_true")
@@ -192,34 +192,56 @@ def run_ours(args, rank, world, local):
         P.generate_slots(g, model, 1, first, N, store)
         return g.last_batch_stats()
 
-    for i in range(args.warmup):
-        step(i)
-    barrier()
-    clocks = Clocks(local)
-    launches0 = P.launch_count()
-    total_ms, sample_ms, insp, ent, members, deferred = 0.0, 0.0, 0, 0, 0, 0
-    for i in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps, outside the events
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        st = step(args.warmup + i)
-        e1.record(stream)
-        e1.synchronize()
-        total_ms += e0.elapsed_time(e1)
-        sample_ms += st.sample_ms
-        insp += st.edges_inspected
-        ent += st.entries_read
-        members += st.members
-        deferred += st.deferred
-    barrier()
-    launches = P.launch_count() - launches0
-    clk = clocks.stop()
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
-    value = world * N * args.steps / (max_ms / 1e3)
+    def measure(scan):
+        """W untimed + K timed steps; per-step CUDA events on the graph's stream."""
+        g.set_option("lt_scan", 1 if scan == "bsearch" else 0)
+        for i in range(args.warmup):
+            step(i)
+        barrier()
+        clocks = Clocks(local)
+        launches0 = P.launch_count()
+        r = {"total_ms": 0.0, "sample_ms": 0.0, "insp": 0, "ent": 0, "members": 0,
+             "deferred": 0}
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps, outside the events
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st = step(args.warmup + i)
+            e1.record(stream)
+            e1.synchronize()
+            r["total_ms"] += e0.elapsed_time(e1)
+            r["sample_ms"] += st.sample_ms
+            r["insp"] += st.edges_inspected
+            r["ent"] += st.entries_read
+            r["members"] += st.members
+            r["deferred"] += st.deferred
+        barrier()
+        r["launches"] = P.launch_count() - launches0
+        r["clocks"] = clocks.stop()
+        t = torch.tensor([r["total_ms"]], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        r["max_ms"] = float(t.item())
+        r["value"] = world * N * args.steps / (r["max_ms"] / 1e3)
+        per_launch_ms = r["sample_ms"] / args.steps
+        linear = scan == "linear" or model == 0
+        alg = 8 * (r["insp"] if linear else r["ent"]) / args.steps
+        r["per_launch_ms"] = per_launch_ms
+        r["achieved"] = alg / (per_launch_ms / 1e3) / 1e9
+        r["bytes_rule"] = ("8 B x reference-equivalent inspected entries" if linear
+                           else "8 B x CDF probes actually read")
+        return r
+
+    main = measure(args.lt_scan if model == 1 else "ic")
+    max_ms, value = main["max_ms"], main["value"]
+    insp, members, deferred = main["insp"], main["members"], main["deferred"]
+    launches, clk = main["launches"], main["clocks"]
+    linear_block = None
+    if model == 1 and args.lt_scan != "linear":
+        lin = measure("linear")
+        linear_block = lin
+        g.set_option("lt_scan", 1 if args.lt_scan == "bsearch" else 0)
 
     # ---- end to end through the public API with host buffers -----------------
     pin = [torch.from_numpy(a).pin_memory() for a in (roff, rsrc, rw)]
@@ -247,21 +269,19 @@ def run_ours(args, rank, world, local):
     e2e_value = world * N / float(e2e_s.item())
 
     peak, peak_src = measured_peak()
-    per_launch_ms = sample_ms / args.steps
-    if args.lt_scan == "linear" or model == 0:
-        alg_bytes = 8 * insp / args.steps  # one 8-byte CDF entry (LT) / edge record (IC)
-    else:
-        alg_bytes = 8 * ent / args.steps  # bytes the binary search actually reads
-    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
+    per_launch_ms = main["per_launch_ms"]
+    achieved = main["achieved"]
+
+    def ncu_traffic(scan):
+        prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("traffic_bytes_per_launch", {}).get(
-                    f"{args.workload}:{args.lt_scan}")
+                return json.load(f).get("traffic_bytes_per_launch", {}).get(
+                    f"{args.workload}:{scan}")
         except Exception:
-            traffic = None
+            return None
+
+    traffic = ncu_traffic(args.lt_scan if model == 1 else "ic")
 
     line = {
         "metric": "rrr_sets_per_sec", "value": value, "unit": "sets/s", "n_gpus": world,
@@ -283,16 +303,25 @@ def run_ours(args, rank, world, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_sample_lt" if model == 1 else "k_sample_ic",
-                     "bytes": "8 B x reference-equivalent inspected entries"
-                              if (args.lt_scan == "linear" or model == 0)
-                              else "8 B x CDF probes actually read",
-                     "peak_source": peak_src},
+                     "bytes": main["bytes_rule"], "peak_source": peak_src},
         "gpu_launches": launches,
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": "sets/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": len(e2e_times),
                 "includes": "pinned H2D graph upload, K0 layout, sampling, D2H sets+counter"},
     }
+    if linear_block is not None:
+        lb = linear_block
+        line["linear_scan"] = {
+            "note": "same batches with the reference's linear CDF scan (warp-cooperative "
+                    "16-byte loads); identical sets",
+            "value": lb["value"], "unit": "sets/s", "ms_per_step": lb["max_ms"] / args.steps,
+            "edges_inspected_per_sec": world * lb["insp"] / (lb["max_ms"] / 1e3),
+            "roofline": {"bound": "hbm", "achieved": lb["achieved"], "peak": peak, "unit": "GB/s",
+                         "frac": lb["achieved"] / peak, "traffic": ncu_traffic("linear"),
+                         "kernel": "k_sample_lt", "bytes": lb["bytes_rule"],
+                         "peak_source": peak_src},
+            "gpu_launches": lb["launches"], "clocks": lb["clocks"]}
 
     # ---- CPU reference beside it (rank 0, N=1 only) --------------------------
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -53,9 +53,12 @@ uint64_t rrg_graph_num_edges(const rrg_graph* g);
 
 /* Tuning knobs; none changes any output bit. */
 typedef enum {
-  RRG_OPT_LT_SCAN = 0,  /* 0 = linear CDF scan (reference trip count), 1 = binary search */
+  RRG_OPT_LT_SCAN = 0,  /* 0 = linear CDF scan (reference trip count), 1 = binary search
+                           (default; picks the identical index, reads ~log2(deg) entries) */
   RRG_OPT_LT_COOP_MIN = 1, /* in-list length from which LT scans go warp-cooperative */
-  RRG_OPT_IC_INNER = 2  /* IC edge steps per scheduling round (1..64) */
+  RRG_OPT_IC_INNER = 2, /* IC edge steps per scheduling round (1..64) */
+  RRG_OPT_IC_COOP_MIN = 3 /* IC in-list length from which the warp expands it cooperatively
+                             (GF(2) jump-ahead segments); UINT32_MAX disables */
 } rrg_option;
 rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value);
 
@@ -203,6 +206,9 @@ uint64_t rrg_launch_count(void);
 /* Test hook: the integer Bernoulli threshold used by the IC kernel
  * (uniform01() < (double)w  <=>  (next_u64() >> 11) < threshold(w)). */
 uint64_t rrg_debug_bernoulli_threshold(uint32_t weight_bits);
+/* Test hook: advances a xoshiro256** state (4 words) by k draws with the GF(2)
+ * jump matrices the IC hub expansion uses (csrc/jump.cpp). */
+void rrg_debug_jump(const uint64_t* state_in, uint64_t k, uint64_t* state_out);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,211 @@
+// rrgpu.hpp -- C++17 adapter over the C ABI (include/rrgpu.h).
+//
+// Mirrors the reference's operator API (rrflow 0.1.0, proj/include/rrflow) so a
+// caller such as proj/tools/rrflow.cpp:104 switches by swapping one include
+// and namespace. Same defaults, slot/stream semantics, side
+// effects and exception classes:
+//   RRG_EINVAL -> std::invalid_argument   RRG_ENOMEM -> rrgpu::BatchOutOfMemory
+//   RRG_ECUDA  -> std::runtime_error
+// Header-only; link with librrgpu.so.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../rrgpu.h"
+
+namespace rrgpu {
+
+enum class DiffusionModel { IC, LT };  // graph.hpp:19
+
+// sampling.hpp:148-154
+struct BatchOutOfMemory : std::runtime_error {
+  explicit BatchOutOfMemory(uint64_t generated, const std::string& why)
+      : std::runtime_error("out of memory after generating " + std::to_string(generated) +
+                           " RRR sets: " + why),
+        sets_generated(generated) {}
+  uint64_t sets_generated;
+};
+
+inline void check(rrg_status st, uint64_t generated = 0) {
+  if (st == RRG_OK) return;
+  const std::string msg = rrg_last_error();
+  if (st == RRG_EINVAL) throw std::invalid_argument(msg);
+  if (st == RRG_ENOMEM) throw BatchOutOfMemory(generated, msg);
+  throw std::runtime_error(msg);
+}
+
+inline rrg_model to_c(DiffusionModel m) { return m == DiffusionModel::IC ? RRG_IC : RRG_LT; }
+
+// Device-resident transpose of rrflow::Graph (graph.hpp:34-59). Build it from the
+// reference graph's reverse arrays verbatim: Graph g(rg.num_vertices,
+// rg.reverse_offsets, rg.reverse_sources, rg.reverse_weights).
+class Graph {
+ public:
+  Graph(uint32_t n, const std::vector<uint64_t>& reverse_offsets,
+        const std::vector<uint32_t>& reverse_sources, const std::vector<float>& reverse_weights) {
+    if (reverse_offsets.size() != static_cast<size_t>(n) + 1)
+      throw std::invalid_argument("reverse_offsets must hold n + 1 entries");
+    rrg_graph* h = nullptr;
+    check(rrg_graph_create(n, reverse_sources.size(), reverse_offsets.data(),
+                           reverse_sources.data(), reverse_weights.data(), &h));
+    h_.reset(h);
+  }
+  uint32_t num_vertices() const { return rrg_graph_num_vertices(h_.get()); }
+  uint64_t num_edges() const { return rrg_graph_num_edges(h_.get()); }
+  rrg_graph* handle() const { return h_.get(); }
+
+ private:
+  struct Del {
+    void operator()(rrg_graph* g) const { rrg_graph_destroy(g); }
+  };
+  std::unique_ptr<rrg_graph, Del> h_;
+};
+
+// RRRStore + the fused Counter of generate_batch_fused (rrr_store.hpp, counter.hpp).
+class RRRStore {
+ public:
+  explicit RRRStore(const Graph& g) : n_(g.num_vertices()) {
+    rrg_store* h = nullptr;
+    check(rrg_store_create(g.handle(), &h));
+    h_.reset(h);
+  }
+  uint64_t size() const {
+    uint64_t s = 0;
+    check(rrg_store_info(h_.get(), &s, nullptr, nullptr));
+    return s;
+  }
+  uint64_t total_member_count() const {
+    uint64_t m = 0;
+    check(rrg_store_info(h_.get(), nullptr, &m, nullptr));
+    return m;
+  }
+  uint32_t max_set_size() const {
+    uint32_t x = 0;
+    check(rrg_store_info(h_.get(), nullptr, nullptr, &x));
+    return x;
+  }
+  // Members of set `idx` in visit order (root first).
+  std::vector<uint32_t> set(uint64_t idx) const {
+    uint64_t off[2];
+    check(rrg_store_export(h_.get(), idx, 1, off, nullptr));
+    std::vector<uint32_t> out(off[1]);
+    check(rrg_store_export(h_.get(), idx, 1, off, out.data()));
+    return out;
+  }
+  // Counter::get for every vertex (counter.hpp:29)
+  std::vector<uint64_t> counter() const {
+    std::vector<uint64_t> out(n_);
+    check(rrg_store_counter(h_.get(), out.data()));
+    return out;
+  }
+  rrg_store* handle() const { return h_.get(); }
+
+ private:
+  struct Del {
+    void operator()(rrg_store* s) const { rrg_store_destroy(s); }
+  };
+  uint32_t n_;
+  std::unique_ptr<rrg_store, Del> h_;
+};
+
+// sampling.hpp:159-199. `fused` plays the role of the Counter* argument.
+inline void generate_batch(const Graph& g, DiffusionModel model, uint64_t run_seed,
+                           uint64_t count, RRRStore& store, bool fused = true,
+                           uint32_t density_divisor = 64) {
+  uint64_t made = 0;
+  check(rrg_generate_batch(g.handle(), to_c(model), run_seed, count, store.handle(),
+                           fused ? 1 : 0, density_divisor, &made),
+        made);
+}
+
+// selection.hpp:19-22
+struct SeedSet {
+  std::vector<uint32_t> seeds;
+  std::vector<uint64_t> marginal_counts;
+};
+
+// selection.hpp:209-243 (prebuilt = the store's fused counter).
+inline SeedSet select_seeds(RRRStore& store, uint32_t n, uint32_t k,
+                            double adaptive_threshold = 0.25, bool prebuilt = true) {
+  if (k < 1) throw std::invalid_argument("select_seeds: k must be >= 1");
+  if (k > n) throw std::invalid_argument("select_seeds: k exceeds vertex count");
+  SeedSet out;
+  out.seeds.resize(k);
+  out.marginal_counts.resize(k);
+  check(rrg_select_seeds(store.handle(), k, adaptive_threshold, prebuilt ? 1 : 0,
+                         out.seeds.data(), out.marginal_counts.data(), nullptr, nullptr,
+                         nullptr));
+  return out;
+}
+
+// selection.hpp:340-358
+inline double fraction_covered(RRRStore& store, const std::vector<uint32_t>& seeds) {
+  double f = 0.0;
+  check(rrg_fraction_covered(store.handle(), seeds.data(), static_cast<uint32_t>(seeds.size()),
+                             &f));
+  return f;
+}
+
+// imm.hpp:27-54
+struct ImmConfig {
+  uint32_t k = 50;
+  double epsilon = 0.5;
+  DiffusionModel model = DiffusionModel::IC;
+  unsigned workers = 1;
+  uint64_t rng_seed = 1;
+  double ell = 1.0;
+  double adaptive_threshold = 0.25;
+};
+
+struct ImmTimings {
+  double generate_rrrsets = 0.0;
+  double find_most_influential = 0.0;
+  double total = 0.0;
+};
+
+struct ImmResult {
+  SeedSet seeds;
+  uint64_t theta = 0;
+  uint64_t theta_prime = 0;
+  double lower_bound = 0.0;
+  ImmTimings timings;
+  uint64_t sets_generated = 0;
+  double mean_set_size = 0.0;
+  uint32_t max_set_size = 0;
+  double mean_coverage_fraction = 0.0;
+};
+
+// imm.hpp:214-251
+inline ImmResult run_imm(const Graph& g, const ImmConfig& cfg) {
+  rrg_imm_config c;
+  rrg_imm_config_default(&c);
+  c.k = cfg.k;
+  c.epsilon = cfg.epsilon;
+  c.model = to_c(cfg.model);
+  c.workers = cfg.workers;
+  c.rng_seed = cfg.rng_seed;
+  c.ell = cfg.ell;
+  c.adaptive_threshold = cfg.adaptive_threshold;
+  ImmResult r;
+  const uint32_t k = cfg.k ? cfg.k : 1;
+  r.seeds.seeds.resize(k);
+  r.seeds.marginal_counts.resize(k);
+  rrg_imm_result out{};
+  check(rrg_run_imm(g.handle(), &c, r.seeds.seeds.data(), r.seeds.marginal_counts.data(), &out));
+  r.theta = out.theta;
+  r.theta_prime = out.theta_prime;
+  r.lower_bound = out.lower_bound;
+  r.timings = {out.t_generate, out.t_select, out.t_total};
+  r.sets_generated = out.sets_generated;
+  r.mean_set_size = out.mean_set_size;
+  r.max_set_size = out.max_set_size;
+  r.mean_coverage_fraction = out.mean_coverage_fraction;
+  return r;
+}
+
+}  // namespace rrgpu

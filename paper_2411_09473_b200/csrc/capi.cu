@@ -61,7 +61,7 @@ using namespace rrgpu;
 namespace {
 
 constexpr int kMaxBlocksPerSm = 4;
-constexpr uint32_t kBigWorkersMax = 256;
+constexpr uint32_t kBigWorkersMax = 1024;
 
 void ensure_lane_scratch(rrg_graph* g, uint64_t lanes) {
   LaneScratch& sc = g->scratch;
@@ -239,6 +239,10 @@ rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value) {
       if (value < 1 || value > 64) return invalid("ic_inner must be in [1, 64]");
       g->ic_inner = static_cast<uint32_t>(value);
       return RRG_OK;
+    case RRG_OPT_IC_COOP_MIN:
+      if (value < 1) return invalid("ic_coop_min must be >= 1");
+      g->ic_coop_min = static_cast<uint32_t>(std::min<int64_t>(value, UINT32_MAX));
+      return RRG_OK;
   }
   return invalid("unknown option");
 }
@@ -364,6 +368,9 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.ctl = g->ctl.ptr;
       p.lt_scan = (g->lt_scan == kLtBsearch && g->cdf_monotone) ? kLtBsearch : kLtLinear;
       p.coop_min = g->coop_min;
+      p.jmat = g->jmat.ptr;
+      p.dupfree = g->dupfree.ptr;
+      p.ic_coop_min = g->ic_coop_min;
 
       // One launch: reset the per-launch counters (keep cursor and tallies),
       // run, read the control block back.
@@ -376,8 +383,8 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         p.restage = restage_out;
         RRG_CUDA(cudaEventRecord(g->ev0, st));
         if (big) {
-          const uint32_t workers =
-              static_cast<uint32_t>(std::min<uint64_t>(n_items, kBigWorkersMax));
+          const uint32_t workers = static_cast<uint32_t>(std::min<uint64_t>(
+              n_items, std::min<uint64_t>(kBigWorkersMax, 4ull * g->num_sms)));
           ensure_big_scratch(g, workers);
           launch_big(model, p, list, static_cast<uint32_t>(n_items), g->big.bitmaps.ptr,
                      g->big.lists.ptr, workers, st);

@@ -128,6 +128,49 @@ __device__ __forceinline__ void tab_insert(uint64_t* tab, uint32_t tag, uint32_t
   tab[h] = (static_cast<uint64_t>(tag) << 32) | v;
 }
 
+// Concurrent insert (several lanes filling one lane's table in the cooperative
+// hub expansion). An entry with a stale tag is free; claim it with a CAS.
+__device__ __forceinline__ void tab_insert_atomic(uint64_t* tab, uint32_t tag, uint32_t lg,
+                                                  uint32_t v) {
+  const uint32_t mask = (1u << lg) - 1;
+  uint32_t h = vhash(v) >> (32 - lg);
+  const unsigned long long want = (static_cast<unsigned long long>(tag) << 32) | v;
+  while (true) {
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(tab + h);
+    if (static_cast<uint32_t>(e >> 32) == tag) {
+      h = (h + 1) & mask;
+      continue;
+    }
+    if (atomicCAS(reinterpret_cast<unsigned long long*>(tab + h), e, want) == e) return;
+  }
+}
+
+// s <- M s over GF(2)^256 (state words a,b,c,d = bits 0..255), M column-major:
+// column i = 4 words at M + 4 i (csrc/jump.cpp).
+__device__ __forceinline__ void gf2_matvec(const uint64_t* __restrict__ M, uint64_t& a,
+                                           uint64_t& b, uint64_t& c, uint64_t& d) {
+  uint64_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+  const uint64_t in[4] = {a, b, c, d};
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    uint64_t bits = in[w];
+    while (bits) {
+      const int i = __ffsll(static_cast<long long>(bits)) - 1;
+      bits &= bits - 1;
+      const ulonglong2* col = reinterpret_cast<const ulonglong2*>(M + 4 * (64 * w + i));
+      const ulonglong2 x = __ldg(col), y = __ldg(col + 1);
+      o0 ^= x.x;
+      o1 ^= x.y;
+      o2 ^= y.x;
+      o3 ^= y.y;
+    }
+  }
+  a = o0;
+  b = o1;
+  c = o2;
+  d = o3;
+}
+
 // 128-bit register filter in front of the table: a clear bit proves absence.
 struct Filter {
   uint64_t lo, hi;

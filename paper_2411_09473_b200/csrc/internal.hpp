@@ -90,10 +90,13 @@ struct rrg_graph {
   rrgpu::DevBuf<float> w;        // f32[m]   transpose weights
   rrgpu::DevBuf<uint2> rec;      // IC: {source, weight bits} per in-edge (lazy)
   rrgpu::DevBuf<double> cdf;     // LT: sequential fp64 prefix per in-list (lazy, +2 pad)
+  rrgpu::DevBuf<uint64_t> jmat;  // IC: jump matrices T^(32 l), l = 1..31
+  rrgpu::DevBuf<uint8_t> dupfree;  // IC: per-vertex strictly-increasing-sources flag
+  uint32_t ic_coop_min = 256;    // IC: in-lists at least this long expand warp-cooperatively
   bool rec_ready = false;
   bool cdf_ready = false;
   bool cdf_monotone = true;
-  int lt_scan = rrgpu::kLtLinear;
+  int lt_scan = rrgpu::kLtBsearch;  // fastest exact search; linear = reference trip count
   uint32_t coop_min = 64;        // LT: in-lists at least this long are scanned warp-cooperatively
   uint32_t ic_inner = 8;         // IC: edge steps per flat-loop iteration
   rrgpu::LaneScratch scratch;
@@ -164,6 +167,10 @@ struct SampleParams {
   SampleCtl* ctl;
   int lt_scan;
   uint32_t coop_min;
+  // IC cooperative expansion of long in-lists
+  const uint64_t* jmat;     // 31 GF(2) matrices T^(32 l), l = 1..31 (jump.cpp)
+  const uint8_t* dupfree;   // per vertex: in-list sources strictly increasing
+  uint32_t ic_coop_min;     // in-lists at least this long go warp-cooperative
 };
 
 void prepare_ic(rrg_graph* g);
@@ -176,6 +183,7 @@ int sampler_blocks_per_sm(int model, uint32_t ic_inner);
 void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, cudaStream_t s);
 void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t nlist,
                 uint32_t* bitmaps, uint32_t* lists, uint32_t workers, cudaStream_t s);
+std::vector<uint64_t> segment_matrices(uint64_t seg, int count);  // jump.cpp
 uint64_t launches();  // kernels launched by this library so far (bench evidence)
 void count_launch(uint64_t k = 1);
 

@@ -104,9 +104,150 @@ __device__ __forceinline__ void lane_insert(uint32_t* mem, uint64_t* tab, uint32
 }
 
 // ---------------------------------------------------------------------------
+// Cooperative IC expansion of ONE lane's long in-list by the whole warp.
+//
+// The in-list of a dequeued vertex is consumed in windows of 1024 edges. With
+// duplicate-free sources (K0 flag) the visited status of every edge is fixed
+// at list start, so
+//   1. the warp computes the unvisited mask of each 32-edge chunk (coalesced
+//      source loads, filter + table of the owner lane); chunk c -> lane c;
+//   2. the window's U draws are the next U positions of the slot's stream:
+//      lane l owns positions [32 l, 32 l + 32), reaches its first one with one
+//      GF(2) matrix T^(32 l) (csrc/jump.cpp) and draws for its unvisited edges
+//      in CSR order -- exactly the draws the reference makes, in its order;
+//   3. accepted sources are appended in CSR order (ballot prefix), inserted into
+//      the owner's table (CAS) and filter; the stream continues from the state
+//      of the lane that made the window's last draw.
+// Returns false when the set would exceed kMemCap (the slot is deferred).
+// ---------------------------------------------------------------------------
+struct CoopState {
+  uint64_t a, b, c, d;  // owner's RNG state
+  uint64_t flo, fhi;    // owner's filter
+  uint32_t tag, lg, nmem;
+};
+
+struct CoopSmem {
+  uint32_t mask[32];
+  uint32_t pre[32];
+  uint32_t acc[32];
+  unsigned long long st[4];
+};
+
+__device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uint32_t* mem,
+                            uint64_t* tab, CoopState& s, CoopSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  const Filter f{s.flo, s.fhi};
+  uint64_t add_lo = 0, add_hi = 0;
+  for (uint32_t wb = jb; wb < je; wb += 1024) {
+    const uint32_t nch = (min(1024u, je - wb) + 31) >> 5;
+    // 1. unvisited mask per chunk
+    uint32_t mymask = 0;
+    for (uint32_t c = 0; c < nch; ++c) {
+      const uint32_t j = wb + 32 * c + lane;
+      bool unv = false;
+      if (j < je) {
+        const uint32_t v = __ldg(p.src + j);
+        unv = !(f.maybe(v) && tab_contains(tab, s.tag, s.lg, v));
+      }
+      const unsigned m = __ballot_sync(kFull, unv);
+      if (lane == static_cast<int>(c)) mymask = m;
+    }
+    const uint32_t cnt = __popc(mymask);
+    uint32_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t U = __shfl_sync(kFull, incl, 31);
+    if (U == 0) continue;
+    sm.mask[lane] = mymask;
+    sm.pre[lane] = incl - cnt;
+    sm.acc[lane] = 0;
+    __syncwarp();
+    // 2. lane l draws stream positions [32 l, min(U, 32 l + 32))
+    const uint32_t r0 = 32u * lane;
+    if (r0 < U) {
+      Xoshiro st{s.a, s.b, s.c, s.d};
+      if (lane) gf2_matvec(p.jmat + static_cast<size_t>(lane - 1) * 1024, st.a, st.b, st.c, st.d);
+      uint32_t c = 0;  // chunk holding unvisited rank r0
+      for (uint32_t step = 16; step; step >>= 1)
+        if (c + step < nch && sm.pre[c + step] <= r0) c += step;
+      uint32_t m = sm.mask[c];
+      for (uint32_t k = r0 - sm.pre[c]; k; --k) m &= m - 1;
+      const uint32_t need = min(32u, U - r0);
+      uint32_t acc = 0;
+      for (uint32_t done = 0; done < need;) {
+        if (!m) {
+          if (acc) atomicOr(&sm.acc[c], acc);
+          acc = 0;
+          m = sm.mask[++c];
+          continue;
+        }
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        if (st.u53() < bernoulli_threshold(__ldg(p.rec + wb + 32 * c + bit).y)) acc |= 1u << bit;
+        ++done;
+      }
+      if (acc) atomicOr(&sm.acc[c], acc);
+      if (r0 + need == U) {
+        sm.st[0] = st.a;
+        sm.st[1] = st.b;
+        sm.st[2] = st.c;
+        sm.st[3] = st.d;
+      }
+    }
+    __syncwarp();
+    s.a = sm.st[0];
+    s.b = sm.st[1];
+    s.c = sm.st[2];
+    s.d = sm.st[3];
+    // 3. append the accepted sources in CSR order
+    const uint32_t am_lane = lane < static_cast<int>(nch) ? sm.acc[lane] : 0u;
+    uint32_t A = __popc(am_lane);
+    for (int o = 16; o; o >>= 1) A += __shfl_xor_sync(kFull, A, o);
+    if (A) {
+      if (s.nmem + A > kMemCap) return false;
+      uint32_t lg2 = s.lg;
+      while (2 * (s.nmem + A) > (1u << lg2)) ++lg2;
+      if (lg2 != s.lg) {  // grow: re-insert the members under a fresh tag
+        s.lg = lg2;
+        ++s.tag;
+        for (uint32_t t = lane; t < s.nmem; t += 32) tab_insert_atomic(tab, s.tag, s.lg, mem[t]);
+        __syncwarp();
+      }
+      unsigned cm = __ballot_sync(kFull, am_lane != 0);
+      while (cm) {
+        const int c = __ffs(cm) - 1;
+        cm &= cm - 1;
+        const uint32_t am = __shfl_sync(kFull, am_lane, c);
+        if ((am >> lane) & 1u) {
+          const uint32_t v = __ldg(p.src + wb + 32 * c + lane);
+          mem[s.nmem + __popc(am & lanemask_lt())] = v;
+          tab_insert_atomic(tab, s.tag, s.lg, v);
+          const uint32_t b = Filter::bit(v);
+          if (b & 64) add_hi |= 1ull << (b & 63);
+          else add_lo |= 1ull << (b & 63);
+        }
+        s.nmem += __popc(am);
+      }
+    }
+    __syncwarp();
+  }
+  for (int o = 16; o; o >>= 1) {
+    add_lo |= __shfl_xor_sync(kFull, add_lo, o);
+    add_hi |= __shfl_xor_sync(kFull, add_hi, o);
+  }
+  s.flo |= add_lo;
+  s.fhi |= add_hi;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // K1: IC sampler (sampling.hpp:90-111 per slot, :177-189 per batch)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBlock) k_sample_ic(const SampleParams p, const uint32_t inner) {
+  __shared__ CoopSmem coop_sm[kBlock / 32];
+  const int lane = threadIdx.x & 31;
   const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   uint32_t* mem = p.lists + gid * kMemCap;
   uint64_t* tab = p.tabs + gid * kTabCap;
@@ -114,7 +255,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_ic(const SampleParams p, cons
   Xoshiro rng{0, 0, 0, 0};
   Filter flt;
   flt.clear();
-  bool active = false, exhausted = false;
+  bool active = false, exhausted = false, want_coop = false;
   uint32_t idx = 0, nmem = 0, head = 0, lg = kTabLog0, j = 0, jend = 0;
   uint64_t insp = 0;
 
@@ -134,6 +275,43 @@ __global__ void __launch_bounds__(kBlock) k_sample_ic(const SampleParams p, cons
       active = true;
     }
     if (__all_sync(kFull, !active)) break;
+
+    // long duplicate-free in-lists: the whole warp expands them, one lane at a time
+    unsigned cm = __ballot_sync(kFull, active && want_coop);
+    if (cm) __syncwarp();
+    while (cm) {
+      const int L = __ffs(cm) - 1;
+      cm &= cm - 1;
+      CoopState s;
+      s.a = __shfl_sync(kFull, rng.a, L);
+      s.b = __shfl_sync(kFull, rng.b, L);
+      s.c = __shfl_sync(kFull, rng.c, L);
+      s.d = __shfl_sync(kFull, rng.d, L);
+      s.flo = __shfl_sync(kFull, flt.lo, L);
+      s.fhi = __shfl_sync(kFull, flt.hi, L);
+      s.tag = __shfl_sync(kFull, tag, L);
+      s.lg = __shfl_sync(kFull, lg, L);
+      s.nmem = __shfl_sync(kFull, nmem, L);
+      const uint32_t jb = __shfl_sync(kFull, j, L), je = __shfl_sync(kFull, jend, L);
+      const uint64_t gl = gid - lane + L;
+      const bool ok = coop_expand(p, jb, je, p.lists + gl * kMemCap, p.tabs + gl * kTabCap, s,
+                                  coop_sm[threadIdx.x >> 5]);
+      if (lane == L) {
+        want_coop = false;
+        if (ok) {
+          rng = Xoshiro{s.a, s.b, s.c, s.d};
+          flt.lo = s.flo;
+          flt.hi = s.fhi;
+          tag = s.tag;
+          lg = s.lg;
+          nmem = s.nmem;
+          j = jend;
+        } else {
+          defer_slot(p, idx);
+          active = false;
+        }
+      }
+    }
     if (!active) continue;
 
     if (j < jend) {
@@ -158,6 +336,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_ic(const SampleParams p, cons
       j = p.off[u];
       jend = p.off[u + 1];
       insp += jend - j;
+      want_coop = jend - j >= p.ic_coop_min && p.dupfree[u];
     } else {
       emit_set(p, idx, mem, nmem);
       active = false;
@@ -284,14 +463,22 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// Big-set path: warp per deferred slot, n-bit visited map, lane 0 replays the
-// reference loop serially; the warp writes out and clears the map.
+// Big-set path: warp per deferred slot with an n-bit visited map. IC: the warp
+// loads 32 in-edges per chunk (coalesced), tests visited and computes the
+// Bernoulli thresholds in parallel, lane 0 (the slot's RNG) draws only for
+// the unvisited edges in CSR order, and the accepted sources are appended in
+// lane order. A chunk whose sources repeat falls back to lane 0 replaying it
+// edge by edge against the live map, so the sequential semantics hold exactly.
+// LT walks are replayed serially by lane 0. The warp writes out and clears.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, const int model,
                                                        const uint32_t* list, const uint32_t nlist,
                                                        uint32_t* bitmaps, uint32_t* lists,
                                                        const uint32_t workers) {
+  __shared__ uint64_t s_thr[kBlock / 32][32];
+  __shared__ uint32_t s_src[kBlock / 32][32];
   const int lane = threadIdx.x & 31;
+  const int wl = threadIdx.x >> 5;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= workers) return;
   const uint64_t words = (static_cast<uint64_t>(p.n) + 31) / 32;
@@ -301,28 +488,66 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
   for (uint32_t t = w; t < nlist; t += workers) {
     const uint32_t idx = list[t];
     uint32_t nmem = 0;
-    if (lane == 0) {
-      Xoshiro rng;
-      rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
-      const uint32_t root = static_cast<uint32_t>(rng.below(p.n));
+    Xoshiro rng;
+    rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
+    const uint32_t root = static_cast<uint32_t>(rng.below(p.n));
+    if (model == RRG_IC) {
+      if (lane == 0) {
+        mem[0] = root;
+        vis[root >> 5] |= 1u << (root & 31);
+      }
+      nmem = 1;
+      __syncwarp();
+      for (uint32_t head = 0; head < nmem; ++head) {
+        const uint32_t uu = mem[head];
+        const uint32_t jb = p.off[uu], je = p.off[uu + 1];
+        insp += je - jb;
+        for (uint32_t base = jb; base < je; base += 32) {
+          const uint32_t j = base + lane;
+          const bool valid = j < je;
+          const uint2 r = valid ? p.rec[j] : make_uint2(0xffffffffu, 0);
+          const bool unv = valid && !((vis[r.x >> 5] >> (r.x & 31)) & 1u);
+          const unsigned peers = __match_any_sync(kFull, r.x);
+          const bool dup = valid && (peers & lanemask_lt()) != 0;
+          const unsigned um = __ballot_sync(kFull, unv);
+          s_thr[wl][lane] = bernoulli_threshold(r.y);
+          s_src[wl][lane] = r.x;
+          __syncwarp();
+          unsigned acc = 0;
+          const bool any_dup = __any_sync(kFull, dup);
+          if (lane == 0) {
+            if (!any_dup) {
+              for (unsigned mm = um; mm; mm &= mm - 1) {
+                const int l = __ffs(mm) - 1;
+                if (rng.u53() < s_thr[wl][l]) acc |= 1u << l;
+              }
+            } else {
+              const int nv = static_cast<int>(min(32u, je - base));
+              for (int l = 0; l < nv; ++l) {  // edge-by-edge against the live map
+                const uint32_t v = s_src[wl][l];
+                if ((vis[v >> 5] >> (v & 31)) & 1u) continue;
+                if (rng.u53() < s_thr[wl][l]) {
+                  vis[v >> 5] |= 1u << (v & 31);
+                  acc |= 1u << l;
+                }
+              }
+            }
+          }
+          acc = __shfl_sync(kFull, acc, 0);
+          if ((acc >> lane) & 1u) {
+            mem[nmem + __popc(acc & lanemask_lt())] = r.x;
+            atomicOr(vis + (r.x >> 5), 1u << (r.x & 31));
+          }
+          nmem += __popc(acc);
+          __syncwarp();
+        }
+      }
+      if (lane != 0) insp = 0;  // counted once per warp below
+    } else if (lane == 0) {
       mem[0] = root;
       nmem = 1;
       vis[root >> 5] |= 1u << (root & 31);
-      if (model == RRG_IC) {
-        for (uint32_t head = 0; head < nmem; ++head) {
-          const uint32_t uu = mem[head];
-          const uint32_t jb = p.off[uu], je = p.off[uu + 1];
-          insp += je - jb;
-          for (uint32_t j = jb; j < je; ++j) {
-            const uint2 r = p.rec[j];
-            if ((vis[r.x >> 5] >> (r.x & 31)) & 1u) continue;
-            if (rng.u53() < bernoulli_threshold(r.y)) {
-              vis[r.x >> 5] |= 1u << (r.x & 31);
-              mem[nmem++] = r.x;
-            }
-          }
-        }
-      } else {
+      {
         uint32_t uu = root;
         for (;;) {
           const double d = rng.u01();
@@ -381,6 +606,20 @@ __global__ void k_build_rec(const uint32_t* src, const float* w, uint2* rec, uin
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     rec[j] = make_uint2(src[j], __float_as_uint(w[j]));
+  }
+}
+
+// Warp per vertex: 1 iff the in-list's sources strictly increase (no duplicate
+// sources), the precondition of the cooperative IC expansion.
+__global__ void k_dupfree(const uint32_t* off, const uint32_t* src, uint32_t n, uint8_t* out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * blockDim.x / 32;
+  for (uint64_t v = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; v < n;
+       v += warps) {
+    bool bad = false;
+    for (uint32_t j = off[v] + 1 + lane; j < off[v + 1]; j += 32) bad |= src[j] <= src[j - 1];
+    bad = __any_sync(kFull, bad);
+    if (lane == 0) out[v] = bad ? 0 : 1;
   }
 }
 
@@ -479,6 +718,17 @@ void prepare_ic(rrg_graph* g) {
     RRG_CUDA(cudaGetLastError());
     count_launch();
   }
+  g->dupfree.reserve_discard(g->n ? g->n : 1);
+  if (g->n) {
+    k_dupfree<<<g->num_sms * 16, 256, 0, g->stream>>>(g->off.ptr, g->src.ptr, g->n,
+                                                      g->dupfree.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+  }
+  const std::vector<uint64_t> jm = segment_matrices(32, 31);
+  g->jmat.reserve_discard(jm.size());
+  RRG_CUDA(cudaMemcpyAsync(g->jmat.ptr, jm.data(), jm.size() * 8, cudaMemcpyHostToDevice,
+                           g->stream));
   RRG_CUDA(cudaStreamSynchronize(g->stream));
   g->rec_ready = true;
 }

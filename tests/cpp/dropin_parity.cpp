@@ -1,0 +1,122 @@
+// dropin_parity.cpp -- the C++ drop-in, exercised the way a reference caller
+// would use it. TEST INFRASTRUCTURE (needs the reference headers; built by
+// tests/cpp/Makefile only where /root/reference exists).
+//
+// For each case an rrflow::Graph is built by the reference itself; the same
+// graph is handed to the GPU through rrgpu::Graph(num_vertices, reverse_offsets,
+// reverse_sources, reverse_weights) -- the one-line switch INTEGRATION.md
+// describes -- and run_imm / generate_batch / select_seeds of both libraries
+// are compared field by field. Exit code 0 iff everything is bit-identical.
+#include <cstdio>
+#include <vector>
+
+#include "rrflow/imm.hpp"
+#include "rrflow/sampling.hpp"
+#include "rrflow/selection.hpp"
+#include "rrgpu/rrgpu.hpp"
+
+namespace {
+
+int failures = 0;
+
+void expect(bool ok, const char* what, int case_id) {
+  std::printf("[%s] case %d: %s\n", ok ? "PASS" : "FAIL", case_id, what);
+  if (!ok) ++failures;
+}
+
+rrgpu::DiffusionModel to_gpu(rrflow::DiffusionModel m) {
+  return m == rrflow::DiffusionModel::IC ? rrgpu::DiffusionModel::IC : rrgpu::DiffusionModel::LT;
+}
+
+}  // namespace
+
+int main() {
+  struct Case {
+    rrflow::SynthKind kind;
+    uint32_t n;
+    double param;
+    uint64_t seed;
+    rrflow::DiffusionModel model;
+    uint32_t k;
+  };
+  const std::vector<Case> cases = {
+      {rrflow::SynthKind::scc_core, 200, 0.25, 19, rrflow::DiffusionModel::IC, 3},
+      {rrflow::SynthKind::scc_core, 2000, 0.05, 7, rrflow::DiffusionModel::IC, 10},
+      {rrflow::SynthKind::scc_core, 2000, 0.05, 7, rrflow::DiffusionModel::LT, 10},
+      {rrflow::SynthKind::erdos_renyi, 3000, 0.002, 11, rrflow::DiffusionModel::IC, 20},
+      {rrflow::SynthKind::erdos_renyi, 3000, 0.002, 11, rrflow::DiffusionModel::LT, 20},
+  };
+  int id = 0;
+  for (const Case& c : cases) {
+    ++id;
+    rrflow::Graph g = rrflow::synth_graph(c.kind, c.n, c.param, c.seed);
+    rrflow::generate_ic_weights(g, c.seed + 1);
+    if (c.model == rrflow::DiffusionModel::LT) rrflow::normalize_lt_weights(g);
+
+    // --- the switch: same reverse arrays, GPU graph ---------------------------
+    rrgpu::Graph dg(g.num_vertices, g.reverse_offsets, g.reverse_sources, g.reverse_weights);
+
+    rrflow::ImmConfig rc;
+    rc.k = c.k;
+    rc.model = c.model;
+    rc.workers = 4;
+    rc.rng_seed = 5;
+    const rrflow::ImmResult ref = rrflow::run_imm(g, rc);
+
+    rrgpu::ImmConfig gc;
+    gc.k = c.k;
+    gc.model = to_gpu(c.model);
+    gc.workers = 4;
+    gc.rng_seed = 5;
+    const rrgpu::ImmResult got = rrgpu::run_imm(dg, gc);
+
+    expect(ref.seeds.seeds == got.seeds.seeds, "run_imm seeds", id);
+    expect(ref.seeds.marginal_counts == got.seeds.marginal_counts, "run_imm marginals", id);
+    expect(ref.theta == got.theta && ref.theta_prime == got.theta_prime, "theta, theta'", id);
+    expect(ref.lower_bound == got.lower_bound, "lower bound", id);
+    expect(ref.sets_generated == got.sets_generated && ref.max_set_size == got.max_set_size &&
+               ref.mean_set_size == got.mean_set_size,
+           "set statistics", id);
+
+    // --- operator level: generate_batch + select_seeds -----------------------
+    rrflow::WorkPool pool(4);
+    rrflow::RRRStore rstore(g.num_vertices, pool.workers());
+    rrflow::Counter counter(g.num_vertices);
+    rrflow::generate_batch(g, c.model, 9, 3000, pool, rstore, &counter);
+    rrgpu::RRRStore gstore(dg);
+    rrgpu::generate_batch(dg, gc.model, 9, 3000, gstore, true);
+    bool same_sets = rstore.size() == gstore.size();
+    for (uint64_t j = 0; same_sets && j < rstore.size(); ++j) {
+      std::vector<uint32_t> a;
+      rstore.set(j).for_each_member([&](uint32_t v) { a.push_back(v); });
+      std::vector<uint32_t> b = gstore.set(j);
+      std::sort(b.begin(), b.end());
+      same_sets = a == b && gstore.set(j).front() == rstore.set(j).root;
+    }
+    expect(same_sets, "generate_batch sets (slot by slot)", id);
+    const std::vector<uint64_t> gc_counter = gstore.counter();
+    bool same_counter = true;
+    for (uint32_t v = 0; v < g.num_vertices; ++v) same_counter &= counter.get(v) == gc_counter[v];
+    expect(same_counter, "fused counter", id);
+    const rrflow::SeedSet rs = rrflow::select_seeds(rstore, g.num_vertices, c.k, pool, 0.25,
+                                                    &counter);
+    const rrgpu::SeedSet gs = rrgpu::select_seeds(gstore, g.num_vertices, c.k, 0.25, true);
+    expect(rs.seeds == gs.seeds && rs.marginal_counts == gs.marginal_counts, "select_seeds", id);
+  }
+  // error mapping: k > n -> std::invalid_argument, like validate_config
+  {
+    rrflow::Graph g = rrflow::synth_graph(rrflow::SynthKind::erdos_renyi, 5, 0.5, 1);
+    rrgpu::Graph dg(g.num_vertices, g.reverse_offsets, g.reverse_sources, g.reverse_weights);
+    rrgpu::ImmConfig gc;
+    gc.k = 6;
+    bool threw = false;
+    try {
+      rrgpu::run_imm(dg, gc);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    expect(threw, "k > n throws std::invalid_argument", 0);
+  }
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL PASS", failures);
+  return failures ? 1 : 0;
+}

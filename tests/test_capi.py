@@ -66,6 +66,36 @@ def test_bernoulli_threshold_equals_double_compare():
             assert (k < t) == expect, (w, k, t)
 
 
+def test_jump_ahead_matches_sequential_draws(port):
+    """T^k s == k calls of next_u64 (prng.hpp:33-43) for the GF(2) jump matrices."""
+    import ctypes as C
+    from paper_2411_09473_b200._lib import lib
+
+    def splitmix_state(seed):
+        s = []
+        x = seed
+        for _ in range(4):
+            x = (x + 0x9e3779b97f4a7c15) & (2**64 - 1)
+            z = x
+            z = ((z ^ (z >> 30)) * 0xbf58476d1ce4e5b9) & (2**64 - 1)
+            z = ((z ^ (z >> 27)) * 0x94d049bb133111eb) & (2**64 - 1)
+            s.append(z ^ (z >> 31))
+        return s
+
+    def out_of(s):  # xoshiro256** output of state s
+        r = (s[1] * 5) & (2**64 - 1)
+        r = ((r << 7) | (r >> 57)) & (2**64 - 1)
+        return (r * 9) & (2**64 - 1)
+
+    seed = port.derive_stream_seed(1, 12345)
+    draws = port.draws(seed, 5000)
+    s0 = (C.c_uint64 * 4)(*splitmix_state(seed))
+    for k in [0, 1, 2, 31, 32, 33, 1000, 4095, 4999]:
+        out = (C.c_uint64 * 4)()
+        lib.rrg_debug_jump(s0, k, out)
+        assert out_of(list(out)) == int(draws[k]), k
+
+
 def test_generators_are_deterministic_and_simple():
     from paper_2411_09473_b200 import graphs
     for name, n, m in [("cfg1", 1 << 10, 1 << 13), ("cfg3", 5000, 40000), ("cfg4", 5000, 40000),

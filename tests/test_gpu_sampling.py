@@ -81,6 +81,34 @@ def test_lt_cooperative_scan_threshold_changes_nothing(cuda, oracle, coop_min):
     assert_sets_equal(off, mem, ref)
 
 
+@pytest.mark.parametrize("coop_min", [1, 33, 256, 1 << 30])
+@pytest.mark.parametrize("name,n,m", [("cfg1", 1 << 11, 1 << 15), ("cfg5", 20000, 300000),
+                                      ("cfg3", 30000, 500000)])
+def test_ic_cooperative_expansion_is_exact(cuda, oracle, coop_min, name, n, m):
+    """Warp-cooperative in-list expansion with GF(2) jump-ahead segments draws the
+    same stream positions as the serial loop, whatever the threshold."""
+    cfg = graphs.scaled(graphs.CONFIGS[name], n, m)
+    arrays = graphs.generate(cfg)
+    _, st, off, mem = gpu_sample(arrays, IC, 21, 2000, ic_coop_min=coop_min)
+    ref = oracle.graph(*arrays).sample(IC, 21, 0, 2000, workers=4)
+    assert_sets_equal(off, mem, ref, msg=f"{name} coop_min={coop_min}")
+    assert (st.counter() == ref.counter).all()
+
+
+def test_ic_cooperative_expansion_with_duplicate_sources(cuda, oracle):
+    """Parallel edges disable the cooperative path for that in-list only."""
+    rng = np.random.default_rng(77)
+    n, m = 3000, 60000
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, 40, m).astype(np.uint32)  # long in-lists with repeats
+    keep = src != dst
+    w = rng.uniform(0.0, 0.05, keep.sum()).astype(np.float32)
+    arrays = P.build_graph(n, src[keep], dst[keep], w)
+    _, st, off, mem = gpu_sample(arrays, IC, 4, 1500, ic_coop_min=1)
+    ref = oracle.graph(*arrays).sample(IC, 4, 0, 1500)
+    assert_sets_equal(off, mem, ref)
+
+
 @pytest.mark.parametrize("inner", [1, 3, 32])
 def test_ic_inner_steps_change_nothing(cuda, oracle, inner):
     cfg = graphs.scaled(graphs.CONFIGS["cfg1"], 1 << 10, 1 << 14)
