@@ -191,6 +191,24 @@ class RRRStore:
                                    ptr(mem, C.c_uint32)))
         return off, mem
 
+    def export_into(self, offsets: np.ndarray, members: np.ndarray, first: int = 0,
+                    count: Optional[int] = None) -> int:
+        """Like export() but into caller-owned (e.g. pinned) host arrays; returns
+        the member count written. offsets needs count+1 entries."""
+        if count is None:
+            count = self.size() - first
+        check(lib.rrg_store_export(self._h, first, count, ptr(offsets, C.c_uint64), None))
+        total = int(offsets[count])
+        if total > members.size:
+            raise ValueError("members buffer too small")
+        check(lib.rrg_store_export(self._h, first, count, ptr(offsets, C.c_uint64),
+                                   ptr(members, C.c_uint32)))
+        return total
+
+    def counter_into(self, out: np.ndarray) -> np.ndarray:
+        check(lib.rrg_store_counter(self._h, ptr(out, C.c_uint64)))
+        return out
+
     def sets(self, first: int = 0, count: Optional[int] = None, sort: bool = True):
         off, mem = self.export(first, count)
         out = [mem[off[i]:off[i + 1]] for i in range(off.size - 1)]

@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <map>
+#include <mutex>
 #include <cstring>
 #include <new>
 #include <stdexcept>
@@ -24,9 +26,62 @@ void set_error(const std::string& msg) { t_err = msg; }
 
 namespace {
 std::atomic<uint64_t> g_launches{0};
+
+// Free blocks per device, keyed by size. Blocks are only ever reused for requests
+// between half and all of their size, so waste stays bounded.
+struct Pool {
+  std::mutex mu;
+  std::map<int, std::multimap<size_t, void*>> free_blocks;
+};
+Pool& pool() {
+  static Pool* p = new Pool;  // never destroyed: outlives every static DevBuf
+  return *p;
 }
+}  // namespace
+
 uint64_t launches() { return g_launches.load(); }
 void count_launch(uint64_t k) { g_launches += k; }
+
+void* pool_alloc(size_t bytes, size_t* granted) {
+  if (bytes == 0) bytes = 1;
+  bytes = (bytes + 255) & ~static_cast<size_t>(255);
+  int dev = 0;
+  RRG_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lock(pool().mu);
+    auto& fb = pool().free_blocks[dev];
+    auto it = fb.lower_bound(bytes);
+    if (it != fb.end() && it->first <= 2 * bytes) {
+      void* p = it->second;
+      *granted = it->first;
+      fb.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    // release every cached block of this device and retry once
+    cudaGetLastError();
+    std::lock_guard<std::mutex> lock(pool().mu);
+    for (auto& kv : pool().free_blocks[dev]) cudaFree(kv.second);
+    pool().free_blocks[dev].clear();
+    e = cudaMalloc(&p, bytes);
+  }
+  if (e != cudaSuccess) throw CudaError{e, "cudaMalloc"};
+  *granted = bytes;
+  return p;
+}
+
+void pool_free(void* p, size_t bytes) {
+  if (!p) return;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) == cudaSuccess) dev = attr.device;
+  std::lock_guard<std::mutex> lock(pool().mu);
+  pool().free_blocks[dev].emplace(bytes, p);
+}
 
 // Converts exceptions at the C boundary into status codes.
 template <typename Fn>
@@ -636,10 +691,12 @@ rrg_status rrg_store_counter(const rrg_store* s, uint64_t* counts) {
   if (!s || !counts) return invalid("null argument");
   return guarded([&]() -> rrg_status {
     rrg_graph* g = s->g;
-    std::vector<uint32_t> c(g->n);
-    d2h(c.data(), s->counter.ptr, g->n, g->stream);
+    if (!g->n) return RRG_OK;
+    auto* ms = const_cast<rrg_store*>(s);  // scratch only; the store's state is unchanged
+    ms->wide.reserve_discard(g->n);
+    launch_widen(s->counter.ptr, ms->wide.ptr, g->n, g->stream);
+    d2h(counts, ms->wide.ptr, g->n, g->stream);
     sync(g);
-    for (uint32_t v = 0; v < g->n; ++v) counts[v] = c[v];
     return RRG_OK;
   });
 }

@@ -25,37 +25,48 @@ struct CudaError {
     if (e_ != cudaSuccess) throw ::rrgpu::CudaError{e_, #call};          \
   } while (0)
 
+// Process-wide caching allocator (per device): freed blocks are kept and reused
+// for requests of 1/2..1x their size, so graph/store churn (the e2e path creates
+// a graph per call) does not pay cudaMalloc/cudaFree every time.
+void* pool_alloc(size_t bytes, size_t* granted);
+void pool_free(void* p, size_t bytes);
+
 // Owning device buffer, grow-only.
 template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t cap = 0;  // elements
+  size_t bytes = 0;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) pool_free(ptr, bytes);
     ptr = nullptr;
     cap = 0;
+    bytes = 0;
   }
   // Ensures capacity >= n elements; contents are NOT preserved.
   void reserve_discard(size_t n) {
     if (n <= cap) return;
     release();
-    RRG_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
-    cap = n;
+    size_t got = 0;
+    ptr = static_cast<T*>(pool_alloc(n * sizeof(T), &got));
+    bytes = got;
+    cap = got / sizeof(T);
   }
   // Ensures capacity >= n elements, preserving the first `keep` elements.
   void reserve_keep(size_t n, size_t keep, cudaStream_t s) {
     if (n <= cap) return;
-    T* np = nullptr;
-    RRG_CUDA(cudaMalloc(&np, n * sizeof(T)));
+    size_t got = 0;
+    T* np = static_cast<T*>(pool_alloc(n * sizeof(T), &got));
     if (keep) RRG_CUDA(cudaMemcpyAsync(np, ptr, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
     RRG_CUDA(cudaStreamSynchronize(s));
     release();
     ptr = np;
-    cap = n;
+    bytes = got;
+    cap = got / sizeof(T);
   }
 };
 
@@ -139,6 +150,7 @@ struct rrg_store {
   rrgpu::DevBuf<uint8_t> selected;
   rrgpu::DevBuf<uint32_t> snap;
   rrgpu::DevBuf<uint32_t> status;
+  rrgpu::DevBuf<uint64_t> wide;  // u64 staging of counter exports
 };
 
 namespace rrgpu {
@@ -201,6 +213,7 @@ void launch_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
                    uint32_t* status, cudaStream_t s);
 void launch_fraction(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
                      const uint8_t* in_seed_set, unsigned long long* hits, cudaStream_t s);
+void launch_widen(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t s);
 
 // ---- select.cu --------------------------------------------------------------
 struct SelectParams {

@@ -428,13 +428,23 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
         }
         ent += (pick < e ? pick + 1 : e) - b;
       } else {
-        // upper_bound: first cdf[t] > d (cdf is non-decreasing)
+        // upper_bound (first cdf[t] > d; cdf non-decreasing) as a 16-ary search:
+        // 15 independent pivot loads per level keep the dependent round trips
+        // at log16(deg) instead of log2(deg). Invariant: answer in [lo, hi].
         uint32_t lo = b, hi = e;
-        while (lo < hi) {
-          const uint32_t mid = lo + ((hi - lo) >> 1);
+        while (hi - lo > 16) {
+          const uint32_t step = (hi - lo) >> 4;
+          uint32_t below = 0;  // pivots with cdf <= d form a prefix
+#pragma unroll
+          for (uint32_t t = 1; t < 16; ++t) below += __ldg(p.cdf + lo + t * step) <= d ? 1u : 0u;
+          ent += 15;
+          const uint32_t nlo = below ? lo + below * step + 1 : lo;
+          hi = below < 15 ? lo + (below + 1) * step : hi;
+          lo = nlo;
+        }
+        while (lo < hi && __ldg(p.cdf + lo) <= d) {
+          ++lo;
           ++ent;
-          if (p.cdf[mid] > d) hi = mid;
-          else lo = mid + 1;
         }
         pick = lo;
       }

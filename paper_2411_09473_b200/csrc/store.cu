@@ -184,6 +184,12 @@ __global__ void k_fraction(const uint64_t* off, const uint32_t* mem, uint64_t ns
   if (lane == 0 && local) atomicAdd(hits, local);
 }
 
+__global__ void k_widen(const uint32_t* in, uint64_t* out, uint64_t n) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+
 int grid_for(uint64_t warps_needed) {
   const uint64_t blocks = (warps_needed * 32 + 255) / 256;
   return static_cast<int>(blocks < 1 ? 1 : (blocks > 65535 ? 65535 : blocks));
@@ -224,6 +230,13 @@ void launch_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
                    uint32_t* status, cudaStream_t s) {
   if (!nsets) return;
   k_invert<<<grid_for(nsets), 256, 0, s>>>(off, mem, nsets, icur, ioff, inv, status);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_widen(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t s) {
+  if (!n) return;
+  k_widen<<<1184, 256, 0, s>>>(in, out, n);
   RRG_CUDA(cudaGetLastError());
   count_launch();
 }
