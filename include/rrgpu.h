@@ -57,8 +57,9 @@ typedef enum {
                            (default; picks the identical index, reads ~log2(deg) entries) */
   RRG_OPT_LT_COOP_MIN = 1, /* in-list length from which LT scans go warp-cooperative */
   RRG_OPT_IC_INNER = 2, /* IC edge steps per scheduling round (1..64) */
-  RRG_OPT_IC_COOP_MIN = 3 /* IC in-list length from which the warp expands it cooperatively
+  RRG_OPT_IC_COOP_MIN = 3, /* IC in-list length from which the warp expands it cooperatively
                              (GF(2) jump-ahead segments); UINT32_MAX disables */
+  RRG_OPT_LT_KARY = 4   /* arity of the LT CDF search: 2, 4, 8 or 16 (default 16) */
 } rrg_option;
 rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value);
 

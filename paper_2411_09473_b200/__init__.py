@@ -117,7 +117,8 @@ class Graph:
         check(lib.rrg_graph_set_stream(self._h, C.c_void_p(cuda_stream_handle or None)))
 
     def set_option(self, opt: str, value: int) -> None:
-        code = {"lt_scan": 0, "lt_coop_min": 1, "ic_inner": 2, "ic_coop_min": 3}[opt]
+        code = {"lt_scan": 0, "lt_coop_min": 1, "ic_inner": 2, "ic_coop_min": 3,
+                "lt_kary": 4}[opt]
         check(lib.rrg_graph_set_option(self._h, code, int(value)))
 
     def last_batch_stats(self) -> "BatchStats":

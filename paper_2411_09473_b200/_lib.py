@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librrgpu.so")
+LIB_PATH = os.environ.get("RRGPU_LIB") or os.path.join(_HERE, "librrgpu.so")
 
 RRG_OK, RRG_EINVAL, RRG_ENOMEM, RRG_ECUDA = 0, 1, 2, 3
 

@@ -294,6 +294,11 @@ rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value) {
       if (value < 1 || value > 64) return invalid("ic_inner must be in [1, 64]");
       g->ic_inner = static_cast<uint32_t>(value);
       return RRG_OK;
+    case RRG_OPT_LT_KARY:
+      if (value != 2 && value != 4 && value != 8 && value != 16)
+        return invalid("lt_kary must be 2, 4, 8 or 16");
+      g->lt_kary = static_cast<int>(value);
+      return RRG_OK;
     case RRG_OPT_IC_COOP_MIN:
       if (value < 1) return invalid("ic_coop_min must be >= 1");
       g->ic_coop_min = static_cast<uint32_t>(std::min<int64_t>(value, UINT32_MAX));
@@ -423,7 +428,8 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.ctl = g->ctl.ptr;
       p.lt_scan = (g->lt_scan == kLtBsearch && g->cdf_monotone) ? kLtBsearch : kLtLinear;
       p.coop_min = g->coop_min;
-      p.jmat = g->jmat.ptr;
+      p.jtab = g->jtab.ptr;
+      p.lt_kary = g->lt_kary;
       p.dupfree = g->dupfree.ptr;
       p.ic_coop_min = g->ic_coop_min;
 

@@ -171,6 +171,38 @@ __device__ __forceinline__ void gf2_matvec(const uint64_t* __restrict__ M, uint6
   d = o3;
 }
 
+// Same product with byte tables (jump.cpp segment_tables): 32 independent
+// 32-byte loads, all in flight at once, then XORs.
+__device__ __forceinline__ void gf2_jump_tables(const uint64_t* __restrict__ T, uint64_t& a,
+                                                uint64_t& b, uint64_t& c, uint64_t& d) {
+  const uint64_t in[4] = {a, b, c, d};
+  uint64_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {  // one state word per group: 8 loads in flight
+    ulonglong2 x[8], y[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int p = 8 * g + q;
+      const uint32_t byte = static_cast<uint32_t>(in[g] >> (8 * q)) & 255u;
+      const ulonglong2* e =
+          reinterpret_cast<const ulonglong2*>(T + (static_cast<size_t>(p) * 256 + byte) * 4);
+      x[q] = __ldg(e);
+      y[q] = __ldg(e + 1);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      o0 ^= x[q].x;
+      o1 ^= x[q].y;
+      o2 ^= y[q].x;
+      o3 ^= y[q].y;
+    }
+  }
+  a = o0;
+  b = o1;
+  c = o2;
+  d = o3;
+}
+
 // 128-bit register filter in front of the table: a clear bit proves absence.
 struct Filter {
   uint64_t lo, hi;

@@ -101,7 +101,7 @@ struct rrg_graph {
   rrgpu::DevBuf<float> w;        // f32[m]   transpose weights
   rrgpu::DevBuf<uint2> rec;      // IC: {source, weight bits} per in-edge (lazy)
   rrgpu::DevBuf<double> cdf;     // LT: sequential fp64 prefix per in-list (lazy, +2 pad)
-  rrgpu::DevBuf<uint64_t> jmat;  // IC: jump matrices T^(32 l), l = 1..31
+  rrgpu::DevBuf<uint64_t> jtab;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint8_t> dupfree;  // IC: per-vertex strictly-increasing-sources flag
   uint32_t ic_coop_min = 256;    // IC: in-lists at least this long expand warp-cooperatively
   bool rec_ready = false;
@@ -109,6 +109,7 @@ struct rrg_graph {
   bool cdf_monotone = true;
   int lt_scan = rrgpu::kLtBsearch;  // fastest exact search; linear = reference trip count
   uint32_t coop_min = 64;        // LT: in-lists at least this long are scanned warp-cooperatively
+  int lt_kary = 16;              // LT: arity of the CDF search
   uint32_t ic_inner = 8;         // IC: edge steps per flat-loop iteration
   rrgpu::LaneScratch scratch;
   rrgpu::BigScratch big;
@@ -179,8 +180,9 @@ struct SampleParams {
   SampleCtl* ctl;
   int lt_scan;
   uint32_t coop_min;
+  int lt_kary;              // LT search arity (2, 4, 8, 16)
   // IC cooperative expansion of long in-lists
-  const uint64_t* jmat;     // 31 GF(2) matrices T^(32 l), l = 1..31 (jump.cpp)
+  const uint64_t* jtab;     // byte tables of T^(32 l), l = 1..31 (jump.cpp segment_tables)
   const uint8_t* dupfree;   // per vertex: in-list sources strictly increasing
   uint32_t ic_coop_min;     // in-lists at least this long go warp-cooperative
 };
@@ -196,6 +198,7 @@ void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inne
 void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t nlist,
                 uint32_t* bitmaps, uint32_t* lists, uint32_t workers, cudaStream_t s);
 std::vector<uint64_t> segment_matrices(uint64_t seg, int count);  // jump.cpp
+std::vector<uint64_t> segment_tables(uint64_t seg, int count);    // jump.cpp (byte tables)
 uint64_t launches();  // kernels launched by this library so far (bench evidence)
 void count_launch(uint64_t k = 1);
 

@@ -86,6 +86,31 @@ std::vector<uint64_t> segment_matrices(uint64_t seg, int count) {
   return out;
 }
 
+// Byte tables of the same matrices ("four Russians"): for byte position p of
+// the state and byte value x, tab[p][x] = XOR of the columns 8p+i with bit i of x
+// set. A jump is then 32 independent 32-byte loads XORed together instead of a
+// data-dependent walk over up to 256 columns. Layout per matrix: [32][256][4].
+std::vector<uint64_t> segment_tables(uint64_t seg, int count) {
+  const std::vector<uint64_t> mats = segment_matrices(seg, count);
+  std::vector<uint64_t> out(static_cast<size_t>(count) * 32 * 256 * 4);
+  for (int l = 0; l < count; ++l) {
+    const uint64_t* m = mats.data() + static_cast<size_t>(l) * 1024;
+    uint64_t* t = out.data() + static_cast<size_t>(l) * 32 * 256 * 4;
+    for (int p = 0; p < 32; ++p) {
+      for (int x = 0; x < 256; ++x) {
+        uint64_t acc[4] = {0, 0, 0, 0};
+        for (int i = 0; i < 8; ++i) {
+          if (!((x >> i) & 1)) continue;
+          const uint64_t* col = m + static_cast<size_t>(8 * p + i) * 4;
+          for (int w = 0; w < 4; ++w) acc[w] ^= col[w];
+        }
+        std::memcpy(t + (static_cast<size_t>(p) * 256 + x) * 4, acc, sizeof(acc));
+      }
+    }
+  }
+  return out;
+}
+
 }  // namespace rrgpu
 
 extern "C" void rrg_debug_jump(const uint64_t* state_in, uint64_t k, uint64_t* state_out) {

@@ -110,19 +110,21 @@ __device__ __forceinline__ void lane_insert(uint32_t* mem, uint64_t* tab, uint32
 // duplicate-free sources (K0 flag) the visited status of every edge is fixed
 // at list start, so
 //   1. the warp computes the unvisited mask of each 32-edge chunk (coalesced
-//      source loads, filter + table of the owner lane); chunk c -> lane c;
+//      record loads, four chunks in flight; visited = owner's filter + table,
+//      or the n-bit map on the big-set path); chunk c -> lane c; the Bernoulli
+//      thresholds of the window are staged in shared memory;
 //   2. the window's U draws are the next U positions of the slot's stream:
-//      lane l owns positions [32 l, 32 l + 32), reaches its first one with one
-//      GF(2) matrix T^(32 l) (csrc/jump.cpp) and draws for its unvisited edges
-//      in CSR order -- exactly the draws the reference makes, in its order;
-//   3. accepted sources are appended in CSR order (ballot prefix), inserted into
-//      the owner's table (CAS) and filter; the stream continues from the state
-//      of the lane that made the window's last draw.
-// Returns false when the set would exceed kMemCap (the slot is deferred).
+//      lane l owns positions [32 l, 32 l + 32), reaches its first one with the
+//      byte tables of T^(32 l) (csrc/jump.cpp) and draws for its unvisited
+//      edges in CSR order -- exactly the draws the reference makes, in order;
+//   3. accepted sources are appended in CSR order (ballot prefix) and marked
+//      visited (owner's table by CAS + filter, or the bit map); the stream
+//      continues from the state of the lane that made the window's last draw.
+// Returns false when a lane set would exceed kMemCap (the slot is deferred).
 // ---------------------------------------------------------------------------
 struct CoopState {
   uint64_t a, b, c, d;  // owner's RNG state
-  uint64_t flo, fhi;    // owner's filter
+  uint64_t flo, fhi;    // owner's filter (lane sets)
   uint32_t tag, lg, nmem;
 };
 
@@ -130,27 +132,42 @@ struct CoopSmem {
   uint32_t mask[32];
   uint32_t pre[32];
   uint32_t acc[32];
+  uint32_t thr[1024];  // weight bits of the window's edges
   unsigned long long st[4];
 };
 
+template <bool kBitmap>
 __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uint32_t* mem,
-                            uint64_t* tab, CoopState& s, CoopSmem& sm) {
+                            uint64_t* tab, uint32_t* vis, CoopState& s, CoopSmem& sm) {
   const int lane = threadIdx.x & 31;
   const Filter f{s.flo, s.fhi};
   uint64_t add_lo = 0, add_hi = 0;
   for (uint32_t wb = jb; wb < je; wb += 1024) {
     const uint32_t nch = (min(1024u, je - wb) + 31) >> 5;
-    // 1. unvisited mask per chunk
+    // 1. unvisited mask per chunk, four chunks of records in flight
     uint32_t mymask = 0;
-    for (uint32_t c = 0; c < nch; ++c) {
-      const uint32_t j = wb + 32 * c + lane;
-      bool unv = false;
-      if (j < je) {
-        const uint32_t v = __ldg(p.src + j);
-        unv = !(f.maybe(v) && tab_contains(tab, s.tag, s.lg, v));
+    for (uint32_t c0 = 0; c0 < nch; c0 += 4) {
+      uint2 r[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t j = wb + 32 * (c0 + q) + lane;
+        r[q] = (c0 + q < nch && j < je) ? __ldg(p.rec + j) : make_uint2(0u, 0u);
       }
-      const unsigned m = __ballot_sync(kFull, unv);
-      if (lane == static_cast<int>(c)) mymask = m;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t c = c0 + q;
+        if (c >= nch) break;
+        const uint32_t j = wb + 32 * c + lane;
+        bool unv = false;
+        if (j < je) {
+          const uint32_t v = r[q].x;
+          if (kBitmap) unv = !((vis[v >> 5] >> (v & 31)) & 1u);
+          else unv = !(f.maybe(v) && tab_contains(tab, s.tag, s.lg, v));
+          sm.thr[32 * c + lane] = r[q].y;
+        }
+        const unsigned m = __ballot_sync(kFull, unv);
+        if (lane == static_cast<int>(c)) mymask = m;
+      }
     }
     const uint32_t cnt = __popc(mymask);
     uint32_t incl = cnt;
@@ -168,7 +185,9 @@ __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uin
     const uint32_t r0 = 32u * lane;
     if (r0 < U) {
       Xoshiro st{s.a, s.b, s.c, s.d};
-      if (lane) gf2_matvec(p.jmat + static_cast<size_t>(lane - 1) * 1024, st.a, st.b, st.c, st.d);
+      if (lane)
+        gf2_jump_tables(p.jtab + static_cast<size_t>(lane - 1) * (32 * 256 * 4), st.a, st.b, st.c,
+                        st.d);
       uint32_t c = 0;  // chunk holding unvisited rank r0
       for (uint32_t step = 16; step; step >>= 1)
         if (c + step < nch && sm.pre[c + step] <= r0) c += step;
@@ -185,7 +204,7 @@ __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uin
         }
         const int bit = __ffs(m) - 1;
         m &= m - 1;
-        if (st.u53() < bernoulli_threshold(__ldg(p.rec + wb + 32 * c + bit).y)) acc |= 1u << bit;
+        if (st.u53() < bernoulli_threshold(sm.thr[32 * c + bit])) acc |= 1u << bit;
         ++done;
       }
       if (acc) atomicOr(&sm.acc[c], acc);
@@ -206,14 +225,16 @@ __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uin
     uint32_t A = __popc(am_lane);
     for (int o = 16; o; o >>= 1) A += __shfl_xor_sync(kFull, A, o);
     if (A) {
-      if (s.nmem + A > kMemCap) return false;
-      uint32_t lg2 = s.lg;
-      while (2 * (s.nmem + A) > (1u << lg2)) ++lg2;
-      if (lg2 != s.lg) {  // grow: re-insert the members under a fresh tag
-        s.lg = lg2;
-        ++s.tag;
-        for (uint32_t t = lane; t < s.nmem; t += 32) tab_insert_atomic(tab, s.tag, s.lg, mem[t]);
-        __syncwarp();
+      if (!kBitmap) {
+        if (s.nmem + A > kMemCap) return false;
+        uint32_t lg2 = s.lg;
+        while (2 * (s.nmem + A) > (1u << lg2)) ++lg2;
+        if (lg2 != s.lg) {  // grow: re-insert the members under a fresh tag
+          s.lg = lg2;
+          ++s.tag;
+          for (uint32_t t = lane; t < s.nmem; t += 32) tab_insert_atomic(tab, s.tag, s.lg, mem[t]);
+          __syncwarp();
+        }
       }
       unsigned cm = __ballot_sync(kFull, am_lane != 0);
       while (cm) {
@@ -223,10 +244,14 @@ __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uin
         if ((am >> lane) & 1u) {
           const uint32_t v = __ldg(p.src + wb + 32 * c + lane);
           mem[s.nmem + __popc(am & lanemask_lt())] = v;
-          tab_insert_atomic(tab, s.tag, s.lg, v);
-          const uint32_t b = Filter::bit(v);
-          if (b & 64) add_hi |= 1ull << (b & 63);
-          else add_lo |= 1ull << (b & 63);
+          if (kBitmap) {
+            atomicOr(vis + (v >> 5), 1u << (v & 31));
+          } else {
+            tab_insert_atomic(tab, s.tag, s.lg, v);
+            const uint32_t b = Filter::bit(v);
+            if (b & 64) add_hi |= 1ull << (b & 63);
+            else add_lo |= 1ull << (b & 63);
+          }
         }
         s.nmem += __popc(am);
       }
@@ -245,7 +270,11 @@ __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uin
 // ---------------------------------------------------------------------------
 // K1: IC sampler (sampling.hpp:90-111 per slot, :177-189 per batch)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_sample_ic(const SampleParams p, const uint32_t inner) {
+#ifndef RRG_IC_MIN_BLOCKS
+#define RRG_IC_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
+    k_sample_ic(const SampleParams p, const uint32_t inner) {
   __shared__ CoopSmem coop_sm[kBlock / 32];
   const int lane = threadIdx.x & 31;
   const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -294,8 +323,8 @@ __global__ void __launch_bounds__(kBlock) k_sample_ic(const SampleParams p, cons
       s.nmem = __shfl_sync(kFull, nmem, L);
       const uint32_t jb = __shfl_sync(kFull, j, L), je = __shfl_sync(kFull, jend, L);
       const uint64_t gl = gid - lane + L;
-      const bool ok = coop_expand(p, jb, je, p.lists + gl * kMemCap, p.tabs + gl * kTabCap, s,
-                                  coop_sm[threadIdx.x >> 5]);
+      const bool ok = coop_expand<false>(p, jb, je, p.lists + gl * kMemCap, p.tabs + gl * kTabCap,
+                                         nullptr, s, coop_sm[threadIdx.x >> 5]);
       if (lane == L) {
         want_coop = false;
         if (ok) {
@@ -349,6 +378,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_ic(const SampleParams p, cons
 // ---------------------------------------------------------------------------
 // K2: LT sampler (sampling.hpp:117-145 per slot)
 // ---------------------------------------------------------------------------
+template <int KARY>
 __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
   const int lane = threadIdx.x & 31;
   const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -386,36 +416,42 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
     const bool coop = active && linear && (e - b) >= p.coop_min;
     unsigned cm = __ballot_sync(kFull, coop);
     while (cm) {
-      // warp-cooperative linear scan of one lane's long in-list: 64 entries per
-      // iteration, one 16-byte load per lane, first hit by ballot
+      // warp-cooperative linear scan of one lane's long in-list: 4 x 64 entries
+      // per iteration (four independent 16-byte loads per lane in flight), the
+      // first hit located by ballot
       const int L = __ffs(cm) - 1;
       cm &= cm - 1;
       const uint32_t bL = __shfl_sync(kFull, b, L);
       const uint32_t eL = __shfl_sync(kFull, e, L);
       const double dL = __shfl_sync(kFull, d, L);
       uint32_t found = eL;
-      uint32_t chunks = 0;
-      for (uint32_t base = bL & ~1u; base < eL; base += 64) {
-        const uint32_t i0 = base + 2 * lane;
-        bool h0 = false, h1 = false;
-        if (i0 < eL) {
-          const double2 c = __ldg(reinterpret_cast<const double2*>(p.cdf + i0));
-          h0 = i0 >= bL && dL < c.x;
-          h1 = i0 + 1 < eL && dL < c.y;
+      uint64_t read = 0;
+      for (uint32_t base = bL & ~1u; base < eL && found == eL; base += 256) {
+        double2 c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t i0 = base + 64 * u + 2 * lane;
+          c[u] = i0 < eL ? __ldg(reinterpret_cast<const double2*>(p.cdf + i0))
+                         : make_double2(0.0, 0.0);
         }
-        ++chunks;
-        const unsigned hm = __ballot_sync(kFull, h0 || h1);
-        if (hm) {
-          const int f = __ffs(hm) - 1;
-          const unsigned first0 = __ballot_sync(kFull, h0);
-          found = base + 2 * f + (((first0 >> f) & 1u) ? 0 : 1);
-          break;
+        read += min(256u, eL - base);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t i0 = base + 64 * u + 2 * lane;
+          const bool h0 = i0 < eL && i0 >= bL && dL < c[u].x;
+          const bool h1 = i0 + 1 < eL && i0 + 1 >= bL && dL < c[u].y;
+          const unsigned hm = __ballot_sync(kFull, h0 || h1);
+          if (hm) {
+            const int f = __ffs(hm) - 1;
+            const unsigned first0 = __ballot_sync(kFull, h0);
+            found = base + 64 * u + 2 * f + (((first0 >> f) & 1u) ? 0 : 1);
+            break;
+          }
         }
       }
       if (lane == L) {
         pick = found;
-        const uint64_t span = static_cast<uint64_t>(chunks) * 64;
-        ent += (span < (uint64_t)(eL - (bL & ~1u))) ? span : (uint64_t)(eL - (bL & ~1u));
+        ent += read;
       }
     }
     if (active && !coop) {
@@ -428,18 +464,19 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
         }
         ent += (pick < e ? pick + 1 : e) - b;
       } else {
-        // upper_bound (first cdf[t] > d; cdf non-decreasing) as a 16-ary search:
-        // 15 independent pivot loads per level keep the dependent round trips
-        // at log16(deg) instead of log2(deg). Invariant: answer in [lo, hi].
+        // upper_bound (first cdf[t] > d; cdf non-decreasing) as a K-ary search:
+        // K-1 independent pivot loads per level keep the dependent round trips
+        // at logK(deg) instead of log2(deg). Invariant: answer in [lo, hi].
         uint32_t lo = b, hi = e;
-        while (hi - lo > 16) {
-          const uint32_t step = (hi - lo) >> 4;
+        while (hi - lo > static_cast<uint32_t>(KARY)) {
+          const uint32_t step = (hi - lo) / KARY;
           uint32_t below = 0;  // pivots with cdf <= d form a prefix
 #pragma unroll
-          for (uint32_t t = 1; t < 16; ++t) below += __ldg(p.cdf + lo + t * step) <= d ? 1u : 0u;
-          ent += 15;
+          for (uint32_t t = 1; t < KARY; ++t)
+            below += __ldg(p.cdf + lo + t * step) <= d ? 1u : 0u;
+          ent += KARY - 1;
           const uint32_t nlo = below ? lo + below * step + 1 : lo;
-          hi = below < 15 ? lo + (below + 1) * step : hi;
+          hi = below < KARY - 1 ? lo + (below + 1) * step : hi;
           lo = nlo;
         }
         while (lo < hi && __ldg(p.cdf + lo) <= d) {
@@ -487,6 +524,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
                                                        const uint32_t workers) {
   __shared__ uint64_t s_thr[kBlock / 32][32];
   __shared__ uint32_t s_src[kBlock / 32][32];
+  __shared__ CoopSmem coop_sm[kBlock / 32];
   const int lane = threadIdx.x & 31;
   const int wl = threadIdx.x >> 5;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -512,6 +550,14 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
         const uint32_t uu = mem[head];
         const uint32_t jb = p.off[uu], je = p.off[uu + 1];
         insp += je - jb;
+        if (je - jb >= p.ic_coop_min && p.dupfree[uu]) {
+          CoopState s{rng.a, rng.b, rng.c, rng.d, 0, 0, 0, 0, nmem};
+          coop_expand<true>(p, jb, je, mem, nullptr, vis, s, coop_sm[wl]);
+          rng = Xoshiro{s.a, s.b, s.c, s.d};
+          nmem = s.nmem;
+          __syncwarp();
+          continue;
+        }
         for (uint32_t base = jb; base < je; base += 32) {
           const uint32_t j = base + lane;
           const bool valid = j < je;
@@ -544,6 +590,10 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
             }
           }
           acc = __shfl_sync(kFull, acc, 0);
+          rng.a = __shfl_sync(kFull, rng.a, 0);  // keep the stream warp-uniform
+          rng.b = __shfl_sync(kFull, rng.b, 0);
+          rng.c = __shfl_sync(kFull, rng.c, 0);
+          rng.d = __shfl_sync(kFull, rng.d, 0);
           if ((acc >> lane) & 1u) {
             mem[nmem + __popc(acc & lanemask_lt())] = r.x;
             atomicOr(vis + (r.x >> 5), 1u << (r.x & 31));
@@ -635,17 +685,47 @@ __global__ void k_dupfree(const uint32_t* off, const uint32_t* src, uint32_t n, 
 
 // Sequential fp64 prefix per in-list, the exact add order of sampling.hpp:128-131.
 // One thread per vertex; `bad` flags a non-monotone prefix (NaN / negative weight).
+// Long in-lists stream through registers 32 weights at a time (eight 16-byte
+// loads in flight, sixteen 16-byte stores), so a 540K-entry hub costs ~the
+// dependent fp64 add chain rather than a memory round trip per entry.
 __global__ void k_build_cdf(const uint32_t* off, const float* w, double* cdf, uint32_t n,
                             uint32_t* bad) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     double acc = 0.0;
+    bool neg = false;
+    uint32_t j = off[v];
     const uint32_t e = off[v + 1];
-    for (uint32_t j = off[v]; j < e; ++j) {
+    for (; j < e && (j & 3u); ++j) {  // head up to a 16-byte boundary
       const float x = w[j];
-      if (!(x >= 0.0f)) *bad = 1;
+      neg |= !(x >= 0.0f);
       acc = __dadd_rn(acc, static_cast<double>(x));
       cdf[j] = acc;
     }
+    for (; j + 32 <= e; j += 32) {
+      float4 q[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) q[t] = __ldg(reinterpret_cast<const float4*>(w + j) + t);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float xs[4] = {q[t].x, q[t].y, q[t].z, q[t].w};
+        double out[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          neg |= !(xs[u] >= 0.0f);
+          acc = __dadd_rn(acc, static_cast<double>(xs[u]));
+          out[u] = acc;
+        }
+        reinterpret_cast<double2*>(cdf + j)[2 * t] = make_double2(out[0], out[1]);
+        reinterpret_cast<double2*>(cdf + j)[2 * t + 1] = make_double2(out[2], out[3]);
+      }
+    }
+    for (; j < e; ++j) {
+      const float x = w[j];
+      neg |= !(x >= 0.0f);
+      acc = __dadd_rn(acc, static_cast<double>(x));
+      cdf[j] = acc;
+    }
+    if (neg) *bad = 1;
   }
 }
 
@@ -698,16 +778,22 @@ int sampler_blocks_per_sm(int model, uint32_t) {
   if (model == RRG_IC)
     RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_ic, kBlock, 0));
   else
-    RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_lt, kBlock, 0));
+    RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_lt<16>, kBlock, 0));
   return b < 1 ? 1 : b;
 }
 
 void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner,
                     cudaStream_t s) {
-  if (model == RRG_IC)
+  if (model == RRG_IC) {
     k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
-  else
-    k_sample_lt<<<grid, kBlock, 0, s>>>(p);
+  } else {
+    switch (p.lt_kary) {
+      case 2: k_sample_lt<2><<<grid, kBlock, 0, s>>>(p); break;
+      case 4: k_sample_lt<4><<<grid, kBlock, 0, s>>>(p); break;
+      case 8: k_sample_lt<8><<<grid, kBlock, 0, s>>>(p); break;
+      default: k_sample_lt<16><<<grid, kBlock, 0, s>>>(p); break;
+    }
+  }
   RRG_CUDA(cudaGetLastError());
   count_launch();
 }
@@ -735,9 +821,9 @@ void prepare_ic(rrg_graph* g) {
     RRG_CUDA(cudaGetLastError());
     count_launch();
   }
-  const std::vector<uint64_t> jm = segment_matrices(32, 31);
-  g->jmat.reserve_discard(jm.size());
-  RRG_CUDA(cudaMemcpyAsync(g->jmat.ptr, jm.data(), jm.size() * 8, cudaMemcpyHostToDevice,
+  static const std::vector<uint64_t> jt = segment_tables(32, 31);  // host, built once
+  g->jtab.reserve_discard(jt.size());
+  RRG_CUDA(cudaMemcpyAsync(g->jtab.ptr, jt.data(), jt.size() * 8, cudaMemcpyHostToDevice,
                            g->stream));
   RRG_CUDA(cudaStreamSynchronize(g->stream));
   g->rec_ready = true;

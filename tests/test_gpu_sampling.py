@@ -62,11 +62,12 @@ def test_top_ups_continue_the_slot_stream(cuda, oracle, model):
     assert (st.counter() == ref.counter).all()
 
 
-def test_lt_binary_search_mode_is_identical(cuda, oracle):
+@pytest.mark.parametrize("kary", [2, 4, 8, 16])
+def test_lt_search_mode_is_identical(cuda, oracle, kary):
     cfg = graphs.scaled(graphs.CONFIGS["cfg4"], 40000, 600000)
     arrays = graphs.generate(cfg)
     _, st_a, off_a, mem_a = gpu_sample(arrays, LT, 3, 4000, lt_scan=0)
-    _, st_b, off_b, mem_b = gpu_sample(arrays, LT, 3, 4000, lt_scan=1)
+    _, st_b, off_b, mem_b = gpu_sample(arrays, LT, 3, 4000, lt_scan=1, lt_kary=kary)
     assert (off_a == off_b).all() and (mem_a == mem_b).all()
     ref = oracle.graph(*arrays).sample(LT, 3, 0, 4000, workers=4)
     assert_sets_equal(off_b, mem_b, ref)
