@@ -59,7 +59,11 @@ typedef enum {
   RRG_OPT_IC_INNER = 2, /* IC edge steps per scheduling round (1..64) */
   RRG_OPT_IC_COOP_MIN = 3, /* IC in-list length from which the warp expands it cooperatively
                              (GF(2) jump-ahead segments); UINT32_MAX disables */
-  RRG_OPT_LT_KARY = 4   /* arity of the LT CDF search: 2, 4, 8 or 16 (default 16) */
+  RRG_OPT_LT_KARY = 4,  /* arity of the LT CDF search: 2, 4, 8 or 16 (default 8) */
+  RRG_OPT_IC_MODE = 5,  /* IC schedule: 0 auto (pilot-measured), 1 lane per sample,
+                           2 warp per sample */
+  RRG_OPT_IC_WARP_MIN_INSP = 6 /* auto: warp per sample once the mean inspected
+                                  in-edges per set reaches this value */
 } rrg_option;
 rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value);
 

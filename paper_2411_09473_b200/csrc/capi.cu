@@ -294,6 +294,14 @@ rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value) {
       if (value < 1 || value > 64) return invalid("ic_inner must be in [1, 64]");
       g->ic_inner = static_cast<uint32_t>(value);
       return RRG_OK;
+    case RRG_OPT_IC_MODE:
+      if (value < 0 || value > 2) return invalid("ic_mode must be 0 (auto), 1 (lane) or 2 (warp)");
+      g->ic_mode = static_cast<int>(value);
+      return RRG_OK;
+    case RRG_OPT_IC_WARP_MIN_INSP:
+      if (value < 0) return invalid("ic_warp_min_insp must be >= 0");
+      g->ic_warp_min_insp = static_cast<double>(value);
+      return RRG_OK;
     case RRG_OPT_LT_KARY:
       if (value != 2 && value != 4 && value != 8 && value != 16)
         return invalid("lt_kary must be 2, 4, 8 or 16");
@@ -393,7 +401,14 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
     const auto t0 = std::chrono::steady_clock::now();
     rrg_batch_stats acc{};
     for (uint64_t done = 0; done < count;) {
-      const uint64_t c = std::min(kChunk, count - done);
+      uint64_t c = std::min(kChunk, count - done);
+      // IC execution mode: lane per sample (light sets) or warp per sample (heavy,
+      // hub-dominated sets). Auto mode measures a pilot chunk on a new graph
+      // first; sub-batches append in slot order, so splitting changes nothing.
+      if (model == RRG_IC && g->ic_mode == 0 && g->ic_mean_insp < 0) c = std::min<uint64_t>(c, 2048);
+      const bool ic_warp =
+          model == RRG_IC &&
+          (g->ic_mode == 2 || (g->ic_mode == 0 && g->ic_mean_insp >= g->ic_warp_min_insp));
       // staging sized from the running mean set size (first batch: a guess;
       // sets that do not fit are re-run once staging has grown)
       const double per_set = s->nsets ? static_cast<double>(s->total) / s->nsets * 1.5 + 8 : 96.0;
@@ -452,9 +467,10 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         } else {
           p.list = list;
           p.count = n_items;
-          const uint64_t grid_need = (n_items + block - 1) / block;
+          const uint64_t per_block = ic_warp ? block / 32 : block;  // samples per block
+          const uint64_t grid_need = (n_items + per_block - 1) / per_block;
           launch_sampler(model, p, static_cast<int>(std::min<uint64_t>(full_grid, grid_need)),
-                         g->ic_inner, st);
+                         g->ic_inner, ic_warp, st);
         }
         RRG_CUDA(cudaEventRecord(g->ev1, st));
         d2h(&ctl, g->ctl.ptr, 1, st);
@@ -501,6 +517,10 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         }
       }
       acc.edges_inspected += ctl.inspected;
+      if (model == RRG_IC) {
+        const double mean = static_cast<double>(ctl.inspected) / static_cast<double>(c);
+        g->ic_mean_insp = g->ic_mean_insp < 0 ? mean : 0.5 * (g->ic_mean_insp + mean);
+      }
       acc.entries_read += ctl.entries;
       const uint64_t before = s->total;
       commit_staged(s, c);

@@ -104,12 +104,15 @@ struct rrg_graph {
   rrgpu::DevBuf<uint64_t> jtab;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint8_t> dupfree;  // IC: per-vertex strictly-increasing-sources flag
   uint32_t ic_coop_min = 256;    // IC: in-lists at least this long expand warp-cooperatively
+  int ic_mode = 0;               // IC: 0 auto, 1 lane per sample, 2 warp per sample
+  double ic_mean_insp = -1.0;    // IC: running mean of inspected in-edges per set
+  double ic_warp_min_insp = 32768.0;  // auto: warp per sample from this mean on
   bool rec_ready = false;
   bool cdf_ready = false;
   bool cdf_monotone = true;
   int lt_scan = rrgpu::kLtBsearch;  // fastest exact search; linear = reference trip count
   uint32_t coop_min = 64;        // LT: in-lists at least this long are scanned warp-cooperatively
-  int lt_kary = 16;              // LT: arity of the CDF search
+  int lt_kary = 8;               // LT: arity of the CDF search (8 measured best at cfg4)
   uint32_t ic_inner = 8;         // IC: edge steps per flat-loop iteration
   rrgpu::LaneScratch scratch;
   rrgpu::BigScratch big;
@@ -175,6 +178,7 @@ struct SampleParams {
   uint32_t* slot_len;
   uint32_t* counter;
   const uint32_t* list;  // optional batch-local slot list (reruns); count = its length
+  uint32_t idx_base;     // range mode: batch-local index of dispenser item 0
   uint32_t* deferred;    // out: slots for the big-set path
   uint32_t* restage;     // out: slots refused for lack of staging
   SampleCtl* ctl;
@@ -194,7 +198,8 @@ void prepare_lt(rrg_graph* g);
 uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64);
 int sampler_block();
 int sampler_blocks_per_sm(int model, uint32_t ic_inner);
-void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, cudaStream_t s);
+void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, bool ic_warp,
+                    cudaStream_t s);
 void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t nlist,
                 uint32_t* bitmaps, uint32_t* lists, uint32_t workers, cudaStream_t s);
 std::vector<uint64_t> segment_matrices(uint64_t seg, int count);  // jump.cpp

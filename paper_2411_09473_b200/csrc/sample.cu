@@ -19,6 +19,7 @@
 // full -- are deferred to k_big (warp per set, n-bit visited map), which
 // replays the same stream from the start.
 #include <cooperative_groups.h>
+#include <cuda_pipeline.h>
 
 #include "internal.hpp"
 
@@ -85,7 +86,7 @@ __device__ __forceinline__ bool fetch_slot(const SampleParams& p, bool need, boo
     exhausted = true;
     return false;
   }
-  idx = p.list ? p.list[k] : static_cast<uint32_t>(k);
+  idx = p.list ? p.list[k] : p.idx_base + static_cast<uint32_t>(k);
   return true;
 }
 
@@ -373,6 +374,158 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
   }
   p.tags[gid] = tag;
   flush_counters(p, insp, insp);
+}
+
+// ---------------------------------------------------------------------------
+// K1w: IC sampler, WARP per sample -- for heavy samples (hub-dominated graphs
+// such as cfg5, where a set inspects ~1M in-edges and there are fewer sets than
+// lanes). The warp keeps one sample's state warp-uniform (CoopState) in lane
+// 0's scratch; long duplicate-free in-lists go through coop_expand, short ones
+// through 32-edge chunks: coalesced loads, visited and thresholds in parallel,
+// the draws for the chunk's unvisited edges made in CSR order (lane 0), an
+// exact edge-by-edge replay when a chunk repeats a source.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(const SampleParams p) {
+  __shared__ CoopSmem coop_sm[kBlock / 32];
+  __shared__ uint64_t s_thr[kBlock / 32][32];
+  __shared__ uint32_t s_src[kBlock / 32][32];
+  const int lane = threadIdx.x & 31;
+  const int wl = threadIdx.x >> 5;
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  uint32_t* mem = p.lists + gw * 32 * kMemCap;  // lane 0's scratch region
+  uint64_t* tab = p.tabs + gw * 32 * kTabCap;
+  uint32_t tag = p.tags[gw * 32];
+  uint64_t insp = 0;
+  for (;;) {
+    unsigned long long k = 0;
+    if (lane == 0) k = atomicAdd(&p.ctl->next, 1ull);
+    k = __shfl_sync(kFull, k, 0);
+    if (k >= p.count) break;
+    const uint32_t idx = p.list ? p.list[k] : p.idx_base + static_cast<uint32_t>(k);
+    Xoshiro rng;
+    rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
+    const uint32_t root = static_cast<uint32_t>(rng.below(p.n));
+    CoopState s{rng.a, rng.b, rng.c, rng.d, 0, 0, ++tag, kTabLog0, 1};
+    Filter flt;
+    flt.clear();
+    flt.add(root);
+    s.flo = flt.lo;
+    s.fhi = flt.hi;
+    if (lane == 0) {
+      mem[0] = root;
+      tab_insert(tab, s.tag, s.lg, root);
+    }
+    __syncwarp();
+    bool ok = true;
+    for (uint32_t head = 0; head < s.nmem && ok; ++head) {
+      const uint32_t u = mem[head];
+      const uint32_t jb = p.off[u], je = p.off[u + 1];
+      insp += je - jb;
+      if (je - jb >= p.ic_coop_min && p.dupfree[u]) {
+        ok = coop_expand<false>(p, jb, je, mem, tab, nullptr, s, coop_sm[wl]);
+        __syncwarp();
+        continue;
+      }
+      for (uint32_t base = jb; base < je && ok; base += 32) {
+        const uint32_t j = base + lane;
+        const bool valid = j < je;
+        const uint2 r = valid ? __ldg(p.rec + j) : make_uint2(0xffffffffu, 0);
+        const Filter f{s.flo, s.fhi};
+        const bool unv = valid && !(f.maybe(r.x) && tab_contains(tab, s.tag, s.lg, r.x));
+        const unsigned peers = __match_any_sync(kFull, r.x);
+        const bool dup = valid && (peers & lanemask_lt()) != 0;
+        const unsigned um = __ballot_sync(kFull, unv);
+        const bool any_dup = __any_sync(kFull, dup);
+        if (!um) continue;  // every source already visited: no draws
+        s_thr[wl][lane] = bernoulli_threshold(r.y);
+        s_src[wl][lane] = r.x;
+        __syncwarp();
+        Xoshiro st{s.a, s.b, s.c, s.d};
+        unsigned acc = 0;
+        if (lane == 0) {
+          if (!any_dup) {
+            for (unsigned mm = um; mm; mm &= mm - 1) {
+              const int l = __ffs(mm) - 1;
+              if (st.u53() < s_thr[wl][l]) acc |= 1u << l;
+            }
+          } else {  // repeated sources: edge by edge against the live set
+            const int nv = static_cast<int>(min(32u, je - base));
+            for (int l = 0; l < nv; ++l) {
+              const uint32_t v = s_src[wl][l];
+              bool seen = f.maybe(v) && tab_contains(tab, s.tag, s.lg, v);
+              for (int q = 0; q < l && !seen; ++q) seen = ((acc >> q) & 1u) && s_src[wl][q] == v;
+              if (seen) continue;
+              if (st.u53() < s_thr[wl][l]) acc |= 1u << l;
+            }
+          }
+        }
+        acc = __shfl_sync(kFull, acc, 0);
+        s.a = __shfl_sync(kFull, st.a, 0);
+        s.b = __shfl_sync(kFull, st.b, 0);
+        s.c = __shfl_sync(kFull, st.c, 0);
+        s.d = __shfl_sync(kFull, st.d, 0);
+        const uint32_t A = __popc(acc);
+        if (A) {
+          if (s.nmem + A > kMemCap) {
+            ok = false;
+            break;
+          }
+          uint32_t lg2 = s.lg;
+          while (2 * (s.nmem + A) > (1u << lg2)) ++lg2;
+          if (lg2 != s.lg) {
+            s.lg = lg2;
+            ++s.tag;
+            for (uint32_t t = lane; t < s.nmem; t += 32) tab_insert_atomic(tab, s.tag, s.lg, mem[t]);
+            __syncwarp();
+          }
+          uint64_t add_lo = 0, add_hi = 0;
+          if ((acc >> lane) & 1u) {
+            mem[s.nmem + __popc(acc & lanemask_lt())] = r.x;
+            tab_insert_atomic(tab, s.tag, s.lg, r.x);
+            const uint32_t b = Filter::bit(r.x);
+            if (b & 64) add_hi = 1ull << (b & 63);
+            else add_lo = 1ull << (b & 63);
+          }
+          for (int o = 16; o; o >>= 1) {
+            add_lo |= __shfl_xor_sync(kFull, add_lo, o);
+            add_hi |= __shfl_xor_sync(kFull, add_hi, o);
+          }
+          s.flo |= add_lo;
+          s.fhi |= add_hi;
+          s.nmem += A;
+        }
+        __syncwarp();
+      }
+    }
+    tag = s.tag;
+    if (!ok) {
+      if (lane == 0) defer_slot(p, idx);
+      continue;
+    }
+    // write-out: staging + fused counter, warp-parallel
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(&p.ctl->cursor, (unsigned long long)s.nmem);
+    pos = __shfl_sync(kFull, pos, 0);
+    if (pos + s.nmem > p.stage_cap) {
+      if (lane == 0) restage_slot(p, idx, s.nmem);
+      continue;
+    }
+    for (uint32_t t = lane; t < s.nmem; t += 32) {
+      const uint32_t v = mem[t];
+      p.stage[pos + t] = v;
+      if (p.counter) atomicAdd(p.counter + v, 1u);
+    }
+    if (lane == 0) {
+      p.slot_start[idx] = pos;
+      p.slot_len[idx] = s.nmem;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    p.tags[gw * 32] = tag;
+    atomicAdd(&p.ctl->inspected, (unsigned long long)insp);
+    atomicAdd(&p.ctl->entries, (unsigned long long)insp);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -689,12 +842,16 @@ __global__ void k_dupfree(const uint32_t* off, const uint32_t* src, uint32_t n, 
 // loads in flight, sixteen 16-byte stores), so a 540K-entry hub costs ~the
 // dependent fp64 add chain rather than a memory round trip per entry.
 __global__ void k_build_cdf(const uint32_t* off, const float* w, double* cdf, uint32_t n,
-                            uint32_t* bad) {
+                            uint32_t* bad, uint32_t long_min, uint32_t* longv, uint32_t* nlong) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     double acc = 0.0;
     bool neg = false;
     uint32_t j = off[v];
     const uint32_t e = off[v + 1];
+    if (e - j >= long_min) {  // hubs: warp per list (k_build_cdf_long)
+      longv[atomicAdd(nlong, 1u)] = v;
+      continue;
+    }
     for (; j < e && (j & 3u); ++j) {  // head up to a 16-byte boundary
       const float x = w[j];
       neg |= !(x >= 0.0f);
@@ -726,6 +883,71 @@ __global__ void k_build_cdf(const uint32_t* off, const float* w, double* cdf, ui
       cdf[j] = acc;
     }
     if (neg) *bad = 1;
+  }
+}
+
+// Hub in-lists: one warp per list. The warp streams the weights into shared
+// memory with asynchronous copies (LDGSTS), double-buffered 512 entries ahead,
+// while lane 0 runs the dependent fp64 add chain out of shared memory; the warp
+// then writes the 512 prefix values back with coalesced stores. The chain
+// itself -- the reference's sequential order -- is the only serial part.
+constexpr int kCdfChunk = 512;
+constexpr int kCdfWarps = 4;
+__global__ void __launch_bounds__(kCdfWarps * 32)
+    k_build_cdf_long(const uint32_t* off, const float* w, double* cdf, const uint32_t* longv,
+                     const uint32_t* nlong, uint32_t* bad) {
+  __shared__ float sw[kCdfWarps][2][kCdfChunk];
+  __shared__ double sd[kCdfWarps][kCdfChunk];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const uint32_t nw = gridDim.x * kCdfWarps;
+  for (uint32_t i = blockIdx.x * kCdfWarps + wl; i < *nlong; i += nw) {
+    const uint32_t v = longv[i];
+    const uint32_t b = off[v], e = off[v + 1];
+    auto fetch = [&](uint32_t c0, int buf) {
+      const uint32_t len = min(static_cast<uint32_t>(kCdfChunk), e - c0);
+      for (uint32_t t = lane; t < len; t += 32)
+        __pipeline_memcpy_async(&sw[wl][buf][t], w + c0 + t, sizeof(float));
+      __pipeline_commit();
+    };
+    double acc = 0.0;
+    bool neg = false;
+    fetch(b, 0);
+    int cur = 0;
+    for (uint32_t c0 = b; c0 < e; c0 += kCdfChunk, cur ^= 1) {
+      const uint32_t len = min(static_cast<uint32_t>(kCdfChunk), e - c0);
+      if (c0 + kCdfChunk < e) {
+        fetch(c0 + kCdfChunk, cur ^ 1);
+        __pipeline_wait_prior(1);  // this chunk landed; the next stays in flight
+      } else {
+        __pipeline_wait_prior(0);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const float* x = sw[wl][cur];
+        double* y = sd[wl];
+        uint32_t t = 0;
+        for (; t + 8 <= len; t += 8) {
+          float xs[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) xs[u] = x[t + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            neg |= !(xs[u] >= 0.0f);
+            acc = __dadd_rn(acc, static_cast<double>(xs[u]));
+            y[t + u] = acc;
+          }
+        }
+        for (; t < len; ++t) {
+          neg |= !(x[t] >= 0.0f);
+          acc = __dadd_rn(acc, static_cast<double>(x[t]));
+          y[t] = acc;
+        }
+      }
+      __syncwarp();
+      for (uint32_t t = lane; t < len; t += 32) cdf[c0 + t] = sd[wl][t];
+      __syncwarp();
+    }
+    if (lane == 0 && neg) *bad = 1;
   }
 }
 
@@ -782,10 +1004,11 @@ int sampler_blocks_per_sm(int model, uint32_t) {
   return b < 1 ? 1 : b;
 }
 
-void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner,
+void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, bool ic_warp,
                     cudaStream_t s) {
   if (model == RRG_IC) {
-    k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
+    if (ic_warp) k_sample_ic_warp<<<grid, kBlock, 0, s>>>(p);
+    else k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
   } else {
     switch (p.lt_kary) {
       case 2: k_sample_lt<2><<<grid, kBlock, 0, s>>>(p); break;
@@ -832,15 +1055,24 @@ void prepare_ic(rrg_graph* g) {
 void prepare_lt(rrg_graph* g) {
   if (g->cdf_ready) return;
   g->cdf.reserve_discard(g->m + 2);  // +2: the paired 16-byte loads may touch cdf[m]
-  RRG_CUDA(cudaMemsetAsync(g->cdf.ptr, 0, (g->m + 2) * sizeof(double), g->stream));
-  DevBuf<uint32_t> bad;
-  bad.reserve_discard(1);
-  RRG_CUDA(cudaMemsetAsync(bad.ptr, 0, 4, g->stream));
+  RRG_CUDA(cudaMemsetAsync(g->cdf.ptr + g->m, 0, 2 * sizeof(double), g->stream));
+  DevBuf<uint32_t> bad;  // [0] bad flag, [1] number of hub lists
+  bad.reserve_discard(2);
+  RRG_CUDA(cudaMemsetAsync(bad.ptr, 0, 8, g->stream));
   if (g->m) {
+    DevBuf<uint32_t> longv;
+    longv.reserve_discard(g->n);
+    const uint32_t long_min = 4096;
     const int blocks = (g->n + 127) / 128;
-    k_build_cdf<<<blocks, 128, 0, g->stream>>>(g->off.ptr, g->w.ptr, g->cdf.ptr, g->n, bad.ptr);
+    k_build_cdf<<<blocks, 128, 0, g->stream>>>(g->off.ptr, g->w.ptr, g->cdf.ptr, g->n, bad.ptr,
+                                              long_min, longv.ptr, bad.ptr + 1);
     RRG_CUDA(cudaGetLastError());
     count_launch();
+    k_build_cdf_long<<<g->num_sms * 4, kCdfWarps * 32, 0, g->stream>>>(
+        g->off.ptr, g->w.ptr, g->cdf.ptr, longv.ptr, bad.ptr + 1, bad.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+    RRG_CUDA(cudaStreamSynchronize(g->stream));  // longv is released at scope end
   }
   uint32_t hbad = 0;
   RRG_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, 4, cudaMemcpyDeviceToHost, g->stream));

@@ -82,15 +82,17 @@ def test_lt_cooperative_scan_threshold_changes_nothing(cuda, oracle, coop_min):
     assert_sets_equal(off, mem, ref)
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("coop_min", [1, 33, 256, 1 << 30])
 @pytest.mark.parametrize("name,n,m", [("cfg1", 1 << 11, 1 << 15), ("cfg5", 20000, 300000),
                                       ("cfg3", 30000, 500000)])
-def test_ic_cooperative_expansion_is_exact(cuda, oracle, coop_min, name, n, m):
+def test_ic_cooperative_expansion_is_exact(cuda, oracle, coop_min, name, n, m, mode):
     """Warp-cooperative in-list expansion with GF(2) jump-ahead segments draws the
-    same stream positions as the serial loop, whatever the threshold."""
+    same stream positions as the serial loop, whatever the threshold, in both
+    the lane-per-sample (1) and warp-per-sample (2) schedules."""
     cfg = graphs.scaled(graphs.CONFIGS[name], n, m)
     arrays = graphs.generate(cfg)
-    _, st, off, mem = gpu_sample(arrays, IC, 21, 2000, ic_coop_min=coop_min)
+    _, st, off, mem = gpu_sample(arrays, IC, 21, 2000, ic_coop_min=coop_min, ic_mode=mode)
     ref = oracle.graph(*arrays).sample(IC, 21, 0, 2000, workers=4)
     assert_sets_equal(off, mem, ref, msg=f"{name} coop_min={coop_min}")
     assert (st.counter() == ref.counter).all()
@@ -105,9 +107,10 @@ def test_ic_cooperative_expansion_with_duplicate_sources(cuda, oracle):
     keep = src != dst
     w = rng.uniform(0.0, 0.05, keep.sum()).astype(np.float32)
     arrays = P.build_graph(n, src[keep], dst[keep], w)
-    _, st, off, mem = gpu_sample(arrays, IC, 4, 1500, ic_coop_min=1)
     ref = oracle.graph(*arrays).sample(IC, 4, 0, 1500)
-    assert_sets_equal(off, mem, ref)
+    for mode in (1, 2):
+        _, st, off, mem = gpu_sample(arrays, IC, 4, 1500, ic_coop_min=1, ic_mode=mode)
+        assert_sets_equal(off, mem, ref)
 
 
 @pytest.mark.parametrize("inner", [1, 3, 32])
