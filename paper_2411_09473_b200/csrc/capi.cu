@@ -409,6 +409,14 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       const bool ic_warp =
           model == RRG_IC &&
           (g->ic_mode == 2 || (g->ic_mode == 0 && g->ic_mean_insp >= g->ic_warp_min_insp));
+      // Tagged tables are never cleared, which is only sound while every region
+      // keeps one owner; re-zero them when the region layout changes.
+      if (g->scratch.layout != (ic_warp ? 1 : 0)) {
+        LaneScratch& sc = g->scratch;
+        RRG_CUDA(cudaMemsetAsync(sc.tabs.ptr, 0, sc.lanes * kTabCap * sizeof(uint64_t), st));
+        RRG_CUDA(cudaMemsetAsync(sc.tags.ptr, 0, sc.lanes * sizeof(uint32_t), st));
+        sc.layout = ic_warp ? 1 : 0;
+      }
       // staging sized from the running mean set size (first batch: a guess;
       // sets that do not fit are re-run once staging has grown)
       const double per_set = s->nsets ? static_cast<double>(s->total) / s->nsets * 1.5 + 8 : 96.0;

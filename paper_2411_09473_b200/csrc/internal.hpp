@@ -75,6 +75,7 @@ enum LtScan : int { kLtLinear = 0, kLtBsearch = 1 };
 // Per-lane sampler scratch: visit-order list + tagged hash table + tag.
 struct LaneScratch {
   uint64_t lanes = 0;
+  int layout = 0;  // 0: one region per lane (IC lane mode, LT); 1: one per warp (IC warp mode)
   DevBuf<uint32_t> lists;
   DevBuf<uint64_t> tabs;
   DevBuf<uint32_t> tags;
@@ -106,7 +107,8 @@ struct rrg_graph {
   uint32_t ic_coop_min = 256;    // IC: in-lists at least this long expand warp-cooperatively
   int ic_mode = 0;               // IC: 0 auto, 1 lane per sample, 2 warp per sample
   double ic_mean_insp = -1.0;    // IC: running mean of inspected in-edges per set
-  double ic_warp_min_insp = 32768.0;  // auto: warp per sample from this mean on
+  double ic_warp_min_insp = 1024.0;  // auto: warp per sample from this mean on (cfg1 5.5K
+                                     // and cfg5 986K run faster per warp; cfg3 237 per lane)
   bool rec_ready = false;
   bool cdf_ready = false;
   bool cdf_monotone = true;

@@ -139,7 +139,8 @@ struct CoopSmem {
 
 template <bool kBitmap>
 __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uint32_t* mem,
-                            uint64_t* tab, uint32_t* vis, CoopState& s, CoopSmem& sm) {
+                            uint64_t* tab, uint32_t* vis, CoopState& s, CoopSmem& sm,
+                            uint32_t memcap = kMemCap) {
   const int lane = threadIdx.x & 31;
   const Filter f{s.flo, s.fhi};
   uint64_t add_lo = 0, add_hi = 0;
@@ -227,7 +228,7 @@ __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uin
     for (int o = 16; o; o >>= 1) A += __shfl_xor_sync(kFull, A, o);
     if (A) {
       if (!kBitmap) {
-        if (s.nmem + A > kMemCap) return false;
+        if (s.nmem + A > memcap) return false;
         uint32_t lg2 = s.lg;
         while (2 * (s.nmem + A) > (1u << lg2)) ++lg2;
         if (lg2 != s.lg) {  // grow: re-insert the members under a fresh tag
@@ -379,12 +380,15 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
 // ---------------------------------------------------------------------------
 // K1w: IC sampler, WARP per sample -- for heavy samples (hub-dominated graphs
 // such as cfg5, where a set inspects ~1M in-edges and there are fewer sets than
-// lanes). The warp keeps one sample's state warp-uniform (CoopState) in lane
-// 0's scratch; long duplicate-free in-lists go through coop_expand, short ones
-// through 32-edge chunks: coalesced loads, visited and thresholds in parallel,
-// the draws for the chunk's unvisited edges made in CSR order (lane 0), an
-// exact edge-by-edge replay when a chunk repeats a source.
+// lanes). The warp keeps one sample's state warp-uniform (CoopState) and owns
+// the scratch of all its 32 lanes as ONE region (32K members, 64K-entry
+// table), so sets up to 32K members never leave the kernel. Long
+// duplicate-free in-lists go through coop_expand, short ones through 32-edge
+// chunks: coalesced loads, visited and thresholds in parallel, the draws for
+// the chunk's unvisited edges made in CSR order (lane 0), an exact
+// edge-by-edge replay when a chunk repeats a source.
 // ---------------------------------------------------------------------------
+constexpr uint32_t kWarpMemCap = 32 * kMemCap;
 __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(const SampleParams p) {
   __shared__ CoopSmem coop_sm[kBlock / 32];
   __shared__ uint64_t s_thr[kBlock / 32][32];
@@ -392,7 +396,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
   const int lane = threadIdx.x & 31;
   const int wl = threadIdx.x >> 5;
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  uint32_t* mem = p.lists + gw * 32 * kMemCap;  // lane 0's scratch region
+  uint32_t* mem = p.lists + gw * 32 * kMemCap;  // the warp's 32 lane regions, contiguous
   uint64_t* tab = p.tabs + gw * 32 * kTabCap;
   uint32_t tag = p.tags[gw * 32];
   uint64_t insp = 0;
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
       const uint32_t jb = p.off[u], je = p.off[u + 1];
       insp += je - jb;
       if (je - jb >= p.ic_coop_min && p.dupfree[u]) {
-        ok = coop_expand<false>(p, jb, je, mem, tab, nullptr, s, coop_sm[wl]);
+        ok = coop_expand<false>(p, jb, je, mem, tab, nullptr, s, coop_sm[wl], kWarpMemCap);
         __syncwarp();
         continue;
       }
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
         s.d = __shfl_sync(kFull, st.d, 0);
         const uint32_t A = __popc(acc);
         if (A) {
-          if (s.nmem + A > kMemCap) {
+          if (s.nmem + A > kWarpMemCap) {
             ok = false;
             break;
           }
