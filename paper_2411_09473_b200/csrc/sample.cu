@@ -40,12 +40,13 @@ __device__ __forceinline__ void restage_slot(const SampleParams& p, uint32_t idx
 }
 
 // Writes a finished set to staging, bumps the fused counter, records the slot.
-__device__ __forceinline__ void emit_set(const SampleParams& p, uint32_t idx, const uint32_t* mem,
+// False when staging is full (the slot is re-run later and counted then).
+__device__ __forceinline__ bool emit_set(const SampleParams& p, uint32_t idx, const uint32_t* mem,
                                          uint32_t nmem) {
   const unsigned long long pos = atomicAdd(&p.ctl->cursor, (unsigned long long)nmem);
   if (pos + nmem > p.stage_cap) {
     restage_slot(p, idx, nmem);
-    return;
+    return false;
   }
   uint32_t* out = p.stage + pos;
   for (uint32_t t = 0; t < nmem; ++t) {
@@ -55,6 +56,7 @@ __device__ __forceinline__ void emit_set(const SampleParams& p, uint32_t idx, co
   }
   p.slot_start[idx] = pos;
   p.slot_len[idx] = nmem;
+  return true;
 }
 
 __device__ __forceinline__ void flush_counters(const SampleParams& p, uint64_t insp,
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
   flt.clear();
   bool active = false, exhausted = false, want_coop = false;
   uint32_t idx = 0, nmem = 0, head = 0, lg = kTabLog0, j = 0, jend = 0;
-  uint64_t insp = 0;
+  uint64_t insp = 0, sinsp = 0;  // committed / current sample's inspected in-edges
 
   for (;;) {
     if (fetch_slot(p, !active && !exhausted, exhausted, idx)) {
@@ -300,6 +302,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
       mem[0] = root;
       nmem = 1;
       head = 0;
+      sinsp = 0;
       j = jend = 0;
       tab_insert(tab, tag, lg, root);
       flt.add(root);
@@ -366,10 +369,10 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
       const uint32_t u = mem[head++];  // FIFO dequeue (sampling.hpp:96-97)
       j = p.off[u];
       jend = p.off[u + 1];
-      insp += jend - j;
+      sinsp += jend - j;
       want_coop = jend - j >= p.ic_coop_min && p.dupfree[u];
     } else {
-      emit_set(p, idx, mem, nmem);
+      if (emit_set(p, idx, mem, nmem)) insp += sinsp;
       active = false;
     }
   }
@@ -421,10 +424,11 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
     }
     __syncwarp();
     bool ok = true;
+    uint64_t sinsp = 0;
     for (uint32_t head = 0; head < s.nmem && ok; ++head) {
       const uint32_t u = mem[head];
       const uint32_t jb = p.off[u], je = p.off[u + 1];
-      insp += je - jb;
+      sinsp += je - jb;
       if (je - jb >= p.ic_coop_min && p.dupfree[u]) {
         ok = coop_expand<false>(p, jb, je, mem, tab, nullptr, s, coop_sm[wl], kWarpMemCap);
         __syncwarp();
@@ -523,6 +527,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
       p.slot_start[idx] = pos;
       p.slot_len[idx] = s.nmem;
     }
+    insp += sinsp;
     __syncwarp();
   }
   if (lane == 0) {
@@ -545,7 +550,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
   Xoshiro rng{0, 0, 0, 0};
   bool active = false, exhausted = false;
   uint32_t idx = 0, nmem = 0, lg = kTabLog0, u = 0;
-  uint64_t insp = 0, ent = 0;
+  uint64_t insp = 0, sinsp = 0, ent = 0;
   const bool linear = p.lt_scan == kLtLinear;
 
   for (;;) {
@@ -556,6 +561,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
       lg = kTabLog0;
       mem[0] = u;
       nmem = 1;
+      sinsp = 0;
       tab_insert(tab, tag, lg, u);
       active = true;
     }
@@ -644,7 +650,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
       }
     }
     if (!active) continue;
-    insp += (pick < e ? pick + 1 : e) - b;  // reference trip count (sampling.hpp:130-136)
+    sinsp += (pick < e ? pick + 1 : e) - b;  // reference trip count (sampling.hpp:130-136)
     bool stop = pick >= e;
     uint32_t v = 0;
     if (!stop) {
@@ -652,7 +658,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
       stop = tab_contains(tab, tag, lg, v);  // chosen already visited (:137)
     }
     if (stop) {
-      emit_set(p, idx, mem, nmem);
+      if (emit_set(p, idx, mem, nmem)) insp += sinsp;
       active = false;
     } else if (nmem == kMemCap) {
       defer_slot(p, idx);
@@ -689,10 +695,11 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
   const uint64_t words = (static_cast<uint64_t>(p.n) + 31) / 32;
   uint32_t* vis = bitmaps + w * words;
   uint32_t* mem = lists + static_cast<uint64_t>(w) * p.n;
-  uint64_t insp = 0;
+  uint64_t insp = 0;  // lane 0: committed; sinsp: this set
   for (uint32_t t = w; t < nlist; t += workers) {
     const uint32_t idx = list[t];
     uint32_t nmem = 0;
+    uint64_t sinsp = 0;
     Xoshiro rng;
     rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
     const uint32_t root = static_cast<uint32_t>(rng.below(p.n));
@@ -706,7 +713,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
       for (uint32_t head = 0; head < nmem; ++head) {
         const uint32_t uu = mem[head];
         const uint32_t jb = p.off[uu], je = p.off[uu + 1];
-        insp += je - jb;
+        sinsp += je - jb;
         if (je - jb >= p.ic_coop_min && p.dupfree[uu]) {
           CoopState s{rng.a, rng.b, rng.c, rng.d, 0, 0, 0, 0, nmem};
           coop_expand<true>(p, jb, je, mem, nullptr, vis, s, coop_sm[wl]);
@@ -759,7 +766,6 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
           __syncwarp();
         }
       }
-      if (lane != 0) insp = 0;  // counted once per warp below
     } else if (lane == 0) {
       mem[0] = root;
       nmem = 1;
@@ -776,7 +782,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
               break;
             }
           }
-          insp += (pick < je ? pick + 1 : je) - jb;
+          sinsp += (pick < je ? pick + 1 : je) - jb;
           if (pick >= je) break;
           const uint32_t v = p.src[pick];
           if ((vis[v >> 5] >> (v & 31)) & 1u) break;
@@ -802,6 +808,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
       if (lane == 0) {
         p.slot_start[idx] = pos;
         p.slot_len[idx] = nmem;
+        insp += sinsp;
       }
     }
     for (uint32_t i = lane; i < nmem; i += 32) {

@@ -156,6 +156,43 @@ def test_big_set_path(cuda, oracle):
     assert (st.counter() == ref.counter).all()
 
 
+@pytest.mark.parametrize("mode", [1, 2])
+def test_giant_sets_both_schedules(cuda, oracle, mode):
+    """Supercritical IC: sets of tens of thousands of members (> the 32K warp
+    budget for some) go through the warp region and the big-set path."""
+    rng = np.random.default_rng(11)
+    n, m = 40000, 400000
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    keep = src != dst
+    w = rng.uniform(0.1, 0.45, keep.sum()).astype(np.float32)
+    arrays = P.build_graph(n, src[keep], dst[keep], w)
+    g, st, off, mem = gpu_sample(arrays, IC, 17, 300, ic_mode=mode)
+    ref = oracle.graph(*arrays).sample(IC, 17, 0, 300, workers=8)
+    assert np.diff(ref.offsets.astype(np.int64)).max() > 1024
+    assert_sets_equal(off, mem, ref)
+    assert (st.counter() == ref.counter).all()
+
+
+@pytest.mark.parametrize("name,model,mode", [("cfg1", IC, 1), ("cfg1", IC, 2), ("cfg2", LT, 0),
+                                             ("cfg4", LT, 0)])
+def test_inspected_edges_equal_reference_trip_count(cuda, port, name, model, mode):
+    """edges_inspected (the roofline numerator) counts exactly the reference's
+    loop trips (sampling.hpp:100-106, :130-136), including re-run slots."""
+    cfg = graphs.scaled(graphs.CONFIGS[name], 1 << 12, 1 << 16) if name != "cfg4" else \
+        graphs.scaled(graphs.CONFIGS[name], 40000, 600000)
+    arrays = graphs.generate(cfg)
+    for scan in ((0, 1) if model == LT else (0,)):
+        g = P.Graph(*arrays)
+        g.set_option("lt_scan", scan)
+        if model == IC:
+            g.set_option("ic_mode", mode)
+        st = P.RRRStore(g)
+        P.generate_batch(g, model, 2, 5000, st)
+        ref = port.graph(*arrays).sample(model, 2, 0, 5000, workers=4)
+        assert g.last_batch_stats().edges_inspected == ref.inspected
+
+
 def test_duplicate_edges_and_weights_edge_cases(cuda, oracle):
     """Parallel edges (kept by load_edge_list, graph.hpp:163-165), zero, one,
     subnormal and >1 weights, isolated vertices."""
