@@ -139,10 +139,28 @@ struct CoopSmem {
   unsigned long long st[4];
 };
 
-template <bool kBitmap>
+// Visited structures of coop_expand / the warp kernel:
+//   kVisLane   owner lane's 128-bit register filter + tagged table (lane mode)
+//   kVisBitmap exact n-bit map (big-set path)
+//   kVisSmem   32K-bit shared-memory filter + tagged table (warp mode: sets of
+//              thousands of members would saturate a register filter)
+constexpr int kVisLane = 0, kVisBitmap = 1, kVisSmem = 2;
+constexpr uint32_t kSmemFilterWords = 1024;  // 32K bits per warp
+__device__ __forceinline__ uint32_t sfilt_bit(uint32_t v) { return (v * 0x2545F491u) >> 17; }
+__device__ __forceinline__ bool sfilt_maybe(const uint32_t* sf, uint32_t v) {
+  const uint32_t b = sfilt_bit(v);
+  return (sf[b >> 5] >> (b & 31)) & 1u;
+}
+__device__ __forceinline__ void sfilt_add(uint32_t* sf, uint32_t v) {
+  const uint32_t b = sfilt_bit(v);
+  atomicOr(sf + (b >> 5), 1u << (b & 31));
+}
+
+template <int kVis>
 __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uint32_t* mem,
                             uint64_t* tab, uint32_t* vis, CoopState& s, CoopSmem& sm,
-                            uint32_t memcap = kMemCap) {
+                            uint32_t memcap = kMemCap, uint32_t* sfilt = nullptr) {
+  constexpr bool kBitmap = kVis == kVisBitmap;
   const int lane = threadIdx.x & 31;
   const Filter f{s.flo, s.fhi};
   uint64_t add_lo = 0, add_hi = 0;
@@ -165,7 +183,8 @@ __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uin
         bool unv = false;
         if (j < je) {
           const uint32_t v = r[q].x;
-          if (kBitmap) unv = !((vis[v >> 5] >> (v & 31)) & 1u);
+          if (kVis == kVisBitmap) unv = !((vis[v >> 5] >> (v & 31)) & 1u);
+          else if (kVis == kVisSmem) unv = !(sfilt_maybe(sfilt, v) && tab_contains(tab, s.tag, s.lg, v));
           else unv = !(f.maybe(v) && tab_contains(tab, s.tag, s.lg, v));
           sm.thr[32 * c + lane] = r[q].y;
         }
@@ -248,13 +267,17 @@ __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uin
         if ((am >> lane) & 1u) {
           const uint32_t v = __ldg(p.src + wb + 32 * c + lane);
           mem[s.nmem + __popc(am & lanemask_lt())] = v;
-          if (kBitmap) {
+          if (kVis == kVisBitmap) {
             atomicOr(vis + (v >> 5), 1u << (v & 31));
           } else {
             tab_insert_atomic(tab, s.tag, s.lg, v);
-            const uint32_t b = Filter::bit(v);
-            if (b & 64) add_hi |= 1ull << (b & 63);
-            else add_lo |= 1ull << (b & 63);
+            if (kVis == kVisSmem) {
+              sfilt_add(sfilt, v);
+            } else {
+              const uint32_t b = Filter::bit(v);
+              if (b & 64) add_hi |= 1ull << (b & 63);
+              else add_lo |= 1ull << (b & 63);
+            }
           }
         }
         s.nmem += __popc(am);
@@ -328,7 +351,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
       s.nmem = __shfl_sync(kFull, nmem, L);
       const uint32_t jb = __shfl_sync(kFull, j, L), je = __shfl_sync(kFull, jend, L);
       const uint64_t gl = gid - lane + L;
-      const bool ok = coop_expand<false>(p, jb, je, p.lists + gl * kMemCap, p.tabs + gl * kTabCap,
+      const bool ok = coop_expand<kVisLane>(p, jb, je, p.lists + gl * kMemCap, p.tabs + gl * kTabCap,
                                          nullptr, s, coop_sm[threadIdx.x >> 5]);
       if (lane == L) {
         want_coop = false;
@@ -392,8 +415,12 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
 // edge-by-edge replay when a chunk repeats a source.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kWarpMemCap = 32 * kMemCap;
+constexpr size_t kWarpKernelDynSmem =
+    (kBlock / 32) * (sizeof(CoopSmem) + kSmemFilterWords * sizeof(uint32_t));
 __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(const SampleParams p) {
-  __shared__ CoopSmem coop_sm[kBlock / 32];
+  extern __shared__ __align__(16) unsigned char k_dsm[];
+  CoopSmem* coop_sm = reinterpret_cast<CoopSmem*>(k_dsm);
+  uint32_t* filt_all = reinterpret_cast<uint32_t*>(coop_sm + kBlock / 32);
   __shared__ uint64_t s_thr[kBlock / 32][32];
   __shared__ uint32_t s_src[kBlock / 32][32];
   const int lane = threadIdx.x & 31;
@@ -401,6 +428,8 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   uint32_t* mem = p.lists + gw * 32 * kMemCap;  // the warp's 32 lane regions, contiguous
   uint64_t* tab = p.tabs + gw * 32 * kTabCap;
+  uint32_t* sf = filt_all + wl * kSmemFilterWords;  // the warp's 32K-bit filter
+  for (uint32_t t = lane; t < kSmemFilterWords; t += 32) sf[t] = 0;
   uint32_t tag = p.tags[gw * 32];
   uint64_t insp = 0;
   for (;;) {
@@ -413,14 +442,10 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
     rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
     const uint32_t root = static_cast<uint32_t>(rng.below(p.n));
     CoopState s{rng.a, rng.b, rng.c, rng.d, 0, 0, ++tag, kTabLog0, 1};
-    Filter flt;
-    flt.clear();
-    flt.add(root);
-    s.flo = flt.lo;
-    s.fhi = flt.hi;
     if (lane == 0) {
       mem[0] = root;
       tab_insert(tab, s.tag, s.lg, root);
+      sfilt_add(sf, root);
     }
     __syncwarp();
     bool ok = true;
@@ -430,7 +455,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
       const uint32_t jb = p.off[u], je = p.off[u + 1];
       sinsp += je - jb;
       if (je - jb >= p.ic_coop_min && p.dupfree[u]) {
-        ok = coop_expand<false>(p, jb, je, mem, tab, nullptr, s, coop_sm[wl], kWarpMemCap);
+        ok = coop_expand<kVisSmem>(p, jb, je, mem, tab, nullptr, s, coop_sm[wl], kWarpMemCap, sf);
         __syncwarp();
         continue;
       }
@@ -438,8 +463,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
         const uint32_t j = base + lane;
         const bool valid = j < je;
         const uint2 r = valid ? __ldg(p.rec + j) : make_uint2(0xffffffffu, 0);
-        const Filter f{s.flo, s.fhi};
-        const bool unv = valid && !(f.maybe(r.x) && tab_contains(tab, s.tag, s.lg, r.x));
+        const bool unv = valid && !(sfilt_maybe(sf, r.x) && tab_contains(tab, s.tag, s.lg, r.x));
         const unsigned peers = __match_any_sync(kFull, r.x);
         const bool dup = valid && (peers & lanemask_lt()) != 0;
         const unsigned um = __ballot_sync(kFull, unv);
@@ -460,7 +484,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
             const int nv = static_cast<int>(min(32u, je - base));
             for (int l = 0; l < nv; ++l) {
               const uint32_t v = s_src[wl][l];
-              bool seen = f.maybe(v) && tab_contains(tab, s.tag, s.lg, v);
+              bool seen = sfilt_maybe(sf, v) && tab_contains(tab, s.tag, s.lg, v);
               for (int q = 0; q < l && !seen; ++q) seen = ((acc >> q) & 1u) && s_src[wl][q] == v;
               if (seen) continue;
               if (st.u53() < s_thr[wl][l]) acc |= 1u << l;
@@ -486,26 +510,19 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
             for (uint32_t t = lane; t < s.nmem; t += 32) tab_insert_atomic(tab, s.tag, s.lg, mem[t]);
             __syncwarp();
           }
-          uint64_t add_lo = 0, add_hi = 0;
           if ((acc >> lane) & 1u) {
             mem[s.nmem + __popc(acc & lanemask_lt())] = r.x;
             tab_insert_atomic(tab, s.tag, s.lg, r.x);
-            const uint32_t b = Filter::bit(r.x);
-            if (b & 64) add_hi = 1ull << (b & 63);
-            else add_lo = 1ull << (b & 63);
+            sfilt_add(sf, r.x);
           }
-          for (int o = 16; o; o >>= 1) {
-            add_lo |= __shfl_xor_sync(kFull, add_lo, o);
-            add_hi |= __shfl_xor_sync(kFull, add_hi, o);
-          }
-          s.flo |= add_lo;
-          s.fhi |= add_hi;
           s.nmem += A;
         }
         __syncwarp();
       }
     }
     tag = s.tag;
+    for (uint32_t t = lane; t < kSmemFilterWords; t += 32) sf[t] = 0;  // filter per sample
+    __syncwarp();
     if (!ok) {
       if (lane == 0) defer_slot(p, idx);
       continue;
@@ -716,7 +733,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
         sinsp += je - jb;
         if (je - jb >= p.ic_coop_min && p.dupfree[uu]) {
           CoopState s{rng.a, rng.b, rng.c, rng.d, 0, 0, 0, 0, nmem};
-          coop_expand<true>(p, jb, je, mem, nullptr, vis, s, coop_sm[wl]);
+          coop_expand<kVisBitmap>(p, jb, je, mem, nullptr, vis, s, coop_sm[wl]);
           rng = Xoshiro{s.a, s.b, s.c, s.d};
           nmem = s.nmem;
           __syncwarp();
@@ -1018,7 +1035,15 @@ int sampler_blocks_per_sm(int model, uint32_t) {
 void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, bool ic_warp,
                     cudaStream_t s) {
   if (model == RRG_IC) {
-    if (ic_warp) k_sample_ic_warp<<<grid, kBlock, 0, s>>>(p);
+    if (ic_warp) {
+      static bool attr_set = false;  // > 48 KB of dynamic shared memory needs opting in
+      if (!attr_set) {
+        RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kWarpKernelDynSmem)));
+        attr_set = true;
+      }
+      k_sample_ic_warp<<<grid, kBlock, kWarpKernelDynSmem, s>>>(p);
+    }
     else k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
   } else {
     switch (p.lt_kary) {
