@@ -124,11 +124,14 @@ void ensure_lane_scratch(rrg_graph* g, uint64_t lanes) {
   sc.lists.release();
   sc.tabs.release();
   sc.tags.release();
+  sc.wtags.release();
   sc.lists.reserve_discard(lanes * kMemCap);
   sc.tabs.reserve_discard(lanes * kTabCap);
   sc.tags.reserve_discard(lanes);
+  sc.wtags.reserve_discard(lanes / 32 + 1);
   RRG_CUDA(cudaMemsetAsync(sc.tabs.ptr, 0, lanes * kTabCap * sizeof(uint64_t), g->stream));
   RRG_CUDA(cudaMemsetAsync(sc.tags.ptr, 0, lanes * sizeof(uint32_t), g->stream));
+  RRG_CUDA(cudaMemsetAsync(sc.wtags.ptr, 0, (lanes / 32 + 1) * sizeof(uint32_t), g->stream));
   sc.lanes = lanes;
 }
 
@@ -409,14 +412,6 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       const bool ic_warp =
           model == RRG_IC &&
           (g->ic_mode == 2 || (g->ic_mode == 0 && g->ic_mean_insp >= g->ic_warp_min_insp));
-      // Tagged tables are never cleared, which is only sound while every region
-      // keeps one owner; re-zero them when the region layout changes.
-      if (g->scratch.layout != (ic_warp ? 1 : 0)) {
-        LaneScratch& sc = g->scratch;
-        RRG_CUDA(cudaMemsetAsync(sc.tabs.ptr, 0, sc.lanes * kTabCap * sizeof(uint64_t), st));
-        RRG_CUDA(cudaMemsetAsync(sc.tags.ptr, 0, sc.lanes * sizeof(uint32_t), st));
-        sc.layout = ic_warp ? 1 : 0;
-      }
       // staging sized from the running mean set size (first batch: a guess;
       // sets that do not fit are re-run once staging has grown)
       const double per_set = s->nsets ? static_cast<double>(s->total) / s->nsets * 1.5 + 8 : 96.0;
@@ -443,6 +438,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.lists = g->scratch.lists.ptr;
       p.tabs = g->scratch.tabs.ptr;
       p.tags = g->scratch.tags.ptr;
+      p.wtags = g->scratch.wtags.ptr;
       p.stage = s->stage.ptr;
       p.stage_cap = s->stage.cap;
       p.slot_start = s->slot_start.ptr;
@@ -456,29 +452,30 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.dupfree = g->dupfree.ptr;
       p.ic_coop_min = g->ic_coop_min;
 
-      // One launch: reset the per-launch counters (keep cursor and tallies),
-      // run, read the control block back.
-      auto run = [&](bool big, const uint32_t* list, uint64_t n_items, uint32_t* restage_out) {
+      // One launch of `kind` over `list` (nullptr: the range [0, n_items)). The
+      // per-launch counters reset here; the deferral list accumulates over a pass.
+      enum Kind { kMain, kMainWarp, kBig };
+      auto launch = [&](Kind kind, const uint32_t* list, uint64_t n_items, uint32_t* restage_out) {
         ctl.next = 0;
         ctl.restage_members = 0;
-        ctl.ndeferred = 0;
         ctl.nrestage = 0;
         RRG_CUDA(cudaMemcpyAsync(g->ctl.ptr, &ctl, sizeof(SampleCtl), cudaMemcpyHostToDevice, st));
         p.restage = restage_out;
         RRG_CUDA(cudaEventRecord(g->ev0, st));
-        if (big) {
+        if (kind == kBig) {
           const uint32_t workers = static_cast<uint32_t>(std::min<uint64_t>(
               n_items, std::min<uint64_t>(kBigWorkersMax, 4ull * g->num_sms)));
           ensure_big_scratch(g, workers);
           launch_big(model, p, list, static_cast<uint32_t>(n_items), g->big.bitmaps.ptr,
                      g->big.lists.ptr, workers, st);
         } else {
+          const bool warp = kind == kMainWarp;
           p.list = list;
           p.count = n_items;
-          const uint64_t per_block = ic_warp ? block / 32 : block;  // samples per block
+          const uint64_t per_block = warp ? block / 32 : block;  // samples per block
           const uint64_t grid_need = (n_items + per_block - 1) / per_block;
           launch_sampler(model, p, static_cast<int>(std::min<uint64_t>(full_grid, grid_need)),
-                         g->ic_inner, ic_warp, st);
+                         g->ic_inner, warp, st);
         }
         RRG_CUDA(cudaEventRecord(g->ev1, st));
         d2h(&ctl, g->ctl.ptr, 1, st);
@@ -494,35 +491,35 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         p.stage = s->stage.ptr;
         p.stage_cap = s->stage.cap;
       };
-      // Big-set path over `list`; its staging refusals are re-run on it.
-      auto run_big = [&](const uint32_t* list, uint64_t n_items) {
-        uint32_t* bufs[2] = {s->deferred2.ptr, s->bigre.ptr};
+      // A pass: `kind` over `list`, then over its staging refusals (after staging
+      // has grown) until none remain. Returns the number of deferred slots, which
+      // are in `defer_out`.
+      auto pass = [&](Kind kind, const uint32_t* list, uint64_t n_items,
+                      uint32_t* defer_out) -> uint64_t {
+        ctl.ndeferred = 0;
+        p.deferred = defer_out;
+        uint32_t* rb[2] = {s->restage.ptr, s->restage2.ptr};
         for (int it = 0; n_items > 0; ++it) {
-          if (it > 64) throw std::runtime_error("big-set path did not converge");
-          run(true, list, n_items, bufs[it & 1]);
-          acc.deferred += (it == 0) ? n_items : 0;
+          if (it > 64) throw std::runtime_error("staging did not converge");
+          launch(kind, list, n_items, rb[it & 1]);
           n_items = ctl.nrestage;
-          list = bufs[it & 1];
+          list = rb[it & 1];
           if (n_items) grow_staging();
         }
+        return ctl.ndeferred;
       };
-      // main sampler over the batch, then over staging refusals until none remain
-      p.deferred = s->deferred.ptr;
-      const uint32_t* list = nullptr;
-      uint64_t n_items = c;
-      uint32_t* rbufs[2] = {s->restage.ptr, s->restage2.ptr};
-      for (int it = 0; n_items > 0; ++it) {
-        if (it > 64) throw std::runtime_error("staging did not converge");
-        uint32_t* out = rbufs[it & 1];
-        run(false, list, n_items, out);
-        const uint64_t ndef = ctl.ndeferred, nre = ctl.nrestage, rmem = ctl.restage_members;
-        if (ndef) run_big(s->deferred.ptr, ndef);  // may overwrite ctl.nrestage
-        n_items = nre;
-        list = out;
-        if (nre) {
-          ctl.restage_members = rmem;
-          grow_staging();
-        }
+      // main schedule, then the wider schedules for the sets it could not hold:
+      // lane (1K members) -> warp (32K members, IC) -> big-set path (n members)
+      uint64_t ndef = pass(ic_warp ? kMainWarp : kMain, nullptr, c, s->deferred.ptr);
+      const uint32_t* dlist = s->deferred.ptr;
+      if (ndef && model == RRG_IC && !ic_warp) {
+        acc.deferred += ndef;
+        ndef = pass(kMainWarp, dlist, ndef, s->deferred2.ptr);
+        dlist = s->deferred2.ptr;
+      }
+      if (ndef) {
+        acc.deferred += ndef;
+        pass(kBig, dlist, ndef, s->bigre.ptr);
       }
       acc.edges_inspected += ctl.inspected;
       if (model == RRG_IC) {

@@ -73,12 +73,16 @@ struct DevBuf {
 enum LtScan : int { kLtLinear = 0, kLtBsearch = 1 };
 
 // Per-lane sampler scratch: visit-order list + tagged hash table + tag.
+// Tagged tables are never cleared; that is sound because the two region
+// layouts draw tags from disjoint ranges: lane regions (IC lane mode, LT) use
+// tags in [1, 2^31) from `tags`, warp regions (IC warp mode, 32 lane regions
+// as one) use tags in [2^31, 2^32) from `wtags`. Zeroed memory matches neither.
 struct LaneScratch {
   uint64_t lanes = 0;
-  int layout = 0;  // 0: one region per lane (IC lane mode, LT); 1: one per warp (IC warp mode)
   DevBuf<uint32_t> lists;
   DevBuf<uint64_t> tabs;
   DevBuf<uint32_t> tags;
+  DevBuf<uint32_t> wtags;
 };
 
 // Big-set path scratch: one n-bit map and one n-entry list per worker warp.
@@ -174,6 +178,7 @@ struct SampleParams {
   uint32_t* lists;
   uint64_t* tabs;
   uint32_t* tags;
+  uint32_t* wtags;       // warp-region tag counters (IC warp mode)
   uint32_t* stage;
   uint64_t stage_cap;
   uint64_t* slot_start;

@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
   uint64_t* tab = p.tabs + gw * 32 * kTabCap;
   uint32_t* sf = filt_all + wl * kSmemFilterWords;  // the warp's 32K-bit filter
   for (uint32_t t = lane; t < kSmemFilterWords; t += 32) sf[t] = 0;
-  uint32_t tag = p.tags[gw * 32];
+  uint32_t tag = p.wtags[gw] | 0x80000000u;  // warp-region tags: [2^31, 2^32)
   uint64_t insp = 0;
   for (;;) {
     unsigned long long k = 0;
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
     __syncwarp();
   }
   if (lane == 0) {
-    p.tags[gw * 32] = tag;
+    p.wtags[gw] = tag;
     atomicAdd(&p.ctl->inspected, (unsigned long long)insp);
     atomicAdd(&p.ctl->entries, (unsigned long long)insp);
   }

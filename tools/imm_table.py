@@ -31,8 +31,9 @@ for name in names:
         t = time.time()
         r = P.run_imm(g, icfg)
         walls.append(time.time() - t)
+    og = orc.graph(*arrays)  # rrflow::Graph construction is not part of run_imm
     t = time.time()
-    rr = orc.graph(*arrays).imm(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model, workers=cores)
+    rr = og.imm(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model, workers=cores)
     cpu_s = time.time() - t
     print(json.dumps({
         "cfg": name, "k": cfg.k, "n": int(arrays[0].size - 1), "arcs": int(arrays[1].size),
