@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <cstring>
@@ -117,6 +119,15 @@ namespace {
 
 constexpr int kMaxBlocksPerSm = 4;
 constexpr uint32_t kBigWorkersMax = 1024;
+
+// RRGPU_DEBUG=1 prints one line per sampler launch to stderr.
+bool debug_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RRGPU_DEBUG");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
 
 void ensure_lane_scratch(rrg_graph* g, uint64_t lanes) {
   LaneScratch& sc = g->scratch;
@@ -448,6 +459,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.lt_scan = (g->lt_scan == kLtBsearch && g->cdf_monotone) ? kLtBsearch : kLtLinear;
       p.coop_min = g->coop_min;
       p.jtab = g->jtab.ptr;
+      p.jtab16 = g->jtab16.ptr;
       p.lt_kary = g->lt_kary;
       p.dupfree = g->dupfree.ptr;
       p.ic_coop_min = g->ic_coop_min;
@@ -483,6 +495,12 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         float ms = 0.0f;
         RRG_CUDA(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
         sample_ms += ms;
+        if (debug_enabled())
+          std::fprintf(stderr, "[rrgpu] launch kind=%d model=%d items=%llu ms=%.3f deferred=%u "
+                               "restage=%u cursor=%llu cap=%zu\n",
+                       static_cast<int>(kind), static_cast<int>(model),
+                       static_cast<unsigned long long>(n_items), ms, ctl.ndeferred, ctl.nrestage,
+                       static_cast<unsigned long long>(ctl.cursor), s->stage.cap);
       };
       auto grow_staging = [&]() {
         const uint64_t ncap = std::max<uint64_t>(

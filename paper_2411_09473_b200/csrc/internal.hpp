@@ -107,6 +107,7 @@ struct rrg_graph {
   rrgpu::DevBuf<uint2> rec;      // IC: {source, weight bits} per in-edge (lazy)
   rrgpu::DevBuf<double> cdf;     // LT: sequential fp64 prefix per in-list (lazy, +2 pad)
   rrgpu::DevBuf<uint64_t> jtab;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
+  rrgpu::DevBuf<uint64_t> jtab16;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint8_t> dupfree;  // IC: per-vertex strictly-increasing-sources flag
   uint32_t ic_coop_min = 256;    // IC: in-lists at least this long expand warp-cooperatively
   int ic_mode = 0;               // IC: 0 auto, 1 lane per sample, 2 warp per sample
@@ -194,6 +195,7 @@ struct SampleParams {
   int lt_kary;              // LT search arity (2, 4, 8, 16)
   // IC cooperative expansion of long in-lists
   const uint64_t* jtab;     // byte tables of T^(32 l), l = 1..31 (jump.cpp segment_tables)
+  const uint64_t* jtab16;   // byte tables of T^(16 l), l = 1..31 (warp-schedule windows)
   const uint8_t* dupfree;   // per vertex: in-list sources strictly increasing
   uint32_t ic_coop_min;     // in-lists at least this long go warp-cooperative
 };

@@ -404,31 +404,53 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
 }
 
 // ---------------------------------------------------------------------------
-// K1w: IC sampler, WARP per sample -- for heavy samples (hub-dominated graphs
-// such as cfg5, where a set inspects ~1M in-edges and there are fewer sets than
-// lanes). The warp keeps one sample's state warp-uniform (CoopState) and owns
-// the scratch of all its 32 lanes as ONE region (32K members, 64K-entry
-// table), so sets up to 32K members never leave the kernel. Long
-// duplicate-free in-lists go through coop_expand, short ones through 32-edge
-// chunks: coalesced loads, visited and thresholds in parallel, the draws for
-// the chunk's unvisited edges made in CSR order (lane 0), an exact
-// edge-by-edge replay when a chunk repeats a source.
+// K1w: IC sampler, WARP per sample. The warp keeps one sample's state
+// warp-uniform and owns the scratch of all its 32 lanes as ONE region (32K
+// members, 64K-entry table, 32K-bit shared-memory filter), so sets up to 32K
+// members never leave the kernel.
+//
+// The sample's draw sequence is the concatenation, in FIFO order, of the
+// in-lists of the queued vertices (sampling.hpp:96-106). The warp consumes it
+// in WINDOWS of up to 512 in-edges that may span many in-lists:
+//   1. window edges are loaded coalesced (32 per chunk, four chunks in flight);
+//      unvisited = not in the visited set at window start. A source that is
+//      unvisited and occurs twice in the window would change status inside
+//      it, so the window is cut right before the second occurrence (found
+//      with match_any inside a chunk and a shared-memory hash set across
+//      chunks); every edge left in the window then has its reference status;
+//   2. lane l draws stream positions [16 l, 16 l + 16) of the window's
+//      unvisited edges after a jump by T^(16 l) (byte tables, jump.cpp);
+//   3. accepted sources are appended in window order and marked visited.
+// The next window starts where this one was cut. Short in-lists of a giant
+// near-critical set (cfg3) and hub in-lists (cfg5) go through the same path.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kWarpMemCap = 32 * kMemCap;
-constexpr size_t kWarpKernelDynSmem =
-    (kBlock / 32) * (sizeof(CoopSmem) + kSmemFilterWords * sizeof(uint32_t));
+constexpr uint32_t kWin = 512;
+constexpr uint32_t kWinChunks = kWin / 32;
+constexpr uint32_t kDupSlots = 1024;
+struct WinSmem {
+  uint32_t mask[kWinChunks];
+  uint32_t pre[kWinChunks];
+  uint32_t acc[kWinChunks];
+  uint32_t thr[kWin];
+  uint32_t src[kWin];
+  uint32_t dup[kDupSlots];
+  uint32_t lstart[32];
+  uint32_t lpre[32];
+  unsigned long long st[4];
+  uint32_t filt[kSmemFilterWords];
+};
+constexpr size_t kWarpKernelDynSmem = (kBlock / 32) * sizeof(WinSmem);
+
 __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(const SampleParams p) {
   extern __shared__ __align__(16) unsigned char k_dsm[];
-  CoopSmem* coop_sm = reinterpret_cast<CoopSmem*>(k_dsm);
-  uint32_t* filt_all = reinterpret_cast<uint32_t*>(coop_sm + kBlock / 32);
-  __shared__ uint64_t s_thr[kBlock / 32][32];
-  __shared__ uint32_t s_src[kBlock / 32][32];
   const int lane = threadIdx.x & 31;
   const int wl = threadIdx.x >> 5;
+  WinSmem& ws = reinterpret_cast<WinSmem*>(k_dsm)[wl];
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   uint32_t* mem = p.lists + gw * 32 * kMemCap;  // the warp's 32 lane regions, contiguous
   uint64_t* tab = p.tabs + gw * 32 * kTabCap;
-  uint32_t* sf = filt_all + wl * kSmemFilterWords;  // the warp's 32K-bit filter
+  uint32_t* sf = ws.filt;
   for (uint32_t t = lane; t < kSmemFilterWords; t += 32) sf[t] = 0;
   uint32_t tag = p.wtags[gw] | 0x80000000u;  // warp-region tags: [2^31, 2^32)
   uint64_t insp = 0;
@@ -449,76 +471,196 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
     }
     __syncwarp();
     bool ok = true;
-    uint64_t sinsp = 0;
-    for (uint32_t head = 0; head < s.nmem && ok; ++head) {
-      const uint32_t u = mem[head];
-      const uint32_t jb = p.off[u], je = p.off[u + 1];
-      sinsp += je - jb;
-      if (je - jb >= p.ic_coop_min && p.dupfree[u]) {
-        ok = coop_expand<kVisSmem>(p, jb, je, mem, tab, nullptr, s, coop_sm[wl], kWarpMemCap, sf);
-        __syncwarp();
-        continue;
+    uint32_t qi = 0;             // queue position of the in-list being consumed
+    uint32_t qj = p.off[root];   // its next in-edge
+    while (qi < s.nmem && ok) {
+      // ---- window: up to 32 queued in-lists from (qi, qj), at most kWin edges
+      const uint32_t nq = s.nmem;
+      const bool lvalid = qi + lane < nq;
+      uint32_t lb = 0, le = 0;
+      if (lvalid) {
+        const uint32_t v = mem[qi + lane];
+        lb = lane == 0 ? qj : p.off[v];
+        le = p.off[v + 1];
       }
-      for (uint32_t base = jb; base < je && ok; base += 32) {
-        const uint32_t j = base + lane;
-        const bool valid = j < je;
-        const uint2 r = valid ? __ldg(p.rec + j) : make_uint2(0xffffffffu, 0);
-        const bool unv = valid && !(sfilt_maybe(sf, r.x) && tab_contains(tab, s.tag, s.lg, r.x));
-        const unsigned peers = __match_any_sync(kFull, r.x);
-        const bool dup = valid && (peers & lanemask_lt()) != 0;
-        const unsigned um = __ballot_sync(kFull, unv);
-        const bool any_dup = __any_sync(kFull, dup);
-        if (!um) continue;  // every source already visited: no draws
-        s_thr[wl][lane] = bernoulli_threshold(r.y);
-        s_src[wl][lane] = r.x;
-        __syncwarp();
-        Xoshiro st{s.a, s.b, s.c, s.d};
-        unsigned acc = 0;
-        if (lane == 0) {
-          if (!any_dup) {
-            for (unsigned mm = um; mm; mm &= mm - 1) {
-              const int l = __ffs(mm) - 1;
-              if (st.u53() < s_thr[wl][l]) acc |= 1u << l;
-            }
-          } else {  // repeated sources: edge by edge against the live set
-            const int nv = static_cast<int>(min(32u, je - base));
-            for (int l = 0; l < nv; ++l) {
-              const uint32_t v = s_src[wl][l];
-              bool seen = sfilt_maybe(sf, v) && tab_contains(tab, s.tag, s.lg, v);
-              for (int q = 0; q < l && !seen; ++q) seen = ((acc >> q) & 1u) && s_src[wl][q] == v;
-              if (seen) continue;
-              if (st.u53() < s_thr[wl][l]) acc |= 1u << l;
-            }
+      const uint32_t len = le - lb;
+      uint32_t incl = len;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t total = __shfl_sync(kFull, incl, 31);
+      ws.lstart[lane] = lb;
+      ws.lpre[lane] = incl - len;
+      for (uint32_t t = lane; t < kDupSlots; t += 32) ws.dup[t] = 0xffffffffu;
+      __syncwarp();
+      uint32_t ecur = min(kWin, total);
+      // ---- 1. unvisited masks; cut before the first repeated unvisited source
+      uint32_t mymask = 0;
+      bool cut = false;
+      for (uint32_t c0 = 0; 32 * c0 < ecur && !cut; c0 += 4) {
+        uint2 r[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t e = 32 * (c0 + q4) + lane;
+          r[q4] = make_uint2(0xffffffffu, 0u);
+          if (e < ecur) {
+            uint32_t t = 0;  // in-list holding window position e: last t with lpre[t] <= e
+            for (uint32_t step = 16; step; step >>= 1)
+              if (t + step < 32 && ws.lpre[t + step] <= e) t += step;
+            r[q4] = __ldg(p.rec + ws.lstart[t] + (e - ws.lpre[t]));
           }
         }
-        acc = __shfl_sync(kFull, acc, 0);
-        s.a = __shfl_sync(kFull, st.a, 0);
-        s.b = __shfl_sync(kFull, st.b, 0);
-        s.c = __shfl_sync(kFull, st.c, 0);
-        s.d = __shfl_sync(kFull, st.d, 0);
-        const uint32_t A = __popc(acc);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t c = c0 + q4;
+          if (32 * c >= ecur || cut) break;
+          const uint32_t e = 32 * c + lane;
+          const uint32_t v = r[q4].x;
+          bool unv = e < ecur && !(sfilt_maybe(sf, v) && tab_contains(tab, s.tag, s.lg, v));
+          const unsigned um = __ballot_sync(kFull, unv);
+          const unsigned peers = __match_any_sync(kFull, v);
+          bool dup = unv && (peers & um & lanemask_lt()) != 0;
+          if (unv && !dup) {  // first in this chunk: probe / insert the window's set
+            uint32_t h = vhash(v) >> 22;
+            while (true) {
+              const uint32_t cur = ws.dup[h];
+              if (cur == v) {
+                dup = true;
+                break;
+              }
+              if (cur == 0xffffffffu) {
+                const uint32_t prev = atomicCAS(&ws.dup[h], 0xffffffffu, v);
+                if (prev == 0xffffffffu) break;
+                if (prev == v) {
+                  dup = true;
+                  break;
+                }
+                continue;
+              }
+              h = (h + 1) & (kDupSlots - 1);
+            }
+          }
+          const unsigned dm = __ballot_sync(kFull, dup);
+          if (dm) {
+            ecur = 32 * c + (__ffs(dm) - 1);
+            cut = true;
+          }
+          unv = unv && e < ecur;
+          if (unv) {
+            ws.thr[e] = r[q4].y;
+            ws.src[e] = v;
+          }
+          const unsigned m = __ballot_sync(kFull, unv);
+          if (lane == static_cast<int>(c)) mymask = m;
+        }
+      }
+      const uint32_t nch = (ecur + 31) >> 5;
+      const uint32_t cnt = __popc(mymask);
+      uint32_t ui = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, ui, o);
+        if (lane >= o) ui += y;
+      }
+      const uint32_t U = __shfl_sync(kFull, ui, 31);
+      if (lane < static_cast<int>(kWinChunks)) {
+        ws.mask[lane] = mymask;
+        ws.pre[lane] = ui - cnt;
+        ws.acc[lane] = 0;
+      }
+      __syncwarp();
+      if (U) {
+        // ---- 2. lane l draws positions [16 l, 16 l + 16) of the window
+        const uint32_t r0 = 16u * lane;
+        if (r0 < U) {
+          Xoshiro st{s.a, s.b, s.c, s.d};
+          if (lane)
+            gf2_jump_tables(p.jtab16 + static_cast<size_t>(lane - 1) * (32 * 256 * 4), st.a, st.b,
+                            st.c, st.d);
+          uint32_t c = 0;
+          for (uint32_t step = 8; step; step >>= 1)
+            if (c + step < nch && ws.pre[c + step] <= r0) c += step;
+          uint32_t m = ws.mask[c];
+          for (uint32_t k2 = r0 - ws.pre[c]; k2; --k2) m &= m - 1;
+          const uint32_t need = min(16u, U - r0);
+          uint32_t acc = 0;
+          for (uint32_t done = 0; done < need;) {
+            if (!m) {
+              if (acc) atomicOr(&ws.acc[c], acc);
+              acc = 0;
+              m = ws.mask[++c];
+              continue;
+            }
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            if (st.u53() < bernoulli_threshold(ws.thr[32 * c + bit])) acc |= 1u << bit;
+            ++done;
+          }
+          if (acc) atomicOr(&ws.acc[c], acc);
+          if (r0 + need == U) {
+            ws.st[0] = st.a;
+            ws.st[1] = st.b;
+            ws.st[2] = st.c;
+            ws.st[3] = st.d;
+          }
+        }
+        __syncwarp();
+        s.a = ws.st[0];
+        s.b = ws.st[1];
+        s.c = ws.st[2];
+        s.d = ws.st[3];
+        // ---- 3. append the accepted sources in window order
+        const uint32_t am_lane = lane < static_cast<int>(nch) ? ws.acc[lane] : 0u;
+        uint32_t A = __popc(am_lane);
+        for (int o = 16; o; o >>= 1) A += __shfl_xor_sync(kFull, A, o);
         if (A) {
           if (s.nmem + A > kWarpMemCap) {
             ok = false;
-            break;
+          } else {
+            uint32_t lg2 = s.lg;
+            while (2 * (s.nmem + A) > (1u << lg2)) ++lg2;
+            if (lg2 != s.lg) {  // grow: re-insert the members under a fresh tag
+              s.lg = lg2;
+              ++s.tag;
+              for (uint32_t t = lane; t < s.nmem; t += 32) tab_insert_atomic(tab, s.tag, s.lg, mem[t]);
+              __syncwarp();
+            }
+            unsigned cmk = __ballot_sync(kFull, am_lane != 0);
+            while (cmk) {
+              const int c = __ffs(cmk) - 1;
+              cmk &= cmk - 1;
+              const uint32_t am = __shfl_sync(kFull, am_lane, c);
+              if ((am >> lane) & 1u) {
+                const uint32_t v = ws.src[32 * c + lane];
+                mem[s.nmem + __popc(am & lanemask_lt())] = v;
+                tab_insert_atomic(tab, s.tag, s.lg, v);
+                sfilt_add(sf, v);
+              }
+              s.nmem += __popc(am);
+            }
           }
-          uint32_t lg2 = s.lg;
-          while (2 * (s.nmem + A) > (1u << lg2)) ++lg2;
-          if (lg2 != s.lg) {
-            s.lg = lg2;
-            ++s.tag;
-            for (uint32_t t = lane; t < s.nmem; t += 32) tab_insert_atomic(tab, s.tag, s.lg, mem[t]);
-            __syncwarp();
-          }
-          if ((acc >> lane) & 1u) {
-            mem[s.nmem + __popc(acc & lanemask_lt())] = r.x;
-            tab_insert_atomic(tab, s.tag, s.lg, r.x);
-            sfilt_add(sf, r.x);
-          }
-          s.nmem += A;
         }
-        __syncwarp();
       }
+      // ---- advance past the ecur consumed edges
+      const unsigned partial = __ballot_sync(kFull, lvalid && incl > ecur);
+      if (partial) {
+        const int t = __ffs(partial) - 1;
+        qi += t;
+        qj = ws.lstart[t] + (ecur - ws.lpre[t]);
+      } else {
+        qi += min(32u, nq - qi);
+        if (qi < s.nmem) qj = p.off[mem[qi]];
+      }
+      __syncwarp();
+    }
+    // inspected in-edges of the set = sum of its members' in-degrees
+    uint64_t sinsp = 0;
+    if (ok) {
+      for (uint32_t t = lane; t < s.nmem; t += 32) {
+        const uint32_t v = mem[t];
+        sinsp += p.off[v + 1] - p.off[v];
+      }
+      for (int o = 16; o; o >>= 1) sinsp += __shfl_xor_sync(kFull, sinsp, o);
     }
     tag = s.tag;
     for (uint32_t t = lane; t < kSmemFilterWords; t += 32) sf[t] = 0;  // filter per sample
@@ -1081,8 +1223,12 @@ void prepare_ic(rrg_graph* g) {
     count_launch();
   }
   static const std::vector<uint64_t> jt = segment_tables(32, 31);  // host, built once
+  static const std::vector<uint64_t> jt16 = segment_tables(16, 31);
   g->jtab.reserve_discard(jt.size());
+  g->jtab16.reserve_discard(jt16.size());
   RRG_CUDA(cudaMemcpyAsync(g->jtab.ptr, jt.data(), jt.size() * 8, cudaMemcpyHostToDevice,
+                           g->stream));
+  RRG_CUDA(cudaMemcpyAsync(g->jtab16.ptr, jt16.data(), jt16.size() * 8, cudaMemcpyHostToDevice,
                            g->stream));
   RRG_CUDA(cudaStreamSynchronize(g->stream));
   g->rec_ready = true;
