@@ -450,6 +450,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.tabs = g->scratch.tabs.ptr;
       p.tags = g->scratch.tags.ptr;
       p.wtags = g->scratch.wtags.ptr;
+      p.lanes = g->scratch.lanes;
       p.stage = s->stage.ptr;
       p.stage_cap = s->stage.cap;
       p.slot_start = s->slot_start.ptr;
@@ -466,7 +467,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
 
       // One launch of `kind` over `list` (nullptr: the range [0, n_items)). The
       // per-launch counters reset here; the deferral list accumulates over a pass.
-      enum Kind { kMain, kMainWarp, kBig };
+      enum Kind { kMain, kMainWarp, kWarpWide, kBig };
       auto launch = [&](Kind kind, const uint32_t* list, uint64_t n_items, uint32_t* restage_out) {
         ctl.next = 0;
         ctl.restage_members = 0;
@@ -481,13 +482,17 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
           launch_big(model, p, list, static_cast<uint32_t>(n_items), g->big.bitmaps.ptr,
                      g->big.lists.ptr, workers, st);
         } else {
-          const bool warp = kind == kMainWarp;
+          const int sched = kind == kMainWarp ? kSchedWarp
+                            : kind == kWarpWide ? kSchedWarpWide : kSchedLane;
           p.list = list;
           p.count = n_items;
-          const uint64_t per_block = warp ? block / 32 : block;  // samples per block
+          const uint64_t per_block = sched == kSchedLane ? block : block / 32;  // samples/block
+          uint64_t grid_cap = full_grid;
+          if (sched == kSchedWarpWide) grid_cap = g->scratch.lanes / 256 / (block / 32);
           const uint64_t grid_need = (n_items + per_block - 1) / per_block;
-          launch_sampler(model, p, static_cast<int>(std::min<uint64_t>(full_grid, grid_need)),
-                         g->ic_inner, warp, st);
+          launch_sampler(model, p,
+                         static_cast<int>(std::max<uint64_t>(1, std::min(grid_cap, grid_need))),
+                         g->ic_inner, sched, st);
         }
         RRG_CUDA(cudaEventRecord(g->ev1, st));
         d2h(&ctl, g->ctl.ptr, 1, st);
@@ -529,11 +534,19 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       // main schedule, then the wider schedules for the sets it could not hold:
       // lane (1K members) -> warp (32K members, IC) -> big-set path (n members)
       uint64_t ndef = pass(ic_warp ? kMainWarp : kMain, nullptr, c, s->deferred.ptr);
-      const uint32_t* dlist = s->deferred.ptr;
-      if (ndef && model == RRG_IC && !ic_warp) {
-        acc.deferred += ndef;
-        ndef = pass(kMainWarp, dlist, ndef, s->deferred2.ptr);
-        dlist = s->deferred2.ptr;
+      uint32_t* dlist = s->deferred.ptr;
+      uint32_t* dspare = s->deferred2.ptr;
+      if (model == RRG_IC) {
+        if (ndef && !ic_warp) {
+          acc.deferred += ndef;
+          ndef = pass(kMainWarp, dlist, ndef, dspare);
+          std::swap(dlist, dspare);
+        }
+        if (ndef) {
+          acc.deferred += ndef;
+          ndef = pass(kWarpWide, dlist, ndef, dspare);
+          std::swap(dlist, dspare);
+        }
       }
       if (ndef) {
         acc.deferred += ndef;

@@ -73,10 +73,10 @@ struct DevBuf {
 enum LtScan : int { kLtLinear = 0, kLtBsearch = 1 };
 
 // Per-lane sampler scratch: visit-order list + tagged hash table + tag.
-// Tagged tables are never cleared; that is sound because the two region
-// layouts draw tags from disjoint ranges: lane regions (IC lane mode, LT) use
-// tags in [1, 2^31) from `tags`, warp regions (IC warp mode, 32 lane regions
-// as one) use tags in [2^31, 2^32) from `wtags`. Zeroed memory matches neither.
+// Tagged tables are never cleared; that is sound because the region layouts
+// draw tags from disjoint ranges: lane regions (IC lane mode, LT) use tags in
+// [1, 2^31) from `tags`; warp regions of 32 lanes use [2^31, 3*2^30) and of 256
+// lanes [3*2^30, 2^32), both counted in `wtags`. Zeroed memory matches none.
 struct LaneScratch {
   uint64_t lanes = 0;
   DevBuf<uint32_t> lists;
@@ -180,6 +180,7 @@ struct SampleParams {
   uint64_t* tabs;
   uint32_t* tags;
   uint32_t* wtags;       // warp-region tag counters (IC warp mode)
+  uint64_t lanes;        // lane scratch regions allocated
   uint32_t* stage;
   uint64_t stage_cap;
   uint64_t* slot_start;
@@ -207,7 +208,10 @@ void prepare_lt(rrg_graph* g);
 uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64);
 int sampler_block();
 int sampler_blocks_per_sm(int model, uint32_t ic_inner);
-void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, bool ic_warp,
+// IC schedules: lane per sample; warp per sample over its 32 lanes' scratch
+// (sets up to 32K members); warp per sample over 256 lanes' scratch (256K).
+enum Schedule : int { kSchedLane = 0, kSchedWarp = 1, kSchedWarpWide = 2 };
+void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, int schedule,
                     cudaStream_t s);
 void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t nlist,
                 uint32_t* bitmaps, uint32_t* lists, uint32_t workers, cudaStream_t s);

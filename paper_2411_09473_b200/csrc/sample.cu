@@ -428,7 +428,7 @@ constexpr uint32_t kWarpMemCap = 32 * kMemCap;
 constexpr uint32_t kWin = 512;
 constexpr uint32_t kWinChunks = kWin / 32;
 constexpr uint32_t kDupSlots = 1024;
-struct WinSmem {
+struct WinFields {
   uint32_t mask[kWinChunks];
   uint32_t pre[kWinChunks];
   uint32_t acc[kWinChunks];
@@ -438,21 +438,38 @@ struct WinSmem {
   uint32_t lstart[32];
   uint32_t lpre[32];
   unsigned long long st[4];
+};
+struct WinSmem {
+  union {
+    WinFields win;   // multi-list windows
+    CoopSmem coop;   // one long duplicate-free in-list (coop_expand)
+  } u;
   uint32_t filt[kSmemFilterWords];
 };
 constexpr size_t kWarpKernelDynSmem = (kBlock / 32) * sizeof(WinSmem);
 
+// kRegionLanes: how many lane scratch regions one warp owns as ONE region --
+// 32 (its own lanes: 32K members) or 256 (eight warps' lanes: 256K members,
+// used for the few sets a 32-lane region could not hold). Each size draws its
+// table tags from its own quarter of the tag space (see LaneScratch).
+template <int kRegionLanes>
 __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(const SampleParams p) {
+  constexpr uint32_t kRegionMemCap = kRegionLanes * kMemCap;
+  constexpr uint32_t kTagBase = kRegionLanes == 32 ? 0x80000000u : 0xC0000000u;
   extern __shared__ __align__(16) unsigned char k_dsm[];
   const int lane = threadIdx.x & 31;
   const int wl = threadIdx.x >> 5;
-  WinSmem& ws = reinterpret_cast<WinSmem*>(k_dsm)[wl];
+  WinSmem& wsm = reinterpret_cast<WinSmem*>(k_dsm)[wl];
+  WinFields& ws = wsm.u.win;
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  uint32_t* mem = p.lists + gw * 32 * kMemCap;  // the warp's 32 lane regions, contiguous
-  uint64_t* tab = p.tabs + gw * 32 * kTabCap;
-  uint32_t* sf = ws.filt;
+  const uint64_t region = gw * kRegionLanes;  // first lane region owned by this warp
+  if (region + kRegionLanes > p.lanes) return;
+  uint32_t* mem = p.lists + region * kMemCap;  // kRegionLanes lane regions, contiguous
+  uint64_t* tab = p.tabs + region * kTabCap;
+  uint32_t* sf = wsm.filt;
   for (uint32_t t = lane; t < kSmemFilterWords; t += 32) sf[t] = 0;
-  uint32_t tag = p.wtags[gw] | 0x80000000u;  // warp-region tags: [2^31, 2^32)
+  const uint64_t tslot = region / 32;  // tag counter of this region (unique per size)
+  uint32_t tag = kTagBase | (p.wtags[tslot] & 0x3fffffffu);
   uint64_t insp = 0;
   for (;;) {
     unsigned long long k = 0;
@@ -474,6 +491,18 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
     uint32_t qi = 0;             // queue position of the in-list being consumed
     uint32_t qj = p.off[root];   // its next in-edge
     while (qi < s.nmem && ok) {
+      {  // a long duplicate-free in-list at the head: 1024-edge windows of one list
+        const uint32_t u = mem[qi];
+        const uint32_t je = p.off[u + 1];
+        if (je - qj >= p.ic_coop_min && p.dupfree[u]) {
+          ok = coop_expand<kVisSmem>(p, qj, je, mem, tab, nullptr, s, wsm.u.coop, kRegionMemCap,
+                                     sf);
+          ++qi;
+          if (qi < s.nmem) qj = p.off[mem[qi]];
+          __syncwarp();
+          continue;
+        }
+      }
       // ---- window: up to 32 queued in-lists from (qi, qj), at most kWin edges
       const uint32_t nq = s.nmem;
       const bool lvalid = qi + lane < nq;
@@ -614,7 +643,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
         uint32_t A = __popc(am_lane);
         for (int o = 16; o; o >>= 1) A += __shfl_xor_sync(kFull, A, o);
         if (A) {
-          if (s.nmem + A > kWarpMemCap) {
+          if (s.nmem + A > kRegionMemCap) {
             ok = false;
           } else {
             uint32_t lg2 = s.lg;
@@ -690,7 +719,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
     __syncwarp();
   }
   if (lane == 0) {
-    p.wtags[gw] = tag;
+    p.wtags[tslot] = tag;
     atomicAdd(&p.ctl->inspected, (unsigned long long)insp);
     atomicAdd(&p.ctl->entries, (unsigned long long)insp);
   }
@@ -1174,19 +1203,25 @@ int sampler_blocks_per_sm(int model, uint32_t) {
   return b < 1 ? 1 : b;
 }
 
-void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, bool ic_warp,
+void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, int schedule,
                     cudaStream_t s) {
   if (model == RRG_IC) {
-    if (ic_warp) {
+    if (schedule != kSchedLane) {
       static bool attr_set = false;  // > 48 KB of dynamic shared memory needs opting in
       if (!attr_set) {
-        RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_warp<32>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kWarpKernelDynSmem)));
+        RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_warp<256>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kWarpKernelDynSmem)));
         attr_set = true;
       }
-      k_sample_ic_warp<<<grid, kBlock, kWarpKernelDynSmem, s>>>(p);
+      if (schedule == kSchedWarp) k_sample_ic_warp<32><<<grid, kBlock, kWarpKernelDynSmem, s>>>(p);
+      else k_sample_ic_warp<256><<<grid, kBlock, kWarpKernelDynSmem, s>>>(p);
+    } else {
+      k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
     }
-    else k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
   } else {
     switch (p.lt_kary) {
       case 2: k_sample_lt<2><<<grid, kBlock, 0, s>>>(p); break;
