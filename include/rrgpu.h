@@ -165,6 +165,12 @@ rrg_status rrg_store_export(const rrg_store* s, uint64_t first, uint64_t count, 
 /* Appends literal sets (e.g. the oracle's), updating the fused counter. */
 rrg_status rrg_store_import(rrg_store* s, uint64_t count, const uint64_t* offsets,
                             const uint32_t* members);
+/* Appends sets [first, first+count) of `src` to `dst` (device to device, same graph),
+ * adding them to dst's fused counter. Slot j's set depends only on (run_seed, j), so
+ * sets sampled ahead of need into a side store are exactly the sets a later top-up of
+ * dst would draw for those slots (the IMM driver's speculative top-ups use this). */
+rrg_status rrg_store_append_from(rrg_store* dst, const rrg_store* src, uint64_t first,
+                                 uint64_t count);
 /* Fused occurrence counter as u64[n] (Counter::get, counter.hpp:29). */
 rrg_status rrg_store_counter(const rrg_store* s, uint64_t* counts);
 

@@ -221,6 +221,10 @@ class RRRStore:
         check(lib.rrg_store_import(self._h, offsets.size - 1, ptr(offsets, C.c_uint64),
                                    ptr(members, C.c_uint32)))
 
+    def append_from(self, src: "RRRStore", first: int, count: int) -> None:
+        """Appends src's sets [first, first+count) (device to device)."""
+        check(lib.rrg_store_append_from(self._h, src.handle, int(first), int(count)))
+
     def counter(self) -> np.ndarray:
         out = np.zeros(self.graph.num_vertices, dtype=np.uint64)
         check(lib.rrg_store_counter(self._h, ptr(out, C.c_uint64)))

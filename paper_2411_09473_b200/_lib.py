@@ -104,6 +104,7 @@ SIGNATURES = [
     ("rrg_run_imm", C.c_int, [vp, C.POINTER(ImmConfigC), u32p, u64p, C.POINTER(ImmResultC)]),
     ("rrg_store_export", C.c_int, [vp, C.c_uint64, C.c_uint64, u64p, u32p]),
     ("rrg_store_import", C.c_int, [vp, C.c_uint64, u64p, u32p]),
+    ("rrg_store_append_from", C.c_int, [vp, vp, C.c_uint64, C.c_uint64]),
     ("rrg_store_counter", C.c_int, [vp, u64p]),
     ("rrg_build_transpose", C.c_int,
      [C.c_uint32, C.c_uint64, u32p, u32p, f32p, u64p, u32p, f32p]),

@@ -502,10 +502,11 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         sample_ms += ms;
         if (debug_enabled())
           std::fprintf(stderr, "[rrgpu] launch kind=%d model=%d items=%llu ms=%.3f deferred=%u "
-                               "restage=%u cursor=%llu cap=%zu\n",
+                               "restage=%u cursor=%llu cap=%zu windows=%llu cuts=%llu\n",
                        static_cast<int>(kind), static_cast<int>(model),
                        static_cast<unsigned long long>(n_items), ms, ctl.ndeferred, ctl.nrestage,
-                       static_cast<unsigned long long>(ctl.cursor), s->stage.cap);
+                       static_cast<unsigned long long>(ctl.cursor), s->stage.cap, ctl.windows,
+                       ctl.cuts);
       };
       auto grow_staging = [&]() {
         const uint64_t ncap = std::max<uint64_t>(
@@ -704,6 +705,44 @@ rrg_status rrg_store_export(const rrg_store* s, uint64_t first, uint64_t count, 
       d2h(members, s->mem.ptr + base, off[count] - base, g->stream);
       sync(g);
     }
+    return RRG_OK;
+  });
+}
+
+rrg_status rrg_store_append_from(rrg_store* dst, const rrg_store* src, uint64_t first,
+                                 uint64_t count) {
+  if (!dst || !src) return invalid("null store");
+  if (dst->g != src->g) return invalid("append_from: stores of different graphs");
+  if (dst == src) return invalid("append_from: source and destination are the same store");
+  if (first + count > src->nsets) return invalid("append_from: range out of bounds");
+  if (count == 0) return RRG_OK;
+  return guarded([&]() -> rrg_status {
+    rrg_graph* g = dst->g;
+    const cudaStream_t st = g->stream;
+    uint64_t ends[2] = {0, 0};
+    d2h(ends, src->off.ptr + first, 1, st);
+    d2h(ends + 1, src->off.ptr + first + count, 1, st);
+    sync(g);
+    const uint64_t added = ends[1] - ends[0];
+    if (dst->total + added > dst->mem.cap)
+      dst->mem.reserve_keep(std::max<uint64_t>(dst->total + added, dst->mem.cap + dst->mem.cap / 2),
+                            dst->total, st);
+    if (dst->nsets + count + 1 > dst->off.cap)
+      dst->off.reserve_keep(
+          std::max<uint64_t>(dst->nsets + count + 1, dst->off.cap + dst->off.cap / 2),
+          dst->nsets + 1, st);
+    if (added)
+      RRG_CUDA(cudaMemcpyAsync(dst->mem.ptr + dst->total, src->mem.ptr + ends[0], added * 4,
+                               cudaMemcpyDeviceToDevice, st));
+    launch_rebase(src->off.ptr + first, count, dst->total, dst->off.ptr + dst->nsets,
+                  dst->maxlen_dev.ptr, st);
+    launch_recount(dst->off.ptr + dst->nsets, dst->mem.ptr, count, dst->counter.ptr, st);
+    uint32_t mx = 0;
+    d2h(&mx, dst->maxlen_dev.ptr, 1, st);
+    sync(g);
+    dst->nsets += count;
+    dst->total += added;
+    dst->max_len = mx;
     return RRG_OK;
   });
 }

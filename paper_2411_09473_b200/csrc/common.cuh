@@ -229,6 +229,8 @@ struct SampleCtl {
   unsigned long long inspected;   // reference-equivalent in-edges inspected
   unsigned long long entries;     // adjacency entries actually read by the kernel
   unsigned long long restage_members;  // members of sets refused for lack of staging
+  unsigned long long windows;     // IC warp schedule: windows processed (diagnostics)
+  unsigned long long cuts;        // IC warp schedule: windows cut at a repeated source
   unsigned int ndeferred;         // slots handed to the big-set path (set > kMemCap)
   unsigned int nrestage;          // slots to re-run once staging has grown
 };

@@ -142,16 +142,52 @@ rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
   rrg_status st = rrg_store_create(g, &store.s);
   if (st != RRG_OK) return st;
 
+  // Top-ups. Slot j's set depends only on (rng_seed, j) (sampling.hpp:179), so
+  // sets for slots a later round may need can be sampled ahead into a side
+  // store and committed only when (and if) a top-up reaches them: the main
+  // store ends up with exactly the reference's sets. Small batches are bound by
+  // the latency of their largest set, so one batch covering the next rounds
+  // costs about what one round's batch does.
+  StoreGuard ahead_store;
+  uint64_t ahead_first = 0, ahead_count = 0;
   uint64_t size = 0;
-  auto top_up = [&](uint64_t target) -> rrg_status {
+  auto top_up = [&](uint64_t target, uint64_t ahead) -> rrg_status {
     if (target <= size) return RRG_OK;
     const auto t = std::chrono::steady_clock::now();
-    uint64_t made = 0;
-    const rrg_status s = rrg_generate_batch(g, model, cfg->rng_seed, target - size, store.s,
-                                            /*fused=*/1, 64, &made);
-    size += made;
+    rrg_status s = RRG_OK;
+    const bool covered = ahead_count && ahead_first <= size && target <= ahead_first + ahead_count;
+    if (!covered) {
+      if (!ahead_store.s) {
+        s = rrg_store_create(g, &ahead_store.s);
+        if (s != RRG_OK) return s;
+      } else {
+        rrg_store_clear(ahead_store.s);
+      }
+      const uint64_t want = std::max(target, ahead) - size;
+      uint64_t made = 0;
+      s = rrg_generate_slots(g, model, cfg->rng_seed, size, want, ahead_store.s, /*fused=*/0, 64,
+                             &made);
+      ahead_first = size;
+      ahead_count = made;
+      if (s != RRG_OK) {
+        out->t_generate += seconds_since(t);
+        return s;
+      }
+    }
+    s = rrg_store_append_from(store.s, ahead_store.s, size - ahead_first, target - size);
+    if (s == RRG_OK) size = target;
     out->t_generate += seconds_since(t);
     return s;
+  };
+  // how far ahead to sample: the next rounds' budgets while the batch stays small
+  constexpr uint64_t kAheadMax = 1ull << 16;
+  auto ahead_for = [&](unsigned i, unsigned rounds_total) -> uint64_t {
+    uint64_t best = 0;
+    for (unsigned j = i + 1; j <= std::min(rounds_total, i + 2); ++j) {
+      const uint64_t tj = theta_for_round(n, cfg->k, cfg->epsilon, ell, j);
+      if (tj > size && tj - size <= kAheadMax) best = std::max(best, tj);
+    }
+    return best;
   };
   std::vector<uint32_t> trial_seeds(cfg->k);
   std::vector<uint64_t> trial_marg(cfg->k);
@@ -169,7 +205,7 @@ rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
   double estimated_spread = 0.0;
   bool triggered = false;
   for (unsigned i = 1; i <= rounds; ++i) {
-    st = top_up(theta_for_round(n, cfg->k, cfg->epsilon, ell, i));
+    st = top_up(theta_for_round(n, cfg->k, cfg->epsilon, ell, i), ahead_for(i, rounds));
     if (st != RRG_OK) return st;
     uint64_t covered = 0;
     st = select(trial_seeds.data(), trial_marg.data(), &covered);
@@ -188,7 +224,7 @@ rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
   out->theta = set_theta(n, cfg->k, cfg->epsilon, ell, out->lower_bound);
 
   // final top-up and selection (imm.hpp:227-241)
-  st = top_up(out->theta);
+  st = top_up(out->theta, 0);
   if (st != RRG_OK) return st;
   st = select(seeds, marginals, nullptr);
   if (st != RRG_OK) return st;

@@ -235,6 +235,8 @@ void launch_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
 void launch_fraction(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
                      const uint8_t* in_seed_set, unsigned long long* hits, cudaStream_t s);
 void launch_widen(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t s);
+void launch_rebase(const uint64_t* in, uint64_t count, uint64_t base, uint64_t* out,
+                   uint32_t* maxlen, cudaStream_t s);
 
 // ---- select.cu --------------------------------------------------------------
 struct SelectParams {

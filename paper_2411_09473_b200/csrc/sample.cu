@@ -584,6 +584,10 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
           if (lane == static_cast<int>(c)) mymask = m;
         }
       }
+      if (lane == 0) {
+        atomicAdd(&p.ctl->windows, 1ull);
+        if (cut) atomicAdd(&p.ctl->cuts, 1ull);
+      }
       const uint32_t nch = (ecur + 31) >> 5;
       const uint32_t cnt = __popc(mymask);
       uint32_t ui = cnt;

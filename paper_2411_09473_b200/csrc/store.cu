@@ -4,6 +4,8 @@
 // Replaces RRRStore::place / finalize (rrr_store.hpp:41-60), build_counter
 // (selection.hpp:79-95) and the membership probes of decrement_update
 // (selection.hpp:137-149), which become a vertex -> set-id index.
+#include <algorithm>
+
 #include "internal.hpp"
 
 namespace rrgpu {
@@ -184,6 +186,21 @@ __global__ void k_fraction(const uint64_t* off, const uint32_t* mem, uint64_t ns
   if (lane == 0 && local) atomicAdd(hits, local);
 }
 
+// Offsets of sets copied from another store: out[i] = in[i] - in[0] + base for
+// i in [1, count]; also the longest copied set.
+__global__ void k_rebase(const uint64_t* in, uint64_t count, uint64_t base, uint64_t* out,
+                         uint32_t* maxlen) {
+  uint32_t mx = 0;
+  const uint64_t zero = in[0];
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x + 1; i <= count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    out[i] = in[i] - zero + base;
+    mx = max(mx, static_cast<uint32_t>(in[i] - in[i - 1]));
+  }
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxlen, mx);
+}
+
 __global__ void k_widen(const uint32_t* in, uint64_t* out, uint64_t n) {
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -230,6 +247,15 @@ void launch_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
                    uint32_t* status, cudaStream_t s) {
   if (!nsets) return;
   k_invert<<<grid_for(nsets), 256, 0, s>>>(off, mem, nsets, icur, ioff, inv, status);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_rebase(const uint64_t* in, uint64_t count, uint64_t base, uint64_t* out,
+                   uint32_t* maxlen, cudaStream_t s) {
+  if (!count) return;
+  const uint64_t blocks = std::min<uint64_t>((count + 255) / 256, 4096);
+  k_rebase<<<static_cast<unsigned>(blocks), 256, 0, s>>>(in, count, base, out, maxlen);
   RRG_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -73,6 +73,26 @@ def test_lt_search_mode_is_identical(cuda, oracle, kary):
     assert_sets_equal(off_b, mem_b, ref)
 
 
+def test_append_from_side_store_equals_direct_top_up(cuda):
+    """Sets sampled ahead into a side store (generate_slots) and appended later are
+    exactly the sets a direct top-up draws (slot j <- stream j)."""
+    cfg = graphs.scaled(graphs.CONFIGS["cfg1"], 1 << 11, 1 << 15)
+    arrays = graphs.generate(cfg)
+    g = P.Graph(*arrays)
+    direct = P.RRRStore(g)
+    P.generate_batch(g, IC, 3, 3000, direct)
+    main = P.RRRStore(g)
+    P.generate_batch(g, IC, 3, 1000, main)
+    side = P.RRRStore(g)
+    P.generate_slots(g, IC, 3, 1000, 2500, side, fused=False)
+    main.append_from(side, 0, 1200)
+    main.append_from(side, 1200, 800)
+    a, b = direct.export(), main.export()
+    assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
+    assert (direct.counter() == main.counter()).all()
+    assert direct.max_set_size() == main.max_set_size()
+
+
 @pytest.mark.parametrize("coop_min", [2, 7, 64, 1 << 30])
 def test_lt_cooperative_scan_threshold_changes_nothing(cuda, oracle, coop_min):
     cfg = graphs.scaled(graphs.CONFIGS["cfg2"], 1 << 10, 1 << 14)
