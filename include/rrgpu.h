@@ -61,7 +61,7 @@ typedef enum {
                              (GF(2) jump-ahead segments); UINT32_MAX disables */
   RRG_OPT_LT_KARY = 4,  /* arity of the LT CDF search: 2, 4, 8 or 16 (default 8) */
   RRG_OPT_IC_MODE = 5,  /* IC schedule: 0 auto (pilot-measured), 1 lane per sample,
-                           2 warp per sample */
+                           2 warp per sample, 3 thread block per sample */
   RRG_OPT_IC_WARP_MIN_INSP = 6 /* auto: warp per sample once the mean inspected
                                   in-edges per set reaches this value */
 } rrg_option;

@@ -309,7 +309,8 @@ rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value) {
       g->ic_inner = static_cast<uint32_t>(value);
       return RRG_OK;
     case RRG_OPT_IC_MODE:
-      if (value < 0 || value > 2) return invalid("ic_mode must be 0 (auto), 1 (lane) or 2 (warp)");
+      if (value < 0 || value > 3)
+        return invalid("ic_mode must be 0 (auto), 1 (lane), 2 (warp) or 3 (block)");
       g->ic_mode = static_cast<int>(value);
       return RRG_OK;
     case RRG_OPT_IC_WARP_MIN_INSP:
@@ -461,13 +462,14 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.coop_min = g->coop_min;
       p.jtab = g->jtab.ptr;
       p.jtab16 = g->jtab16.ptr;
+      p.jtab256 = g->jtab256.ptr;
       p.lt_kary = g->lt_kary;
       p.dupfree = g->dupfree.ptr;
       p.ic_coop_min = g->ic_coop_min;
 
       // One launch of `kind` over `list` (nullptr: the range [0, n_items)). The
       // per-launch counters reset here; the deferral list accumulates over a pass.
-      enum Kind { kMain, kMainWarp, kWarpWide, kBig };
+      enum Kind { kMain, kMainWarp, kCta, kBig };
       auto launch = [&](Kind kind, const uint32_t* list, uint64_t n_items, uint32_t* restage_out) {
         ctl.next = 0;
         ctl.restage_members = 0;
@@ -482,13 +484,12 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
           launch_big(model, p, list, static_cast<uint32_t>(n_items), g->big.bitmaps.ptr,
                      g->big.lists.ptr, workers, st);
         } else {
-          const int sched = kind == kMainWarp ? kSchedWarp
-                            : kind == kWarpWide ? kSchedWarpWide : kSchedLane;
+          const int sched = kind == kMainWarp ? kSchedWarp : kind == kCta ? kSchedCta : kSchedLane;
           p.list = list;
           p.count = n_items;
-          const uint64_t per_block = sched == kSchedLane ? block : block / 32;  // samples/block
+          const uint64_t per_block = sched == kSchedLane ? block : sched == kSchedWarp ? block / 32 : 1;
           uint64_t grid_cap = full_grid;
-          if (sched == kSchedWarpWide) grid_cap = g->scratch.lanes / 256 / (block / 32);
+          if (sched == kSchedCta) grid_cap = g->scratch.lanes / block;
           const uint64_t grid_need = (n_items + per_block - 1) / per_block;
           launch_sampler(model, p,
                          static_cast<int>(std::max<uint64_t>(1, std::min(grid_cap, grid_need))),
@@ -533,19 +534,15 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         return ctl.ndeferred;
       };
       // main schedule, then the wider schedules for the sets it could not hold:
-      // lane (1K members) -> warp (32K members, IC) -> big-set path (n members)
-      uint64_t ndef = pass(ic_warp ? kMainWarp : kMain, nullptr, c, s->deferred.ptr);
+      // lane (1K members) or warp (32K) -> block (256K, IC) -> big-set path (n)
+      const Kind main_kind = model == RRG_IC && g->ic_mode == 3 ? kCta : ic_warp ? kMainWarp : kMain;
+      uint64_t ndef = pass(main_kind, nullptr, c, s->deferred.ptr);
       uint32_t* dlist = s->deferred.ptr;
       uint32_t* dspare = s->deferred2.ptr;
       if (model == RRG_IC) {
-        if (ndef && !ic_warp) {
+        if (ndef && main_kind != kCta) {
           acc.deferred += ndef;
-          ndef = pass(kMainWarp, dlist, ndef, dspare);
-          std::swap(dlist, dspare);
-        }
-        if (ndef) {
-          acc.deferred += ndef;
-          ndef = pass(kWarpWide, dlist, ndef, dspare);
+          ndef = pass(kCta, dlist, ndef, dspare);
           std::swap(dlist, dspare);
         }
       }

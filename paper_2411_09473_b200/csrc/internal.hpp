@@ -108,6 +108,7 @@ struct rrg_graph {
   rrgpu::DevBuf<double> cdf;     // LT: sequential fp64 prefix per in-list (lazy, +2 pad)
   rrgpu::DevBuf<uint64_t> jtab;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab16;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
+  rrgpu::DevBuf<uint64_t> jtab256;  // IC: byte tables of T^(256 a), a = 1..15 (3.75 MB)
   rrgpu::DevBuf<uint8_t> dupfree;  // IC: per-vertex strictly-increasing-sources flag
   uint32_t ic_coop_min = 256;    // IC: in-lists at least this long expand warp-cooperatively
   int ic_mode = 0;               // IC: 0 auto, 1 lane per sample, 2 warp per sample
@@ -197,6 +198,7 @@ struct SampleParams {
   // IC cooperative expansion of long in-lists
   const uint64_t* jtab;     // byte tables of T^(32 l), l = 1..31 (jump.cpp segment_tables)
   const uint64_t* jtab16;   // byte tables of T^(16 l), l = 1..31 (warp-schedule windows)
+  const uint64_t* jtab256;  // byte tables of T^(256 a), a = 1..15 (CTA-schedule windows)
   const uint8_t* dupfree;   // per vertex: in-list sources strictly increasing
   uint32_t ic_coop_min;     // in-lists at least this long go warp-cooperative
 };
@@ -209,8 +211,8 @@ uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64);
 int sampler_block();
 int sampler_blocks_per_sm(int model, uint32_t ic_inner);
 // IC schedules: lane per sample; warp per sample over its 32 lanes' scratch
-// (sets up to 32K members); warp per sample over 256 lanes' scratch (256K).
-enum Schedule : int { kSchedLane = 0, kSchedWarp = 1, kSchedWarpWide = 2 };
+// (sets up to 32K members); CTA per sample over its 256 lanes' scratch (256K).
+enum Schedule : int { kSchedLane = 0, kSchedWarp = 1, kSchedCta = 2 };
 void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, int schedule,
                     cudaStream_t s);
 void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t nlist,

@@ -413,32 +413,70 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
 // in-lists of the queued vertices (sampling.hpp:96-106). The warp consumes it
 // in WINDOWS of up to 512 in-edges that may span many in-lists:
 //   1. window edges are loaded coalesced (32 per chunk, four chunks in flight);
-//      unvisited = not in the visited set at window start. A source that is
-//      unvisited and occurs twice in the window would change status inside
-//      it, so the window is cut right before the second occurrence (found
-//      with match_any inside a chunk and a shared-memory hash set across
-//      chunks); every edge left in the window then has its reference status;
+//      unvisited = not in the visited set at window start;
 //   2. lane l draws stream positions [16 l, 16 l + 16) of the window's
 //      unvisited edges after a jump by T^(16 l) (byte tables, jump.cpp);
-//   3. accepted sources are appended in window order and marked visited.
-// The next window starts where this one was cut. Short in-lists of a giant
-// near-critical set (cfg3) and hub in-lists (cfg5) go through the same path.
+//   3. this is the reference's draw sequence exactly up to the first edge
+//      whose source an earlier edge of the same window ACCEPTED (the reference
+//      would not draw there). Accepted sources go into a shared-memory map
+//      source -> first accepting position; the window is cut at the first
+//      drawn edge that finds an earlier position, the stream state is
+//      recomputed for the draws before the cut (jump + < 16 steps), and the
+//      accepted sources before the cut are appended in window order.
+// A repeated source only cuts when its earlier occurrence was accepted (about
+// the edge probability), not whenever it repeats. The next window starts at
+// the cut. Short in-lists of a giant near-critical set (cfg3) and hub
+// in-lists (cfg5) go through the same path.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kWarpMemCap = 32 * kMemCap;
 constexpr uint32_t kWin = 512;
 constexpr uint32_t kWinChunks = kWin / 32;
-constexpr uint32_t kDupSlots = 1024;
+constexpr int kAmapLog = 9;
+constexpr uint32_t kAmapSlots = 1u << kAmapLog;  // = kWin >= distinct accepted sources
 struct WinFields {
   uint32_t mask[kWinChunks];
   uint32_t pre[kWinChunks];
   uint32_t acc[kWinChunks];
   uint32_t thr[kWin];
   uint32_t src[kWin];
-  uint32_t dup[kDupSlots];
+  unsigned long long amap[kAmapSlots];  // accepted source -> first accepting position
   uint32_t lstart[32];
   uint32_t lpre[32];
   unsigned long long st[4];
 };
+// Accepted-source map of a window (2^kLog slots): slot = (source << 32 |
+// position); the first accepting position wins by atomicMin (same key, smaller
+// position). Full map (more distinct accepted sources than slots): false.
+template <int kLog>
+__device__ __forceinline__ bool amap_insert(unsigned long long* map, uint32_t v, uint32_t e) {
+  constexpr uint32_t kSlots = 1u << kLog;
+  const unsigned long long want = (static_cast<unsigned long long>(v) << 32) | e;
+  uint32_t h = vhash(v) >> (32 - kLog);
+  for (uint32_t probe = 0; probe < kSlots; ++probe, h = (h + 1) & (kSlots - 1)) {
+    unsigned long long cur = map[h];
+    if (cur == ~0ull) {
+      cur = atomicCAS(map + h, ~0ull, want);
+      if (cur == ~0ull) return true;
+    }
+    if ((cur >> 32) == v) {
+      atomicMin(map + h, want);
+      return true;
+    }
+  }
+  return false;
+}
+// First accepting position of v in the window, or ~0u.
+template <int kLog>
+__device__ __forceinline__ uint32_t amap_first(const unsigned long long* map, uint32_t v) {
+  constexpr uint32_t kSlots = 1u << kLog;
+  uint32_t h = vhash(v) >> (32 - kLog);
+  for (uint32_t probe = 0; probe < kSlots; ++probe, h = (h + 1) & (kSlots - 1)) {
+    const unsigned long long cur = map[h];
+    if (cur == ~0ull) return 0xffffffffu;
+    if ((cur >> 32) == v) return static_cast<uint32_t>(cur);
+  }
+  return 0xffffffffu;
+}
 struct WinSmem {
   union {
     WinFields win;   // multi-list windows
@@ -521,13 +559,12 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
       const uint32_t total = __shfl_sync(kFull, incl, 31);
       ws.lstart[lane] = lb;
       ws.lpre[lane] = incl - len;
-      for (uint32_t t = lane; t < kDupSlots; t += 32) ws.dup[t] = 0xffffffffu;
       __syncwarp();
       uint32_t ecur = min(kWin, total);
-      // ---- 1. unvisited masks; cut before the first repeated unvisited source
+      for (uint32_t t = lane; t < kAmapSlots; t += 32) ws.amap[t] = ~0ull;
+      // ---- 1. unvisited masks (status at window start)
       uint32_t mymask = 0;
-      bool cut = false;
-      for (uint32_t c0 = 0; 32 * c0 < ecur && !cut; c0 += 4) {
+      for (uint32_t c0 = 0; 32 * c0 < ecur; c0 += 4) {
         uint2 r[4];
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
@@ -543,39 +580,10 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const uint32_t c = c0 + q4;
-          if (32 * c >= ecur || cut) break;
+          if (32 * c >= ecur) break;
           const uint32_t e = 32 * c + lane;
           const uint32_t v = r[q4].x;
-          bool unv = e < ecur && !(sfilt_maybe(sf, v) && tab_contains(tab, s.tag, s.lg, v));
-          const unsigned um = __ballot_sync(kFull, unv);
-          const unsigned peers = __match_any_sync(kFull, v);
-          bool dup = unv && (peers & um & lanemask_lt()) != 0;
-          if (unv && !dup) {  // first in this chunk: probe / insert the window's set
-            uint32_t h = vhash(v) >> 22;
-            while (true) {
-              const uint32_t cur = ws.dup[h];
-              if (cur == v) {
-                dup = true;
-                break;
-              }
-              if (cur == 0xffffffffu) {
-                const uint32_t prev = atomicCAS(&ws.dup[h], 0xffffffffu, v);
-                if (prev == 0xffffffffu) break;
-                if (prev == v) {
-                  dup = true;
-                  break;
-                }
-                continue;
-              }
-              h = (h + 1) & (kDupSlots - 1);
-            }
-          }
-          const unsigned dm = __ballot_sync(kFull, dup);
-          if (dm) {
-            ecur = 32 * c + (__ffs(dm) - 1);
-            cut = true;
-          }
-          unv = unv && e < ecur;
+          const bool unv = e < ecur && !(sfilt_maybe(sf, v) && tab_contains(tab, s.tag, s.lg, v));
           if (unv) {
             ws.thr[e] = r[q4].y;
             ws.src[e] = v;
@@ -584,11 +592,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
           if (lane == static_cast<int>(c)) mymask = m;
         }
       }
-      if (lane == 0) {
-        atomicAdd(&p.ctl->windows, 1ull);
-        if (cut) atomicAdd(&p.ctl->cuts, 1ull);
-      }
-      const uint32_t nch = (ecur + 31) >> 5;
+      uint32_t nch = (ecur + 31) >> 5;
       const uint32_t cnt = __popc(mymask);
       uint32_t ui = cnt;
       for (int o = 1; o < 32; o <<= 1) {
@@ -602,6 +606,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
         ws.acc[lane] = 0;
       }
       __syncwarp();
+      bool cut = false;
       if (U) {
         // ---- 2. lane l draws positions [16 l, 16 l + 16) of the window
         const uint32_t r0 = 16u * lane;
@@ -638,12 +643,58 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
           }
         }
         __syncwarp();
+        uint32_t am_lane = lane < static_cast<int>(nch) ? ws.acc[lane] : 0u;
+        const unsigned acm = __ballot_sync(kFull, am_lane != 0);
+        if (acm) {
+          // ---- 3a. every edge drew as if its source were still unvisited. That
+          // is the reference's draw sequence up to the first drawn edge whose
+          // source an EARLIER edge of the window accepted: cut right there.
+          uint32_t fail = 0xffffffffu;
+          for (unsigned t = acm; t; t &= t - 1) {
+            const int c = __ffs(t) - 1;
+            const uint32_t am = __shfl_sync(kFull, am_lane, c);
+            const uint32_t e = 32 * c + lane;
+            if (((am >> lane) & 1u) && !amap_insert<kAmapLog>(ws.amap, ws.src[e], e)) fail = min(fail, e);
+          }
+          __syncwarp();
+          uint32_t cpos = __reduce_min_sync(kFull, fail);
+          for (uint32_t c = __ffs(acm) - 1; c < nch && 32 * c < cpos; ++c) {
+            const uint32_t e = 32 * c + lane;
+            const bool conf = ((ws.mask[c] >> lane) & 1u) && amap_first<kAmapLog>(ws.amap, ws.src[e]) < e;
+            const unsigned b = __ballot_sync(kFull, conf);
+            if (b) {
+              cpos = min(cpos, 32 * c + __ffs(b) - 1);
+              break;
+            }
+          }
+          if (cpos < ecur) {
+            // the stream resumes after the draws of the edges before the cut
+            cut = true;
+            const uint32_t cc = cpos >> 5, cb = cpos & 31;
+            const uint32_t R = ws.pre[cc] + __popc(ws.mask[cc] & ((1u << cb) - 1u));
+            if (lane == static_cast<int>(R >> 4)) {
+              Xoshiro st{s.a, s.b, s.c, s.d};
+              if (lane)
+                gf2_jump_tables(p.jtab16 + static_cast<size_t>(lane - 1) * (32 * 256 * 4), st.a,
+                                st.b, st.c, st.d);
+              for (uint32_t k2 = R & 15u; k2; --k2) st.next();
+              ws.st[0] = st.a;
+              ws.st[1] = st.b;
+              ws.st[2] = st.c;
+              ws.st[3] = st.d;
+            }
+            if (lane > static_cast<int>(cc)) am_lane = 0;
+            else if (lane == static_cast<int>(cc)) am_lane &= (1u << cb) - 1u;
+            ecur = cpos;
+            nch = (ecur + 31) >> 5;
+            __syncwarp();
+          }
+        }
         s.a = ws.st[0];
         s.b = ws.st[1];
         s.c = ws.st[2];
         s.d = ws.st[3];
         // ---- 3. append the accepted sources in window order
-        const uint32_t am_lane = lane < static_cast<int>(nch) ? ws.acc[lane] : 0u;
         uint32_t A = __popc(am_lane);
         for (int o = 16; o; o >>= 1) A += __shfl_xor_sync(kFull, A, o);
         if (A) {
@@ -673,6 +724,10 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
             }
           }
         }
+      }
+      if (lane == 0) {
+        atomicAdd(&p.ctl->windows, 1ull);
+        if (cut) atomicAdd(&p.ctl->cuts, 1ull);
       }
       // ---- advance past the ecur consumed edges
       const unsigned partial = __ballot_sync(kFull, lvalid && incl > ecur);
@@ -727,6 +782,402 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
     atomicAdd(&p.ctl->inspected, (unsigned long long)insp);
     atomicAdd(&p.ctl->entries, (unsigned long long)insp);
   }
+}
+
+// ---------------------------------------------------------------------------
+// K1c: IC sampler, CTA per sample, for the sets the warp schedule could not
+// hold (up to 256K members: the block's 256 lane regions as one). Same window
+// algorithm as K1w, eight times wider: a window holds up to 8 x 512 in-edges
+// of up to 256 queued in-lists, warp w classifies positions [512 w, 512 w +
+// 512) against the visited set at window start, a CTA scan of the warps'
+// unvisited counts gives warp w its first stream position P_w (warp-
+// cooperative jumps by T^(256 a) and T^(16 b), then c < 16 steps; P_w = 256 a +
+// 16 b + c), and the accepted-source map is CTA-wide, so the conflict cut is
+// the reference's across warps. The visited filter is 256K bits.
+// ---------------------------------------------------------------------------
+constexpr int kCtaWarps = kBlock / 32;
+constexpr uint32_t kCtaWin = kCtaWarps * kWin;  // 4096 in-edges
+constexpr int kCtaAmapLog = 11;                 // 2048 slots; a full map cuts the window
+constexpr uint32_t kCtaFilterWords = 8192;      // 256K bits
+constexpr uint32_t kJumpTableWords = 32 * 256 * 4;
+struct CtaWarpFields {
+  uint32_t mask[kWinChunks];
+  uint32_t pre[kWinChunks];
+  uint32_t acc[kWinChunks];
+  uint32_t thr[kWin];
+  uint32_t src[kWin];
+};
+struct CtaSmem {
+  CtaWarpFields w[kCtaWarps];
+  unsigned long long amap[1u << kCtaAmapLog];
+  uint32_t filt[kCtaFilterWords];
+  uint32_t lstart[kBlock];
+  uint32_t lpre[kBlock];
+  unsigned long long st[4];
+  unsigned long long next;
+  uint32_t wsum[kCtaWarps];
+  uint32_t wU[kCtaWarps];
+  uint32_t wA[kCtaWarps];
+  uint32_t cut;
+  uint32_t adv_qi;
+  uint32_t adv_qj;
+  uint32_t any_acc;
+};
+constexpr size_t kCtaKernelDynSmem = sizeof(CtaSmem);
+__device__ __forceinline__ uint32_t cfilt_bit(uint32_t v) { return (v * 0x2545F491u) >> 14; }
+__device__ __forceinline__ bool cfilt_maybe(const uint32_t* sf, uint32_t v) {
+  const uint32_t b = cfilt_bit(v);
+  return (sf[b >> 5] >> (b & 31)) & 1u;
+}
+__device__ __forceinline__ void cfilt_add(uint32_t* sf, uint32_t v) {
+  const uint32_t b = cfilt_bit(v);
+  atomicOr(sf + (b >> 5), 1u << (b & 31));
+}
+
+// Warp-cooperative jump: every lane holds the same state; lane i looks up byte
+// i of it in the byte tables (one 32-byte load) and the warp XOR-reduces.
+__device__ __forceinline__ void warp_jump(const uint64_t* __restrict__ T, Xoshiro& st) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t wv = lane < 8 ? st.a : lane < 16 ? st.b : lane < 24 ? st.c : st.d;
+  const uint32_t byte = static_cast<uint32_t>(wv >> (8 * (lane & 7))) & 255u;
+  const ulonglong2* e = reinterpret_cast<const ulonglong2*>(T + (static_cast<size_t>(lane) * 256 + byte) * 4);
+  ulonglong2 x = __ldg(e), y = __ldg(e + 1);
+  for (int o = 16; o; o >>= 1) {
+    x.x ^= __shfl_xor_sync(kFull, x.x, o);
+    x.y ^= __shfl_xor_sync(kFull, x.y, o);
+    y.x ^= __shfl_xor_sync(kFull, y.x, o);
+    y.y ^= __shfl_xor_sync(kFull, y.y, o);
+  }
+  st = Xoshiro{x.x, x.y, y.x, y.y};
+}
+// T^P st for P < 4096, warp-uniform.
+__device__ __forceinline__ Xoshiro warp_advance(const SampleParams& p, Xoshiro st, uint32_t P) {
+  const uint32_t a = P >> 8, b = (P >> 4) & 15u, c = P & 15u;
+  if (a) warp_jump(p.jtab256 + static_cast<size_t>(a - 1) * kJumpTableWords, st);
+  if (b) warp_jump(p.jtab16 + static_cast<size_t>(b - 1) * kJumpTableWords, st);
+  for (uint32_t t = 0; t < c; ++t) st.next();
+  return st;
+}
+
+__global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(const SampleParams p) {
+  constexpr uint32_t kCap = kBlock * kMemCap;
+  extern __shared__ __align__(16) unsigned char k_dsm[];
+  CtaSmem& cs = *reinterpret_cast<CtaSmem*>(k_dsm);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int wl = tid >> 5;
+  CtaWarpFields& ws = cs.w[wl];
+  const uint64_t region = static_cast<uint64_t>(blockIdx.x) * kBlock;
+  if (region + kBlock > p.lanes) return;  // uniform per block
+  uint32_t* mem = p.lists + region * kMemCap;
+  uint64_t* tab = p.tabs + region * kTabCap;
+  uint32_t* sf = cs.filt;
+  for (uint32_t t = tid; t < kCtaFilterWords; t += kBlock) sf[t] = 0;
+  // same 256-lane regions and tag range as the 256-lane warp layout
+  const uint64_t tslot = region / 32;
+  uint32_t tag = 0xC0000000u | (p.wtags[tslot] & 0x3fffffffu);
+  uint64_t insp = 0;
+  const uint32_t wbase = kWin * wl;  // this warp's first window position
+  for (;;) {
+    __syncthreads();  // previous sample written out, filter cleared
+    if (tid == 0) cs.next = atomicAdd(&p.ctl->next, 1ull);
+    __syncthreads();
+    const unsigned long long k = cs.next;
+    if (k >= p.count) break;
+    const uint32_t idx = p.list ? p.list[k] : p.idx_base + static_cast<uint32_t>(k);
+    Xoshiro s;
+    s.seed(stream_seed(p.run_seed, p.base_slot + idx));      // sampling.hpp:179
+    const uint32_t root = static_cast<uint32_t>(s.below(p.n));  // :180
+    uint32_t stag = ++tag, lg = kTabLog0, nmem = 1;
+    if (tid == 0) {
+      mem[0] = root;
+      tab_insert(tab, stag, lg, root);
+      cfilt_add(sf, root);
+    }
+    bool ok = true;
+    uint32_t qi = 0, qj = p.off[root];
+    while (qi < nmem && ok) {
+      // ---- window layout: up to 256 queued in-lists from (qi, qj)
+      __syncthreads();  // members / table / filter of the last window visible
+      const uint32_t nq = nmem;
+      const bool lvalid = qi + tid < nq;
+      uint32_t lb = 0, le = 0;
+      if (lvalid) {
+        const uint32_t v = mem[qi + tid];
+        lb = tid == 0 ? qj : p.off[v];
+        le = p.off[v + 1];
+      }
+      const uint32_t len = le - lb;
+      uint32_t incl = len;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) cs.wsum[wl] = incl;
+      for (uint32_t t = tid; t < (1u << kCtaAmapLog); t += kBlock) cs.amap[t] = ~0ull;
+      if (tid == 0) {
+        cs.cut = 0xffffffffu;
+        cs.adv_qi = 0xffffffffu;
+        cs.any_acc = 0;
+      }
+      __syncthreads();
+      uint32_t total = 0;
+      for (int w = 0; w < kCtaWarps; ++w) {
+        const uint32_t x = cs.wsum[w];
+        if (w < wl) incl += x;
+        total += x;
+      }
+      cs.lstart[tid] = lb;
+      cs.lpre[tid] = lvalid ? incl - len : 0xffffffffu;
+      __syncthreads();
+      uint32_t ecur = min(kCtaWin, total);
+      // ---- 1. warp wl classifies positions [wbase, wbase + 512) (status at window start)
+      uint32_t mymask = 0;
+      const uint32_t wend = wbase < ecur ? min(kWin, ecur - wbase) : 0u;
+      for (uint32_t c0 = 0; 32 * c0 < wend; c0 += 4) {
+        uint2 r[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t el = 32 * (c0 + q4) + lane;
+          r[q4] = make_uint2(0xffffffffu, 0u);
+          if (el < wend) {
+            const uint32_t e = wbase + el;
+            uint32_t t = 0;  // last list t with lpre[t] <= e
+            for (uint32_t step = kBlock / 2; step; step >>= 1)
+              if (cs.lpre[t + step] <= e) t += step;
+            r[q4] = __ldg(p.rec + cs.lstart[t] + (e - cs.lpre[t]));
+          }
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t c = c0 + q4;
+          if (32 * c >= wend) break;
+          const uint32_t el = 32 * c + lane;
+          const uint32_t v = r[q4].x;
+          const bool unv = el < wend && !(cfilt_maybe(sf, v) && tab_contains(tab, stag, lg, v));
+          if (unv) {
+            ws.thr[el] = r[q4].y;
+            ws.src[el] = v;
+          }
+          const unsigned m = __ballot_sync(kFull, unv);
+          if (lane == static_cast<int>(c)) mymask = m;
+        }
+      }
+      const uint32_t cnt = __popc(mymask);
+      uint32_t ui = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, ui, o);
+        if (lane >= o) ui += y;
+      }
+      const uint32_t Uw = __shfl_sync(kFull, ui, 31);
+      if (lane < static_cast<int>(kWinChunks)) {
+        ws.mask[lane] = mymask;
+        ws.pre[lane] = ui - cnt;
+        ws.acc[lane] = 0;
+      }
+      if (lane == 0) cs.wU[wl] = Uw;
+      __syncthreads();
+      uint32_t Pw = 0, U = 0;
+      for (int w = 0; w < kCtaWarps; ++w) {
+        const uint32_t x = cs.wU[w];
+        if (w < wl) Pw += x;
+        U += x;
+      }
+      bool cut = false;
+      if (U) {
+        // ---- 2. warp wl draws stream positions [P_w, P_w + U_w); lane l the
+        // 16 from P_w + 16 l
+        const uint32_t nch = (wend + 31) >> 5;
+        if (Uw) {
+          const Xoshiro wst = warp_advance(p, s, Pw);
+          const uint32_t r0 = 16u * lane;
+          if (r0 < Uw) {
+            Xoshiro st = wst;
+            if (lane) gf2_jump_tables(p.jtab16 + static_cast<size_t>(lane - 1) * kJumpTableWords,
+                                      st.a, st.b, st.c, st.d);
+            uint32_t c = 0;
+            for (uint32_t step = 8; step; step >>= 1)
+              if (c + step < nch && ws.pre[c + step] <= r0) c += step;
+            uint32_t m = ws.mask[c];
+            for (uint32_t k2 = r0 - ws.pre[c]; k2; --k2) m &= m - 1;
+            const uint32_t need = min(16u, Uw - r0);
+            uint32_t acc = 0;
+            for (uint32_t done = 0; done < need;) {
+              if (!m) {
+                if (acc) atomicOr(&ws.acc[c], acc);
+                acc = 0;
+                m = ws.mask[++c];
+                continue;
+              }
+              const int bit = __ffs(m) - 1;
+              m &= m - 1;
+              if (st.u53() < bernoulli_threshold(ws.thr[32 * c + bit])) acc |= 1u << bit;
+              ++done;
+            }
+            if (acc) atomicOr(&ws.acc[c], acc);
+            if (Pw + r0 + need == U) {
+              cs.st[0] = st.a;
+              cs.st[1] = st.b;
+              cs.st[2] = st.c;
+              cs.st[3] = st.d;
+            }
+          }
+        }
+        __syncwarp();
+        // ---- 3a. accepted sources -> first accepting position (CTA-wide map)
+        uint32_t am_lane = lane < static_cast<int>(nch) ? ws.acc[lane] : 0u;
+        const unsigned acm = __ballot_sync(kFull, am_lane != 0);
+        uint32_t fail = 0xffffffffu;
+        for (unsigned t = acm; t; t &= t - 1) {
+          const int c = __ffs(t) - 1;
+          const uint32_t am = __shfl_sync(kFull, am_lane, c);
+          const uint32_t el = 32 * c + lane;
+          if (((am >> lane) & 1u) && !amap_insert<kCtaAmapLog>(cs.amap, ws.src[el], wbase + el))
+            fail = min(fail, wbase + el);
+        }
+        fail = __reduce_min_sync(kFull, fail);
+        if (lane == 0) {
+          if (fail != 0xffffffffu) atomicMin(&cs.cut, fail);
+          if (acm) cs.any_acc = 1;
+        }
+        __syncthreads();
+        if (cs.any_acc) {
+          // ---- 3b. the first drawn edge whose source an earlier edge accepted
+          const uint32_t lim = cs.cut;
+          for (uint32_t c = 0; c < nch && wbase + 32 * c < lim; ++c) {
+            const uint32_t m = ws.mask[c];
+            if (!m) continue;
+            const uint32_t el = 32 * c + lane;
+            const bool conf = ((m >> lane) & 1u) &&
+                              amap_first<kCtaAmapLog>(cs.amap, ws.src[el]) < wbase + el;
+            const unsigned b = __ballot_sync(kFull, conf);
+            if (b) {
+              if (lane == 0) atomicMin(&cs.cut, wbase + 32 * c + __ffs(b) - 1);
+              break;
+            }
+          }
+          __syncthreads();
+          const uint32_t cpos = cs.cut;
+          if (cpos < ecur) {
+            cut = true;
+            const uint32_t cw = cpos / kWin, cl = cpos % kWin, cc = cl >> 5, cb = cl & 31;
+            if (wl == static_cast<int>(cw)) {
+              // the stream resumes after the draws of the edges before the cut
+              const uint32_t Rl = ws.pre[cc] + __popc(ws.mask[cc] & ((1u << cb) - 1u));
+              const Xoshiro wst = warp_advance(p, s, Pw);
+              if (lane == static_cast<int>(Rl >> 4)) {
+                Xoshiro st = wst;
+                if (lane) gf2_jump_tables(p.jtab16 + static_cast<size_t>(lane - 1) * kJumpTableWords,
+                                          st.a, st.b, st.c, st.d);
+                for (uint32_t k2 = Rl & 15u; k2; --k2) st.next();
+                cs.st[0] = st.a;
+                cs.st[1] = st.b;
+                cs.st[2] = st.c;
+                cs.st[3] = st.d;
+              }
+              if (lane > static_cast<int>(cc)) am_lane = 0;
+              else if (lane == static_cast<int>(cc)) am_lane &= (1u << cb) - 1u;
+            } else if (wl > static_cast<int>(cw)) {
+              am_lane = 0;
+            }
+            ecur = cpos;
+          }
+        }
+        // ---- 4. append the accepted sources in window order
+        uint32_t Aw = __popc(am_lane);
+        for (int o = 16; o; o >>= 1) Aw += __shfl_xor_sync(kFull, Aw, o);
+        if (lane == 0) cs.wA[wl] = Aw;
+        __syncthreads();
+        s = Xoshiro{cs.st[0], cs.st[1], cs.st[2], cs.st[3]};
+        uint32_t Apre = 0, A = 0;
+        for (int w = 0; w < kCtaWarps; ++w) {
+          const uint32_t x = cs.wA[w];
+          if (w < wl) Apre += x;
+          A += x;
+        }
+        if (A) {
+          if (nmem + A > kCap) {
+            ok = false;
+          } else {
+            uint32_t lg2 = lg;
+            while (2 * (nmem + A) > (1u << lg2)) ++lg2;
+            if (lg2 != lg) {  // grow: re-insert the members under a fresh tag
+              lg = lg2;
+              ++stag;
+              for (uint32_t t = tid; t < nmem; t += kBlock) tab_insert_atomic(tab, stag, lg, mem[t]);
+              __syncthreads();
+            }
+            uint32_t base = nmem + Apre;
+            unsigned cmk = __ballot_sync(kFull, am_lane != 0);
+            while (cmk) {
+              const int c = __ffs(cmk) - 1;
+              cmk &= cmk - 1;
+              const uint32_t am = __shfl_sync(kFull, am_lane, c);
+              if ((am >> lane) & 1u) {
+                const uint32_t v = ws.src[32 * c + lane];
+                mem[base + __popc(am & lanemask_lt())] = v;
+                tab_insert_atomic(tab, stag, lg, v);
+                cfilt_add(sf, v);
+              }
+              base += __popc(am);
+            }
+            nmem += A;
+          }
+        }
+      }
+      if (tid == 0) {
+        atomicAdd(&p.ctl->windows, 1ull);
+        if (cut) atomicAdd(&p.ctl->cuts, 1ull);
+      }
+      // ---- advance past the ecur consumed edges: the first list not wholly consumed
+      if (lvalid && incl > ecur && incl - len <= ecur) {
+        cs.adv_qi = qi + tid;
+        cs.adv_qj = lb + (ecur - (incl - len));
+      }
+      __syncthreads();
+      if (cs.adv_qi != 0xffffffffu) {
+        qi = cs.adv_qi;
+        qj = cs.adv_qj;
+      } else {
+        qi += min(static_cast<uint32_t>(kBlock), nq - qi);
+        if (qi < nmem) qj = p.off[mem[qi]];
+      }
+    }
+    __syncthreads();
+    // inspected in-edges of the set = sum of its members' in-degrees
+    uint64_t sinsp = 0;
+    if (ok)
+      for (uint32_t t = tid; t < nmem; t += kBlock) sinsp += p.off[mem[t] + 1] - p.off[mem[t]];
+    tag = stag;
+    for (uint32_t t = tid; t < kCtaFilterWords; t += kBlock) sf[t] = 0;  // filter per sample
+    if (!ok) {
+      if (tid == 0) defer_slot(p, idx);
+      continue;
+    }
+    if (tid == 0) cs.next = atomicAdd(&p.ctl->cursor, (unsigned long long)nmem);
+    __syncthreads();
+    const unsigned long long pos = cs.next;
+    if (pos + nmem > p.stage_cap) {
+      if (tid == 0) restage_slot(p, idx, nmem);
+      continue;
+    }
+    for (uint32_t t = tid; t < nmem; t += kBlock) {
+      const uint32_t v = mem[t];
+      p.stage[pos + t] = v;
+      if (p.counter) atomicAdd(p.counter + v, 1u);
+    }
+    if (tid == 0) {
+      p.slot_start[idx] = pos;
+      p.slot_len[idx] = nmem;
+    }
+    insp += sinsp;
+  }
+  for (int o = 16; o; o >>= 1) insp += __shfl_xor_sync(kFull, insp, o);
+  if (lane == 0 && insp) {
+    atomicAdd(&p.ctl->inspected, (unsigned long long)insp);
+    atomicAdd(&p.ctl->entries, (unsigned long long)insp);
+  }
+  if (tid == 0) p.wtags[tslot] = tag;
 }
 
 // ---------------------------------------------------------------------------
@@ -1216,13 +1667,12 @@ void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inne
         RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_warp<32>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kWarpKernelDynSmem)));
-        RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_warp<256>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kWarpKernelDynSmem)));
+        RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kCtaKernelDynSmem)));
         attr_set = true;
       }
       if (schedule == kSchedWarp) k_sample_ic_warp<32><<<grid, kBlock, kWarpKernelDynSmem, s>>>(p);
-      else k_sample_ic_warp<256><<<grid, kBlock, kWarpKernelDynSmem, s>>>(p);
+      else k_sample_ic_cta<<<grid, kBlock, kCtaKernelDynSmem, s>>>(p);
     } else {
       k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
     }
@@ -1263,8 +1713,12 @@ void prepare_ic(rrg_graph* g) {
   }
   static const std::vector<uint64_t> jt = segment_tables(32, 31);  // host, built once
   static const std::vector<uint64_t> jt16 = segment_tables(16, 31);
+  static const std::vector<uint64_t> jt256 = segment_tables(256, 15);
   g->jtab.reserve_discard(jt.size());
   g->jtab16.reserve_discard(jt16.size());
+  g->jtab256.reserve_discard(jt256.size());
+  RRG_CUDA(cudaMemcpyAsync(g->jtab256.ptr, jt256.data(), jt256.size() * 8, cudaMemcpyHostToDevice,
+                           g->stream));
   RRG_CUDA(cudaMemcpyAsync(g->jtab.ptr, jt.data(), jt.size() * 8, cudaMemcpyHostToDevice,
                            g->stream));
   RRG_CUDA(cudaMemcpyAsync(g->jtab16.ptr, jt16.data(), jt16.size() * 8, cudaMemcpyHostToDevice,

@@ -102,7 +102,7 @@ def test_lt_cooperative_scan_threshold_changes_nothing(cuda, oracle, coop_min):
     assert_sets_equal(off, mem, ref)
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 @pytest.mark.parametrize("coop_min", [1, 33, 256, 1 << 30])
 @pytest.mark.parametrize("name,n,m", [("cfg1", 1 << 11, 1 << 15), ("cfg5", 20000, 300000),
                                       ("cfg3", 30000, 500000)])
@@ -128,7 +128,7 @@ def test_ic_cooperative_expansion_with_duplicate_sources(cuda, oracle):
     w = rng.uniform(0.0, 0.05, keep.sum()).astype(np.float32)
     arrays = P.build_graph(n, src[keep], dst[keep], w)
     ref = oracle.graph(*arrays).sample(IC, 4, 0, 1500)
-    for mode in (1, 2):
+    for mode in (1, 2, 3):
         _, st, off, mem = gpu_sample(arrays, IC, 4, 1500, ic_coop_min=1, ic_mode=mode)
         assert_sets_equal(off, mem, ref)
 
@@ -176,10 +176,10 @@ def test_big_set_path(cuda, oracle):
     assert (st.counter() == ref.counter).all()
 
 
-@pytest.mark.parametrize("mode", [1, 2])
-def test_giant_sets_both_schedules(cuda, oracle, mode):
+@pytest.mark.parametrize("mode", [1, 2, 3])
+def test_giant_sets_all_schedules(cuda, oracle, mode):
     """Supercritical IC: sets of tens of thousands of members (> the 32K warp
-    budget for some) go through the warp region and the big-set path."""
+    budget for some) go through the warp, block and big-set paths."""
     rng = np.random.default_rng(11)
     n, m = 40000, 400000
     src = rng.integers(0, n, m).astype(np.uint32)
@@ -194,7 +194,8 @@ def test_giant_sets_both_schedules(cuda, oracle, mode):
     assert (st.counter() == ref.counter).all()
 
 
-@pytest.mark.parametrize("name,model,mode", [("cfg1", IC, 1), ("cfg1", IC, 2), ("cfg2", LT, 0),
+@pytest.mark.parametrize("name,model,mode", [("cfg1", IC, 1), ("cfg1", IC, 2), ("cfg1", IC, 3),
+                                             ("cfg2", LT, 0),
                                              ("cfg4", LT, 0)])
 def test_inspected_edges_equal_reference_trip_count(cuda, port, name, model, mode):
     """edges_inspected (the roofline numerator) counts exactly the reference's
