@@ -564,6 +564,11 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
       for (uint32_t t = lane; t < kAmapSlots; t += 32) ws.amap[t] = ~0ull;
       // ---- 1. unvisited masks (status at window start)
       uint32_t mymask = 0;
+      uint32_t thi = 0;  // in-list holding the window's last position
+      if (ecur)
+        for (uint32_t step = 16; step; step >>= 1)
+          if (thi + step < 32 && ws.lpre[thi + step] <= ecur - 1) thi += step;
+      const uint32_t top = thi ? 1u << (31 - __clz(thi)) : 0u;
       for (uint32_t c0 = 0; 32 * c0 < ecur; c0 += 4) {
         uint2 r[4];
 #pragma unroll
@@ -571,9 +576,9 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
           const uint32_t e = 32 * (c0 + q4) + lane;
           r[q4] = make_uint2(0xffffffffu, 0u);
           if (e < ecur) {
-            uint32_t t = 0;  // in-list holding window position e: last t with lpre[t] <= e
-            for (uint32_t step = 16; step; step >>= 1)
-              if (t + step < 32 && ws.lpre[t + step] <= e) t += step;
+            uint32_t t = 0;  // in-list holding window position e: last t <= thi with lpre[t] <= e
+            for (uint32_t step = top; step; step >>= 1)
+              if (t + step <= thi && ws.lpre[t + step] <= e) t += step;
             r[q4] = __ldg(p.rec + ws.lstart[t] + (e - ws.lpre[t]));
           }
         }
@@ -894,11 +899,12 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       tab_insert(tab, stag, lg, root);
       cfilt_add(sf, root);
     }
+    __syncthreads();
     bool ok = true;
     uint32_t qi = 0, qj = p.off[root];
     while (qi < nmem && ok) {
-      // ---- window layout: up to 256 queued in-lists from (qi, qj)
-      __syncthreads();  // members / table / filter of the last window visible
+      // ---- window layout: up to 256 queued in-lists from (qi, qj). The
+      // barrier closing the previous window made its members visible.
       const uint32_t nq = nmem;
       const bool lvalid = qi + tid < nq;
       uint32_t lb = 0, le = 0;
@@ -915,12 +921,12 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       }
       if (lane == 31) cs.wsum[wl] = incl;
       for (uint32_t t = tid; t < (1u << kCtaAmapLog); t += kBlock) cs.amap[t] = ~0ull;
-      if (tid == 0) {
+      __syncthreads();
+      if (tid == 0) {  // after the barrier: every thread has read the previous window's
         cs.cut = 0xffffffffu;
         cs.adv_qi = 0xffffffffu;
         cs.any_acc = 0;
       }
-      __syncthreads();
       uint32_t total = 0;
       for (int w = 0; w < kCtaWarps; ++w) {
         const uint32_t x = cs.wsum[w];
@@ -934,6 +940,17 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       // ---- 1. warp wl classifies positions [wbase, wbase + 512) (status at window start)
       uint32_t mymask = 0;
       const uint32_t wend = wbase < ecur ? min(kWin, ecur - wbase) : 0u;
+      // lists holding this warp's first and last position (warp-uniform); the
+      // per-edge search then only spans [tlo, thi] -- usually one list
+      uint32_t tlo = 0, thi = 0;
+      if (wend) {
+        for (uint32_t step = kBlock / 2; step; step >>= 1) {
+          if (cs.lpre[tlo + step] <= wbase) tlo += step;
+          if (cs.lpre[thi + step] <= wbase + wend - 1) thi += step;
+        }
+      }
+      const uint32_t span = thi - tlo;
+      const uint32_t top = span ? 1u << (31 - __clz(span)) : 0u;
       for (uint32_t c0 = 0; 32 * c0 < wend; c0 += 4) {
         uint2 r[4];
 #pragma unroll
@@ -942,9 +959,9 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
           r[q4] = make_uint2(0xffffffffu, 0u);
           if (el < wend) {
             const uint32_t e = wbase + el;
-            uint32_t t = 0;  // last list t with lpre[t] <= e
-            for (uint32_t step = kBlock / 2; step; step >>= 1)
-              if (cs.lpre[t + step] <= e) t += step;
+            uint32_t t = tlo;  // last list t in [tlo, thi] with lpre[t] <= e
+            for (uint32_t step = top; step; step >>= 1)
+              if (t + step <= thi && cs.lpre[t + step] <= e) t += step;
             r[q4] = __ldg(p.rec + cs.lstart[t] + (e - cs.lpre[t]));
           }
         }
