@@ -128,6 +128,22 @@ __device__ __forceinline__ void tab_insert(uint64_t* tab, uint32_t tag, uint32_t
   tab[h] = (static_cast<uint64_t>(tag) << 32) | v;
 }
 
+// One probe chain for "visited?" and, if not, "insert": true when v was present.
+__device__ __forceinline__ bool tab_find_or_insert(uint64_t* tab, uint32_t tag, uint32_t lg,
+                                                   uint32_t v) {
+  const uint32_t mask = (1u << lg) - 1;
+  uint32_t h = vhash(v) >> (32 - lg);
+  while (true) {
+    const uint64_t e = tab[h];
+    if (static_cast<uint32_t>(e >> 32) != tag) {
+      tab[h] = (static_cast<uint64_t>(tag) << 32) | v;
+      return false;
+    }
+    if (static_cast<uint32_t>(e) == v) return true;
+    h = (h + 1) & mask;
+  }
+}
+
 // Concurrent insert (several lanes filling one lane's table in the cooperative
 // hub expansion). An entry with a stale tag is free; claim it with a CAS.
 __device__ __forceinline__ void tab_insert_atomic(uint64_t* tab, uint32_t tag, uint32_t lg,

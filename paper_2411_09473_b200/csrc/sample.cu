@@ -1200,6 +1200,10 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
 // ---------------------------------------------------------------------------
 // K2: LT sampler (sampling.hpp:117-145 per slot)
 // ---------------------------------------------------------------------------
+constexpr uint32_t kLtTabLog0 = 8;        // walks average ~80 steps (cfg4): fewer rehashes
+constexpr uint32_t kWarpSearchMin = 256;  // in-lists longer than this may be warp-searched
+constexpr int kWarpSearchLanes = 2;       // ... when at most this many lanes need one
+
 template <int KARY>
 __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
   const int lane = threadIdx.x & 31;
@@ -1210,6 +1214,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
   Xoshiro rng{0, 0, 0, 0};
   bool active = false, exhausted = false;
   uint32_t idx = 0, nmem = 0, lg = kTabLog0, u = 0;
+  uint32_t nb = 0, ne = 0;  // in-list bounds of u, loaded as soon as u is known
   uint64_t insp = 0, sinsp = 0, ent = 0;
   const bool linear = p.lt_scan == kLtLinear;
 
@@ -1217,8 +1222,10 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
     if (fetch_slot(p, !active && !exhausted, exhausted, idx)) {
       rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
       u = static_cast<uint32_t>(rng.below(p.n));
+      nb = p.off[u];
+      ne = p.off[u + 1];
       ++tag;
-      lg = kTabLog0;
+      lg = kLtTabLog0;
       mem[0] = u;
       nmem = 1;
       sinsp = 0;
@@ -1232,9 +1239,10 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
     double d = 0.0;
     if (active) {
       d = rng.u01();  // sampling.hpp:127 -- always consumed
-      b = p.off[u];
-      e = p.off[u + 1];
+      b = nb;
+      e = ne;
     }
+    uint32_t vsel = 0;  // source of `pick` when the search already loaded it
     uint32_t pick = e;  // index of the first cdf entry > d, or e for "none"
     const bool coop = active && linear && (e - b) >= p.coop_min;
     unsigned cm = __ballot_sync(kFull, coop);
@@ -1277,7 +1285,62 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
         ent += read;
       }
     }
-    if (active && !coop) {
+    // Few deep searches pending in the warp (the batch tail: one long walk left):
+    // the whole warp searches each of those lists, 128 pivots per round trip,
+    // instead of the owner's K-ary descent (~log8(deg) round trips).
+    bool wsearched = false;
+    if (!linear) {
+      unsigned dm = __ballot_sync(kFull, active && e - b > kWarpSearchMin);
+      if (dm && __popc(dm) <= kWarpSearchLanes) {
+        while (dm) {
+          const int L = __ffs(dm) - 1;
+          dm &= dm - 1;
+          uint32_t lo = __shfl_sync(kFull, b, L), hi = __shfl_sync(kFull, e, L);
+          const uint32_t eL = hi;
+          const double dL = __shfl_sync(kFull, d, L);
+          uint64_t read = 0;
+          // invariant: answer (first cdf > dL, or eL) in [lo, hi]
+          while (hi - lo > 128u) {
+            const uint32_t step = (hi - lo) / 129u;
+            uint32_t below = 0;
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q)
+              below += __ldg(p.cdf + lo + (4u * lane + q + 1u) * step) <= dL ? 1u : 0u;
+            below = __reduce_add_sync(kFull, below);  // pivots <= dL form a prefix
+            read += 128;
+            const uint32_t nlo = below ? lo + below * step + 1 : lo;
+            hi = below < 128u ? lo + (below + 1) * step : hi;
+            lo = nlo;
+          }
+          uint32_t below = 0;
+          uint32_t sq[5];
+#pragma unroll
+          for (uint32_t q = 0; q < 4; ++q) {
+            const uint32_t i = lo + 4u * lane + q;
+            if (i < hi && __ldg(p.cdf + i) <= dL) ++below;
+            sq[q] = i < eL && i <= hi ? __ldg(p.src + i) : 0u;
+          }
+          sq[4] = 0;
+          below = __reduce_add_sync(kFull, below);
+          read += hi - lo;
+          const uint32_t pk = lo + below;
+          // source of pk: lane (below / 4), slot below % 4 (below == 128: lane 32 -> reload)
+          uint32_t vv = 0;
+#pragma unroll
+          for (uint32_t q = 0; q < 4; ++q)
+            if ((below & 3u) == q) vv = sq[q];
+          vv = __shfl_sync(kFull, vv, (below >> 2) & 31u);
+          if (below >= 128u && pk < eL) vv = __ldg(p.src + pk);
+          if (lane == L) {
+            pick = pk;
+            vsel = vv;
+            ent += read;
+            wsearched = true;
+          }
+        }
+      }
+    }
+    if (active && !coop && !wsearched) {
       if (linear) {
         for (uint32_t t = b; t < e; ++t) {
           if (d < p.cdf[t]) {
@@ -1302,11 +1365,21 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
           hi = below < KARY - 1 ? lo + (below + 1) * step : hi;
           lo = nlo;
         }
-        while (lo < hi && __ldg(p.cdf + lo) <= d) {
-          ++lo;
-          ++ent;
+        // last level: the <= K entries of [lo, hi) and the sources of [lo, hi]
+        // in one round trip (independent loads); pick = lo + #(cdf <= d)
+        uint32_t cnt = 0;
+        uint32_t sv[KARY + 1];
+#pragma unroll
+        for (uint32_t t = 0; t <= static_cast<uint32_t>(KARY); ++t) {
+          const uint32_t i = lo + t;
+          sv[t] = i < e && i <= hi ? __ldg(p.src + i) : 0u;
+          if (t < static_cast<uint32_t>(KARY) && i < hi && __ldg(p.cdf + i) <= d) ++cnt;
         }
-        pick = lo;
+        ent += hi - lo;
+        pick = lo + cnt;
+#pragma unroll
+        for (uint32_t t = 0; t <= static_cast<uint32_t>(KARY); ++t)
+          if (t == cnt) vsel = sv[t];
       }
     }
     if (!active) continue;
@@ -1314,8 +1387,10 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
     bool stop = pick >= e;
     uint32_t v = 0;
     if (!stop) {
-      v = p.src[pick];
-      stop = tab_contains(tab, tag, lg, v);  // chosen already visited (:137)
+      v = (linear || coop) ? p.src[pick] : vsel;
+      nb = p.off[v];  // next step's list, in flight with the visited probe
+      ne = p.off[v + 1];
+      stop = tab_find_or_insert(tab, tag, lg, v);  // chosen already visited (:137)
     }
     if (stop) {
       if (emit_set(p, idx, mem, nmem)) insp += sinsp;
@@ -1323,8 +1398,13 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
     } else if (nmem == kMemCap) {
       defer_slot(p, idx);
       active = false;
-    } else {
-      lane_insert(mem, tab, tag, lg, nmem, v);
+    } else {  // v is in the table already (tab_find_or_insert)
+      mem[nmem++] = v;
+      if (2 * nmem > (1u << lg)) {  // grow: re-insert under a fresh tag
+        ++lg;
+        ++tag;
+        for (uint32_t t = 0; t < nmem; ++t) tab_insert(tab, tag, lg, mem[t]);
+      }
       u = v;
     }
   }
