@@ -106,6 +106,7 @@ __host__ __device__ __forceinline__ uint64_t bernoulli_threshold(uint32_t bits) 
 constexpr uint32_t kMemCap = 1024;  // members per lane before deferring to the big path
 constexpr uint32_t kTabCap = 2048;  // max table entries per lane (2 x kMemCap)
 constexpr uint32_t kTabLog0 = 6;    // initial table log2 capacity
+constexpr uint32_t kLtRecSmall = 8; // LT vertex record holds the whole in-list up to this degree
 
 __device__ __forceinline__ uint32_t vhash(uint32_t v) { return v * 0x9E3779B1u; }
 

@@ -1217,13 +1217,24 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
   uint32_t nb = 0, ne = 0;  // in-list bounds of u, loaded as soon as u is known
   uint64_t insp = 0, sinsp = 0, ent = 0;
   const bool linear = p.lt_scan == kLtLinear;
+  // search mode: u's 128-byte vertex record (k_build_ltrec), loaded as soon as
+  // u is known -- bounds, and the whole list or the first search level
+  const bool recs = !linear && p.ltrec != nullptr;
+  uint4 rr[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) rr[i] = make_uint4(0, 0, 0, 0);
 
   for (;;) {
     if (fetch_slot(p, !active && !exhausted, exhausted, idx)) {
       rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
       u = static_cast<uint32_t>(rng.below(p.n));
-      nb = p.off[u];
-      ne = p.off[u + 1];
+      if (recs) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rr[i] = __ldg(p.ltrec + static_cast<size_t>(u) * 8 + i);
+      } else {
+        nb = p.off[u];
+        ne = p.off[u + 1];
+      }
       ++tag;
       lg = kLtTabLog0;
       mem[0] = u;
@@ -1239,11 +1250,44 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
     double d = 0.0;
     if (active) {
       d = rng.u01();  // sampling.hpp:127 -- always consumed
-      b = nb;
-      e = ne;
+      b = recs ? rr[0].x : nb;
+      e = recs ? rr[0].x + rr[0].y : ne;
     }
     uint32_t vsel = 0;  // source of `pick` when the search already loaded it
     uint32_t pick = e;  // index of the first cdf entry > d, or e for "none"
+    uint32_t slo = b, shi = e;  // search range: answer (first cdf > d, or e) in [slo, shi]
+    bool picked = false;        // resolved from the vertex record alone
+    if (recs && active) {
+      const uint32_t deg = e - b;
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(rr);
+      if (deg <= kLtRecSmall) {  // whole list in the record: count entries <= d
+        uint32_t cnt = 0;
+#pragma unroll
+        for (uint32_t t = 0; t < kLtRecSmall; ++t) {
+          const double c = __longlong_as_double(
+              (static_cast<long long>(w[3 + 2 * t]) << 32) | w[2 + 2 * t]);
+          if (t < deg && c <= d) ++cnt;
+        }
+#pragma unroll
+        for (uint32_t t = 0; t < kLtRecSmall; ++t)
+          if (t == cnt) vsel = w[18 + t];
+        pick = b + cnt;
+        ent += deg;
+        picked = true;
+      } else {  // 16-ary first level from the record's pivots
+        const uint32_t step = max(1u, deg / 16u);
+        uint32_t below = 0;
+#pragma unroll
+        for (uint32_t t = 1; t <= 15; ++t) {
+          const double c = __longlong_as_double(
+              (static_cast<long long>(w[2 * t + 1]) << 32) | w[2 * t]);
+          below += c <= d ? 1u : 0u;
+        }
+        ent += 15;
+        slo = below ? b + below * step + 1 : b;
+        shi = below < 15 ? min(e, b + (below + 1) * step) : e;
+      }
+    }
     const bool coop = active && linear && (e - b) >= p.coop_min;
     unsigned cm = __ballot_sync(kFull, coop);
     while (cm) {
@@ -1290,13 +1334,13 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
     // instead of the owner's K-ary descent (~log8(deg) round trips).
     bool wsearched = false;
     if (!linear) {
-      unsigned dm = __ballot_sync(kFull, active && e - b > kWarpSearchMin);
+      unsigned dm = __ballot_sync(kFull, active && !picked && shi - slo > kWarpSearchMin);
       if (dm && __popc(dm) <= kWarpSearchLanes) {
         while (dm) {
           const int L = __ffs(dm) - 1;
           dm &= dm - 1;
-          uint32_t lo = __shfl_sync(kFull, b, L), hi = __shfl_sync(kFull, e, L);
-          const uint32_t eL = hi;
+          uint32_t lo = __shfl_sync(kFull, slo, L), hi = __shfl_sync(kFull, shi, L);
+          const uint32_t eL = __shfl_sync(kFull, e, L);
           const double dL = __shfl_sync(kFull, d, L);
           uint64_t read = 0;
           // invariant: answer (first cdf > dL, or eL) in [lo, hi]
@@ -1340,7 +1384,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
         }
       }
     }
-    if (active && !coop && !wsearched) {
+    if (active && !coop && !wsearched && !picked) {
       if (linear) {
         for (uint32_t t = b; t < e; ++t) {
           if (d < p.cdf[t]) {
@@ -1353,7 +1397,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
         // upper_bound (first cdf[t] > d; cdf non-decreasing) as a K-ary search:
         // K-1 independent pivot loads per level keep the dependent round trips
         // at logK(deg) instead of log2(deg). Invariant: answer in [lo, hi].
-        uint32_t lo = b, hi = e;
+        uint32_t lo = slo, hi = shi;
         while (hi - lo > static_cast<uint32_t>(KARY)) {
           const uint32_t step = (hi - lo) / KARY;
           uint32_t below = 0;  // pivots with cdf <= d form a prefix
@@ -1388,8 +1432,13 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
     uint32_t v = 0;
     if (!stop) {
       v = (linear || coop) ? p.src[pick] : vsel;
-      nb = p.off[v];  // next step's list, in flight with the visited probe
-      ne = p.off[v + 1];
+      if (recs) {  // next step's record, in flight with the visited probe
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rr[i] = __ldg(p.ltrec + static_cast<size_t>(v) * 8 + i);
+      } else {
+        nb = p.off[v];  // next step's list, in flight with the visited probe
+        ne = p.off[v + 1];
+      }
       stop = tab_find_or_insert(tab, tag, lg, v);  // chosen already visited (:137)
     }
     if (stop) {
@@ -1715,6 +1764,42 @@ __global__ void k_offsets_u32(const uint64_t* off64, uint32_t* off32, uint32_t n
   }
 }
 
+// LT vertex record (128 B, one line): in-list start and degree, then for
+// degree <= 8 the whole CDF and the sources, else the 15 pivots of a 16-ary
+// first search level (cdf[b + t * step], t = 1..15). One load per walk step
+// replaces the offsets load and the first search level(s).
+__global__ void k_build_ltrec(const uint32_t* off, const double* cdf, const uint32_t* src,
+                              uint32_t n, uint32_t* rec) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const uint32_t b = off[u], deg = off[u + 1] - b;
+  uint32_t w[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) w[i] = 0;
+  w[0] = b;
+  w[1] = deg;
+  if (deg <= kLtRecSmall) {
+    for (uint32_t t = 0; t < deg; ++t) {
+      const unsigned long long x = __double_as_longlong(cdf[b + t]);
+      w[2 + 2 * t] = static_cast<uint32_t>(x);
+      w[3 + 2 * t] = static_cast<uint32_t>(x >> 32);
+      w[18 + t] = src[b + t];
+    }
+  } else {
+    const uint32_t step = max(1u, deg / 16u);
+    for (uint32_t t = 1; t <= 15; ++t) {
+      const uint32_t i = t * step;
+      const double v = i < deg ? cdf[b + i] : 2.0;  // past the list: never <= a draw
+      const unsigned long long x = __double_as_longlong(v);
+      w[2 * t] = static_cast<uint32_t>(x);
+      w[2 * t + 1] = static_cast<uint32_t>(x >> 32);
+    }
+  }
+  uint4* out = reinterpret_cast<uint4*>(rec + static_cast<size_t>(u) * 32);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) out[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+}
+
 __global__ void k_check_sources(const uint32_t* src, uint64_t m, uint32_t n, uint32_t* bad) {
   bool ok = true;
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
@@ -1850,6 +1935,14 @@ void prepare_lt(rrg_graph* g) {
   RRG_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
   RRG_CUDA(cudaStreamSynchronize(g->stream));
   g->cdf_monotone = hbad == 0;
+  if (g->cdf_monotone && g->n) {
+    g->ltrec.reserve_discard(static_cast<size_t>(g->n) * 32);
+    k_build_ltrec<<<(g->n + 255) / 256, 256, 0, g->stream>>>(g->off.ptr, g->cdf.ptr, g->src.ptr,
+                                                           g->n, g->ltrec.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+    RRG_CUDA(cudaStreamSynchronize(g->stream));
+  }
   g->cdf_ready = true;
 }
 
