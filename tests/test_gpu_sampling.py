@@ -62,6 +62,30 @@ def test_top_ups_continue_the_slot_stream(cuda, oracle, model):
     assert (st.counter() == ref.counter).all()
 
 
+@pytest.mark.parametrize("kary", [2, 8, 16])
+def test_lt_vertex_records_at_boundary_degrees(cuda, oracle, kary):
+    """In-degrees around the vertex-record cases (whole list up to 8, 16-ary
+    pivots above, step 1 below 16), the search arities and the warp-wide tail
+    search (> 256), with zero weights (flat CDF runs) and sums below 1."""
+    rng = np.random.default_rng(41)
+    degs = list(range(0, 20)) + [31, 32, 33, 127, 128, 129, 255, 256, 257, 258, 1023, 1024,
+                                 1025, 4095, 4096, 4097]
+    n = len(degs)
+    dst = np.repeat(np.arange(n, dtype=np.uint32), degs)
+    src = rng.integers(0, n, dst.size).astype(np.uint32)
+    w = rng.uniform(0.0, 1.0, dst.size).astype(np.float32)
+    w[rng.random(dst.size) < 0.2] = 0.0
+    roff, rsrc, rw = P.build_graph(n, src, dst, w)
+    P.normalize_lt_weights(roff, rw)
+    rw *= np.float32(0.97)  # leave "no in-neighbour chosen" reachable
+    arrays = (roff, rsrc, rw)
+    _, _, off_a, mem_a = gpu_sample(arrays, LT, 13, 6000, lt_scan=0)
+    _, _, off_b, mem_b = gpu_sample(arrays, LT, 13, 6000, lt_scan=1, lt_kary=kary)
+    assert (off_a == off_b).all() and (mem_a == mem_b).all()
+    ref = oracle.graph(*arrays).sample(LT, 13, 0, 6000, workers=4)
+    assert_sets_equal(off_b, mem_b, ref)
+
+
 @pytest.mark.parametrize("kary", [2, 4, 8, 16])
 def test_lt_search_mode_is_identical(cuda, oracle, kary):
     cfg = graphs.scaled(graphs.CONFIGS["cfg4"], 40000, 600000)
