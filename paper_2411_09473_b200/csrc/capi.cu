@@ -445,6 +445,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.src = g->src.ptr;
       p.cdf = g->cdf.ptr;
       p.ltrec = reinterpret_cast<const uint4*>(g->ltrec.ptr);
+      p.ltnodes = g->ltnodes.ptr;
       p.run_seed = run_seed;
       p.base_slot = first_slot + done;
       p.count = c;

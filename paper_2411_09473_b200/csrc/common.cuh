@@ -108,6 +108,29 @@ constexpr uint32_t kTabCap = 2048;  // max table entries per lane (2 x kMemCap)
 constexpr uint32_t kTabLog0 = 6;    // initial table log2 capacity
 constexpr uint32_t kLtRecSmall = 8; // LT vertex record holds the whole in-list up to this degree
 
+// LT search tree over one in-list's CDF (upper_bound: first cdf > d, or the
+// list end). A node over candidate range [lo, hi] holds P pivots cdf[lo + t s],
+// s = max(1, ceil((hi - lo) / (P + 1))), t = 1..P (a pivot at or past hi never
+// counts); with `below` pivots <= d the answer lies in the child range below,
+// of length <= s (so the tree depth follows from the degree alone).
+// The root (P = 14) sits in the vertex record, inner nodes (P = 15) in 128-byte
+// lines; nodes exist while hi - lo > kLtRecSmall. Child c of node x is node
+// 16 x + 1 + c (root x = 0), stored at slot x - 1 of the vertex's node array.
+constexpr uint32_t kLtRootPivots = 14;
+constexpr uint32_t kLtNodePivots = 15;
+__device__ __host__ __forceinline__ uint32_t lt_step(uint32_t lo, uint32_t hi, uint32_t P) {
+  const uint32_t s = (hi - lo + P) / (P + 1);
+  return s ? s : 1u;
+}
+__device__ __host__ __forceinline__ void lt_child(uint32_t& lo, uint32_t& hi, uint32_t P,
+                                                  uint32_t below) {
+  const uint32_t s = lt_step(lo, hi, P);
+  const uint32_t nlo = below ? lo + below * s + 1 : lo;
+  const uint32_t cap = lo + (below + 1) * s;
+  hi = below < P ? (cap < hi ? cap : hi) : hi;
+  lo = nlo;
+}
+
 __device__ __forceinline__ uint32_t vhash(uint32_t v) { return v * 0x9E3779B1u; }
 
 __device__ __forceinline__ bool tab_contains(const uint64_t* tab, uint32_t tag, uint32_t lg,

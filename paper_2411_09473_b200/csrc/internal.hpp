@@ -107,6 +107,8 @@ struct rrg_graph {
   rrgpu::DevBuf<uint2> rec;      // IC: {source, weight bits} per in-edge (lazy)
   rrgpu::DevBuf<double> cdf;     // LT: sequential fp64 prefix per in-list (lazy, +2 pad)
   rrgpu::DevBuf<uint32_t> ltrec; // LT: 128-byte vertex records (k_build_ltrec), monotone CDF only
+  rrgpu::DevBuf<uint64_t> ltnodeoff;  // LT: first search-tree slot per vertex (u64[n+1])
+  rrgpu::DevBuf<double> ltnodes;      // LT: search-tree nodes, 16 doubles (15 pivots) each
   rrgpu::DevBuf<uint64_t> jtab;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab16;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab256;  // IC: byte tables of T^(256 a), a = 1..15 (3.75 MB)
@@ -176,6 +178,7 @@ struct SampleParams {
   const uint32_t* src;
   const double* cdf;
   const uint4* ltrec;    // LT vertex records (search mode), 8 x uint4 per vertex
+  const double* ltnodes; // LT search-tree nodes (16 doubles each)
   uint64_t run_seed;
   uint64_t base_slot;
   uint64_t count;

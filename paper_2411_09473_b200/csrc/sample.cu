@@ -49,7 +49,18 @@ __device__ __forceinline__ bool emit_set(const SampleParams& p, uint32_t idx, co
     return false;
   }
   uint32_t* out = p.stage + pos;
-  for (uint32_t t = 0; t < nmem; ++t) {
+  uint32_t t = 0;
+  for (; t + 8 <= nmem; t += 8) {  // eight member loads in flight per round trip
+    uint32_t v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = mem[t + q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      out[t + q] = v[q];
+      if (p.counter) atomicAdd(p.counter + v[q], 1u);
+    }
+  }
+  for (; t < nmem; ++t) {
     const uint32_t v = mem[t];
     out[t] = v;
     if (p.counter) atomicAdd(p.counter + v, 1u);
@@ -1201,8 +1212,6 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
 // K2: LT sampler (sampling.hpp:117-145 per slot)
 // ---------------------------------------------------------------------------
 constexpr uint32_t kLtTabLog0 = 8;        // walks average ~80 steps (cfg4): fewer rehashes
-constexpr uint32_t kWarpSearchMin = 256;  // in-lists longer than this may be warp-searched
-constexpr int kWarpSearchLanes = 2;       // ... when at most this many lanes need one
 
 template <int KARY>
 __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
@@ -1274,18 +1283,33 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
         pick = b + cnt;
         ent += deg;
         picked = true;
-      } else {  // 16-ary first level from the record's pivots
-        const uint32_t step = max(1u, deg / 16u);
+      } else {  // the root's 14 pivots, then the vertex's search-tree nodes
         uint32_t below = 0;
 #pragma unroll
-        for (uint32_t t = 1; t <= 15; ++t) {
+        for (uint32_t t = 1; t <= kLtRootPivots; ++t) {
           const double c = __longlong_as_double(
-              (static_cast<long long>(w[2 * t + 1]) << 32) | w[2 * t]);
+              (static_cast<long long>(w[2 * t + 3]) << 32) | w[2 * t + 2]);
           below += c <= d ? 1u : 0u;
         }
-        ent += 15;
-        slo = below ? b + below * step + 1 : b;
-        shi = below < 15 ? min(e, b + (below + 1) * step) : e;
+        ent += kLtRootPivots;
+        uint32_t lo = b, hi = e;
+        lt_child(lo, hi, kLtRootPivots, below);
+        const uint64_t nbase = (static_cast<uint64_t>(w[3]) << 32) | w[2];
+        uint32_t x = 1 + below;
+        while (hi - lo > kLtRecSmall) {  // one 128-byte node per level
+          const double2* nd = reinterpret_cast<const double2*>(p.ltnodes + (nbase + x - 1) * 16);
+          double2 q[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) q[i] = __ldg(nd + i);
+          uint32_t bl = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) bl += (q[i].x <= d ? 1u : 0u) + (q[i].y <= d ? 1u : 0u);
+          ent += kLtNodePivots;
+          lt_child(lo, hi, kLtNodePivots, bl);
+          x = 16 * x + 1 + bl;
+        }
+        slo = lo;
+        shi = hi;
       }
     }
     const bool coop = active && linear && (e - b) >= p.coop_min;
@@ -1329,62 +1353,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
         ent += read;
       }
     }
-    // Few deep searches pending in the warp (the batch tail: one long walk left):
-    // the whole warp searches each of those lists, 128 pivots per round trip,
-    // instead of the owner's K-ary descent (~log8(deg) round trips).
-    bool wsearched = false;
-    if (!linear) {
-      unsigned dm = __ballot_sync(kFull, active && !picked && shi - slo > kWarpSearchMin);
-      if (dm && __popc(dm) <= kWarpSearchLanes) {
-        while (dm) {
-          const int L = __ffs(dm) - 1;
-          dm &= dm - 1;
-          uint32_t lo = __shfl_sync(kFull, slo, L), hi = __shfl_sync(kFull, shi, L);
-          const uint32_t eL = __shfl_sync(kFull, e, L);
-          const double dL = __shfl_sync(kFull, d, L);
-          uint64_t read = 0;
-          // invariant: answer (first cdf > dL, or eL) in [lo, hi]
-          while (hi - lo > 128u) {
-            const uint32_t step = (hi - lo) / 129u;
-            uint32_t below = 0;
-#pragma unroll
-            for (uint32_t q = 0; q < 4; ++q)
-              below += __ldg(p.cdf + lo + (4u * lane + q + 1u) * step) <= dL ? 1u : 0u;
-            below = __reduce_add_sync(kFull, below);  // pivots <= dL form a prefix
-            read += 128;
-            const uint32_t nlo = below ? lo + below * step + 1 : lo;
-            hi = below < 128u ? lo + (below + 1) * step : hi;
-            lo = nlo;
-          }
-          uint32_t below = 0;
-          uint32_t sq[5];
-#pragma unroll
-          for (uint32_t q = 0; q < 4; ++q) {
-            const uint32_t i = lo + 4u * lane + q;
-            if (i < hi && __ldg(p.cdf + i) <= dL) ++below;
-            sq[q] = i < eL && i <= hi ? __ldg(p.src + i) : 0u;
-          }
-          sq[4] = 0;
-          below = __reduce_add_sync(kFull, below);
-          read += hi - lo;
-          const uint32_t pk = lo + below;
-          // source of pk: lane (below / 4), slot below % 4 (below == 128: lane 32 -> reload)
-          uint32_t vv = 0;
-#pragma unroll
-          for (uint32_t q = 0; q < 4; ++q)
-            if ((below & 3u) == q) vv = sq[q];
-          vv = __shfl_sync(kFull, vv, (below >> 2) & 31u);
-          if (below >= 128u && pk < eL) vv = __ldg(p.src + pk);
-          if (lane == L) {
-            pick = pk;
-            vsel = vv;
-            ent += read;
-            wsearched = true;
-          }
-        }
-      }
-    }
-    if (active && !coop && !wsearched && !picked) {
+    if (active && !coop && !picked) {
       if (linear) {
         for (uint32_t t = b; t < e; ++t) {
           if (d < p.cdf[t]) {
@@ -1765,11 +1734,11 @@ __global__ void k_offsets_u32(const uint64_t* off64, uint32_t* off32, uint32_t n
 }
 
 // LT vertex record (128 B, one line): in-list start and degree, then for
-// degree <= 8 the whole CDF and the sources, else the 15 pivots of a 16-ary
-// first search level (cdf[b + t * step], t = 1..15). One load per walk step
-// replaces the offsets load and the first search level(s).
+// degree <= 8 the whole CDF and the sources, else the first slot of the
+// vertex's search-tree nodes (u64) and the root's 14 pivots. One load per walk
+// step replaces the offsets load and the first search level.
 __global__ void k_build_ltrec(const uint32_t* off, const double* cdf, const uint32_t* src,
-                              uint32_t n, uint32_t* rec) {
+                              const uint64_t* nodeoff, uint32_t n, uint32_t* rec) {
   const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n) return;
   const uint32_t b = off[u], deg = off[u + 1] - b;
@@ -1786,18 +1755,77 @@ __global__ void k_build_ltrec(const uint32_t* off, const double* cdf, const uint
       w[18 + t] = src[b + t];
     }
   } else {
-    const uint32_t step = max(1u, deg / 16u);
-    for (uint32_t t = 1; t <= 15; ++t) {
+    w[2] = static_cast<uint32_t>(nodeoff[u]);
+    w[3] = static_cast<uint32_t>(nodeoff[u] >> 32);
+    const uint32_t step = lt_step(0, deg, kLtRootPivots);
+    for (uint32_t t = 1; t <= kLtRootPivots; ++t) {
       const uint32_t i = t * step;
       const double v = i < deg ? cdf[b + i] : 2.0;  // past the list: never <= a draw
       const unsigned long long x = __double_as_longlong(v);
-      w[2 * t] = static_cast<uint32_t>(x);
-      w[2 * t + 1] = static_cast<uint32_t>(x >> 32);
+      w[2 + 2 * t] = static_cast<uint32_t>(x);
+      w[3 + 2 * t] = static_cast<uint32_t>(x >> 32);
     }
   }
   uint4* out = reinterpret_cast<uint4*>(rec + static_cast<size_t>(u) * 32);
 #pragma unroll
   for (int i = 0; i < 8; ++i) out[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+}
+
+// Node slots of a vertex's search tree: 16^k per level k >= 1 while the
+// child ranges of the level above (<= the step) still exceed kLtRecSmall.
+__global__ void k_count_ltnodes(const uint32_t* off, uint32_t n, uint32_t* cnt) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  uint32_t len = off[u + 1] - off[u];
+  uint64_t slots = 0, width = 16;
+  uint32_t P = kLtRootPivots;
+  if (len > kLtRecSmall) {
+    for (;;) {
+      const uint32_t cl = lt_step(0, len, P);  // longest child range
+      if (cl <= kLtRecSmall) break;
+      slots += width;
+      width *= 16;
+      len = cl;
+      P = kLtNodePivots;
+    }
+  }
+  cnt[u] = static_cast<uint32_t>(slots);
+}
+
+// One block per vertex: slot s (node x = s + 1) follows its path from the root
+// and stores its 15 pivots (unreachable slots: sentinels).
+__global__ void k_build_ltnodes(const uint32_t* off, const double* cdf, const uint64_t* nodeoff,
+                                uint32_t n, double* nodes) {
+  for (uint32_t u = blockIdx.x; u < n; u += gridDim.x) {
+    const uint64_t base = nodeoff[u];
+    const uint32_t cnt = static_cast<uint32_t>(nodeoff[u + 1] - base);
+    if (!cnt) continue;
+    const uint32_t b = off[u], e = off[u + 1];
+    for (uint32_t s = threadIdx.x; s < cnt; s += blockDim.x) {
+      uint32_t dig[12];
+      int nd = 0;
+      for (uint32_t x = s + 1; x; x = (x - 1) / 16) dig[nd++] = (x - 1) % 16;
+      uint32_t lo = b, hi = e;
+      bool ok = true;
+      for (int k = nd - 1; k >= 0 && ok; --k) {
+        const uint32_t P = k == nd - 1 ? kLtRootPivots : kLtNodePivots;
+        if (dig[k] > P || hi - lo <= kLtRecSmall) {
+          ok = false;
+          break;
+        }
+        lt_child(lo, hi, P, dig[k]);
+        if (lo > hi) ok = false;
+      }
+      ok = ok && hi - lo > kLtRecSmall;
+      double* out = nodes + (base + s) * 16;
+      const uint32_t st = ok ? lt_step(lo, hi, kLtNodePivots) : 1u;
+      for (uint32_t t = 1; t <= kLtNodePivots; ++t) {
+        const uint32_t i = lo + t * st;
+        out[t - 1] = ok && i < hi ? cdf[i] : 2.0;
+      }
+      out[15] = 2.0;
+    }
+  }
 }
 
 __global__ void k_check_sources(const uint32_t* src, uint64_t m, uint32_t n, uint32_t* bad) {
@@ -1936,9 +1964,29 @@ void prepare_lt(rrg_graph* g) {
   RRG_CUDA(cudaStreamSynchronize(g->stream));
   g->cdf_monotone = hbad == 0;
   if (g->cdf_monotone && g->n) {
+    // search trees of the long in-lists, then the vertex records
+    DevBuf<uint32_t> cnt;
+    cnt.reserve_discard(g->n);
+    k_count_ltnodes<<<(g->n + 255) / 256, 256, 0, g->stream>>>(g->off.ptr, g->n, cnt.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+    g->ltnodeoff.reserve_discard(static_cast<size_t>(g->n) + 1);
+    DevBuf<uint64_t> tmp;
+    exclusive_scan_u32(cnt.ptr, g->ltnodeoff.ptr, g->n, tmp, g->stream);
+    uint64_t slots = 0;
+    RRG_CUDA(cudaMemcpyAsync(&slots, g->ltnodeoff.ptr + g->n, 8, cudaMemcpyDeviceToHost,
+                             g->stream));
+    RRG_CUDA(cudaStreamSynchronize(g->stream));
+    g->ltnodes.reserve_discard(slots ? slots * 16 : 16);
+    if (slots) {
+      k_build_ltnodes<<<std::min<uint32_t>(g->n, 65535u * 4), 128, 0, g->stream>>>(
+          g->off.ptr, g->cdf.ptr, g->ltnodeoff.ptr, g->n, g->ltnodes.ptr);
+      RRG_CUDA(cudaGetLastError());
+      count_launch();
+    }
     g->ltrec.reserve_discard(static_cast<size_t>(g->n) * 32);
-    k_build_ltrec<<<(g->n + 255) / 256, 256, 0, g->stream>>>(g->off.ptr, g->cdf.ptr, g->src.ptr,
-                                                           g->n, g->ltrec.ptr);
+    k_build_ltrec<<<(g->n + 255) / 256, 256, 0, g->stream>>>(
+        g->off.ptr, g->cdf.ptr, g->src.ptr, g->ltnodeoff.ptr, g->n, g->ltrec.ptr);
     RRG_CUDA(cudaGetLastError());
     count_launch();
     RRG_CUDA(cudaStreamSynchronize(g->stream));
