@@ -417,13 +417,26 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
     rrg_batch_stats acc{};
     for (uint64_t done = 0; done < count;) {
       uint64_t c = std::min(kChunk, count - done);
-      // IC execution mode: lane per sample (light sets) or warp per sample (heavy,
-      // hub-dominated sets). Auto mode measures a pilot chunk on a new graph
-      // first; sub-batches append in slot order, so splitting changes nothing.
+      // IC execution mode. Auto mode measures a pilot chunk on a new graph first
+      // (block schedule: bounded latency whatever the set sizes); sub-batches
+      // append in slot order, so splitting changes nothing. Then: hub-dominated
+      // sets (mean inspected >= ic_hub_insp) -> warp per sample (per-edge
+      // throughput); batches of few inspected edges in total -> block per sample
+      // (latency: the largest sets finish 4-8x sooner); heavy large batches ->
+      // warp; light large batches -> lane.
       if (model == RRG_IC && g->ic_mode == 0 && g->ic_mean_insp < 0) c = std::min<uint64_t>(c, 2048);
-      const bool ic_warp =
-          model == RRG_IC &&
-          (g->ic_mode == 2 || (g->ic_mode == 0 && g->ic_mean_insp >= g->ic_warp_min_insp));
+      bool ic_warp = false, ic_cta = false;
+      if (model == RRG_IC) {
+        const double mean = g->ic_mean_insp;
+        if (g->ic_mode == 2) ic_warp = true;
+        else if (g->ic_mode == 3) ic_cta = true;
+        else if (g->ic_mode == 0) {
+          if (mean < 0) ic_cta = true;
+          else if (mean >= g->ic_hub_insp) ic_warp = true;
+          else if (static_cast<double>(c) * mean <= g->ic_cta_max_edges) ic_cta = true;
+          else ic_warp = mean >= g->ic_warp_min_insp;
+        }
+      }
       // staging sized from the running mean set size (first batch: a guess;
       // sets that do not fit are re-run once staging has grown)
       const double per_set = s->nsets ? static_cast<double>(s->total) / s->nsets * 1.5 + 8 : 96.0;
@@ -537,7 +550,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       };
       // main schedule, then the wider schedules for the sets it could not hold:
       // lane (1K members) or warp (32K) -> block (256K, IC) -> big-set path (n)
-      const Kind main_kind = model == RRG_IC && g->ic_mode == 3 ? kCta : ic_warp ? kMainWarp : kMain;
+      const Kind main_kind = ic_cta ? kCta : ic_warp ? kMainWarp : kMain;
       uint64_t ndef = pass(main_kind, nullptr, c, s->deferred.ptr);
       uint32_t* dlist = s->deferred.ptr;
       uint32_t* dspare = s->deferred2.ptr;

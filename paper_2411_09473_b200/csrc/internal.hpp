@@ -114,8 +114,11 @@ struct rrg_graph {
   rrgpu::DevBuf<uint64_t> jtab256;  // IC: byte tables of T^(256 a), a = 1..15 (3.75 MB)
   rrgpu::DevBuf<uint8_t> dupfree;  // IC: per-vertex strictly-increasing-sources flag
   uint32_t ic_coop_min = 256;    // IC: in-lists at least this long expand warp-cooperatively
-  int ic_mode = 0;               // IC: 0 auto, 1 lane per sample, 2 warp per sample
+  int ic_mode = 0;               // IC: 0 auto, 1 lane, 2 warp, 3 block per sample
   double ic_mean_insp = -1.0;    // IC: running mean of inspected in-edges per set
+  double ic_hub_insp = 1e5;       // auto: warp per sample from this mean on (cfg5 ~1M)
+  double ic_cta_max_edges = 1.5e8;  // auto: block per sample up to this many expected
+                                    // inspected edges per batch (cfg1 IMM, cfg3 65K)
   double ic_warp_min_insp = 1024.0;  // auto: warp per sample from this mean on (cfg1 5.5K
                                      // and cfg5 986K run faster per warp; cfg3 237 per lane)
   bool rec_ready = false;

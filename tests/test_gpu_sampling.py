@@ -193,7 +193,7 @@ def test_big_set_path(cuda, oracle):
     src, dst = src[keep], dst[keep]
     w = rng.uniform(0.2, 0.6, src.size).astype(np.float32)
     arrays = P.build_graph(n, src, dst, w)
-    g, st, off, mem = gpu_sample(arrays, IC, 9, 600)
+    g, st, off, mem = gpu_sample(arrays, IC, 9, 600, ic_mode=1)
     assert g.last_batch_stats().deferred > 0
     ref = oracle.graph(*arrays).sample(IC, 9, 0, 600, workers=4)
     assert_sets_equal(off, mem, ref)

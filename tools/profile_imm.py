@@ -11,13 +11,15 @@ from paper_2411_09473_b200 import graphs  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("workload")
 ap.add_argument("--repeat", type=int, default=3)
+ap.add_argument("--ic-mode", type=int, default=0)
 a = ap.parse_args()
 cfg = graphs.CONFIGS[a.workload]
 arrays = graphs.generate(cfg)
 g = P.Graph(*arrays)
 g.prepare(cfg.model)
+g.set_option("ic_mode", a.ic_mode)
 for i in range(a.repeat):
     t = time.time()
     r = P.run_imm(g, P.ImmConfig(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model))
-    print(f"{cfg.name} imm {1e3 * (time.time() - t):.1f} ms theta {r.theta} theta' {r.theta_prime} "
+    print(f"{cfg.name} mode {a.ic_mode} imm {1e3 * (time.time() - t):.1f} ms theta {r.theta} theta' {r.theta_prime} "
           f"lb {r.lower_bound:.1f} timings {r.timings}", flush=True)
