@@ -106,18 +106,22 @@ __host__ __device__ __forceinline__ uint64_t bernoulli_threshold(uint32_t bits) 
 constexpr uint32_t kMemCap = 1024;  // members per lane before deferring to the big path
 constexpr uint32_t kTabCap = 2048;  // max table entries per lane (2 x kMemCap)
 constexpr uint32_t kTabLog0 = 6;    // initial table log2 capacity
-constexpr uint32_t kLtRecSmall = 8; // LT vertex record holds the whole in-list up to this degree
+constexpr uint32_t kLtRecSmall = 6; // LT vertex record holds the whole in-list up to this degree
+constexpr uint32_t kLtLeaf = 8;     // search trees narrow to at most this many CDF entries
 
 // LT search tree over one in-list's CDF (upper_bound: first cdf > d, or the
 // list end). A node over candidate range [lo, hi] holds P pivots cdf[lo + t s],
 // s = max(1, ceil((hi - lo) / (P + 1))), t = 1..P (a pivot at or past hi never
 // counts); with `below` pivots <= d the answer lies in the child range below,
-// of length <= s (so the tree depth follows from the degree alone).
-// The root (P = 14) sits in the vertex record, inner nodes (P = 15) in 128-byte
-// lines; nodes exist while hi - lo > kLtRecSmall. Child c of node x is node
-// 16 x + 1 + c (root x = 0), stored at slot x - 1 of the vertex's node array.
-constexpr uint32_t kLtRootPivots = 14;
-constexpr uint32_t kLtNodePivots = 15;
+// of length <= s (so the tree depth follows from the degree alone). The root
+// (P = 13) sits in the 64-byte vertex record, inner nodes (P = 31) in 128-byte
+// lines; nodes exist while hi - lo > kLtLeaf. Child c of node x is node
+// 32 x + 1 + c (root x = 0), stored at slot x - 1 of the vertex's node array.
+// Pivots are stored as floats rounded DOWN (f <= p < next(f)): counts are exact,
+// a pivot with f <= d < next(f) is re-read from the fp64 CDF (lt_count_le).
+constexpr uint32_t kLtRootPivots = 13;
+constexpr uint32_t kLtNodePivots = 31;
+constexpr uint32_t kLtFanout = 32;
 __device__ __host__ __forceinline__ uint32_t lt_step(uint32_t lo, uint32_t hi, uint32_t P) {
   const uint32_t s = (hi - lo + P) / (P + 1);
   return s ? s : 1u;
@@ -129,6 +133,23 @@ __device__ __host__ __forceinline__ void lt_child(uint32_t& lo, uint32_t& hi, ui
   const uint32_t cap = lo + (below + 1) * s;
   hi = below < P ? (cap < hi ? cap : hi) : hi;
   lo = nlo;
+}
+// Exact number of entries p_t <= d among P sorted entries stored as rounded-down
+// floats w[t] (entry t at cdf[first + t * step]), given dbits = the bits of d
+// rounded down to float. For non-negative floats the bit patterns order like
+// the values, so f < fd proves p < next(f) <= fd <= d, f > fd proves p >= f > d,
+// and only f == fd (d within one float ulp of p) is re-read from the fp64 CDF.
+template <uint32_t P>
+__device__ __forceinline__ uint32_t lt_count_le(const uint32_t* w, uint32_t dbits, double d,
+                                                const double* cdf, uint32_t first, uint32_t step) {
+  uint32_t sure = 0, maybe = 0;
+#pragma unroll
+  for (uint32_t t = 0; t < P; ++t) {
+    sure += w[t] < dbits ? 1u : 0u;
+    maybe += w[t] <= dbits ? 1u : 0u;
+  }
+  while (sure < maybe && __ldg(cdf + first + sure * step) <= d) ++sure;
+  return sure;
 }
 
 __device__ __forceinline__ uint32_t vhash(uint32_t v) { return v * 0x9E3779B1u; }

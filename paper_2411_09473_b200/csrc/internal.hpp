@@ -106,9 +106,9 @@ struct rrg_graph {
   rrgpu::DevBuf<float> w;        // f32[m]   transpose weights
   rrgpu::DevBuf<uint2> rec;      // IC: {source, weight bits} per in-edge (lazy)
   rrgpu::DevBuf<double> cdf;     // LT: sequential fp64 prefix per in-list (lazy, +2 pad)
-  rrgpu::DevBuf<uint32_t> ltrec; // LT: 128-byte vertex records (k_build_ltrec), monotone CDF only
+  rrgpu::DevBuf<uint32_t> ltrec; // LT: 64-byte vertex records (k_build_ltrec), monotone CDF only
   rrgpu::DevBuf<uint64_t> ltnodeoff;  // LT: first search-tree slot per vertex (u64[n+1])
-  rrgpu::DevBuf<double> ltnodes;      // LT: search-tree nodes, 16 doubles (15 pivots) each
+  rrgpu::DevBuf<uint32_t> ltnodes;    // LT: search-tree nodes, 32 floats (31 pivots) each
   rrgpu::DevBuf<uint64_t> jtab;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab16;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab256;  // IC: byte tables of T^(256 a), a = 1..15 (3.75 MB)
@@ -180,8 +180,8 @@ struct SampleParams {
   const uint2* rec;
   const uint32_t* src;
   const double* cdf;
-  const uint4* ltrec;    // LT vertex records (search mode), 8 x uint4 per vertex
-  const double* ltnodes; // LT search-tree nodes (16 doubles each)
+  const uint4* ltrec;    // LT vertex records (search mode), 4 x uint4 per vertex
+  const uint32_t* ltnodes;  // LT search-tree nodes (32 floats each)
   uint64_t run_seed;
   uint64_t base_slot;
   uint64_t count;

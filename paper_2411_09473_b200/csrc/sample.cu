@@ -1226,12 +1226,12 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
   uint32_t nb = 0, ne = 0;  // in-list bounds of u, loaded as soon as u is known
   uint64_t insp = 0, sinsp = 0, ent = 0;
   const bool linear = p.lt_scan == kLtLinear;
-  // search mode: u's 128-byte vertex record (k_build_ltrec), loaded as soon as
+  // search mode: u's 64-byte vertex record (k_build_ltrec), loaded as soon as
   // u is known -- bounds, and the whole list or the first search level
   const bool recs = !linear && p.ltrec != nullptr;
-  uint4 rr[8];
+  uint4 rr[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) rr[i] = make_uint4(0, 0, 0, 0);
+  for (int i = 0; i < 4; ++i) rr[i] = make_uint4(0, 0, 0, 0);
 
   for (;;) {
     if (fetch_slot(p, !active && !exhausted, exhausted, idx)) {
@@ -1239,7 +1239,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
       u = static_cast<uint32_t>(rng.below(p.n));
       if (recs) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) rr[i] = __ldg(p.ltrec + static_cast<size_t>(u) * 8 + i);
+        for (int i = 0; i < 4; ++i) rr[i] = __ldg(p.ltrec + static_cast<size_t>(u) * 4 + i);
       } else {
         nb = p.off[u];
         ne = p.off[u + 1];
@@ -1268,45 +1268,35 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
     bool picked = false;        // resolved from the vertex record alone
     if (recs && active) {
       const uint32_t deg = e - b;
+      const uint32_t dbits = __float_as_uint(__double2float_rd(d));  // d in [0, 1)
       const uint32_t* w = reinterpret_cast<const uint32_t*>(rr);
       if (deg <= kLtRecSmall) {  // whole list in the record: count entries <= d
-        uint32_t cnt = 0;
-#pragma unroll
-        for (uint32_t t = 0; t < kLtRecSmall; ++t) {
-          const double c = __longlong_as_double(
-              (static_cast<long long>(w[3 + 2 * t]) << 32) | w[2 + 2 * t]);
-          if (t < deg && c <= d) ++cnt;
-        }
+        const uint32_t cnt = lt_count_le<kLtRecSmall>(w + 2, dbits, d, p.cdf, b, 1);
 #pragma unroll
         for (uint32_t t = 0; t < kLtRecSmall; ++t)
-          if (t == cnt) vsel = w[18 + t];
+          if (t == cnt) vsel = w[8 + t];
         pick = b + cnt;
         ent += deg;
         picked = true;
-      } else {  // the root's 14 pivots, then the vertex's search-tree nodes
-        uint32_t below = 0;
-#pragma unroll
-        for (uint32_t t = 1; t <= kLtRootPivots; ++t) {
-          const double c = __longlong_as_double(
-              (static_cast<long long>(w[2 * t + 3]) << 32) | w[2 * t + 2]);
-          below += c <= d ? 1u : 0u;
-        }
-        ent += kLtRootPivots;
+      } else {  // the root's 13 pivots, then the vertex's search-tree nodes
         uint32_t lo = b, hi = e;
+        const uint32_t st0 = lt_step(lo, hi, kLtRootPivots);
+        const uint32_t below = lt_count_le<kLtRootPivots>(w + 3, dbits, d, p.cdf, lo + st0, st0);
+        ent += kLtRootPivots;
         lt_child(lo, hi, kLtRootPivots, below);
-        const uint64_t nbase = (static_cast<uint64_t>(w[3]) << 32) | w[2];
+        const uint32_t nbase = w[2];
         uint32_t x = 1 + below;
-        while (hi - lo > kLtRecSmall) {  // one 128-byte node per level
-          const double2* nd = reinterpret_cast<const double2*>(p.ltnodes + (nbase + x - 1) * 16);
-          double2 q[8];
+        while (hi - lo > kLtLeaf) {  // one 128-byte node (31 pivots) per level
+          const uint4* nd = reinterpret_cast<const uint4*>(p.ltnodes + (static_cast<size_t>(nbase) + x - 1) * 32);
+          uint4 q[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) q[i] = __ldg(nd + i);
-          uint32_t bl = 0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) bl += (q[i].x <= d ? 1u : 0u) + (q[i].y <= d ? 1u : 0u);
+          const uint32_t st = lt_step(lo, hi, kLtNodePivots);
+          const uint32_t bl = lt_count_le<kLtNodePivots>(reinterpret_cast<const uint32_t*>(q),
+                                                         dbits, d, p.cdf, lo + st, st);
           ent += kLtNodePivots;
           lt_child(lo, hi, kLtNodePivots, bl);
-          x = 16 * x + 1 + bl;
+          x = kLtFanout * x + 1 + bl;
         }
         slo = lo;
         shi = hi;
@@ -1403,7 +1393,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
       v = (linear || coop) ? p.src[pick] : vsel;
       if (recs) {  // next step's record, in flight with the visited probe
 #pragma unroll
-        for (int i = 0; i < 8; ++i) rr[i] = __ldg(p.ltrec + static_cast<size_t>(v) * 8 + i);
+        for (int i = 0; i < 4; ++i) rr[i] = __ldg(p.ltrec + static_cast<size_t>(v) * 4 + i);
       } else {
         nb = p.off[v];  // next step's list, in flight with the visited probe
         ne = p.off[v + 1];
@@ -1733,58 +1723,55 @@ __global__ void k_offsets_u32(const uint64_t* off64, uint32_t* off32, uint32_t n
   }
 }
 
-// LT vertex record (128 B, one line): in-list start and degree, then for
-// degree <= 8 the whole CDF and the sources, else the first slot of the
-// vertex's search-tree nodes (u64) and the root's 14 pivots. One load per walk
-// step replaces the offsets load and the first search level.
+// LT vertex record (64 B): in-list start and degree, then for degree <= 6 the
+// whole CDF (floats rounded down) and the sources, else the first slot of the
+// vertex's search-tree nodes and the root's 13 pivots. One load per walk step
+// replaces the offsets load and the first search level.
+__device__ __forceinline__ uint32_t lt_fdown(double x) { return __float_as_uint(__double2float_rd(x)); }
+constexpr uint32_t kLtSentinel = 0x40000000u;  // 2.0f: never <= a draw in [0, 1)
+
 __global__ void k_build_ltrec(const uint32_t* off, const double* cdf, const uint32_t* src,
                               const uint64_t* nodeoff, uint32_t n, uint32_t* rec) {
   const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n) return;
   const uint32_t b = off[u], deg = off[u + 1] - b;
-  uint32_t w[32];
+  uint32_t w[16];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) w[i] = 0;
+  for (int i = 0; i < 16; ++i) w[i] = 0;
   w[0] = b;
   w[1] = deg;
   if (deg <= kLtRecSmall) {
-    for (uint32_t t = 0; t < deg; ++t) {
-      const unsigned long long x = __double_as_longlong(cdf[b + t]);
-      w[2 + 2 * t] = static_cast<uint32_t>(x);
-      w[3 + 2 * t] = static_cast<uint32_t>(x >> 32);
-      w[18 + t] = src[b + t];
+    for (uint32_t t = 0; t < kLtRecSmall; ++t) {
+      w[2 + t] = t < deg ? lt_fdown(cdf[b + t]) : kLtSentinel;
+      w[8 + t] = t < deg ? src[b + t] : 0u;
     }
   } else {
     w[2] = static_cast<uint32_t>(nodeoff[u]);
-    w[3] = static_cast<uint32_t>(nodeoff[u] >> 32);
     const uint32_t step = lt_step(0, deg, kLtRootPivots);
     for (uint32_t t = 1; t <= kLtRootPivots; ++t) {
       const uint32_t i = t * step;
-      const double v = i < deg ? cdf[b + i] : 2.0;  // past the list: never <= a draw
-      const unsigned long long x = __double_as_longlong(v);
-      w[2 + 2 * t] = static_cast<uint32_t>(x);
-      w[3 + 2 * t] = static_cast<uint32_t>(x >> 32);
+      w[2 + t] = i < deg ? lt_fdown(cdf[b + i]) : kLtSentinel;
     }
   }
-  uint4* out = reinterpret_cast<uint4*>(rec + static_cast<size_t>(u) * 32);
+  uint4* out = reinterpret_cast<uint4*>(rec + static_cast<size_t>(u) * 16);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) out[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+  for (int i = 0; i < 4; ++i) out[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
 }
 
-// Node slots of a vertex's search tree: 16^k per level k >= 1 while the
-// child ranges of the level above (<= the step) still exceed kLtRecSmall.
+// Node slots of a vertex's search tree: 32^k per level k >= 1 while the
+// child ranges of the level above (<= the step) still exceed kLtLeaf.
 __global__ void k_count_ltnodes(const uint32_t* off, uint32_t n, uint32_t* cnt) {
   const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n) return;
   uint32_t len = off[u + 1] - off[u];
-  uint64_t slots = 0, width = 16;
+  uint64_t slots = 0, width = kLtFanout;
   uint32_t P = kLtRootPivots;
   if (len > kLtRecSmall) {
     for (;;) {
       const uint32_t cl = lt_step(0, len, P);  // longest child range
-      if (cl <= kLtRecSmall) break;
+      if (cl <= kLtLeaf) break;
       slots += width;
-      width *= 16;
+      width *= kLtFanout;
       len = cl;
       P = kLtNodePivots;
     }
@@ -1793,37 +1780,38 @@ __global__ void k_count_ltnodes(const uint32_t* off, uint32_t n, uint32_t* cnt) 
 }
 
 // One block per vertex: slot s (node x = s + 1) follows its path from the root
-// and stores its 15 pivots (unreachable slots: sentinels).
+// and stores its 31 pivots (unreachable slots: sentinels).
 __global__ void k_build_ltnodes(const uint32_t* off, const double* cdf, const uint64_t* nodeoff,
-                                uint32_t n, double* nodes) {
+                                uint32_t n, uint32_t* nodes) {
   for (uint32_t u = blockIdx.x; u < n; u += gridDim.x) {
     const uint64_t base = nodeoff[u];
     const uint32_t cnt = static_cast<uint32_t>(nodeoff[u + 1] - base);
     if (!cnt) continue;
     const uint32_t b = off[u], e = off[u + 1];
     for (uint32_t s = threadIdx.x; s < cnt; s += blockDim.x) {
-      uint32_t dig[12];
+      uint32_t dig[8];
       int nd = 0;
-      for (uint32_t x = s + 1; x; x = (x - 1) / 16) dig[nd++] = (x - 1) % 16;
+      for (uint32_t x = s + 1; x; x = (x - 1) / kLtFanout) dig[nd++] = (x - 1) % kLtFanout;
       uint32_t lo = b, hi = e;
       bool ok = true;
       for (int k = nd - 1; k >= 0 && ok; --k) {
         const uint32_t P = k == nd - 1 ? kLtRootPivots : kLtNodePivots;
-        if (dig[k] > P || hi - lo <= kLtRecSmall) {
+        const uint32_t lim = k == nd - 1 ? kLtRecSmall : kLtLeaf;  // the parent must narrow
+        if (dig[k] > P || hi - lo <= lim) {
           ok = false;
           break;
         }
         lt_child(lo, hi, P, dig[k]);
         if (lo > hi) ok = false;
       }
-      ok = ok && hi - lo > kLtRecSmall;
-      double* out = nodes + (base + s) * 16;
+      ok = ok && hi - lo > kLtLeaf;
+      uint32_t* out = nodes + (base + s) * 32;
       const uint32_t st = ok ? lt_step(lo, hi, kLtNodePivots) : 1u;
       for (uint32_t t = 1; t <= kLtNodePivots; ++t) {
         const uint32_t i = lo + t * st;
-        out[t - 1] = ok && i < hi ? cdf[i] : 2.0;
+        out[t - 1] = ok && i < hi ? lt_fdown(cdf[i]) : kLtSentinel;
       }
-      out[15] = 2.0;
+      out[31] = kLtSentinel;
     }
   }
 }
@@ -1977,14 +1965,20 @@ void prepare_lt(rrg_graph* g) {
     RRG_CUDA(cudaMemcpyAsync(&slots, g->ltnodeoff.ptr + g->n, 8, cudaMemcpyDeviceToHost,
                              g->stream));
     RRG_CUDA(cudaStreamSynchronize(g->stream));
-    g->ltnodes.reserve_discard(slots ? slots * 16 : 16);
+    if (slots >= (1ull << 32)) {  // node slots are u32 in the records: use the plain search
+      g->ltrec.release();
+      g->ltnodes.release();
+      g->cdf_ready = true;
+      return;
+    }
+    g->ltnodes.reserve_discard(slots ? slots * 32 : 32);
     if (slots) {
       k_build_ltnodes<<<std::min<uint32_t>(g->n, 65535u * 4), 128, 0, g->stream>>>(
           g->off.ptr, g->cdf.ptr, g->ltnodeoff.ptr, g->n, g->ltnodes.ptr);
       RRG_CUDA(cudaGetLastError());
       count_launch();
     }
-    g->ltrec.reserve_discard(static_cast<size_t>(g->n) * 32);
+    g->ltrec.reserve_discard(static_cast<size_t>(g->n) * 16);
     k_build_ltrec<<<(g->n + 255) / 256, 256, 0, g->stream>>>(
         g->off.ptr, g->cdf.ptr, g->src.ptr, g->ltnodeoff.ptr, g->n, g->ltrec.ptr);
     RRG_CUDA(cudaGetLastError());
