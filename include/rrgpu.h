@@ -217,6 +217,8 @@ uint64_t rrg_launch_count(void);
 /* Test hook: the integer Bernoulli threshold used by the IC kernel
  * (uniform01() < (double)w  <=>  (next_u64() >> 11) < threshold(w)). */
 uint64_t rrg_debug_bernoulli_threshold(uint32_t weight_bits);
+/* The 32-bit threshold stored in IC edge records: T >> 21, saturated at 2^32-1. */
+uint32_t rrg_debug_bernoulli_thr_hi(uint32_t weight_bits);
 /* Test hook: advances a xoshiro256** state (4 words) by k draws with the GF(2)
  * jump matrices the IC hub expansion uses (csrc/jump.cpp). */
 void rrg_debug_jump(const uint64_t* state_in, uint64_t k, uint64_t* state_out);

@@ -114,6 +114,7 @@ SIGNATURES = [
     ("rrg_last_error", C.c_char_p, []),
     ("rrg_version", C.c_char_p, []),
     ("rrg_debug_bernoulli_threshold", C.c_uint64, [C.c_uint32]),
+    ("rrg_debug_bernoulli_thr_hi", C.c_uint32, [C.c_uint32]),
     ("rrg_debug_jump", None, [u64p, C.c_uint64, u64p]),
 ]
 

@@ -201,6 +201,7 @@ const char* rrg_last_error(void) { return rrgpu::t_err.c_str(); }
 uint64_t rrg_launch_count(void) { return rrgpu::launches(); }
 const char* rrg_version(void) { return "rrgpu 0.1.0 (sm_100a; reference rrflow 0.1.0)"; }
 uint64_t rrg_debug_bernoulli_threshold(uint32_t bits) { return bernoulli_threshold(bits); }
+uint32_t rrg_debug_bernoulli_thr_hi(uint32_t bits) { return bern_thr_hi(bits); }
 
 rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* roff, const uint32_t* rsrc,
                             const float* rw, rrg_graph** out) {
@@ -456,6 +457,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.off = g->off.ptr;
       p.rec = g->rec.ptr;
       p.src = g->src.ptr;
+      p.w = g->w.ptr;
       p.cdf = g->cdf.ptr;
       p.ltrec = reinterpret_cast<const uint4*>(g->ltrec.ptr);
       p.ltnodes = g->ltnodes.ptr;

@@ -97,6 +97,18 @@ __host__ __device__ __forceinline__ uint64_t bernoulli_threshold(uint32_t bits) 
   return ((mant - 1) >> rs) + 1;                       // ceil(mant / 2^rs)
 }
 
+// IC edge records carry T_hi = T >> 21 of T = ceil(w 2^53) (saturated at
+// 2^32 - 1) instead of the weight: with k = x >> 11, x >> 32 = k >> 21, so
+// x >> 32 < T_hi accepts and x >> 32 > T_hi rejects exactly; a tie
+// (probability 2^-32) is settled from the f32 weight (bern_tie).
+__host__ __device__ __forceinline__ uint32_t bern_thr_hi(uint32_t wbits) {
+  const uint64_t hi = bernoulli_threshold(wbits) >> 21;
+  return hi >= 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(hi);
+}
+__device__ __forceinline__ bool bern_tie(uint64_t x, const float* w, uint32_t j) {
+  return (x >> 11) < bernoulli_threshold(__float_as_uint(__ldg(w + j)));
+}
+
 // ---------------------------------------------------------------------------
 // Per-lane visited set: open addressing over u64 entries (tag << 32 | vertex).
 // An entry is live only while its tag equals the lane's current tag, so a new

@@ -179,6 +179,7 @@ struct SampleParams {
   const uint32_t* off;
   const uint2* rec;
   const uint32_t* src;
+  const float* w;        // IC: f32 weights (Bernoulli ties, big-set path)
   const double* cdf;
   const uint4* ltrec;    // LT vertex records (search mode), 4 x uint4 per vertex
   const uint32_t* ltnodes;  // LT search-tree nodes (32 floats each)

@@ -167,6 +167,17 @@ __device__ __forceinline__ void sfilt_add(uint32_t* sf, uint32_t v) {
   atomicOr(sf + (b >> 5), 1u << (b & 31));
 }
 
+// In-edge index of window position e: last list t with lpre[t] <= e (lists
+// past the window carry lpre >= the window size). Only the rare Bernoulli tie
+// needs it.
+__device__ __noinline__ uint32_t win_edge(const uint32_t* lstart, const uint32_t* lpre,
+                                          uint32_t nlists, uint32_t e) {
+  uint32_t t = 0;
+  for (uint32_t step = nlists / 2; step; step >>= 1)
+    if (t + step < nlists && lpre[t + step] <= e) t += step;
+  return lstart[t] + (e - lpre[t]);
+}
+
 template <int kVis>
 __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uint32_t* mem,
                             uint64_t* tab, uint32_t* vis, CoopState& s, CoopSmem& sm,
@@ -238,7 +249,9 @@ __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uin
         }
         const int bit = __ffs(m) - 1;
         m &= m - 1;
-        if (st.u53() < bernoulli_threshold(sm.thr[32 * c + bit])) acc |= 1u << bit;
+        const uint64_t x = st.next();
+        const uint32_t kh = static_cast<uint32_t>(x >> 32), th = sm.thr[32 * c + bit];
+        if (kh < th || (kh == th && bern_tie(x, p.w, wb + 32 * c + bit))) acc |= 1u << bit;
         ++done;
       }
       if (acc) atomicOr(&sm.acc[c], acc);
@@ -389,7 +402,9 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS)
         const uint2 r = p.rec[j];
         const uint32_t v = r.x;
         if (flt.maybe(v) && tab_contains(tab, tag, lg, v)) continue;  // visited: no draw
-        if (rng.u53() < bernoulli_threshold(r.y)) {
+        const uint64_t x = rng.next();
+        const uint32_t kh = static_cast<uint32_t>(x >> 32);
+        if (kh < r.y || (kh == r.y && bern_tie(x, p.w, j))) {
           if (nmem == kMemCap) {
             defer_slot(p, idx);
             active = false;
@@ -647,7 +662,10 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
             }
             const int bit = __ffs(m) - 1;
             m &= m - 1;
-            if (st.u53() < bernoulli_threshold(ws.thr[32 * c + bit])) acc |= 1u << bit;
+            const uint64_t x = st.next();
+            const uint32_t kh = static_cast<uint32_t>(x >> 32), th = ws.thr[32 * c + bit];
+            if (kh < th || (kh == th && bern_tie(x, p.w, win_edge(ws.lstart, ws.lpre, 32, 32 * c + bit))))
+              acc |= 1u << bit;
             ++done;
           }
           if (acc) atomicOr(&ws.acc[c], acc);
@@ -1039,7 +1057,11 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               }
               const int bit = __ffs(m) - 1;
               m &= m - 1;
-              if (st.u53() < bernoulli_threshold(ws.thr[32 * c + bit])) acc |= 1u << bit;
+              const uint64_t x = st.next();
+              const uint32_t kh = static_cast<uint32_t>(x >> 32), th = ws.thr[32 * c + bit];
+              if (kh < th ||
+                  (kh == th && bern_tie(x, p.w, win_edge(cs.lstart, cs.lpre, kBlock, wbase + 32 * c + bit))))
+                acc |= 1u << bit;
               ++done;
             }
             if (acc) atomicOr(&ws.acc[c], acc);
@@ -1478,7 +1500,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
           const unsigned peers = __match_any_sync(kFull, r.x);
           const bool dup = valid && (peers & lanemask_lt()) != 0;
           const unsigned um = __ballot_sync(kFull, unv);
-          s_thr[wl][lane] = bernoulli_threshold(r.y);
+          s_thr[wl][lane] = valid ? bernoulli_threshold(__float_as_uint(__ldg(p.w + j))) : 0ull;
           s_src[wl][lane] = r.x;
           __syncwarp();
           unsigned acc = 0;
@@ -1577,7 +1599,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
 __global__ void k_build_rec(const uint32_t* src, const float* w, uint2* rec, uint64_t m) {
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    rec[j] = make_uint2(src[j], __float_as_uint(w[j]));
+    rec[j] = make_uint2(src[j], bern_thr_hi(__float_as_uint(w[j])));
   }
 }
 

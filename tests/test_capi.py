@@ -66,6 +66,28 @@ def test_bernoulli_threshold_equals_double_compare():
             assert (k < t) == expect, (w, k, t)
 
 
+def test_record_threshold_high_word_decides_like_the_double_compare():
+    """IC records keep T >> 21: x >> 32 < T_hi accepts, > rejects, a tie falls back to
+    the full threshold -- identical to uniform01() < (double)w for every x."""
+    from paper_2411_09473_b200._lib import lib
+    rng = np.random.default_rng(2)
+    weights = list(rng.random(200).astype(np.float32)) + [
+        0.0, 1.0, 1.5, 1e-45, 2.0 ** -24, 2.0 ** -53, float("inf"), -1.0, float("nan"),
+        np.float32(1 / 3), np.nextafter(np.float32(1.0), np.float32(0.0))]
+    for w in weights:
+        bits = f32_bits(float(np.float32(w)))
+        t = lib.rrg_debug_bernoulli_threshold(bits)
+        th = lib.rrg_debug_bernoulli_thr_hi(bits)
+        xs = [int(x) for x in rng.integers(0, 2**63, 8, dtype=np.uint64)] + [0, 2**64 - 1]
+        xs += [(th << 32) | int(lo) for lo in rng.integers(0, 2**32, 8)]  # ties
+        xs += [(th << 32), (th << 32) | 0xFFFFFFFF]
+        for x in xs:
+            x &= 2**64 - 1
+            kh, k = x >> 32, x >> 11
+            got = kh < th or (kh == th and k < t)
+            assert got == ((k * 2.0 ** -53) < float(np.float32(w))), (w, hex(x))
+
+
 def test_jump_ahead_matches_sequential_draws(port):
     """T^k s == k calls of next_u64 (prng.hpp:33-43) for the GF(2) jump matrices."""
     import ctypes as C
