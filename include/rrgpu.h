@@ -173,6 +173,13 @@ rrg_status rrg_store_append_from(rrg_store* dst, const rrg_store* src, uint64_t 
                                  uint64_t count);
 /* Fused occurrence counter as u64[n] (Counter::get, counter.hpp:29). */
 rrg_status rrg_store_counter(const rrg_store* s, uint64_t* counts);
+/* Enqueues, on `stream` (a cudaStream_t), the device-to-host copies of the whole
+ * store: offsets u64[nsets+1], members u32[total] and, if `counts` is non-null, the
+ * counter as u64[n]; returns without waiting. Host buffers should be pinned. The
+ * store must not be modified or destroyed until `stream` has completed. Lets a
+ * caller overlap one batch's export with the next batch's sampling. */
+rrg_status rrg_store_export_all_async(const rrg_store* s, uint64_t* offsets, uint32_t* members,
+                                      uint64_t* counts, void* stream);
 
 /* ---- host-side graph preparation (plumbing that feeds both sides) ---------- */
 /* detail::build_graph (graph.hpp:69-115): transpose of an edge list in the

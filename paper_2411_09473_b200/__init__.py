@@ -206,6 +206,20 @@ class RRRStore:
                                    ptr(members, C.c_uint32)))
         return total
 
+    def export_all_async(self, offsets: np.ndarray, members: np.ndarray,
+                         counts: Optional[np.ndarray], stream: int) -> int:
+        """Enqueues the D2H copies of the whole store (offsets, members, counter) on
+        the CUDA stream handle `stream` and returns the member count without
+        waiting; synchronize the stream before reading the buffers or touching
+        the store again."""
+        total = self.total_member_count()
+        if offsets.size < self.size() + 1 or members.size < total:
+            raise ValueError("export buffers too small")
+        check(lib.rrg_store_export_all_async(
+            self._h, ptr(offsets, C.c_uint64), ptr(members, C.c_uint32),
+            ptr(counts, C.c_uint64) if counts is not None else None, C.c_void_p(stream)))
+        return total
+
     def counter_into(self, out: np.ndarray) -> np.ndarray:
         check(lib.rrg_store_counter(self._h, ptr(out, C.c_uint64)))
         return out

@@ -802,6 +802,31 @@ rrg_status rrg_store_import(rrg_store* s, uint64_t count, const uint64_t* offset
   });
 }
 
+rrg_status rrg_store_export_all_async(const rrg_store* s, uint64_t* offsets, uint32_t* members,
+                                      uint64_t* counts, void* stream) {
+  if (!s || !offsets || (s->total && !members)) return invalid("null argument");
+  return guarded([&]() -> rrg_status {
+    rrg_graph* g = s->g;
+    const cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    auto* ms = const_cast<rrg_store*>(s);  // scratch only; the store's sets are unchanged
+    // the copies follow everything already enqueued on the graph's stream
+    RRG_CUDA(cudaEventRecord(g->ev1, g->stream));
+    RRG_CUDA(cudaStreamWaitEvent(cs, g->ev1, 0));
+    RRG_CUDA(cudaMemcpyAsync(offsets, s->off.ptr, (s->nsets + 1) * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, cs));
+    if (s->total)
+      RRG_CUDA(cudaMemcpyAsync(members, s->mem.ptr, s->total * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, cs));
+    if (counts && g->n) {
+      ms->wide.reserve_discard(g->n);
+      launch_widen(s->counter.ptr, ms->wide.ptr, g->n, cs);
+      RRG_CUDA(cudaMemcpyAsync(counts, ms->wide.ptr, g->n * sizeof(uint64_t),
+                               cudaMemcpyDeviceToHost, cs));
+    }
+    return RRG_OK;
+  });
+}
+
 rrg_status rrg_store_counter(const rrg_store* s, uint64_t* counts) {
   if (!s || !counts) return invalid("null argument");
   return guarded([&]() -> rrg_status {

@@ -117,6 +117,23 @@ def test_append_from_side_store_equals_direct_top_up(cuda):
     assert direct.max_set_size() == main.max_set_size()
 
 
+def test_export_all_async_equals_sync_export(cuda):
+    """The pipelined export (copy stream) returns exactly export() + counter()."""
+    import torch
+    cfg = graphs.scaled(graphs.CONFIGS["cfg2"], 1 << 11, 1 << 15)
+    g = P.Graph(*graphs.generate(cfg))
+    st = P.RRRStore(g)
+    P.generate_batch(g, LT, 5, 3000, st)
+    off, mem = st.export()
+    o = torch.empty(st.size() + 1, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    m = torch.empty(st.total_member_count(), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+    c = torch.empty(g.num_vertices, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    s = torch.cuda.Stream()
+    assert st.export_all_async(o, m, c, s.cuda_stream) == mem.size
+    s.synchronize()
+    assert (o == off).all() and (m == mem).all() and (c == st.counter()).all()
+
+
 @pytest.mark.parametrize("coop_min", [2, 7, 64, 1 << 30])
 def test_lt_cooperative_scan_threshold_changes_nothing(cuda, oracle, coop_min):
     cfg = graphs.scaled(graphs.CONFIGS["cfg2"], 1 << 10, 1 << 14)
