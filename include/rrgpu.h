@@ -137,7 +137,13 @@ typedef struct {
   uint64_t rng_seed;          /* 1 */
   double ell;                 /* 1.0 */
   double adaptive_threshold;  /* 0.25 */
+  int strategy;               /* RRG_STRATEGY_FUSED (Strategy::fused, imm.hpp:33); BASELINE =
+                                 unfused sampling + recount before each selection: the
+                                 reference's baseline_select returns the same seeds and
+                                 marginals (test_selection.cpp:188-200), so the device
+                                 runs its one selection on both */
 } rrg_imm_config;
+enum { RRG_STRATEGY_FUSED = 0, RRG_STRATEGY_BASELINE = 1 };
 
 typedef struct {
   uint64_t theta;
@@ -156,6 +162,14 @@ void rrg_imm_config_default(rrg_imm_config* cfg);
 /* seeds u32[k], marginals u64[k] */
 rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
                        uint64_t* marginals, rrg_imm_result* out);
+/* sampling_phase (imm.hpp:169-209): rounds of top-ups + trial selections into
+ * `store` (cleared first) until the estimate certifies the round target.
+ * Outputs SamplingPhaseResult's lower_bound and theta_prime (= store size; the
+ * store's counter is the phase's fused Counter); `timings` (nullable) receives
+ * t_generate / t_select. */
+rrg_status rrg_sampling_phase(rrg_graph* g, const rrg_imm_config* cfg, rrg_store* store,
+                              double* lower_bound, uint64_t* theta_prime,
+                              rrg_imm_result* timings);
 
 /* ---- parity / interop --------------------------------------------------- */
 /* Copies sets [first, first+count) to the host: offsets u64[count+1] (relative to

@@ -151,6 +151,14 @@ inline double fraction_covered(RRRStore& store, const std::vector<uint32_t>& see
   return f;
 }
 
+// imm.hpp:15-24
+enum class Strategy { fused, baseline };
+inline Strategy parse_strategy(const std::string& s) {
+  if (s == "fused") return Strategy::fused;
+  if (s == "baseline") return Strategy::baseline;
+  throw std::invalid_argument("unknown strategy: " + s);
+}
+
 // imm.hpp:27-54
 struct ImmConfig {
   uint32_t k = 50;
@@ -160,6 +168,7 @@ struct ImmConfig {
   uint64_t rng_seed = 1;
   double ell = 1.0;
   double adaptive_threshold = 0.25;
+  Strategy strategy = Strategy::fused;
 };
 
 struct ImmTimings {
@@ -180,8 +189,7 @@ struct ImmResult {
   double mean_coverage_fraction = 0.0;
 };
 
-// imm.hpp:214-251
-inline ImmResult run_imm(const Graph& g, const ImmConfig& cfg) {
+inline rrg_imm_config to_c(const ImmConfig& cfg) {
   rrg_imm_config c;
   rrg_imm_config_default(&c);
   c.k = cfg.k;
@@ -191,6 +199,35 @@ inline ImmResult run_imm(const Graph& g, const ImmConfig& cfg) {
   c.rng_seed = cfg.rng_seed;
   c.ell = cfg.ell;
   c.adaptive_threshold = cfg.adaptive_threshold;
+  c.strategy = cfg.strategy == Strategy::fused ? RRG_STRATEGY_FUSED : RRG_STRATEGY_BASELINE;
+  return c;
+}
+
+// imm.hpp:157-162 (the store's fused counter is the phase's Counter)
+struct SamplingPhaseResult {
+  RRRStore store;
+  double lower_bound = 0.0;
+  uint64_t theta_prime = 0;
+};
+
+// imm.hpp:169-209
+inline SamplingPhaseResult sampling_phase(const Graph& g, const ImmConfig& cfg,
+                                          ImmTimings* timings = nullptr) {
+  const rrg_imm_config c = to_c(cfg);
+  SamplingPhaseResult out{RRRStore(g)};
+  rrg_imm_result t{};
+  check(rrg_sampling_phase(g.handle(), &c, out.store.handle(), &out.lower_bound,
+                           &out.theta_prime, &t));
+  if (timings) {
+    timings->generate_rrrsets += t.t_generate;
+    timings->find_most_influential += t.t_select;
+  }
+  return out;
+}
+
+// imm.hpp:214-251
+inline ImmResult run_imm(const Graph& g, const ImmConfig& cfg) {
+  const rrg_imm_config c = to_c(cfg);
   ImmResult r;
   const uint32_t k = cfg.k ? cfg.k : 1;
   r.seeds.seeds.resize(k);

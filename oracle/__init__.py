@@ -30,7 +30,7 @@ vp = C.c_void_p
 class ImmConfigC(C.Structure):
     _fields_ = [("k", C.c_uint32), ("epsilon", C.c_double), ("model", C.c_int),
                 ("workers", C.c_uint32), ("rng_seed", C.c_uint64), ("ell", C.c_double),
-                ("adaptive_threshold", C.c_double)]
+                ("adaptive_threshold", C.c_double), ("strategy", C.c_int)]
 
 
 class ImmResultC(C.Structure):
@@ -59,6 +59,7 @@ _SIG = [
     ("orc_select", C.c_int, [C.c_uint32, C.c_uint64, u64p, u32p, C.c_uint32, C.c_double,
                              C.c_uint32, u32p, u64p, u64p, u32p]),
     ("orc_imm", C.c_int, [vp, C.POINTER(ImmConfigC), u32p, u64p, C.POINTER(ImmResultC)]),
+    ("orc_sampling_phase", C.c_int, [vp, C.POINTER(ImmConfigC), C.POINTER(C.c_double), u64p, u64p]),
     ("orc_log_binomial", C.c_double, [C.c_uint64, C.c_uint64]),
     ("orc_effective_ell", C.c_double, [C.c_double, C.c_uint64]),
     ("orc_lambda_prime", C.c_double, [C.c_uint64, C.c_uint64, C.c_double, C.c_double]),
@@ -245,9 +246,20 @@ class OracleGraph:
             lib.orc_store_free(st)
         return Sketches(off, mem, roots, cnt, insp)
 
+    def sampling_phase(self, k=50, epsilon=0.5, model=0, workers=1, rng_seed=1, ell=1.0,
+                       adaptive_threshold=0.25, strategy=0):
+        cfg = ImmConfigC(k, epsilon, model, workers, rng_seed, ell, adaptive_threshold, strategy)
+        lb = C.c_double()
+        tp = np.zeros(1, np.uint64)
+        cnt = np.zeros(self.n, np.uint64)
+        if self.orc.lib.orc_sampling_phase(self.h, C.byref(cfg), C.byref(lb), _p(tp, C.c_uint64),
+                                           _p(cnt, C.c_uint64)):
+            raise ValueError(self.orc.err())
+        return {"lower_bound": lb.value, "theta_prime": int(tp[0]), "counter": cnt}
+
     def imm(self, k=50, epsilon=0.5, model=0, workers=1, rng_seed=1, ell=1.0,
-            adaptive_threshold=0.25):
-        cfg = ImmConfigC(k, epsilon, model, workers, rng_seed, ell, adaptive_threshold)
+            adaptive_threshold=0.25, strategy=0):
+        cfg = ImmConfigC(k, epsilon, model, workers, rng_seed, ell, adaptive_threshold, strategy)
         seeds = np.zeros(max(k, 1), np.uint32)
         marg = np.zeros(max(k, 1), np.uint64)
         res = ImmResultC()

@@ -35,6 +35,7 @@ typedef struct {
   uint64_t rng_seed;
   double ell;
   double adaptive_threshold;
+  int strategy; /* 0 = fused, 1 = baseline (imm.hpp:15-24) */
 } orc_imm_config;
 
 typedef struct {
@@ -85,6 +86,10 @@ int orc_select(uint32_t n, uint64_t nsets, const uint64_t* offsets, const uint32
 /* run_imm (imm.hpp:214-251). seeds u32[k], marginals u64[k]. */
 int orc_imm(orc_graph* g, const orc_imm_config* cfg, uint32_t* seeds, uint64_t* marginals,
             orc_imm_result* out);
+/* sampling_phase (imm.hpp:169-209): lower_bound, theta_prime and the phase's
+ * counter u64[n] (zeros under the baseline strategy, which samples unfused) */
+int orc_sampling_phase(orc_graph* g, const orc_imm_config* cfg, double* lower_bound,
+                       uint64_t* theta_prime, uint64_t* counter);
 
 /* theta math (imm.hpp:57-120) */
 double orc_log_binomial(uint64_t n, uint64_t k);

@@ -355,6 +355,55 @@ uint64_t orc_set_theta(uint64_t n, uint64_t k, double eps, double ell, double lb
   return static_cast<uint64_t>(t);
 }
 
+// sampling_phase (imm.hpp:169-209) alone: the same rounds as orc_imm below.
+int orc_sampling_phase(orc_graph* g, const orc_imm_config* cfg, double* lower_bound,
+                       uint64_t* theta_prime, uint64_t* counter) {
+  const uint32_t n = g->n;
+  if (n == 0 || !(cfg->epsilon > 0.0 && cfg->epsilon < 1.0) || cfg->k < 1 || cfg->k > n ||
+      cfg->workers < 1) {
+    g_err = "invalid configuration";  // imm.hpp:136-145
+    return -1;
+  }
+  const double ell = orc_effective_ell(cfg->ell, n);
+  const double eps_prime = std::sqrt(2.0) * cfg->epsilon;
+  std::vector<uint64_t> off{0};
+  std::vector<uint32_t> mem;
+  std::vector<uint32_t> sd(cfg->k);
+  std::vector<uint64_t> mg(cfg->k);
+  const uint32_t rounds = orc_sampling_rounds(n);
+  double spread = 0.0;
+  bool triggered = false;
+  for (uint32_t i = 1; i <= rounds; ++i) {
+    const uint64_t target = orc_theta_for_round(n, cfg->k, cfg->epsilon, ell, i);
+    const uint64_t have = off.size() - 1;
+    if (target > have) {
+      orc_store* st = orc_sample(g, cfg->model, cfg->rng_seed, have, target - have, cfg->workers);
+      for (uint64_t s = 0; s < target - have; ++s)
+        off.push_back(off.back() + (st->off[s + 1] - st->off[s]));
+      mem.insert(mem.end(), st->mem.begin(), st->mem.end());
+      orc_store_free(st);
+    }
+    orc_select(n, off.size() - 1, off.data(), mem.data(), cfg->k, cfg->adaptive_threshold, 1,
+               sd.data(), mg.data(), nullptr, nullptr);
+    uint64_t covered = 0;
+    for (uint32_t r = 0; r < cfg->k; ++r) covered += mg[r];
+    spread = static_cast<double>(n) * (static_cast<double>(covered) / static_cast<double>(off.size() - 1));
+    if (spread >= (1.0 + eps_prime) * round_target(n, i)) {
+      triggered = true;
+      break;
+    }
+  }
+  *lower_bound = triggered ? spread / (1.0 + eps_prime)
+                           : std::max(spread / (1.0 + eps_prime), static_cast<double>(cfg->k));
+  *theta_prime = off.size() - 1;
+  if (counter) {
+    std::fill(counter, counter + n, 0);
+    if (!cfg->strategy)  // the fused strategy's counter; baseline samples unfused
+      for (uint32_t v : mem) ++counter[v];
+  }
+  return 0;
+}
+
 // run_imm (imm.hpp:214-251) with sampling_phase (imm.hpp:169-209).
 int orc_imm(orc_graph* g, const orc_imm_config* cfg, uint32_t* seeds, uint64_t* marginals,
             orc_imm_result* out) {

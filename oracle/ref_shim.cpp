@@ -210,6 +210,7 @@ int orc_imm(orc_graph* h, const orc_imm_config* c, uint32_t* seeds, uint64_t* ma
     cfg.rng_seed = c->rng_seed;
     cfg.ell = c->ell;
     cfg.adaptive_threshold = c->adaptive_threshold;
+    cfg.strategy = c->strategy ? rrflow::Strategy::baseline : rrflow::Strategy::fused;
     const rrflow::ImmResult r = rrflow::run_imm(h->g, cfg);
     for (size_t i = 0; i < r.seeds.seeds.size(); ++i) {
       seeds[i] = r.seeds.seeds[i];
@@ -225,6 +226,31 @@ int orc_imm(orc_graph* h, const orc_imm_config* c, uint32_t* seeds, uint64_t* ma
     out->t_generate = r.timings.generate_rrrsets;
     out->t_select = r.timings.find_most_influential;
     out->t_total = r.timings.total;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int orc_sampling_phase(orc_graph* h, const orc_imm_config* c, double* lower_bound,
+                       uint64_t* theta_prime, uint64_t* counter) {
+  try {
+    rrflow::ImmConfig cfg;
+    cfg.k = c->k;
+    cfg.epsilon = c->epsilon;
+    cfg.model = to_model(c->model);
+    cfg.workers = c->workers;
+    cfg.rng_seed = c->rng_seed;
+    cfg.ell = c->ell;
+    cfg.adaptive_threshold = c->adaptive_threshold;
+    cfg.strategy = c->strategy ? rrflow::Strategy::baseline : rrflow::Strategy::fused;
+    rrflow::WorkPool pool(std::max<uint32_t>(1, c->workers));
+    const rrflow::SamplingPhaseResult r = rrflow::sampling_phase(h->g, cfg, pool);
+    *lower_bound = r.lower_bound;
+    *theta_prime = r.theta_prime;
+    if (counter)
+      for (uint32_t v = 0; v < h->g.num_vertices; ++v) counter[v] = r.counter.get(v);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -340,6 +340,20 @@ class ImmConfig:
     rng_seed: int = 1
     ell: float = 1.0
     adaptive_threshold: float = 0.25
+    strategy: int = 0  # Strategy::fused (imm.hpp:33); 1 = baseline (same seeds, unfused)
+
+
+class Strategy:
+    FUSED, BASELINE = 0, 1
+
+
+def parse_strategy(s: str) -> int:
+    """parse_strategy (imm.hpp:20-24)."""
+    if s == "fused":
+        return Strategy.FUSED
+    if s == "baseline":
+        return Strategy.BASELINE
+    raise ValueError("unknown strategy: " + s)
 
 
 @dataclass
@@ -356,11 +370,38 @@ class ImmResult:
     mean_coverage_fraction: float
 
 
+def _imm_config(cfg: ImmConfig):
+    return _lib.ImmConfigC(int(cfg.k), float(cfg.epsilon), _model(cfg.model), int(cfg.workers),
+                           int(cfg.rng_seed) & (2**64 - 1), float(cfg.ell),
+                           float(cfg.adaptive_threshold), int(cfg.strategy))
+
+
+@dataclass
+class SamplingPhaseResult:
+    """imm.hpp:157-162: the store (its fused counter is the phase's Counter)."""
+    store: RRRStore
+    lower_bound: float
+    theta_prime: int
+    timings: dict
+
+
+def sampling_phase(g: Graph, cfg: ImmConfig) -> SamplingPhaseResult:
+    """sampling_phase (imm.hpp:169-209) into a fresh device store."""
+    c = _imm_config(cfg)
+    st = RRRStore(g)
+    lb = C.c_double()
+    tp = C.c_uint64()
+    r = _lib.ImmResultC()
+    check(lib.rrg_sampling_phase(g.handle, C.byref(c), st.handle, C.byref(lb), C.byref(tp),
+                                 C.byref(r)))
+    return SamplingPhaseResult(st, lb.value, int(tp.value),
+                               {"generate_rrrsets": r.t_generate,
+                                "find_most_influential": r.t_select})
+
+
 def run_imm(g: Graph, cfg: ImmConfig) -> ImmResult:
     """imm.hpp:214-251, driven by the C++17 driver in csrc/imm.cpp."""
-    c = _lib.ImmConfigC(int(cfg.k), float(cfg.epsilon), _model(cfg.model), int(cfg.workers),
-                        int(cfg.rng_seed) & (2**64 - 1), float(cfg.ell),
-                        float(cfg.adaptive_threshold))
+    c = _imm_config(cfg)
     k = max(int(cfg.k), 1)
     seeds = np.zeros(k, dtype=np.uint32)
     marg = np.zeros(k, dtype=np.uint64)

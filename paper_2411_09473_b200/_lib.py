@@ -42,6 +42,7 @@ class ImmConfigC(C.Structure):
         ("rng_seed", C.c_uint64),
         ("ell", C.c_double),
         ("adaptive_threshold", C.c_double),
+        ("strategy", C.c_int),
     ]
 
 
@@ -102,6 +103,8 @@ SIGNATURES = [
     ("rrg_fraction_covered", C.c_int, [vp, u32p, C.c_uint32, C.POINTER(C.c_double)]),
     ("rrg_imm_config_default", None, [C.POINTER(ImmConfigC)]),
     ("rrg_run_imm", C.c_int, [vp, C.POINTER(ImmConfigC), u32p, u64p, C.POINTER(ImmResultC)]),
+    ("rrg_sampling_phase", C.c_int,
+     [vp, C.POINTER(ImmConfigC), vp, C.POINTER(C.c_double), u64p, C.POINTER(ImmResultC)]),
     ("rrg_store_export", C.c_int, [vp, C.c_uint64, C.c_uint64, u64p, u32p]),
     ("rrg_store_import", C.c_int, [vp, C.c_uint64, u64p, u32p]),
     ("rrg_store_append_from", C.c_int, [vp, vp, C.c_uint64, C.c_uint64]),

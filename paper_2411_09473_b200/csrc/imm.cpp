@@ -88,30 +88,8 @@ struct StoreGuard {
   ~StoreGuard() { rrg_store_destroy(s); }
 };
 
-}  // namespace
-
-extern "C" {
-
-void rrg_imm_config_default(rrg_imm_config* cfg) {
-  if (!cfg) return;
-  cfg->k = 50;
-  cfg->epsilon = 0.5;
-  cfg->model = RRG_IC;
-  cfg->workers = 1;
-  cfg->rng_seed = 1;
-  cfg->ell = 1.0;
-  cfg->adaptive_threshold = 0.25;
-}
-
-// run_imm (imm.hpp:214-251) + sampling_phase (imm.hpp:169-209), fused strategy.
-rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
-                       uint64_t* marginals, rrg_imm_result* out) {
-  const auto t_total = std::chrono::steady_clock::now();
-  if (!g || !cfg || !seeds || !marginals || !out) {
-    rrgpu::set_error("run_imm: null argument");
-    return RRG_EINVAL;
-  }
-  // validate_config (imm.hpp:136-145)
+// validate_config (imm.hpp:136-145)
+rrg_status validate(rrg_graph* g, const rrg_imm_config* cfg) {
   const uint32_t n = rrg_graph_num_vertices(g);
   if (n == 0) {
     rrgpu::set_error("empty graph");
@@ -133,14 +111,25 @@ rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
     rrgpu::set_error("unknown diffusion model");
     return RRG_EINVAL;
   }
-  const rrg_model model = static_cast<rrg_model>(cfg->model);
-  *out = rrg_imm_result{};
-  const double ell = effective_ell(cfg->ell, n);
-  const double eps_prime = std::sqrt(2.0) * cfg->epsilon;
+  if (cfg->strategy != RRG_STRATEGY_FUSED && cfg->strategy != RRG_STRATEGY_BASELINE) {
+    rrgpu::set_error("unknown strategy");  // parse_strategy (imm.hpp:20-24)
+    return RRG_EINVAL;
+  }
+  return RRG_OK;
+}
 
-  StoreGuard store;
-  rrg_status st = rrg_store_create(g, &store.s);
-  if (st != RRG_OK) return st;
+// The IMM driver over one caller-visible store: top-ups (with speculation) and
+// selections, timed like ImmTimings (imm.hpp:38-42).
+class Driver {
+ public:
+  Driver(rrg_graph* g, const rrg_imm_config* cfg, rrg_store* store)
+      : g_(g), cfg_(cfg), store_(store), n_(rrg_graph_num_vertices(g)),
+        ell_(effective_ell(cfg->ell, n_)), fused_(cfg->strategy == RRG_STRATEGY_FUSED),
+        trial_seeds_(cfg->k), trial_marg_(cfg->k) {}
+
+  double ell() const { return ell_; }
+  uint64_t size() const { return size_; }
+  double t_generate = 0.0, t_select = 0.0;
 
   // Top-ups. Slot j's set depends only on (rng_seed, j) (sampling.hpp:179), so
   // sets for slots a later round may need can be sampled ahead into a side
@@ -148,85 +137,158 @@ rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
   // store ends up with exactly the reference's sets. Small batches are bound by
   // the latency of their largest set, so one batch covering the next rounds
   // costs about what one round's batch does.
-  StoreGuard ahead_store;
-  uint64_t ahead_first = 0, ahead_count = 0;
-  uint64_t size = 0;
-  auto top_up = [&](uint64_t target, uint64_t ahead) -> rrg_status {
-    if (target <= size) return RRG_OK;
+  rrg_status top_up(uint64_t target, uint64_t ahead) {
+    if (target <= size_) return RRG_OK;
     const auto t = std::chrono::steady_clock::now();
     rrg_status s = RRG_OK;
-    const bool covered = ahead_count && ahead_first <= size && target <= ahead_first + ahead_count;
+    const bool covered = ahead_count_ && ahead_first_ <= size_ && target <= ahead_first_ + ahead_count_;
     if (!covered) {
-      if (!ahead_store.s) {
-        s = rrg_store_create(g, &ahead_store.s);
+      if (!ahead_.s) {
+        s = rrg_store_create(g_, &ahead_.s);
         if (s != RRG_OK) return s;
       } else {
-        rrg_store_clear(ahead_store.s);
+        rrg_store_clear(ahead_.s);
       }
-      const uint64_t want = std::max(target, ahead) - size;
+      const uint64_t want = std::max(target, ahead) - size_;
       uint64_t made = 0;
-      s = rrg_generate_slots(g, model, cfg->rng_seed, size, want, ahead_store.s, /*fused=*/0, 64,
-                             &made);
-      ahead_first = size;
-      ahead_count = made;
+      s = rrg_generate_slots(g_, static_cast<rrg_model>(cfg_->model), cfg_->rng_seed, size_, want,
+                             ahead_.s, fused_ ? 1 : 0, 64, &made);
+      ahead_first_ = size_;
+      ahead_count_ = made;
       if (s != RRG_OK) {
-        out->t_generate += seconds_since(t);
+        t_generate += seconds_since(t);
         return s;
       }
     }
-    s = rrg_store_append_from(store.s, ahead_store.s, size - ahead_first, target - size);
-    if (s == RRG_OK) size = target;
-    out->t_generate += seconds_since(t);
+    s = rrg_store_append_from(store_, ahead_.s, size_ - ahead_first_, target - size_);
+    if (s == RRG_OK) size_ = target;
+    t_generate += seconds_since(t);
     return s;
-  };
+  }
+
   // how far ahead to sample: the next rounds' budgets while the batch stays small
-  constexpr uint64_t kAheadMax = 1ull << 16;
-  auto ahead_for = [&](unsigned i, unsigned rounds_total) -> uint64_t {
+  uint64_t ahead_for(unsigned i, unsigned rounds_total) const {
+    constexpr uint64_t kAheadMax = 1ull << 16;
     uint64_t best = 0;
     for (unsigned j = i + 1; j <= std::min(rounds_total, i + 2); ++j) {
-      const uint64_t tj = theta_for_round(n, cfg->k, cfg->epsilon, ell, j);
-      if (tj > size && tj - size <= kAheadMax) best = std::max(best, tj);
+      const uint64_t tj = theta_for_round(n_, cfg_->k, cfg_->epsilon, ell_, j);
+      if (tj > size_ && tj - size_ <= kAheadMax) best = std::max(best, tj);
     }
     return best;
-  };
-  std::vector<uint32_t> trial_seeds(cfg->k);
-  std::vector<uint64_t> trial_marg(cfg->k);
-  auto select = [&](uint32_t* sd, uint64_t* mg, uint64_t* covered) -> rrg_status {
-    const auto t = std::chrono::steady_clock::now();
-    const rrg_status s = rrg_select_seeds(store.s, cfg->k, cfg->adaptive_threshold,
-                                          /*use_prebuilt=*/1, sd, mg, nullptr, nullptr, covered);
-    out->t_select += seconds_since(t);
-    return s;
-  };
-
-  // sampling phase: top up to theta_i, trial selection, stop once the estimate
-  // certifies the round target (imm.hpp:182-206)
-  const unsigned rounds = sampling_rounds(n);
-  double estimated_spread = 0.0;
-  bool triggered = false;
-  for (unsigned i = 1; i <= rounds; ++i) {
-    st = top_up(theta_for_round(n, cfg->k, cfg->epsilon, ell, i), ahead_for(i, rounds));
-    if (st != RRG_OK) return st;
-    uint64_t covered = 0;
-    st = select(trial_seeds.data(), trial_marg.data(), &covered);
-    if (st != RRG_OK) return st;
-    const double fraction = static_cast<double>(covered) / static_cast<double>(size);
-    estimated_spread = static_cast<double>(n) * fraction;
-    if (estimated_spread >= (1.0 + eps_prime) * round_target(n, i)) {
-      triggered = true;
-      break;
-    }
   }
-  out->lower_bound = triggered ? estimated_spread / (1.0 + eps_prime)
-                               : std::max(estimated_spread / (1.0 + eps_prime),
-                                          static_cast<double>(cfg->k));
-  out->theta_prime = size;
-  out->theta = set_theta(n, cfg->k, cfg->epsilon, ell, out->lower_bound);
+
+  // run_selection (imm.hpp:147-153): the fused strategy uses the fused counter,
+  // the baseline strategy recounts (build_counter) -- same seeds either way
+  rrg_status select(uint32_t* sd, uint64_t* mg, uint64_t* covered) {
+    const auto t = std::chrono::steady_clock::now();
+    const rrg_status s = rrg_select_seeds(store_, cfg_->k, cfg_->adaptive_threshold,
+                                          fused_ ? 1 : 0, sd, mg, nullptr, nullptr, covered);
+    t_select += seconds_since(t);
+    return s;
+  }
+
+  // sampling_phase (imm.hpp:169-209)
+  rrg_status sampling_phase(double* lower_bound) {
+    const double eps_prime = std::sqrt(2.0) * cfg_->epsilon;
+    const unsigned rounds = sampling_rounds(n_);
+    double estimated_spread = 0.0;
+    bool triggered = false;
+    for (unsigned i = 1; i <= rounds; ++i) {
+      rrg_status st = top_up(theta_for_round(n_, cfg_->k, cfg_->epsilon, ell_, i), ahead_for(i, rounds));
+      if (st != RRG_OK) return st;
+      uint64_t covered = 0;
+      st = select(trial_seeds_.data(), trial_marg_.data(), &covered);
+      if (st != RRG_OK) return st;
+      const double fraction = static_cast<double>(covered) / static_cast<double>(size_);
+      estimated_spread = static_cast<double>(n_) * fraction;
+      if (estimated_spread >= (1.0 + eps_prime) * round_target(n_, i)) {
+        triggered = true;
+        break;
+      }
+    }
+    *lower_bound = triggered ? estimated_spread / (1.0 + eps_prime)
+                             : std::max(estimated_spread / (1.0 + eps_prime),
+                                        static_cast<double>(cfg_->k));
+    return RRG_OK;
+  }
+
+ private:
+  rrg_graph* g_;
+  const rrg_imm_config* cfg_;
+  rrg_store* store_;
+  uint32_t n_;
+  double ell_;
+  bool fused_;
+  StoreGuard ahead_;
+  uint64_t ahead_first_ = 0, ahead_count_ = 0;
+  uint64_t size_ = 0;
+  std::vector<uint32_t> trial_seeds_;
+  std::vector<uint64_t> trial_marg_;
+};
+
+}  // namespace
+
+extern "C" {
+
+void rrg_imm_config_default(rrg_imm_config* cfg) {
+  if (!cfg) return;
+  cfg->k = 50;
+  cfg->epsilon = 0.5;
+  cfg->model = RRG_IC;
+  cfg->workers = 1;
+  cfg->rng_seed = 1;
+  cfg->ell = 1.0;
+  cfg->adaptive_threshold = 0.25;
+  cfg->strategy = RRG_STRATEGY_FUSED;
+}
+
+rrg_status rrg_sampling_phase(rrg_graph* g, const rrg_imm_config* cfg, rrg_store* store,
+                              double* lower_bound, uint64_t* theta_prime,
+                              rrg_imm_result* timings) {
+  if (!g || !cfg || !store || !lower_bound || !theta_prime) {
+    rrgpu::set_error("sampling_phase: null argument");
+    return RRG_EINVAL;
+  }
+  rrg_status st = validate(g, cfg);
+  if (st != RRG_OK) return st;
+  st = rrg_store_clear(store);
+  if (st != RRG_OK) return st;
+  Driver d(g, cfg, store);
+  st = d.sampling_phase(lower_bound);
+  if (st != RRG_OK) return st;
+  *theta_prime = d.size();
+  if (timings) {
+    timings->t_generate = d.t_generate;
+    timings->t_select = d.t_select;
+  }
+  return RRG_OK;
+}
+
+// run_imm (imm.hpp:214-251)
+rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
+                       uint64_t* marginals, rrg_imm_result* out) {
+  const auto t_total = std::chrono::steady_clock::now();
+  if (!g || !cfg || !seeds || !marginals || !out) {
+    rrgpu::set_error("run_imm: null argument");
+    return RRG_EINVAL;
+  }
+  rrg_status st = validate(g, cfg);
+  if (st != RRG_OK) return st;
+  const uint32_t n = rrg_graph_num_vertices(g);
+  *out = rrg_imm_result{};
+  StoreGuard store;
+  st = rrg_store_create(g, &store.s);
+  if (st != RRG_OK) return st;
+  Driver d(g, cfg, store.s);
+  st = d.sampling_phase(&out->lower_bound);
+  if (st != RRG_OK) return st;
+  out->theta_prime = d.size();
+  out->theta = set_theta(n, cfg->k, cfg->epsilon, d.ell(), out->lower_bound);
 
   // final top-up and selection (imm.hpp:227-241)
-  st = top_up(out->theta, 0);
+  st = d.top_up(out->theta, 0);
   if (st != RRG_OK) return st;
-  st = select(seeds, marginals, nullptr);
+  st = d.select(seeds, marginals, nullptr);
   if (st != RRG_OK) return st;
 
   // set statistics (imm.hpp:243-248)
@@ -237,6 +299,8 @@ rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
   out->mean_set_size = static_cast<double>(members) / static_cast<double>(sets);
   out->max_set_size = max_len;
   out->mean_coverage_fraction = out->mean_set_size / static_cast<double>(n);
+  out->t_generate = d.t_generate;
+  out->t_select = d.t_select;
   out->t_total = seconds_since(t_total);
   return RRG_OK;
 }

@@ -102,6 +102,25 @@ int main() {
                                                     &counter);
     const rrgpu::SeedSet gs = rrgpu::select_seeds(gstore, g.num_vertices, c.k, 0.25, true);
     expect(rs.seeds == gs.seeds && rs.marginal_counts == gs.marginal_counts, "select_seeds", id);
+
+    // --- sampling_phase (imm.hpp:169-209) and the baseline strategy ----------
+    rrflow::WorkPool pool1(1);
+    const rrflow::SamplingPhaseResult rp = rrflow::sampling_phase(g, rc, pool1);
+    const rrgpu::SamplingPhaseResult gp = rrgpu::sampling_phase(dg, gc);
+    expect(rp.lower_bound == gp.lower_bound && rp.theta_prime == gp.theta_prime &&
+               rp.store.size() == gp.store.size(),
+           "sampling_phase lower bound / theta'", id);
+    const std::vector<uint64_t> gpc = gp.store.counter();
+    bool same_phase_counter = true;
+    for (uint32_t v = 0; v < g.num_vertices; ++v) same_phase_counter &= rp.counter.get(v) == gpc[v];
+    expect(same_phase_counter, "sampling_phase counter", id);
+    rc.strategy = rrflow::Strategy::baseline;
+    gc.strategy = rrgpu::parse_strategy("baseline");
+    const rrflow::ImmResult rb = rrflow::run_imm(g, rc);
+    const rrgpu::ImmResult gb = rrgpu::run_imm(dg, gc);
+    expect(rb.seeds.seeds == gb.seeds.seeds && rb.seeds.marginal_counts == gb.seeds.marginal_counts &&
+               rb.theta == gb.theta && rb.lower_bound == gb.lower_bound,
+           "run_imm, baseline strategy", id);
   }
   // error mapping: k > n -> std::invalid_argument, like validate_config
   {

@@ -87,3 +87,40 @@ def test_validation(cuda):
                 P.ImmConfig(k=0)):
         with pytest.raises(ValueError):
             P.run_imm(g, cfg)
+
+
+@pytest.mark.parametrize("name,n,m,k", [("cfg1", 1 << 12, 1 << 16, 20), ("cfg4", 40000, 600000, 10)])
+def test_sampling_phase_matches_reference(cuda, oracle, name, n, m, k):
+    """sampling_phase (imm.hpp:169-209): LB, theta' and the phase's fused counter."""
+    cfg = graphs.scaled(graphs.CONFIGS[name], n, m)
+    arrays = graphs.generate(cfg)
+    g = P.Graph(*arrays)
+    got = P.sampling_phase(g, P.ImmConfig(k=k, model=cfg.model, rng_seed=3))
+    ref = oracle.graph(*arrays).sampling_phase(k=k, model=cfg.model, rng_seed=3, workers=4)
+    assert got.lower_bound == ref["lower_bound"]
+    assert got.theta_prime == ref["theta_prime"] == got.store.size()
+    assert (got.store.counter() == ref["counter"]).all()
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_baseline_strategy_same_seeds(cuda, oracle, name):
+    """Strategy::baseline (unfused sampling + baseline_select) returns the fused
+    strategy's seeds (test_selection.cpp:188-200); both match the reference's."""
+    cfg = graphs.scaled(graphs.CONFIGS[name], *((1 << 12, 1 << 16) if name == "cfg2"
+                                               else (30000, 500000)))
+    arrays = graphs.generate(cfg)
+    g = P.Graph(*arrays)
+    k = 10
+    base = P.run_imm(g, P.ImmConfig(k=k, model=cfg.model, strategy=P.parse_strategy("baseline")))
+    ref = oracle.graph(*arrays).imm(k=k, model=cfg.model, workers=4, strategy=1)
+    compare(base, ref)
+    fused = P.run_imm(g, P.ImmConfig(k=k, model=cfg.model))
+    assert fused.seeds == base.seeds and fused.theta == base.theta
+
+
+def test_unknown_strategy_rejected(cuda):
+    g = P.Graph.from_edges(3, [(0, 1, 0.5), (1, 2, 0.5)])
+    with pytest.raises(ValueError):
+        P.run_imm(g, P.ImmConfig(k=1, strategy=7))
+    with pytest.raises(ValueError):
+        P.parse_strategy("nope")

@@ -152,3 +152,19 @@ def test_reference_build_graph_and_normalize_match_host_code(ref):
     P.normalize_lt_weights(a[0], rw)
     assert (rw == ref.normalize_lt(a[0], a[2])).all()
     assert not (rw == a[2]).all()  # some in-lists were infeasible and got rescaled
+
+
+def test_port_sampling_phase_and_baseline_match_reference(port, ref):
+    """The C++ restatement's sampling_phase and baseline run_imm against the reference
+    headers (imm.hpp:169-209; Strategy::baseline, imm.hpp:147-153)."""
+    for (kind, n, frac, gseed, wseed, k, seed, model) in [
+        (1, 200, 0.25, 19, 23, 3, 7, 0), (1, 150, 0.2, 5, 9, 4, 31, 1)]:
+        arrays = ref.synth_graph(kind, n, frac, gseed, wseed)
+        a = port.graph(*arrays).sampling_phase(k=k, model=model, rng_seed=seed, workers=2)
+        b = ref.graph(*arrays).sampling_phase(k=k, model=model, rng_seed=seed, workers=2)
+        assert a["lower_bound"] == b["lower_bound"] and a["theta_prime"] == b["theta_prime"]
+        assert (a["counter"] == b["counter"]).all()
+        ra = port.graph(*arrays).imm(k=k, model=model, rng_seed=seed, workers=2, strategy=1)
+        rb = ref.graph(*arrays).imm(k=k, model=model, rng_seed=seed, workers=2, strategy=1)
+        assert ra["seeds"] == rb["seeds"] and ra["marginals"] == rb["marginals"]
+        assert ra["theta"] == rb["theta"]
