@@ -62,8 +62,12 @@ typedef enum {
   RRG_OPT_LT_KARY = 4,  /* arity of the LT CDF search: 2, 4, 8 or 16 (default 8) */
   RRG_OPT_IC_MODE = 5,  /* IC schedule: 0 auto (pilot-measured), 1 lane per sample,
                            2 warp per sample, 3 thread block per sample */
-  RRG_OPT_IC_WARP_MIN_INSP = 6 /* auto: warp per sample once the mean inspected
-                                  in-edges per set reaches this value */
+  RRG_OPT_IC_WARP_MIN_INSP = 6, /* auto: warp per sample once the mean inspected
+                                   in-edges per set reaches this value */
+  RRG_OPT_IC_RNG = 7 /* IC randomness: 0 (default) the reference's per-slot stream,
+                        sets bit-identical; 1 FAST: counter-based per-edge draws with
+                        geometric skipping over equal-weight in-lists -- same set
+                        distribution, statistical parity only */
 } rrg_option;
 rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value);
 

@@ -323,6 +323,10 @@ rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value) {
         return invalid("lt_kary must be 2, 4, 8 or 16");
       g->lt_kary = static_cast<int>(value);
       return RRG_OK;
+    case RRG_OPT_IC_RNG:
+      if (value != 0 && value != 1) return invalid("ic_rng must be 0 (exact) or 1 (fast)");
+      g->ic_rng = static_cast<int>(value);
+      return RRG_OK;
     case RRG_OPT_IC_COOP_MIN:
       if (value < 1) return invalid("ic_coop_min must be >= 1");
       g->ic_coop_min = static_cast<uint32_t>(std::min<int64_t>(value, UINT32_MAX));
@@ -406,6 +410,8 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
   return guarded([&]() -> rrg_status {
     if (model == RRG_IC) prepare_ic(g);
     else prepare_lt(g);
+    const bool ic_fast = model == RRG_IC && g->ic_rng == 1;
+    if (ic_fast) prepare_ic_fast(g);
     if (!fused) s->counter_complete = false;
     const cudaStream_t st = g->stream;
     const int block = sampler_block();
@@ -425,7 +431,8 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       // throughput); batches of few inspected edges in total -> block per sample
       // (latency: the largest sets finish 4-8x sooner); heavy large batches ->
       // warp; light large batches -> lane.
-      if (model == RRG_IC && g->ic_mode == 0 && g->ic_mean_insp < 0) c = std::min<uint64_t>(c, 2048);
+      if (model == RRG_IC && !ic_fast && g->ic_mode == 0 && g->ic_mean_insp < 0)
+        c = std::min<uint64_t>(c, 2048);
       bool ic_warp = false, ic_cta = false;
       if (model == RRG_IC) {
         const double mean = g->ic_mean_insp;
@@ -482,11 +489,12 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.jtab256 = g->jtab256.ptr;
       p.lt_kary = g->lt_kary;
       p.dupfree = g->dupfree.ptr;
+      p.uniformw = g->uniformw.ptr;
       p.ic_coop_min = g->ic_coop_min;
 
       // One launch of `kind` over `list` (nullptr: the range [0, n_items)). The
       // per-launch counters reset here; the deferral list accumulates over a pass.
-      enum Kind { kMain, kMainWarp, kCta, kBig };
+      enum Kind { kMain, kMainWarp, kCta, kBig, kFast, kFastBig, kFastLane };
       auto launch = [&](Kind kind, const uint32_t* list, uint64_t n_items, uint32_t* restage_out) {
         ctl.next = 0;
         ctl.restage_members = 0;
@@ -494,7 +502,25 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         RRG_CUDA(cudaMemcpyAsync(g->ctl.ptr, &ctl, sizeof(SampleCtl), cudaMemcpyHostToDevice, st));
         p.restage = restage_out;
         RRG_CUDA(cudaEventRecord(g->ev0, st));
-        if (kind == kBig) {
+        if (kind == kFastLane) {
+          p.list = list;
+          p.count = n_items;
+          const uint64_t grid_need = (n_items + block - 1) / block;
+          launch_fast_lane(p, static_cast<int>(std::max<uint64_t>(1, std::min(full_grid, grid_need))),
+                           st);
+        } else if (kind == kFast || kind == kFastBig) {
+          p.list = list;
+          p.count = n_items;
+          uint32_t workers = 0;
+          if (kind == kFastBig) {
+            workers = static_cast<uint32_t>(std::min<uint64_t>(
+                n_items, std::min<uint64_t>(kBigWorkersMax, 4ull * g->num_sms)));
+            ensure_big_scratch(g, workers);
+          }
+          const uint64_t grid_need = (n_items + block / 32 - 1) / (block / 32);
+          launch_fast(p, static_cast<int>(std::max<uint64_t>(1, std::min(full_grid, grid_need))),
+                      kind == kFastBig, g->big.bitmaps.ptr, g->big.lists.ptr, workers, st);
+        } else if (kind == kBig) {
           const uint32_t workers = static_cast<uint32_t>(std::min<uint64_t>(
               n_items, std::min<uint64_t>(kBigWorkersMax, 4ull * g->num_sms)));
           ensure_big_scratch(g, workers);
@@ -552,11 +578,27 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       };
       // main schedule, then the wider schedules for the sets it could not hold:
       // lane (1K members) or warp (32K) -> block (256K, IC) -> big-set path (n)
-      const Kind main_kind = ic_cta ? kCta : ic_warp ? kMainWarp : kMain;
+      // fast IC: lane per sample (ic_mode 1) or warp per sample (2, 3); auto: lane
+      // for large batches (throughput), warp for small ones (latency of the
+      // largest sets: cfg5 32K sets 5.1 ms per warp vs 9.2 ms per lane)
+      const bool fast_lane = ic_fast && (g->ic_mode == 1 || (g->ic_mode == 0 && c >= (1u << 17)));
+      const Kind main_kind = fast_lane ? kFastLane : ic_fast ? kFast
+                             : ic_cta ? kCta : ic_warp ? kMainWarp : kMain;
       uint64_t ndef = pass(main_kind, nullptr, c, s->deferred.ptr);
       uint32_t* dlist = s->deferred.ptr;
       uint32_t* dspare = s->deferred2.ptr;
-      if (model == RRG_IC) {
+      if (ic_fast) {
+        if (ndef && fast_lane) {
+          acc.deferred += ndef;
+          ndef = pass(kFast, dlist, ndef, dspare);
+          std::swap(dlist, dspare);
+        }
+        if (ndef) {
+          acc.deferred += ndef;
+          pass(kFastBig, dlist, ndef, dspare);
+          ndef = 0;
+        }
+      } else if (model == RRG_IC) {
         if (ndef && main_kind != kCta) {
           acc.deferred += ndef;
           ndef = pass(kCta, dlist, ndef, dspare);
@@ -568,7 +610,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         pass(kBig, dlist, ndef, s->bigre.ptr);
       }
       acc.edges_inspected += ctl.inspected;
-      if (model == RRG_IC) {
+      if (model == RRG_IC && !ic_fast) {
         const double mean = static_cast<double>(ctl.inspected) / static_cast<double>(c);
         g->ic_mean_insp = g->ic_mean_insp < 0 ? mean : 0.5 * (g->ic_mean_insp + mean);
       }

@@ -113,6 +113,9 @@ struct rrg_graph {
   rrgpu::DevBuf<uint64_t> jtab16;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab256;  // IC: byte tables of T^(256 a), a = 1..15 (3.75 MB)
   rrgpu::DevBuf<uint8_t> dupfree;  // IC: per-vertex strictly-increasing-sources flag
+  rrgpu::DevBuf<uint8_t> uniformw; // IC fast mode: per-vertex "all in-weights equal" flag
+  bool uniform_ready = false;
+  int ic_rng = 0;                // IC: 0 the reference's stream (exact), 1 fast (statistical)
   uint32_t ic_coop_min = 256;    // IC: in-lists at least this long expand warp-cooperatively
   int ic_mode = 0;               // IC: 0 auto, 1 lane, 2 warp, 3 block per sample
   double ic_mean_insp = -1.0;    // IC: running mean of inspected in-edges per set
@@ -209,10 +212,16 @@ struct SampleParams {
   const uint64_t* jtab16;   // byte tables of T^(16 l), l = 1..31 (warp-schedule windows)
   const uint64_t* jtab256;  // byte tables of T^(256 a), a = 1..15 (CTA-schedule windows)
   const uint8_t* dupfree;   // per vertex: in-list sources strictly increasing
+  const uint8_t* uniformw;  // IC fast mode: per vertex, all in-weights equal
   uint32_t ic_coop_min;     // in-lists at least this long go warp-cooperative
 };
 
 void prepare_ic(rrg_graph* g);
+void prepare_ic_fast(rrg_graph* g);
+// IC fast (statistical) sampler: warp region tables, or n-bit maps (bitmap)
+void launch_fast(const SampleParams& p, int grid, bool bitmap, uint32_t* bitmaps, uint32_t* lists,
+                 uint32_t workers, cudaStream_t s);
+void launch_fast_lane(const SampleParams& p, int grid, cudaStream_t s);
 void prepare_lt(rrg_graph* g);
 // converts d_off64 into g->off and validates offsets/sources on the device;
 // returns a bit mask of violations (1 offsets, 2 sources), 0 if clean

@@ -1231,6 +1231,288 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
 }
 
 // ---------------------------------------------------------------------------
+// K1f: opt-in FAST IC sampler (RRG_OPT_IC_RNG = 1). Not
+// the reference's draw sequence: every in-edge's liveness comes from a
+// counter-based stream keyed by (slot, vertex, edge), so the lists of one
+// vertex need no serial order and runs of equal weights are sampled by
+// geometric skipping (the next live edge after G ~ Geometric(p) dead ones).
+// Each edge is live with probability w independently, so a set is distributed
+// as the reference's (the RIS reverse-reachable set over live edges); parity is
+// statistical (tests/test_gpu_fast.py). Roots are the reference's (slot stream).
+// Warp per sample: the warp takes one dequeued vertex at a time; a weight-
+// uniform in-list is cut into 32 lane segments, each skipping with its own
+// substream; other lists are drawn 32 edges per round. kBitmap: n-bit visited
+// map + n-entry list (big-set scratch, no size cap), else the warp's 32-lane
+// region table (32K members, larger sets deferred to the bitmap variant).
+// ---------------------------------------------------------------------------
+// Equal-weight in-lists are cut into fixed segments, each skipped with its own
+// substream, so every variant (lane, warp, bitmap) draws the same live edges
+// and a deferred slot is re-run to the same set.
+constexpr uint32_t kFastSeg = 1u << 16;
+__device__ __forceinline__ uint64_t fast_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+// uniform in (0, 1] from draw i of the (slot, vertex) stream ku
+__device__ __forceinline__ double fast_u01(uint64_t ku, uint64_t i) {
+  return static_cast<double>((fast_mix(ku + 0x9e3779b97f4a7c15ULL * (i + 1)) >> 11) + 1) * 0x1.0p-53;
+}
+
+template <bool kBitmap>
+__global__ void __launch_bounds__(kBlock) k_sample_ic_fast(const SampleParams p, uint32_t* bitmaps,
+                                                           uint32_t* lists, uint32_t workers) {
+  constexpr uint32_t kCap = kBitmap ? 0xffffffffu : 32 * kMemCap;
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  uint32_t* mem;
+  uint32_t* vis = nullptr;
+  uint64_t* tab = nullptr;
+  uint64_t tslot = 0;
+  uint32_t tag = 0;
+  if (kBitmap) {
+    if (gw >= workers) return;
+    const uint64_t words = (static_cast<uint64_t>(p.n) + 31) / 32;
+    vis = bitmaps + gw * words;
+    mem = lists + gw * p.n;
+  } else {
+    const uint64_t region = gw * 32;
+    if (region + 32 > p.lanes) return;
+    mem = p.lists + region * kMemCap;
+    tab = p.tabs + region * kTabCap;
+    tslot = region / 32;  // same layout and tag range as the 32-lane warp schedule
+    tag = 0x80000000u | (p.wtags[tslot] & 0x3fffffffu);
+  }
+  uint64_t insp = 0;
+  for (;;) {
+    unsigned long long k = 0;
+    if (lane == 0) k = atomicAdd(&p.ctl->next, 1ull);
+    k = __shfl_sync(kFull, k, 0);
+    if (k >= p.count) break;
+    const uint32_t idx = p.list ? p.list[k] : p.idx_base + static_cast<uint32_t>(k);
+    const uint64_t seed = stream_seed(p.run_seed, p.base_slot + idx);
+    Xoshiro rng;
+    rng.seed(seed);
+    const uint32_t root = static_cast<uint32_t>(rng.below(p.n));  // the reference's root
+    const uint64_t key = fast_mix(seed ^ 0xD1B54A32D192ED03ULL);
+    uint32_t lg = kTabLog0, nmem = 1;
+    if (!kBitmap) ++tag;
+    if (lane == 0) {
+      mem[0] = root;
+      if (kBitmap) vis[root >> 5] |= 1u << (root & 31);
+      else tab_insert(tab, tag, lg, root);
+    }
+    __syncwarp();
+    bool ok = true;
+    uint64_t sinsp = 0;
+    for (uint32_t qi = 0; qi < nmem && ok; ++qi) {
+      const uint32_t u = mem[qi];
+      const uint32_t b = p.off[u], e = p.off[u + 1];
+      if (b == e) continue;
+      sinsp += e - b;
+      const uint64_t ku = fast_mix(key ^ (0x9e3779b97f4a7c15ULL * (static_cast<uint64_t>(u) + 1)));
+      bool uni = p.uniformw[u] != 0;
+      bool all_live = false;  // equal weights >= 1: every edge live, no draws
+      double pw = 0.0, lq = 0.0;
+      uint32_t sg = lane, pos = 0, s1 = 0, cnum = 0;  // lane: segments lane, lane + 32, ...
+      const uint32_t nseg = (e - b + kFastSeg - 1) / kFastSeg;
+      if (uni) {
+        pw = static_cast<double>(__ldg(p.w + b));
+        if (!(pw > 0.0)) continue;  // 0, negative, NaN: never live (prng.hpp:62)
+        if (pw >= 1.0) {
+          uni = false;
+          all_live = true;
+        }
+        lq = pw >= 1.0 ? 0.0 : log1p(-pw);
+        pos = b + sg * kFastSeg;
+        s1 = sg < nseg ? min(e, pos + kFastSeg) : pos;
+      }
+      for (uint32_t c0 = b;; c0 += 32) {
+        // one candidate per lane per round: the lane's next live edge
+        uint32_t cand = 0xffffffffu;
+        if (uni) {
+          while (sg < nseg) {
+            if (pos < s1 && pw < 1.0) {
+              const double g = floor(log(fast_u01(ku, (static_cast<uint64_t>(sg) << 32) | cnum++)) / lq);
+              pos = g >= static_cast<double>(s1 - pos) ? s1 : pos + static_cast<uint32_t>(g);
+            }
+            if (pos < s1) {
+              cand = pos++;
+              break;
+            }
+            sg += 32;  // the lane's next segment
+            pos = b + sg * kFastSeg;
+            s1 = sg < nseg ? min(e, pos + kFastSeg) : pos;
+            cnum = 0;
+          }
+        } else {
+          if (c0 >= e) break;
+          const uint32_t t = c0 + lane;
+          if (t < e && (all_live || fast_u01(ku, t - b) <= static_cast<double>(__ldg(p.w + t))))
+            cand = t;
+        }
+        if (uni && !__any_sync(kFull, cand != 0xffffffffu)) break;
+        const uint32_t v = cand != 0xffffffffu ? __ldg(p.src + cand) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(kFull, v);
+        bool fresh = cand != 0xffffffffu && (peers & lanemask_lt()) == 0;  // first lane with v
+        if (fresh) fresh = kBitmap ? !((vis[v >> 5] >> (v & 31)) & 1u) : !tab_contains(tab, tag, lg, v);
+        const unsigned fm = __ballot_sync(kFull, fresh);
+        if (fm) {
+          const uint32_t A = __popc(fm);
+          if (nmem + A > kCap) {
+            ok = false;
+            break;
+          }
+          if (!kBitmap) {
+            uint32_t lg2 = lg;
+            while (2 * (nmem + A) > (1u << lg2)) ++lg2;
+            if (lg2 != lg) {  // grow: re-insert the members under a fresh tag
+              lg = lg2;
+              ++tag;
+              for (uint32_t t = lane; t < nmem; t += 32) tab_insert_atomic(tab, tag, lg, mem[t]);
+              __syncwarp();
+            }
+          }
+          if (fresh) {
+            mem[nmem + __popc(fm & lanemask_lt())] = v;
+            if (kBitmap) atomicOr(vis + (v >> 5), 1u << (v & 31));
+            else tab_insert_atomic(tab, tag, lg, v);
+          }
+          nmem += A;
+        }
+        __syncwarp();
+      }
+    }
+    if (!ok) {
+      if (lane == 0) defer_slot(p, idx);
+    } else {
+      unsigned long long spos = 0;
+      if (lane == 0) spos = atomicAdd(&p.ctl->cursor, (unsigned long long)nmem);
+      spos = __shfl_sync(kFull, spos, 0);
+      if (spos + nmem > p.stage_cap) {
+        if (lane == 0) restage_slot(p, idx, nmem);
+      } else {
+        for (uint32_t t = lane; t < nmem; t += 32) {
+          const uint32_t v = mem[t];
+          p.stage[spos + t] = v;
+          if (p.counter) atomicAdd(p.counter + v, 1u);
+        }
+        if (lane == 0) {
+          p.slot_start[idx] = spos;
+          p.slot_len[idx] = nmem;
+        }
+        insp += sinsp;
+      }
+    }
+    if (kBitmap) {
+      for (uint32_t t = lane; t < nmem; t += 32) {
+        const uint32_t v = mem[t];
+        atomicAnd(vis + (v >> 5), ~(1u << (v & 31)));
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (!kBitmap) p.wtags[tslot] = tag;
+    atomicAdd(&p.ctl->inspected, (unsigned long long)insp);
+    atomicAdd(&p.ctl->entries, (unsigned long long)insp);
+  }
+}
+
+// Lane per sample variant of the fast sampler (light sets, e.g. cfg3): the lane
+// walks its own BFS; an equal-weight in-list costs one geometric draw per live
+// edge (+1), any other list one hash draw per edge. Sets beyond the lane's 1K
+// members are deferred to the warp variant.
+__global__ void __launch_bounds__(kBlock) k_sample_ic_fast_lane(const SampleParams p) {
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t* mem = p.lists + gid * kMemCap;
+  uint64_t* tab = p.tabs + gid * kTabCap;
+  uint32_t tag = p.tags[gid];
+  bool exhausted = false;
+  uint64_t insp = 0;
+  for (;;) {
+    uint32_t idx = 0;
+    const bool got = fetch_slot(p, !exhausted, exhausted, idx);
+    if (__all_sync(kFull, exhausted)) break;
+    if (!got) continue;
+    const uint64_t seed = stream_seed(p.run_seed, p.base_slot + idx);
+    Xoshiro rng;
+    rng.seed(seed);
+    const uint32_t root = static_cast<uint32_t>(rng.below(p.n));  // the reference's root
+    const uint64_t key = fast_mix(seed ^ 0xD1B54A32D192ED03ULL);
+    ++tag;
+    uint32_t lg = kTabLog0, nmem = 1;
+    Filter flt;
+    flt.clear();
+    mem[0] = root;
+    tab_insert(tab, tag, lg, root);
+    flt.add(root);
+    bool ok = true;
+    uint64_t sinsp = 0;
+    for (uint32_t qi = 0; qi < nmem && ok; ++qi) {
+      const uint32_t u = mem[qi];
+      const uint32_t b = p.off[u], e = p.off[u + 1];
+      if (b == e) continue;
+      sinsp += e - b;
+      const uint64_t ku = fast_mix(key ^ (0x9e3779b97f4a7c15ULL * (static_cast<uint64_t>(u) + 1)));
+      const bool uni = p.uniformw[u] != 0;
+      double pw = 0.0, lq = 0.0;
+      if (uni) {
+        pw = static_cast<double>(__ldg(p.w + b));
+        if (!(pw > 0.0)) continue;
+        lq = pw >= 1.0 ? 0.0 : log1p(-pw);
+      }
+      uint32_t cnum = 0, send = min(e, b + kFastSeg);
+      for (uint32_t t = b; t < e; ++t) {
+        if (uni) {
+          if (pw < 1.0) {  // the next live edge: skip G ~ Geometric(pw) dead ones
+            const double g = floor(log(fast_u01(ku, (static_cast<uint64_t>((t - b) / kFastSeg) << 32) | cnum++)) / lq);
+            if (g >= static_cast<double>(send - t)) {  // segment exhausted: the next one
+              t = send - 1;
+              send = min(e, send + kFastSeg);
+              cnum = 0;
+              continue;
+            }
+            t += static_cast<uint32_t>(g);
+          }
+        } else if (fast_u01(ku, t - b) > static_cast<double>(__ldg(p.w + t))) {
+          continue;
+        }
+        const uint32_t v = __ldg(p.src + t);
+        if (flt.maybe(v) && tab_contains(tab, tag, lg, v)) continue;
+        if (nmem == kMemCap) {
+          ok = false;
+          break;
+        }
+        lane_insert(mem, tab, tag, lg, nmem, v);
+        flt.add(v);
+      }
+    }
+    if (!ok) {
+      defer_slot(p, idx);
+    } else if (emit_set(p, idx, mem, nmem)) {
+      insp += sinsp;
+    }
+  }
+  p.tags[gid] = tag;
+  flush_counters(p, insp, insp);
+}
+
+// K0 for the fast sampler: 1 iff every in-weight of the vertex has the same bits.
+__global__ void k_uniform_weights(const uint32_t* off, const float* w, uint32_t n, uint8_t* out) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n;
+       v += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t b = off[v], e = off[v + 1];
+    const uint32_t w0 = b < e ? __float_as_uint(w[b]) : 0u;
+    bool same = true;
+    for (uint32_t t = b + lane; t < e && same; t += 32) same = __float_as_uint(w[t]) == w0;
+    same = __all_sync(kFull, same);
+    if (lane == 0) out[v] = (b < e && same) ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2: LT sampler (sampling.hpp:117-145 per slot)
 // ---------------------------------------------------------------------------
 constexpr uint32_t kLtTabLog0 = 8;        // walks average ~80 steps (cfg4): fewer rehashes
@@ -1914,6 +2196,37 @@ void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t
   k_sample_big<<<grid, kBlock, 0, s>>>(p, model, list, nlist, bitmaps, lists, workers);
   RRG_CUDA(cudaGetLastError());
   count_launch();
+}
+
+void launch_fast_lane(const SampleParams& p, int grid, cudaStream_t s) {
+  k_sample_ic_fast_lane<<<grid, kBlock, 0, s>>>(p);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_fast(const SampleParams& p, int grid, bool bitmap, uint32_t* bitmaps, uint32_t* lists,
+                 uint32_t workers, cudaStream_t s) {
+  if (bitmap) {
+    k_sample_ic_fast<true><<<(workers * 32 + kBlock - 1) / kBlock, kBlock, 0, s>>>(p, bitmaps, lists,
+                                                                                  workers);
+  } else {
+    k_sample_ic_fast<false><<<grid, kBlock, 0, s>>>(p, nullptr, nullptr, 0);
+  }
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void prepare_ic_fast(rrg_graph* g) {
+  if (g->uniform_ready) return;
+  g->uniformw.reserve_discard(g->n ? g->n : 1);
+  if (g->n) {
+    k_uniform_weights<<<g->num_sms * 16, 256, 0, g->stream>>>(g->off.ptr, g->w.ptr, g->n,
+                                                            g->uniformw.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+    RRG_CUDA(cudaStreamSynchronize(g->stream));
+  }
+  g->uniform_ready = true;
 }
 
 void prepare_ic(rrg_graph* g) {

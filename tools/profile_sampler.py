@@ -17,6 +17,7 @@ ap.add_argument("--m", type=int, default=0)
 ap.add_argument("--ic-coop-min", type=int, default=0)
 ap.add_argument("--lt-kary", type=int, default=0)
 ap.add_argument("--ic-mode", type=int, default=0)
+ap.add_argument("--ic-rng", type=int, default=0, help="1 = fast statistical IC sampling")
 a = ap.parse_args()
 cfg = graphs.CONFIGS[a.workload]
 if a.n:
@@ -30,13 +31,14 @@ if a.ic_coop_min:
 if a.lt_kary:
     g.set_option("lt_kary", a.lt_kary)
 g.set_option("ic_mode", a.ic_mode)
+g.set_option("ic_rng", a.ic_rng)
 st = P.RRRStore(g)
 P.generate_batch(g, cfg.model, 99, a.sets, st)
 st.clear()
 t = time.time()
 P.generate_batch(g, cfg.model, 1, a.sets, st)
 s = g.last_batch_stats()
-print(f"{cfg.name} coop_min {a.ic_coop_min} kary {a.lt_kary} mode {a.ic_mode} sets {s.sets} insp/set {s.edges_inspected / s.sets:.0f} members/set "
+print(f"{cfg.name} rng {a.ic_rng} coop_min {a.ic_coop_min} kary {a.lt_kary} mode {a.ic_mode} sets {s.sets} insp/set {s.edges_inspected / s.sets:.0f} members/set "
       f"{s.members / s.sets:.1f} deferred {s.deferred} sample {s.sample_ms:.2f} ms "
       f"{s.sets / s.sample_ms * 1e3:.3e} sets/s {s.edges_inspected / s.sample_ms * 1e3:.3e} edges/s "
       f"wall {1e3 * (time.time() - t):.1f} ms")
