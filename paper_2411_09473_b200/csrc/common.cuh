@@ -119,21 +119,25 @@ constexpr uint32_t kMemCap = 1024;  // members per lane before deferring to the 
 constexpr uint32_t kTabCap = 2048;  // max table entries per lane (2 x kMemCap)
 constexpr uint32_t kTabLog0 = 6;    // initial table log2 capacity
 constexpr uint32_t kLtRecSmall = 6; // LT vertex record holds the whole in-list up to this degree
-constexpr uint32_t kLtLeaf = 8;     // search trees narrow to at most this many CDF entries
+constexpr uint32_t kLtLeafMin = 2;  // child ranges up to this go to the plain final stage
+constexpr uint32_t kLtLeafMax = 15; // ranges up to this get a LEAF: their CDF and sources
 
 // LT search tree over one in-list's CDF (upper_bound: first cdf > d, or the
 // list end). A node over candidate range [lo, hi] holds P pivots cdf[lo + t s],
 // s = max(1, ceil((hi - lo) / (P + 1))), t = 1..P (a pivot at or past hi never
 // counts); with `below` pivots <= d the answer lies in the child range below,
 // of length <= s (so the tree depth follows from the degree alone). The root
-// (P = 13) sits in the 64-byte vertex record, inner nodes (P = 31) in 128-byte
-// lines; nodes exist while hi - lo > kLtLeaf. Child c of node x is node
-// 32 x + 1 + c (root x = 0), stored at slot x - 1 of the vertex's node array.
-// Pivots are stored as floats rounded DOWN (f <= p < next(f)): counts are exact,
-// a pivot with f <= d < next(f) is re-read from the fp64 CDF (lt_count_le).
+// (P = 13) sits in the 64-byte vertex record; below it, 128-byte nodes exist
+// for child ranges longer than kLtLeafMin: inner nodes (P = 31) while the range
+// exceeds kLtLeafMax, else a leaf holding cdf[lo, hi) and src[lo, hi], which
+// resolves the step with no further load. Level 1 has 14 slots (the root's
+// children), each deeper level 32 times the one above (mixed-radix numbering).
+// Pivots and leaf entries are floats rounded DOWN (f <= p < next(f)): counts are
+// exact, an entry with f == the draw rounded down is re-read from the fp64 CDF.
 constexpr uint32_t kLtRootPivots = 13;
 constexpr uint32_t kLtNodePivots = 31;
 constexpr uint32_t kLtFanout = 32;
+constexpr uint32_t kLtRootFanout = kLtRootPivots + 1;
 __device__ __host__ __forceinline__ uint32_t lt_step(uint32_t lo, uint32_t hi, uint32_t P) {
   const uint32_t s = (hi - lo + P) / (P + 1);
   return s ? s : 1u;

@@ -1588,19 +1588,30 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
         const uint32_t below = lt_count_le<kLtRootPivots>(w + 3, dbits, d, p.cdf, lo + st0, st0);
         ent += kLtRootPivots;
         lt_child(lo, hi, kLtRootPivots, below);
-        const uint32_t nbase = w[2];
-        uint32_t x = 1 + below;
-        while (hi - lo > kLtLeaf) {  // one 128-byte node (31 pivots) per level
-          const uint4* nd = reinterpret_cast<const uint4*>(p.ltnodes + (static_cast<size_t>(nbase) + x - 1) * 32);
+        uint64_t level_base = w[2], idx = below, width = kLtRootFanout;
+        while (hi - lo > kLtLeafMin) {  // one 128-byte node per level
+          const uint4* nd = reinterpret_cast<const uint4*>(p.ltnodes + (level_base + idx) * 32);
           uint4 q[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) q[i] = __ldg(nd + i);
+          const uint32_t* qw = reinterpret_cast<const uint32_t*>(q);
+          if (hi - lo <= kLtLeafMax) {  // leaf: cdf[lo, hi) and src[lo, hi] resolve the step
+            const uint32_t cnt = lt_count_le<kLtLeafMax>(qw, dbits, d, p.cdf, lo, 1);
+#pragma unroll
+            for (uint32_t t = 0; t <= kLtLeafMax; ++t)
+              if (t == cnt) vsel = qw[kLtLeafMax + t];
+            ent += hi - lo;
+            pick = lo + cnt;
+            picked = true;
+            break;
+          }
           const uint32_t st = lt_step(lo, hi, kLtNodePivots);
-          const uint32_t bl = lt_count_le<kLtNodePivots>(reinterpret_cast<const uint32_t*>(q),
-                                                         dbits, d, p.cdf, lo + st, st);
+          const uint32_t bl = lt_count_le<kLtNodePivots>(qw, dbits, d, p.cdf, lo + st, st);
           ent += kLtNodePivots;
           lt_child(lo, hi, kLtNodePivots, bl);
-          x = kLtFanout * x + 1 + bl;
+          level_base += width;
+          idx = idx * kLtFanout + bl;
+          width *= kLtFanout;
         }
         slo = lo;
         shi = hi;
@@ -2062,19 +2073,21 @@ __global__ void k_build_ltrec(const uint32_t* off, const double* cdf, const uint
   for (int i = 0; i < 4; ++i) out[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
 }
 
-// Node slots of a vertex's search tree: 32^k per level k >= 1 while the
-// child ranges of the level above (<= the step) still exceed kLtLeaf.
+// Node slots of a vertex's search tree: level 1 has 14, each deeper level 32x
+// the one above, while the child ranges of the level above (<= its step) still
+// exceed kLtLeafMin; a level whose ranges fit kLtLeafMax is the last (leaves).
 __global__ void k_count_ltnodes(const uint32_t* off, uint32_t n, uint32_t* cnt) {
   const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n) return;
   uint32_t len = off[u + 1] - off[u];
-  uint64_t slots = 0, width = kLtFanout;
+  uint64_t slots = 0, width = kLtRootFanout;
   uint32_t P = kLtRootPivots;
   if (len > kLtRecSmall) {
     for (;;) {
       const uint32_t cl = lt_step(0, len, P);  // longest child range
-      if (cl <= kLtLeaf) break;
+      if (cl <= kLtLeafMin) break;
       slots += width;
+      if (cl <= kLtLeafMax) break;
       width *= kLtFanout;
       len = cl;
       P = kLtNodePivots;
@@ -2085,37 +2098,55 @@ __global__ void k_count_ltnodes(const uint32_t* off, uint32_t n, uint32_t* cnt) 
 
 // One block per vertex: slot s (node x = s + 1) follows its path from the root
 // and stores its 31 pivots (unreachable slots: sentinels).
-__global__ void k_build_ltnodes(const uint32_t* off, const double* cdf, const uint64_t* nodeoff,
-                                uint32_t n, uint32_t* nodes) {
+__global__ void k_build_ltnodes(const uint32_t* off, const double* cdf, const uint32_t* src,
+                                const uint64_t* nodeoff, uint32_t n, uint32_t* nodes) {
   for (uint32_t u = blockIdx.x; u < n; u += gridDim.x) {
     const uint64_t base = nodeoff[u];
     const uint32_t cnt = static_cast<uint32_t>(nodeoff[u + 1] - base);
     if (!cnt) continue;
     const uint32_t b = off[u], e = off[u + 1];
     for (uint32_t s = threadIdx.x; s < cnt; s += blockDim.x) {
-      uint32_t dig[8];
-      int nd = 0;
-      for (uint32_t x = s + 1; x; x = (x - 1) / kLtFanout) dig[nd++] = (x - 1) % kLtFanout;
+      // level and index of slot s (level 1: 14 slots, then x32 per level)
+      uint64_t r = s, width = kLtRootFanout;
+      int level = 1;
+      while (r >= width) {
+        r -= width;
+        width *= kLtFanout;
+        ++level;
+      }
+      uint32_t dig[8];  // child digits, root's first
+      for (int k = level - 1; k >= 1; --k) {
+        dig[k] = static_cast<uint32_t>(r % kLtFanout);
+        r /= kLtFanout;
+      }
+      dig[0] = static_cast<uint32_t>(r);
       uint32_t lo = b, hi = e;
       bool ok = true;
-      for (int k = nd - 1; k >= 0 && ok; --k) {
-        const uint32_t P = k == nd - 1 ? kLtRootPivots : kLtNodePivots;
-        const uint32_t lim = k == nd - 1 ? kLtRecSmall : kLtLeaf;  // the parent must narrow
-        if (dig[k] > P || hi - lo <= lim) {
+      for (int k = 0; k < level && ok; ++k) {  // parents must be inner nodes (or the root)
+        const uint32_t P = k == 0 ? kLtRootPivots : kLtNodePivots;
+        if (dig[k] > P || (k > 0 && hi - lo <= kLtLeafMax)) {
           ok = false;
           break;
         }
         lt_child(lo, hi, P, dig[k]);
         if (lo > hi) ok = false;
       }
-      ok = ok && hi - lo > kLtLeaf;
+      ok = ok && hi - lo > kLtLeafMin;
       uint32_t* out = nodes + (base + s) * 32;
-      const uint32_t st = ok ? lt_step(lo, hi, kLtNodePivots) : 1u;
-      for (uint32_t t = 1; t <= kLtNodePivots; ++t) {
-        const uint32_t i = lo + t * st;
-        out[t - 1] = ok && i < hi ? lt_fdown(cdf[i]) : kLtSentinel;
+      if (ok && hi - lo <= kLtLeafMax) {  // leaf: cdf[lo, hi) and src[lo, hi]
+        for (uint32_t t = 0; t < kLtLeafMax; ++t)
+          out[t] = lo + t < hi ? lt_fdown(cdf[lo + t]) : kLtSentinel;
+        for (uint32_t t = 0; t <= kLtLeafMax; ++t)
+          out[kLtLeafMax + t] = lo + t <= hi && lo + t < e ? src[lo + t] : 0u;
+        out[31] = 0u;
+      } else {
+        const uint32_t st = ok ? lt_step(lo, hi, kLtNodePivots) : 1u;
+        for (uint32_t t = 1; t <= kLtNodePivots; ++t) {
+          const uint32_t i = lo + t * st;
+          out[t - 1] = ok && i < hi ? lt_fdown(cdf[i]) : kLtSentinel;
+        }
+        out[31] = kLtSentinel;
       }
-      out[31] = kLtSentinel;
     }
   }
 }
@@ -2309,7 +2340,7 @@ void prepare_lt(rrg_graph* g) {
     g->ltnodes.reserve_discard(slots ? slots * 32 : 32);
     if (slots) {
       k_build_ltnodes<<<std::min<uint32_t>(g->n, 65535u * 4), 128, 0, g->stream>>>(
-          g->off.ptr, g->cdf.ptr, g->ltnodeoff.ptr, g->n, g->ltnodes.ptr);
+          g->off.ptr, g->cdf.ptr, g->src.ptr, g->ltnodeoff.ptr, g->n, g->ltnodes.ptr);
       RRG_CUDA(cudaGetLastError());
       count_launch();
     }
