@@ -53,8 +53,10 @@ uint64_t rrg_graph_num_edges(const rrg_graph* g);
 
 /* Tuning knobs; none changes any output bit. */
 typedef enum {
-  RRG_OPT_LT_SCAN = 0,  /* 0 = linear CDF scan (reference trip count), 1 = binary search
-                           (default; picks the identical index, reads ~log2(deg) entries) */
+  RRG_OPT_LT_SCAN = 0,  /* 0 = linear CDF scan (reference trip count), 1 = search tree
+                           (picks the identical index in ~log32(deg) node loads), 2 = guide
+                           table (default; identical index, one 32-byte load per step;
+                           falls back to 1 when the table does not fit in free HBM) */
   RRG_OPT_LT_COOP_MIN = 1, /* in-list length from which LT scans go warp-cooperative */
   RRG_OPT_IC_INNER = 2, /* IC edge steps per scheduling round (1..64) */
   RRG_OPT_IC_COOP_MIN = 3, /* IC in-list length from which the warp expands it cooperatively
@@ -67,7 +69,9 @@ typedef enum {
   RRG_OPT_IC_RNG = 7 /* IC randomness: 0 (default) the reference's per-slot stream,
                         sets bit-identical; 1 FAST: counter-based per-edge draws with
                         geometric skipping over equal-weight in-lists -- same set
-                        distribution, statistical parity only */
+                        distribution, statistical parity only */,
+  RRG_OPT_LT_GUIDE_MULT = 8 /* LT guide buckets per in-edge, 1..16 (default 2; table =
+                               32 B x mult x m; larger = fewer multi-entry buckets) */
 } rrg_option;
 rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value);
 

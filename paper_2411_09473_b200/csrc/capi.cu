@@ -268,7 +268,7 @@ rrg_status rrg_graph_prepare(rrg_graph* g, rrg_model model) {
   if (model != RRG_IC && model != RRG_LT) return invalid("unknown diffusion model");
   return guarded([&]() -> rrg_status {
     if (model == RRG_IC) prepare_ic(g);
-    else prepare_lt(g);
+    else prepare_lt_mode(g);
     return RRG_OK;
   });
 }
@@ -298,8 +298,13 @@ rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value) {
   if (!g) return invalid("null graph");
   switch (opt) {
     case RRG_OPT_LT_SCAN:
-      if (value != kLtLinear && value != kLtBsearch) return invalid("LT scan must be 0 or 1");
+      if (value != kLtLinear && value != kLtBsearch && value != kLtGuide)
+        return invalid("LT scan must be 0 (linear), 1 (search tree) or 2 (guide table)");
       g->lt_scan = static_cast<int>(value);
+      return RRG_OK;
+    case RRG_OPT_LT_GUIDE_MULT:
+      if (value < 1 || value > 16) return invalid("lt_guide_mult must be in [1, 16]");
+      g->lt_guide_mult = static_cast<uint32_t>(value);
       return RRG_OK;
     case RRG_OPT_LT_COOP_MIN:
       if (value < 2) return invalid("coop_min must be >= 2");
@@ -408,14 +413,15 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
   g->last = rrg_batch_stats{};
   if (count == 0) return RRG_OK;
   return guarded([&]() -> rrg_status {
+    int lt_mode = kLtLinear;
     if (model == RRG_IC) prepare_ic(g);
-    else prepare_lt(g);
+    else lt_mode = prepare_lt_mode(g);
     const bool ic_fast = model == RRG_IC && g->ic_rng == 1;
     if (ic_fast) prepare_ic_fast(g);
     if (!fused) s->counter_complete = false;
     const cudaStream_t st = g->stream;
     const int block = sampler_block();
-    const int per_sm = std::min(kMaxBlocksPerSm, sampler_blocks_per_sm(model, g->ic_inner));
+    const int per_sm = std::min(kMaxBlocksPerSm, sampler_blocks_per_sm(model, g->ic_inner, lt_mode));
     const uint64_t full_grid = static_cast<uint64_t>(g->num_sms) * per_sm;
     ensure_lane_scratch(g, full_grid * block);
     const uint64_t kChunk = 1ull << 30;  // batch-local indices are u32
@@ -482,7 +488,9 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.slot_len = s->slot_len.ptr;
       p.counter = fused ? s->counter.ptr : nullptr;
       p.ctl = g->ctl.ptr;
-      p.lt_scan = (g->lt_scan == kLtBsearch && g->cdf_monotone) ? kLtBsearch : kLtLinear;
+      p.lt_scan = lt_mode;
+      p.ltguide = g->ltguide.ptr;
+      p.lt_guide_mult = g->lt_guide_mult;
       p.coop_min = g->coop_min;
       p.jtab = g->jtab.ptr;
       p.jtab16 = g->jtab16.ptr;

@@ -168,6 +168,27 @@ __device__ __forceinline__ uint32_t lt_count_le(const uint32_t* w, uint32_t dbit
   return sure;
 }
 
+// LT guide table (indexed search over each in-list's CDF). Vertex u with
+// degree D gets G = mult * D buckets of equal width on the draw's 53-bit
+// integer x53 (uniform01() = x53 * 2^-53): bucket g = floor(x53 * G / 2^53),
+// i.e. x53 in [ceil(g 2^53 / G), ceil((g+1) 2^53 / G)). With A_g = #{cdf <= the
+// bucket's smallest draw}, every draw of bucket g picks an index in
+// [A_g, A_{g+1}] (the CDF is non-decreasing), so the entry of bucket g resolves
+// the step by itself when the span A_{g+1} - A_g is 0 (no CDF entry falls in
+// the bucket) or 1 (one compare against cdf[A_g], stored as a float rounded
+// down; equality re-reads the fp64 CDF). Longer spans (rare: ~mult^-2 / 2 of
+// the buckets) search cdf[A_g, A_{g+1}). The entry also carries what the NEXT
+// step needs of the chosen source -- its id, in-list offset and degree -- so a
+// walk step is one 32-byte load. Entry words (guide[2 i], guide[2 i + 1]):
+//   x: A_g (local index)  y: pivot bits | kGuideSpan0 | kGuideSearch
+//   z, w, x': candidate A_g     -> source id (kGuideNone past the list), off, deg
+//   y', z', w': candidate A_g+1 -> source id, off, deg   (span 1)
+//               or y' = span                              (kGuideSearch)
+constexpr uint32_t kGuideNone = 0xffffffffu;
+constexpr uint32_t kGuideSpan0 = 0x40000000u;   // pivots are floats in [0, 1]: bits 30, 31 free
+constexpr uint32_t kGuideSearch = 0x80000000u;
+constexpr uint32_t kGuidePivot = 0x3fffffffu;
+
 __device__ __forceinline__ uint32_t vhash(uint32_t v) { return v * 0x9E3779B1u; }
 
 __device__ __forceinline__ bool tab_contains(const uint64_t* tab, uint32_t tag, uint32_t lg,

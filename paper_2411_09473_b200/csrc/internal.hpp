@@ -70,7 +70,7 @@ struct DevBuf {
   }
 };
 
-enum LtScan : int { kLtLinear = 0, kLtBsearch = 1 };
+enum LtScan : int { kLtLinear = 0, kLtBsearch = 1, kLtGuide = 2 };
 
 // Per-lane sampler scratch: visit-order list + tagged hash table + tag.
 // Tagged tables are never cleared; that is sound because the region layouts
@@ -109,6 +109,10 @@ struct rrg_graph {
   rrgpu::DevBuf<uint32_t> ltrec; // LT: 64-byte vertex records (k_build_ltrec), monotone CDF only
   rrgpu::DevBuf<uint64_t> ltnodeoff;  // LT: first search-tree slot per vertex (u64[n+1])
   rrgpu::DevBuf<uint32_t> ltnodes;    // LT: search-tree nodes, 32 floats (31 pivots) each
+  rrgpu::DevBuf<uint4> ltguide;  // LT: guide table, 32 bytes per bucket (common.cuh), lazy
+  uint32_t lt_guide_mult = 2;    // LT: guide buckets per in-edge
+  uint32_t lt_guide_built = 0;   // multiplier the current table was built with (0: none)
+  bool lt_search_ready = false;  // LT: records + search trees built
   rrgpu::DevBuf<uint64_t> jtab;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab16;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab256;  // IC: byte tables of T^(256 a), a = 1..15 (3.75 MB)
@@ -186,6 +190,8 @@ struct SampleParams {
   const double* cdf;
   const uint4* ltrec;    // LT vertex records (search mode), 4 x uint4 per vertex
   const uint32_t* ltnodes;  // LT search-tree nodes (32 floats each)
+  const uint4* ltguide;     // LT guide table (guide mode), 2 x uint4 per bucket
+  uint32_t lt_guide_mult;   // LT guide buckets per in-edge
   uint64_t run_seed;
   uint64_t base_slot;
   uint64_t count;
@@ -222,12 +228,16 @@ void prepare_ic_fast(rrg_graph* g);
 void launch_fast(const SampleParams& p, int grid, bool bitmap, uint32_t* bitmaps, uint32_t* lists,
                  uint32_t workers, cudaStream_t s);
 void launch_fast_lane(const SampleParams& p, int grid, cudaStream_t s);
-void prepare_lt(rrg_graph* g);
+void prepare_lt(rrg_graph* g);  // fp64 CDF + monotone flag
+// prepare_lt + what the graph's LT scan mode needs; returns the mode to launch
+// (guide falls back to search when the table does not fit, both to linear
+// when the CDF is not monotone)
+int prepare_lt_mode(rrg_graph* g);
 // converts d_off64 into g->off and validates offsets/sources on the device;
 // returns a bit mask of violations (1 offsets, 2 sources), 0 if clean
 uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64);
 int sampler_block();
-int sampler_blocks_per_sm(int model, uint32_t ic_inner);
+int sampler_blocks_per_sm(int model, uint32_t ic_inner, int lt_mode = 1);
 // IC schedules: lane per sample; warp per sample over its 32 lanes' scratch
 // (sets up to 32K members); CTA per sample over its 256 lanes' scratch (256K).
 enum Schedule : int { kSchedLane = 0, kSchedWarp = 1, kSchedCta = 2 };

@@ -1735,6 +1735,299 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
   flush_counters(p, insp, ent);
 }
 
+// Guide-mode LT step resolution (common.cuh, "LT guide table"): the bucket
+// entry (e0, e1) of vertex u for draw x gives the chosen index `pick` (local;
+// deg_u = none) and what the next step needs of the chosen source.
+__device__ __forceinline__ void lt_guide_resolve(const SampleParams& p, const uint4 e0,
+                                                 const uint4 e1, uint64_t x, uint32_t offu,
+                                                 uint32_t degu, uint32_t& pick, uint32_t& v,
+                                                 uint32_t& offv, uint32_t& degv, uint64_t& ent) {
+  const uint32_t A = e0.x;
+  const uint32_t pw = e0.y;
+  if (pw & kGuideSpan0) {  // no CDF entry inside the bucket: index A_g whatever the draw
+    pick = A;
+    v = e0.z;
+    offv = e0.w;
+    degv = e1.x;
+    return;
+  }
+  const double d = __ull2double_rn(x >> 11) * 0x1.0p-53;  // uniform01(), exact
+  const uint32_t dbits = __float_as_uint(__double2float_rd(d));
+  if (!(pw & kGuideSearch)) {  // one entry: pick A_g + [cdf[A_g] <= d]
+    const uint32_t f = pw & kGuidePivot;
+    const bool le = f < dbits || (f == dbits && __ldg(p.cdf + offu + A) <= d);
+    if (le) {
+      pick = A + 1;
+      v = e1.y;
+      offv = e1.z;
+      degv = e1.w;
+    } else {
+      pick = A;
+      v = e0.z;
+      offv = e0.w;
+      degv = e1.x;
+    }
+    return;
+  }
+  // span >= 2 (rare): count cdf[A_g, A_g + span) <= d, eight loads in flight
+  const uint32_t span = e1.y;
+  const double* c = p.cdf + offu + A;
+  uint32_t cnt = 0;
+  for (uint32_t t = 0; t < span; t += 8) {
+    double q[8];
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) q[k] = t + k < span ? __ldg(c + t + k) : 2.0;
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) cnt += q[k] <= d ? 1u : 0u;
+    if (cnt < t + 8) break;  // the entries are sorted: the first one > d ends the count
+  }
+  ent += span;
+  pick = A + cnt;
+  if (pick < degu) {
+    v = __ldg(p.src + offu + pick);
+    offv = __ldg(p.off + v);
+    degv = __ldg(p.off + v + 1) - offv;
+  } else {
+    v = kGuideNone;
+  }
+}
+
+__device__ __forceinline__ void lt_guide_fetch(const SampleParams& p, uint32_t offu, uint32_t degu,
+                                               uint64_t x, uint4& e0, uint4& e1) {
+  if (!degu) return;
+  const uint64_t G = static_cast<uint64_t>(degu) * p.lt_guide_mult;
+  const uint64_t gi = static_cast<uint64_t>(offu) * p.lt_guide_mult + __umul64hi(x & ~0x7ffull, G);
+  e0 = __ldg(p.ltguide + 2 * gi);
+  e1 = __ldg(p.ltguide + 2 * gi + 1);
+}
+
+// Visited set of a guide-mode walk while it is short: a 1024-bit filter per lane
+// in shared memory (two bits per member; lane words interleaved across the
+// block, so every access is bank-conflict free) in front of the walk's member
+// list. Only a filter hit scans the list (the whole warp, one round trip), so
+// the common "not visited" answer never leaves the SM, and the per-lane hash
+// tables (global memory, DRAM-bound once 150K lanes each own one) are used only
+// by walks longer than kLtFiltMax members.
+constexpr uint32_t kLtFiltWords = 32;
+constexpr uint32_t kLtFiltMax = 128;
+constexpr uint32_t kTabLog = 11;  // 2^11 = kTabCap entries: load <= 1/2 up to kMemCap members
+static_assert((1u << kTabLog) == kTabCap, "guide-mode tables use the whole lane table");
+__device__ __forceinline__ void lfilt_bits(uint32_t v, uint32_t& w1, uint32_t& b1, uint32_t& w2,
+                                           uint32_t& b2) {
+  const uint32_t h = v * 0x9E3779B1u;
+  w1 = h >> 27;
+  b1 = (h >> 22) & 31u;
+  w2 = (h >> 17) & 31u;
+  b2 = (h >> 12) & 31u;
+}
+// Warp-cooperative emit (all 32 lanes, converged): every lane with `pending`
+// has a finished set in its own member list; the warp copies them one after the
+// other into staging -- each set's members loaded 32 per round trip by the whole
+// warp (instead of 8 per round trip by its lane while the warp's other lanes
+// wait at the reconvergence point) -- with the fused counter increments.
+// Returns, to each pending lane, whether its set was written (false: staging
+// full; the slot was recorded for a re-run).
+__device__ __forceinline__ bool warp_emit_pending(const SampleParams& p, bool pending,
+                                                  uint32_t idx, uint32_t nmem,
+                                                  const uint32_t* lists_warp) {
+  const int lane = threadIdx.x & 31;
+  unsigned em = __ballot_sync(kFull, pending);
+  bool mine = false;
+  while (em) {
+    const int L = __ffs(em) - 1;
+    em &= em - 1;
+    const uint32_t nL = __shfl_sync(kFull, nmem, L);
+    const uint32_t iL = __shfl_sync(kFull, idx, L);
+    unsigned long long pos = 0;
+    if (lane == L) pos = atomicAdd(&p.ctl->cursor, (unsigned long long)nL);
+    pos = __shfl_sync(kFull, pos, L);
+    if (pos + nL > p.stage_cap) {
+      if (lane == L) restage_slot(p, iL, nL);
+      continue;
+    }
+    const uint32_t* __restrict__ src = lists_warp + static_cast<size_t>(L) * kMemCap;
+    uint32_t* __restrict__ out = p.stage + pos;
+    for (uint32_t t = 0; t < nL; t += 128) {
+      uint32_t v[4];
+#pragma unroll
+      for (uint32_t k = 0; k < 4; ++k) {
+        const uint32_t i = t + 32 * k + lane;
+        v[k] = i < nL ? src[i] : 0u;
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < 4; ++k) {
+        const uint32_t i = t + 32 * k + lane;
+        if (i < nL) {
+          out[i] = v[k];
+          if (p.counter) atomicAdd(p.counter + v[k], 1u);
+        }
+      }
+    }
+    if (lane == L) {
+      p.slot_start[iL] = pos;
+      p.slot_len[iL] = nL;
+      mine = true;
+    }
+  }
+  return mine;
+}
+
+// K2g: LT walk, guide mode. Lane per walk; every step is ONE 32-byte load (the
+// bucket entry of the current vertex for this step's draw), issued as soon as
+// the previous step chose its source; the draw of the step after is computed
+// while it is in flight, and the chosen source's visited test runs against the
+// shared-memory filter. Same index as the reference's linear scan
+// (sampling.hpp:127-137), same draws in the same order.
+__global__ void __launch_bounds__(kBlock, 4) k_sample_lt_guide(const SampleParams p) {
+  __shared__ uint32_t filt_all[kLtFiltWords * kBlock];
+  uint32_t* filt = filt_all + threadIdx.x;  // word w at filt[w * kBlock]
+  const int lane = threadIdx.x & 31;
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t* mem = p.lists + gid * kMemCap;
+  const uint32_t* lists_warp = p.lists + (gid - lane) * kMemCap;
+  uint64_t* tabs_warp = p.tabs + (gid - lane) * kTabCap;
+  uint64_t* tab = p.tabs + gid * kTabCap;
+  uint32_t tag = p.tags[gid];
+  Xoshiro rng{0, 0, 0, 0};
+  // per-lane walk state; `pending` / `check` / `rebuild` are resolved by the
+  // whole warp at the top of the loop
+  bool active = false, exhausted = false, big = false;
+  bool pending = false;  // walk ended: its set waits for the cooperative emit
+  bool check = false;    // chosen source vchk hit the filter: scan the members
+  bool rebuild = false;  // walk reached kLtFiltMax members: fill its hash table
+  uint32_t idx = 0, nmem = 0;
+  uint32_t offu = 0, degu = 0, vchk = 0, offc = 0, degc = 0;
+  uint64_t x = 0, xn = 0;  // this step's draw (its entry is in e0/e1) and the next step's
+  uint4 e0 = make_uint4(0, 0, 0, 0), e1 = make_uint4(0, 0, 0, 0);
+  uint64_t insp = 0, sinsp = 0, ent = 0;
+
+  for (;;) {
+    // (1) filter hits: the warp scans each such lane's members (<= kLtFiltMax,
+    //     one round trip) for its chosen source
+    unsigned cm = __ballot_sync(kFull, check);
+    while (cm) {
+      const int L = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const uint32_t nL = __shfl_sync(kFull, nmem, L);
+      const uint32_t vL = __shfl_sync(kFull, vchk, L);
+      const uint32_t* mL = lists_warp + static_cast<size_t>(L) * kMemCap;
+      uint32_t q[kLtFiltMax / 32];
+#pragma unroll
+      for (uint32_t k = 0; k < kLtFiltMax / 32; ++k) {
+        const uint32_t i = 32 * k + lane;
+        q[k] = i < nL ? mL[i] : kGuideNone;
+      }
+      bool hit = false;
+#pragma unroll
+      for (uint32_t k = 0; k < kLtFiltMax / 32; ++k) hit |= q[k] == vL;
+      hit = __any_sync(kFull, hit);
+      if (lane == L) {
+        check = false;
+        if (hit) {  // chosen already visited (sampling.hpp:137): the walk ends
+          pending = true;
+          active = false;
+        } else {  // a new member; its next step's entry is already in flight
+          uint32_t w1, b1, w2, b2;
+          lfilt_bits(vL, w1, b1, w2, b2);
+          filt[w1 * kBlock] |= 1u << b1;
+          filt[w2 * kBlock] |= 1u << b2;
+          mem[nmem++] = vL;
+          offu = offc;
+          degu = degc;
+          rebuild = nmem == kLtFiltMax;
+        }
+      }
+    }
+    // (2) finished walks -> staging (cooperative copy + fused counter)
+    if (warp_emit_pending(p, pending, idx, nmem, lists_warp)) insp += sinsp;
+    pending = false;
+    // (3) walks that outgrew the filter: the warp inserts their members into
+    //     their (fresh-tagged) per-lane tables, kTabCap entries, load <= 1/2
+    unsigned rm = __ballot_sync(kFull, rebuild);
+    if (rebuild) {
+      ++tag;
+      big = true;
+      rebuild = false;
+    }
+    while (rm) {
+      const int L = __ffs(rm) - 1;
+      rm &= rm - 1;
+      const uint32_t nL = __shfl_sync(kFull, nmem, L);
+      const uint32_t tL = __shfl_sync(kFull, tag, L);
+      const uint32_t* mL = lists_warp + static_cast<size_t>(L) * kMemCap;
+      uint64_t* tL_tab = tabs_warp + static_cast<size_t>(L) * kTabCap;
+      for (uint32_t i = lane; i < nL; i += 32) tab_insert_atomic(tL_tab, tL, kTabLog, mL[i]);
+    }
+    __syncwarp();
+
+    if (fetch_slot(p, !active && !exhausted, exhausted, idx)) {
+      rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
+      const uint32_t u = static_cast<uint32_t>(rng.below(p.n));
+      offu = __ldg(p.off + u);
+      degu = __ldg(p.off + u + 1) - offu;
+      x = rng.next();  // the first step's draw (sampling.hpp:127)
+      lt_guide_fetch(p, offu, degu, x, e0, e1);
+      xn = rng.next();
+#pragma unroll
+      for (uint32_t w = 0; w < kLtFiltWords; ++w) filt[w * kBlock] = 0u;
+      uint32_t w1, b1, w2, b2;
+      lfilt_bits(u, w1, b1, w2, b2);
+      filt[w1 * kBlock] |= 1u << b1;
+      filt[w2 * kBlock] |= 1u << b2;
+      big = false;
+      mem[0] = u;
+      nmem = 1;
+      sinsp = 0;
+      active = true;
+    }
+    if (__all_sync(kFull, !active)) break;
+    if (!active) continue;
+
+    uint32_t pick = degu, v = kGuideNone, offv = 0, degv = 0;
+    if (degu) {
+      lt_guide_resolve(p, e0, e1, x, offu, degu, pick, v, offv, degv, ent);
+      ent += 4;  // the 32-byte bucket entry (in 8-byte units)
+    }
+    sinsp += pick < degu ? pick + 1 : degu;  // reference trip count (sampling.hpp:130-136)
+    bool stop = v == kGuideNone;
+    if (!stop) {
+      lt_guide_fetch(p, offv, degv, xn, e0, e1);  // next step's entry, in flight now
+      x = xn;
+      xn = rng.next();
+      if (big) {
+        stop = tab_find_or_insert(tab, tag, kTabLog, v);  // chosen already visited (:137)
+      } else {
+        uint32_t w1, b1, w2, b2;
+        lfilt_bits(v, w1, b1, w2, b2);
+        const uint32_t f1 = filt[w1 * kBlock], f2 = filt[w2 * kBlock];
+        if ((f1 >> b1) & (f2 >> b2) & 1u) {  // maybe visited: the warp scans (1)
+          check = true;
+          vchk = v;
+          offc = offv;
+          degc = degv;
+          continue;
+        }
+        filt[w1 * kBlock] |= 1u << b1;
+        filt[w2 * kBlock] |= 1u << b2;
+      }
+    }
+    if (stop) {  // written by the warp at the top of the loop
+      pending = true;
+      active = false;
+    } else if (nmem == kMemCap) {
+      defer_slot(p, idx);
+      active = false;
+    } else {
+      mem[nmem++] = v;
+      rebuild = !big && nmem == kLtFiltMax;
+      offu = offv;
+      degu = degv;
+    }
+  }
+  p.tags[gid] = tag;
+  flush_counters(p, insp, ent);
+}
+
 // ---------------------------------------------------------------------------
 // Big-set path: warp per deferred slot with an n-bit visited map. IC: the warp
 // loads 32 in-edges per chunk (coalesced), tests visited and computes the
@@ -2151,6 +2444,106 @@ __global__ void k_build_ltnodes(const uint32_t* off, const double* cdf, const ui
   }
 }
 
+// Guide table (common.cuh "LT guide table"): thread per chunk of kGuideChunk
+// consecutive buckets of the flat bucket space [0, mult m) (vertex u owns
+// [mult off[u], mult off[u+1])). The chunk finds its first vertex and A_g by
+// binary search, then merges buckets against the CDF: A_{g+1} = #{cdf <= the
+// smallest draw of bucket g+1}, that draw kept exactly as Q + (R > 0) with
+// g 2^53 = Q G + R updated incrementally.
+constexpr uint32_t kGuideChunk = 64;
+
+__device__ __forceinline__ void guide_cand(const uint32_t* off, const uint32_t* src, uint32_t b,
+                                           uint32_t deg, uint32_t j, uint32_t& v, uint32_t& ov,
+                                           uint32_t& dv) {
+  if (j < deg) {
+    v = __ldg(src + b + j);
+    ov = __ldg(off + v);
+    dv = __ldg(off + v + 1) - ov;
+  } else {
+    v = kGuideNone;
+    ov = 0;
+    dv = 0;
+  }
+}
+
+__global__ void k_build_ltguide(const uint32_t* off, const double* cdf, const uint32_t* src,
+                                uint32_t n, uint64_t m, uint32_t mult, uint4* guide) {
+  const uint64_t total = static_cast<uint64_t>(mult) * m;
+  const uint64_t nchunks = (total + kGuideChunk - 1) / kGuideChunk;
+  const uint64_t two53 = 1ull << 53;
+  for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < nchunks;
+       c += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t i = c * kGuideChunk;
+    const uint64_t iend = min(i + kGuideChunk, total);
+    // the vertex owning bucket i: the largest u with off[u] <= i / mult
+    const uint32_t q = static_cast<uint32_t>(i / mult);
+    uint32_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+      const uint32_t mid = lo + (hi - lo + 1) / 2;
+      if (__ldg(off + mid) <= q) lo = mid;
+      else hi = mid - 1;
+    }
+    uint32_t u = lo;
+    uint32_t b = __ldg(off + u), deg = __ldg(off + u + 1) - b;
+    uint64_t G = static_cast<uint64_t>(mult) * deg;
+    uint64_t g = i - static_cast<uint64_t>(mult) * b;
+    uint64_t q0 = two53 / G, r0 = two53 % G;
+    const unsigned __int128 N = static_cast<unsigned __int128>(g) << 53;
+    uint64_t Q = static_cast<uint64_t>(N / G), R = static_cast<uint64_t>(N % G);
+    // A_g = #{cdf <= dmin_g}: binary search on the sorted in-list
+    const double d0 = static_cast<double>(Q + (R ? 1 : 0)) * 0x1.0p-53;
+    uint32_t A = 0, ahi = deg;
+    while (A < ahi) {
+      const uint32_t mid = A + (ahi - A) / 2;
+      if (__ldg(cdf + b + mid) <= d0) A = mid + 1;
+      else ahi = mid;
+    }
+    for (; i < iend; ++i, ++g) {
+      if (g == G) {  // next vertex with in-edges; its bucket 0 has the draw 0
+        do {
+          ++u;
+          b = __ldg(off + u);
+          deg = __ldg(off + u + 1) - b;
+        } while (deg == 0);
+        G = static_cast<uint64_t>(mult) * deg;
+        g = 0;
+        q0 = two53 / G;
+        r0 = two53 % G;
+        Q = 0;
+        R = 0;
+        A = 0;
+        while (A < deg && __ldg(cdf + b + A) <= 0.0) ++A;
+      }
+      uint64_t Q1 = Q + q0, R1 = R + r0;
+      if (R1 >= G) {
+        R1 -= G;
+        ++Q1;
+      }
+      const double d1 = static_cast<double>(Q1 + (R1 ? 1 : 0)) * 0x1.0p-53;  // 1.0 for g+1 = G
+      uint32_t A1 = A;
+      while (A1 < deg && __ldg(cdf + b + A1) <= d1) ++A1;
+      const uint32_t span = A1 - A;
+      uint4 e0, e1;
+      e0.x = A;
+      e0.y = (A < deg ? lt_fdown(__ldg(cdf + b + A)) : 0u) |
+             (span == 0 ? kGuideSpan0 : span >= 2 ? kGuideSearch : 0u);
+      guide_cand(off, src, b, deg, A, e0.z, e0.w, e1.x);
+      if (span == 1) {
+        guide_cand(off, src, b, deg, A + 1, e1.y, e1.z, e1.w);
+      } else {
+        e1.y = span >= 2 ? span : kGuideNone;
+        e1.z = 0;
+        e1.w = 0;
+      }
+      guide[2 * i] = e0;
+      guide[2 * i + 1] = e1;
+      A = A1;
+      Q = Q1;
+      R = R1;
+    }
+  }
+}
+
 __global__ void k_check_sources(const uint32_t* src, uint64_t m, uint32_t n, uint32_t* bad) {
   bool ok = true;
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
@@ -2182,10 +2575,12 @@ uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64) {
 
 int sampler_block() { return kBlock; }
 
-int sampler_blocks_per_sm(int model, uint32_t) {
+int sampler_blocks_per_sm(int model, uint32_t, int lt_mode) {
   int b = 0;
   if (model == RRG_IC)
     RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_ic, kBlock, 0));
+  else if (lt_mode == kLtGuide)
+    RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_lt_guide, kBlock, 0));
   else
     RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_lt<16>, kBlock, 0));
   return b < 1 ? 1 : b;
@@ -2209,6 +2604,8 @@ void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inne
     } else {
       k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
     }
+  } else if (p.lt_scan == kLtGuide) {
+    k_sample_lt_guide<<<grid, kBlock, 0, s>>>(p);
   } else {
     switch (p.lt_kary) {
       case 2: k_sample_lt<2><<<grid, kBlock, 0, s>>>(p); break;
@@ -2317,41 +2714,76 @@ void prepare_lt(rrg_graph* g) {
   RRG_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
   RRG_CUDA(cudaStreamSynchronize(g->stream));
   g->cdf_monotone = hbad == 0;
-  if (g->cdf_monotone && g->n) {
-    // search trees of the long in-lists, then the vertex records
-    DevBuf<uint32_t> cnt;
-    cnt.reserve_discard(g->n);
-    k_count_ltnodes<<<(g->n + 255) / 256, 256, 0, g->stream>>>(g->off.ptr, g->n, cnt.ptr);
-    RRG_CUDA(cudaGetLastError());
-    count_launch();
-    g->ltnodeoff.reserve_discard(static_cast<size_t>(g->n) + 1);
-    DevBuf<uint64_t> tmp;
-    exclusive_scan_u32(cnt.ptr, g->ltnodeoff.ptr, g->n, tmp, g->stream);
-    uint64_t slots = 0;
-    RRG_CUDA(cudaMemcpyAsync(&slots, g->ltnodeoff.ptr + g->n, 8, cudaMemcpyDeviceToHost,
-                             g->stream));
-    RRG_CUDA(cudaStreamSynchronize(g->stream));
-    if (slots >= (1ull << 32)) {  // node slots are u32 in the records: use the plain search
-      g->ltrec.release();
-      g->ltnodes.release();
-      g->cdf_ready = true;
-      return;
-    }
-    g->ltnodes.reserve_discard(slots ? slots * 32 : 32);
-    if (slots) {
-      k_build_ltnodes<<<std::min<uint32_t>(g->n, 65535u * 4), 128, 0, g->stream>>>(
-          g->off.ptr, g->cdf.ptr, g->src.ptr, g->ltnodeoff.ptr, g->n, g->ltnodes.ptr);
-      RRG_CUDA(cudaGetLastError());
-      count_launch();
-    }
-    g->ltrec.reserve_discard(static_cast<size_t>(g->n) * 16);
-    k_build_ltrec<<<(g->n + 255) / 256, 256, 0, g->stream>>>(
-        g->off.ptr, g->cdf.ptr, g->src.ptr, g->ltnodeoff.ptr, g->n, g->ltrec.ptr);
-    RRG_CUDA(cudaGetLastError());
-    count_launch();
-    RRG_CUDA(cudaStreamSynchronize(g->stream));
-  }
   g->cdf_ready = true;
+}
+
+// LT search mode: vertex records + search trees (monotone CDF only).
+void prepare_lt_search(rrg_graph* g) {
+  if (g->lt_search_ready) return;
+  g->lt_search_ready = true;
+  if (!g->cdf_monotone || !g->n) return;
+  DevBuf<uint32_t> cnt;
+  cnt.reserve_discard(g->n);
+  k_count_ltnodes<<<(g->n + 255) / 256, 256, 0, g->stream>>>(g->off.ptr, g->n, cnt.ptr);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+  g->ltnodeoff.reserve_discard(static_cast<size_t>(g->n) + 1);
+  DevBuf<uint64_t> tmp;
+  exclusive_scan_u32(cnt.ptr, g->ltnodeoff.ptr, g->n, tmp, g->stream);
+  uint64_t slots = 0;
+  RRG_CUDA(cudaMemcpyAsync(&slots, g->ltnodeoff.ptr + g->n, 8, cudaMemcpyDeviceToHost,
+                           g->stream));
+  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  if (slots >= (1ull << 32)) {  // node slots are u32 in the records: use the plain search
+    g->ltrec.release();
+    g->ltnodes.release();
+    return;
+  }
+  g->ltnodes.reserve_discard(slots ? slots * 32 : 32);
+  if (slots) {
+    k_build_ltnodes<<<std::min<uint32_t>(g->n, 65535u * 4), 128, 0, g->stream>>>(
+        g->off.ptr, g->cdf.ptr, g->src.ptr, g->ltnodeoff.ptr, g->n, g->ltnodes.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+  }
+  g->ltrec.reserve_discard(static_cast<size_t>(g->n) * 16);
+  k_build_ltrec<<<(g->n + 255) / 256, 256, 0, g->stream>>>(
+      g->off.ptr, g->cdf.ptr, g->src.ptr, g->ltnodeoff.ptr, g->n, g->ltrec.ptr);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+  RRG_CUDA(cudaStreamSynchronize(g->stream));
+}
+
+// LT guide mode: 32 bytes per bucket, mult buckets per in-edge. False (and no
+// table) when the CDF is not monotone or the table would not fit in free HBM.
+bool prepare_lt_guide(rrg_graph* g) {
+  if (!g->cdf_monotone || !g->m) return false;
+  if (g->lt_guide_built == g->lt_guide_mult && g->ltguide.ptr) return true;
+  g->ltguide.release();
+  g->lt_guide_built = 0;
+  const uint64_t entries = static_cast<uint64_t>(g->lt_guide_mult) * g->m;
+  size_t freeb = 0, totalb = 0;
+  RRG_CUDA(cudaMemGetInfo(&freeb, &totalb));
+  if (entries * 32 + (2ull << 30) > freeb) return false;
+  g->ltguide.reserve_discard(2 * entries);
+  const uint64_t chunks = (entries + kGuideChunk - 1) / kGuideChunk;
+  const uint64_t grid = std::min<uint64_t>((chunks + 127) / 128, 1u << 20);
+  k_build_ltguide<<<static_cast<unsigned>(grid), 128, 0, g->stream>>>(
+      g->off.ptr, g->cdf.ptr, g->src.ptr, g->n, g->m, g->lt_guide_mult, g->ltguide.ptr);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  g->lt_guide_built = g->lt_guide_mult;
+  return true;
+}
+
+// The structures the graph's LT scan mode needs; returns the mode launches use.
+int prepare_lt_mode(rrg_graph* g) {
+  prepare_lt(g);
+  if (g->lt_scan == kLtGuide && prepare_lt_guide(g)) return kLtGuide;
+  if (g->lt_scan == kLtLinear || !g->cdf_monotone) return kLtLinear;
+  prepare_lt_search(g);
+  return kLtBsearch;
 }
 
 }  // namespace rrgpu

@@ -49,6 +49,12 @@ def test_cfg4_full_size_lt(cuda, oracle, cfg4_graph):
     P.generate_batch(g, 1, 1, 1 << 14, st_b)
     off_b, mem_b = st_b.export()
     assert (off_b == off[: off_b.size]).all() and (mem_b == mem[: mem_b.size]).all()
+    g.set_option("lt_scan", 2)
+    st_c = P.RRRStore(g)
+    P.generate_batch(g, 1, 1, 1 << 16, st_c)
+    off_c, mem_c = st_c.export()
+    assert (off_c == off).all() and (mem_c == mem).all(), "guide mode != search mode"
+    assert (st_c.counter() == st_a.counter()).all()
 
 
 @pytest.mark.parametrize("name,count", [("cfg1", 1 << 20), ("cfg3", 1 << 20)])

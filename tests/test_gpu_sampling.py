@@ -97,6 +97,97 @@ def test_lt_search_mode_is_identical(cuda, oracle, kary):
     assert_sets_equal(off_b, mem_b, ref)
 
 
+def _boundary_lt_graph(seed, skew=False):
+    rng = np.random.default_rng(seed)
+    degs = list(range(0, 20)) + [31, 32, 33, 127, 128, 129, 255, 256, 257, 258, 1023, 1024,
+                                 1025, 4095, 4096, 4097]
+    n = len(degs)
+    dst = np.repeat(np.arange(n, dtype=np.uint32), degs)
+    src = rng.integers(0, n, dst.size).astype(np.uint32)
+    w = rng.uniform(0.0, 1.0, dst.size).astype(np.float32)
+    w[rng.random(dst.size) < 0.2] = 0.0
+    if skew:  # heavy-tailed weights: many CDF entries per guide bucket (search spans)
+        w = (w ** 8).astype(np.float32)
+    roff, rsrc, rw = P.build_graph(n, src, dst, w)
+    P.normalize_lt_weights(roff, rw)
+    rw *= np.float32(0.97)  # leave "no in-neighbour chosen" reachable
+    return roff, rsrc, rw
+
+
+@pytest.mark.parametrize("mult", [1, 2, 3, 16])
+@pytest.mark.parametrize("skew", [False, True])
+def test_lt_guide_mode_is_identical(cuda, oracle, mult, skew):
+    """Guide-table steps (lt_scan 2, common.cuh) pick the reference's index:
+    boundary degrees, zero weights (flat CDF runs = empty buckets), sums below 1,
+    heavy-tailed weights (buckets spanning several entries), every multiplier."""
+    arrays = _boundary_lt_graph(43, skew)
+    _, _, off_a, mem_a = gpu_sample(arrays, LT, 13, 6000, lt_scan=0)
+    g, _, off_b, mem_b = gpu_sample(arrays, LT, 13, 6000, lt_scan=2, lt_guide_mult=mult)
+    assert (off_a == off_b).all() and (mem_a == mem_b).all()
+    ref = oracle.graph(*arrays).sample(LT, 13, 0, 6000, workers=4)
+    assert_sets_equal(off_b, mem_b, ref)
+
+
+def test_lt_guide_mode_full_weight_and_exact_ties(cuda, oracle):
+    """In-lists whose CDF reaches exactly 1.0, single in-edges of weight 1 and
+    weights that are exact dyadic fractions (CDF entries on bucket edges)."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    degs = rng.integers(0, 9, n)
+    dst = np.repeat(np.arange(n, dtype=np.uint32), degs)
+    src = rng.integers(0, n, dst.size).astype(np.uint32)
+    w = np.empty(dst.size, np.float32)
+    pos = 0
+    for v, d in enumerate(degs):
+        if d:
+            w[pos:pos + d] = np.float32(1.0 / d) if v % 3 else np.float32(2.0 ** -int(np.log2(d) + 1))
+        pos += d
+    arrays = P.build_graph(n, src, dst, w)
+    for mult in (1, 2, 4):
+        _, _, off_a, mem_a = gpu_sample(arrays, LT, 5, 5000, lt_scan=0)
+        _, _, off_b, mem_b = gpu_sample(arrays, LT, 5, 5000, lt_scan=2, lt_guide_mult=mult)
+        assert (off_a == off_b).all() and (mem_a == mem_b).all()
+    ref = oracle.graph(*arrays).sample(LT, 5, 0, 5000, workers=4)
+    assert_sets_equal(off_b, mem_b, ref)
+
+
+def test_lt_guide_mode_long_walks(cuda, oracle):
+    """Walks past the shared-memory filter (128 members: per-lane table from
+    there, with growth) and past the lane budget (1024: big-set path), plus
+    revisits at every distance: a weight-1 chain with random back edges."""
+    rng = np.random.default_rng(8)
+    n = 3000
+    dst = np.arange(n - 1, dtype=np.uint32)
+    src = dst + 1
+    w = np.ones(n - 1, np.float32)
+    # a quarter of the chain vertices also draw from a random earlier vertex
+    extra = rng.choice(n - 1, (n - 1) // 4, replace=False).astype(np.uint32)
+    src = np.concatenate([src, rng.integers(0, n, extra.size).astype(np.uint32)])
+    dst = np.concatenate([dst, extra])
+    w = np.concatenate([w, np.full(extra.size, 0.02, np.float32)])
+    roff, rsrc, rw = P.build_graph(n, src, dst, w)
+    P.normalize_lt_weights(roff, rw)
+    arrays = (roff, rsrc, rw)
+    _, _, off_a, mem_a = gpu_sample(arrays, LT, 21, 3000, lt_scan=0)
+    g, _, off_b, mem_b = gpu_sample(arrays, LT, 21, 3000, lt_scan=2)
+    sizes = np.diff(off_b.astype(np.int64))
+    assert sizes.max() > 1024 and ((sizes > 128) & (sizes < 1024)).sum() > 100
+    assert (off_a == off_b).all() and (mem_a == mem_b).all()
+    ref = oracle.graph(*arrays).sample(LT, 21, 0, 3000, workers=4)
+    assert_sets_equal(off_b, mem_b, ref)
+
+
+def test_lt_guide_mode_cfg4_shape(cuda, oracle):
+    cfg = graphs.scaled(graphs.CONFIGS["cfg4"], 40000, 600000)
+    arrays = graphs.generate(cfg)
+    _, st_a, off_a, mem_a = gpu_sample(arrays, LT, 3, 4000, lt_scan=0)
+    _, st_b, off_b, mem_b = gpu_sample(arrays, LT, 3, 4000, lt_scan=2)
+    assert (off_a == off_b).all() and (mem_a == mem_b).all()
+    assert (st_a.counter() == st_b.counter()).all()
+    ref = oracle.graph(*arrays).sample(LT, 3, 0, 4000, workers=4)
+    assert_sets_equal(off_b, mem_b, ref)
+
+
 def test_append_from_side_store_equals_direct_top_up(cuda):
     """Sets sampled ahead into a side store (generate_slots) and appended later are
     exactly the sets a direct top-up draws (slot j <- stream j)."""
@@ -244,7 +335,7 @@ def test_inspected_edges_equal_reference_trip_count(cuda, port, name, model, mod
     cfg = graphs.scaled(graphs.CONFIGS[name], 1 << 12, 1 << 16) if name != "cfg4" else \
         graphs.scaled(graphs.CONFIGS[name], 40000, 600000)
     arrays = graphs.generate(cfg)
-    for scan in ((0, 1) if model == LT else (0,)):
+    for scan in ((0, 1, 2) if model == LT else (0,)):
         g = P.Graph(*arrays)
         g.set_option("lt_scan", scan)
         if model == IC:

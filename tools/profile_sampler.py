@@ -17,6 +17,7 @@ ap.add_argument("--m", type=int, default=0)
 ap.add_argument("--ic-coop-min", type=int, default=0)
 ap.add_argument("--lt-kary", type=int, default=0)
 ap.add_argument("--ic-mode", type=int, default=0)
+ap.add_argument("--lt-guide-mult", type=int, default=0)
 ap.add_argument("--ic-rng", type=int, default=0, help="1 = fast statistical IC sampling")
 a = ap.parse_args()
 cfg = graphs.CONFIGS[a.workload]
@@ -24,8 +25,12 @@ if a.n:
     cfg = graphs.scaled(cfg, a.n, a.m)
 arrays = graphs.generate(cfg)
 g = P.Graph(*arrays)
-g.prepare(cfg.model)
 g.set_option("lt_scan", a.lt_scan)
+if a.lt_guide_mult:
+    g.set_option("lt_guide_mult", a.lt_guide_mult)
+t = time.time()
+g.prepare(cfg.model)
+print(f"prepare {1e3 * (time.time() - t):.1f} ms (lt_scan {a.lt_scan})")
 if a.ic_coop_min:
     g.set_option("ic_coop_min", a.ic_coop_min)
 if a.lt_kary:
@@ -38,7 +43,7 @@ st.clear()
 t = time.time()
 P.generate_batch(g, cfg.model, 1, a.sets, st)
 s = g.last_batch_stats()
-print(f"{cfg.name} rng {a.ic_rng} coop_min {a.ic_coop_min} kary {a.lt_kary} mode {a.ic_mode} sets {s.sets} insp/set {s.edges_inspected / s.sets:.0f} members/set "
+print(f"{cfg.name} scan {a.lt_scan} mult {a.lt_guide_mult} rng {a.ic_rng} coop_min {a.ic_coop_min} kary {a.lt_kary} mode {a.ic_mode} sets {s.sets} insp/set {s.edges_inspected / s.sets:.0f} members/set "
       f"{s.members / s.sets:.1f} deferred {s.deferred} sample {s.sample_ms:.2f} ms "
       f"{s.sets / s.sample_ms * 1e3:.3e} sets/s {s.edges_inspected / s.sample_ms * 1e3:.3e} edges/s "
       f"wall {1e3 * (time.time() - t):.1f} ms")
