@@ -454,7 +454,10 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       // staging sized from the running mean set size (first batch: a guess;
       // sets that do not fit are re-run once staging has grown)
       const double per_set = s->nsets ? static_cast<double>(s->total) / s->nsets * 1.5 + 8 : 96.0;
-      const uint64_t want = std::min<uint64_t>(static_cast<uint64_t>(c * per_set) + (1u << 20),
+      // guide-mode LT warps allocate staging in kStageChunk (2048) member chunks:
+      // slack for one partly used chunk per warp of the grid
+      const uint64_t slack = lt_mode == kLtGuide ? full_grid * (block / 32) * 2048 : 0;
+      const uint64_t want = std::min<uint64_t>(static_cast<uint64_t>(c * per_set) + (1u << 20) + slack,
                                                1ull << 31);
       if (want > s->stage.cap) s->stage.reserve_discard(want);
       s->slot_start.reserve_discard(c);

@@ -103,6 +103,36 @@ __device__ __forceinline__ bool fetch_slot(const SampleParams& p, bool need, boo
   return true;
 }
 
+// Warp-queued slot dispenser: the warp takes kSlotChunk batch-local indices at a
+// time (one atomic per chunk instead of one per walk; the dispenser word is a
+// single L2 address every warp of the grid contends on) and hands them to its
+// lanes in lane order. A lane that finds the queue short waits one iteration;
+// `exhausted` only once the dispenser is empty too. wq_next/wq_end are
+// warp-uniform.
+constexpr uint32_t kSlotChunk = 32;
+__device__ __forceinline__ bool fetch_slot_q(const SampleParams& p, bool need, bool& exhausted,
+                                             uint32_t& idx, uint64_t& wq_next, uint64_t& wq_end) {
+  const unsigned nm = __ballot_sync(kFull, need);
+  if (!nm) return false;
+  const int lane = threadIdx.x & 31;
+  if (wq_next >= wq_end && wq_end < p.count) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&p.ctl->next, (unsigned long long)kSlotChunk);
+    base = __shfl_sync(kFull, base, 0);
+    wq_next = base;
+    wq_end = base >= p.count ? p.count : min(static_cast<uint64_t>(base) + kSlotChunk, p.count);
+  }
+  const uint64_t k = wq_next + __popc(nm & lanemask_lt());
+  wq_next = min(wq_next + __popc(nm), wq_end);
+  if (!need) return false;
+  if (k >= wq_end) {
+    if (wq_end >= p.count) exhausted = true;
+    return false;
+  }
+  idx = p.list ? p.list[k] : p.idx_base + static_cast<uint32_t>(k);
+  return true;
+}
+
 // Inserts v into the lane's visited set (member list + table), growing the
 // table by rehash when the load would exceed 1/2.
 __device__ __forceinline__ void lane_insert(uint32_t* mem, uint64_t* tab, uint32_t& tag,
@@ -1827,9 +1857,15 @@ __device__ __forceinline__ void lfilt_bits(uint32_t v, uint32_t& w1, uint32_t& b
 // wait at the reconvergence point) -- with the fused counter increments.
 // Returns, to each pending lane, whether its set was written (false: staging
 // full; the slot was recorded for a re-run).
+// Staging positions come from a warp-private chunk of kStageChunk members
+// (sc_next/sc_end, warp-uniform) refilled from the shared cursor, so the
+// returning atomic on that one address is paid once per chunk, not per set;
+// the host reserves grid-warps x kStageChunk of slack for the chunk tails.
+constexpr uint32_t kStageChunk = 2048;
 __device__ __forceinline__ bool warp_emit_pending(const SampleParams& p, bool pending,
                                                   uint32_t idx, uint32_t nmem,
-                                                  const uint32_t* lists_warp) {
+                                                  const uint32_t* lists_warp,
+                                                  uint64_t& sc_next, uint64_t& sc_end) {
   const int lane = threadIdx.x & 31;
   unsigned em = __ballot_sync(kFull, pending);
   bool mine = false;
@@ -1839,8 +1875,18 @@ __device__ __forceinline__ bool warp_emit_pending(const SampleParams& p, bool pe
     const uint32_t nL = __shfl_sync(kFull, nmem, L);
     const uint32_t iL = __shfl_sync(kFull, idx, L);
     unsigned long long pos = 0;
-    if (lane == L) pos = atomicAdd(&p.ctl->cursor, (unsigned long long)nL);
-    pos = __shfl_sync(kFull, pos, L);
+    if (sc_end - sc_next >= nL) {
+      pos = sc_next;
+      sc_next += nL;
+    } else {
+      const uint32_t take = nL > kStageChunk ? nL : kStageChunk;
+      if (lane == L) pos = atomicAdd(&p.ctl->cursor, (unsigned long long)take);
+      pos = __shfl_sync(kFull, pos, L);
+      if (take == kStageChunk) {
+        sc_next = pos + nL;
+        sc_end = pos + take < p.stage_cap ? pos + take : p.stage_cap;
+      }
+    }
     if (pos + nL > p.stage_cap) {
       if (lane == L) restage_slot(p, iL, nL);
       continue;
@@ -1900,6 +1946,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_sample_lt_guide(const SampleParam
   uint64_t x = 0, xn = 0;  // this step's draw (its entry is in e0/e1) and the next step's
   uint4 e0 = make_uint4(0, 0, 0, 0), e1 = make_uint4(0, 0, 0, 0);
   uint64_t insp = 0, sinsp = 0, ent = 0;
+  uint64_t wq_next = 0, wq_end = 0, sc_next = 0, sc_end = 0;  // warp-uniform queues
 
   for (;;) {
     // (1) filter hits: the warp scans each such lane's members (<= kLtFiltMax,
@@ -1939,7 +1986,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_sample_lt_guide(const SampleParam
       }
     }
     // (2) finished walks -> staging (cooperative copy + fused counter)
-    if (warp_emit_pending(p, pending, idx, nmem, lists_warp)) insp += sinsp;
+    if (warp_emit_pending(p, pending, idx, nmem, lists_warp, sc_next, sc_end)) insp += sinsp;
     pending = false;
     // (3) walks that outgrew the filter: the warp inserts their members into
     //     their (fresh-tagged) per-lane tables, kTabCap entries, load <= 1/2
@@ -1960,7 +2007,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_sample_lt_guide(const SampleParam
     }
     __syncwarp();
 
-    if (fetch_slot(p, !active && !exhausted, exhausted, idx)) {
+    if (fetch_slot_q(p, !active && !exhausted, exhausted, idx, wq_next, wq_end)) {
       rng.seed(stream_seed(p.run_seed, p.base_slot + idx));
       const uint32_t u = static_cast<uint32_t>(rng.below(p.n));
       offu = __ldg(p.off + u);

@@ -8,5 +8,5 @@ run() {  # name kernel-regex command...
     timeout 900 $NCU -k regex:$kr -o gpurun_out/$name -f "$@" > gpurun_out/$name.ncu.log 2>&1
   echo "$name rc=$?"; tail -1 gpurun_out/$name.log
 }
-run g_cfg4_65k k_sample_lt_guide python tools/profile_sampler.py cfg4 --sets 65536 --lt-scan 2
+#run g_cfg4_65k k_sample_lt_guide python tools/profile_sampler.py cfg4 --sets 65536 --lt-scan 2
 run g_cfg4_1m k_sample_lt_guide python tools/profile_sampler.py cfg4 --sets 1048576 --lt-scan 2
