@@ -33,6 +33,31 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+SCAN = {"linear": 0, "bsearch": 1, "guide": 2}
+KERNEL = {"linear": "k_sample_lt", "bsearch": "k_sample_lt", "guide": "k_sample_lt_guide"}
+BYTES_RULE = {
+    "linear": "8 B x reference-equivalent inspected CDF entries",
+    "bsearch": "8 B x CDF entries and tree pivots actually read",
+    "guide": "32 B per guide bucket entry loaded (one per walk step) + 8 B x CDF entries "
+             "read by multi-entry buckets",
+    "ic": "8 B x reference-equivalent inspected in-edges",
+}
+
+
+def gather_ceiling():
+    """Measured on this GPU: dependent random 32-B gathers per second from an
+    8 GB table (tools/gather/gather_probe.cu) -- the ceiling of a kernel whose
+    every step is one such load (the guide-mode LT walk)."""
+    import ctypes
+    path = os.path.join(ROOT, "tools", "gather", "libgather_probe.so")
+    try:
+        lib = ctypes.CDLL(path)
+        lib.gather_ceiling.restype = ctypes.c_double
+        lib.gather_ceiling.argtypes = [ctypes.c_double, ctypes.c_int]
+        v = lib.gather_ceiling(8.0, 256)
+        return v if v > 0 else None
+    except OSError:
+        return None
 
 
 def parse():
@@ -42,8 +67,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg4")
-    ap.add_argument("--sets", type=int, default=1 << 16)
-    ap.add_argument("--lt-scan", default="bsearch", choices=["linear", "bsearch"])
+    ap.add_argument("--sets", type=int, default=1 << 20)
+    ap.add_argument("--lt-scan", default="guide", choices=["linear", "bsearch", "guide"])
+    ap.add_argument("--small-sets", type=int, default=1 << 16,
+                    help="batch of the extra small-batch line (IMM-like, tail-bound); 0 = skip")
+    ap.add_argument("--linear-sets", type=int, default=1 << 16,
+                    help="batch of the reference-trip-count (linear CDF scan) line; 0 = skip")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-imm", action="store_true")
@@ -182,22 +211,23 @@ def run_ours(args, rank, world, local):
     stream = torch.cuda.current_stream()
     g = P.Graph(roff, rsrc, rw)
     g.set_stream(stream.cuda_stream)
+    g.set_option("lt_scan", SCAN[args.lt_scan])
     g.prepare(model)
-    g.set_option("lt_scan", 1 if args.lt_scan == "bsearch" else 0)
     store = P.RRRStore(g)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def step(i):
+    def step(i, nb):
         store.clear()
-        first = (i * world + rank) * N
-        P.generate_slots(g, model, 1, first, N, store)
+        first = (i * world + rank) * nb
+        P.generate_slots(g, model, 1, first, nb, store)
         return g.last_batch_stats()
 
-    def measure(scan):
-        """W untimed + K timed steps; per-step CUDA events on the graph's stream."""
-        g.set_option("lt_scan", 1 if scan == "bsearch" else 0)
+    def measure(scan, nb):
+        """W untimed + K timed steps of nb sets; per-step CUDA events on the graph's stream."""
+        if model == 1:
+            g.set_option("lt_scan", SCAN[scan])
         for i in range(args.warmup):
-            step(i)
+            step(i, nb)
         barrier()
         clocks = Clocks(local)
         launches0 = P.launch_count()
@@ -208,7 +238,7 @@ def run_ours(args, rank, world, local):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            st = step(args.warmup + i)
+            st = step(args.warmup + i, nb)
             e1.record(stream)
             e1.synchronize()
             r["total_ms"] += e0.elapsed_time(e1)
@@ -224,25 +254,29 @@ def run_ours(args, rank, world, local):
         if dist:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         r["max_ms"] = float(t.item())
-        r["value"] = world * N * args.steps / (r["max_ms"] / 1e3)
+        r["value"] = world * nb * args.steps / (r["max_ms"] / 1e3)
         per_launch_ms = r["sample_ms"] / args.steps
-        linear = scan == "linear" or model == 0
+        linear = scan in ("linear", "ic")
         alg = 8 * (r["insp"] if linear else r["ent"]) / args.steps
         r["per_launch_ms"] = per_launch_ms
         r["achieved"] = alg / (per_launch_ms / 1e3) / 1e9
-        r["bytes_rule"] = ("8 B x reference-equivalent inspected entries" if linear
-                           else "8 B x CDF probes actually read")
+        r["bytes_rule"] = BYTES_RULE[scan]
+        r["nb"] = nb
         return r
 
-    main = measure(args.lt_scan if model == 1 else "ic")
+    scan_main = args.lt_scan if model == 1 else "ic"
+    main = measure(scan_main, N)
     max_ms, value = main["max_ms"], main["value"]
     insp, members, deferred = main["insp"], main["members"], main["deferred"]
     launches, clk = main["launches"], main["clocks"]
     linear_block = None
-    if model == 1 and args.lt_scan != "linear":
-        lin = measure("linear")
-        linear_block = lin
-        g.set_option("lt_scan", 1 if args.lt_scan == "bsearch" else 0)
+    small_block = None
+    if model == 1 and args.lt_scan != "linear" and args.linear_sets:
+        linear_block = measure("linear", args.linear_sets)
+    if args.small_sets and args.small_sets != N:
+        small_block = measure(scan_main, args.small_sets)
+    if model == 1:
+        g.set_option("lt_scan", SCAN[args.lt_scan])
 
     # ---- end to end through the public API with host buffers -----------------
     # warm: the graph was built once from host arrays (as the reference's
@@ -252,7 +286,7 @@ def run_ours(args, rank, world, local):
     pin = [torch.from_numpy(a).pin_memory() for a in (roff, rsrc, rw)]
     host = [p.numpy() for p in pin]
     out_off = torch.empty(N + 1, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
-    out_mem = torch.empty(max(1, int(4 * members / args.steps) + (1 << 20)),
+    out_mem = torch.empty(max(1, int(1.25 * members / args.steps) + (1 << 20)),
                           dtype=torch.int32).pin_memory().numpy().view(np.uint32)
     out_cnt = torch.empty(n, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
 
@@ -262,7 +296,7 @@ def run_ours(args, rank, world, local):
         (rrg_store_export_all_async); every step's D2H is inside the timed region."""
         nonlocal out_mem
         gw = P.Graph(*host)
-        gw.set_option("lt_scan", 1 if args.lt_scan == "bsearch" else 0)
+        gw.set_option("lt_scan", SCAN[args.lt_scan])
         stores = [P.RRRStore(gw), P.RRRStore(gw)]
         mems = [out_mem, np.empty_like(out_mem)]
         mems = [torch.from_numpy(m).pin_memory().numpy() for m in mems]
@@ -308,14 +342,14 @@ def run_ours(args, rank, world, local):
         times, h2d, d2h = [], 0, 0
         gw = None if cold else P.Graph(*host)
         if gw is not None:
-            gw.set_option("lt_scan", 1 if args.lt_scan == "bsearch" else 0)
+            gw.set_option("lt_scan", SCAN[args.lt_scan])
         sw = None if cold else P.RRRStore(gw)
         for i in range(args.e2e_steps + 1):
             barrier()
             t0 = time.perf_counter()
             if cold:
                 ge = P.Graph(*host)  # H2D of the transpose arrays from pinned memory
-                ge.set_option("lt_scan", 1 if args.lt_scan == "bsearch" else 0)
+                ge.set_option("lt_scan", SCAN[args.lt_scan])
                 se = P.RRRStore(ge)
             else:
                 ge, se = gw, sw
@@ -378,7 +412,7 @@ def run_ours(args, rank, world, local):
         "sampler_ms_per_step": per_launch_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_sample_lt" if model == 1 else "k_sample_ic",
+                     "kernel": KERNEL.get(scan_main, "k_sample_ic"),
                      "bytes": main["bytes_rule"], "peak_source": peak_src},
         "gpu_launches": launches,
         "clocks": clk,
@@ -392,11 +426,34 @@ def run_ours(args, rank, world, local):
                      "d2h_bytes_per_step": cold_d2h, "steps": cold_n,
                      "includes": "per step: pinned H2D graph upload + K0 layout + the e2e step"},
     }
+    if scan_main == "guide":
+        # the guide walk's step is one dependent random 32-B gather: its ceiling is
+        # the measured dependent-gather rate of this GPU, not streaming HBM bandwidth
+        ceil = gather_ceiling()
+        got = achieved * 1e9 / 32
+        line["roofline"]["gather_ceiling"] = {
+            "achieved": got, "peak": ceil, "unit": "dependent random 32-B gathers/s",
+            "frac": (got / ceil) if ceil else None,
+            "peak_source": "measured live: tools/gather/gather_probe.cu (8 GB table, "
+                           "1-8 x 256 chains per SM, best)"}
+    if small_block is not None:
+        sb = small_block
+        line["small_batch"] = {
+            "note": "same measurement at an IMM-sized batch: bounded by the longest walk "
+                    "(one dependent gather per step), not by throughput",
+            "sets_per_step": sb["nb"], "value": sb["value"], "unit": "sets/s",
+            "ms_per_step": sb["max_ms"] / args.steps,
+            "roofline": {"bound": "hbm", "achieved": sb["achieved"], "peak": peak,
+                         "unit": "GB/s", "frac": sb["achieved"] / peak,
+                         "kernel": KERNEL.get(scan_main, "k_sample_ic"),
+                         "bytes": sb["bytes_rule"], "peak_source": peak_src},
+            "gpu_launches": sb["launches"], "clocks": sb["clocks"]}
     if linear_block is not None:
         lb = linear_block
         line["linear_scan"] = {
-            "note": "same batches with the reference's linear CDF scan (warp-cooperative "
-                    "16-byte loads); identical sets",
+            "note": "the reference's linear CDF scan (warp-cooperative 16-byte loads) on "
+                    f"{lb['nb']}-set batches; identical sets",
+            "sets_per_step": lb["nb"],
             "value": lb["value"], "unit": "sets/s", "ms_per_step": lb["max_ms"] / args.steps,
             "edges_inspected_per_sec": world * lb["insp"] / (lb["max_ms"] / 1e3),
             "roofline": {"bound": "hbm", "achieved": lb["achieved"], "peak": peak, "unit": "GB/s",
@@ -411,7 +468,7 @@ def run_ours(args, rank, world, local):
         orc = Oracle("reference" if available("reference") else "port")
         og = orc.graph(roff, rsrc, rw)
         cores = cpu_cores()
-        ncpu = N
+        ncpu = min(N, 1 << 16)  # bounded CPU sample (~1-2 s on 16 cores)
         t0 = time.perf_counter()
         sk = og.sample(model, 1, 0, ncpu, workers=cores)
         dt = time.perf_counter() - t0

@@ -1827,8 +1827,12 @@ __device__ __forceinline__ void lt_guide_fetch(const SampleParams& p, uint32_t o
   if (!degu) return;
   const uint64_t G = static_cast<uint64_t>(degu) * p.lt_guide_mult;
   const uint64_t gi = static_cast<uint64_t>(offu) * p.lt_guide_mult + __umul64hi(x & ~0x7ffull, G);
-  e0 = __ldg(p.ltguide + 2 * gi);
-  e1 = __ldg(p.ltguide + 2 * gi + 1);
+  // one 256-bit load (sm_100: LDG.256), not allocated in L1: the entry is one
+  // 32-byte sector and is never re-read by this SM
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(e0.x), "=r"(e0.y), "=r"(e0.z), "=r"(e0.w), "=r"(e1.x), "=r"(e1.y),
+                 "=r"(e1.z), "=r"(e1.w)
+               : "l"(p.ltguide + 2 * gi));
 }
 
 // Visited set of a guide-mode walk while it is short: a 1024-bit filter per lane
