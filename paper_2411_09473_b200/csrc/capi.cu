@@ -660,29 +660,44 @@ rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double /*adaptive_threshol
     const cudaStream_t st = g->stream;
     const uint32_t n = g->n;
     s->wcnt.reserve_discard(n);
-    if (use_prebuilt) {
+    if (use_prebuilt && s->counter_complete) {
       RRG_CUDA(cudaMemcpyAsync(s->wcnt.ptr, s->counter.ptr, 4ull * n, cudaMemcpyDeviceToDevice,
                                st));
     } else {
       RRG_CUDA(cudaMemsetAsync(s->wcnt.ptr, 0, 4ull * n, st));
       launch_recount(s->off.ptr, s->mem.ptr, s->nsets, s->wcnt.ptr, st);
     }
-    // K5: inverted index from the starting tally (all sets live: revive_all, :215)
-    s->ioff.reserve_discard(static_cast<uint64_t>(n) + 1);
-    exclusive_scan_u32(s->wcnt.ptr, s->ioff.ptr, n, s->scan_tmp, st);
-    s->icur.reserve_discard(n);
-    RRG_CUDA(cudaMemcpyAsync(s->icur.ptr, s->ioff.ptr, 8ull * n, cudaMemcpyDeviceToDevice, st));
-    s->inv.reserve_discard(s->total ? s->total : 1);
     RRG_CUDA(cudaMemsetAsync(s->status.ptr, 0, 8, st));
-    launch_invert(s->off.ptr, s->mem.ptr, s->nsets, s->icur.ptr, s->ioff.ptr, s->inv.ptr,
-                  s->status.ptr, st);
+    // Scan mode (stores up to kScanMaxMembers, 128 MB: every round re-reads the
+    // flat members, L2-resident) needs no index; larger stores get K5, the
+    // inverted index vertex -> sets from the starting tally (all sets live:
+    // revive_all, selection.hpp:215).
+    constexpr uint64_t kScanMaxMembers = 1ull << 25;
+    const char* force_index = std::getenv("RRGPU_SELECT_INDEX");  // tests: the index path
+    const bool scan = s->total <= kScanMaxMembers &&
+                      !(force_index && *force_index && *force_index != '0');
+    if (scan) {
+      s->inv.reserve_discard(s->total ? s->total : 1);  // the blanked working copy
+      s->span.reserve_discard(s->total ? s->total : 1);
+      launch_set_spans(s->off.ptr, s->mem.ptr, s->nsets, s->span.ptr, s->inv.ptr, st);
+    } else {
+      s->ioff.reserve_discard(static_cast<uint64_t>(n) + 1);
+      exclusive_scan_u32(s->wcnt.ptr, s->ioff.ptr, n, s->scan_tmp, st);
+      s->icur.reserve_discard(n);
+      RRG_CUDA(cudaMemcpyAsync(s->icur.ptr, s->ioff.ptr, 8ull * n, cudaMemcpyDeviceToDevice, st));
+      s->inv.reserve_discard(s->total ? s->total : 1);
+      launch_invert(s->off.ptr, s->mem.ptr, s->nsets, s->icur.ptr, s->ioff.ptr, s->inv.ptr,
+                    s->status.ptr, st);
+    }
     s->covered.reserve_discard(s->nsets ? s->nsets : 1);
     RRG_CUDA(cudaMemsetAsync(s->covered.ptr, 0, 4ull * (s->nsets ? s->nsets : 1), st));
     s->keys.reserve_discard(k);
     s->marg.reserve_discard(k);
     s->seeds.reserve_discard(k);
     s->selected.reserve_discard(n);
-    RRG_CUDA(cudaMemsetAsync(s->keys.ptr, 0, 8ull * k, st));
+    const uint64_t ntiles = (static_cast<uint64_t>(n) + (1u << kSelTileLog) - 1) >> kSelTileLog;
+    s->tmax.reserve_discard(ntiles);
+    s->tdirty.reserve_discard(ntiles);
     RRG_CUDA(cudaMemsetAsync(s->marg.ptr, 0, 8ull * k, st));
     RRG_CUDA(cudaMemsetAsync(s->selected.ptr, 0, n, st));
     if (round_counters) s->snap.reserve_discard(static_cast<uint64_t>(k) * n);
@@ -701,6 +716,13 @@ rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double /*adaptive_threshol
     p.selected = s->selected.ptr;
     p.snap = round_counters ? s->snap.ptr : nullptr;
     p.status = s->status.ptr;
+    p.nsets = s->nsets;
+    p.total = s->total;
+    p.tmax = s->tmax.ptr;
+    p.dirty = s->tdirty.ptr;
+    p.scan = scan ? 1 : 0;
+    p.span = s->span.ptr;
+    p.wmem = s->inv.ptr;
     launch_select(p, g->num_sms, st);
     uint32_t status[2] = {0, 0};
     std::vector<unsigned long long> marg(k);

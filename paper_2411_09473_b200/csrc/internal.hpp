@@ -131,7 +131,7 @@ struct rrg_graph {
   bool rec_ready = false;
   bool cdf_ready = false;
   bool cdf_monotone = true;
-  int lt_scan = rrgpu::kLtBsearch;  // fastest exact search; linear = reference trip count
+  int lt_scan = rrgpu::kLtGuide;  // guide table (falls back to the search tree, then linear)
   uint32_t coop_min = 64;        // LT: in-lists at least this long are scanned warp-cooperatively
   int lt_kary = 8;               // LT: arity of the CDF search (8 measured best at cfg4)
   uint32_t ic_inner = 8;         // IC: edge steps per flat-loop iteration
@@ -175,6 +175,9 @@ struct rrg_store {
   rrgpu::DevBuf<uint8_t> selected;
   rrgpu::DevBuf<uint32_t> snap;
   rrgpu::DevBuf<uint32_t> status;
+  rrgpu::DevBuf<unsigned long long> tmax;  // selection: per-tile max keys
+  rrgpu::DevBuf<uint32_t> tdirty;          // selection: per-tile dirty flags
+  rrgpu::DevBuf<uint64_t> span;            // selection (scan mode): member -> set span
   rrgpu::DevBuf<uint64_t> wide;  // u64 staging of counter exports
 };
 
@@ -259,6 +262,8 @@ void launch_compact(const uint32_t* stage, const uint64_t* slot_start, const uin
                     uint64_t* off_out, uint32_t* maxlen, cudaStream_t s);
 void launch_recount(const uint64_t* off, const uint32_t* mem, uint64_t nsets, uint32_t* counter,
                     cudaStream_t s);
+void launch_set_spans(const uint64_t* off, const uint32_t* mem, uint64_t nsets, uint64_t* span,
+                      uint32_t* wmem, cudaStream_t s);
 void launch_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
                    unsigned long long* icur, const uint64_t* ioff, uint32_t* inv,
                    uint32_t* status, cudaStream_t s);
@@ -275,6 +280,8 @@ struct SelectParams {
   uint32_t* cnt;
   const uint64_t* ioff;
   const uint32_t* inv;
+  const uint64_t* span;  // scan mode: per member, its set's start << 32 | length
+  uint32_t* wmem;        // scan mode: working copy of the members, covered sets blanked
   const uint64_t* off;
   const uint32_t* mem;
   uint32_t* covered;
@@ -284,7 +291,14 @@ struct SelectParams {
   uint8_t* selected;
   uint32_t* snap;      // k*n or null
   uint32_t* status;    // [0] = rounds completed
+  uint64_t nsets;
+  uint64_t total;      // members stored (scan mode reads mem[0, total) each round)
+  unsigned long long* tmax;  // per-tile max packed key (kSelTile vertices per tile)
+  uint32_t* dirty;     // per tile: a count in it changed this round
+  int scan;            // 1: find the sets holding v by scanning the flat members
+                       // (no inverted index); 0: inverted index ioff/inv
 };
+constexpr uint32_t kSelTileLog = 11;  // 2048 vertices per argmax tile
 void launch_select(const SelectParams& p, int num_sms, cudaStream_t s);
 
 }  // namespace rrgpu

@@ -2,15 +2,26 @@
 //
 // Replaces select_seeds (selection.hpp:209-243) with parallel_argmax (:100-125),
 // decrement_update (:130-156) and fill_remaining_seeds (:61-72). One cooperative
-// persistent launch runs every round; grid-wide barriers separate
-//   A) argmax: block max over packed keys (count << 32 | ~v) -> one 64-bit
-//      atomicMax per block. Max count wins; ties go to the lowest id, exactly
-//      the reference's rule (:113, :119-120).
-//   B) cover: every set in inv[v] (inverted index, store.cu) is claimed once
-//      with atomicExch on its covered flag; the winner counts it in the round's
-//      marginal and decrements each member's count (Counter::sub, counter.hpp:28).
-// The host sees nothing until all k rounds are done.
+// persistent launch runs every round; the host sees nothing until all k rounds
+// are done. The argmax is incremental: the vertices are cut into tiles of
+// 2^kSelTileLog, each with its max packed key (count << 32 | ~v: max count wins,
+// ties go to the lowest id -- the reference's rule, :113, :119-120), and a round
+// only re-reduces the tiles whose counts changed. A round:
+//   A) every block reduces the tile maxima (a few KB, L2) to the same key, so
+//      the argmax needs no grid barrier of its own;
+//   B) cover: each live set holding v is claimed once (atomicExch on its
+//      covered flag); the claimer counts it in the round's marginal and the warp
+//      decrements each member (Counter::sub, counter.hpp:28), flagging its tile.
+//      The sets holding v are found by scanning the flat member buffer (scan
+//      mode: a few MB per round at BASELINE sizes, L2-resident, and no index to
+//      build) or through the inverted index vertex -> sets (index mode, for
+//      stores too large to re-read every round);
+//   -- grid barrier --
+//   C) the dirty tiles are re-reduced;
+//   -- grid barrier --
 #include <cooperative_groups.h>
+
+#include <cstdlib>
 
 #include "internal.hpp"
 
@@ -21,44 +32,93 @@ namespace rrgpu {
 namespace {
 
 constexpr int kSelBlock = 512;
+constexpr uint32_t kSelTile = 1u << kSelTileLog;
+constexpr uint32_t kBlank = 0xffffffffu;  // never a vertex id (ids < n <= 2^32 - 1)
+constexpr uint32_t kAllTilesMax = 64;     // up to this many tiles: re-reduce all, no flags
 
 __device__ __forceinline__ unsigned long long pack_key(uint32_t count, uint32_t v) {
   return (static_cast<unsigned long long>(count) << 32) | (0xffffffffu - v);
 }
 
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+  return a > b ? a : b;
+}
+
+// Block-wide max; every thread gets the result. `red` holds kSelBlock/32 words.
+__device__ __forceinline__ unsigned long long block_max(unsigned long long x,
+                                                        unsigned long long* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) x = umax64(x, __shfl_xor_sync(kFull, x, o));
+  __syncthreads();  // red may still be read by a previous call
+  if (lane == 0) red[wid] = x;
+  __syncthreads();
+  x = lane < kSelBlock / 32 ? red[lane] : 0ull;
+  for (int o = 16; o; o >>= 1) x = umax64(x, __shfl_xor_sync(kFull, x, o));
+  return x;
+}
+
+// Max key of tile t by one warp (every lane gets it): 2048 counts as 16
+// independent 16-byte loads per lane, shuffle reduction, no block barrier.
+__device__ __forceinline__ unsigned long long tile_max_warp(const SelectParams& p, uint32_t t) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lo = t << kSelTileLog;
+  unsigned long long best = 0;
+  if (lo + kSelTile <= p.n) {
+    const uint4* c4 = reinterpret_cast<const uint4*>(p.cnt + lo);
+    uint4 q[kSelTile / 128];
+#pragma unroll
+    for (uint32_t i = 0; i < kSelTile / 128; ++i) q[i] = c4[i * 32 + lane];
+#pragma unroll
+    for (uint32_t i = 0; i < kSelTile / 128; ++i) {
+      const uint32_t v = lo + (i * 32 + lane) * 4;
+      best = umax64(best, pack_key(q[i].x, v));
+      best = umax64(best, pack_key(q[i].y, v + 1));
+      best = umax64(best, pack_key(q[i].z, v + 2));
+      best = umax64(best, pack_key(q[i].w, v + 3));
+    }
+  } else {
+    for (uint32_t v = lo + lane; v < p.n; v += 32) best = umax64(best, pack_key(p.cnt[v], v));
+  }
+  for (int o = 16; o; o >>= 1) best = umax64(best, __shfl_xor_sync(kFull, best, o));
+  return best;
+}
+
+// The warp decrements every member of set s (claimed by one of its lanes).
+__device__ __forceinline__ void warp_cover(const SelectParams& p, uint64_t s) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t b = p.off[s], e = p.off[s + 1];
+  for (uint64_t j = b + lane; j < e; j += 32) {
+    const uint32_t u = p.mem[j];
+    atomicSub(p.cnt + u, 1u);
+    p.dirty[u >> kSelTileLog] = 1u;
+  }
+}
+
+template <bool kScan>
 __global__ void __launch_bounds__(kSelBlock) k_select(const SelectParams p) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ unsigned long long warp_best[kSelBlock / 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ unsigned long long red[kSelBlock / 32];
+  const int lane = threadIdx.x & 31;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t gwarp = tid >> 5;
   const uint64_t nwarps = nthreads >> 5;
+  const uint32_t ntiles = (p.n + kSelTile - 1) >> kSelTileLog;
+
+  for (uint64_t t = gwarp; t < ntiles; t += nwarps) {
+    const unsigned long long m = tile_max_warp(p, static_cast<uint32_t>(t));
+    if (lane == 0) {
+      p.tmax[t] = m;
+      p.dirty[t] = 0u;
+    }
+  }
+  grid.sync();
 
   for (uint32_t r = 0; r < p.k; ++r) {
-    // ---- A: argmax over counts ------------------------------------------
+    // ---- A: argmax over the tile maxima (every block, same answer) ---------
     unsigned long long best = 0;
-    for (uint64_t v = tid; v < p.n; v += nthreads) {
-      const unsigned long long key = pack_key(p.cnt[v], static_cast<uint32_t>(v));
-      best = key > best ? key : best;
-    }
-    for (int o = 16; o; o >>= 1) {
-      const unsigned long long y = __shfl_xor_sync(kFull, best, o);
-      best = y > best ? y : best;
-    }
-    if (lane == 0) warp_best[wid] = best;
-    __syncthreads();
-    if (wid == 0) {
-      best = lane < kSelBlock / 32 ? warp_best[lane] : 0;
-      for (int o = 16; o; o >>= 1) {
-        const unsigned long long y = __shfl_xor_sync(kFull, best, o);
-        best = y > best ? y : best;
-      }
-      if (lane == 0) atomicMax(p.keys + r, best);
-    }
-    grid.sync();
-
-    const unsigned long long key = p.keys[r];
+    for (uint32_t t = threadIdx.x; t < ntiles; t += kSelBlock) best = umax64(best, p.tmax[t]);
+    const unsigned long long key = block_max(best, red);
     const uint32_t top = static_cast<uint32_t>(key >> 32);
     const uint32_t v = 0xffffffffu - static_cast<uint32_t>(key);
     if (top == 0) {
@@ -75,31 +135,88 @@ __global__ void __launch_bounds__(kSelBlock) k_select(const SelectParams p) {
         }
         p.status[0] = r;  // rounds with a counter snapshot
       }
-      return;  // uniform: every block read the same key
+      return;  // uniform: every block computed the same key
     }
 
-    // ---- B: cover the sets holding v --------------------------------------
-    const uint64_t ib = p.ioff[v], ie = p.ioff[v + 1];
+    // ---- B: cover the live sets holding v ------------------------------------
     unsigned long long killed = 0;
-    for (uint64_t t = ib + gwarp; t < ie; t += nwarps) {
-      const uint32_t s = p.inv[t];
-      uint32_t was = 0;
-      if (lane == 0) was = atomicExch(p.covered + s, 1u);
-      was = __shfl_sync(kFull, was, 0);
-      if (was) continue;
-      killed += lane == 0;
-      for (uint64_t j = p.off[s] + lane; j < p.off[s + 1]; j += 32) atomicSub(p.cnt + p.mem[j], 1u);
+    if (kScan) {
+      // warp w scans members [256 w', 256 w' + 256) of the working copy for v,
+      // eight per lane. Covered sets are blanked there, so every match is a live
+      // set, found by exactly one lane: no claim needed; that warp decrements and
+      // blanks the set.
+      const uint64_t nchunk = (p.total + 255) / 256;
+      for (uint64_t c = gwarp; c < nchunk; c += nwarps) {
+        const uint64_t base = c * 256 + static_cast<uint64_t>(lane) * 8;
+        uint32_t q[8];
+        if (base + 8 <= p.total) {
+          const uint4 a = *reinterpret_cast<const uint4*>(p.wmem + base);
+          const uint4 b = *reinterpret_cast<const uint4*>(p.wmem + base + 4);
+          q[0] = a.x; q[1] = a.y; q[2] = a.z; q[3] = a.w;
+          q[4] = b.x; q[5] = b.y; q[6] = b.z; q[7] = b.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) q[j] = base + j < p.total ? p.wmem[base + j] : kBlank;
+        }
+        uint32_t hits = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hits |= (q[j] == v ? 1u : 0u) << j;
+        unsigned hm = __ballot_sync(kFull, hits != 0);
+        killed += __popc(hits);
+        while (hm) {  // lanes with matches, one set at a time per warp
+          const int L = __ffs(hm) - 1;
+          const uint32_t hL = __shfl_sync(kFull, hits, L);
+          const int j = __ffs(hL) - 1;
+          if (lane == L) {
+            hits &= hits - 1;
+          }
+          if (!(hL & (hL - 1))) hm &= hm - 1;
+          const uint64_t w = p.span[base - static_cast<uint64_t>(lane) * 8 +
+                                    static_cast<uint64_t>(L) * 8 + j];
+          const uint64_t sb = w >> 32, se = sb + (w & 0xffffffffull);
+          for (uint64_t t = sb + lane; t < se; t += 32) {
+            const uint32_t u = p.wmem[t];
+            atomicSub(p.cnt + u, 1u);
+            p.dirty[u >> kSelTileLog] = 1u;
+            p.wmem[t] = kBlank;
+          }
+        }
+      }
+    } else {
+      const uint64_t ib = p.ioff[v], ie = p.ioff[v + 1];
+      for (uint64_t t = ib + gwarp; t < ie; t += nwarps) {
+        const uint32_t s = p.inv[t];
+        uint32_t was = 0;
+        if (lane == 0) was = atomicExch(p.covered + s, 1u);
+        was = __shfl_sync(kFull, was, 0);
+        if (was) continue;
+        killed += lane == 0;
+        warp_cover(p, s);
+      }
     }
+    for (int o = 16; o; o >>= 1) killed += __shfl_xor_sync(kFull, killed, o);
     if (lane == 0 && killed) atomicAdd(p.marg + r, killed);
     if (tid == 0) {
+      p.keys[r] = key;
       p.seeds[r] = v;
       p.selected[v] = 1;
     }
     grid.sync();
+
+    // ---- C: re-reduce the tiles whose counts changed -------------------------
     if (p.snap) {
       uint32_t* out = p.snap + static_cast<uint64_t>(r) * p.n;
       for (uint64_t u = tid; u < p.n; u += nthreads) out[u] = p.cnt[u];
     }
+    for (uint64_t t = gwarp; t < ntiles; t += nwarps) {
+      if (ntiles > kAllTilesMax && !p.dirty[t]) continue;  // uniform in the warp
+      const unsigned long long m = tile_max_warp(p, static_cast<uint32_t>(t));
+      if (lane == 0) {
+        p.tmax[t] = m;
+        p.dirty[t] = 0u;
+      }
+    }
+    grid.sync();
   }
   if (tid == 0) p.status[0] = p.k;
 }
@@ -107,17 +224,20 @@ __global__ void __launch_bounds__(kSelBlock) k_select(const SelectParams p) {
 }  // namespace
 
 void launch_select(const SelectParams& p, int num_sms, cudaStream_t s) {
+  const void* fn = p.scan ? reinterpret_cast<const void*>(k_select<true>)
+                          : reinterpret_cast<const void*>(k_select<false>);
   int per_sm = 0;
-  RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select, kSelBlock, 0));
+  RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSelBlock, 0));
   if (per_sm < 1) per_sm = 1;
   if (per_sm > 2) per_sm = 2;
+  if (const char* e = std::getenv("RRGPU_SELECT_BLOCKS_PER_SM")) {  // tuning
+    const int v = std::atoi(e);
+    if (v >= 1 && v <= per_sm) per_sm = v;
+  }
   int grid = num_sms * per_sm;
-  const uint64_t want = (static_cast<uint64_t>(p.n) + kSelBlock - 1) / kSelBlock;
-  if (want < static_cast<uint64_t>(grid)) grid = static_cast<int>(want < 1 ? 1 : want);
   SelectParams args = p;
   void* kargs[] = {&args};
-  RRG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_select), dim3(grid),
-                                       dim3(kSelBlock), kargs, 0, s));
+  RRG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSelBlock), kargs, 0, s));
   count_launch();
 }
 

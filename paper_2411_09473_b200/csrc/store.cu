@@ -154,6 +154,24 @@ __global__ void k_recount(const uint64_t* off, const uint32_t* mem, uint64_t nse
   }
 }
 
+// Scan-mode selection inputs: a working copy of the members (covered sets get
+// blanked in it) and, per member, its set's span (start << 32 | length), so a
+// member matching the round's seed names the whole set in one load.
+__global__ void k_set_spans(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
+                            uint64_t* span, uint32_t* wmem) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * blockDim.x / 32;
+  for (uint64_t s = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; s < nsets;
+       s += warps) {
+    const uint64_t b = off[s], e = off[s + 1];
+    const uint64_t w = (b << 32) | (e - b);
+    for (uint64_t t = b + lane; t < e; t += 32) {
+      span[t] = w;
+      wmem[t] = mem[t];
+    }
+  }
+}
+
 // K5: vertex -> ids of the sets containing it. icur starts at ioff[v].
 __global__ void k_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
                          unsigned long long* icur, const uint64_t* ioff, uint32_t* inv,
@@ -238,6 +256,14 @@ void launch_recount(const uint64_t* off, const uint32_t* mem, uint64_t nsets, ui
                     cudaStream_t s) {
   if (!nsets) return;
   k_recount<<<grid_for(nsets), 256, 0, s>>>(off, mem, nsets, counter);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_set_spans(const uint64_t* off, const uint32_t* mem, uint64_t nsets, uint64_t* span,
+                      uint32_t* wmem, cudaStream_t s) {
+  if (!nsets) return;
+  k_set_spans<<<grid_for(nsets), 256, 0, s>>>(off, mem, nsets, span, wmem);
   RRG_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -62,8 +62,19 @@ def test_exhaustion_fill_skips_selected(cuda):
     assert s.seeds == [3, 5, 0, 1, 2] and s.marginal_counts == [2, 1, 0, 0, 0]
 
 
+@pytest.fixture(params=["scan", "index"])
+def select_mode(request, monkeypatch):
+    """Both ways of finding the sets that hold the round's seed: scanning the
+    flat members (default up to 2^25 members) and the inverted index."""
+    if request.param == "index":
+        monkeypatch.setenv("RRGPU_SELECT_INDEX", "1")
+    else:
+        monkeypatch.delenv("RRGPU_SELECT_INDEX", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("trial", range(12))
-def test_random_stores_match_reference_with_round_counters(cuda, oracle, trial):
+def test_random_stores_match_reference_with_round_counters(cuda, oracle, trial, select_mode):
     """acceptance.cpp:128-155 (criterion 02) + :111-126 (criterion 01)."""
     rng = np.random.default_rng(202 + trial)
     n = int(2 + rng.integers(0, 400))
@@ -85,7 +96,29 @@ def test_random_stores_match_reference_with_round_counters(cuda, oracle, trial):
             assert (s.round_counters == rc).all()
 
 
-def test_sampled_store_selection_matches_reference(cuda, oracle):
+@pytest.mark.parametrize("n,nsets,k", [(20000, 5000, 40), (70000, 3000, 60)])
+def test_many_tiles_match_reference(cuda, oracle, select_mode, n, nsets, k):
+    """Vertex counts spanning many argmax tiles (2048 vertices each): maxima kept
+    per tile and re-reduced only where a count changed."""
+    rng = np.random.default_rng(n + nsets)
+    # skewed membership: a few hot vertices (ties across tiles) plus a long tail
+    sizes = rng.integers(1, 40, nsets)
+    hot = rng.choice(n, 64, replace=False)
+    lists = []
+    for sz in sizes:
+        pool = np.concatenate([rng.choice(hot, min(sz // 3 + 1, 64), replace=False),
+                               rng.integers(0, n, sz)])
+        lists.append(np.unique(pool)[:sz].tolist())
+    g, st = store_from_lists(n, lists)
+    off = np.zeros(nsets + 1, np.uint64)
+    off[1:] = np.cumsum([len(l) for l in lists])
+    mem = np.concatenate([np.sort(np.array(l, np.uint32)) for l in lists]).astype(np.uint32)
+    seeds, marg = oracle.select(n, off, mem, k)
+    s = P.select_seeds(st, n, k)
+    assert s.seeds == seeds and s.marginal_counts == marg
+
+
+def test_sampled_store_selection_matches_reference(cuda, oracle, select_mode):
     """Selection over the GPU's own sampled store vs the reference's select_seeds
     over the reference's store (identical collections by the sampling parity)."""
     from paper_2411_09473_b200 import graphs
