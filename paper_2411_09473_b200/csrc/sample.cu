@@ -2549,6 +2549,9 @@ __global__ void k_build_ltguide(const uint32_t* off, const double* cdf, const ui
       if (__ldg(cdf + b + mid) <= d0) A = mid + 1;
       else ahi = mid;
     }
+    uint32_t cu = 0xffffffffu, cA = 0xffffffffu;  // the vertex and index c0 describes
+    bool cA1ok = false;                            // c1 describes index cA + 1
+    uint3 c0 = make_uint3(0, 0, 0), c1 = make_uint3(0, 0, 0);
     for (; i < iend; ++i, ++g) {
       if (g == G) {  // next vertex with in-edges; its bucket 0 has the draw 0
         do {
@@ -2578,16 +2581,38 @@ __global__ void k_build_ltguide(const uint32_t* off, const double* cdf, const ui
       e0.x = A;
       e0.y = (A < deg ? lt_fdown(__ldg(cdf + b + A)) : 0u) |
              (span == 0 ? kGuideSpan0 : span >= 2 ? kGuideSearch : 0u);
-      guide_cand(off, src, b, deg, A, e0.z, e0.w, e1.x);
+      // candidate infos, reused while consecutive buckets share A (about mult
+      // buckets per CDF entry): the source's offsets are random L2 reads
+      if (u != cu || A != cA) {
+        if (u == cu && A == cA + 1 && cA1ok) {
+          c0 = c1;
+        } else {
+          guide_cand(off, src, b, deg, A, c0.x, c0.y, c0.z);
+        }
+        cu = u;
+        cA = A;
+        cA1ok = false;
+      }
+      e0.z = c0.x;
+      e0.w = c0.y;
+      e1.x = c0.z;
       if (span == 1) {
-        guide_cand(off, src, b, deg, A + 1, e1.y, e1.z, e1.w);
+        if (!cA1ok) {
+          guide_cand(off, src, b, deg, A + 1, c1.x, c1.y, c1.z);
+          cA1ok = true;
+        }
+        e1.y = c1.x;
+        e1.z = c1.y;
+        e1.w = c1.z;
       } else {
         e1.y = span >= 2 ? span : kGuideNone;
         e1.z = 0;
         e1.w = 0;
       }
-      guide[2 * i] = e0;
-      guide[2 * i + 1] = e1;
+      asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(guide + 2 * i),
+                   "r"(e0.x), "r"(e0.y), "r"(e0.z), "r"(e0.w), "r"(e1.x), "r"(e1.y), "r"(e1.z),
+                   "r"(e1.w)
+                   : "memory");  // one 32-byte sector (STG.256)
       A = A1;
       Q = Q1;
       R = R1;
