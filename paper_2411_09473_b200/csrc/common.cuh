@@ -269,30 +269,35 @@ __device__ __forceinline__ void gf2_matvec(const uint64_t* __restrict__ M, uint6
   d = o3;
 }
 
+// 32-byte table entry in one load (sm_100: LDG.256).
+__device__ __forceinline__ void ld_u64x4(const uint64_t* p, uint64_t& a, uint64_t& b, uint64_t& c,
+                                         uint64_t& d) {
+  asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+               : "l"(p));
+}
+
 // Same product with byte tables (jump.cpp segment_tables): 32 independent
-// 32-byte loads, all in flight at once, then XORs.
+// 32-byte loads (one LDG.256 each), 16 in flight at a time, then XORs.
 __device__ __forceinline__ void gf2_jump_tables(const uint64_t* __restrict__ T, uint64_t& a,
                                                 uint64_t& b, uint64_t& c, uint64_t& d) {
   const uint64_t in[4] = {a, b, c, d};
   uint64_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {  // one state word per group: 8 loads in flight
-    ulonglong2 x[8], y[8];
+  for (int g = 0; g < 4; g += 2) {  // two state words per group: 16 loads in flight
+    uint64_t x0[16], x1[16], x2[16], x3[16];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < 16; ++q) {
       const int p = 8 * g + q;
-      const uint32_t byte = static_cast<uint32_t>(in[g] >> (8 * q)) & 255u;
-      const ulonglong2* e =
-          reinterpret_cast<const ulonglong2*>(T + (static_cast<size_t>(p) * 256 + byte) * 4);
-      x[q] = __ldg(e);
-      y[q] = __ldg(e + 1);
+      const uint32_t byte = static_cast<uint32_t>(in[g + (q >> 3)] >> (8 * (q & 7))) & 255u;
+      ld_u64x4(T + (static_cast<size_t>(p) * 256 + byte) * 4, x0[q], x1[q], x2[q], x3[q]);
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      o0 ^= x[q].x;
-      o1 ^= x[q].y;
-      o2 ^= y[q].x;
-      o3 ^= y[q].y;
+    for (int q = 0; q < 16; ++q) {
+      o0 ^= x0[q];
+      o1 ^= x1[q];
+      o2 ^= x2[q];
+      o3 ^= x3[q];
     }
   }
   a = o0;

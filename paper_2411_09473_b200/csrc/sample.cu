@@ -863,6 +863,7 @@ constexpr int kCtaWarps = kBlock / 32;
 constexpr uint32_t kCtaWin = kCtaWarps * kWin;  // 4096 in-edges
 constexpr int kCtaAmapLog = 11;                 // 2048 slots; a full map cuts the window
 constexpr uint32_t kCtaFilterWords = 8192;      // 256K bits
+constexpr uint32_t kCtaFastMin = 1024;          // single-list fast windows from this length
 constexpr uint32_t kJumpTableWords = 32 * 256 * 4;
 struct CtaWarpFields {
   uint32_t mask[kWinChunks];
@@ -962,6 +963,151 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
     bool ok = true;
     uint32_t qi = 0, qj = p.off[root];
     while (qi < nmem && ok) {
+      // ---- fast window: a slice of ONE duplicate-free in-list of at least
+      // kCtaFastMin remaining edges (hub lists). The visited set is frozen
+      // inside the window and no source repeats in it, so every unvisited edge
+      // draws and no acceptance can void a later draw: no accepted-source map,
+      // no conflict cut, no per-edge list search, three barriers.
+      {
+        const uint32_t fv = mem[qi];
+        const uint32_t fe = p.off[fv + 1];
+        if (fe - qj >= kCtaFastMin && p.dupfree[fv]) {  // uniform across the block
+          const uint32_t E = min(fe - qj, kCtaWin);
+          const uint32_t wend = wbase < E ? min(kWin, E - wbase) : 0u;
+          const uint32_t nch = (wend + 31) >> 5;
+          uint32_t mymask = 0;
+          for (uint32_t c0 = 0; c0 < nch; c0 += 4) {
+            uint2 r[4];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const uint32_t el = 32 * (c0 + q4) + lane;
+              r[q4] = el < wend ? __ldg(p.rec + qj + wbase + el) : make_uint2(0xffffffffu, 0u);
+            }
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const uint32_t c = c0 + q4;
+              if (c >= nch) break;
+              const uint32_t el = 32 * c + lane;
+              const uint32_t v = r[q4].x;
+              const bool unv = el < wend && !(cfilt_maybe(sf, v) && tab_contains(tab, stag, lg, v));
+              if (unv) {
+                ws.thr[el] = r[q4].y;
+                ws.src[el] = v;
+              }
+              const unsigned m = __ballot_sync(kFull, unv);
+              if (lane == static_cast<int>(c)) mymask = m;
+            }
+          }
+          const uint32_t cnt = __popc(mymask);
+          uint32_t ui = cnt;
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, ui, o);
+            if (lane >= o) ui += y;
+          }
+          const uint32_t Uw = __shfl_sync(kFull, ui, 31);
+          if (lane < static_cast<int>(kWinChunks)) {
+            ws.mask[lane] = mymask;
+            ws.pre[lane] = ui - cnt;
+            ws.acc[lane] = 0;
+          }
+          if (lane == 0) cs.wU[wl] = Uw;
+          __syncthreads();  // (1) unvisited counts
+          uint32_t Pw = 0, U = 0;
+          for (int w = 0; w < kCtaWarps; ++w) {
+            const uint32_t x = cs.wU[w];
+            if (w < wl) Pw += x;
+            U += x;
+          }
+          if (Uw) {  // warp wl draws stream positions [P_w, P_w + U_w); lane l the 16 from P_w + 16 l
+            const Xoshiro wst = warp_advance(p, s, Pw);
+            const uint32_t r0 = 16u * lane;
+            if (r0 < Uw) {
+              Xoshiro st = wst;
+              if (lane) gf2_jump_tables(p.jtab16 + static_cast<size_t>(lane - 1) * kJumpTableWords,
+                                        st.a, st.b, st.c, st.d);
+              uint32_t c = 0;
+              for (uint32_t step = 8; step; step >>= 1)
+                if (c + step < nch && ws.pre[c + step] <= r0) c += step;
+              uint32_t m = ws.mask[c];
+              for (uint32_t k2 = r0 - ws.pre[c]; k2; --k2) m &= m - 1;
+              const uint32_t need = min(16u, Uw - r0);
+              uint32_t acc = 0;
+              for (uint32_t done = 0; done < need;) {
+                if (!m) {
+                  if (acc) atomicOr(&ws.acc[c], acc);
+                  acc = 0;
+                  m = ws.mask[++c];
+                  continue;
+                }
+                const int bit = __ffs(m) - 1;
+                m &= m - 1;
+                const uint64_t x = st.next();
+                const uint32_t kh = static_cast<uint32_t>(x >> 32), th = ws.thr[32 * c + bit];
+                if (kh < th || (kh == th && bern_tie(x, p.w, qj + wbase + 32 * c + bit)))
+                  acc |= 1u << bit;
+                ++done;
+              }
+              if (acc) atomicOr(&ws.acc[c], acc);
+              if (Pw + r0 + need == U) {
+                cs.st[0] = st.a;
+                cs.st[1] = st.b;
+                cs.st[2] = st.c;
+                cs.st[3] = st.d;
+              }
+            }
+          }
+          __syncwarp();
+          const uint32_t am_lane = lane < static_cast<int>(nch) ? ws.acc[lane] : 0u;
+          uint32_t Aw = __popc(am_lane);
+          for (int o = 16; o; o >>= 1) Aw += __shfl_xor_sync(kFull, Aw, o);
+          if (lane == 0) cs.wA[wl] = Aw;
+          __syncthreads();  // (2) accepted counts, the stream after the window
+          if (U) s = Xoshiro{cs.st[0], cs.st[1], cs.st[2], cs.st[3]};
+          uint32_t Apre = 0, A = 0;
+          for (int w = 0; w < kCtaWarps; ++w) {
+            const uint32_t x = cs.wA[w];
+            if (w < wl) Apre += x;
+            A += x;
+          }
+          if (A) {
+            if (nmem + A > kCap) {
+              ok = false;
+            } else {
+              uint32_t lg2 = lg;
+              while (2 * (nmem + A) > (1u << lg2)) ++lg2;
+              if (lg2 != lg) {  // grow: re-insert the members under a fresh tag
+                lg = lg2;
+                ++stag;
+                for (uint32_t t = tid; t < nmem; t += kBlock) tab_insert_atomic(tab, stag, lg, mem[t]);
+                __syncthreads();
+              }
+              uint32_t base = nmem + Apre;
+              unsigned cmk = __ballot_sync(kFull, am_lane != 0);
+              while (cmk) {  // accepted sources in CSR order
+                const int c = __ffs(cmk) - 1;
+                cmk &= cmk - 1;
+                const uint32_t am = __shfl_sync(kFull, am_lane, c);
+                if ((am >> lane) & 1u) {
+                  const uint32_t v = ws.src[32 * c + lane];
+                  mem[base + __popc(am & lanemask_lt())] = v;
+                  tab_insert_atomic(tab, stag, lg, v);
+                  cfilt_add(sf, v);
+                }
+                base += __popc(am);
+              }
+              nmem += A;
+            }
+          }
+          if (tid == 0) atomicAdd(&p.ctl->windows, 1ull);
+          __syncthreads();  // (3) members appended; cs fields free for the next window
+          qj += E;
+          if (qj == fe) {
+            ++qi;
+            if (qi < nmem) qj = p.off[mem[qi]];
+          }
+          continue;
+        }
+      }
       // ---- window layout: up to 256 queued in-lists from (qi, qj). The
       // barrier closing the previous window made its members visible.
       const uint32_t nq = nmem;

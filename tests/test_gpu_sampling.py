@@ -250,6 +250,42 @@ def test_ic_cooperative_expansion_is_exact(cuda, oracle, coop_min, name, n, m, m
     assert (st.counter() == ref.counter).all()
 
 
+@pytest.mark.parametrize("mode", [2, 3])
+def test_ic_hub_lists_single_list_windows(cuda, oracle, mode):
+    """Duplicate-free hub in-lists around the block schedule's single-list fast
+    window (>= 1024 remaining edges, 4096 per window): lengths at the boundaries,
+    sources that are already visited (hubs feed each other), certain accepts
+    (weight 1) and a mix of small and near-zero weights."""
+    rng = np.random.default_rng(2024)
+    n = 30000
+    hub_deg = [1023, 1024, 1025, 4095, 4096, 4097, 8193, 20000, 3000, 1500]
+    src, dst, w = [], [], []
+    for h, d in enumerate(hub_deg):
+        s_ = rng.choice(np.arange(len(hub_deg), n), d - 4, replace=False)
+        s_ = np.concatenate([s_, [(h + 1) % len(hub_deg), (h + 3) % len(hub_deg),
+                                  (h + 5) % len(hub_deg), (h + 7) % len(hub_deg)]])
+        ww = rng.uniform(0.0, 0.004, d)
+        ww[rng.random(d) < 0.002] = 1.0
+        ww[rng.random(d) < 0.05] = 0.0
+        src.append(s_)
+        dst.append(np.full(d, h))
+        w.append(ww)
+    m2 = 150000  # background edges: every vertex reaches the hubs
+    src.append(rng.integers(0, n, m2))
+    dst.append(rng.integers(0, n, m2))
+    w.append(rng.uniform(0.0, 0.3, m2))
+    src = np.concatenate(src).astype(np.uint32)
+    dst = np.concatenate(dst).astype(np.uint32)
+    w = np.concatenate(w).astype(np.float32)
+    keep = src != dst
+    pairs = np.unique(np.stack([src[keep], dst[keep]]), axis=1, return_index=True)[1]
+    arrays = P.build_graph(n, src[keep][pairs], dst[keep][pairs], w[keep][pairs])
+    _, st, off, mem = gpu_sample(arrays, IC, 31, 1500, ic_mode=mode)
+    ref = oracle.graph(*arrays).sample(IC, 31, 0, 1500, workers=4)
+    assert_sets_equal(off, mem, ref)
+    assert (st.counter() == ref.counter).all()
+
+
 def test_ic_cooperative_expansion_with_duplicate_sources(cuda, oracle):
     """Parallel edges disable the cooperative path for that in-list only."""
     rng = np.random.default_rng(77)
