@@ -203,6 +203,40 @@ __device__ __forceinline__ bool tab_contains(const uint64_t* tab, uint32_t tag, 
   }
 }
 
+// K membership tests with every first probe in flight at once (the classify
+// loops used to wait one dependent round trip per 32-edge chunk): bit q of
+// `maybe` asks for v[q] (a filter hit); returns bit q set when v[q] is present.
+template <int K>
+__device__ __forceinline__ uint32_t tab_contains_batch(const uint64_t* tab, uint32_t tag,
+                                                       uint32_t lg, const uint32_t (&v)[K],
+                                                       uint32_t maybe) {
+  if (!maybe) return 0u;
+  const uint32_t mask = (1u << lg) - 1;
+  uint32_t h[K];
+  uint64_t e[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    h[q] = vhash(v[q]) >> (32 - lg);
+    e[q] = ((maybe >> q) & 1u) ? tab[h[q]] : 0ull;
+  }
+  uint32_t found = 0;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    if (!((maybe >> q) & 1u)) continue;
+    uint64_t x = e[q];
+    uint32_t hh = h[q];
+    while (static_cast<uint32_t>(x >> 32) == tag) {
+      if (static_cast<uint32_t>(x) == v[q]) {
+        found |= 1u << q;
+        break;
+      }
+      hh = (hh + 1) & mask;
+      x = tab[hh];
+    }
+  }
+  return found;
+}
+
 __device__ __forceinline__ void tab_insert(uint64_t* tab, uint32_t tag, uint32_t lg, uint32_t v) {
   const uint32_t mask = (1u << lg) - 1;
   uint32_t h = vhash(v) >> (32 - lg);

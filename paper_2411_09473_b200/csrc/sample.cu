@@ -186,6 +186,13 @@ struct CoopSmem {
 //   kVisSmem   32K-bit shared-memory filter + tagged table (warp mode: sets of
 //              thousands of members would saturate a register filter)
 constexpr int kVisLane = 0, kVisBitmap = 1, kVisSmem = 2;
+// records in flight per lane while classifying a window (one 256-byte chunk of
+// the in-list per load per warp): the classification is one dependent round
+// trip per kClassifyBatch chunks
+#ifndef RRG_CLASSIFY_BATCH
+#define RRG_CLASSIFY_BATCH 8
+#endif
+constexpr int kClassifyBatch = RRG_CLASSIFY_BATCH;
 constexpr uint32_t kSmemFilterWords = 1024;  // 32K bits per warp
 __device__ __forceinline__ uint32_t sfilt_bit(uint32_t v) { return (v * 0x2545F491u) >> 17; }
 __device__ __forceinline__ bool sfilt_maybe(const uint32_t* sf, uint32_t v) {
@@ -220,24 +227,37 @@ __device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uin
     const uint32_t nch = (min(1024u, je - wb) + 31) >> 5;
     // 1. unvisited mask per chunk, four chunks of records in flight
     uint32_t mymask = 0;
-    for (uint32_t c0 = 0; c0 < nch; c0 += 4) {
-      uint2 r[4];
+    for (uint32_t c0 = 0; c0 < nch; c0 += kClassifyBatch) {
+      uint2 r[kClassifyBatch];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kClassifyBatch; ++q) {
         const uint32_t j = wb + 32 * (c0 + q) + lane;
         r[q] = (c0 + q < nch && j < je) ? __ldg(p.rec + j) : make_uint2(0u, 0u);
       }
+      uint32_t seen = 0;  // bit q: record q's source is visited
+      if (kVis == kVisBitmap) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kClassifyBatch; ++q)
+          seen |= ((vis[r[q].x >> 5] >> (r[q].x & 31)) & 1u) << q;
+      } else {
+        uint32_t vv[kClassifyBatch], maybe = 0;
+#pragma unroll
+        for (int q = 0; q < kClassifyBatch; ++q) {
+          vv[q] = r[q].x;
+          const uint32_t j = wb + 32 * (c0 + q) + lane;
+          const bool hit = kVis == kVisSmem ? sfilt_maybe(sfilt, vv[q]) : f.maybe(vv[q]);
+          maybe |= (c0 + q < nch && j < je && hit ? 1u : 0u) << q;
+        }
+        seen = tab_contains_batch<kClassifyBatch>(tab, s.tag, s.lg, vv, maybe);
+      }
+#pragma unroll
+      for (int q = 0; q < kClassifyBatch; ++q) {
         const uint32_t c = c0 + q;
         if (c >= nch) break;
         const uint32_t j = wb + 32 * c + lane;
         bool unv = false;
         if (j < je) {
-          const uint32_t v = r[q].x;
-          if (kVis == kVisBitmap) unv = !((vis[v >> 5] >> (v & 31)) & 1u);
-          else if (kVis == kVisSmem) unv = !(sfilt_maybe(sfilt, v) && tab_contains(tab, s.tag, s.lg, v));
-          else unv = !(f.maybe(v) && tab_contains(tab, s.tag, s.lg, v));
+          unv = !((seen >> q) & 1u);
           sm.thr[32 * c + lane] = r[q].y;
         }
         const unsigned m = __ballot_sync(kFull, unv);
@@ -638,13 +658,20 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
             r[q4] = __ldg(p.rec + ws.lstart[t] + (e - ws.lpre[t]));
           }
         }
+        uint32_t vv[4], maybe = 0;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          vv[q4] = r[q4].x;
+          maybe |= (32 * (c0 + q4) + lane < ecur && sfilt_maybe(sf, vv[q4]) ? 1u : 0u) << q4;
+        }
+        const uint32_t seen = tab_contains_batch<4>(tab, s.tag, s.lg, vv, maybe);
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const uint32_t c = c0 + q4;
           if (32 * c >= ecur) break;
           const uint32_t e = 32 * c + lane;
           const uint32_t v = r[q4].x;
-          const bool unv = e < ecur && !(sfilt_maybe(sf, v) && tab_contains(tab, s.tag, s.lg, v));
+          const bool unv = e < ecur && !((seen >> q4) & 1u);
           if (unv) {
             ws.thr[e] = r[q4].y;
             ws.src[e] = v;
@@ -976,20 +1003,27 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
           const uint32_t wend = wbase < E ? min(kWin, E - wbase) : 0u;
           const uint32_t nch = (wend + 31) >> 5;
           uint32_t mymask = 0;
-          for (uint32_t c0 = 0; c0 < nch; c0 += 4) {
-            uint2 r[4];
+          for (uint32_t c0 = 0; c0 < nch; c0 += kClassifyBatch) {
+            uint2 r[kClassifyBatch];
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
+            for (int q4 = 0; q4 < kClassifyBatch; ++q4) {
               const uint32_t el = 32 * (c0 + q4) + lane;
               r[q4] = el < wend ? __ldg(p.rec + qj + wbase + el) : make_uint2(0xffffffffu, 0u);
             }
+            uint32_t vv[kClassifyBatch], maybe = 0;
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
+            for (int q4 = 0; q4 < kClassifyBatch; ++q4) {
+              vv[q4] = r[q4].x;
+              maybe |= (32 * (c0 + q4) + lane < wend && cfilt_maybe(sf, vv[q4]) ? 1u : 0u) << q4;
+            }
+            const uint32_t seen = tab_contains_batch<kClassifyBatch>(tab, stag, lg, vv, maybe);
+#pragma unroll
+            for (int q4 = 0; q4 < kClassifyBatch; ++q4) {
               const uint32_t c = c0 + q4;
               if (c >= nch) break;
               const uint32_t el = 32 * c + lane;
               const uint32_t v = r[q4].x;
-              const bool unv = el < wend && !(cfilt_maybe(sf, v) && tab_contains(tab, stag, lg, v));
+              const bool unv = el < wend && !((seen >> q4) & 1u);
               if (unv) {
                 ws.thr[el] = r[q4].y;
                 ws.src[el] = v;
@@ -1170,13 +1204,20 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             r[q4] = __ldg(p.rec + cs.lstart[t] + (e - cs.lpre[t]));
           }
         }
+        uint32_t vv[4], maybe = 0;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          vv[q4] = r[q4].x;
+          maybe |= (32 * (c0 + q4) + lane < wend && cfilt_maybe(sf, vv[q4]) ? 1u : 0u) << q4;
+        }
+        const uint32_t seen = tab_contains_batch<4>(tab, stag, lg, vv, maybe);
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const uint32_t c = c0 + q4;
           if (32 * c >= wend) break;
           const uint32_t el = 32 * c + lane;
           const uint32_t v = r[q4].x;
-          const bool unv = el < wend && !(cfilt_maybe(sf, v) && tab_contains(tab, stag, lg, v));
+          const bool unv = el < wend && !((seen >> q4) & 1u);
           if (unv) {
             ws.thr[el] = r[q4].y;
             ws.src[el] = v;
