@@ -19,6 +19,7 @@
 // full -- are deferred to k_big (warp per set, n-bit visited map), which
 // replays the same stream from the start.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cuda_pipeline.h>
 
 #include "internal.hpp"
@@ -2022,24 +2023,24 @@ __device__ __forceinline__ void lt_guide_fetch(const SampleParams& p, uint32_t o
                : "l"(p.ltguide + 2 * gi));
 }
 
-// Visited set of a guide-mode walk while it is short: a 1024-bit filter per lane
-// in shared memory (two bits per member; lane words interleaved across the
-// block, so every access is bank-conflict free) in front of the walk's member
-// list. Only a filter hit scans the list (the whole warp, one round trip), so
+// Visited set of a guide-mode walk while it is short: a 2048-bit filter per lane
+// (1024 in the A/B variant) in shared memory (two bits per member; lane words
+// interleaved across the block, so every access is bank-conflict free) in front
+// of the walk's member list. Only a filter hit scans the list (the whole warp, one round trip), so
 // the common "not visited" answer never leaves the SM, and the per-lane hash
 // tables (global memory, DRAM-bound once 150K lanes each own one) are used only
 // by walks longer than kLtFiltMax members.
-constexpr uint32_t kLtFiltWords = 32;
-constexpr uint32_t kLtFiltMax = 128;
 constexpr uint32_t kTabLog = 11;  // 2^11 = kTabCap entries: load <= 1/2 up to kMemCap members
 static_assert((1u << kTabLog) == kTabCap, "guide-mode tables use the whole lane table");
+// kFiltLog: log2 of the filter words per lane (5: 1024 bits, 6: 2048 bits)
+template <int kFiltLog>
 __device__ __forceinline__ void lfilt_bits(uint32_t v, uint32_t& w1, uint32_t& b1, uint32_t& w2,
                                            uint32_t& b2) {
   const uint32_t h = v * 0x9E3779B1u;
-  w1 = h >> 27;
-  b1 = (h >> 22) & 31u;
-  w2 = (h >> 17) & 31u;
-  b2 = (h >> 12) & 31u;
+  w1 = h >> (32 - kFiltLog);
+  b1 = (h >> (27 - kFiltLog)) & 31u;
+  w2 = (h >> (22 - kFiltLog)) & ((1u << kFiltLog) - 1u);
+  b2 = (h >> (17 - kFiltLog)) & 31u;
 }
 // Warp-cooperative emit (all 32 lanes, converged): every lane with `pending`
 // has a finished set in its own member list; the warp copies them one after the
@@ -2115,8 +2116,10 @@ __device__ __forceinline__ bool warp_emit_pending(const SampleParams& p, bool pe
 // while it is in flight, and the chosen source's visited test runs against the
 // shared-memory filter. Same index as the reference's linear scan
 // (sampling.hpp:127-137), same draws in the same order.
-__global__ void __launch_bounds__(kBlock, 4) k_sample_lt_guide(const SampleParams p) {
-  __shared__ uint32_t filt_all[kLtFiltWords * kBlock];
+template <int kFiltLog, uint32_t kLtFiltMax, int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) k_sample_lt_guide(const SampleParams p) {
+  constexpr uint32_t kLtFiltWords = 1u << kFiltLog;
+  extern __shared__ uint32_t filt_all[];  // kLtFiltWords * kBlock words
   uint32_t* filt = filt_all + threadIdx.x;  // word w at filt[w * kBlock]
   const int lane = threadIdx.x & 31;
   const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -2166,7 +2169,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_sample_lt_guide(const SampleParam
           active = false;
         } else {  // a new member; its next step's entry is already in flight
           uint32_t w1, b1, w2, b2;
-          lfilt_bits(vL, w1, b1, w2, b2);
+          lfilt_bits<kFiltLog>(vL, w1, b1, w2, b2);
           filt[w1 * kBlock] |= 1u << b1;
           filt[w2 * kBlock] |= 1u << b2;
           mem[nmem++] = vL;
@@ -2209,7 +2212,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_sample_lt_guide(const SampleParam
 #pragma unroll
       for (uint32_t w = 0; w < kLtFiltWords; ++w) filt[w * kBlock] = 0u;
       uint32_t w1, b1, w2, b2;
-      lfilt_bits(u, w1, b1, w2, b2);
+      lfilt_bits<kFiltLog>(u, w1, b1, w2, b2);
       filt[w1 * kBlock] |= 1u << b1;
       filt[w2 * kBlock] |= 1u << b2;
       big = false;
@@ -2236,7 +2239,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_sample_lt_guide(const SampleParam
         stop = tab_find_or_insert(tab, tag, kTabLog, v);  // chosen already visited (:137)
       } else {
         uint32_t w1, b1, w2, b2;
-        lfilt_bits(v, w1, b1, w2, b2);
+        lfilt_bits<kFiltLog>(v, w1, b1, w2, b2);
         const uint32_t f1 = filt[w1 * kBlock], f2 = filt[w2 * kBlock];
         if ((f1 >> b1) & (f2 >> b2) & 1u) {  // maybe visited: the warp scans (1)
           check = true;
@@ -2836,6 +2839,30 @@ uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64) {
   return h;
 }
 
+// Guide-mode walk variant. Default: 2048-bit filters, walks use the hash table
+// from 384 members, 64 KB of shared memory per block, three blocks per SM (80
+// registers, no spills): cfg4 2^20 walks 4.2 ms. RRGPU_LT_FILTER=0 selects the
+// first design (1024 bits, table from 128 members, 32 KB, four blocks at 64
+// registers with spills: 6.1 ms) for A/B runs.
+using LtGuideFn = void (*)(SampleParams);
+int lt_filter_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("RRGPU_LT_FILTER");
+    return e && *e == '0' ? 0 : 1;
+  }();
+  return v;
+}
+LtGuideFn lt_guide_kernel() {
+  static bool attr = false;
+  if (!attr) {
+    RRG_CUDA(cudaFuncSetAttribute(k_sample_lt_guide<6, 384, 3>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    attr = true;
+  }
+  return lt_filter_variant() ? k_sample_lt_guide<6, 384, 3> : k_sample_lt_guide<5, 128, 4>;
+}
+size_t lt_guide_smem() { return (lt_filter_variant() ? 64u : 32u) * kBlock * 4u; }
+
 int sampler_block() { return kBlock; }
 
 int sampler_blocks_per_sm(int model, uint32_t, int lt_mode) {
@@ -2843,7 +2870,8 @@ int sampler_blocks_per_sm(int model, uint32_t, int lt_mode) {
   if (model == RRG_IC)
     RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_ic, kBlock, 0));
   else if (lt_mode == kLtGuide)
-    RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_lt_guide, kBlock, 0));
+    RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, lt_guide_kernel(), kBlock,
+                                                           lt_guide_smem()));
   else
     RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_lt<16>, kBlock, 0));
   return b < 1 ? 1 : b;
@@ -2868,7 +2896,7 @@ void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inne
       k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
     }
   } else if (p.lt_scan == kLtGuide) {
-    k_sample_lt_guide<<<grid, kBlock, 0, s>>>(p);
+    lt_guide_kernel()<<<grid, kBlock, lt_guide_smem(), s>>>(p);
   } else {
     switch (p.lt_kary) {
       case 2: k_sample_lt<2><<<grid, kBlock, 0, s>>>(p); break;

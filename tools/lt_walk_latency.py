@@ -12,7 +12,7 @@ cfg = graphs.CONFIGS[name]
 arrays = graphs.generate(cfg)
 g = P.Graph(*arrays)
 g.prepare(cfg.model)
-g.set_option("lt_scan", 1)
+g.set_option("lt_scan", int(sys.argv[3]) if len(sys.argv) > 3 else 2)
 st = P.RRRStore(g)
 P.generate_slots(g, cfg.model, 1, 0, N, st)
 off, _ = st.export()
