@@ -118,6 +118,7 @@ using namespace rrgpu;
 namespace {
 
 constexpr int kMaxBlocksPerSm = 4;
+constexpr uint32_t kListMinHost = 8192;  // = kListMin (sample.cu): in-lists expanded whole
 constexpr uint32_t kBigWorkersMax = 1024;
 
 // RRGPU_DEBUG=1 prints one line per sampler launch to stderr.
@@ -417,7 +418,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
     if (model == RRG_IC) prepare_ic(g);
     else lt_mode = prepare_lt_mode(g);
     const bool ic_fast = model == RRG_IC && g->ic_rng == 1;
-    if (ic_fast) prepare_ic_fast(g);
+    if (model == RRG_IC) prepare_ic_fast(g);  // uniform-weight flags (fast mode, list expansion)
     if (!fused) s->counter_complete = false;
     const cudaStream_t st = g->stream;
     const int block = sampler_block();
@@ -446,7 +447,12 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         else if (g->ic_mode == 3) ic_cta = true;
         else if (g->ic_mode == 0) {
           if (mean < 0) ic_cta = true;
-          else if (mean >= g->ic_hub_insp) ic_warp = true;
+          else if (mean >= g->ic_hub_insp) {
+            // hub-dominated sets: block per sample when its long in-lists are
+            // expanded whole (cfg5 IMM 0.60 s vs 0.80 s per warp), else warp
+            if (g->max_indeg >= kListMinHost && g->max_indeg < (1u << 24)) ic_cta = true;
+            else ic_warp = true;
+          }
           else if (static_cast<double>(c) * mean <= g->ic_cta_max_edges) ic_cta = true;
           else ic_warp = mean >= g->ic_warp_min_insp;
         }
@@ -498,6 +504,19 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.jtab = g->jtab.ptr;
       p.jtab16 = g->jtab16.ptr;
       p.jtab256 = g->jtab256.ptr;
+      p.jtabhi = g->jtabhi.ptr;
+      p.lx = nullptr;
+      p.lx_wmax = 0;
+      if (model == RRG_IC && !ic_fast && g->max_indeg >= kListMinHost &&
+          g->max_indeg < (1u << 24)) {
+        // list expansion of long duplicate-free in-lists (CTA schedule): per CTA
+        // 34 words per 512-edge sub-window of the largest in-list
+        const uint32_t wmax = (g->max_indeg + 511) / 512;
+        const uint64_t ctas = g->scratch.lanes / block;
+        g->lx.reserve_discard(ctas * (wmax * 34ull + 2));
+        p.lx = g->lx.ptr;
+        p.lx_wmax = wmax;
+      }
       p.lt_kary = g->lt_kary;
       p.dupfree = g->dupfree.ptr;
       p.uniformw = g->uniformw.ptr;

@@ -116,6 +116,9 @@ struct rrg_graph {
   rrgpu::DevBuf<uint64_t> jtab;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab16;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab256;  // IC: byte tables of T^(256 a), a = 1..15 (3.75 MB)
+  rrgpu::DevBuf<uint64_t> jtabhi;   // IC: byte tables of T^(16^k a), k = 3, 4, 5, a = 1..15 (11.25 MB)
+  uint32_t max_indeg = 0;           // IC: largest in-list (list-expansion scratch sizing)
+  rrgpu::DevBuf<uint32_t> lx;       // IC: per-CTA list-expansion scratch (masks, counts)
   rrgpu::DevBuf<uint8_t> dupfree;  // IC: per-vertex strictly-increasing-sources flag
   rrgpu::DevBuf<uint8_t> uniformw; // IC fast mode: per-vertex "all in-weights equal" flag
   bool uniform_ready = false;
@@ -220,6 +223,9 @@ struct SampleParams {
   const uint64_t* jtab;     // byte tables of T^(32 l), l = 1..31 (jump.cpp segment_tables)
   const uint64_t* jtab16;   // byte tables of T^(16 l), l = 1..31 (warp-schedule windows)
   const uint64_t* jtab256;  // byte tables of T^(256 a), a = 1..15 (CTA-schedule windows)
+  const uint64_t* jtabhi;   // byte tables of T^(16^k a), k = 3..5, a = 1..15 (list expansion)
+  uint32_t* lx;             // per-CTA list-expansion scratch (CTA schedule), or null
+  uint32_t lx_wmax;         // sub-windows of 512 edges the scratch holds per CTA
   const uint8_t* dupfree;   // per vertex: in-list sources strictly increasing
   const uint8_t* uniformw;  // IC fast mode: per vertex, all in-weights equal
   uint32_t ic_coop_min;     // in-lists at least this long go warp-cooperative

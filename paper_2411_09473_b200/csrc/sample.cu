@@ -892,6 +892,7 @@ constexpr uint32_t kCtaWin = kCtaWarps * kWin;  // 4096 in-edges
 constexpr int kCtaAmapLog = 11;                 // 2048 slots; a full map cuts the window
 constexpr uint32_t kCtaFilterWords = 8192;      // 256K bits
 constexpr uint32_t kCtaFastMin = 1024;          // single-list fast windows from this length
+constexpr uint32_t kListMin = 8192;             // whole-list expansion from this length (= kListMinHost)
 constexpr uint32_t kJumpTableWords = 32 * 256 * 4;
 struct CtaWarpFields {
   uint32_t mask[kWinChunks];
@@ -899,6 +900,7 @@ struct CtaWarpFields {
   uint32_t acc[kWinChunks];
   uint32_t thr[kWin];
   uint32_t src[kWin];
+  unsigned long long st[4];  // list expansion: the warp's stream state after a sub-window
 };
 struct CtaSmem {
   CtaWarpFields w[kCtaWarps];
@@ -952,6 +954,49 @@ __device__ __forceinline__ Xoshiro warp_advance(const SampleParams& p, Xoshiro s
   return st;
 }
 
+// T^P st for P < 2^24, warp-uniform: one warp-cooperative table jump per
+// nonzero base-16 digit above the first (jtab16, jtab256, jtabhi), then c < 16
+// steps. The factors are powers of one matrix, so their order is free.
+__device__ __forceinline__ Xoshiro warp_advance_far(const SampleParams& p, Xoshiro st, uint32_t P) {
+  const uint32_t d5 = (P >> 20) & 15u, d4 = (P >> 16) & 15u, d3 = (P >> 12) & 15u;
+  if (d5) warp_jump(p.jtabhi + static_cast<size_t>(30 + d5 - 1) * kJumpTableWords, st);
+  if (d4) warp_jump(p.jtabhi + static_cast<size_t>(15 + d4 - 1) * kJumpTableWords, st);
+  if (d3) warp_jump(p.jtabhi + static_cast<size_t>(d3 - 1) * kJumpTableWords, st);
+  return warp_advance(p, st, P & 0xfffu);
+}
+
+// Block-wide exclusive scan of x[0, W) in place (global memory); x[W] = total,
+// which is also returned. Thread t scans a contiguous run of the entries.
+__device__ __forceinline__ uint32_t block_exscan_global(uint32_t* x, uint32_t W, uint32_t* wsum) {
+  const int tid = threadIdx.x, lane = tid & 31, wl = tid >> 5;
+  const uint32_t per = (W + kBlock - 1) / kBlock;
+  const uint32_t lo = min(W, per * tid), hi = min(W, lo + per);
+  uint32_t sum = 0;
+  for (uint32_t i = lo; i < hi; ++i) sum += x[i];
+  uint32_t incl = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[wl] = incl;
+  __syncthreads();
+  uint32_t base = 0, total = 0;
+  for (int w = 0; w < kBlock / 32; ++w) {
+    const uint32_t v = wsum[w];
+    if (w < wl) base += v;
+    total += v;
+  }
+  uint32_t run = base + incl - sum;
+  for (uint32_t i = lo; i < hi; ++i) {
+    const uint32_t t = x[i];
+    x[i] = run;
+    run += t;
+  }
+  if (tid == 0) x[W] = total;
+  __syncthreads();  // prefix visible; wsum free again
+  return total;
+}
+
 __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(const SampleParams p) {
   constexpr uint32_t kCap = kBlock * kMemCap;
   extern __shared__ __align__(16) unsigned char k_dsm[];
@@ -991,6 +1036,213 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
     bool ok = true;
     uint32_t qi = 0, qj = p.off[root];
     while (qi < nmem && ok) {
+      // ---- whole-list expansion: a duplicate-free in-list with at least kListMin
+      // remaining edges. Its unvisited edges draw consecutive stream positions in
+      // CSR order whatever gets accepted inside it (no source repeats and the
+      // visited set only changes when its accepted sources are appended), so the
+      // list is cut into 512-edge sub-windows that are classified in parallel
+      // (1), prefix-summed into stream positions (2), drawn in parallel -- warp
+      // wl walks a contiguous run of sub-windows, jumping once to its first
+      // position (3) -- and appended in CSR order (4). Four barriers per list
+      // instead of two per 4,096 edges.
+      if (p.lx) {
+        const uint32_t fv = mem[qi];
+        const uint32_t fe = p.off[fv + 1];
+        const uint32_t L = fe - qj;
+        if (L >= kListMin && L < (1u << 24) && p.dupfree[fv]) {  // uniform across the block
+          const uint32_t W = (L + kWin - 1) / kWin;
+          uint32_t* xm = p.lx + static_cast<size_t>(blockIdx.x) * (p.lx_wmax * 34ull + 2);
+          uint32_t* xa = xm + 16ull * p.lx_wmax;
+          uint32_t* xc = xa + 16ull * p.lx_wmax;
+          uint32_t* xA = xc + p.lx_wmax + 1;
+          const uint32_t t0 = (W * wl) / kCtaWarps, t1 = (W * (wl + 1)) / kCtaWarps;
+          // (1) unvisited masks and counts per sub-window
+          for (uint32_t t = t0; t < t1; ++t) {
+            const uint32_t tb = t * kWin;
+            const uint32_t wend = min(kWin, L - tb);
+            const uint32_t nch = (wend + 31) >> 5;
+            uint32_t mymask = 0;
+            {  // the sub-window's 16 source loads all in flight, then the probes
+              uint32_t vv[kWinChunks], maybe = 0;
+#pragma unroll
+              for (int q = 0; q < static_cast<int>(kWinChunks); ++q) {
+                const uint32_t el = 32 * q + lane;
+                vv[q] = el < wend ? __ldg(p.src + qj + tb + el) : 0u;
+              }
+#pragma unroll
+              for (int q = 0; q < static_cast<int>(kWinChunks); ++q)
+                maybe |= (32 * q + lane < wend && cfilt_maybe(sf, vv[q]) ? 1u : 0u) << q;
+              const uint32_t seen = tab_contains_batch<kWinChunks>(tab, stag, lg, vv, maybe);
+#pragma unroll
+              for (int q = 0; q < static_cast<int>(kWinChunks); ++q) {
+                const unsigned m = __ballot_sync(kFull, 32 * q + lane < wend && !((seen >> q) & 1u));
+                if (lane == q) mymask = m;
+              }
+            }
+            if (lane < static_cast<int>(kWinChunks)) xm[16 * t + lane] = mymask;
+            uint32_t cnt = __popc(mymask);
+            for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+            if (lane == 0) xc[t] = cnt;
+          }
+          __syncthreads();
+          // (2) stream positions of the sub-windows
+          const uint32_t U = block_exscan_global(xc, W, cs.wsum);
+          // (3) draws; warp wl's state walks its sub-windows in order
+          const bool uni = p.uniformw != nullptr && p.uniformw[fv];
+          const uint32_t uthr = uni ? __ldg(&p.rec[qj].y) : 0u;  // every edge's threshold
+          if (t0 < t1) {
+            Xoshiro wst = warp_advance_far(p, s, xc[t0]);
+            for (uint32_t t = t0; t < t1; ++t) {
+              const uint32_t Ut = xc[t + 1] - xc[t];
+              if (Ut == 0) {
+                if (lane < static_cast<int>(kWinChunks)) xa[16 * t + lane] = 0u;
+                if (lane == 0) xA[t] = 0u;
+                continue;
+              }
+              const uint32_t tb = t * kWin;
+              const uint32_t wend = min(kWin, L - tb);
+              const uint32_t nch = (wend + 31) >> 5;
+              const uint32_t r0 = 16u * lane;
+              Xoshiro st = wst;  // this lane's segment start, loads in flight with the mask's
+              if (lane && r0 < Ut)
+                gf2_jump_tables(p.jtab16 + static_cast<size_t>(lane - 1) * kJumpTableWords, st.a,
+                                st.b, st.c, st.d);
+              const uint32_t mw = lane < static_cast<int>(nch) ? xm[16 * t + lane] : 0u;
+              uint32_t ui = __popc(mw);
+              for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, ui, o);
+                if (lane >= o) ui += y;
+              }
+              if (lane < static_cast<int>(kWinChunks)) {
+                ws.mask[lane] = mw;
+                ws.pre[lane] = ui - __popc(mw);
+                ws.acc[lane] = 0;
+              }
+              if (!uni) {
+                for (uint32_t c0 = 0; c0 < nch; c0 += kClassifyBatch) {
+                  uint32_t th[kClassifyBatch];
+#pragma unroll
+                  for (int q = 0; q < kClassifyBatch; ++q) {
+                    const uint32_t el = 32 * (c0 + q) + lane;
+                    th[q] = el < wend ? __ldg(&p.rec[qj + tb + el].y) : 0u;
+                  }
+#pragma unroll
+                  for (int q = 0; q < kClassifyBatch; ++q) {
+                    const uint32_t el = 32 * (c0 + q) + lane;
+                    if (el < wend) ws.thr[el] = th[q];
+                  }
+                }
+              }
+              __syncwarp();
+              if (uni && Ut == kWin) {
+                // every edge of the sub-window draws: lane l's ranks are positions
+                // [16 l, 16 l + 16), no mask walk; lanes 2c and 2c+1 fill chunk c
+                uint32_t a16 = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const uint64_t x = st.next();
+                  const uint32_t kh = static_cast<uint32_t>(x >> 32);
+                  if (kh < uthr || (kh == uthr && bern_tie(x, p.w, qj + tb + r0 + i))) a16 |= 1u << i;
+                }
+                const uint32_t hi16 = __shfl_down_sync(kFull, a16, 1);
+                if (!(lane & 1)) ws.acc[lane >> 1] = a16 | (hi16 << 16);
+                if (lane == 31) {
+                  ws.st[0] = st.a;
+                  ws.st[1] = st.b;
+                  ws.st[2] = st.c;
+                  ws.st[3] = st.d;
+                }
+              } else if (r0 < Ut) {
+                uint32_t c = 0;
+                for (uint32_t step = 8; step; step >>= 1)
+                  if (c + step < nch && ws.pre[c + step] <= r0) c += step;
+                uint32_t m = ws.mask[c];
+                for (uint32_t k2 = r0 - ws.pre[c]; k2; --k2) m &= m - 1;
+                const uint32_t need = min(16u, Ut - r0);
+                uint32_t acc = 0;
+                for (uint32_t done = 0; done < need;) {
+                  if (!m) {
+                    if (acc) atomicOr(&ws.acc[c], acc);
+                    acc = 0;
+                    m = ws.mask[++c];
+                    continue;
+                  }
+                  const int bit = __ffs(m) - 1;
+                  m &= m - 1;
+                  const uint64_t x = st.next();
+                  const uint32_t kh = static_cast<uint32_t>(x >> 32);
+                  const uint32_t th = uni ? uthr : ws.thr[32 * c + bit];
+                  if (kh < th || (kh == th && bern_tie(x, p.w, qj + tb + 32 * c + bit)))
+                    acc |= 1u << bit;
+                  ++done;
+                }
+                if (acc) atomicOr(&ws.acc[c], acc);
+                if (r0 + need == Ut) {
+                  ws.st[0] = st.a;
+                  ws.st[1] = st.b;
+                  ws.st[2] = st.c;
+                  ws.st[3] = st.d;
+                }
+              }
+              __syncwarp();
+              wst = Xoshiro{ws.st[0], ws.st[1], ws.st[2], ws.st[3]};
+              const uint32_t aw = lane < static_cast<int>(kWinChunks) ? ws.acc[lane] : 0u;
+              if (lane < static_cast<int>(kWinChunks)) xa[16 * t + lane] = aw;
+              uint32_t na = __popc(aw);
+              for (int o = 16; o; o >>= 1) na += __shfl_xor_sync(kFull, na, o);
+              if (lane == 0) xA[t] = na;
+              __syncwarp();
+            }
+            if (t1 == W && lane == 0) {  // the stream after the list
+              cs.st[0] = wst.a;
+              cs.st[1] = wst.b;
+              cs.st[2] = wst.c;
+              cs.st[3] = wst.d;
+            }
+          }
+          __syncthreads();
+          // (4) accepted sources, appended in CSR order
+          const uint32_t A = block_exscan_global(xA, W, cs.wsum);
+          if (U) s = Xoshiro{cs.st[0], cs.st[1], cs.st[2], cs.st[3]};
+          if (A) {
+            if (nmem + A > kCap) {
+              ok = false;
+            } else {
+              uint32_t lg2 = lg;
+              while (2 * (nmem + A) > (1u << lg2)) ++lg2;
+              if (lg2 != lg) {  // grow: re-insert the members under a fresh tag
+                lg = lg2;
+                ++stag;
+                for (uint32_t t = tid; t < nmem; t += kBlock) tab_insert_atomic(tab, stag, lg, mem[t]);
+                __syncthreads();
+              }
+              for (uint32_t t = t0; t < t1; ++t) {
+                uint32_t base = nmem + xA[t];
+                const uint32_t aw = lane < static_cast<int>(kWinChunks) ? xa[16 * t + lane] : 0u;
+                unsigned cmk = __ballot_sync(kFull, aw != 0);
+                while (cmk) {
+                  const int c = __ffs(cmk) - 1;
+                  cmk &= cmk - 1;
+                  const uint32_t am = __shfl_sync(kFull, aw, c);
+                  if ((am >> lane) & 1u) {
+                    const uint32_t v = __ldg(p.src + qj + t * kWin + 32 * c + lane);
+                    mem[base + __popc(am & lanemask_lt())] = v;
+                    tab_insert_atomic(tab, stag, lg, v);
+                    cfilt_add(sf, v);
+                  }
+                  base += __popc(am);
+                }
+              }
+              nmem += A;
+            }
+          }
+          if (tid == 0) atomicAdd(&p.ctl->windows, 1ull);
+          __syncthreads();  // members appended; scratch and cs free
+          ++qi;
+          if (qi < nmem) qj = p.off[mem[qi]];
+          continue;
+        }
+      }
       // ---- fast window: a slice of ONE duplicate-free in-list of at least
       // kCtaFastMin remaining edges (hub lists). The visited set is frozen
       // inside the window and no source repeats in it, so every unvisited edge
@@ -2810,6 +3062,14 @@ __global__ void k_build_ltguide(const uint32_t* off, const double* cdf, const ui
   }
 }
 
+__global__ void k_max_degree(const uint32_t* off, uint32_t n, uint32_t* out) {
+  uint32_t best = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    best = max(best, off[v + 1] - off[v]);
+  for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(kFull, best, o));
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+}
+
 __global__ void k_check_sources(const uint32_t* src, uint64_t m, uint32_t n, uint32_t* bad) {
   bool ok = true;
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
@@ -2966,6 +3226,29 @@ void prepare_ic(rrg_graph* g) {
   static const std::vector<uint64_t> jt = segment_tables(32, 31);  // host, built once
   static const std::vector<uint64_t> jt16 = segment_tables(16, 31);
   static const std::vector<uint64_t> jt256 = segment_tables(256, 15);
+  static const std::vector<uint64_t> jthi = [] {  // T^(4096 a), T^(65536 a), T^(2^20 a)
+    std::vector<uint64_t> v;
+    for (uint64_t seg : {4096ull, 65536ull, 1048576ull}) {
+      const std::vector<uint64_t> t = segment_tables(seg, 15);
+      v.insert(v.end(), t.begin(), t.end());
+    }
+    return v;
+  }();
+  g->jtabhi.reserve_discard(jthi.size());
+  RRG_CUDA(cudaMemcpyAsync(g->jtabhi.ptr, jthi.data(), jthi.size() * 8, cudaMemcpyHostToDevice,
+                           g->stream));
+  {  // largest in-list: sizes the list-expansion scratch
+    DevBuf<uint32_t> mx;
+    mx.reserve_discard(1);
+    RRG_CUDA(cudaMemsetAsync(mx.ptr, 0, 4, g->stream));
+    if (g->n) {
+      k_max_degree<<<g->num_sms * 8, 256, 0, g->stream>>>(g->off.ptr, g->n, mx.ptr);
+      RRG_CUDA(cudaGetLastError());
+      count_launch();
+    }
+    RRG_CUDA(cudaMemcpyAsync(&g->max_indeg, mx.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
+    RRG_CUDA(cudaStreamSynchronize(g->stream));
+  }
   g->jtab.reserve_discard(jt.size());
   g->jtab16.reserve_discard(jt16.size());
   g->jtab256.reserve_discard(jt256.size());

@@ -253,12 +253,13 @@ def test_ic_cooperative_expansion_is_exact(cuda, oracle, coop_min, name, n, m, m
 @pytest.mark.parametrize("mode", [2, 3])
 def test_ic_hub_lists_single_list_windows(cuda, oracle, mode):
     """Duplicate-free hub in-lists around the block schedule's single-list fast
-    window (>= 1024 remaining edges, 4096 per window): lengths at the boundaries,
+    window (>= 1024 remaining edges, 4096 per window) and whole-list expansion
+    (>= 8192: 512-edge sub-windows, several per warp): lengths at the boundaries,
     sources that are already visited (hubs feed each other), certain accepts
     (weight 1) and a mix of small and near-zero weights."""
     rng = np.random.default_rng(2024)
-    n = 30000
-    hub_deg = [1023, 1024, 1025, 4095, 4096, 4097, 8193, 20000, 3000, 1500]
+    n = 100000
+    hub_deg = [1023, 1024, 1025, 4095, 4096, 4097, 8191, 8192, 8193, 20000, 70001, 3000, 1500]
     src, dst, w = [], [], []
     for h, d in enumerate(hub_deg):
         s_ = rng.choice(np.arange(len(hub_deg), n), d - 4, replace=False)
