@@ -95,7 +95,7 @@ __device__ __forceinline__ void warp_cover(const SelectParams& p, uint64_t s) {
 }
 
 template <bool kScan>
-__global__ void __launch_bounds__(kSelBlock) k_select(const SelectParams p) {
+__global__ void __launch_bounds__(kSelBlock, 1) k_select(const SelectParams p) {
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long red[kSelBlock / 32];
   const int lane = threadIdx.x & 31;
@@ -161,24 +161,53 @@ __global__ void __launch_bounds__(kSelBlock) k_select(const SelectParams p) {
         uint32_t hits = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) hits |= (q[j] == v ? 1u : 0u) << j;
-        unsigned hm = __ballot_sync(kFull, hits != 0);
         killed += __popc(hits);
-        while (hm) {  // lanes with matches, one set at a time per warp
-          const int L = __ffs(hm) - 1;
-          const uint32_t hL = __shfl_sync(kFull, hits, L);
-          const int j = __ffs(hL) - 1;
-          if (lane == L) {
-            hits &= hits - 1;
-          }
-          if (!(hL & (hL - 1))) hm &= hm - 1;
-          const uint64_t w = p.span[base - static_cast<uint64_t>(lane) * 8 +
-                                    static_cast<uint64_t>(L) * 8 + j];
-          const uint64_t sb = w >> 32, se = sb + (w & 0xffffffffull);
-          for (uint64_t t = sb + lane; t < se; t += 32) {
-            const uint32_t u = p.wmem[t];
-            atomicSub(p.cnt + u, 1u);
-            p.dirty[u >> kSelTileLog] = 1u;
-            p.wmem[t] = kBlank;
+        // matched sets: every matching lane loads the span of its lowest match at
+        // once (one round trip for the warp), then the warp covers the sets one
+        // after the other with the next set's first 128 members loaded while the
+        // current one is decremented
+        while (__any_sync(kFull, hits != 0)) {
+          const uint64_t w = hits ? p.span[c * 256 + static_cast<uint64_t>(lane) * 8 + (__ffs(hits) - 1)]
+                                  : 0ull;
+          unsigned hm = __ballot_sync(kFull, hits != 0);
+          if (hits) hits &= hits - 1;
+          uint64_t wL = __shfl_sync(kFull, w, __ffs(hm) - 1);
+          uint32_t pre[4];
+          auto load4 = [&](uint64_t ww, uint32_t (&r)[4]) {
+            const uint64_t sb = ww >> 32, len = ww & 0xffffffffull;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t i = static_cast<uint64_t>(lane) + 32u * k;
+              r[k] = i < len ? p.wmem[sb + i] : kBlank;
+            }
+          };
+          load4(wL, pre);
+          while (hm) {
+            hm &= hm - 1;
+            uint32_t cur[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cur[k] = pre[k];
+            const uint64_t wC = wL;
+            if (hm) {  // next set's members in flight during this set's decrements
+              wL = __shfl_sync(kFull, w, __ffs(hm) - 1);
+              load4(wL, pre);
+            }
+            const uint64_t sb = wC >> 32, se = sb + (wC & 0xffffffffull);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t t = sb + lane + 32u * k;
+              if (t < se) {
+                atomicSub(p.cnt + cur[k], 1u);
+                p.dirty[cur[k] >> kSelTileLog] = 1u;
+                p.wmem[t] = kBlank;
+              }
+            }
+            for (uint64_t t = sb + lane + 128; t < se; t += 32) {  // sets past 128 members
+              const uint32_t u = p.wmem[t];
+              atomicSub(p.cnt + u, 1u);
+              p.dirty[u >> kSelTileLog] = 1u;
+              p.wmem[t] = kBlank;
+            }
           }
         }
       }
