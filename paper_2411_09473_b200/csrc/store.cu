@@ -143,6 +143,56 @@ __global__ void k_compact(const uint32_t* stage, const uint64_t* slot_start,
   if (lane == 0 && mx) atomicMax(maxlen, mx);
 }
 
+// K3 for large batches: block per run of kCompactSets consecutive slots. Their
+// outputs are one contiguous range of the store, so threads stride over OUTPUT
+// positions (coalesced stores, four gathers in flight each) and find their slot
+// by a binary search over the run's prefix in shared memory. The warp-per-set
+// kernel above waits one round trip per set (~80 members); this one streams.
+constexpr uint32_t kCompactSets = 128;
+__global__ void __launch_bounds__(256) k_compact_runs(const uint32_t* stage, const uint64_t* slot_start,
+                                                      const uint32_t* slot_len, const uint64_t* scan,
+                                                      uint64_t base_total, uint64_t count,
+                                                      uint32_t* mem_out, uint64_t* off_out,
+                                                      uint32_t* maxlen) {
+  __shared__ uint64_t s_pre[kCompactSets + 1];
+  __shared__ uint64_t s_src[kCompactSets];
+  const uint64_t s0 = static_cast<uint64_t>(blockIdx.x) * kCompactSets;
+  const uint32_t ns = static_cast<uint32_t>(count - s0 < kCompactSets ? count - s0 : kCompactSets);
+  uint32_t mx = 0;
+  for (uint32_t i = threadIdx.x; i <= ns; i += blockDim.x) {
+    s_pre[i] = scan[s0 + i];
+    if (i < ns) {
+      s_src[i] = slot_start[s0 + i];
+      const uint32_t len = slot_len[s0 + i];
+      off_out[s0 + i + 1] = base_total + scan[s0 + i] + len;
+      mx = max(mx, len);
+    }
+  }
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxlen, mx);
+  __syncthreads();
+  const uint64_t lo = s_pre[0], hi = s_pre[ns];
+  for (uint64_t o0 = lo + threadIdx.x; o0 < hi; o0 += 4ull * blockDim.x) {
+    uint32_t v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t o = o0 + static_cast<uint64_t>(q) * blockDim.x;
+      v[q] = 0;
+      if (o < hi) {
+        uint32_t k = 0;  // last slot with s_pre[k] <= o
+        for (uint32_t step = kCompactSets / 2; step; step >>= 1)
+          if (k + step < ns && s_pre[k + step] <= o) k += step;
+        v[q] = __ldg(stage + s_src[k] + (o - s_pre[k]));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t o = o0 + static_cast<uint64_t>(q) * blockDim.x;
+      if (o < hi) mem_out[base_total + o] = v[q];
+    }
+  }
+}
+
 // K4: occurrence histogram over stored sets (build_counter, selection.hpp:79-95).
 __global__ void k_recount(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
                           uint32_t* counter) {
@@ -246,8 +296,14 @@ void launch_compact(const uint32_t* stage, const uint64_t* slot_start, const uin
                     const uint64_t* scan, uint64_t base_total, uint64_t count, uint32_t* mem_out,
                     uint64_t* off_out, uint32_t* maxlen, cudaStream_t s) {
   if (!count) return;
-  k_compact<<<grid_for(count), 256, 0, s>>>(stage, slot_start, slot_len, scan, base_total, count,
-                                            mem_out, off_out, maxlen);
+  if (count >= 4096) {
+    const uint64_t blocks = (count + kCompactSets - 1) / kCompactSets;
+    k_compact_runs<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        stage, slot_start, slot_len, scan, base_total, count, mem_out, off_out, maxlen);
+  } else {
+    k_compact<<<grid_for(count), 256, 0, s>>>(stage, slot_start, slot_len, scan, base_total, count,
+                                              mem_out, off_out, maxlen);
+  }
   RRG_CUDA(cudaGetLastError());
   count_launch();
 }
