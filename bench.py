@@ -76,6 +76,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-imm", action="store_true")
+    ap.add_argument("--no-graph-prep", action="store_true",
+                    help="skip the edge-list -> transpose comparison (device vs reference)")
     ap.add_argument("--ref-sets", type=int, default=1 << 14,
                     help="sets per step of the reference arm (bounded CPU sample)")
     return ap.parse_args()
@@ -225,6 +227,52 @@ def run_reference(args, rank):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def graph_prep(P, orc, roff, rsrc, rw, model):
+    """the workload's graph rebuilt from a shuffled edge list --
+    the device path (pinned H2D of the list + transpose + normalize_lt_weights on
+    the GPU, rrg_graph_create_from_edges) beside the reference's own
+    detail::build_graph + normalize_lt_weights (oracle/_ref, one host thread);
+    the device arrays are checked bit for bit against the reference's."""
+    import ctypes as C
+    import torch
+    n, m = roff.size - 1, rsrc.size
+    rng = np.random.default_rng(2411)
+    perm = rng.permutation(m)
+    dst = np.repeat(np.arange(n, dtype=np.uint32), np.diff(roff.astype(np.int64)))
+    pin = [torch.from_numpy(a[perm]).pin_memory().numpy() for a in (rsrc, dst, rw)]
+    lib = P.lib
+    ts = []
+    for _ in range(3):
+        h = C.c_void_p()
+        t0 = time.perf_counter()
+        P.check(lib.rrg_graph_create_from_edges(
+            n, m, P.ptr(pin[0], C.c_uint32), P.ptr(pin[1], C.c_uint32),
+            P.ptr(pin[2], C.c_float), 1 if model == 1 else 0, C.byref(h)))
+        ts.append(time.perf_counter() - t0)
+        if _ < 2:
+            lib.rrg_graph_destroy(h)
+    ro = np.zeros(n + 1, np.uint64)
+    rs = np.zeros(m, np.uint32)
+    rws = np.zeros(m, np.float32)
+    P.check(lib.rrg_graph_export_transpose(h, P.ptr(ro, C.c_uint64), P.ptr(rs, C.c_uint32),
+                                           P.ptr(rws, C.c_float)))
+    lib.rrg_graph_destroy(h)
+    t0 = time.perf_counter()
+    r_off, r_src, r_w = orc.build_graph(n, pin[0], pin[1], pin[2])
+    if model == 1:
+        r_w = orc.normalize_lt(r_off, r_w)
+    t_ref = time.perf_counter() - t0
+    same = bool((ro == r_off).all() and (rs == r_src).all() and
+                (rws.view(np.uint32) == r_w.view(np.uint32)).all())
+    return {"edges": int(m), "device_s": min(ts), "reference_s": t_ref,
+            "speedup": t_ref / min(ts), "identical_to_reference": same,
+            "device": "pinned H2D of the edge list + stable radix sort by (dst, src) + "
+                      "gather + offsets" + (" + normalize_lt_weights" if model == 1 else "")
+                      + " (rrg_graph_create_from_edges, best of 3)",
+            "reference": "detail::build_graph" + (" + normalize_lt_weights" if model == 1 else "")
+                         + f" ({orc.kind}), one host thread"}
 
 
 def run_ours(args, rank, world, local):
@@ -529,6 +577,8 @@ def run_ours(args, rank, world, local):
             "value": ncpu / dt, "unit": "sets/s", "cores": cores, "kind": orc.kind,
             "sample": f"generate_batch_fused of slots [0,{ncpu}) on WorkPool({cores})",
             "seconds": dt, "gpu_sets_match_reference": same}
+        if not args.no_graph_prep:
+            line["graph_prep"] = graph_prep(P, orc, roff, rsrc, rw, model)
         if not args.no_imm:
             store.close()
             icfg = P.ImmConfig(k=cfg.k, epsilon=cfg.epsilon, model=model)

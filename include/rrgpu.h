@@ -47,6 +47,20 @@ void rrg_graph_destroy(rrg_graph* g);
 rrg_status rrg_graph_prepare(rrg_graph* g, rrg_model model);
 /* Runs every subsequent call of this graph and its stores on `cuda_stream`
  * (a cudaStream_t; NULL restores the graph's private stream). */
+/* On-device graph preparation: uploads an edge list
+ * (src[i] -> dst[i], weight w[i]) and builds the transpose on the device in the
+ * in-list order of detail::build_graph (graph.hpp:69-115: sources ascending,
+ * parallel edges in input order), then, if normalize_lt != 0, applies
+ * normalize_lt_weights (graph.hpp:207-235) to it -- bit-identical to
+ * rrg_build_transpose + rrg_normalize_lt_weights + rrg_graph_create. Errors:
+ * RRG_EINVAL for an id >= n or (normalize) a negative weight, like the
+ * reference's std::runtime_error. m < 2^31. */
+rrg_status rrg_graph_create_from_edges(uint32_t n, uint64_t m, const uint32_t* src,
+                                       const uint32_t* dst, const float* w, int normalize_lt,
+                                       rrg_graph** out);
+/* The device transpose back on the host: roff u64[n+1], rsrc u32[m], rw f32[m]. */
+rrg_status rrg_graph_export_transpose(const rrg_graph* g, uint64_t* roff, uint32_t* rsrc,
+                                      float* rw);
 rrg_status rrg_graph_set_stream(rrg_graph* g, void* cuda_stream);
 uint32_t rrg_graph_num_vertices(const rrg_graph* g);
 uint64_t rrg_graph_num_edges(const rrg_graph* g);

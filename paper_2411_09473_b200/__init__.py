@@ -103,6 +103,37 @@ class Graph:
             w = np.zeros(0, np.float32)
         return cls(*build_graph(n, src, dst, w))
 
+    @classmethod
+    def from_edge_arrays(cls, n: int, src, dst, w, normalize_lt: bool = False) -> "Graph":
+        """Device-built transpose of an edge list (rrg_graph_create_from_edges):
+        detail::build_graph's in-list order and, with normalize_lt,
+        normalize_lt_weights -- both on the GPU. The host copies of the reverse
+        arrays are fetched back (export_transpose) so the object reads like one
+        built from host arrays."""
+        src = np.ascontiguousarray(src, dtype=np.uint32)
+        dst = np.ascontiguousarray(dst, dtype=np.uint32)
+        w = np.ascontiguousarray(w, dtype=np.float32)
+        h = C.c_void_p()
+        check(lib.rrg_graph_create_from_edges(n, src.size, ptr(src, C.c_uint32),
+                                              ptr(dst, C.c_uint32), ptr(w, C.c_float),
+                                              1 if normalize_lt else 0, C.byref(h)))
+        g = cls.__new__(cls)
+        g._h = h
+        g.num_vertices = int(n)
+        g.num_edges = int(src.size)
+        g.reverse_offsets, g.reverse_sources, g.reverse_weights = g.export_transpose()
+        return g
+
+    def export_transpose(self):
+        """(reverse_offsets u64[n+1], reverse_sources u32[m], reverse_weights f32[m])
+        as held on the device."""
+        roff = np.zeros(self.num_vertices + 1, np.uint64)
+        rsrc = np.zeros(self.num_edges, np.uint32)
+        rw = np.zeros(self.num_edges, np.float32)
+        check(lib.rrg_graph_export_transpose(self._h, ptr(roff, C.c_uint64),
+                                             ptr(rsrc, C.c_uint32), ptr(rw, C.c_float)))
+        return roff, rsrc, rw
+
     @property
     def handle(self):
         return self._h

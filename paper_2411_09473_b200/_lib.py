@@ -82,6 +82,9 @@ class GenSpec(C.Structure):
 # (name, restype, argtypes) for every symbol of include/rrgpu.h
 SIGNATURES = [
     ("rrg_graph_create", C.c_int, [C.c_uint32, C.c_uint64, u64p, u32p, f32p, C.POINTER(vp)]),
+    ("rrg_graph_create_from_edges", C.c_int,
+     [C.c_uint32, C.c_uint64, u32p, u32p, f32p, C.c_int, C.POINTER(vp)]),
+    ("rrg_graph_export_transpose", C.c_int, [vp, u64p, u32p, f32p]),
     ("rrg_graph_destroy", None, [vp]),
     ("rrg_graph_prepare", C.c_int, [vp, C.c_int]),
     ("rrg_graph_set_stream", C.c_int, [vp, vp]),

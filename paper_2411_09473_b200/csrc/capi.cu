@@ -255,6 +255,68 @@ rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* roff, const 
   return RRG_OK;
 }
 
+rrg_status rrg_graph_create_from_edges(uint32_t n, uint64_t m, const uint32_t* src,
+                                       const uint32_t* dst, const float* w, int normalize_lt,
+                                       rrg_graph** out) {
+  if (!out) return invalid("rrg_graph_create_from_edges: null output");
+  *out = nullptr;
+  if (m >= (1ull << 31)) return invalid("rrg_graph_create_from_edges: m must be < 2^31");
+  if (m && (!src || !dst || !w)) return invalid("rrg_graph_create_from_edges: null edge arrays");
+  if (n == UINT32_MAX) return invalid("rrg_graph_create_from_edges: n must be < 2^32 - 1");
+  if (n == 0 && m != 0) return invalid("rrg_graph_create_from_edges: edges without vertices");
+  auto* g = new (std::nothrow) rrg_graph;
+  if (!g) return RRG_ENOMEM;
+  const rrg_status st = guarded([&]() -> rrg_status {
+    RRG_CUDA(cudaGetDevice(&g->device));
+    RRG_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device));
+    RRG_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    g->own_stream = true;
+    RRG_CUDA(cudaEventCreate(&g->ev0));
+    RRG_CUDA(cudaEventCreate(&g->ev1));
+    g->n = n;
+    g->m = m;
+    g->ctl.reserve_discard(1);
+    DevBuf<uint32_t> d_src, d_dst;
+    DevBuf<float> d_w;
+    d_src.reserve_discard(m ? m : 1);
+    d_dst.reserve_discard(m ? m : 1);
+    d_w.reserve_discard(m ? m : 1);
+    if (m) {
+      RRG_CUDA(cudaMemcpyAsync(d_src.ptr, src, m * 4, cudaMemcpyHostToDevice, g->stream));
+      RRG_CUDA(cudaMemcpyAsync(d_dst.ptr, dst, m * 4, cudaMemcpyHostToDevice, g->stream));
+      RRG_CUDA(cudaMemcpyAsync(d_w.ptr, w, m * 4, cudaMemcpyHostToDevice, g->stream));
+    }
+    const uint64_t r = build_transpose_device(g, d_src.ptr, d_dst.ptr, d_w.ptr, normalize_lt != 0);
+    if (r == 1) return invalid("rrg_graph_create_from_edges: vertex id out of range");
+    if (r >= 2)
+      return invalid(("normalize_lt_weights: negative edge weight on vertex " +
+                      std::to_string(r - 2)).c_str());
+    return RRG_OK;
+  });
+  if (st != RRG_OK) {
+    rrg_graph_destroy(g);
+    return st;
+  }
+  *out = g;
+  return RRG_OK;
+}
+
+rrg_status rrg_graph_export_transpose(const rrg_graph* g, uint64_t* roff, uint32_t* rsrc,
+                                      float* rw) {
+  if (!g || !roff || (g->m && (!rsrc || !rw))) return invalid("null argument");
+  return guarded([&]() -> rrg_status {
+    std::vector<uint32_t> off(static_cast<size_t>(g->n) + 1);
+    d2h(off.data(), g->off.ptr, off.size(), g->stream);
+    if (g->m) {
+      d2h(rsrc, g->src.ptr, g->m, g->stream);
+      d2h(rw, g->w.ptr, g->m, g->stream);
+    }
+    sync(const_cast<rrg_graph*>(g));
+    for (size_t i = 0; i < off.size(); ++i) roff[i] = off[i];
+    return RRG_OK;
+  });
+}
+
 void rrg_graph_destroy(rrg_graph* g) {
   if (!g) return;
   if (g->stream) cudaStreamSynchronize(g->stream);

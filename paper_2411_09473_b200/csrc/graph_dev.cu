@@ -1,0 +1,153 @@
+// graph_dev.cu -- on-device graph preparation.
+//
+// A caller holding an edge list uploads it once and the device builds what
+// rrg_graph_create takes, instead of the host-side detail::build_graph
+// (graph.hpp:69-115) and normalize_lt_weights (graph.hpp:207-235):
+//   * transpose: the reference's in-list of v holds v's in-edges ordered by
+//     source id, parallel edges in input order (a stable counting sort by
+//     source, then one by target). That is a STABLE sort of the edges by the
+//     64-bit key (dst << 32 | src): one radix sort of (key, edge index) pairs,
+//     then a gather of the weights; offsets come from the run boundaries of the
+//     sorted keys (no atomics on hub counters);
+//   * normalize_lt_weights, restated per in-list with the same sequential fp64
+//     sums, the same float roundings and the same 64-attempt deflation, so the
+//     weights are bit-identical (the library builds with --fmad=false).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "internal.hpp"
+
+namespace rrgpu {
+
+namespace {
+
+__global__ void k_edge_keys(const uint32_t* src, const uint32_t* dst, uint64_t m, uint32_t n,
+                            unsigned long long* keys, uint32_t* idx, uint32_t* bad) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t s = src[i], d = dst[i];
+    if (s >= n || d >= n) atomicOr(bad, 1u);
+    keys[i] = (static_cast<unsigned long long>(d) << 32) | s;
+    idx[i] = static_cast<uint32_t>(i);
+  }
+}
+
+// Sorted keys -> transpose sources, weights and u32 offsets: the first edge of
+// target d fills off[v] for every v in (previous target, d]; the last edge
+// fills the tail up to off[n] = m.
+__global__ void k_scatter_transpose(const unsigned long long* keys, const uint32_t* idx,
+                                    const float* w_in, uint64_t m, uint32_t n, uint32_t* off,
+                                    uint32_t* rsrc, float* rw) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long k = keys[i];
+    const uint32_t d = static_cast<uint32_t>(k >> 32);
+    rsrc[i] = static_cast<uint32_t>(k);
+    rw[i] = w_in[idx[i]];
+    const uint32_t prev = i ? static_cast<uint32_t>(keys[i - 1] >> 32) : 0u;
+    if (i == 0) {
+      for (uint32_t v = 0; v <= d; ++v) off[v] = 0;
+    } else if (d != prev) {
+      for (uint32_t v = prev + 1; v <= d; ++v) off[v] = static_cast<uint32_t>(i);
+    }
+    if (i + 1 == m)
+      for (uint32_t v = d + 1; v <= n; ++v) off[v] = static_cast<uint32_t>(m);
+  }
+}
+
+// normalize_lt_weights (graph.hpp:207-235) for in-list v, sequential like the
+// reference: sum of the float weights in fp64; if above 1, scale = 1/sum,
+// deflated by (1 - 2^-20) until the fp64 sum of the float-rounded scaled
+// weights is <= 1 (at most 64 attempts), then the weights are rescaled.
+__device__ void normalize_list(float* w, uint32_t b, uint32_t e, uint32_t v, uint32_t* bad) {
+  double sum = 0.0;
+  for (uint32_t j = b; j < e; ++j) {
+    const float x = w[j];
+    if (x < 0.0f) {
+      atomicMin(bad, v);  // the reference throws at the first such vertex
+      return;
+    }
+    sum = __dadd_rn(sum, static_cast<double>(x));
+  }
+  if (sum <= 1.0) return;
+  double scale = __ddiv_rn(1.0, sum);
+  for (int attempt = 0; attempt < 64; ++attempt) {
+    double scaled = 0.0;
+    for (uint32_t j = b; j < e; ++j)
+      scaled = __dadd_rn(scaled, static_cast<double>(__double2float_rn(
+                                     __dmul_rn(static_cast<double>(w[j]), scale))));
+    if (scaled <= 1.0) break;
+    scale = __dmul_rn(scale, 1.0 - 0x1.0p-20);
+  }
+  for (uint32_t j = b; j < e; ++j)
+    w[j] = __double2float_rn(__dmul_rn(static_cast<double>(w[j]), scale));
+}
+
+__global__ void k_normalize_lt(const uint32_t* off, uint32_t n, float* w, uint32_t* bad) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    normalize_list(w, off[v], off[v + 1], v, bad);
+}
+
+}  // namespace
+
+// Builds g->off/src/w from an edge list already on the device (d_src, d_dst, d_w).
+// Returns 0, or 1 for an out-of-range vertex id, or 2 + v for a negative weight
+// on vertex v (normalize only).
+uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint32_t* d_dst,
+                                const float* d_w, bool normalize) {
+  const uint32_t n = g->n;
+  const uint64_t m = g->m;
+  const cudaStream_t st = g->stream;
+  g->off.reserve_discard(static_cast<size_t>(n) + 1);
+  g->src.reserve_discard(m ? m : 1);
+  g->w.reserve_discard(m ? m : 1);
+  DevBuf<uint32_t> bad;
+  bad.reserve_discard(2);
+  const uint32_t init[2] = {0u, 0xffffffffu};
+  RRG_CUDA(cudaMemcpyAsync(bad.ptr, init, 8, cudaMemcpyHostToDevice, st));
+  if (m == 0) {
+    RRG_CUDA(cudaMemsetAsync(g->off.ptr, 0, (static_cast<size_t>(n) + 1) * 4, st));
+  } else {
+    DevBuf<unsigned long long> keys, keys2;
+    DevBuf<uint32_t> idx, idx2;
+    keys.reserve_discard(m);
+    keys2.reserve_discard(m);
+    idx.reserve_discard(m);
+    idx2.reserve_discard(m);
+    const int grid = g->num_sms * 8;
+    k_edge_keys<<<grid, 256, 0, st>>>(d_src, d_dst, m, n, keys.ptr, idx.ptr, bad.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+    int vbits = 1;
+    while (vbits < 32 && (1ull << vbits) < n) ++vbits;
+    size_t temp_bytes = 0;
+    RRG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys.ptr, keys2.ptr, idx.ptr,
+                                             idx2.ptr, static_cast<int64_t>(m), 0, 32 + vbits,
+                                             st));
+    DevBuf<uint8_t> temp;
+    temp.reserve_discard(temp_bytes ? temp_bytes : 1);
+    RRG_CUDA(cub::DeviceRadixSort::SortPairs(temp.ptr, temp_bytes, keys.ptr, keys2.ptr, idx.ptr,
+                                             idx2.ptr, static_cast<int64_t>(m), 0, 32 + vbits,
+                                             st));
+    count_launch();
+    k_scatter_transpose<<<grid, 256, 0, st>>>(keys2.ptr, idx2.ptr, d_w, m, n, g->off.ptr,
+                                              g->src.ptr, g->w.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+    RRG_CUDA(cudaStreamSynchronize(st));  // temporaries are released at scope end
+  }
+  uint32_t hb[2] = {0, 0};
+  RRG_CUDA(cudaMemcpyAsync(hb, bad.ptr, 8, cudaMemcpyDeviceToHost, st));
+  RRG_CUDA(cudaStreamSynchronize(st));
+  if (hb[0]) return 1;
+  if (normalize && n) {
+    k_normalize_lt<<<(n + 127) / 128, 128, 0, st>>>(g->off.ptr, n, g->w.ptr, bad.ptr + 1);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+    RRG_CUDA(cudaMemcpyAsync(hb, bad.ptr, 8, cudaMemcpyDeviceToHost, st));
+    RRG_CUDA(cudaStreamSynchronize(st));
+    if (hb[1] != 0xffffffffu) return 2ull + hb[1];
+  }
+  return 0;
+}
+
+}  // namespace rrgpu

@@ -231,6 +231,10 @@ struct SampleParams {
   uint32_t ic_coop_min;     // in-lists at least this long go warp-cooperative
 };
 
+// graph_dev.cu: device transpose (+ normalize_lt_weights) of an edge list on the
+// device into g->off/src/w; 0 ok, 1 vertex out of range, 2 + v negative weight at v
+uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint32_t* d_dst,
+                                const float* d_w, bool normalize);
 void prepare_ic(rrg_graph* g);
 void prepare_ic_fast(rrg_graph* g);
 // IC fast (statistical) sampler: warp region tables, or n-bit maps (bitmap)

@@ -1,0 +1,79 @@
+"""On-device graph preparation: the transpose of an edge
+list in detail::build_graph's in-list order (graph.hpp:69-115) and
+normalize_lt_weights (graph.hpp:207-235), built on the GPU, must be
+byte-identical to the host restatements (pinned to the reference by
+tests/test_oracle_pin.py), and sampling on it must give the same sets."""
+import numpy as np
+import pytest
+
+import paper_2411_09473_b200 as P
+from helpers import assert_sets_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def edge_list(seed, n, m, hub=0, dup=0.05, wlo=0.0, whi=1.0):
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    if hub:  # one vertex with a long in-list, sources in random order
+        src = np.concatenate([src, rng.integers(0, n, hub).astype(np.uint32)])
+        dst = np.concatenate([dst, np.full(hub, n // 3, np.uint32)])
+    k = int(dup * src.size)  # parallel edges, in shuffled positions
+    pick = rng.integers(0, src.size, k)
+    src = np.concatenate([src, src[pick]])
+    dst = np.concatenate([dst, dst[pick]])
+    perm = rng.permutation(src.size)
+    src, dst = src[perm], dst[perm]
+    w = rng.uniform(wlo, whi, src.size).astype(np.float32)
+    w[rng.random(src.size) < 0.05] = 0.0
+    return src, dst, w
+
+
+def same_bits(a, b):
+    return a.shape == b.shape and (a.view(np.uint32) == b.view(np.uint32)).all()
+
+
+@pytest.mark.parametrize("n,m,hub", [(1, 0, 0), (7, 30, 0), (5000, 60000, 0),
+                                     (40000, 300000, 120000), (70000, 50000, 0)])
+def test_device_transpose_matches_build_graph(cuda, oracle, n, m, hub):
+    src, dst, w = edge_list(n + m, n, m, hub)
+    roff, rsrc, rw = oracle.build_graph(n, src, dst, w)  # detail::build_graph itself
+    g = P.Graph.from_edge_arrays(n, src, dst, w)
+    assert (g.reverse_offsets == roff).all()
+    assert (g.reverse_sources == rsrc).all()
+    assert same_bits(g.reverse_weights, rw)
+
+
+@pytest.mark.parametrize("whi", [0.01, 0.3, 1.0, 3.0])
+def test_device_normalize_matches_normalize_lt_weights(cuda, oracle, whi):
+    """Sums below one (untouched), above one (deflation loop), exact ones."""
+    n = 20000
+    src, dst, w = edge_list(int(whi * 100), n, 200000, hub=60000, whi=whi)
+    roff, rsrc, rw = oracle.build_graph(n, src, dst, w)
+    rw_n = oracle.normalize_lt(roff, rw.copy())
+    g = P.Graph.from_edge_arrays(n, src, dst, w, normalize_lt=True)
+    assert (g.reverse_sources == rsrc).all()
+    assert same_bits(g.reverse_weights, rw_n)
+
+
+def test_device_graph_errors(cuda):
+    with pytest.raises(ValueError):
+        P.Graph.from_edge_arrays(4, [0, 5], [1, 2], [0.5, 0.5])
+    with pytest.raises(ValueError):
+        P.Graph.from_edge_arrays(4, [0, 1], [1, 2], [0.5, -0.5], normalize_lt=True)
+    g = P.Graph.from_edge_arrays(4, [0, 1], [1, 2], [0.5, -0.5])  # no normalization: kept
+    assert g.reverse_weights.tolist() == [0.5, -0.5]
+
+
+@pytest.mark.parametrize("model", [0, 1])
+def test_sampling_on_device_built_graph(cuda, oracle, model):
+    n = 3000
+    src, dst, w = edge_list(9, n, 40000, hub=5000, whi=0.2 if model == 0 else 1.0)
+    g = P.Graph.from_edge_arrays(n, src, dst, w, normalize_lt=model == 1)
+    st = P.RRRStore(g)
+    P.generate_batch(g, model, 5, 3000, st)
+    off, mem = st.export()
+    arrays = (g.reverse_offsets, g.reverse_sources, g.reverse_weights)
+    ref = oracle.graph(*arrays).sample(model, 5, 0, 3000, workers=4)
+    assert_sets_equal(off, mem, ref)
