@@ -567,15 +567,16 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.jtab16 = g->jtab16.ptr;
       p.jtab256 = g->jtab256.ptr;
       p.jtabhi = g->jtabhi.ptr;
+      p.jtab64 = g->jtab64.ptr;
       p.lx = nullptr;
       p.lx_wmax = 0;
       if (model == RRG_IC && !ic_fast && g->max_indeg >= kListMinHost &&
           g->max_indeg < (1u << 24)) {
         // list expansion of long duplicate-free in-lists (CTA schedule): per CTA
-        // 34 words per 512-edge sub-window of the largest in-list
-        const uint32_t wmax = (g->max_indeg + 511) / 512;
+        // 2 x (kLxWin / 32) + 2 words per sub-window of the largest in-list
+        const uint32_t wmax = (g->max_indeg + kLxWin - 1) / kLxWin;
         const uint64_t ctas = g->scratch.lanes / block;
-        g->lx.reserve_discard(ctas * (wmax * 34ull + 2));
+        g->lx.reserve_discard(ctas * (wmax * (2ull * kLxWin / 32 + 2) + 2));
         p.lx = g->lx.ptr;
         p.lx_wmax = wmax;
       }

@@ -72,6 +72,12 @@ struct DevBuf {
 
 enum LtScan : int { kLtLinear = 0, kLtBsearch = 1, kLtGuide = 2 };
 
+// IC whole-list expansion (sample.cu): 32-edge chunks per lane of a sub-window
+#ifndef RRG_LX_CPL
+#define RRG_LX_CPL 1
+#endif
+constexpr uint32_t kLxWin = 1024u * RRG_LX_CPL;  // edges per list-expansion sub-window
+
 // Per-lane sampler scratch: visit-order list + tagged hash table + tag.
 // Tagged tables are never cleared; that is sound because the region layouts
 // draw tags from disjoint ranges: lane regions (IC lane mode, LT) use tags in
@@ -117,6 +123,7 @@ struct rrg_graph {
   rrgpu::DevBuf<uint64_t> jtab16;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab256;  // IC: byte tables of T^(256 a), a = 1..15 (3.75 MB)
   rrgpu::DevBuf<uint64_t> jtabhi;   // IC: byte tables of T^(16^k a), k = 3, 4, 5, a = 1..15 (11.25 MB)
+  rrgpu::DevBuf<uint64_t> jtab64;   // IC: byte tables of T^(kLxPer l), l = 1..31 (list expansion)
   uint32_t max_indeg = 0;           // IC: largest in-list (list-expansion scratch sizing)
   rrgpu::DevBuf<uint32_t> lx;       // IC: per-CTA list-expansion scratch (masks, counts)
   rrgpu::DevBuf<uint8_t> dupfree;  // IC: per-vertex strictly-increasing-sources flag
@@ -224,6 +231,7 @@ struct SampleParams {
   const uint64_t* jtab16;   // byte tables of T^(16 l), l = 1..31 (warp-schedule windows)
   const uint64_t* jtab256;  // byte tables of T^(256 a), a = 1..15 (CTA-schedule windows)
   const uint64_t* jtabhi;   // byte tables of T^(16^k a), k = 3..5, a = 1..15 (list expansion)
+  const uint64_t* jtab64;   // byte tables of T^(kLxPer l), l = 1..31 (list-expansion lanes)
   uint32_t* lx;             // per-CTA list-expansion scratch (CTA schedule), or null
   uint32_t lx_wmax;         // sub-windows of 512 edges the scratch holds per CTA
   const uint8_t* dupfree;   // per vertex: in-list sources strictly increasing

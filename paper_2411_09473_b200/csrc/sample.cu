@@ -894,12 +894,21 @@ constexpr uint32_t kCtaFilterWords = 8192;      // 256K bits
 constexpr uint32_t kCtaFastMin = 1024;          // single-list fast windows from this length
 constexpr uint32_t kListMin = 8192;             // whole-list expansion from this length (= kListMinHost)
 constexpr uint32_t kJumpTableWords = 32 * 256 * 4;
+constexpr int kLxCpl = RRG_LX_CPL;            // list expansion: 32-edge chunks per lane
+constexpr uint32_t kLxPer = 32u * kLxCpl;     // draws per lane per sub-window
+constexpr uint32_t kLxWords = 32u * kLxCpl;   // mask words (chunks) per sub-window
 struct CtaWarpFields {
   uint32_t mask[kWinChunks];
   uint32_t pre[kWinChunks];
   uint32_t acc[kWinChunks];
-  uint32_t thr[kWin];
-  uint32_t src[kWin];
+  union {
+    struct {
+      uint32_t thr[kWin];
+      uint32_t src[kWin];
+    };
+    uint32_t lxthr[2 * kWin];  // list expansion: the sub-window's thresholds (unequal weights)
+  };
+  uint32_t lxmask[kLxWords], lxpre[kLxWords], lxacc[kLxWords];  // list expansion: per chunk
   unsigned long long st[4];  // list expansion: the warp's stream state after a sub-window
 };
 struct CtaSmem {
@@ -1040,7 +1049,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       // remaining edges. Its unvisited edges draw consecutive stream positions in
       // CSR order whatever gets accepted inside it (no source repeats and the
       // visited set only changes when its accepted sources are appended), so the
-      // list is cut into 512-edge sub-windows that are classified in parallel
+      // list is cut into 1024-edge sub-windows that are classified in parallel
       // (1), prefix-summed into stream positions (2), drawn in parallel -- warp
       // wl walks a contiguous run of sub-windows, jumping once to its first
       // position (3) -- and appended in CSR order (4). Four barriers per list
@@ -1049,76 +1058,86 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
         const uint32_t fv = mem[qi];
         const uint32_t fe = p.off[fv + 1];
         const uint32_t L = fe - qj;
-        if (L >= kListMin && L < (1u << 24) && p.dupfree[fv]) {  // uniform across the block
-          const uint32_t W = (L + kWin - 1) / kWin;
-          uint32_t* xm = p.lx + static_cast<size_t>(blockIdx.x) * (p.lx_wmax * 34ull + 2);
-          uint32_t* xa = xm + 16ull * p.lx_wmax;
-          uint32_t* xc = xa + 16ull * p.lx_wmax;
+        const bool uni = p.uniformw != nullptr && p.uniformw[fv];  // one threshold (WC)
+        if (L >= kListMin && L < (1u << 24) && p.dupfree[fv] &&
+            (uni || kLxWin <= 2 * kWin)) {  // uniform across the block
+          const uint32_t W = (L + kLxWin - 1) / kLxWin;
+          uint32_t* xm = p.lx + static_cast<size_t>(blockIdx.x) * (p.lx_wmax * (2ull * kLxWords + 2) + 2);
+          uint32_t* xa = xm + static_cast<uint64_t>(kLxWords) * p.lx_wmax;
+          uint32_t* xc = xa + static_cast<uint64_t>(kLxWords) * p.lx_wmax;
           uint32_t* xA = xc + p.lx_wmax + 1;
           const uint32_t t0 = (W * wl) / kCtaWarps, t1 = (W * (wl + 1)) / kCtaWarps;
-          // (1) unvisited masks and counts per sub-window
+          // (1) unvisited masks and counts per sub-window: lane c ends with the
+          //     mask of 32-edge chunk c
           for (uint32_t t = t0; t < t1; ++t) {
-            const uint32_t tb = t * kWin;
-            const uint32_t wend = min(kWin, L - tb);
-            const uint32_t nch = (wend + 31) >> 5;
-            uint32_t mymask = 0;
-            {  // the sub-window's 16 source loads all in flight, then the probes
-              uint32_t vv[kWinChunks], maybe = 0;
+            const uint32_t tb = t * kLxWin;
+            const uint32_t wend = min(kLxWin, L - tb);
+            uint32_t mymask[kLxCpl] = {};
+            uint32_t cnt = 0;
 #pragma unroll
-              for (int q = 0; q < static_cast<int>(kWinChunks); ++q) {
-                const uint32_t el = 32 * q + lane;
+            for (int part = 0; part < 2 * kLxCpl; ++part) {  // 16 loads in flight, then the probes
+              uint32_t vv[16], maybe = 0;
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                const uint32_t el = 32 * (16 * part + q) + lane;
                 vv[q] = el < wend ? __ldg(p.src + qj + tb + el) : 0u;
               }
 #pragma unroll
-              for (int q = 0; q < static_cast<int>(kWinChunks); ++q)
-                maybe |= (32 * q + lane < wend && cfilt_maybe(sf, vv[q]) ? 1u : 0u) << q;
-              const uint32_t seen = tab_contains_batch<kWinChunks>(tab, stag, lg, vv, maybe);
+              for (int q = 0; q < 16; ++q)
+                maybe |= (32 * (16 * part + q) + lane < wend && cfilt_maybe(sf, vv[q]) ? 1u : 0u) << q;
+              const uint32_t seen = tab_contains_batch<16>(tab, stag, lg, vv, maybe);
 #pragma unroll
-              for (int q = 0; q < static_cast<int>(kWinChunks); ++q) {
-                const unsigned m = __ballot_sync(kFull, 32 * q + lane < wend && !((seen >> q) & 1u));
-                if (lane == q) mymask = m;
+              for (int q = 0; q < 16; ++q) {
+                const int c = 16 * part + q;
+                const unsigned m = __ballot_sync(kFull, 32 * c + lane < wend && !((seen >> q) & 1u));
+                cnt += __popc(m);
+                if (lane == (c & 31)) mymask[c >> 5] = m;
               }
             }
-            if (lane < static_cast<int>(kWinChunks)) xm[16 * t + lane] = mymask;
-            uint32_t cnt = __popc(mymask);
-            for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+#pragma unroll
+            for (int i = 0; i < kLxCpl; ++i) xm[kLxWords * t + 32 * i + lane] = mymask[i];
             if (lane == 0) xc[t] = cnt;
           }
           __syncthreads();
           // (2) stream positions of the sub-windows
           const uint32_t U = block_exscan_global(xc, W, cs.wsum);
-          // (3) draws; warp wl's state walks its sub-windows in order
-          const bool uni = p.uniformw != nullptr && p.uniformw[fv];
+          // (3) draws; warp wl's state walks its sub-windows in order, lane l
+          //     draws ranks [32 l, 32 l + 32) after one jump by T^(32 l)
           const uint32_t uthr = uni ? __ldg(&p.rec[qj].y) : 0u;  // every edge's threshold
           if (t0 < t1) {
             Xoshiro wst = warp_advance_far(p, s, xc[t0]);
             for (uint32_t t = t0; t < t1; ++t) {
               const uint32_t Ut = xc[t + 1] - xc[t];
               if (Ut == 0) {
-                if (lane < static_cast<int>(kWinChunks)) xa[16 * t + lane] = 0u;
+#pragma unroll
+                for (int i = 0; i < kLxCpl; ++i) xa[kLxWords * t + 32 * i + lane] = 0u;
                 if (lane == 0) xA[t] = 0u;
                 continue;
               }
-              const uint32_t tb = t * kWin;
-              const uint32_t wend = min(kWin, L - tb);
+              const uint32_t tb = t * kLxWin;
+              const uint32_t wend = min(kLxWin, L - tb);
               const uint32_t nch = (wend + 31) >> 5;
-              const uint32_t r0 = 16u * lane;
-              Xoshiro st = wst;  // this lane's segment start, loads in flight with the mask's
+              const uint32_t r0 = kLxPer * lane;
+              Xoshiro st = wst;  // this lane's segment start, loads in flight with the masks'
               if (lane && r0 < Ut)
-                gf2_jump_tables(p.jtab16 + static_cast<size_t>(lane - 1) * kJumpTableWords, st.a,
+                gf2_jump_tables(p.jtab64 + static_cast<size_t>(lane - 1) * kJumpTableWords, st.a,
                                 st.b, st.c, st.d);
-              const uint32_t mw = lane < static_cast<int>(nch) ? xm[16 * t + lane] : 0u;
-              uint32_t ui = __popc(mw);
-              for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(kFull, ui, o);
-                if (lane >= o) ui += y;
+              uint32_t mw[kLxCpl], run = 0;
+#pragma unroll
+              for (int i = 0; i < kLxCpl; ++i) mw[i] = xm[kLxWords * t + 32 * i + lane];
+#pragma unroll
+              for (int i = 0; i < kLxCpl; ++i) {  // chunk 32 i + lane: prefix over chunks
+                uint32_t ui = __popc(mw[i]);
+                for (int o = 1; o < 32; o <<= 1) {
+                  const uint32_t y = __shfl_up_sync(kFull, ui, o);
+                  if (lane >= o) ui += y;
+                }
+                ws.lxmask[32 * i + lane] = mw[i];
+                ws.lxpre[32 * i + lane] = run + ui - __popc(mw[i]);
+                ws.lxacc[32 * i + lane] = 0;
+                run += __shfl_sync(kFull, ui, 31);
               }
-              if (lane < static_cast<int>(kWinChunks)) {
-                ws.mask[lane] = mw;
-                ws.pre[lane] = ui - __popc(mw);
-                ws.acc[lane] = 0;
-              }
-              if (!uni) {
+              if (!uni) {  // unequal weights: the sub-window's thresholds to shared memory
                 for (uint32_t c0 = 0; c0 < nch; c0 += kClassifyBatch) {
                   uint32_t th[kClassifyBatch];
 #pragma unroll
@@ -1129,23 +1148,25 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
 #pragma unroll
                   for (int q = 0; q < kClassifyBatch; ++q) {
                     const uint32_t el = 32 * (c0 + q) + lane;
-                    if (el < wend) ws.thr[el] = th[q];
+                    if (el < wend) ws.lxthr[el] = th[q];
                   }
                 }
               }
               __syncwarp();
-              if (uni && Ut == kWin) {
-                // every edge of the sub-window draws: lane l's ranks are positions
-                // [16 l, 16 l + 16), no mask walk; lanes 2c and 2c+1 fill chunk c
-                uint32_t a16 = 0;
+              if (uni && Ut == kLxWin) {
+                // every edge draws: lane l's ranks are exactly chunks kLxCpl l + i
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                  const uint64_t x = st.next();
-                  const uint32_t kh = static_cast<uint32_t>(x >> 32);
-                  if (kh < uthr || (kh == uthr && bern_tie(x, p.w, qj + tb + r0 + i))) a16 |= 1u << i;
+                for (int c = 0; c < kLxCpl; ++c) {
+                  uint32_t a32 = 0;
+#pragma unroll 8
+                  for (int i = 0; i < 32; ++i) {
+                    const uint64_t x = st.next();
+                    const uint32_t kh = static_cast<uint32_t>(x >> 32);
+                    if (kh < uthr || (kh == uthr && bern_tie(x, p.w, qj + tb + r0 + 32 * c + i)))
+                      a32 |= 1u << i;
+                  }
+                  ws.lxacc[kLxCpl * lane + c] = a32;
                 }
-                const uint32_t hi16 = __shfl_down_sync(kFull, a16, 1);
-                if (!(lane & 1)) ws.acc[lane >> 1] = a16 | (hi16 << 16);
                 if (lane == 31) {
                   ws.st[0] = st.a;
                   ws.st[1] = st.b;
@@ -1154,29 +1175,29 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
                 }
               } else if (r0 < Ut) {
                 uint32_t c = 0;
-                for (uint32_t step = 8; step; step >>= 1)
-                  if (c + step < nch && ws.pre[c + step] <= r0) c += step;
-                uint32_t m = ws.mask[c];
-                for (uint32_t k2 = r0 - ws.pre[c]; k2; --k2) m &= m - 1;
-                const uint32_t need = min(16u, Ut - r0);
+                for (uint32_t step = kLxWords / 2; step; step >>= 1)
+                  if (c + step < nch && ws.lxpre[c + step] <= r0) c += step;
+                uint32_t m = ws.lxmask[c];
+                for (uint32_t k2 = r0 - ws.lxpre[c]; k2; --k2) m &= m - 1;
+                const uint32_t need = min(kLxPer, Ut - r0);
                 uint32_t acc = 0;
                 for (uint32_t done = 0; done < need;) {
                   if (!m) {
-                    if (acc) atomicOr(&ws.acc[c], acc);
+                    if (acc) atomicOr(&ws.lxacc[c], acc);
                     acc = 0;
-                    m = ws.mask[++c];
+                    m = ws.lxmask[++c];
                     continue;
                   }
                   const int bit = __ffs(m) - 1;
                   m &= m - 1;
                   const uint64_t x = st.next();
                   const uint32_t kh = static_cast<uint32_t>(x >> 32);
-                  const uint32_t th = uni ? uthr : ws.thr[32 * c + bit];
+                  const uint32_t th = uni ? uthr : ws.lxthr[32 * c + bit];
                   if (kh < th || (kh == th && bern_tie(x, p.w, qj + tb + 32 * c + bit)))
                     acc |= 1u << bit;
                   ++done;
                 }
-                if (acc) atomicOr(&ws.acc[c], acc);
+                if (acc) atomicOr(&ws.lxacc[c], acc);
                 if (r0 + need == Ut) {
                   ws.st[0] = st.a;
                   ws.st[1] = st.b;
@@ -1186,9 +1207,13 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               }
               __syncwarp();
               wst = Xoshiro{ws.st[0], ws.st[1], ws.st[2], ws.st[3]};
-              const uint32_t aw = lane < static_cast<int>(kWinChunks) ? ws.acc[lane] : 0u;
-              if (lane < static_cast<int>(kWinChunks)) xa[16 * t + lane] = aw;
-              uint32_t na = __popc(aw);
+              uint32_t na = 0;
+#pragma unroll
+              for (int i = 0; i < kLxCpl; ++i) {
+                const uint32_t aw = ws.lxacc[32 * i + lane];
+                xa[kLxWords * t + 32 * i + lane] = aw;
+                na += __popc(aw);
+              }
               for (int o = 16; o; o >>= 1) na += __shfl_xor_sync(kFull, na, o);
               if (lane == 0) xA[t] = na;
               __syncwarp();
@@ -1218,19 +1243,22 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               }
               for (uint32_t t = t0; t < t1; ++t) {
                 uint32_t base = nmem + xA[t];
-                const uint32_t aw = lane < static_cast<int>(kWinChunks) ? xa[16 * t + lane] : 0u;
-                unsigned cmk = __ballot_sync(kFull, aw != 0);
-                while (cmk) {
-                  const int c = __ffs(cmk) - 1;
-                  cmk &= cmk - 1;
-                  const uint32_t am = __shfl_sync(kFull, aw, c);
-                  if ((am >> lane) & 1u) {
-                    const uint32_t v = __ldg(p.src + qj + t * kWin + 32 * c + lane);
-                    mem[base + __popc(am & lanemask_lt())] = v;
-                    tab_insert_atomic(tab, stag, lg, v);
-                    cfilt_add(sf, v);
+#pragma unroll
+                for (int i = 0; i < kLxCpl; ++i) {  // chunks 32 i .. 32 i + 31, in order
+                  const uint32_t aw = xa[kLxWords * t + 32 * i + lane];
+                  unsigned cmk = __ballot_sync(kFull, aw != 0);
+                  while (cmk) {
+                    const int c = __ffs(cmk) - 1;
+                    cmk &= cmk - 1;
+                    const uint32_t am = __shfl_sync(kFull, aw, c);
+                    if ((am >> lane) & 1u) {
+                      const uint32_t v = __ldg(p.src + qj + t * kLxWin + 32 * (32 * i + c) + lane);
+                      mem[base + __popc(am & lanemask_lt())] = v;
+                      tab_insert_atomic(tab, stag, lg, v);
+                      cfilt_add(sf, v);
+                    }
+                    base += __popc(am);
                   }
-                  base += __popc(am);
                 }
               }
               nmem += A;
@@ -3226,6 +3254,10 @@ void prepare_ic(rrg_graph* g) {
   static const std::vector<uint64_t> jt = segment_tables(32, 31);  // host, built once
   static const std::vector<uint64_t> jt16 = segment_tables(16, 31);
   static const std::vector<uint64_t> jt256 = segment_tables(256, 15);
+  static const std::vector<uint64_t> jt64 = segment_tables(kLxPer, 31);  // list-expansion lanes
+  g->jtab64.reserve_discard(jt64.size());
+  RRG_CUDA(cudaMemcpyAsync(g->jtab64.ptr, jt64.data(), jt64.size() * 8, cudaMemcpyHostToDevice,
+                           g->stream));
   static const std::vector<uint64_t> jthi = [] {  // T^(4096 a), T^(65536 a), T^(2^20 a)
     std::vector<uint64_t> v;
     for (uint64_t seg : {4096ull, 65536ull, 1048576ull}) {

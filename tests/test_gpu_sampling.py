@@ -250,8 +250,9 @@ def test_ic_cooperative_expansion_is_exact(cuda, oracle, coop_min, name, n, m, m
     assert (st.counter() == ref.counter).all()
 
 
+@pytest.mark.parametrize("wc", [False, True])
 @pytest.mark.parametrize("mode", [2, 3])
-def test_ic_hub_lists_single_list_windows(cuda, oracle, mode):
+def test_ic_hub_lists_single_list_windows(cuda, oracle, mode, wc):
     """Duplicate-free hub in-lists around the block schedule's single-list fast
     window (>= 1024 remaining edges, 4096 per window) and whole-list expansion
     (>= 8192: 512-edge sub-windows, several per warp): lengths at the boundaries,
@@ -281,6 +282,11 @@ def test_ic_hub_lists_single_list_windows(cuda, oracle, mode):
     keep = src != dst
     pairs = np.unique(np.stack([src[keep], dst[keep]]), axis=1, return_index=True)[1]
     arrays = P.build_graph(n, src[keep][pairs], dst[keep][pairs], w[keep][pairs])
+    if wc:  # weighted cascade: equal in-weights 1/indeg (the whole-list expansion path)
+        roff = arrays[0].astype(np.int64)
+        deg = np.diff(roff)
+        arrays = (arrays[0], arrays[1],
+                  np.repeat((1.0 / np.maximum(deg, 1)).astype(np.float32), deg))
     _, st, off, mem = gpu_sample(arrays, IC, 31, 1500, ic_mode=mode)
     ref = oracle.graph(*arrays).sample(IC, 31, 0, 1500, workers=4)
     assert_sets_equal(off, mem, ref)
