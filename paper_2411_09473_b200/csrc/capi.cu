@@ -118,7 +118,6 @@ using namespace rrgpu;
 namespace {
 
 constexpr int kMaxBlocksPerSm = 4;
-constexpr uint32_t kListMinHost = 8192;  // = kListMin (sample.cu): in-lists expanded whole
 constexpr uint32_t kBigWorkersMax = 1024;
 
 // RRGPU_DEBUG=1 prints one line per sampler launch to stderr.
@@ -512,7 +511,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
           else if (mean >= g->ic_hub_insp) {
             // hub-dominated sets: block per sample when its long in-lists are
             // expanded whole (cfg5 IMM 0.60 s vs 0.80 s per warp), else warp
-            if (g->max_indeg >= kListMinHost && g->max_indeg < (1u << 24)) ic_cta = true;
+            if (g->max_indeg >= kListMin && g->max_indeg < (1u << 24)) ic_cta = true;
             else ic_warp = true;
           }
           else if (static_cast<double>(c) * mean <= g->ic_cta_max_edges) ic_cta = true;
@@ -570,7 +569,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.jtab64 = g->jtab64.ptr;
       p.lx = nullptr;
       p.lx_wmax = 0;
-      if (model == RRG_IC && !ic_fast && g->max_indeg >= kListMinHost &&
+      if (model == RRG_IC && !ic_fast && g->max_indeg >= kListMin &&
           g->max_indeg < (1u << 24)) {
         // list expansion of long duplicate-free in-lists (CTA schedule): per CTA
         // 2 x (kLxWin / 32) + 2 words per sub-window of the largest in-list

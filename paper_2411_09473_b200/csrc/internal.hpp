@@ -77,6 +77,10 @@ enum LtScan : int { kLtLinear = 0, kLtBsearch = 1, kLtGuide = 2 };
 #define RRG_LX_CPL 1
 #endif
 constexpr uint32_t kLxWin = 1024u * RRG_LX_CPL;  // edges per list-expansion sub-window
+#ifndef RRG_LIST_MIN
+#define RRG_LIST_MIN 8192
+#endif
+constexpr uint32_t kListMin = RRG_LIST_MIN;  // in-lists at least this long are expanded whole
 
 // Per-lane sampler scratch: visit-order list + tagged hash table + tag.
 // Tagged tables are never cleared; that is sound because the region layouts

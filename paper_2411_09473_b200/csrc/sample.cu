@@ -892,7 +892,6 @@ constexpr uint32_t kCtaWin = kCtaWarps * kWin;  // 4096 in-edges
 constexpr int kCtaAmapLog = 11;                 // 2048 slots; a full map cuts the window
 constexpr uint32_t kCtaFilterWords = 8192;      // 256K bits
 constexpr uint32_t kCtaFastMin = 1024;          // single-list fast windows from this length
-constexpr uint32_t kListMin = 8192;             // whole-list expansion from this length (= kListMinHost)
 constexpr uint32_t kJumpTableWords = 32 * 256 * 4;
 constexpr int kLxCpl = RRG_LX_CPL;            // list expansion: 32-edge chunks per lane
 constexpr uint32_t kLxPer = 32u * kLxCpl;     // draws per lane per sub-window
