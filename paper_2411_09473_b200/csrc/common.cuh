@@ -191,15 +191,40 @@ constexpr uint32_t kGuidePivot = 0x3fffffffu;
 
 __device__ __forceinline__ uint32_t vhash(uint32_t v) { return v * 0x9E3779B1u; }
 
+// RRG_PROBE_GUARD (debug builds): a probe chain longer than the table traps
+// with a code naming the loop, instead of spinning forever.
+#ifdef RRG_PROBE_GUARD
+#define RRG_GUARD(cnt, lg, code)                                                   \
+  if (++(cnt) > (2u << (lg))) {                                                    \
+    uint32_t same = 0, minv = 0xffffffffu, maxv = 0;                               \
+    for (uint32_t i_ = 0; i_ < (1u << (lg)); ++i_) {                               \
+      const uint64_t e_ = tab[i_];                                                 \
+      if (static_cast<uint32_t>(e_ >> 32) == tag) {                                \
+        ++same;                                                                    \
+        minv = min(minv, static_cast<uint32_t>(e_));                               \
+        maxv = max(maxv, static_cast<uint32_t>(e_));                               \
+      }                                                                            \
+    }                                                                              \
+    printf("rrgpu probe guard %d: blk %d thr %d tab %p lg %u tag %u v %u same %u "   \
+           "vals %u..%u\n", (code), blockIdx.x, threadIdx.x, (const void*)tab,      \
+           (lg), tag, v, same, minv, maxv);                                         \
+    __trap();                                                                      \
+  }
+#else
+#define RRG_GUARD(cnt, lg, code)
+#endif
+
 __device__ __forceinline__ bool tab_contains(const uint64_t* tab, uint32_t tag, uint32_t lg,
                                              uint32_t v) {
   const uint32_t mask = (1u << lg) - 1;
   uint32_t h = vhash(v) >> (32 - lg);
+  uint32_t guard = 0;
   while (true) {
     const uint64_t e = tab[h];
     if (static_cast<uint32_t>(e >> 32) != tag) return false;
     if (static_cast<uint32_t>(e) == v) return true;
     h = (h + 1) & mask;
+    RRG_GUARD(guard, lg, 1)
   }
 }
 
@@ -208,7 +233,7 @@ __device__ __forceinline__ bool tab_contains(const uint64_t* tab, uint32_t tag, 
 // `maybe` asks for v[q] (a filter hit); returns bit q set when v[q] is present.
 template <int K>
 __device__ __forceinline__ uint32_t tab_contains_batch(const uint64_t* tab, uint32_t tag,
-                                                       uint32_t lg, const uint32_t (&v)[K],
+                                                       uint32_t lg, const uint32_t (&vs)[K],
                                                        uint32_t maybe) {
   if (!maybe) return 0u;
   const uint32_t mask = (1u << lg) - 1;
@@ -216,17 +241,20 @@ __device__ __forceinline__ uint32_t tab_contains_batch(const uint64_t* tab, uint
   uint64_t e[K];
 #pragma unroll
   for (int q = 0; q < K; ++q) {
-    h[q] = vhash(v[q]) >> (32 - lg);
+    h[q] = vhash(vs[q]) >> (32 - lg);
     e[q] = ((maybe >> q) & 1u) ? tab[h[q]] : 0ull;
   }
   uint32_t found = 0;
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     if (!((maybe >> q) & 1u)) continue;
+    const uint32_t v = vs[q];
     uint64_t x = e[q];
     uint32_t hh = h[q];
+    uint32_t guard = 0;
     while (static_cast<uint32_t>(x >> 32) == tag) {
-      if (static_cast<uint32_t>(x) == v[q]) {
+      RRG_GUARD(guard, lg, 4)
+      if (static_cast<uint32_t>(x) == v) {
         found |= 1u << q;
         break;
       }
@@ -240,7 +268,11 @@ __device__ __forceinline__ uint32_t tab_contains_batch(const uint64_t* tab, uint
 __device__ __forceinline__ void tab_insert(uint64_t* tab, uint32_t tag, uint32_t lg, uint32_t v) {
   const uint32_t mask = (1u << lg) - 1;
   uint32_t h = vhash(v) >> (32 - lg);
-  while (static_cast<uint32_t>(tab[h] >> 32) == tag) h = (h + 1) & mask;
+  uint32_t guard = 0;
+  while (static_cast<uint32_t>(tab[h] >> 32) == tag) {
+    h = (h + 1) & mask;
+    RRG_GUARD(guard, lg, 2)
+  }
   tab[h] = (static_cast<uint64_t>(tag) << 32) | v;
 }
 
@@ -267,7 +299,9 @@ __device__ __forceinline__ void tab_insert_atomic(uint64_t* tab, uint32_t tag, u
   const uint32_t mask = (1u << lg) - 1;
   uint32_t h = vhash(v) >> (32 - lg);
   const unsigned long long want = (static_cast<unsigned long long>(tag) << 32) | v;
+  uint32_t guard = 0;
   while (true) {
+    RRG_GUARD(guard, lg, 3)
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(tab + h);
     if (static_cast<uint32_t>(e >> 32) == tag) {
       h = (h + 1) & mask;

@@ -268,6 +268,12 @@ int sampler_blocks_per_sm(int model, uint32_t ic_inner, int lt_mode = 1);
 enum Schedule : int { kSchedLane = 0, kSchedWarp = 1, kSchedCta = 2 };
 void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, int schedule,
                     cudaStream_t s);
+// per-model halves of the two above (sample_ic.cu, sample_lt.cu)
+int ic_blocks_per_sm();
+void launch_ic_sampler(const SampleParams& p, int grid, uint32_t ic_inner, int schedule,
+                       cudaStream_t s);
+int lt_blocks_per_sm(int lt_mode);
+void launch_lt_sampler(const SampleParams& p, int grid, cudaStream_t s);
 void launch_big(int model, const SampleParams& p, const uint32_t* list, uint32_t nlist,
                 uint32_t* bitmaps, uint32_t* lists, uint32_t workers, cudaStream_t s);
 std::vector<uint64_t> segment_matrices(uint64_t seg, int count);  // jump.cpp

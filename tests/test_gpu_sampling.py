@@ -452,3 +452,34 @@ def test_empty_graph_is_rejected(cuda):
     st = P.RRRStore(g)
     with pytest.raises(ValueError):
         P.generate_batch(g, IC, 1, 5, st)
+
+
+@pytest.mark.timeout(300)
+def test_lane_tags_after_failed_cooperative_expansion(cuda, oracle):
+    """Regression: a lane whose cooperative hub expansion grows its table and
+    then overflows the lane budget (the set is deferred) must start its next
+    sample under a tag past the abandoned one. Every sample here does exactly
+    that (root -> hub with a 3,000-edge duplicate-free in-list, ~1,350 accepted),
+    several times per lane; before the fix, later samples on a lane found the
+    abandoned entries live (endless probe chains: cfg3 1M lane batches hung in
+    about half the runs)."""
+    n, hubs, deg = 40000, 10, 3000
+    rng = np.random.default_rng(17)
+    src, dst, w = [], [], []
+    for h in range(hubs):
+        s_ = rng.choice(np.arange(hubs, n), deg, replace=False)
+        src.append(s_)
+        dst.append(np.full(deg, h))
+        w.append(np.full(deg, 0.45))
+    v = np.arange(hubs, n)
+    src.append(v % hubs)
+    dst.append(v)
+    w.append(np.ones(v.size))
+    arrays = P.build_graph(n, np.concatenate(src).astype(np.uint32),
+                           np.concatenate(dst).astype(np.uint32),
+                           np.concatenate(w).astype(np.float32))
+    count = 200000
+    g, st, off, mem = gpu_sample(arrays, IC, 3, count, ic_mode=1)
+    assert g.last_batch_stats().deferred > count // 2
+    ref = oracle.graph(*arrays).sample(IC, 3, 0, 4000, workers=8)
+    assert_sets_equal(off[:4001], mem[:int(off[4000])], ref)
