@@ -483,3 +483,22 @@ def test_lane_tags_after_failed_cooperative_expansion(cuda, oracle):
     assert g.last_batch_stats().deferred > count // 2
     ref = oracle.graph(*arrays).sample(IC, 3, 0, 4000, workers=8)
     assert_sets_equal(off[:4001], mem[:int(off[4000])], ref)
+
+
+def test_lt_nonmonotone_cdf_falls_back_to_the_linear_scan(cuda, oracle):
+    """A negative in-weight makes some in-list's CDF non-monotone: the
+    guide table and search trees would be wrong there, so the graph samples LT
+    with the reference's linear scan -- same sets as the reference."""
+    rng = np.random.default_rng(23)
+    n, m = 2000, 30000
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    keep = src != dst
+    pairs = np.unique(np.stack([src[keep], dst[keep]]), axis=1)
+    w = rng.uniform(0.0, 0.1, pairs.shape[1]).astype(np.float32)
+    w[::97] = -0.05  # (NaN would do the same; the checker cannot round-trip NaN weights)
+    arrays = P.build_graph(n, pairs[0], pairs[1], w)
+    for scan in (2, 1, 0):
+        _, st, off, mem = gpu_sample(arrays, LT, 9, 3000, lt_scan=scan)
+        ref = oracle.graph(*arrays).sample(LT, 9, 0, 3000, workers=4)
+        assert_sets_equal(off, mem, ref, msg=f"lt_scan {scan}")
