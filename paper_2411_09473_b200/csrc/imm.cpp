@@ -184,7 +184,20 @@ class Driver {
     const rrg_status s = rrg_select_seeds(store_, cfg_->k, cfg_->adaptive_threshold,
                                           fused_ ? 1 : 0, sd, mg, nullptr, nullptr, covered);
     t_select += seconds_since(t);
+    if (s == RRG_OK && sd == trial_seeds_.data()) trial_size_ = size_;
     return s;
+  }
+
+  // The final selection (imm.hpp:238) runs on max(theta, theta') sets; when the
+  // final top-up added none, that is the collection the last sampling round
+  // selected on, and select_seeds is a deterministic function of the collection
+  // (it revives every set first, selection.hpp:215): its seeds and marginals are
+  // the last round's. Returns false when a selection is needed.
+  bool reuse_last_selection(uint32_t* sd, uint64_t* mg) const {
+    if (trial_size_ != size_ || size_ == 0) return false;
+    std::copy(trial_seeds_.begin(), trial_seeds_.end(), sd);
+    std::copy(trial_marg_.begin(), trial_marg_.end(), mg);
+    return true;
   }
 
   // sampling_phase (imm.hpp:169-209)
@@ -224,6 +237,7 @@ class Driver {
   uint64_t size_ = 0;
   std::vector<uint32_t> trial_seeds_;
   std::vector<uint64_t> trial_marg_;
+  uint64_t trial_size_ = 0;  // store size the trial seeds were selected on
 };
 
 }  // namespace
@@ -288,8 +302,10 @@ rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
   // final top-up and selection (imm.hpp:227-241)
   st = d.top_up(out->theta, 0);
   if (st != RRG_OK) return st;
-  st = d.select(seeds, marginals, nullptr);
-  if (st != RRG_OK) return st;
+  if (!d.reuse_last_selection(seeds, marginals)) {
+    st = d.select(seeds, marginals, nullptr);
+    if (st != RRG_OK) return st;
+  }
 
   // set statistics (imm.hpp:243-248)
   uint64_t sets = 0, members = 0;
