@@ -82,9 +82,110 @@ __device__ void normalize_list(float* w, uint32_t b, uint32_t e, uint32_t v, uin
     w[j] = __double2float_rn(__dmul_rn(static_cast<double>(w[j]), scale));
 }
 
+// Lists of at least kNormWarpMin in-edges (hubs: cfg4's largest has 543K) go to
+// a warp each, so the sequential fp64 chain is not also a chain of dependent
+// global loads: the lanes load and convert a chunk of kNormChunk addends into
+// shared memory (the next chunk's loads in flight meanwhile) and lane 0 adds
+// them in list order -- the same additions, in the same order, as above.
+constexpr uint32_t kNormWarpMin = 256;
+constexpr uint32_t kNormChunk = 256;
+constexpr int kNormWarps = 8;
+
 __global__ void k_normalize_lt(const uint32_t* off, uint32_t n, float* w, uint32_t* bad) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    normalize_list(w, off[v], off[v + 1], v, bad);
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t b = off[v], e = off[v + 1];
+    if (e - b < kNormWarpMin) normalize_list(w, b, e, v, bad);
+  }
+}
+
+// Sum over w[b, e) in list order of x (scale == 0) or of float(x * scale),
+// both widened to fp64; returns the sum in every lane. *neg is set when an
+// addend is negative (first pass only, like the reference's check).
+__device__ double warp_list_sum(const float* w, uint32_t b, uint32_t e, double scale,
+                                double* sm, bool* neg) {
+  const uint32_t lane = threadIdx.x & 31;
+  float r[kNormChunk / 32];
+  auto load = [&](uint32_t c) {
+#pragma unroll
+    for (uint32_t k = 0; k < kNormChunk / 32; ++k) {
+      const uint32_t i = c + k * 32 + lane;
+      r[k] = i < e ? w[i] : 0.0f;
+    }
+  };
+  double sum = 0.0;
+  bool anyneg = false;
+  load(b);
+  for (uint32_t c = b; c < e; c += kNormChunk) {
+    bool mine = false;
+#pragma unroll
+    for (uint32_t k = 0; k < kNormChunk / 32; ++k) {
+      mine |= r[k] < 0.0f;
+      sm[k * 32 + lane] = scale == 0.0
+          ? static_cast<double>(r[k])
+          : static_cast<double>(__double2float_rn(__dmul_rn(static_cast<double>(r[k]), scale)));
+    }
+    if (__any_sync(0xffffffffu, mine)) {
+      anyneg = true;
+      break;
+    }
+    __syncwarp();
+    if (c + kNormChunk < e) load(c + kNormChunk);
+    if (lane == 0) {
+      const uint32_t cnt = e - c < kNormChunk ? e - c : kNormChunk;
+#pragma unroll 8
+      for (uint32_t i = 0; i < cnt; ++i) sum = __dadd_rn(sum, sm[i]);
+    }
+    __syncwarp();
+  }
+  *neg = anyneg;
+  return __shfl_sync(0xffffffffu, sum, 0);
+}
+
+__global__ void __launch_bounds__(kNormWarps * 32)
+    k_normalize_lt_hubs(const uint32_t* off, uint32_t n, float* w, uint32_t* bad) {
+  __shared__ double smem[kNormWarps][kNormChunk];
+  double* sm = smem[threadIdx.x >> 5];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t base = warp * 32; base < n; base += nwarps * 32) {
+    const uint32_t mv = base + lane;
+    const bool hub = mv < n && off[mv + 1] - off[mv] >= kNormWarpMin;
+    uint32_t hubs = __ballot_sync(0xffffffffu, hub);
+    while (hubs) {
+      const uint32_t v = base + __ffs(hubs) - 1;
+      hubs &= hubs - 1;
+      const uint32_t b = off[v], e = off[v + 1];
+      bool neg = false;
+      const double sum = warp_list_sum(w, b, e, 0.0, sm, &neg);
+      if (neg) {
+        if (lane == 0) atomicMin(bad, v);
+        continue;
+      }
+      if (sum <= 1.0) continue;
+      double scale = __ddiv_rn(1.0, sum);
+      for (int attempt = 0; attempt < 64; ++attempt) {
+        // scale > 0 here (sum is finite > 1, or +inf/NaN giving 0/NaN: then
+        // the scaled pass below uses the sequential form instead).
+        double scaled;
+        if (scale > 0.0) {
+          scaled = warp_list_sum(w, b, e, scale, sm, &neg);
+        } else {
+          scaled = 0.0;
+          if (lane == 0)
+            for (uint32_t j = b; j < e; ++j)
+              scaled = __dadd_rn(scaled, static_cast<double>(__double2float_rn(
+                                             __dmul_rn(static_cast<double>(w[j]), scale))));
+          scaled = __shfl_sync(0xffffffffu, scaled, 0);
+        }
+        if (scaled <= 1.0) break;
+        scale = __dmul_rn(scale, 1.0 - 0x1.0p-20);
+      }
+      for (uint32_t j = b + lane; j < e; j += 32)
+        w[j] = __double2float_rn(__dmul_rn(static_cast<double>(w[j]), scale));
+      __syncwarp();
+    }
+  }
 }
 
 }  // namespace
@@ -141,6 +242,10 @@ uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint3
   if (hb[0]) return 1;
   if (normalize && n) {
     k_normalize_lt<<<(n + 127) / 128, 128, 0, st>>>(g->off.ptr, n, g->w.ptr, bad.ptr + 1);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+    k_normalize_lt_hubs<<<g->num_sms * 4, kNormWarps * 32, 0, st>>>(g->off.ptr, n, g->w.ptr,
+                                                                    bad.ptr + 1);
     RRG_CUDA(cudaGetLastError());
     count_launch();
     RRG_CUDA(cudaMemcpyAsync(hb, bad.ptr, 8, cudaMemcpyDeviceToHost, st));

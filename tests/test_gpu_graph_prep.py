@@ -57,6 +57,27 @@ def test_device_normalize_matches_normalize_lt_weights(cuda, oracle, whi):
     assert same_bits(g.reverse_weights, rw_n)
 
 
+@pytest.mark.parametrize("whi", [0.01, 1.0, 3.0])
+def test_device_normalize_hub_lists(cuda, oracle, whi):
+    """Average in-degree ~260: many lists on either side of the warp-per-list
+    threshold (256 in-edges, k_normalize_lt_hubs), chunk tails of every length."""
+    n = 2000
+    src, dst, w = edge_list(int(whi * 1000) + 7, n, 500000, hub=5000, whi=whi)
+    roff, rsrc, rw = oracle.build_graph(n, src, dst, w)
+    deg = np.diff(roff.astype(np.int64))
+    assert (deg >= 256).sum() > 100 and (deg < 256).sum() > 10
+    rw_n = oracle.normalize_lt(roff, rw.copy())
+    g = P.Graph.from_edge_arrays(n, src, dst, w, normalize_lt=True)
+    assert same_bits(g.reverse_weights, rw_n)
+
+
+def test_device_normalize_negative_on_hub(cuda):
+    src, dst, w = edge_list(5, 100, 50000, hub=3000)
+    w[np.flatnonzero(dst == 33)[-1]] = -0.25  # inside the hub list of vertex 33
+    with pytest.raises(ValueError, match="vertex 33"):
+        P.Graph.from_edge_arrays(100, src, dst, w, normalize_lt=True)
+
+
 def test_device_graph_errors(cuda):
     with pytest.raises(ValueError):
         P.Graph.from_edge_arrays(4, [0, 5], [1, 2], [0.5, 0.5])
