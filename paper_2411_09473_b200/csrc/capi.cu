@@ -280,12 +280,34 @@ rrg_status rrg_graph_create_from_edges(uint32_t n, uint64_t m, const uint32_t* s
     d_src.reserve_discard(m ? m : 1);
     d_dst.reserve_discard(m ? m : 1);
     d_w.reserve_discard(m ? m : 1);
+    // The weights are only read after the sort: their copy (queued behind the
+    // ids on the link) overlaps the key build and the radix sort.
+    cudaStream_t side = nullptr;
+    cudaEvent_t ids_in = nullptr, w_in = nullptr;
+    struct Release {
+      cudaStream_t& s;
+      cudaEvent_t& a;
+      cudaEvent_t& b;
+      ~Release() {
+        if (s) cudaStreamSynchronize(s);
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+        if (s) cudaStreamDestroy(s);
+      }
+    } release{side, ids_in, w_in};
     if (m) {
+      RRG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      RRG_CUDA(cudaEventCreateWithFlags(&ids_in, cudaEventDisableTiming));
+      RRG_CUDA(cudaEventCreateWithFlags(&w_in, cudaEventDisableTiming));
       RRG_CUDA(cudaMemcpyAsync(d_src.ptr, src, m * 4, cudaMemcpyHostToDevice, g->stream));
       RRG_CUDA(cudaMemcpyAsync(d_dst.ptr, dst, m * 4, cudaMemcpyHostToDevice, g->stream));
-      RRG_CUDA(cudaMemcpyAsync(d_w.ptr, w, m * 4, cudaMemcpyHostToDevice, g->stream));
+      RRG_CUDA(cudaEventRecord(ids_in, g->stream));
+      RRG_CUDA(cudaStreamWaitEvent(side, ids_in, 0));
+      RRG_CUDA(cudaMemcpyAsync(d_w.ptr, w, m * 4, cudaMemcpyHostToDevice, side));
+      RRG_CUDA(cudaEventRecord(w_in, side));
     }
-    const uint64_t r = build_transpose_device(g, d_src.ptr, d_dst.ptr, d_w.ptr, normalize_lt != 0);
+    const uint64_t r = build_transpose_device(g, d_src.ptr, d_dst.ptr, d_w.ptr, normalize_lt != 0,
+                                              w_in);
     if (r == 1) return invalid("rrg_graph_create_from_edges: vertex id out of range");
     if (r >= 2)
       return invalid(("normalize_lt_weights: negative edge weight on vertex " +

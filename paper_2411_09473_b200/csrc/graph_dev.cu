@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kNormWarps * 32)
 // Returns 0, or 1 for an out-of-range vertex id, or 2 + v for a negative weight
 // on vertex v (normalize only).
 uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint32_t* d_dst,
-                                const float* d_w, bool normalize) {
+                                const float* d_w, bool normalize, cudaEvent_t w_ready) {
   const uint32_t n = g->n;
   const uint64_t m = g->m;
   const cudaStream_t st = g->stream;
@@ -206,6 +206,7 @@ uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint3
   const uint32_t init[2] = {0u, 0xffffffffu};
   RRG_CUDA(cudaMemcpyAsync(bad.ptr, init, 8, cudaMemcpyHostToDevice, st));
   if (m == 0) {
+    if (w_ready) RRG_CUDA(cudaStreamWaitEvent(st, w_ready, 0));
     RRG_CUDA(cudaMemsetAsync(g->off.ptr, 0, (static_cast<size_t>(n) + 1) * 4, st));
   } else {
     DevBuf<unsigned long long> keys, keys2;
@@ -230,6 +231,7 @@ uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint3
                                              idx2.ptr, static_cast<int64_t>(m), 0, 32 + vbits,
                                              st));
     count_launch();
+    if (w_ready) RRG_CUDA(cudaStreamWaitEvent(st, w_ready, 0));
     k_scatter_transpose<<<grid, 256, 0, st>>>(keys2.ptr, idx2.ptr, d_w, m, n, g->off.ptr,
                                               g->src.ptr, g->w.ptr);
     RRG_CUDA(cudaGetLastError());

@@ -244,9 +244,10 @@ struct SampleParams {
 };
 
 // graph_dev.cu: device transpose (+ normalize_lt_weights) of an edge list on the
-// device into g->off/src/w; 0 ok, 1 vertex out of range, 2 + v negative weight at v
+// device into g->off/src/w; 0 ok, 1 vertex out of range, 2 + v negative weight at v.
+// d_w may still be in flight: w_ready (if set) is waited on before it is read.
 uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint32_t* d_dst,
-                                const float* d_w, bool normalize);
+                                const float* d_w, bool normalize, cudaEvent_t w_ready = nullptr);
 void prepare_ic(rrg_graph* g);
 void prepare_ic_fast(rrg_graph* g);
 // IC fast (statistical) sampler: warp region tables, or n-bit maps (bitmap)
