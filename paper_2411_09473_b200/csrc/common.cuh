@@ -402,6 +402,7 @@ struct SampleCtl {
   unsigned long long restage_members;  // members of sets refused for lack of staging
   unsigned long long windows;     // IC warp schedule: windows processed (diagnostics)
   unsigned long long cuts;        // IC warp schedule: windows cut at a repeated source
+  unsigned long long repairs;     // IC block schedule: conflicts repaired inside a window
   unsigned int ndeferred;         // slots handed to the big-set path (set > kMemCap)
   unsigned int nrestage;          // slots to re-run once staging has grown
 };

@@ -198,6 +198,41 @@ __device__ __forceinline__ uint32_t amap_first(const unsigned long long* map, ui
   }
   return 0xffffffffu;
 }
+// Epoch-tagged variant for the block schedule's in-window repairs: slot =
+// (source << 32 | epoch << 12 | position), positions < 4096; entries of another
+// epoch read as empty, so moving to the next epoch clears the map.
+template <int kLog>
+__device__ __forceinline__ bool amap_insert_ep(unsigned long long* map, uint32_t v, uint32_t e,
+                                               uint32_t ep) {
+  constexpr uint32_t kSlots = 1u << kLog;
+  const unsigned long long want = (static_cast<unsigned long long>(v) << 32) | (ep << 12) | e;
+  uint32_t h = vhash(v) >> (32 - kLog);
+  for (uint32_t probe = 0; probe < kSlots; ++probe, h = (h + 1) & (kSlots - 1)) {
+    unsigned long long cur = map[h];
+    while (((cur >> 12) & 0xfffffu) != ep) {  // empty or stale: claim it
+      const unsigned long long got = atomicCAS(map + h, cur, want);
+      if (got == cur) return true;
+      cur = got;
+    }
+    if ((cur >> 32) == v) {
+      atomicMin(map + h, want);
+      return true;
+    }
+  }
+  return false;
+}
+template <int kLog>
+__device__ __forceinline__ uint32_t amap_first_ep(const unsigned long long* map, uint32_t v,
+                                                  uint32_t ep) {
+  constexpr uint32_t kSlots = 1u << kLog;
+  uint32_t h = vhash(v) >> (32 - kLog);
+  for (uint32_t probe = 0; probe < kSlots; ++probe, h = (h + 1) & (kSlots - 1)) {
+    const unsigned long long cur = map[h];
+    if (((cur >> 12) & 0xfffffu) != ep) return 0xffffffffu;
+    if ((cur >> 32) == v) return static_cast<uint32_t>(cur) & 0xfffu;
+  }
+  return 0xffffffffu;
+}
 struct WinSmem {
   union {
     WinFields win;   // multi-list windows
@@ -565,12 +600,16 @@ struct CtaSmem {
   uint32_t wsum[kCtaWarps];
   uint32_t wU[kCtaWarps];
   uint32_t wA[kCtaWarps];
+  uint32_t xhi[kCtaWin];  // general windows: high word of the draw at each stream rank
   uint32_t cut;
+  uint32_t fcut;  // first edge the window cannot settle (full map, or a repaired tie)
   uint32_t adv_qi;
   uint32_t adv_qj;
   uint32_t any_acc;
 };
 constexpr size_t kCtaKernelDynSmem = sizeof(CtaSmem);
+static_assert(kCtaKernelDynSmem <= 112 * 1024, "two blocks per SM");
+constexpr uint32_t kMaxRepairs = 64;  // repairs per window before falling back to a cut
 __device__ __forceinline__ uint32_t cfilt_bit(uint32_t v) { return (v * 0x2545F491u) >> 14; }
 __device__ __forceinline__ bool cfilt_maybe(const uint32_t* sf, uint32_t v) {
   const uint32_t b = cfilt_bit(v);
@@ -1087,6 +1126,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       __syncthreads();
       if (tid == 0) {  // after the barrier: every thread has read the previous window's
         cs.cut = 0xffffffffu;
+        cs.fcut = 0xffffffffu;
         cs.adv_qi = 0xffffffffu;
         cs.any_acc = 0;
       }
@@ -1203,6 +1243,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               if (kh < th ||
                   (kh == th && bern_tie(x, p.w, win_edge(cs.lstart, cs.lpre, kBlock, wbase + 32 * c + bit))))
                 acc |= 1u << bit;
+              cs.xhi[Pw + r0 + done] = kh;
               ++done;
             }
             if (acc) atomicOr(&ws.acc[c], acc);
@@ -1223,24 +1264,24 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
           const int c = __ffs(t) - 1;
           const uint32_t am = __shfl_sync(kFull, am_lane, c);
           const uint32_t el = 32 * c + lane;
-          if (((am >> lane) & 1u) && !amap_insert<kCtaAmapLog>(cs.amap, ws.src[el], wbase + el))
+          if (((am >> lane) & 1u) && !amap_insert_ep<kCtaAmapLog>(cs.amap, ws.src[el], wbase + el, 0))
             fail = min(fail, wbase + el);
         }
         fail = __reduce_min_sync(kFull, fail);
         if (lane == 0) {
-          if (fail != 0xffffffffu) atomicMin(&cs.cut, fail);
+          if (fail != 0xffffffffu) atomicMin(&cs.fcut, fail);
           if (acm) cs.any_acc = 1;
         }
         __syncthreads();
         if (cs.any_acc) {
           // ---- 3b. the first drawn edge whose source an earlier edge accepted
-          const uint32_t lim = cs.cut;
+          const uint32_t lim = cs.fcut;
           for (uint32_t c = 0; c < nch && wbase + 32 * c < lim; ++c) {
             const uint32_t m = ws.mask[c];
             if (!m) continue;
             const uint32_t el = 32 * c + lane;
-            const bool conf = ((m >> lane) & 1u) &&
-                              amap_first<kCtaAmapLog>(cs.amap, ws.src[el]) < wbase + el;
+            const bool conf = ((m >> lane) & 1u) && wbase + el < lim &&
+                              amap_first_ep<kCtaAmapLog>(cs.amap, ws.src[el], 0) < wbase + el;
             const unsigned b = __ballot_sync(kFull, conf);
             if (b) {
               if (lane == 0) atomicMin(&cs.cut, wbase + 32 * c + __ffs(b) - 1);
@@ -1248,7 +1289,118 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             }
           }
           __syncthreads();
-          const uint32_t cpos = cs.cut;
+          uint32_t rpos = cs.cut, fpos = cs.fcut;
+          // ---- 3c. repair: the conflicting edge at rpos does not draw after all.
+          // Everything before it is settled; after it, edges whose source a
+          // settled edge accepted never draw, the others take the stored draws
+          // at their new (lower) stream ranks, and the next conflict -- now only
+          // possible against a re-decided acceptance -- is repaired in turn. Each
+          // round uses the map under a new epoch (no clearing).
+          uint32_t ep = 0;
+          for (; rpos < fpos && rpos < ecur && ep < kMaxRepairs;) {
+            ++ep;
+            if (lane < static_cast<int>(nch)) {
+              const uint32_t e0 = wbase + 32 * lane;
+              const uint32_t keep = e0 + 32 <= rpos ? ~0u : e0 >= rpos ? 0u : (1u << (rpos - e0)) - 1u;
+              ws.acc[lane] &= keep;
+              if (rpos >= e0 && rpos < e0 + 32) ws.mask[lane] &= ~(1u << (rpos - e0));
+            }
+            __syncwarp();
+            for (uint32_t c = 0; c < nch && wbase + 32 * c < rpos; ++c) {  // settled accepts
+              const uint32_t el = 32 * c + lane;
+              if ((ws.acc[c] >> lane) & 1u) amap_insert_ep<kCtaAmapLog>(cs.amap, ws.src[el], wbase + el, ep);
+            }
+            __syncthreads();
+            if (tid == 0) cs.cut = 0xffffffffu;
+            for (uint32_t c = 0; c < nch; ++c) {  // edges after rpos with a settled source
+              if (wbase + 32 * c + 31 <= rpos) continue;
+              const uint32_t m = ws.mask[c];
+              const uint32_t el = 32 * c + lane;
+              const bool drop = ((m >> lane) & 1u) && wbase + el > rpos &&
+                                amap_first_ep<kCtaAmapLog>(cs.amap, ws.src[el], ep) != 0xffffffffu;
+              const unsigned b = __ballot_sync(kFull, drop);
+              if (lane == 0 && b) ws.mask[c] = m & ~b;
+              __syncwarp();
+            }
+            const uint32_t cnt2 = lane < static_cast<int>(nch) ? __popc(ws.mask[lane]) : 0u;
+            uint32_t ui2 = cnt2;
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(kFull, ui2, o);
+              if (lane >= o) ui2 += y;
+            }
+            if (lane < static_cast<int>(kWinChunks)) ws.pre[lane] = ui2 - cnt2;
+            if (lane == 31) cs.wU[wl] = ui2;
+            __syncthreads();
+            Pw = 0;
+            U = 0;
+            for (int w = 0; w < kCtaWarps; ++w) {
+              const uint32_t x = cs.wU[w];
+              if (w < wl) Pw += x;
+              U += x;
+            }
+            // acceptance after rpos from the stored draws, at the new ranks
+            uint32_t fl = 0xffffffffu;
+            if (lane < static_cast<int>(nch)) {
+              const uint32_t e0 = wbase + 32 * lane;
+              const uint32_t m = ws.mask[lane];
+              const uint32_t after = e0 > rpos ? ~0u : rpos - e0 >= 31 ? 0u : ~0u << (rpos - e0 + 1);
+              uint32_t acc = 0;
+              const uint32_t rb = Pw + ws.pre[lane];
+              for (uint32_t t = m & after; t; t &= t - 1) {
+                const int bit = __ffs(t) - 1;
+                const uint32_t kh = cs.xhi[rb + __popc(m & ((1u << bit) - 1u))];
+                const uint32_t th = ws.thr[32 * lane + bit];
+                if (kh < th) acc |= 1u << bit;
+                else if (kh == th) fl = min(fl, e0 + bit);  // needs the low bits: cut there
+              }
+              ws.acc[lane] |= acc;
+            }
+            __syncwarp();
+            for (uint32_t c = 0; c < nch; ++c) {  // re-decided accepts into the map
+              if (wbase + 32 * c + 31 <= rpos) continue;
+              const uint32_t a = ws.acc[c];
+              const uint32_t el = 32 * c + lane;
+              if (((a >> lane) & 1u) && wbase + el > rpos &&
+                  !amap_insert_ep<kCtaAmapLog>(cs.amap, ws.src[el], wbase + el, ep))
+                fl = min(fl, wbase + el);
+            }
+            fl = __reduce_min_sync(kFull, fl);
+            if (lane == 0 && fl != 0xffffffffu) atomicMin(&cs.fcut, fl);
+            __syncthreads();
+            const uint32_t lim2 = cs.fcut;
+            for (uint32_t c = 0; c < nch && wbase + 32 * c < lim2; ++c) {  // the next conflict
+              if (wbase + 32 * c + 31 <= rpos) continue;
+              const uint32_t m = ws.mask[c];
+              if (!m) continue;
+              const uint32_t el = 32 * c + lane;
+              const bool conf = ((m >> lane) & 1u) && wbase + el > rpos && wbase + el < lim2 &&
+                                amap_first_ep<kCtaAmapLog>(cs.amap, ws.src[el], ep) < wbase + el;
+              const unsigned b = __ballot_sync(kFull, conf);
+              if (b) {
+                if (lane == 0) atomicMin(&cs.cut, wbase + 32 * c + __ffs(b) - 1);
+                break;
+              }
+            }
+            __syncthreads();
+            rpos = cs.cut;
+            fpos = cs.fcut;
+          }
+          if (ep) {
+            am_lane = lane < static_cast<int>(nch) ? ws.acc[lane] : 0u;
+            if (tid == 0) atomicAdd(&p.ctl->repairs, static_cast<unsigned long long>(ep));
+          }
+          const uint32_t cpos = min(rpos, fpos);
+          if (cpos >= ecur && ep && wl == 0) {
+            // the stream resumes after the U draws the repaired window used
+            Xoshiro st = warp_advance(p, s, min(U, kCtaWin - 1));
+            if (U == kCtaWin) st.next();
+            if (lane == 0) {
+              cs.st[0] = st.a;
+              cs.st[1] = st.b;
+              cs.st[2] = st.c;
+              cs.st[3] = st.d;
+            }
+          }
           if (cpos < ecur) {
             cut = true;
             const uint32_t cw = cpos / kWin, cl = cpos % kWin, cc = cl >> 5, cb = cl & 31;

@@ -15,6 +15,12 @@ from oracle import Oracle, available  # noqa: E402
 names = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"]
 orc = Oracle("reference" if available("reference") else "port")
 cores = len(os.sched_getaffinity(0))
+# CUDA context + module load happen once per process: keep them out of the
+# first config's upload time.
+_w = P.Graph(*graphs.generate(graphs.scaled(graphs.CONFIGS["cfg1"], 1024, 8192)))
+_w.prepare(0)
+_w.prepare(1)
+del _w
 for name in names:
     cfg = graphs.CONFIGS[name]
     t = time.time()
@@ -32,9 +38,12 @@ for name in names:
         r = P.run_imm(g, icfg)
         walls.append(time.time() - t)
     og = orc.graph(*arrays)  # rrflow::Graph construction is not part of run_imm
-    t = time.time()
-    rr = og.imm(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model, workers=cores)
-    cpu_s = time.time() - t
+    cpu_walls = []
+    for _ in range(3):  # median of 3, like the GPU side
+        t = time.time()
+        rr = og.imm(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model, workers=cores)
+        cpu_walls.append(time.time() - t)
+    cpu_s = statistics.median(cpu_walls)
     print(json.dumps({
         "cfg": name, "k": cfg.k, "n": int(arrays[0].size - 1), "arcs": int(arrays[1].size),
         "gpu_imm_s": statistics.median(walls), "gpu_upload_k0_s": up_s,
