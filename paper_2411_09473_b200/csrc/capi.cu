@@ -134,10 +134,12 @@ void ensure_lane_scratch(rrg_graph* g, uint64_t lanes) {
   if (sc.lanes >= lanes) return;
   sc.lists.release();
   sc.tabs.release();
+  sc.xhi.release();
   sc.tags.release();
   sc.wtags.release();
   sc.lists.reserve_discard(lanes * kMemCap);
   sc.tabs.reserve_discard(lanes * kTabCap);
+  sc.xhi.reserve_discard((lanes / 256 + 1) * 4096);  // blocks of 256 lanes x kCtaWin
   sc.tags.reserve_discard(lanes);
   sc.wtags.reserve_discard(lanes / 32 + 1);
   RRG_CUDA(cudaMemsetAsync(sc.tabs.ptr, 0, lanes * kTabCap * sizeof(uint64_t), g->stream));
@@ -571,6 +573,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.count = c;
       p.lists = g->scratch.lists.ptr;
       p.tabs = g->scratch.tabs.ptr;
+      p.xhi = g->scratch.xhi.ptr;
       p.tags = g->scratch.tags.ptr;
       p.wtags = g->scratch.wtags.ptr;
       p.lanes = g->scratch.lanes;

@@ -311,6 +311,36 @@ __device__ __forceinline__ void tab_insert_atomic(uint64_t* tab, uint32_t tag, u
   }
 }
 
+// K concurrent inserts (bit q of `pend`: insert vs[q]) with their probes and
+// CASes in flight together: one round trip per probe step instead of K.
+template <int K>
+__device__ __forceinline__ void tab_insert_atomic_batch(uint64_t* tab, uint32_t tag, uint32_t lg,
+                                                        const uint32_t (&vs)[K], uint32_t pend) {
+  const uint32_t mask = (1u << lg) - 1;
+  uint32_t h[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) h[q] = vhash(vs[q]) >> (32 - lg);
+  while (pend) {
+    unsigned long long e[K], r[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      e[q] = ((pend >> q) & 1u) ? *reinterpret_cast<volatile unsigned long long*>(tab + h[q]) : 0ull;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      r[q] = ~e[q];
+      if (((pend >> q) & 1u) && static_cast<uint32_t>(e[q] >> 32) != tag)
+        r[q] = atomicCAS(reinterpret_cast<unsigned long long*>(tab + h[q]), e[q],
+                         (static_cast<unsigned long long>(tag) << 32) | vs[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      if (!((pend >> q) & 1u)) continue;
+      if (static_cast<uint32_t>(e[q] >> 32) == tag) h[q] = (h[q] + 1) & mask;  // taken: next slot
+      else if (r[q] == e[q]) pend &= ~(1u << q);                               // claimed
+    }
+  }
+}
+
 // s <- M s over GF(2)^256 (state words a,b,c,d = bits 0..255), M column-major:
 // column i = 4 words at M + 4 i (csrc/jump.cpp).
 __device__ __forceinline__ void gf2_matvec(const uint64_t* __restrict__ M, uint64_t& a,

@@ -91,6 +91,7 @@ struct LaneScratch {
   uint64_t lanes = 0;
   DevBuf<uint32_t> lists;
   DevBuf<uint64_t> tabs;
+  DevBuf<uint32_t> xhi;  // block IC schedule: a window's draw high words, per block (kCtaWin each)
   DevBuf<uint32_t> tags;
   DevBuf<uint32_t> wtags;
 };
@@ -214,6 +215,7 @@ struct SampleParams {
   uint64_t count;
   uint32_t* lists;
   uint64_t* tabs;
+  uint32_t* xhi;  // per block: 4096 draw high words of the current window
   uint32_t* tags;
   uint32_t* wtags;       // warp-region tag counters (IC warp mode)
   uint64_t lanes;        // lane scratch regions allocated

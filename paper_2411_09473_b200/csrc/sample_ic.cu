@@ -600,7 +600,6 @@ struct CtaSmem {
   uint32_t wsum[kCtaWarps];
   uint32_t wU[kCtaWarps];
   uint32_t wA[kCtaWarps];
-  uint32_t xhi[kCtaWin];  // general windows: high word of the draw at each stream rank
   uint32_t cut;
   uint32_t fcut;  // first edge the window cannot settle (full map, or a repaired tie)
   uint32_t adv_qi;
@@ -608,8 +607,14 @@ struct CtaSmem {
   uint32_t any_acc;
 };
 constexpr size_t kCtaKernelDynSmem = sizeof(CtaSmem);
-static_assert(kCtaKernelDynSmem <= 112 * 1024, "two blocks per SM");
+static_assert(kCtaKernelDynSmem <= 97 * 1024, "two blocks per SM within the 196 KB carveout");
 constexpr uint32_t kMaxRepairs = 64;  // repairs per window before falling back to a cut
+#ifndef RRG_REPAIR_MIN
+#define RRG_REPAIR_MIN 1024
+#endif
+// A conflict is repaired only when at least this many window edges follow it;
+// closer to the window's end a cut (and a fresh window) is cheaper.
+constexpr uint32_t kRepairMin = RRG_REPAIR_MIN;
 __device__ __forceinline__ uint32_t cfilt_bit(uint32_t v) { return (v * 0x2545F491u) >> 14; }
 __device__ __forceinline__ bool cfilt_maybe(const uint32_t* sf, uint32_t v) {
   const uint32_t b = cfilt_bit(v);
@@ -688,6 +693,39 @@ __device__ __forceinline__ uint32_t block_exscan_global(uint32_t* x, uint32_t W,
   return total;
 }
 
+// Block-wide insert of mem[lo, hi) into the sample's table, four probe chains in
+// flight per thread (the appends used to wait one CAS round trip per 32-edge
+// chunk, the grows one per member).
+__device__ __forceinline__ void cta_tab_insert(uint64_t* tab, uint32_t tag, uint32_t lg,
+                                               const uint32_t* mem, uint32_t lo, uint32_t hi) {
+  for (uint32_t b = lo + threadIdx.x; b < hi; b += 4 * kBlock) {
+    uint32_t vs[4], pend = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t i = b + q * kBlock;
+      vs[q] = i < hi ? mem[i] : 0u;
+      pend |= (i < hi ? 1u : 0u) << q;
+    }
+    tab_insert_atomic_batch<4>(tab, tag, lg, vs, pend);
+  }
+}
+
+// RRG_CTA_PHASES (diagnostic builds): thread 0 of each block accumulates the
+// cycles between the schedule's barriers per phase and prints them at exit.
+#ifdef RRG_CTA_PHASES
+#define RRG_PH(k)                           \
+  do {                                      \
+    if (tid == 0) {                         \
+      const long long t_ = clock64();       \
+      ph_[k] += t_ - ph_t_;                 \
+      ph_t_ = t_;                           \
+    }                                       \
+  } while (0)
+#else
+#define RRG_PH(k) \
+  do {            \
+  } while (0)
+#endif
 __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(const SampleParams p) {
   constexpr uint32_t kCap = kBlock * kMemCap;
   extern __shared__ __align__(16) unsigned char k_dsm[];
@@ -700,6 +738,9 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
   if (region + kBlock > p.lanes) return;  // uniform per block
   uint32_t* mem = p.lists + region * kMemCap;
   uint64_t* tab = p.tabs + region * kTabCap;
+  // general windows: high word of the draw at each stream rank (global: kept
+  // out of shared memory so two blocks still leave L1 its share)
+  uint32_t* xhi = p.xhi + static_cast<size_t>(blockIdx.x) * kCtaWin;
   uint32_t* sf = cs.filt;
   for (uint32_t t = tid; t < kCtaFilterWords; t += kBlock) sf[t] = 0;
   // same 256-lane regions and tag range as the 256-lane warp layout
@@ -707,6 +748,9 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
   uint32_t tag = 0xC0000000u | (p.wtags[tslot] & 0x3fffffffu);
   uint64_t insp = 0;
   const uint32_t wbase = kWin * wl;  // this warp's first window position
+#ifdef RRG_CTA_PHASES
+  long long ph_[12] = {0}, ph_t_ = clock64();
+#endif
   for (;;) {
     __syncthreads();  // previous sample written out, filter cleared
     if (tid == 0) cs.next = atomicAdd(&p.ctl->next, 1ull);
@@ -724,6 +768,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       cfilt_add(sf, root);
     }
     __syncthreads();
+    RRG_PH(0);
     bool ok = true;
     uint32_t qi = 0, qj = p.off[root];
     while (qi < nmem && ok) {
@@ -920,7 +965,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               if (lg2 != lg) {  // grow: re-insert the members under a fresh tag
                 lg = lg2;
                 ++stag;
-                for (uint32_t t = tid; t < nmem; t += kBlock) tab_insert_atomic(tab, stag, lg, mem[t]);
+                cta_tab_insert(tab, stag, lg, mem, 0, nmem);
                 __syncthreads();
               }
               for (uint32_t t = t0; t < t1; ++t) {
@@ -936,18 +981,20 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
                     if ((am >> lane) & 1u) {
                       const uint32_t v = __ldg(p.src + qj + t * kLxWin + 32 * (32 * i + c) + lane);
                       mem[base + __popc(am & lanemask_lt())] = v;
-                      tab_insert_atomic(tab, stag, lg, v);
                       cfilt_add(sf, v);
                     }
                     base += __popc(am);
                   }
                 }
               }
+              __syncthreads();  // the appended members are visible block-wide
+              cta_tab_insert(tab, stag, lg, mem, nmem, nmem + A);
               nmem += A;
             }
           }
           if (tid == 0) atomicAdd(&p.ctl->windows, 1ull);
           __syncthreads();  // members appended; scratch and cs free
+          RRG_PH(1);
           ++qi;
           if (qi < nmem) qj = p.off[mem[qi]];
           continue;
@@ -1075,7 +1122,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               if (lg2 != lg) {  // grow: re-insert the members under a fresh tag
                 lg = lg2;
                 ++stag;
-                for (uint32_t t = tid; t < nmem; t += kBlock) tab_insert_atomic(tab, stag, lg, mem[t]);
+                cta_tab_insert(tab, stag, lg, mem, 0, nmem);
                 __syncthreads();
               }
               uint32_t base = nmem + Apre;
@@ -1087,16 +1134,18 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
                 if ((am >> lane) & 1u) {
                   const uint32_t v = ws.src[32 * c + lane];
                   mem[base + __popc(am & lanemask_lt())] = v;
-                  tab_insert_atomic(tab, stag, lg, v);
                   cfilt_add(sf, v);
                 }
                 base += __popc(am);
               }
+              __syncthreads();  // the appended members are visible block-wide
+              cta_tab_insert(tab, stag, lg, mem, nmem, nmem + A);
               nmem += A;
             }
           }
           if (tid == 0) atomicAdd(&p.ctl->windows, 1ull);
           __syncthreads();  // (3) members appended; cs fields free for the next window
+          RRG_PH(2);
           qj += E;
           if (qj == fe) {
             ++qi;
@@ -1139,6 +1188,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       cs.lstart[tid] = lb;
       cs.lpre[tid] = lvalid ? incl - len : 0xffffffffu;
       __syncthreads();
+      RRG_PH(3);
       uint32_t ecur = min(kCtaWin, total);
       // ---- 1. warp wl classifies positions [wbase, wbase + 512) (status at window start)
       uint32_t mymask = 0;
@@ -1204,6 +1254,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       }
       if (lane == 0) cs.wU[wl] = Uw;
       __syncthreads();
+      RRG_PH(4);
       uint32_t Pw = 0, U = 0;
       for (int w = 0; w < kCtaWarps; ++w) {
         const uint32_t x = cs.wU[w];
@@ -1243,7 +1294,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               if (kh < th ||
                   (kh == th && bern_tie(x, p.w, win_edge(cs.lstart, cs.lpre, kBlock, wbase + 32 * c + bit))))
                 acc |= 1u << bit;
-              cs.xhi[Pw + r0 + done] = kh;
+              xhi[Pw + r0 + done] = kh;
               ++done;
             }
             if (acc) atomicOr(&ws.acc[c], acc);
@@ -1273,6 +1324,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
           if (acm) cs.any_acc = 1;
         }
         __syncthreads();
+        RRG_PH(5);
         if (cs.any_acc) {
           // ---- 3b. the first drawn edge whose source an earlier edge accepted
           const uint32_t lim = cs.fcut;
@@ -1289,6 +1341,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             }
           }
           __syncthreads();
+          RRG_PH(6);
           uint32_t rpos = cs.cut, fpos = cs.fcut;
           // ---- 3c. repair: the conflicting edge at rpos does not draw after all.
           // Everything before it is settled; after it, edges whose source a
@@ -1297,7 +1350,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
           // possible against a re-decided acceptance -- is repaired in turn. Each
           // round uses the map under a new epoch (no clearing).
           uint32_t ep = 0;
-          for (; rpos < fpos && rpos < ecur && ep < kMaxRepairs;) {
+          for (; rpos < fpos && rpos + kRepairMin < ecur && ep < kMaxRepairs;) {
             ++ep;
             if (lane < static_cast<int>(nch)) {
               const uint32_t e0 = wbase + 32 * lane;
@@ -1338,22 +1391,33 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               if (w < wl) Pw += x;
               U += x;
             }
-            // acceptance after rpos from the stored draws, at the new ranks
+            // acceptance after rpos from the stored draws, at the new ranks (lane =
+            // position; four chunks' draw loads in flight)
             uint32_t fl = 0xffffffffu;
-            if (lane < static_cast<int>(nch)) {
-              const uint32_t e0 = wbase + 32 * lane;
-              const uint32_t m = ws.mask[lane];
-              const uint32_t after = e0 > rpos ? ~0u : rpos - e0 >= 31 ? 0u : ~0u << (rpos - e0 + 1);
-              uint32_t acc = 0;
-              const uint32_t rb = Pw + ws.pre[lane];
-              for (uint32_t t = m & after; t; t &= t - 1) {
-                const int bit = __ffs(t) - 1;
-                const uint32_t kh = cs.xhi[rb + __popc(m & ((1u << bit) - 1u))];
-                const uint32_t th = ws.thr[32 * lane + bit];
-                if (kh < th) acc |= 1u << bit;
-                else if (kh == th) fl = min(fl, e0 + bit);  // needs the low bits: cut there
+            for (uint32_t c0 = 0; c0 < nch; c0 += 4) {
+              uint32_t kh[4];
+#pragma unroll
+              for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t c = c0 + q;
+                kh[q] = 0xffffffffu;
+                if (c < nch && wbase + 32 * c + 31 > rpos) {
+                  const uint32_t m = ws.mask[c];
+                  if (((m >> lane) & 1u) && wbase + 32 * c + lane > rpos)
+                    kh[q] = xhi[Pw + ws.pre[c] + __popc(m & lanemask_lt())];
+                }
               }
-              ws.acc[lane] |= acc;
+#pragma unroll
+              for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t c = c0 + q;
+                if (c >= nch) break;
+                if (wbase + 32 * c + 31 <= rpos) continue;
+                const uint32_t e = wbase + 32 * c + lane;
+                const bool d = ((ws.mask[c] >> lane) & 1u) && e > rpos;
+                const uint32_t th = ws.thr[32 * c + lane];
+                if (d && kh[q] == th) fl = min(fl, e);  // needs the low bits: cut there
+                const unsigned b = __ballot_sync(kFull, d && kh[q] < th);
+                if (lane == 0 && b) ws.acc[c] |= b;
+              }
             }
             __syncwarp();
             for (uint32_t c = 0; c < nch; ++c) {  // re-decided accepts into the map
@@ -1385,6 +1449,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             rpos = cs.cut;
             fpos = cs.fcut;
           }
+          RRG_PH(7);
           if (ep) {
             am_lane = lane < static_cast<int>(nch) ? ws.acc[lane] : 0u;
             if (tid == 0) atomicAdd(&p.ctl->repairs, static_cast<unsigned long long>(ep));
@@ -1431,6 +1496,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
         for (int o = 16; o; o >>= 1) Aw += __shfl_xor_sync(kFull, Aw, o);
         if (lane == 0) cs.wA[wl] = Aw;
         __syncthreads();
+        RRG_PH(8);
         s = Xoshiro{cs.st[0], cs.st[1], cs.st[2], cs.st[3]};
         uint32_t Apre = 0, A = 0;
         for (int w = 0; w < kCtaWarps; ++w) {
@@ -1447,7 +1513,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             if (lg2 != lg) {  // grow: re-insert the members under a fresh tag
               lg = lg2;
               ++stag;
-              for (uint32_t t = tid; t < nmem; t += kBlock) tab_insert_atomic(tab, stag, lg, mem[t]);
+              cta_tab_insert(tab, stag, lg, mem, 0, nmem);
               __syncthreads();
             }
             uint32_t base = nmem + Apre;
@@ -1459,11 +1525,12 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               if ((am >> lane) & 1u) {
                 const uint32_t v = ws.src[32 * c + lane];
                 mem[base + __popc(am & lanemask_lt())] = v;
-                tab_insert_atomic(tab, stag, lg, v);
                 cfilt_add(sf, v);
               }
               base += __popc(am);
             }
+            __syncthreads();  // the appended members are visible block-wide
+            cta_tab_insert(tab, stag, lg, mem, nmem, nmem + A);
             nmem += A;
           }
         }
@@ -1472,12 +1539,14 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
         atomicAdd(&p.ctl->windows, 1ull);
         if (cut) atomicAdd(&p.ctl->cuts, 1ull);
       }
+      RRG_PH(9);
       // ---- advance past the ecur consumed edges: the first list not wholly consumed
       if (lvalid && incl > ecur && incl - len <= ecur) {
         cs.adv_qi = qi + tid;
         cs.adv_qj = lb + (ecur - (incl - len));
       }
       __syncthreads();
+      RRG_PH(10);
       if (cs.adv_qi != 0xffffffffu) {
         qi = cs.adv_qi;
         qj = cs.adv_qj;
@@ -1487,6 +1556,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       }
     }
     __syncthreads();
+    RRG_PH(11);
     // inspected in-edges of the set = sum of its members' in-degrees
     uint64_t sinsp = 0;
     if (ok)
@@ -1520,6 +1590,18 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
     atomicAdd(&p.ctl->inspected, (unsigned long long)insp);
     atomicAdd(&p.ctl->entries, (unsigned long long)insp);
   }
+#ifdef RRG_CTA_PHASES
+  if (tid == 0) {
+    long long tot = 0;
+    for (int k = 0; k < 12; ++k) tot += ph_[k];
+    if (tot > 2000000)
+      printf("[cta %d] Mcyc total %.2f: between %.2f list %.2f fast %.2f layout %.2f classify %.2f "
+             "draw+3a %.2f 3b %.2f repair %.2f cut %.2f append %.2f advance %.2f tail %.2f\n",
+             blockIdx.x, tot * 1e-6, ph_[0] * 1e-6, ph_[1] * 1e-6, ph_[2] * 1e-6, ph_[3] * 1e-6,
+             ph_[4] * 1e-6, ph_[5] * 1e-6, ph_[6] * 1e-6, ph_[7] * 1e-6, ph_[8] * 1e-6,
+             ph_[9] * 1e-6, ph_[10] * 1e-6, ph_[11] * 1e-6);
+  }
+#endif
   if (tid == 0) p.wtags[tslot] = tag;
 }
 
