@@ -569,7 +569,11 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
 constexpr int kCtaWarps = kBlock / 32;
 constexpr uint32_t kCtaWin = kCtaWarps * kWin;  // 4096 in-edges
 constexpr int kCtaAmapLog = 11;                 // 2048 slots; a full map cuts the window
-constexpr uint32_t kCtaFilterWords = 8192;      // 256K bits
+#ifndef RRG_CTA_FILT_LOG
+#define RRG_CTA_FILT_LOG 18
+#endif
+constexpr int kCtaFiltLog = RRG_CTA_FILT_LOG;  // visited filter: 2^18 bits = 32 KB
+constexpr uint32_t kCtaFilterWords = 1u << (kCtaFiltLog - 5);
 constexpr uint32_t kCtaFastMin = 1024;          // single-list fast windows from this length
 constexpr uint32_t kJumpTableWords = 32 * 256 * 4;
 constexpr int kLxCpl = RRG_LX_CPL;            // list expansion: 32-edge chunks per lane
@@ -615,7 +619,7 @@ constexpr uint32_t kMaxRepairs = 64;  // repairs per window before falling back 
 // A conflict is repaired only when at least this many window edges follow it;
 // closer to the window's end a cut (and a fresh window) is cheaper.
 constexpr uint32_t kRepairMin = RRG_REPAIR_MIN;
-__device__ __forceinline__ uint32_t cfilt_bit(uint32_t v) { return (v * 0x2545F491u) >> 14; }
+__device__ __forceinline__ uint32_t cfilt_bit(uint32_t v) { return (v * 0x2545F491u) >> (32 - kCtaFiltLog); }
 __device__ __forceinline__ bool cfilt_maybe(const uint32_t* sf, uint32_t v) {
   const uint32_t b = cfilt_bit(v);
   return (sf[b >> 5] >> (b & 31)) & 1u;
