@@ -233,6 +233,36 @@ __device__ __forceinline__ uint32_t amap_first_ep(const unsigned long long* map,
   }
   return 0xffffffffu;
 }
+// K lookups of amap_first_ep with their first probes in flight together.
+template <int kLog, int K>
+__device__ __forceinline__ void amap_first_ep_batch(const unsigned long long* map,
+                                                    const uint32_t (&vs)[K], uint32_t want,
+                                                    uint32_t ep, uint32_t (&out)[K]) {
+  constexpr uint32_t kSlots = 1u << kLog;
+  uint32_t h[K];
+  unsigned long long x[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    h[q] = vhash(vs[q]) >> (32 - kLog);
+    x[q] = ((want >> q) & 1u) ? map[h[q]] : 0ull;
+  }
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    out[q] = 0xffffffffu;
+    if (!((want >> q) & 1u)) continue;
+    unsigned long long cur = x[q];
+    uint32_t hh = h[q];
+    for (uint32_t probe = 0; probe < kSlots; ++probe) {
+      if (((cur >> 12) & 0xfffffu) != ep) break;
+      if ((cur >> 32) == vs[q]) {
+        out[q] = static_cast<uint32_t>(cur) & 0xfffu;
+        break;
+      }
+      hh = (hh + 1) & (kSlots - 1);
+      cur = map[hh];
+    }
+  }
+}
 struct WinSmem {
   union {
     WinFields win;   // multi-list windows
@@ -610,6 +640,37 @@ struct CtaSmem {
   uint32_t adv_qj;
   uint32_t any_acc;
 };
+// The first window position in [lo, lim) of warp slice `ws` whose edge draws
+// and whose source the map (epoch ep) holds at an earlier position, folded
+// into *cut with atomicMin; four chunks' lookups in flight at a time.
+__device__ __forceinline__ void warp_first_conflict(const unsigned long long* amap,
+                                                    const CtaWarpFields& ws, uint32_t wbase,
+                                                    uint32_t nch, uint32_t lo, uint32_t lim,
+                                                    uint32_t ep, uint32_t* cut) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t c0 = 0; c0 < nch && wbase + 32 * c0 < lim; c0 += 4) {
+    if (wbase + 32 * (c0 + 4) <= lo) continue;
+    uint32_t vs[4], f[4], want = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+      const uint32_t c = c0 + q, e = wbase + 32 * c + lane;
+      const bool w = c < nch && ((ws.mask[c] >> lane) & 1u) && e >= lo && e < lim;
+      vs[q] = w ? ws.src[32 * c + lane] : 0u;
+      want |= (w ? 1u : 0u) << q;
+    }
+    if (!__any_sync(kFull, want != 0)) continue;
+    amap_first_ep_batch<kCtaAmapLog, 4>(amap, vs, want, ep, f);
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+      const uint32_t e = wbase + 32 * (c0 + q) + lane;
+      const unsigned b = __ballot_sync(kFull, ((want >> q) & 1u) && f[q] < e);
+      if (b) {
+        if (lane == 0) atomicMin(cut, wbase + 32 * (c0 + q) + __ffs(b) - 1);
+        return;
+      }
+    }
+  }
+}
 constexpr size_t kCtaKernelDynSmem = sizeof(CtaSmem);
 static_assert(kCtaKernelDynSmem <= 97 * 1024, "two blocks per SM within the 196 KB carveout");
 constexpr uint32_t kMaxRepairs = 64;  // repairs per window before falling back to a cut
@@ -1332,18 +1393,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
         if (cs.any_acc) {
           // ---- 3b. the first drawn edge whose source an earlier edge accepted
           const uint32_t lim = cs.fcut;
-          for (uint32_t c = 0; c < nch && wbase + 32 * c < lim; ++c) {
-            const uint32_t m = ws.mask[c];
-            if (!m) continue;
-            const uint32_t el = 32 * c + lane;
-            const bool conf = ((m >> lane) & 1u) && wbase + el < lim &&
-                              amap_first_ep<kCtaAmapLog>(cs.amap, ws.src[el], 0) < wbase + el;
-            const unsigned b = __ballot_sync(kFull, conf);
-            if (b) {
-              if (lane == 0) atomicMin(&cs.cut, wbase + 32 * c + __ffs(b) - 1);
-              break;
-            }
-          }
+          warp_first_conflict(cs.amap, ws, wbase, nch, 0u, lim, 0u, &cs.cut);
           __syncthreads();
           RRG_PH(6);
           uint32_t rpos = cs.cut, fpos = cs.fcut;
@@ -1369,14 +1419,22 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             }
             __syncthreads();
             if (tid == 0) cs.cut = 0xffffffffu;
-            for (uint32_t c = 0; c < nch; ++c) {  // edges after rpos with a settled source
-              if (wbase + 32 * c + 31 <= rpos) continue;
-              const uint32_t m = ws.mask[c];
-              const uint32_t el = 32 * c + lane;
-              const bool drop = ((m >> lane) & 1u) && wbase + el > rpos &&
-                                amap_first_ep<kCtaAmapLog>(cs.amap, ws.src[el], ep) != 0xffffffffu;
-              const unsigned b = __ballot_sync(kFull, drop);
-              if (lane == 0 && b) ws.mask[c] = m & ~b;
+            for (uint32_t c0 = 0; c0 < nch; c0 += 4) {  // edges after rpos with a settled source
+              if (wbase + 32 * (c0 + 4) <= rpos + 1) continue;
+              uint32_t vs[4], f[4], want = 0;
+#pragma unroll
+              for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t c = c0 + q, el = 32 * c + lane;
+                const bool w = c < nch && ((ws.mask[c] >> lane) & 1u) && wbase + el > rpos;
+                vs[q] = w ? ws.src[el] : 0u;
+                want |= (w ? 1u : 0u) << q;
+              }
+              amap_first_ep_batch<kCtaAmapLog, 4>(cs.amap, vs, want, ep, f);
+#pragma unroll
+              for (uint32_t q = 0; q < 4; ++q) {
+                const unsigned b = __ballot_sync(kFull, ((want >> q) & 1u) && f[q] != 0xffffffffu);
+                if (lane == 0 && b) ws.mask[c0 + q] &= ~b;
+              }
               __syncwarp();
             }
             const uint32_t cnt2 = lane < static_cast<int>(nch) ? __popc(ws.mask[lane]) : 0u;
@@ -1436,19 +1494,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             if (lane == 0 && fl != 0xffffffffu) atomicMin(&cs.fcut, fl);
             __syncthreads();
             const uint32_t lim2 = cs.fcut;
-            for (uint32_t c = 0; c < nch && wbase + 32 * c < lim2; ++c) {  // the next conflict
-              if (wbase + 32 * c + 31 <= rpos) continue;
-              const uint32_t m = ws.mask[c];
-              if (!m) continue;
-              const uint32_t el = 32 * c + lane;
-              const bool conf = ((m >> lane) & 1u) && wbase + el > rpos && wbase + el < lim2 &&
-                                amap_first_ep<kCtaAmapLog>(cs.amap, ws.src[el], ep) < wbase + el;
-              const unsigned b = __ballot_sync(kFull, conf);
-              if (b) {
-                if (lane == 0) atomicMin(&cs.cut, wbase + 32 * c + __ffs(b) - 1);
-                break;
-              }
-            }
+            warp_first_conflict(cs.amap, ws, wbase, nch, rpos + 1, lim2, ep, &cs.cut);  // the next one
             __syncthreads();
             rpos = cs.cut;
             fpos = cs.fcut;
