@@ -263,6 +263,51 @@ __device__ __forceinline__ void amap_first_ep_batch(const unsigned long long* ma
     }
   }
 }
+// K inserts of amap_insert_ep with their probes and CASes in flight together;
+// returns the mask of the ones that found the map full.
+template <int kLog, int K>
+__device__ __forceinline__ uint32_t amap_insert_ep_batch(unsigned long long* map,
+                                                         const uint32_t (&vs)[K],
+                                                         const uint32_t (&es)[K], uint32_t pend,
+                                                         uint32_t ep) {
+  constexpr uint32_t kSlots = 1u << kLog;
+  uint32_t h[K], probes[K], failed = 0;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    h[q] = vhash(vs[q]) >> (32 - kLog);
+    probes[q] = 0;
+  }
+  while (pend) {
+    unsigned long long cur[K], r[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      cur[q] = ((pend >> q) & 1u) ? *reinterpret_cast<volatile unsigned long long*>(map + h[q]) : 0ull;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      r[q] = ~cur[q];
+      if (((pend >> q) & 1u) && ((cur[q] >> 12) & 0xfffffu) != ep)
+        r[q] = atomicCAS(map + h[q], cur[q],
+                         (static_cast<unsigned long long>(vs[q]) << 32) | (ep << 12) | es[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      if (!((pend >> q) & 1u)) continue;
+      if (((cur[q] >> 12) & 0xfffffu) != ep) {
+        if (r[q] == cur[q]) pend &= ~(1u << q);  // claimed (else: re-read the slot)
+      } else if ((cur[q] >> 32) == vs[q]) {
+        atomicMin(map + h[q], (static_cast<unsigned long long>(vs[q]) << 32) | (ep << 12) | es[q]);
+        pend &= ~(1u << q);
+      } else {
+        h[q] = (h[q] + 1) & (kSlots - 1);
+        if (++probes[q] >= kSlots) {
+          failed |= 1u << q;
+          pend &= ~(1u << q);
+        }
+      }
+    }
+  }
+  return failed;
+}
 struct WinSmem {
   union {
     WinFields win;   // multi-list windows
@@ -640,6 +685,35 @@ struct CtaSmem {
   uint32_t adv_qj;
   uint32_t any_acc;
 };
+// The accepted edges of warp slice `ws` at positions [lo, hi) into the map
+// (epoch ep), four chunks at a time; returns this lane's smallest position
+// that found the map full (or ~0u).
+__device__ __forceinline__ uint32_t warp_map_accepts(unsigned long long* amap,
+                                                     const CtaWarpFields& ws, uint32_t wbase,
+                                                     uint32_t nch, uint32_t lo, uint32_t hi,
+                                                     uint32_t ep) {
+  const int lane = threadIdx.x & 31;
+  uint32_t fail = 0xffffffffu;
+  for (uint32_t c0 = 0; c0 < nch && wbase + 32 * c0 < hi; c0 += 4) {
+    if (wbase + 32 * (c0 + 4) <= lo) continue;
+    uint32_t vs[4], es[4], pend = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+      const uint32_t c = c0 + q, e = wbase + 32 * c + lane;
+      const bool w = c < nch && ((ws.acc[c] >> lane) & 1u) && e >= lo && e < hi;
+      vs[q] = w ? ws.src[32 * c + lane] : 0u;
+      es[q] = e;
+      pend |= (w ? 1u : 0u) << q;
+    }
+    if (!pend) continue;
+    const uint32_t f = amap_insert_ep_batch<kCtaAmapLog, 4>(amap, vs, es, pend, ep);
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q)
+      if ((f >> q) & 1u) fail = min(fail, es[q]);
+  }
+  return fail;
+}
+
 // The first window position in [lo, lim) of warp slice `ws` whose edge draws
 // and whose source the map (epoch ep) holds at an earlier position, folded
 // into *cut with atomicMin; four chunks' lookups in flight at a time.
@@ -1375,14 +1449,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
         // ---- 3a. accepted sources -> first accepting position (CTA-wide map)
         uint32_t am_lane = lane < static_cast<int>(nch) ? ws.acc[lane] : 0u;
         const unsigned acm = __ballot_sync(kFull, am_lane != 0);
-        uint32_t fail = 0xffffffffu;
-        for (unsigned t = acm; t; t &= t - 1) {
-          const int c = __ffs(t) - 1;
-          const uint32_t am = __shfl_sync(kFull, am_lane, c);
-          const uint32_t el = 32 * c + lane;
-          if (((am >> lane) & 1u) && !amap_insert_ep<kCtaAmapLog>(cs.amap, ws.src[el], wbase + el, 0))
-            fail = min(fail, wbase + el);
-        }
+        uint32_t fail = acm ? warp_map_accepts(cs.amap, ws, wbase, nch, 0u, 0xffffffffu, 0u) : 0xffffffffu;
         fail = __reduce_min_sync(kFull, fail);
         if (lane == 0) {
           if (fail != 0xffffffffu) atomicMin(&cs.fcut, fail);
@@ -1413,10 +1480,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               if (rpos >= e0 && rpos < e0 + 32) ws.mask[lane] &= ~(1u << (rpos - e0));
             }
             __syncwarp();
-            for (uint32_t c = 0; c < nch && wbase + 32 * c < rpos; ++c) {  // settled accepts
-              const uint32_t el = 32 * c + lane;
-              if ((ws.acc[c] >> lane) & 1u) amap_insert_ep<kCtaAmapLog>(cs.amap, ws.src[el], wbase + el, ep);
-            }
+            warp_map_accepts(cs.amap, ws, wbase, nch, 0u, rpos, ep);  // settled accepts
             __syncthreads();
             if (tid == 0) cs.cut = 0xffffffffu;
             for (uint32_t c0 = 0; c0 < nch; c0 += 4) {  // edges after rpos with a settled source
@@ -1482,14 +1546,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               }
             }
             __syncwarp();
-            for (uint32_t c = 0; c < nch; ++c) {  // re-decided accepts into the map
-              if (wbase + 32 * c + 31 <= rpos) continue;
-              const uint32_t a = ws.acc[c];
-              const uint32_t el = 32 * c + lane;
-              if (((a >> lane) & 1u) && wbase + el > rpos &&
-                  !amap_insert_ep<kCtaAmapLog>(cs.amap, ws.src[el], wbase + el, ep))
-                fl = min(fl, wbase + el);
-            }
+            fl = min(fl, warp_map_accepts(cs.amap, ws, wbase, nch, rpos + 1, 0xffffffffu, ep));  // re-decided
             fl = __reduce_min_sync(kFull, fl);
             if (lane == 0 && fl != 0xffffffffu) atomicMin(&cs.fcut, fl);
             __syncthreads();
