@@ -502,3 +502,27 @@ def test_lt_nonmonotone_cdf_falls_back_to_the_linear_scan(cuda, oracle):
         _, st, off, mem = gpu_sample(arrays, LT, 9, 3000, lt_scan=scan)
         ref = oracle.graph(*arrays).sample(LT, 9, 0, 3000, workers=4)
         assert_sets_equal(off, mem, ref, msg=f"lt_scan {scan}")
+
+
+@pytest.mark.parametrize("mode", [0, 3])
+def test_ic_window_conflict_repairs(cuda, oracle, mode):
+    """Near-critical IC on short in-lists: giant sets whose 4,096-edge windows of
+    the block schedule hold many repeated sources: conflicts with >= 1,024 edges
+    after them are repaired inside the window (stored draw words, epoch map;
+    ~250 here), the rest cut (~5,900); every set must still be the reference's."""
+    rng = np.random.default_rng(2411)
+    n, deg = 30000, 24
+    dst = np.repeat(np.arange(n, dtype=np.uint32), deg)
+    z = (rng.zipf(1.6, dst.size) % n).astype(np.uint32)  # popular sources repeat
+    u = rng.integers(0, n, dst.size).astype(np.uint32)
+    src = np.where(rng.random(dst.size) < 0.5, z, u).astype(np.uint32)
+    w = rng.uniform(0.0, 0.16, dst.size).astype(np.float32)  # ~87 of 400 sets > 2,000 members
+    keep = src != dst
+    pairs = np.unique(np.stack([src[keep], dst[keep]]), axis=1, return_index=True)[1]
+    arrays = P.build_graph(n, src[keep][pairs], dst[keep][pairs], w[keep][pairs])
+    _, st, off, mem = gpu_sample(arrays, IC, 5, 400, ic_mode=mode)
+    sizes = np.diff(off.astype(np.int64))
+    assert sizes.max() > 2000  # giant sets: multi-window, repair territory
+    ref = oracle.graph(*arrays).sample(IC, 5, 0, 400, workers=4)
+    assert_sets_equal(off, mem, ref)
+    assert (st.counter() == ref.counter).all()
