@@ -888,7 +888,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
   uint64_t insp = 0;
   const uint32_t wbase = kWin * wl;  // this warp's first window position
 #ifdef RRG_CTA_PHASES
-  long long ph_[12] = {0}, ph_t_ = clock64();
+  long long ph_[16] = {0}, ph_t_ = clock64();
 #endif
   for (;;) {
     __syncthreads();  // previous sample written out, filter cleared
@@ -965,8 +965,10 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             if (lane == 0) xc[t] = cnt;
           }
           __syncthreads();
+          RRG_PH(12);
           // (2) stream positions of the sub-windows
           const uint32_t U = block_exscan_global(xc, W, cs.wsum);
+          RRG_PH(13);
           // (3) draws; warp wl's state walks its sub-windows in order, lane l
           //     draws ranks [32 l, 32 l + 32) after one jump by T^(32 l)
           const uint32_t uthr = uni ? __ldg(&p.rec[qj].y) : 0u;  // every edge's threshold
@@ -1092,6 +1094,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             }
           }
           __syncthreads();
+          RRG_PH(14);
           // (4) accepted sources, appended in CSR order
           const uint32_t A = block_exscan_global(xA, W, cs.wsum);
           if (U) s = Xoshiro{cs.st[0], cs.st[1], cs.st[2], cs.st[3]};
@@ -1700,13 +1703,16 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
 #ifdef RRG_CTA_PHASES
   if (tid == 0) {
     long long tot = 0;
-    for (int k = 0; k < 12; ++k) tot += ph_[k];
-    if (tot > 2000000)
+    for (int k = 0; k < 16; ++k) tot += ph_[k];
+    if (tot > 2000000 && blockIdx.x < 3)
       printf("[cta %d] Mcyc total %.2f: between %.2f list %.2f fast %.2f layout %.2f classify %.2f "
              "draw+3a %.2f 3b %.2f repair %.2f cut %.2f append %.2f advance %.2f tail %.2f\n",
              blockIdx.x, tot * 1e-6, ph_[0] * 1e-6, ph_[1] * 1e-6, ph_[2] * 1e-6, ph_[3] * 1e-6,
              ph_[4] * 1e-6, ph_[5] * 1e-6, ph_[6] * 1e-6, ph_[7] * 1e-6, ph_[8] * 1e-6,
              ph_[9] * 1e-6, ph_[10] * 1e-6, ph_[11] * 1e-6);
+    if (tot > 2000000 && blockIdx.x < 3)
+      printf("[cta %d] list: classify %.2f scan %.2f draws %.2f append %.2f\n", blockIdx.x,
+             ph_[12] * 1e-6, ph_[13] * 1e-6, ph_[14] * 1e-6, ph_[1] * 1e-6);
   }
 #endif
   if (tid == 0) p.wtags[tslot] = tag;
