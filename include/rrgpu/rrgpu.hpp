@@ -50,6 +50,8 @@ class Graph {
         const std::vector<uint32_t>& reverse_sources, const std::vector<float>& reverse_weights) {
     if (reverse_offsets.size() != static_cast<size_t>(n) + 1)
       throw std::invalid_argument("reverse_offsets must hold n + 1 entries");
+    if (reverse_sources.size() != reverse_weights.size())
+      throw std::invalid_argument("reverse_sources and reverse_weights differ in length");
     rrg_graph* h = nullptr;
     check(rrg_graph_create(n, reverse_sources.size(), reverse_offsets.data(),
                            reverse_sources.data(), reverse_weights.data(), &h));

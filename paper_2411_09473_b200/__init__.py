@@ -59,6 +59,9 @@ def build_graph(n: int, src, dst, w):
     src = np.ascontiguousarray(src, dtype=np.uint32)
     dst = np.ascontiguousarray(dst, dtype=np.uint32)
     w = np.ascontiguousarray(w, dtype=np.float32)
+    if not (src.size == dst.size == w.size):
+        raise ValueError(f"build_graph: src, dst and w differ in length "
+                         f"({src.size}, {dst.size}, {w.size})")
     m = src.size
     roff = np.zeros(n + 1, dtype=np.uint64)
     rsrc = np.zeros(m, dtype=np.uint32)
@@ -83,6 +86,11 @@ class Graph:
         self.reverse_offsets = np.ascontiguousarray(rev_offsets, dtype=np.uint64)
         self.reverse_sources = np.ascontiguousarray(rev_sources, dtype=np.uint32)
         self.reverse_weights = np.ascontiguousarray(rev_weights, dtype=np.float32)
+        if self.reverse_offsets.size < 1:
+            raise ValueError("Graph: reverse_offsets needs n + 1 >= 1 entries")
+        if self.reverse_weights.size != self.reverse_sources.size:
+            raise ValueError("Graph: reverse_sources and reverse_weights differ in length "
+                             f"({self.reverse_sources.size} vs {self.reverse_weights.size})")
         self.num_vertices = int(self.reverse_offsets.size - 1)
         self.num_edges = int(self.reverse_sources.size)
         h = C.c_void_p()
@@ -113,6 +121,9 @@ class Graph:
         src = np.ascontiguousarray(src, dtype=np.uint32)
         dst = np.ascontiguousarray(dst, dtype=np.uint32)
         w = np.ascontiguousarray(w, dtype=np.float32)
+        if not (src.size == dst.size == w.size):
+            raise ValueError("from_edge_arrays: src, dst and w differ in length "
+                             f"({src.size}, {dst.size}, {w.size})")
         h = C.c_void_p()
         check(lib.rrg_graph_create_from_edges(n, src.size, ptr(src, C.c_uint32),
                                               ptr(dst, C.c_uint32), ptr(w, C.c_float),

@@ -148,6 +148,20 @@ void ensure_lane_scratch(rrg_graph* g, uint64_t lanes) {
   sc.lanes = lanes;
 }
 
+// Worker warps of the big-set path for n_items sets: up to 4 per SM, capped so
+// their n-bit maps + n-entry lists take at most a quarter of the free device
+// memory (the kernel's grid-stride loop takes the remaining sets); >= 1.
+uint32_t big_workers(rrg_graph* g, uint64_t n_items) {
+  uint64_t w = std::min<uint64_t>(n_items, std::min<uint64_t>(kBigWorkersMax, 4ull * g->num_sms));
+  if (g->big.workers >= w) return static_cast<uint32_t>(std::max<uint64_t>(1, w));
+  size_t free_b = 0, total_b = 0;
+  RRG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const uint64_t per = ((static_cast<uint64_t>(g->n) + 31) / 32) * 4 + static_cast<uint64_t>(g->n) * 4;
+  const uint64_t budget = (free_b + static_cast<uint64_t>(g->big.workers) * per) / 4;
+  w = std::min<uint64_t>(w, budget / std::max<uint64_t>(per, 1));
+  return static_cast<uint32_t>(std::max<uint64_t>(1, w));
+}
+
 void ensure_big_scratch(rrg_graph* g, uint32_t workers) {
   BigScratch& b = g->big;
   if (b.workers >= workers) return;
@@ -630,16 +644,14 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
           p.count = n_items;
           uint32_t workers = 0;
           if (kind == kFastBig) {
-            workers = static_cast<uint32_t>(std::min<uint64_t>(
-                n_items, std::min<uint64_t>(kBigWorkersMax, 4ull * g->num_sms)));
+            workers = big_workers(g, n_items);
             ensure_big_scratch(g, workers);
           }
           const uint64_t grid_need = (n_items + block / 32 - 1) / (block / 32);
           launch_fast(p, static_cast<int>(std::max<uint64_t>(1, std::min(full_grid, grid_need))),
                       kind == kFastBig, g->big.bitmaps.ptr, g->big.lists.ptr, workers, st);
         } else if (kind == kBig) {
-          const uint32_t workers = static_cast<uint32_t>(std::min<uint64_t>(
-              n_items, std::min<uint64_t>(kBigWorkersMax, 4ull * g->num_sms)));
+          const uint32_t workers = big_workers(g, n_items);
           ensure_big_scratch(g, workers);
           launch_big(model, p, list, static_cast<uint32_t>(n_items), g->big.bitmaps.ptr,
                      g->big.lists.ptr, workers, st);
@@ -888,7 +900,7 @@ rrg_status rrg_fraction_covered(rrg_store* s, const uint32_t* seeds, uint32_t ns
 rrg_status rrg_store_export(const rrg_store* s, uint64_t first, uint64_t count, uint64_t* offsets,
                             uint32_t* members) {
   if (!s || !offsets) return invalid("null argument");
-  if (first + count > s->nsets) return invalid("export range out of bounds");
+  if (count > s->nsets || first > s->nsets - count) return invalid("export range out of bounds");
   return guarded([&]() -> rrg_status {
     rrg_graph* g = s->g;
     std::vector<uint64_t> off(count + 1);
@@ -909,7 +921,8 @@ rrg_status rrg_store_append_from(rrg_store* dst, const rrg_store* src, uint64_t 
   if (!dst || !src) return invalid("null store");
   if (dst->g != src->g) return invalid("append_from: stores of different graphs");
   if (dst == src) return invalid("append_from: source and destination are the same store");
-  if (first + count > src->nsets) return invalid("append_from: range out of bounds");
+  if (count > src->nsets || first > src->nsets - count)
+    return invalid("append_from: range out of bounds");
   if (count == 0) return RRG_OK;
   return guarded([&]() -> rrg_status {
     rrg_graph* g = dst->g;

@@ -7,8 +7,8 @@
 //     source id, parallel edges in input order (a stable counting sort by
 //     source, then one by target). That is a STABLE sort of the edges by the
 //     64-bit key (dst << 32 | src): one radix sort of (key, edge index) pairs,
-//     then a gather of the weights; offsets come from the run boundaries of the
-//     sorted keys (no atomics on hub counters);
+//     then a gather of the weights; offsets by a lower_bound per vertex over the
+//     sorted keys (no atomics on hub counters, no serial fill of empty runs);
 //   * normalize_lt_weights, restated per in-list with the same sequential fp64
 //     sums, the same float roundings and the same 64-attempt deflation, so the
 //     weights are bit-identical (the library builds with --fmad=false).
@@ -31,26 +31,30 @@ __global__ void k_edge_keys(const uint32_t* src, const uint32_t* dst, uint64_t m
   }
 }
 
-// Sorted keys -> transpose sources, weights and u32 offsets: the first edge of
-// target d fills off[v] for every v in (previous target, d]; the last edge
-// fills the tail up to off[n] = m.
+// Sorted keys -> transpose sources and weights (edge i of the sorted order).
 __global__ void k_scatter_transpose(const unsigned long long* keys, const uint32_t* idx,
-                                    const float* w_in, uint64_t m, uint32_t n, uint32_t* off,
-                                    uint32_t* rsrc, float* rw) {
+                                    const float* w_in, uint64_t m, uint32_t* rsrc, float* rw) {
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long k = keys[i];
-    const uint32_t d = static_cast<uint32_t>(k >> 32);
-    rsrc[i] = static_cast<uint32_t>(k);
+    rsrc[i] = static_cast<uint32_t>(keys[i]);
     rw[i] = w_in[idx[i]];
-    const uint32_t prev = i ? static_cast<uint32_t>(keys[i - 1] >> 32) : 0u;
-    if (i == 0) {
-      for (uint32_t v = 0; v <= d; ++v) off[v] = 0;
-    } else if (d != prev) {
-      for (uint32_t v = prev + 1; v <= d; ++v) off[v] = static_cast<uint32_t>(i);
+  }
+}
+
+// off[v] = index of the first sorted key whose target is >= v (v in [0, n]), one
+// thread per vertex with a lower_bound over the sorted keys: no serial fill of
+// zero-in-degree runs, whatever the gaps between targets.
+__global__ void k_transpose_offsets(const unsigned long long* keys, uint64_t m, uint32_t n,
+                                    uint32_t* off) {
+  for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v <= n;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long key = static_cast<unsigned long long>(v) << 32;
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < key) lo = mid + 1; else hi = mid;
     }
-    if (i + 1 == m)
-      for (uint32_t v = d + 1; v <= n; ++v) off[v] = static_cast<uint32_t>(m);
+    off[v] = static_cast<uint32_t>(lo);
   }
 }
 
@@ -219,6 +223,12 @@ uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint3
     k_edge_keys<<<grid, 256, 0, st>>>(d_src, d_dst, m, n, keys.ptr, idx.ptr, bad.ptr);
     RRG_CUDA(cudaGetLastError());
     count_launch();
+    // Out-of-range ids are rejected before the sort: the keys only carry
+    // 32 + vbits bits, and the offsets below assume every target is < n.
+    uint32_t hbad = 0;
+    RRG_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, 4, cudaMemcpyDeviceToHost, st));
+    RRG_CUDA(cudaStreamSynchronize(st));
+    if (hbad) return 1;
     int vbits = 1;
     while (vbits < 32 && (1ull << vbits) < n) ++vbits;
     size_t temp_bytes = 0;
@@ -232,8 +242,11 @@ uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint3
                                              st));
     count_launch();
     if (w_ready) RRG_CUDA(cudaStreamWaitEvent(st, w_ready, 0));
-    k_scatter_transpose<<<grid, 256, 0, st>>>(keys2.ptr, idx2.ptr, d_w, m, n, g->off.ptr,
-                                              g->src.ptr, g->w.ptr);
+    k_scatter_transpose<<<grid, 256, 0, st>>>(keys2.ptr, idx2.ptr, d_w, m, g->src.ptr,
+                                              g->w.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+    k_transpose_offsets<<<(n + 256) / 256, 256, 0, st>>>(keys2.ptr, m, n, g->off.ptr);
     RRG_CUDA(cudaGetLastError());
     count_launch();
     RRG_CUDA(cudaStreamSynchronize(st));  // temporaries are released at scope end

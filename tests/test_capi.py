@@ -39,6 +39,16 @@ def test_version_and_errors():
     assert "sm_100a" in P.version()
     with pytest.raises(ValueError):
         P.build_graph(3, [0, 5], [1, 1], [0.5, 0.5])  # id out of range
+    # mismatched array lengths are rejected before any copy (no read past a buffer)
+    with pytest.raises(ValueError, match="differ in length"):
+        P.build_graph(3, [0, 1], [1], [0.5, 0.5])
+    with pytest.raises(ValueError, match="differ in length"):
+        P.build_graph(3, [0, 1], [1, 2], [0.5])
+    with pytest.raises(ValueError, match="differ in length"):
+        P.Graph(np.array([0, 1, 2], np.uint64), np.array([0, 1], np.uint32),
+                np.array([0.5], np.float32))
+    with pytest.raises(ValueError, match="differ in length"):
+        P.Graph.from_edge_arrays(3, [0, 1], [1, 2], [0.5])
 
 
 def f32_bits(x):

@@ -85,6 +85,27 @@ def test_device_graph_errors(cuda):
         P.Graph.from_edge_arrays(4, [0, 1], [1, 2], [0.5, -0.5], normalize_lt=True)
     g = P.Graph.from_edge_arrays(4, [0, 1], [1, 2], [0.5, -0.5])  # no normalization: kept
     assert g.reverse_weights.tolist() == [0.5, -0.5]
+    # out-of-range targets are rejected before the sort and the offsets fill
+    for bad_dst in (4, 5, 0xFFFFFFFF):
+        with pytest.raises(ValueError, match="out of range"):
+            P.Graph.from_edge_arrays(4, [0, 1, 2], [1, bad_dst, 3], [0.5, 0.5, 0.5])
+    # the context is still usable afterwards
+    g = P.Graph.from_edge_arrays(4, [0, 1, 2], [1, 3, 3], [0.5, 0.5, 0.5])
+    assert g.reverse_offsets.tolist() == [0, 0, 1, 1, 3]
+    with pytest.raises(ValueError, match="differ in length"):
+        P.Graph.from_edge_arrays(4, [0, 1], [1], [0.5, 0.5])
+
+
+def test_device_graph_long_empty_runs(cuda):
+    """Targets only in the upper half of the id range (and a lone target at 0):
+    the offsets of long zero-in-degree runs are filled in parallel."""
+    n = 1 << 20
+    src = np.array([5, 6, 7, 8], np.uint32)
+    dst = np.array([0, n - 1, n - 1, n // 2], np.uint32)
+    g = P.Graph.from_edge_arrays(n, src, dst, np.full(4, 0.25, np.float32))
+    ref = P.build_graph(n, src, dst, np.full(4, 0.25, np.float32))
+    assert (g.reverse_offsets == ref[0]).all()
+    assert (g.reverse_sources == ref[1]).all()
 
 
 @pytest.mark.parametrize("model", [0, 1])
