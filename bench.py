@@ -78,8 +78,9 @@ def parse():
     ap.add_argument("--no-imm", action="store_true")
     ap.add_argument("--no-graph-prep", action="store_true",
                     help="skip the edge-list -> transpose comparison (device vs reference)")
-    ap.add_argument("--ref-sets", type=int, default=1 << 14,
-                    help="sets per step of the reference arm (bounded CPU sample)")
+    ap.add_argument("--ref-sets", type=int, default=0,
+                    help="sets per step of the reference arm (0 = --sets, the same "
+                         "workload as our arm)")
     return ap.parse_args()
 
 
@@ -178,14 +179,39 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
+def graphs_module():
+    """paper_2411_09473_b200/graphs.py loaded by path, NOT through the package:
+    importing the package would load librrgpu.so, and the reference arm must map
+    no library of ours (its inputs come from the rrgen child process)."""
+    import importlib.util
+    name = "rrgpu_bench_graphs"
+    if name not in sys.modules:
+        spec = importlib.util.spec_from_file_location(
+            name, os.path.join(ROOT, "paper_2411_09473_b200", "graphs.py"))
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules[name] = mod
+        spec.loader.exec_module(mod)
+    return sys.modules[name]
+
+
 def graph_arrays(name):
-    from paper_2411_09473_b200 import graphs
+    graphs = graphs_module()
     cfg = graphs.CONFIGS[name]
     return cfg, graphs.generate(cfg)
 
 
 def workload_desc(cfg, n, m):
     return f"{cfg.name}: {cfg.description} (n={n}, arcs={m}, k={cfg.k})"
+
+
+def bench_config(cfg, n, m, sets_per_step, world):
+    """The `config` object of both arms' lines (identical by construction)."""
+    return {"workload": workload_desc(cfg, n, m), "sets_per_step": sets_per_step, "run_seed": 1,
+            "slots": "rank r, step i: [(i*world+r)*N, +N)",
+            "l2": "graph > L2 (arrays 0.9+ GB at cfg4); the GPU arm also writes a 256 MiB "
+                  "buffer between timed steps (L2 flush)",
+            "generator": "pinned Chung-Lu/R-MAT (rrgen), DESIGN.md Inputs",
+            "parallelism": f"slot-range shards x{world}"}
 
 
 def cpu_cores():
@@ -205,7 +231,7 @@ def run_reference(args, rank):
     cfg, (roff, rsrc, rw) = graph_arrays(args.workload)
     g = orc.graph(roff, rsrc, rw)
     cores = cpu_cores()
-    n_sets = args.ref_sets
+    n_sets = args.ref_sets or args.sets
     for _ in range(args.warmup):
         g.sample(cfg.model, 1, 0, n_sets, workers=cores)
     t0 = time.perf_counter()
@@ -218,8 +244,7 @@ def run_reference(args, rank):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64 cdf / u32 ids", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg, roff.size - 1, rsrc.size),
-                   "sets_per_step": n_sets, "run_seed": 1},
+        "config": bench_config(cfg, roff.size - 1, rsrc.size, n_sets, args.gpus),
         "cpu_baseline": {"value": value, "unit": "sets/s", "cores": cores, "kind": orc.kind,
                          "sample": f"generate_batch_fused of slots [0,{n_sets}) per step "
                                    f"on WorkPool({cores})"},
@@ -488,12 +513,8 @@ def run_ours(args, rank, world, local):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 cdf / u32 ids" if model == 1 else "u64 rng / u32 ids",
         "data": "synthetic",
-        "config": {"workload": workload_desc(cfg, n, m), "sets_per_step": N, "run_seed": 1,
-                   "slots": "rank r, step i: [(i*world+r)*N, +N)",
-                   "lt_scan": args.lt_scan if model == 1 else None,
-                   "l2": "graph > L2 (arrays 0.9+ GB) and 256 MiB L2 flush between steps",
-                   "generator": "pinned Chung-Lu/R-MAT, DESIGN.md Inputs",
-                   "parallelism": f"slot-range shards x{world}"},
+        "config": bench_config(cfg, n, m, N, world),
+        "lt_scan": args.lt_scan if model == 1 else None,
         "edges_inspected_per_sec": world * insp / (max_ms / 1e3),
         "edges_inspected_per_set": insp / (N * args.steps),
         "members_per_set": members / (N * args.steps),

@@ -225,33 +225,6 @@ rrg_status rrg_build_transpose(uint32_t n, uint64_t m, const uint32_t* src, cons
 /* normalize_lt_weights (graph.hpp:207-235) on transpose weights, in place. */
 rrg_status rrg_normalize_lt_weights(uint32_t n, const uint64_t* roff, float* rw);
 
-/* Synthetic BASELINE graphs (pinned generators). Fills the
- * transpose arrays; call with roff == NULL first to learn n and m. */
-typedef enum {
-  RRG_GEN_RMAT = 0,           /* p0=scale, p1..p3 = a,b,c, edges = m (unique, no loops) */
-  RRG_GEN_CHUNG_LU = 1,       /* directed; p0=gamma; flags bit0: correlated in/out */
-  RRG_GEN_CHUNG_LU_UNDIR = 2  /* undirected, m unique pairs -> 2m arcs */
-} rrg_gen_kind;
-typedef enum {
-  RRG_W_WC = 0,               /* f32(1/indeg(v)) */
-  RRG_W_UNIFORM = 1,          /* U(0, scale) f32 */
-  RRG_W_LT_UNIFORM = 2        /* U(0,1) / per-vertex double sum, then normalize_lt_weights */
-} rrg_weight_kind;
-typedef struct {
-  int kind;
-  uint32_t n;
-  uint64_t m;                 /* edges (directed) or unique pairs (undirected) */
-  double p0, p1, p2, p3;
-  uint32_t flags;
-  uint64_t graph_seed;
-  int weights;
-  double weight_scale;
-  uint64_t weight_seed;
-  uint32_t threads;           /* 0 = hardware concurrency */
-} rrg_gen_spec;
-rrg_status rrg_generate_graph(const rrg_gen_spec* spec, uint32_t* n, uint64_t* m, uint64_t* roff,
-                              uint32_t* rsrc, float* rw);
-
 /* ---- misc ------------------------------------------------------------------ */
 const char* rrg_last_error(void);
 const char* rrg_version(void);

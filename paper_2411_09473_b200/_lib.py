@@ -61,24 +61,6 @@ class ImmResultC(C.Structure):
     ]
 
 
-class GenSpec(C.Structure):
-    _fields_ = [
-        ("kind", C.c_int),
-        ("n", C.c_uint32),
-        ("m", C.c_uint64),
-        ("p0", C.c_double),
-        ("p1", C.c_double),
-        ("p2", C.c_double),
-        ("p3", C.c_double),
-        ("flags", C.c_uint32),
-        ("graph_seed", C.c_uint64),
-        ("weights", C.c_int),
-        ("weight_scale", C.c_double),
-        ("weight_seed", C.c_uint64),
-        ("threads", C.c_uint32),
-    ]
-
-
 # (name, restype, argtypes) for every symbol of include/rrgpu.h
 SIGNATURES = [
     ("rrg_graph_create", C.c_int, [C.c_uint32, C.c_uint64, u64p, u32p, f32p, C.POINTER(vp)]),
@@ -116,8 +98,6 @@ SIGNATURES = [
     ("rrg_build_transpose", C.c_int,
      [C.c_uint32, C.c_uint64, u32p, u32p, f32p, u64p, u32p, f32p]),
     ("rrg_normalize_lt_weights", C.c_int, [C.c_uint32, u64p, f32p]),
-    ("rrg_generate_graph", C.c_int,
-     [C.POINTER(GenSpec), u32p, u64p, u64p, u32p, f32p]),
     ("rrg_last_error", C.c_char_p, []),
     ("rrg_version", C.c_char_p, []),
     ("rrg_debug_bernoulli_threshold", C.c_uint64, [C.c_uint32]),
