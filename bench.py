@@ -78,6 +78,11 @@ def parse():
     ap.add_argument("--no-imm", action="store_true")
     ap.add_argument("--no-graph-prep", action="store_true",
                     help="skip the edge-list -> transpose comparison (device vs reference)")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the IC sampling blocks (cfg1, cfg5) and the five-config IMM table")
+    ap.add_argument("--ic-sets", default="cfg1:1048576,cfg5:32768",
+                    help="IC sampling blocks, workload:sets_per_step")
+    ap.add_argument("--imm-configs", default="cfg1,cfg2,cfg3,cfg4,cfg5")
     ap.add_argument("--ref-sets", type=int, default=0,
                     help="sets per step of the reference arm (0 = --sets, the same "
                          "workload as our arm)")
@@ -300,6 +305,131 @@ def graph_prep(P, orc, roff, rsrc, rw, model):
                          + f" ({orc.kind}), one host thread"}
 
 
+def ic_block(args, P, name, nsets, stream, flush, peak, peak_src, orc, cores, traffic_of):
+    """Driver-timed IC sampling on a BASELINE IC config: W untimed +
+    K timed generate_slots of nsets sets (graph resident, L2 flushed between
+    steps), per-step CUDA events; roofline = 8 B x reference-inspected in-edges
+    (one {source, threshold} record per inspected edge, sampling.hpp:100-106) /
+    sampler event time; a bounded cpu_baseline of the reference's
+    generate_batch_fused on the same slots, its sets checked against ours."""
+    import torch
+    cfg, arrays = graph_arrays(name)
+    n, m = arrays[0].size - 1, arrays[1].size
+    g = P.Graph(*arrays)
+    g.set_stream(stream.cuda_stream)
+    g.prepare(0)
+    st = P.RRRStore(g)
+    for i in range(args.warmup):
+        st.clear()
+        P.generate_slots(g, 0, 1, i * nsets, nsets, st)
+    torch.cuda.synchronize()
+    clocks = Clocks(torch.cuda.current_device())
+    l0 = P.launch_count()
+    tot = smp = 0.0
+    insp = members = deferred = 0
+    for i in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st.clear()
+        P.generate_slots(g, 0, 1, (args.warmup + i) * nsets, nsets, st)
+        e1.record(stream)
+        e1.synchronize()
+        b = g.last_batch_stats()
+        tot += e0.elapsed_time(e1)
+        smp += b.sample_ms
+        insp += b.edges_inspected
+        members += b.members
+        deferred += b.deferred
+    launches = P.launch_count() - l0
+    clk = clocks.stop()
+    achieved = 8.0 * insp / (smp / 1e3) / 1e9
+    out = {"workload": workload_desc(cfg, n, m), "sets_per_step": nsets, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": tot / args.steps,
+           "value": nsets * args.steps / (tot / 1e3), "unit": "sets/s",
+           "edges_inspected_per_sec": insp / (tot / 1e3),
+           "edges_inspected_per_set": insp / (nsets * args.steps),
+           "members_per_set": members / (nsets * args.steps), "deferred_sets": deferred,
+           "sampler_ms_per_step": smp / args.steps,
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": traffic_of(f"{name}:ic@{nsets}"),
+                        "kernel": "k_sample_ic_cta / k_sample_ic_warp<32> / k_sample_ic "
+                                  "(auto schedule)",
+                        "bytes": BYTES_RULE["ic"], "peak_source": peak_src},
+           "gpu_launches": launches, "clocks": clk}
+    if orc is not None:
+        og = orc.graph(*arrays)
+        ncpu = max(1, min(nsets, args.ic_cpu_sets.get(name, 2048)))
+        t0 = time.perf_counter()
+        sk = og.sample(0, 1, 0, ncpu, workers=cores)
+        dt = time.perf_counter() - t0
+        st.clear()
+        P.generate_slots(g, 0, 1, 0, ncpu, st)
+        o2, m2 = st.export()
+        same = bool((np.diff(o2.astype(np.int64)) == np.diff(sk.offsets.astype(np.int64))).all())
+        if same:
+            for i in range(ncpu):
+                if not np.array_equal(np.sort(m2[o2[i]:o2[i + 1]]),
+                                      sk.members[sk.offsets[i]:sk.offsets[i + 1]]):
+                    same = False
+                    break
+        same = same and bool((st.counter() == sk.counter).all())
+        out["cpu_baseline"] = {
+            "value": ncpu / dt, "unit": "sets/s", "cores": cores, "kind": orc.kind,
+            "edges_inspected_per_sec": float(sk.inspected) / dt,
+            "sample": f"generate_batch_fused of slots [0,{ncpu}) on WorkPool({cores})",
+            "seconds": dt, "gpu_sets_match_reference": same}
+    st.close()
+    g.close()
+    return out
+
+
+def imm_block(P, name, orc, cores, reps=3):
+    """run_imm on one BASELINE config (k, epsilon of the config): the GPU with the
+    graph resident (median of reps after a warm-up), the GPU from host arrays
+    (upload + K0 + IMM), the reference's run_imm on all host cores; parity flags
+    for seeds, marginals, theta / theta' / LB."""
+    cfg, arrays = graph_arrays(name)
+    n = arrays[0].size - 1
+    icfg = P.ImmConfig(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model)
+    g = P.Graph(*arrays)
+    P.run_imm(g, icfg)
+    walls = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = P.run_imm(g, icfg)
+        walls.append(time.perf_counter() - t0)
+    g.close()
+    t0 = time.perf_counter()
+    ge = P.Graph(*arrays)
+    re_ = P.run_imm(ge, icfg)
+    t_e2e = time.perf_counter() - t0
+    ge.close()
+    out = {"workload": workload_desc(cfg, n, arrays[1].size), "k": cfg.k,
+           "epsilon": cfg.epsilon, "gpu_wall_s": statistics.median(walls),
+           "gpu_wall_s_note": f"median of {reps} after one warm-up, graph resident",
+           "gpu_e2e_wall_s": t_e2e, "gpu_e2e_note": "from host arrays: upload + K0 + IMM",
+           "gpu_timings": r.timings, "theta": r.theta, "theta_prime": r.theta_prime,
+           "sets_generated": r.sets_generated,
+           "influence_estimate": n * sum(r.seeds.marginal_counts) / r.sets_generated,
+           "e2e_same_seeds": re_.seeds.seeds == r.seeds.seeds}
+    if orc is not None:
+        og = orc.graph(*arrays)
+        t0 = time.perf_counter()
+        rr = og.imm(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model, workers=cores)
+        out["cpu_reference_wall_s"] = time.perf_counter() - t0
+        out["cpu_cores"] = cores
+        out["cpu_kind"] = orc.kind
+        out["speedup_resident"] = out["cpu_reference_wall_s"] / out["gpu_wall_s"]
+        out["speedup_e2e"] = out["cpu_reference_wall_s"] / t_e2e
+        out["seeds_match"] = r.seeds.seeds == rr["seeds"]
+        out["marginals_match"] = r.seeds.marginal_counts == rr["marginals"]
+        out["theta_match"] = (r.theta, r.theta_prime, r.lower_bound) == \
+            (rr["theta"], rr["theta_prime"], rr["lower_bound"])
+    return out
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2411_09473_b200 as P
@@ -505,6 +635,14 @@ def run_ours(args, rank, world, local):
         except Exception:
             return None
 
+    def ncu_traffic_key(key):
+        prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        try:
+            with open(prof) as f:
+                return json.load(f).get("traffic_bytes_per_launch", {}).get(key)
+        except Exception:
+            return None
+
     traffic = ncu_traffic(args.lt_scan if model == 1 else "ic")
 
     line = {
@@ -630,6 +768,26 @@ def run_ours(args, rank, world, local):
                 "theta_match": (r.theta, r.theta_prime, r.lower_bound) ==
                                (rr["theta"], rr["theta_prime"], rr["lower_bound"]),
                 "influence_estimate": n * sum(r.seeds.marginal_counts) / r.sets_generated}
+    # ---- IC sampling blocks and the five-config IMM table (rank 0, N=1) ------
+    if rank == 0 and world == 1 and not args.no_extra:
+        orc_x = None
+        if not args.no_cpu_baseline:
+            from oracle import Oracle, available
+            orc_x = Oracle("reference" if available("reference") else "port")
+        try:
+            store.close()
+        except Exception:
+            pass
+        g.close()
+        cores = cpu_cores()
+        line["ic"] = {}
+        for item in filter(None, args.ic_sets.split(",")):
+            name, nb = item.split(":")
+            line["ic"][name] = ic_block(args, P, name, int(nb), stream, flush, peak, peak_src,
+                                        orc_x, cores, ncu_traffic_key)
+        line["imm_all"] = {}
+        for name in filter(None, args.imm_configs.split(",")):
+            line["imm_all"][name] = imm_block(P, name, orc_x, cores)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -639,6 +797,7 @@ def run_ours(args, rank, world, local):
 
 def main():
     args = parse()
+    args.ic_cpu_sets = {"cfg1": 1 << 16, "cfg3": 1 << 16, "cfg5": 2048}
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank)
