@@ -98,13 +98,24 @@ rrg_status rrg_store_clear(rrg_store* s);
 rrg_status rrg_store_info(const rrg_store* s, uint64_t* sets, uint64_t* members,
                           uint32_t* max_set_size);
 
+/* The dense arm (rrr_set.hpp:10-13, :73-90): sets of >= n / density_divisor
+ * members are held as n-bit maps (rows), the rest as id lists. *dense_sets rows
+ * holding *dense_members members in *dense_bytes of HBM; *rebuild_rounds = rounds
+ * of the last rrg_select_seeds on this store that rebuilt the counter from the
+ * surviving sets (rebuild_update, selection.hpp:161-203). Any pointer may be NULL. */
+rrg_status rrg_store_dense_info(const rrg_store* s, uint64_t* dense_sets,
+                                uint64_t* dense_members, uint64_t* dense_bytes,
+                                uint64_t* rebuild_rounds);
+
 /* ---- sampling: generate_batch (sampling.hpp:159-199) --------------------
  * Appends exactly `count` sets at slots [size, size+count); set j is sampled from
  * stream derive_stream_seed(run_seed, j) (sampling.hpp:179, prng.hpp:17-20), so the
  * sets are bit-identical to the reference's. fused != 0 adds every member to the
- * store's occurrence counter (sampling.hpp:184-186). density_divisor only selects
- * the reference's in-memory representation (rrr_set.hpp:73-90) and changes no
- * output; it is accepted for signature parity. On RRG_ENOMEM, *sets_generated holds
+ * store's occurrence counter (sampling.hpp:184-186). density_divisor selects the
+ * in-memory representation exactly as the reference's make_repr / pack_sketch
+ * (rrr_set.hpp:73-90, sampling.hpp:68-84): a set of >= n / density_divisor members
+ * is an n-bit map row (0: never); exports list every set either way (root first,
+ * a row's other members ascending). On RRG_ENOMEM, *sets_generated holds
  * the number of sets that were appended (BatchOutOfMemory, sampling.hpp:148-154). */
 rrg_status rrg_generate_batch(rrg_graph* g, rrg_model model, uint64_t run_seed, uint64_t count,
                               rrg_store* s, int fused, uint32_t density_divisor,
@@ -135,9 +146,11 @@ rrg_status rrg_last_batch_stats(const rrg_graph* g, rrg_batch_stats* out);
  * recounted (build_counter, :79-95). k greedy rounds run on the device with no host
  * round-trip: argmax with ties to the lowest id (:100-125), exhaustion fill with the
  * lowest unselected ids at zero gain (:61-72), decrement through an on-device
- * inverted index (:130-156). adaptive_threshold picks decrement vs rebuild in the
- * reference (:228-231); both are observationally identical (test_selection.cpp:116-137)
- * and the device always decrements, so it changes no output.
+ * inverted index (:130-156), or -- when the round's seed covers more than
+ * adaptive_threshold of the live sets -- a rebuild of the counter from the
+ * surviving sets (rebuild_update, :161-203; the same rule, :226-231). Both give
+ * the same counts (test_selection.cpp:116-137). Dense rows are tested bit by bit
+ * and counted by column sums.
  * seeds u32[k], marginals u64[k]; round_counters (nullable) u64[k*n] receives the
  * per-round counter snapshots (SelectionStats::capture_round_counters, :237-239).
  * *rounds_done (nullable) = rounds that produced a snapshot. The store stays

@@ -221,6 +221,14 @@ class RRRStore:
         check(lib.rrg_store_info(self._h, None, None, C.byref(x)))
         return x.value
 
+    def dense_info(self) -> dict:
+        """The dense arm (rrr_set.hpp:73-90): n-bit map rows, their members and
+        bytes, and the rebuild rounds of the last select_seeds on this store."""
+        v = [C.c_uint64() for _ in range(4)]
+        check(lib.rrg_store_dense_info(self._h, *[C.byref(x) for x in v]))
+        return {"dense_sets": v[0].value, "dense_members": v[1].value,
+                "dense_bytes": v[2].value, "rebuild_rounds": v[3].value}
+
     def clear(self) -> None:
         check(lib.rrg_store_clear(self._h))
 

@@ -182,10 +182,50 @@ void d2h(T* dst, const T* src, size_t count, cudaStream_t s) {
 
 void sync(rrg_graph* g) { RRG_CUDA(cudaStreamSynchronize(g->stream)); }
 
-// Appends `count` already-staged sets (slot_len/slot_start in the store's staging
-// arrays) to the slot-ordered buffer: K3 scan + compaction.
-void commit_staged(rrg_store* s, uint64_t count) {
+// Grows the row pool of the dense arm to hold `need` rows, keeping the rows in use.
+// Grows the row pool of the dense arm to hold `need` rows, keeping the first
+// `keep` (default: the rows in use).
+void ensure_rows(rrg_store* s, uint64_t need, uint64_t keep = UINT64_MAX) {
   rrg_graph* g = s->g;
+  if (keep == UINT64_MAX) keep = s->ndense;
+  if (need * s->dwords <= s->dbits.cap && need <= s->dlen.cap) return;
+  const uint64_t rows = std::max<uint64_t>(need, std::max<uint64_t>(16, s->dlen.cap + s->dlen.cap / 2));
+  s->dbits.reserve_keep(rows * s->dwords, keep * s->dwords, g->stream);
+  s->dlen.reserve_keep(rows, keep, g->stream);
+  s->droot.reserve_keep(rows, keep, g->stream);
+  s->dslot.reserve_keep(rows, keep, g->stream);
+}
+
+uint64_t rows_cap(const rrg_store* s) {
+  return s->dwords ? std::min<uint64_t>(s->dbits.cap / s->dwords, s->dlen.cap) : 0;
+}
+
+// Appends `count` already-staged sets (slot_len/slot_start in the store's staging
+// arrays, bdix per slot: the row the big-set path wrote, else kNoRow) to the
+// slot-ordered buffer: staged lists of >= thr members become rows of the dense
+// arm (make_repr, rrr_set.hpp:82-83), then K3 scan + compaction of the lists.
+// rows_big rows from s->ndense on were written by the big-set path.
+void commit_staged(rrg_store* s, uint64_t count, uint32_t thr, uint64_t rows_big = 0,
+                   uint64_t big_members = 0, uint32_t big_max = 0) {
+  rrg_graph* g = s->g;
+  uint64_t nreq = 0;
+  unsigned long long dc[3] = {0, 0, 0};
+  if (thr != kNoDense && count) {
+    s->dreq.reserve_discard(count);
+    s->dctl.reserve_discard(3);
+    RRG_CUDA(cudaMemsetAsync(s->dctl.ptr, 0, 3 * sizeof(unsigned long long), g->stream));
+    launch_dense_mark(s->slot_len.ptr, count, thr, s->dreq.ptr, s->dctl.ptr, g->stream);
+    d2h(dc, s->dctl.ptr, 1, g->stream);
+    sync(g);
+    nreq = dc[0];
+    if (nreq) {
+      ensure_rows(s, s->ndense + rows_big + nreq, s->ndense + rows_big);
+      launch_densify(s->dreq.ptr, nreq, s->stage.ptr, s->slot_start.ptr, s->slot_len.ptr,
+                     s->bdix.ptr, s->ndense + rows_big, s->nsets, s->dbits.ptr, s->dwords,
+                     s->dlen.ptr, s->droot.ptr, s->dslot.ptr, s->dctl.ptr, g->stream);
+      d2h(dc, s->dctl.ptr, 3, g->stream);
+    }
+  }
   s->scan.reserve_discard(count + 1);
   exclusive_scan_u32(s->slot_len.ptr, s->scan.ptr, count, s->scan_tmp, g->stream);
   uint64_t added = 0;
@@ -199,6 +239,12 @@ void commit_staged(rrg_store* s, uint64_t count) {
   if (need_off > s->off.cap)
     s->off.reserve_keep(std::max<uint64_t>(need_off, s->off.cap + s->off.cap / 2), s->nsets + 1,
                         g->stream);
+  if (s->nsets + count > s->dix.cap)
+    s->dix.reserve_keep(std::max<uint64_t>(s->nsets + count, s->dix.cap + s->dix.cap / 2),
+                        s->nsets, g->stream);
+  if (count)
+    RRG_CUDA(cudaMemcpyAsync(s->dix.ptr + s->nsets, s->bdix.ptr, count * 4,
+                             cudaMemcpyDeviceToDevice, g->stream));
   launch_compact(s->stage.ptr, s->slot_start.ptr, s->slot_len.ptr, s->scan.ptr, s->total, count,
                  s->mem.ptr, s->off.ptr + s->nsets, s->maxlen_dev.ptr, g->stream);
   uint32_t mx = 0;
@@ -207,6 +253,41 @@ void commit_staged(rrg_store* s, uint64_t count) {
   s->nsets += count;
   s->total += added;
   s->max_len = mx;
+  s->ndense += rows_big + nreq;
+  s->dense_members += big_members + dc[1];
+  s->dense_max = std::max<uint32_t>(s->dense_max, std::max<uint32_t>(big_max,
+                                                                     static_cast<uint32_t>(dc[2])));
+}
+
+// bdix[0, count) = kNoRow (every slot of a new batch starts as a list set)
+void reset_batch_rows(rrg_store* s, uint64_t count) {
+  s->bdix.reserve_discard(count ? count : 1);
+  if (count) RRG_CUDA(cudaMemsetAsync(s->bdix.ptr, 0xff, count * 4, s->g->stream));
+}
+
+// counter += occurrences over sets [first, nsets) (build_counter, selection.hpp:79-95):
+// list sets by per-member atomics, rows [row0, ndense) by column sums
+void recount_into(rrg_store* s, uint64_t first, uint64_t row0, uint32_t* counter) {
+  rrg_graph* g = s->g;
+  launch_recount(s->off.ptr + first, s->mem.ptr, s->nsets - first, counter, g->stream);
+  launch_dense_colsum(s->dbits.ptr, s->dwords, g->n, nullptr, row0, s->ndense - row0, counter, +1,
+                      g->stream);
+}
+
+// Materializes sets [first, first + count) as lists (rows decoded root first)
+// into s->xoff (relative offsets, count + 1) / s->xmem; returns the members.
+uint64_t materialize(rrg_store* s, uint64_t first, uint64_t count, cudaStream_t st) {
+  s->xlen.reserve_discard(count ? count : 1);
+  s->xoff.reserve_discard(count + 1);
+  launch_set_lengths(s->off.ptr, s->dix.ptr, s->dlen.ptr, first, count, s->xlen.ptr, st);
+  exclusive_scan_u32(s->xlen.ptr, s->xoff.ptr, count, s->scan_tmp, st);
+  uint64_t tot = 0;
+  d2h(&tot, s->xoff.ptr + count, 1, st);
+  RRG_CUDA(cudaStreamSynchronize(st));
+  s->xmem.reserve_discard(tot ? tot : 1);
+  launch_materialize(s->off.ptr, s->mem.ptr, s->dix.ptr, s->dbits.ptr, s->dwords, s->droot.ptr,
+                     first, count, s->xoff.ptr, s->xmem.ptr, st);
+  return tot;
 }
 
 }  // namespace
@@ -448,6 +529,9 @@ rrg_status rrg_store_create(rrg_graph* g, rrg_store** out) {
   s->g = g;
   const rrg_status st = guarded([&]() -> rrg_status {
     s->off.reserve_discard(1024);
+    s->dix.reserve_discard(1024);
+    s->dctl.reserve_discard(3);
+    s->dwords = static_cast<uint32_t>(((static_cast<uint64_t>(g->n) + 31) / 32 + 3) & ~3ull);
     s->mem.reserve_discard(1 << 16);
     s->counter.reserve_discard(g->n ? g->n : 1);
     s->maxlen_dev.reserve_discard(1);
@@ -481,17 +565,30 @@ rrg_status rrg_store_clear(rrg_store* s) {
     sync(g);
     s->nsets = s->total = 0;
     s->max_len = 0;
+    s->ndense = s->dense_members = 0;
+    s->dense_max = 0;
     s->counter_complete = true;
     return RRG_OK;
   });
+}
+
+rrg_status rrg_store_dense_info(const rrg_store* s, uint64_t* dense_sets,
+                                uint64_t* dense_members, uint64_t* dense_bytes,
+                                uint64_t* rebuild_rounds) {
+  if (!s) return invalid("null store");
+  if (dense_sets) *dense_sets = s->ndense;
+  if (dense_members) *dense_members = s->dense_members;
+  if (dense_bytes) *dense_bytes = s->ndense * s->dwords * 4ull;
+  if (rebuild_rounds) *rebuild_rounds = s->last_rebuilds;
+  return RRG_OK;
 }
 
 rrg_status rrg_store_info(const rrg_store* s, uint64_t* sets, uint64_t* members,
                           uint32_t* max_set_size) {
   if (!s) return invalid("null store");
   if (sets) *sets = s->nsets;
-  if (members) *members = s->total;
-  if (max_set_size) *max_set_size = s->max_len;
+  if (members) *members = s->members();
+  if (max_set_size) *max_set_size = std::max(s->max_len, s->dense_max);
   return RRG_OK;
 }
 
@@ -505,7 +602,7 @@ rrg_status rrg_generate_batch(rrg_graph* g, rrg_model model, uint64_t run_seed, 
 
 rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
                               uint64_t first_slot, uint64_t count, rrg_store* s, int fused,
-                              uint32_t /*density_divisor*/, uint64_t* sets_generated) {
+                              uint32_t density_divisor, uint64_t* sets_generated) {
   if (sets_generated) *sets_generated = 0;
   if (!g || !s || s->g != g) return invalid("generate_batch: graph/store mismatch");
   if (model != RRG_IC && model != RRG_LT) return invalid("unknown diffusion model");
@@ -525,6 +622,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
     const uint64_t full_grid = static_cast<uint64_t>(g->num_sms) * per_sm;
     ensure_lane_scratch(g, full_grid * block);
     const uint64_t kChunk = 1ull << 30;  // batch-local indices are u32
+    const uint32_t dense_thr = dense_threshold(g->n, density_divisor);
     float sample_ms = 0.0f;
     const auto t0 = std::chrono::steady_clock::now();
     rrg_batch_stats acc{};
@@ -572,6 +670,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       s->restage.reserve_discard(c);
       s->restage2.reserve_discard(c);
       s->bigre.reserve_discard(c);
+      reset_batch_rows(s, c);
       SampleCtl ctl{};
       SampleParams p{};
       p.n = g->n;
@@ -622,6 +721,22 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.dupfree = g->dupfree.ptr;
       p.uniformw = g->uniformw.ptr;
       p.ic_coop_min = g->ic_coop_min;
+      // dense arm: the big-set path writes rows from s->ndense on
+      uint64_t drow_avail = rows_cap(s) - s->ndense;
+      p.dense_thr = dense_thr;
+      p.dwords = s->dwords;
+      p.bdix = s->bdix.ptr;
+      p.drow_base = s->ndense;
+      p.set_base = s->nsets;
+      auto set_rows = [&]() {
+        p.dbits = s->dbits.ptr;
+        p.dlen = s->dlen.ptr;
+        p.droot = s->droot.ptr;
+        p.dslot = s->dslot.ptr;
+        p.drow_avail = drow_avail;
+      };
+      set_rows();
+      bool dense_short = false;
 
       // One launch of `kind` over `list` (nullptr: the range [0, n_items)). The
       // per-launch counters reset here; the deferral list accumulates over a pass.
@@ -670,6 +785,9 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         RRG_CUDA(cudaEventRecord(g->ev1, st));
         d2h(&ctl, g->ctl.ptr, 1, st);
         sync(g);
+        // rows requested past the pool were not written (those slots restaged)
+        dense_short = ctl.ndense > p.drow_avail;
+        if (dense_short) ctl.ndense = p.drow_avail;
         float ms = 0.0f;
         RRG_CUDA(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
         sample_ms += ms;
@@ -701,7 +819,13 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
           launch(kind, list, n_items, rb[it & 1]);
           n_items = ctl.nrestage;
           list = rb[it & 1];
-          if (n_items) grow_staging();
+          if (dense_short) {  // the big-set path ran out of rows
+            ensure_rows(s, s->ndense + std::max<uint64_t>(ctl.ndense + n_items, 2 * drow_avail),
+                        s->ndense + ctl.ndense);
+            drow_avail = rows_cap(s) - s->ndense;
+            set_rows();
+          }
+          if (n_items && ctl.restage_members) grow_staging();
         }
         return ctl.ndeferred;
       };
@@ -744,9 +868,9 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         g->ic_mean_insp = g->ic_mean_insp < 0 ? mean : 0.5 * (g->ic_mean_insp + mean);
       }
       acc.entries_read += ctl.entries;
-      const uint64_t before = s->total;
-      commit_staged(s, c);
-      acc.members += s->total - before;
+      const uint64_t before = s->members();
+      commit_staged(s, c, dense_thr, ctl.ndense, ctl.dense_members, ctl.dense_max);
+      acc.members += s->members() - before;
       acc.sets += c;
       done += c;
       if (sets_generated) *sets_generated = done;
@@ -765,7 +889,7 @@ rrg_status rrg_last_batch_stats(const rrg_graph* g, rrg_batch_stats* out) {
   return RRG_OK;
 }
 
-rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double /*adaptive_threshold*/,
+rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double adaptive_threshold,
                             int use_prebuilt, uint32_t* seeds, uint64_t* marginals,
                             uint64_t* round_counters, uint32_t* rounds_done,
                             uint64_t* covered_total) {
@@ -783,7 +907,7 @@ rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double /*adaptive_threshol
                                st));
     } else {
       RRG_CUDA(cudaMemsetAsync(s->wcnt.ptr, 0, 4ull * n, st));
-      launch_recount(s->off.ptr, s->mem.ptr, s->nsets, s->wcnt.ptr, st);
+      recount_into(s, 0, 0, s->wcnt.ptr);
     }
     RRG_CUDA(cudaMemsetAsync(s->status.ptr, 0, 8, st));
     // Scan mode (stores up to kScanMaxMembers, 128 MB: every round re-reads the
@@ -800,7 +924,14 @@ rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double /*adaptive_threshol
       launch_set_spans(s->off.ptr, s->mem.ptr, s->nsets, s->span.ptr, s->inv.ptr, st);
     } else {
       s->ioff.reserve_discard(static_cast<uint64_t>(n) + 1);
-      exclusive_scan_u32(s->wcnt.ptr, s->ioff.ptr, n, s->scan_tmp, st);
+      const uint32_t* lc = s->wcnt.ptr;
+      if (s->ndense) {  // the index holds list sets only: their own counts
+        s->lcnt.reserve_discard(n);
+        RRG_CUDA(cudaMemsetAsync(s->lcnt.ptr, 0, 4ull * n, st));
+        launch_recount(s->off.ptr, s->mem.ptr, s->nsets, s->lcnt.ptr, st);
+        lc = s->lcnt.ptr;
+      }
+      exclusive_scan_u32(lc, s->ioff.ptr, n, s->scan_tmp, st);
       s->icur.reserve_discard(n);
       RRG_CUDA(cudaMemcpyAsync(s->icur.ptr, s->ioff.ptr, 8ull * n, cudaMemcpyDeviceToDevice, st));
       s->inv.reserve_discard(s->total ? s->total : 1);
@@ -841,13 +972,33 @@ rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double /*adaptive_threshol
     p.scan = scan ? 1 : 0;
     p.span = s->span.ptr;
     p.wmem = s->inv.ptr;
+    // dense arm: rows are tested bit by bit; rebuild_update (selection.hpp:161-203)
+    // when the round's seed covers more than adaptive_threshold of the live sets
+    p.nd = s->ndense;
+    p.dwords = s->dwords;
+    p.dbits = s->dbits.ptr;
+    s->dcov.reserve_discard(s->ndense ? s->ndense : 1);
+    s->dkill.reserve_discard(s->ndense ? s->ndense : 1);
+    s->dkn.reserve_discard(k + 1);
+    s->dctl.reserve_discard(3);
+    if (s->ndense) RRG_CUDA(cudaMemsetAsync(s->dcov.ptr, 0, 4ull * s->ndense, st));
+    RRG_CUDA(cudaMemsetAsync(s->dkn.ptr, 0, 4ull * (k + 1), st));
+    RRG_CUDA(cudaMemsetAsync(s->dctl.ptr, 0, 8, st));
+    p.dcov = s->dcov.ptr;
+    p.dkill = s->dkill.ptr;
+    p.dkn = s->dkn.ptr;
+    p.adaptive_threshold = adaptive_threshold;
+    p.rebuilds = s->dctl.ptr;
     launch_select(p, g->num_sms, st);
     uint32_t status[2] = {0, 0};
     std::vector<unsigned long long> marg(k);
     d2h(status, s->status.ptr, 2, st);
     d2h(seeds, s->seeds.ptr, k, st);
     d2h(marg.data(), s->marg.ptr, k, st);
+    unsigned long long rebuilds = 0;
+    d2h(&rebuilds, s->dctl.ptr, 1, st);
     sync(g);
+    s->last_rebuilds = rebuilds;
     if (status[1]) {
       set_error("select_seeds: prebuilt counter does not match the stored sets");
       return RRG_EINVAL;
@@ -889,6 +1040,13 @@ rrg_status rrg_fraction_covered(rrg_store* s, const uint32_t* seeds, uint32_t ns
                              g->stream));
     RRG_CUDA(cudaMemsetAsync(s->marg.ptr, 0, 8, g->stream));
     launch_fraction(s->off.ptr, s->mem.ptr, s->nsets, s->selected.ptr, s->marg.ptr, g->stream);
+    if (s->ndense && nseeds) {  // rows: a bit test per seed
+      s->xlen.reserve_discard(nseeds);
+      RRG_CUDA(cudaMemcpyAsync(s->xlen.ptr, seeds, 4ull * nseeds, cudaMemcpyHostToDevice,
+                               g->stream));
+      launch_dense_fraction(s->dbits.ptr, s->dwords, s->ndense, s->xlen.ptr, nseeds, s->marg.ptr,
+                            g->stream);
+    }
     unsigned long long hits = 0;
     d2h(&hits, s->marg.ptr, 1, g->stream);
     sync(g);
@@ -903,6 +1061,14 @@ rrg_status rrg_store_export(const rrg_store* s, uint64_t first, uint64_t count, 
   if (count > s->nsets || first > s->nsets - count) return invalid("export range out of bounds");
   return guarded([&]() -> rrg_status {
     rrg_graph* g = s->g;
+    if (s->ndense) {  // rows: materialized as lists (root first, then ascending)
+      auto* ms = const_cast<rrg_store*>(s);  // scratch only
+      const uint64_t tot = materialize(ms, first, count, g->stream);
+      d2h(offsets, s->xoff.ptr, count + 1, g->stream);
+      if (members) d2h(members, s->xmem.ptr, tot, g->stream);
+      sync(g);
+      return RRG_OK;
+    }
     std::vector<uint64_t> off(count + 1);
     d2h(off.data(), s->off.ptr + first, count + 1, g->stream);
     sync(g);
@@ -944,7 +1110,53 @@ rrg_status rrg_store_append_from(rrg_store* dst, const rrg_store* src, uint64_t 
                                cudaMemcpyDeviceToDevice, st));
     launch_rebase(src->off.ptr + first, count, dst->total, dst->off.ptr + dst->nsets,
                   dst->maxlen_dev.ptr, st);
+    // dense rows of the range: gathered into new rows of dst, dix rewritten
+    std::vector<uint32_t> dix(count, kNoRow);
+    if (src->ndense) {
+      d2h(dix.data(), src->dix.ptr + first, count, st);
+      sync(g);
+    }
+    std::vector<uint32_t> rows;
+    for (uint64_t i = 0; i < count; ++i)
+      if (dix[i] != kNoRow) rows.push_back(dix[i]);
+    const uint64_t rows0 = dst->ndense;
+    if (!rows.empty()) {
+      const uint64_t nr = rows.size();
+      std::vector<uint32_t> slen(src->ndense), sroot(src->ndense);
+      d2h(slen.data(), src->dlen.ptr, src->ndense, st);
+      d2h(sroot.data(), src->droot.ptr, src->ndense, st);
+      sync(g);
+      ensure_rows(dst, rows0 + nr);
+      std::vector<uint32_t> nlen(nr), nroot(nr), nslot(nr);
+      uint64_t j = 0;
+      for (uint64_t i = 0; i < count; ++i) {
+        if (dix[i] == kNoRow) continue;
+        nlen[j] = slen[dix[i]];
+        nroot[j] = sroot[dix[i]];
+        nslot[j] = static_cast<uint32_t>(dst->nsets + i);
+        dst->dense_members += nlen[j];
+        dst->dense_max = std::max(dst->dense_max, nlen[j]);
+        dix[i] = static_cast<uint32_t>(rows0 + j);
+        ++j;
+      }
+      dst->dreq.reserve_discard(nr);
+      RRG_CUDA(cudaMemcpyAsync(dst->dreq.ptr, rows.data(), nr * 4, cudaMemcpyHostToDevice, st));
+      launch_gather_rows(src->dbits.ptr, src->dwords, dst->dreq.ptr, nr, dst->dbits.ptr, rows0, st);
+      RRG_CUDA(cudaMemcpyAsync(dst->dlen.ptr + rows0, nlen.data(), nr * 4, cudaMemcpyHostToDevice, st));
+      RRG_CUDA(cudaMemcpyAsync(dst->droot.ptr + rows0, nroot.data(), nr * 4, cudaMemcpyHostToDevice,
+                               st));
+      RRG_CUDA(cudaMemcpyAsync(dst->dslot.ptr + rows0, nslot.data(), nr * 4, cudaMemcpyHostToDevice,
+                               st));
+      dst->ndense += nr;
+    }
+    if (dst->nsets + count > dst->dix.cap)
+      dst->dix.reserve_keep(std::max<uint64_t>(dst->nsets + count, dst->dix.cap + dst->dix.cap / 2),
+                            dst->nsets, st);
+    RRG_CUDA(cudaMemcpyAsync(dst->dix.ptr + dst->nsets, dix.data(), count * 4,
+                             cudaMemcpyHostToDevice, st));
     launch_recount(dst->off.ptr + dst->nsets, dst->mem.ptr, count, dst->counter.ptr, st);
+    launch_dense_colsum(dst->dbits.ptr, dst->dwords, g->n, nullptr, rows0, dst->ndense - rows0,
+                        dst->counter.ptr, +1, st);
     uint32_t mx = 0;
     d2h(&mx, dst->maxlen_dev.ptr, 1, st);
     sync(g);
@@ -986,11 +1198,12 @@ rrg_status rrg_store_import(rrg_store* s, uint64_t count, const uint64_t* offset
     RRG_CUDA(cudaMemcpyAsync(s->slot_start.ptr, start.data(), count * 8, cudaMemcpyHostToDevice,
                              st));
     RRG_CUDA(cudaMemcpyAsync(s->slot_len.ptr, len.data(), count * 4, cudaMemcpyHostToDevice, st));
-    const uint64_t nsets0 = s->nsets;
-    commit_staged(s, count);
+    const uint64_t nsets0 = s->nsets, rows0 = s->ndense;
+    reset_batch_rows(s, count);
+    // the reference's default representation switch (make_repr, rrr_set.hpp:73-90)
+    commit_staged(s, count, dense_threshold(g->n, 64));
     // fused counter over the imported sets only
-    s->scan.reserve_discard(1);
-    launch_recount(s->off.ptr + nsets0, s->mem.ptr, count, s->counter.ptr, st);
+    recount_into(s, nsets0, rows0, s->counter.ptr);
     sync(g);
     return RRG_OK;
   });
@@ -998,18 +1211,25 @@ rrg_status rrg_store_import(rrg_store* s, uint64_t count, const uint64_t* offset
 
 rrg_status rrg_store_export_all_async(const rrg_store* s, uint64_t* offsets, uint32_t* members,
                                       uint64_t* counts, void* stream) {
-  if (!s || !offsets || (s->total && !members)) return invalid("null argument");
+  if (!s || !offsets || (s->members() && !members)) return invalid("null argument");
   return guarded([&]() -> rrg_status {
     rrg_graph* g = s->g;
     const cudaStream_t cs = static_cast<cudaStream_t>(stream);
     auto* ms = const_cast<rrg_store*>(s);  // scratch only; the store's sets are unchanged
     // the copies follow everything already enqueued on the graph's stream
+    const uint64_t* off_src = s->off.ptr;
+    const uint32_t* mem_src = s->mem.ptr;
+    if (s->ndense) {  // rows materialized as lists on the graph's stream first
+      materialize(ms, 0, s->nsets, g->stream);
+      off_src = s->xoff.ptr;
+      mem_src = s->xmem.ptr;
+    }
     RRG_CUDA(cudaEventRecord(g->ev1, g->stream));
     RRG_CUDA(cudaStreamWaitEvent(cs, g->ev1, 0));
-    RRG_CUDA(cudaMemcpyAsync(offsets, s->off.ptr, (s->nsets + 1) * sizeof(uint64_t),
+    RRG_CUDA(cudaMemcpyAsync(offsets, off_src, (s->nsets + 1) * sizeof(uint64_t),
                              cudaMemcpyDeviceToHost, cs));
-    if (s->total)
-      RRG_CUDA(cudaMemcpyAsync(members, s->mem.ptr, s->total * sizeof(uint32_t),
+    if (s->members())
+      RRG_CUDA(cudaMemcpyAsync(members, mem_src, s->members() * sizeof(uint32_t),
                                cudaMemcpyDeviceToHost, cs));
     if (counts && g->n) {
       ms->wide.reserve_discard(g->n);

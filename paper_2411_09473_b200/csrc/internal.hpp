@@ -194,6 +194,32 @@ struct rrg_store {
   rrgpu::DevBuf<uint32_t> tdirty;          // selection: per-tile dirty flags
   rrgpu::DevBuf<uint64_t> span;            // selection (scan mode): member -> set span
   rrgpu::DevBuf<uint64_t> wide;  // u64 staging of counter exports
+  // ---- dense arm (rrr_set.hpp:10-13, :73-90; pack_sketch, sampling.hpp:68-84) ----
+  // A set of >= n / density_divisor members is a row of the n-bit map pool
+  // instead of a list: its list range in mem/off is EMPTY (a list set always
+  // holds its root), dix maps the set to its row. Rows of one batch are a
+  // contiguous range (allocation order within it is arbitrary).
+  uint32_t dwords = 0;                 // u32 words per row: ceil(n/32) rounded up to 4
+  uint64_t ndense = 0;                 // rows in use
+  uint64_t dense_members = 0;          // sum of the rows' member counts
+  uint32_t dense_max = 0;              // largest row
+  rrgpu::DevBuf<uint32_t> dbits;       // ndense x dwords
+  rrgpu::DevBuf<uint32_t> dlen;        // per row: member count
+  rrgpu::DevBuf<uint32_t> droot;       // per row: the set's root (RRRSet::root)
+  rrgpu::DevBuf<uint32_t> dslot;       // per row: its set index in the store
+  rrgpu::DevBuf<uint32_t> dix;         // per set: its row, or kNoRow (list set)
+  rrgpu::DevBuf<uint32_t> bdix;        // per batch slot: its row, or kNoRow
+  rrgpu::DevBuf<uint32_t> dreq;        // batch-local slots to convert at commit
+  rrgpu::DevBuf<unsigned long long> dctl;  // [0] rows requested [1] members [2] max
+  rrgpu::DevBuf<uint32_t> dcov;        // selection: per row, covered
+  rrgpu::DevBuf<uint32_t> dkill;       // selection: rows killed in the current round
+  rrgpu::DevBuf<uint32_t> dkn;         // selection: per round, rows killed
+  rrgpu::DevBuf<uint32_t> lcnt;        // selection (index mode): list-only counts
+  rrgpu::DevBuf<uint32_t> xlen;        // export: per set, its member count
+  rrgpu::DevBuf<uint64_t> xoff;        // export: materialized offsets
+  rrgpu::DevBuf<uint32_t> xmem;        // export: materialized members
+  uint64_t last_rebuilds = 0;          // rounds of the last select_seeds that rebuilt
+  uint64_t members() const { return total + dense_members; }
 };
 
 namespace rrgpu {
@@ -243,6 +269,17 @@ struct SampleParams {
   const uint8_t* dupfree;   // per vertex: in-list sources strictly increasing
   const uint8_t* uniformw;  // IC fast mode: per vertex, all in-weights equal
   uint32_t ic_coop_min;     // in-lists at least this long go warp-cooperative
+  // dense arm: the big-set path writes sets of >= dense_thr members as rows
+  uint32_t dense_thr;       // kNoDense: never
+  uint32_t dwords;
+  uint32_t* dbits;
+  uint32_t* dlen;
+  uint32_t* droot;
+  uint32_t* dslot;
+  uint32_t* bdix;           // per batch slot: its row (kNoRow: list)
+  uint64_t drow_base;       // first row of this batch
+  uint64_t drow_avail;      // rows allocated after drow_base
+  uint64_t set_base;        // store index of batch slot 0
 };
 
 // graph_dev.cu: device transpose (+ normalize_lt_weights) of an edge list on the
@@ -283,6 +320,43 @@ std::vector<uint64_t> segment_matrices(uint64_t seg, int count);  // jump.cpp
 std::vector<uint64_t> segment_tables(uint64_t seg, int count);    // jump.cpp (byte tables)
 uint64_t launches();  // kernels launched by this library so far (bench evidence)
 void count_launch(uint64_t k = 1);
+
+// ---- dense.cu ---------------------------------------------------------------
+constexpr uint32_t kNoRow = 0xffffffffu;
+constexpr uint32_t kNoDense = 0xffffffffu;
+// smallest member count with (double)len >= (double)n / divisor (make_repr's
+// switch, rrr_set.hpp:82-83); kNoDense when no set can be dense (divisor 0)
+uint32_t dense_threshold(uint32_t n, uint32_t divisor);
+// batch slots with slot_len >= thr -> dreq (count in dctl[0])
+void launch_dense_mark(const uint32_t* slot_len, uint64_t count, uint32_t thr, uint32_t* dreq,
+                       unsigned long long* dctl, cudaStream_t s);
+// the requested slots' staged lists -> rows [row0, row0 + nreq); their slot_len
+// becomes 0 (empty list range), bdix names the row; members/max into dctl[1..2]
+void launch_densify(const uint32_t* dreq, uint64_t nreq, const uint32_t* stage,
+                    const uint64_t* slot_start, uint32_t* slot_len, uint32_t* bdix, uint64_t row0,
+                    uint64_t set_base, uint32_t* dbits, uint32_t dwords, uint32_t* dlen,
+                    uint32_t* droot, uint32_t* dslot, unsigned long long* dctl, cudaStream_t s);
+// counter[v] += sign * #{rows r in [row0, row0 + nrows) with bit v} (rows given
+// directly, or through `rows` when not null); column sums, no per-member atomics
+void launch_dense_colsum(const uint32_t* dbits, uint32_t dwords, uint32_t n, const uint32_t* rows,
+                         uint64_t row0, uint64_t nrows, uint32_t* counter, int sign,
+                         cudaStream_t s);
+// per set of [first, first + count): its member count (list or row) -> xlen
+void launch_set_lengths(const uint64_t* off, const uint32_t* dix, const uint32_t* dlen,
+                        uint64_t first, uint64_t count, uint32_t* xlen, cudaStream_t s);
+// sets [first, first + count) as lists at xoff (relative): list sets copied,
+// rows decoded root first, then ascending
+void launch_materialize(const uint64_t* off, const uint32_t* mem, const uint32_t* dix,
+                        const uint32_t* dbits, uint32_t dwords, const uint32_t* droot,
+                        uint64_t first, uint64_t count, const uint64_t* xoff, uint32_t* xmem,
+                        cudaStream_t s);
+// fraction_covered over rows: rows holding a flagged vertex -> hits
+void launch_dense_fraction(const uint32_t* dbits, uint32_t dwords, uint64_t nrows,
+                           const uint32_t* seeds, uint32_t nseeds, unsigned long long* hits,
+                           cudaStream_t s);
+// gathers rows src_rows[i] of src into consecutive rows from dst_row0 of dst
+void launch_gather_rows(const uint32_t* src, uint32_t dwords, const uint32_t* src_rows,
+                        uint64_t nrows, uint32_t* dst, uint64_t dst_row0, cudaStream_t s);
 
 // ---- store.cu ---------------------------------------------------------------
 // out[i] = sum_{t<i} in[t] for i in [0, count]; tmp grows as needed.
@@ -328,6 +402,15 @@ struct SelectParams {
   uint32_t* dirty;     // per tile: a count in it changed this round
   int scan;            // 1: find the sets holding v by scanning the flat members
                        // (no inverted index); 0: inverted index ioff/inv
+  // dense arm: rows of the n-bit map pool (their list ranges are empty)
+  uint64_t nd;                 // rows
+  uint32_t dwords;
+  const uint32_t* dbits;
+  uint32_t* dcov;              // per row: covered
+  uint32_t* dkill;             // rows killed this round (kill order)
+  uint32_t* dkn;               // per round: rows killed
+  double adaptive_threshold;   // rebuild_update when top_count / live exceeds it
+  unsigned long long* rebuilds;  // rounds that rebuilt (stats)
 };
 constexpr uint32_t kSelTileLog = 11;  // 2048 vertices per argmax tile
 void launch_select(const SelectParams& p, int num_sms, cudaStream_t s);

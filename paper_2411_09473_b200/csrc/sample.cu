@@ -149,6 +149,48 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
       }
     }
     nmem = __shfl_sync(kFull, nmem, 0);
+    if (nmem >= p.dense_thr) {
+      // dense arm (pack_sketch, sampling.hpp:78-83): the visited map IS the
+      // set's n-bit map -- copied into a row of the pool and cleared in the same
+      // pass; the members only feed the fused counter
+      unsigned long long row = 0;
+      if (lane == 0) row = atomicAdd(&p.ctl->ndense, 1ull);
+      row = __shfl_sync(kFull, row, 0);
+      __syncwarp();
+      if (row < p.drow_avail) {
+        const uint64_t grow = p.drow_base + row;
+        uint32_t* dst = p.dbits + grow * p.dwords;
+        for (uint32_t wd = lane; wd < p.dwords; wd += 32) {
+          uint32_t x = 0;
+          if (wd < words) {
+            x = vis[wd];
+            vis[wd] = 0u;
+          }
+          dst[wd] = x;
+        }
+        if (p.counter)
+          for (uint32_t i = lane; i < nmem; i += 32) atomicAdd(p.counter + mem[i], 1u);
+        if (lane == 0) {
+          p.dlen[grow] = nmem;
+          p.droot[grow] = root;
+          p.dslot[grow] = static_cast<uint32_t>(p.set_base + idx);
+          p.bdix[idx] = static_cast<uint32_t>(grow);
+          p.slot_start[idx] = 0;
+          p.slot_len[idx] = 0;  // empty list range
+          atomicAdd(&p.ctl->dense_members, (unsigned long long)nmem);
+          atomicMax(&p.ctl->dense_max, nmem);
+          insp += sinsp;
+        }
+      } else {
+        if (lane == 0) restage_slot(p, idx, 0);  // the row pool grows, then a re-run
+        for (uint32_t i = lane; i < nmem; i += 32) {
+          const uint32_t v = mem[i];
+          atomicAnd(vis + (v >> 5), ~(1u << (v & 31)));
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     unsigned long long pos = 0;
     if (lane == 0) pos = atomicAdd(&p.ctl->cursor, (unsigned long long)nmem);
     pos = __shfl_sync(kFull, pos, 0);

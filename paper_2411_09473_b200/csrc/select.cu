@@ -6,7 +6,11 @@
 // are done. The argmax is incremental: the vertices are cut into tiles of
 // 2^kSelTileLog, each with its max packed key (count << 32 | ~v: max count wins,
 // ties go to the lowest id -- the reference's rule, :113, :119-120), and a round
-// only re-reduces the tiles whose counts changed. A round:
+// only re-reduces the tiles whose counts changed. Sets of the dense arm (n-bit
+// rows, dense.cu) are found by one bit test each and their counts move by
+// column sums; a round whose seed covers more than adaptive_threshold of the
+// live sets rebuilds the counter from the survivors instead (rebuild_update,
+// selection.hpp:161-203, chosen as at :226-231). A round:
 //   A) every block reduces the tile maxima (a few KB, L2) to the same key, so
 //      the argmax needs no grid barrier of its own;
 //   B) cover: each live set holding v is claimed once (atomicExch on its
@@ -94,6 +98,47 @@ __device__ __forceinline__ void warp_cover(const SelectParams& p, uint64_t s) {
   }
 }
 
+// Column sums over rows of the dense arm, thread per (word, 32-row chunk): the
+// rows' words are added into bit-sliced planes and each vertex of the word
+// gets one atomic with its count. sign < 0: covered rows (rows = the round's
+// kill list), flags the tiles; sign > 0: the live rows (rebuild recount).
+__device__ __forceinline__ void sel_colsum(const SelectParams& p, const uint32_t* rows,
+                                           uint64_t nrows, int sign, uint64_t tid,
+                                           uint64_t nthreads) {
+  const uint64_t nchunks = (nrows + 31) / 32;
+  const uint64_t items = nchunks * p.dwords;
+  for (uint64_t it = tid; it < items; it += nthreads) {
+    const uint64_t c = it / p.dwords;
+    const uint32_t w = static_cast<uint32_t>(it - c * p.dwords);
+    if (static_cast<uint64_t>(w) * 32 >= p.n) continue;
+    uint32_t pl[6] = {0, 0, 0, 0, 0, 0};
+    const uint64_t d1 = c * 32 + 32 < nrows ? c * 32 + 32 : nrows;
+    for (uint64_t d = c * 32; d < d1; ++d) {
+      uint64_t row = d;
+      if (rows) row = rows[d];
+      else if (p.dcov[d]) continue;  // covered rows do not count in a rebuild
+      uint32_t x = p.dbits[row * p.dwords + w];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const uint32_t cy = pl[i] & x;
+        pl[i] ^= x;
+        x = cy;
+      }
+    }
+    uint32_t any = pl[0] | pl[1] | pl[2] | pl[3] | pl[4] | pl[5];
+    if (any && sign < 0) p.dirty[(w * 32) >> kSelTileLog] = 1u;
+    while (any) {
+      const int b = __ffs(any) - 1;
+      any &= any - 1;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) cnt |= ((pl[i] >> b) & 1u) << i;
+      if (sign < 0) atomicSub(p.cnt + w * 32 + b, cnt);
+      else atomicAdd(p.cnt + w * 32 + b, cnt);
+    }
+  }
+}
+
 template <bool kScan>
 __global__ void __launch_bounds__(kSelBlock, 1) k_select(const SelectParams p) {
   cg::grid_group grid = cg::this_grid();
@@ -114,6 +159,7 @@ __global__ void __launch_bounds__(kSelBlock, 1) k_select(const SelectParams p) {
   }
   grid.sync();
 
+  unsigned long long covered_sum = 0;  // sets covered in earlier rounds (every thread)
   for (uint32_t r = 0; r < p.k; ++r) {
     // ---- A: argmax over the tile maxima (every block, same answer) ---------
     unsigned long long best = 0;
@@ -138,9 +184,37 @@ __global__ void __launch_bounds__(kSelBlock, 1) k_select(const SelectParams p) {
       return;  // uniform: every block computed the same key
     }
 
+    // rebuild_update vs decrement_update (selection.hpp:226-231): the same rule,
+    // the same counts either way (test_selection.cpp:116-137)
+    const unsigned long long live = p.nsets - covered_sum;
+    const bool rebuild = live > 0 && static_cast<double>(top) / static_cast<double>(live) >
+                                         p.adaptive_threshold;
+
     // ---- B: cover the live sets holding v ------------------------------------
     unsigned long long killed = 0;
-    if (kScan) {
+    if (rebuild) {
+      // kill only; the survivors are recounted below
+      if (kScan) {
+        const uint64_t nchunk = (p.total + 255) / 256;
+        for (uint64_t c = gwarp; c < nchunk; c += nwarps) {
+          const uint64_t base = c * 256 + static_cast<uint64_t>(lane) * 8;
+          for (int j = 0; j < 8; ++j) {
+            const uint64_t t = base + j;
+            if (t >= p.total || p.wmem[t] != v) continue;
+            ++killed;
+            const uint64_t w = p.span[t];
+            const uint64_t sb = w >> 32, se = sb + (w & 0xffffffffull);
+            for (uint64_t q = sb; q < se; ++q) p.wmem[q] = kBlank;
+          }
+        }
+      } else {
+        const uint64_t ib = p.ioff[v], ie = p.ioff[v + 1];
+        for (uint64_t t = ib + tid; t < ie; t += nthreads) {
+          const uint32_t s = p.inv[t];
+          if (!atomicExch(p.covered + s, 1u)) ++killed;
+        }
+      }
+    } else if (kScan) {
       // warp w scans members [256 w', 256 w' + 256) of the working copy for v,
       // eight per lane. Covered sets are blanked there, so every match is a live
       // set, found by exactly one lane: no claim needed; that warp decrements and
@@ -223,14 +297,49 @@ __global__ void __launch_bounds__(kSelBlock, 1) k_select(const SelectParams p) {
         warp_cover(p, s);
       }
     }
+    // dense rows holding v: a bit test each; the round's kills are listed
+    for (uint64_t d = tid; d < p.nd; d += nthreads) {
+      if (p.dcov[d]) continue;
+      if (!((p.dbits[d * p.dwords + (v >> 5)] >> (v & 31)) & 1u)) continue;
+      p.dcov[d] = 1u;
+      ++killed;
+      p.dkill[atomicAdd(p.dkn + r, 1u)] = static_cast<uint32_t>(d);
+    }
     for (int o = 16; o; o >>= 1) killed += __shfl_xor_sync(kFull, killed, o);
     if (lane == 0 && killed) atomicAdd(p.marg + r, killed);
     if (tid == 0) {
       p.keys[r] = key;
       p.seeds[r] = v;
       p.selected[v] = 1;
+      if (rebuild) atomicAdd(p.rebuilds, 1ull);
     }
     grid.sync();
+    covered_sum += p.marg[r];
+
+    // ---- C0: the counts of the dense rows / the rebuild ----------------------
+    if (rebuild) {
+      for (uint64_t u = tid; u < p.n; u += nthreads) p.cnt[u] = 0u;
+      grid.sync();
+      sel_colsum(p, nullptr, p.nd, +1, tid, nthreads);  // live rows
+      if (kScan) {  // live list sets: the non-blanked entries of the working copy
+        for (uint64_t t = tid; t < p.total; t += nthreads) {
+          const uint32_t u = p.wmem[t];
+          if (u != kBlank) atomicAdd(p.cnt + u, 1u);
+        }
+      } else {
+        for (uint64_t s = gwarp; s < p.nsets; s += nwarps) {
+          if (p.covered[s]) continue;
+          for (uint64_t t = p.off[s] + lane; t < p.off[s + 1]; t += 32) atomicAdd(p.cnt + p.mem[t], 1u);
+        }
+      }
+      grid.sync();
+    } else {
+      const uint32_t ndk = p.dkn[r];
+      if (ndk) {
+        sel_colsum(p, p.dkill, ndk, -1, tid, nthreads);
+        grid.sync();
+      }
+    }
 
     // ---- C: re-reduce the tiles whose counts changed -------------------------
     if (p.snap) {
@@ -238,7 +347,7 @@ __global__ void __launch_bounds__(kSelBlock, 1) k_select(const SelectParams p) {
       for (uint64_t u = tid; u < p.n; u += nthreads) out[u] = p.cnt[u];
     }
     for (uint64_t t = gwarp; t < ntiles; t += nwarps) {
-      if (ntiles > kAllTilesMax && !p.dirty[t]) continue;  // uniform in the warp
+      if (!rebuild && ntiles > kAllTilesMax && !p.dirty[t]) continue;  // uniform in the warp
       const unsigned long long m = tile_max_warp(p, static_cast<uint32_t>(t));
       if (lane == 0) {
         p.tmax[t] = m;

@@ -1,0 +1,217 @@
+"""The dense arm of the store: sets of >= n / density_divisor
+members held as n-bit maps (make_repr / pack_sketch, rrr_set.hpp:73-90,
+sampling.hpp:68-84) and the rebuild-style counter update (rebuild_update,
+selection.hpp:161-203, chosen by adaptive_threshold as at :226-231).
+
+Every check is against the reference (oracle/_ref when built, else the port):
+the sets themselves, the fused counter, seeds / marginals / per-round counter
+snapshots under both update strategies, fraction_covered, store appends and
+imports, and run_imm on a correlated-degree cfg3 (the giant-set regime)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2411_09473_b200 as P
+from paper_2411_09473_b200 import graphs
+from helpers import assert_sets_equal
+
+pytestmark = pytest.mark.gpu
+
+IC, LT = 0, 1
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def supercritical(n=20000, m=200000, lo=0.1, hi=0.45, seed=11):
+    """IC with giant sets: many sets well past n/64 (dense), some small ones."""
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    keep = src != dst
+    w = rng.uniform(lo, hi, keep.sum()).astype(np.float32)
+    return P.build_graph(n, src[keep], dst[keep], w)
+
+
+def cfg3c_scaled(n=60000, m=1_100_000):
+    return graphs.generate(graphs.scaled(graphs.CONFIGS["cfg3c"], n, m))
+
+
+def sample(arrays, model, seed, count, divisor=64, **opts):
+    g = P.Graph(*arrays)
+    for k, v in opts.items():
+        g.set_option(k, v)
+    st = P.RRRStore(g)
+    P.generate_batch(g, model, seed, count, st, density_divisor=divisor)
+    return g, st
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3])
+def test_dense_sets_equal_reference(cuda, oracle, mode):
+    """Sets of every schedule (lane / warp / block lists converted at commit,
+    big-set path rows written from its visited map) equal the reference's."""
+    arrays = supercritical()
+    n = arrays[0].size - 1
+    g, st = sample(arrays, IC, 17, 300, ic_mode=mode)
+    info = st.dense_info()
+    assert info["dense_sets"] > 50, info
+    off, mem = st.export()
+    ref = oracle.graph(*arrays).sample(IC, 17, 0, 300, workers=8)
+    sizes = np.diff(ref.offsets.astype(np.int64))
+    assert info["dense_sets"] == int((sizes >= -(-n // 64)).sum())
+    assert info["dense_members"] == int(sizes[sizes >= -(-n // 64)].sum())
+    assert info["dense_bytes"] == info["dense_sets"] * ((((n + 31) // 32) + 3) // 4 * 4) * 4
+    assert_sets_equal(off, mem, ref)
+    assert (st.counter() == ref.counter).all()
+    assert st.total_member_count() == int(ref.offsets[-1])
+    assert st.max_set_size() == int(sizes.max())
+    # a dense set exports root first, then ascending
+    big = int(np.argmax(sizes))
+    s = mem[off[big]:off[big + 1]]
+    assert s[0] == ref.roots[big] and (np.diff(s[1:].astype(np.int64)) > 0).all()
+
+
+def test_density_divisor_changes_no_output(cuda):
+    arrays = supercritical(seed=3)
+    outs = []
+    for div in (0, 64, 4096, 1 << 30):
+        g, st = sample(arrays, IC, 5, 200, divisor=div)
+        info = st.dense_info()
+        if div == 0:
+            assert info["dense_sets"] == 0
+        if div == 1 << 30:
+            assert info["dense_sets"] == 200  # n / divisor < 1: every set is a row
+        off, mem = st.export()
+        sets = [np.sort(mem[off[i]:off[i + 1]]) for i in range(200)]
+        sel = P.select_seeds(st, arrays[0].size - 1, 12, capture_round_counters=True)
+        outs.append((sets, st.counter(), sel))
+    for sets, cnt, sel in outs[1:]:
+        assert all(np.array_equal(a, b) for a, b in zip(sets, outs[0][0]))
+        assert (cnt == outs[0][1]).all()
+        assert sel.seeds == outs[0][2].seeds and sel.marginal_counts == outs[0][2].marginal_counts
+        assert (sel.round_counters == outs[0][2].round_counters).all()
+
+
+@pytest.mark.parametrize("index", [False, True])
+@pytest.mark.parametrize("threshold", [0.0, 0.25, 2.0])
+def test_selection_over_dense_rows(cuda, oracle, monkeypatch, index, threshold):
+    """Decrement (threshold 2: never rebuild), the reference's rule (0.25) and
+    rebuild every round (0): the same seeds, marginals and per-round counter
+    snapshots as the reference's select_seeds on the same collection."""
+    if index:
+        monkeypatch.setenv("RRGPU_SELECT_INDEX", "1")
+    arrays = supercritical(seed=7)
+    n = arrays[0].size - 1
+    g, st = sample(arrays, IC, 9, 400)
+    assert st.dense_info()["dense_sets"] > 0
+    off, mem = st.export()
+    k = 25
+    seeds, marg, rc = oracle.select(n, off, mem, k, threshold=threshold, capture=True)
+    s = P.select_seeds(st, n, k, adaptive_threshold=threshold, capture_round_counters=True)
+    assert s.seeds == seeds and s.marginal_counts == marg
+    assert (s.round_counters == rc).all()
+    rebuilds = st.dense_info()["rebuild_rounds"]
+    if threshold == 0.0:
+        assert rebuilds == len([m for m in marg if m])
+    if threshold == 2.0:
+        assert rebuilds == 0
+    if threshold == 0.25:
+        assert rebuilds >= 1  # the first seed covers the giant sets
+
+
+def test_fraction_covered_with_dense_rows(cuda):
+    arrays = supercritical(seed=13)
+    g, st = sample(arrays, IC, 2, 300)
+    off, mem = st.export()
+    rng = np.random.default_rng(1)
+    for seeds in ([0], rng.choice(arrays[0].size - 1, 7, replace=False).tolist(), []):
+        want = np.mean([bool(np.isin(seeds, mem[off[i]:off[i + 1]]).any()) for i in range(300)])
+        assert P.fraction_covered(st, seeds) == pytest.approx(want, abs=0)
+
+
+def test_append_from_and_import_keep_dense_rows(cuda, oracle):
+    arrays = supercritical(seed=21)
+    n = arrays[0].size - 1
+    g = P.Graph(*arrays)
+    side = P.RRRStore(g)
+    P.generate_batch(g, IC, 4, 500, side)
+    main = P.RRRStore(g)
+    main.append_from(side, 0, 120)
+    main.append_from(side, 120, 380)
+    direct = P.RRRStore(g)
+    P.generate_batch(g, IC, 4, 500, direct)
+    o1, m1 = main.export()
+    o2, m2 = direct.export()
+    assert (o1 == o2).all() and (m1 == m2).all()
+    assert (main.counter() == direct.counter()).all()
+    assert main.dense_info()["dense_sets"] == direct.dense_info()["dense_sets"] > 0
+    imp = P.RRRStore(g)
+    imp.import_sets(o2, m2)
+    assert imp.dense_info()["dense_sets"] == direct.dense_info()["dense_sets"]
+    o3, m3 = imp.export()
+    sets3 = [np.sort(m3[o3[i]:o3[i + 1]]) for i in range(500)]
+    sets2 = [np.sort(m2[o2[i]:o2[i + 1]]) for i in range(500)]
+    assert all(np.array_equal(a, b) for a, b in zip(sets3, sets2))
+    assert (imp.counter() == direct.counter()).all()
+    a = P.select_seeds(imp, n, 10)
+    b = P.select_seeds(direct, n, 10)
+    assert a.seeds == b.seeds and a.marginal_counts == b.marginal_counts
+
+
+def test_lt_long_walks_become_rows(cuda, oracle):
+    """LT walks past n / 64 members (a weight-1 chain) through the guide walk,
+    the linear scan and the big-set path."""
+    n = 3000
+    dst = np.arange(n - 1, dtype=np.uint32)
+    src = dst + 1
+    roff, rsrc, rw = P.build_graph(n, src, dst, np.ones(n - 1, np.float32))
+    P.normalize_lt_weights(roff, rw)
+    arrays = (roff, rsrc, rw)
+    ref = oracle.graph(*arrays).sample(LT, 3, 0, 800, workers=4)
+    for scan in (0, 2):
+        g, st = sample(arrays, LT, 3, 800, lt_scan=scan)
+        assert st.dense_info()["dense_sets"] > 100
+        off, mem = st.export()
+        assert_sets_equal(off, mem, ref)
+        assert (st.counter() == ref.counter).all()
+
+
+def test_imm_cfg3_correlated_scaled(cuda, oracle):
+    """run_imm on a scaled correlated-degree cfg3 (giant sets, most rounds'
+    first seed covers > 25 % of the sets: rebuilds) vs the reference's."""
+    arrays = cfg3c_scaled()
+    g = P.Graph(*arrays)
+    res = P.run_imm(g, P.ImmConfig(k=20, epsilon=0.5, model=IC, rng_seed=1))
+    ref = oracle.graph(*arrays).imm(k=20, epsilon=0.5, model=IC, workers=os.cpu_count() or 8,
+                                    rng_seed=1)
+    assert res.seeds.seeds == ref["seeds"]
+    assert res.seeds.marginal_counts == ref["marginals"]
+    assert (res.theta, res.theta_prime, res.lower_bound) == \
+        (ref["theta"], ref["theta_prime"], ref["lower_bound"])
+    assert res.sets_generated == ref["sets_generated"]
+    assert res.mean_set_size == ref["mean_set_size"]
+    assert res.max_set_size == ref["max_set_size"]
+
+
+def test_imm_cfg3_correlated_full_size(cuda):
+    """Full-size cfg3c (1.63M vertices, 30.6M arcs, correlated degrees; ~1/3 of
+    the sets are giant) against the golden run_imm the reference computed in the
+    build container (tests/golden/make_imm_full.py)."""
+    path = os.path.join(HERE, "golden", "imm_full_cfg3c.json")
+    if not os.path.exists(path):
+        pytest.skip("golden not generated")
+    with open(path) as f:
+        gold = json.load(f)
+    cfg = graphs.CONFIGS["cfg3c"]
+    arrays = graphs.generate(cfg)
+    assert arrays[0].size - 1 == gold["n"] and arrays[1].size == gold["arcs"]
+    g = P.Graph(*arrays)
+    res = P.run_imm(g, P.ImmConfig(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model, rng_seed=1))
+    ref = gold["result"]
+    assert res.seeds.seeds == ref["seeds"]
+    assert res.seeds.marginal_counts == ref["marginals"]
+    assert (res.theta, res.theta_prime, res.lower_bound) == \
+        (ref["theta"], ref["theta_prime"], ref["lower_bound"])
+    assert res.sets_generated == ref["sets_generated"]
+    assert res.mean_set_size == ref["mean_set_size"]
+    assert res.max_set_size == ref["max_set_size"]
