@@ -860,6 +860,20 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       }
       if (ndef) {
         acc.deferred += ndef;
+        // the big-set path's sets are the largest of the batch: reserve a row for
+        // each when they are dense-sized (bounded by a quarter of the free memory;
+        // a slot that finds no row is re-run after the pool grows)
+        if (dense_thr != kNoDense && dense_thr <= static_cast<uint32_t>(block) * kMemCap) {
+          size_t free_b = 0, total_b = 0;
+          RRG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+          const uint64_t fit = free_b / 4 / (static_cast<uint64_t>(s->dwords) * 4 + 16);
+          const uint64_t want = std::min<uint64_t>(ndef, fit);
+          if (drow_avail - ctl.ndense < want) {
+            ensure_rows(s, s->ndense + ctl.ndense + want, s->ndense + ctl.ndense);
+            drow_avail = rows_cap(s) - s->ndense;
+            set_rows();
+          }
+        }
         pass(kBig, dlist, ndef, s->bigre.ptr);
       }
       acc.edges_inspected += ctl.inspected;
