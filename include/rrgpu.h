@@ -98,6 +98,21 @@ rrg_status rrg_store_clear(rrg_store* s);
 rrg_status rrg_store_info(const rrg_store* s, uint64_t* sets, uint64_t* members,
                           uint32_t* max_set_size);
 
+/* RRRStore::live_count (rrr_store.hpp:84): sets not covered by the last
+ * rrg_select_seeds (the store stays tombstoned, imm.hpp:194-195); every append
+ * (generate_batch, import, append_from) revives all sets, as finalize does. */
+rrg_status rrg_store_live_count(const rrg_store* s, uint64_t* live);
+/* RRRStore::is_live (rrr_store.hpp:62) for sets [first, first+count): out u8[count]. */
+rrg_status rrg_store_live_flags(const rrg_store* s, uint64_t first, uint64_t count, uint8_t* out);
+/* Replaces the store's occurrence counter with a caller-held tally u64[n] (each
+ * < 2^32): the `prebuilt` Counter of select_seeds (selection.hpp:209-218). */
+rrg_status rrg_store_set_counter(rrg_store* s, const uint64_t* counts);
+/* A budget for the store: a batch chunk that would take it past max_members
+ * members fails with RRG_ENOMEM; the sets of earlier chunks stay, the fused
+ * counter matches them, *sets_generated counts them (BatchOutOfMemory,
+ * sampling.hpp:148-154). 0: no limit (device allocation failures behave alike). */
+rrg_status rrg_store_set_member_limit(rrg_store* s, uint64_t max_members);
+
 /* The dense arm (rrr_set.hpp:10-13, :73-90): sets of >= n / density_divisor
  * members are held as n-bit maps (rows), the rest as id lists. *dense_sets rows
  * holding *dense_members members in *dense_bytes of HBM; *rebuild_rounds = rounds

@@ -9,6 +9,7 @@
 // Header-only; link with librrgpu.so.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -99,6 +100,18 @@ class RRRStore {
     check(rrg_store_export(h_.get(), idx, 1, off, out.data()));
     return out;
   }
+  // rrr_store.hpp:84: sets the last select_seeds left uncovered (appends revive all)
+  uint64_t live_count() const {
+    uint64_t x = 0;
+    check(rrg_store_live_count(h_.get(), &x));
+    return x;
+  }
+  // rrr_store.hpp:62
+  bool is_live(uint64_t idx) const {
+    uint8_t f = 0;
+    check(rrg_store_live_flags(h_.get(), idx, 1, &f));
+    return f != 0;
+  }
   // Counter::get for every vertex (counter.hpp:29)
   std::vector<uint64_t> counter() const {
     std::vector<uint64_t> out(n_);
@@ -125,6 +138,72 @@ inline void generate_batch(const Graph& g, DiffusionModel model, uint64_t run_se
         made);
 }
 
+// work_pool.hpp: the device's persistent grids replace the fork-join pool; a
+// WorkPool keeps the reference's signatures and its worker-count contract.
+class WorkPool {
+ public:
+  explicit WorkPool(unsigned workers = 1) : workers_(workers) {
+    if (workers < 1) throw std::invalid_argument("WorkPool: workers must be >= 1");
+  }
+  unsigned workers() const { return workers_; }
+
+ private:
+  unsigned workers_;
+};
+
+// counter.hpp:15-62: a caller-owned per-vertex tally (host values).
+class Counter {
+ public:
+  explicit Counter(uint32_t n) : c_(n, 0) {}
+  uint32_t size() const { return static_cast<uint32_t>(c_.size()); }
+  uint64_t get(uint32_t v) const { return c_.at(v); }
+  void add(uint32_t v, uint64_t d = 1) { c_.at(v) += d; }
+  void sub(uint32_t v, uint64_t d = 1) { c_.at(v) -= d; }
+  void zero() { std::fill(c_.begin(), c_.end(), 0); }
+  Counter clone() const { return *this; }
+  const std::vector<uint64_t>& values() const { return c_; }
+  std::vector<uint64_t>& values() { return c_; }
+
+ private:
+  std::vector<uint64_t> c_;
+};
+
+// sampling.hpp:159-199 with the reference's signature: counter == nullptr samples
+// unfused; otherwise every member of the new sets is added to *counter (the
+// store's fused tally grows by exactly those counts on the device).
+inline void generate_batch(const Graph& g, DiffusionModel model, uint64_t run_seed,
+                           uint64_t count, WorkPool& /*pool*/, RRRStore& store, Counter* counter,
+                           uint32_t density_divisor = 64) {
+  if (counter && counter->size() != g.num_vertices())
+    throw std::invalid_argument("generate_batch: counter size != vertex count");
+  std::vector<uint64_t> before;
+  if (counter) before = store.counter();
+  uint64_t made = 0;
+  const rrg_status st = rrg_generate_batch(g.handle(), to_c(model), run_seed, count,
+                                           store.handle(), counter ? 1 : 0, density_divisor,
+                                           &made);
+  if (counter) {  // also on BatchOutOfMemory: the sets that made it in are counted
+    const std::vector<uint64_t> after = store.counter();
+    for (size_t v = 0; v < after.size(); ++v) counter->values()[v] += after[v] - before[v];
+  }
+  check(st, made);
+}
+
+// sampling.hpp:201-206
+inline void generate_batch_fused(const Graph& g, DiffusionModel model, uint64_t run_seed,
+                                 uint64_t count, Counter& counter, WorkPool& pool,
+                                 RRRStore& store, uint32_t density_divisor = 64) {
+  generate_batch(g, model, run_seed, count, pool, store, &counter, density_divisor);
+}
+
+// selection.hpp:45-49. touches (the reference's CPU touch tally) has no device
+// counterpart and stays 0; the per-round counter snapshots are exact.
+struct SelectionStats {
+  uint64_t touches = 0;
+  bool capture_round_counters = false;
+  std::vector<std::vector<uint64_t>> round_counters;
+};
+
 // selection.hpp:19-22
 struct SeedSet {
   std::vector<uint32_t> seeds;
@@ -142,6 +221,34 @@ inline SeedSet select_seeds(RRRStore& store, uint32_t n, uint32_t k,
   check(rrg_select_seeds(store.handle(), k, adaptive_threshold, prebuilt ? 1 : 0,
                          out.seeds.data(), out.marginal_counts.data(), nullptr, nullptr,
                          nullptr));
+  return out;
+}
+
+// selection.hpp:209-243 with the reference's signature: prebuilt == nullptr
+// recounts the store (build_counter, :79-95), else *prebuilt is the starting tally.
+inline SeedSet select_seeds(RRRStore& store, uint32_t n, uint32_t k, WorkPool& /*pool*/,
+                            double adaptive_threshold = 0.25, const Counter* prebuilt = nullptr,
+                            SelectionStats* stats = nullptr) {
+  if (k < 1) throw std::invalid_argument("select_seeds: k must be >= 1");
+  if (k > n) throw std::invalid_argument("select_seeds: k exceeds vertex count");
+  if (prebuilt) {
+    if (prebuilt->size() != n) throw std::invalid_argument("select_seeds: prebuilt size != n");
+    check(rrg_store_set_counter(store.handle(), prebuilt->values().data()));
+  }
+  SeedSet out;
+  out.seeds.resize(k);
+  out.marginal_counts.resize(k);
+  const bool capture = stats && stats->capture_round_counters;
+  std::vector<uint64_t> snaps(capture ? static_cast<size_t>(k) * n : 0);
+  uint32_t rounds = 0;
+  check(rrg_select_seeds(store.handle(), k, adaptive_threshold, prebuilt ? 1 : 0,
+                         out.seeds.data(), out.marginal_counts.data(),
+                         capture ? snaps.data() : nullptr, &rounds, nullptr));
+  if (capture) {
+    for (uint32_t r = 0; r < rounds; ++r)
+      stats->round_counters.emplace_back(snaps.begin() + static_cast<size_t>(r) * n,
+                                         snaps.begin() + static_cast<size_t>(r + 1) * n);
+  }
   return out;
 }
 

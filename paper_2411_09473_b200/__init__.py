@@ -30,7 +30,7 @@ __all__ = [
     "DiffusionModel", "Graph", "RRRStore", "SeedSet", "ImmConfig", "ImmResult",
     "generate_batch", "generate_batch_fused", "select_seeds", "fraction_covered",
     "run_imm", "build_graph", "normalize_lt_weights", "RRGError", "RRGOutOfMemory",
-    "version", "BatchStats",
+    "version", "BatchStats", "SelectionStats",
 ]
 
 kDefaultDensityDivisor = 64  # rrr_set.hpp:13
@@ -221,6 +221,32 @@ class RRRStore:
         check(lib.rrg_store_info(self._h, None, None, C.byref(x)))
         return x.value
 
+    def live_count(self) -> int:
+        """RRRStore::live_count (rrr_store.hpp:84): sets the last select_seeds left
+        uncovered; every append revives all sets (finalize)."""
+        x = C.c_uint64()
+        check(lib.rrg_store_live_count(self._h, C.byref(x)))
+        return x.value
+
+    def live_flags(self, first: int = 0, count: Optional[int] = None) -> np.ndarray:
+        """RRRStore::is_live (rrr_store.hpp:62) for sets [first, first+count)."""
+        if count is None:
+            count = self.size() - first
+        out = np.zeros(max(count, 1), dtype=np.uint8)
+        check(lib.rrg_store_live_flags(self._h, first, count, ptr(out, C.c_uint8)))
+        return out[:count].astype(bool)
+
+    def set_counter(self, counts) -> None:
+        """A caller-held tally becomes the prebuilt Counter of select_seeds."""
+        c = np.ascontiguousarray(counts, dtype=np.uint64)
+        if c.size != self.graph.num_vertices:
+            raise ValueError("set_counter: need one count per vertex")
+        check(lib.rrg_store_set_counter(self._h, ptr(c, C.c_uint64)))
+
+    def set_member_limit(self, max_members: int) -> None:
+        """RRG_ENOMEM (RRGOutOfMemory) for a batch chunk past max_members (0: none)."""
+        check(lib.rrg_store_set_member_limit(self._h, int(max_members)))
+
     def dense_info(self) -> dict:
         """The dense arm (rrr_set.hpp:73-90): n-bit map rows, their members and
         bytes, and the rebuild rounds of the last select_seeds on this store."""
@@ -351,9 +377,28 @@ class SeedSet:
     covered: int = 0
 
 
+@dataclass
+class SelectionStats:
+    """selection.hpp:45-49. touches (the reference's CPU touch tally) has no
+    device counterpart and stays 0; rebuild_rounds counts the rounds that took
+    rebuild_update (selection.hpp:161-203)."""
+    touches: int = 0
+    capture_round_counters: bool = False
+    round_counters: Optional[np.ndarray] = None
+    rebuild_rounds: int = 0
+
+
 def select_seeds(store: RRRStore, n: int, k: int, adaptive_threshold: float = 0.25,
-                 prebuilt: bool = True, capture_round_counters: bool = False) -> SeedSet:
-    """selection.hpp:209-243 (k rounds resident on the GPU)."""
+                 prebuilt=True, capture_round_counters: bool = False,
+                 stats: Optional[SelectionStats] = None) -> SeedSet:
+    """selection.hpp:209-243 (k rounds resident on the GPU). prebuilt: True = the
+    store's fused counter, False = recount (build_counter), or a per-vertex
+    array = the caller's Counter as the starting tally."""
+    if not isinstance(prebuilt, bool):
+        store.set_counter(prebuilt)
+        prebuilt = True
+    if stats is not None and stats.capture_round_counters:
+        capture_round_counters = True
     if n != store.graph.num_vertices:
         raise ValueError("select_seeds: n does not match the store's graph")
     if k < 1:
@@ -369,6 +414,9 @@ def select_seeds(store: RRRStore, n: int, k: int, adaptive_threshold: float = 0.
                                ptr(seeds, C.c_uint32), ptr(marg, C.c_uint64),
                                ptr(snap, C.c_uint64), C.byref(rounds), C.byref(covered)))
     rc = snap.reshape(k, n)[: rounds.value] if snap is not None else None
+    if stats is not None:
+        stats.round_counters = rc
+        stats.rebuild_rounds = store.dense_info()["rebuild_rounds"]
     return SeedSet([int(x) for x in seeds], [int(x) for x in marg], rc, covered.value)
 
 

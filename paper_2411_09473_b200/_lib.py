@@ -77,6 +77,10 @@ SIGNATURES = [
     ("rrg_store_destroy", None, [vp]),
     ("rrg_store_clear", C.c_int, [vp]),
     ("rrg_store_dense_info", C.c_int, [vp, u64p, u64p, u64p, u64p]),
+    ("rrg_store_live_count", C.c_int, [vp, u64p]),
+    ("rrg_store_live_flags", C.c_int, [vp, C.c_uint64, C.c_uint64, u8p]),
+    ("rrg_store_set_counter", C.c_int, [vp, u64p]),
+    ("rrg_store_set_member_limit", C.c_int, [vp, C.c_uint64]),
     ("rrg_store_info", C.c_int, [vp, u64p, u64p, u32p]),
     ("rrg_generate_batch", C.c_int,
      [vp, C.c_int, C.c_uint64, C.c_uint64, vp, C.c_int, C.c_uint32, u64p]),

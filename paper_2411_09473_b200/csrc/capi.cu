@@ -86,10 +86,19 @@ void pool_free(void* p, size_t bytes) {
 }
 
 // Converts exceptions at the C boundary into status codes.
+// A store limit (rrg_store_set_member_limit) reached: RRG_ENOMEM, like a failed
+// device allocation (BatchOutOfMemory, sampling.hpp:148-154).
+struct OutOfMemory : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 template <typename Fn>
 rrg_status guarded(Fn&& fn) {
   try {
     return fn();
+  } catch (const OutOfMemory& e) {
+    set_error(e.what());
+    return RRG_ENOMEM;
   } catch (const CudaError& e) {
     set_error(std::string(e.where) + ": " + cudaGetErrorString(e.err));
     if (e.err == cudaErrorMemoryAllocation) {
@@ -231,6 +240,10 @@ void commit_staged(rrg_store* s, uint64_t count, uint32_t thr, uint64_t rows_big
   uint64_t added = 0;
   d2h(&added, s->scan.ptr + count, 1, g->stream);
   sync(g);
+  if (s->member_limit &&
+      s->members() + added + big_members + dc[1] > s->member_limit)
+    throw OutOfMemory("store member limit reached (" + std::to_string(s->member_limit) +
+                      " members)");
   const uint64_t need_mem = s->total + added;
   if (need_mem > s->mem.cap)
     s->mem.reserve_keep(std::max<uint64_t>(need_mem, s->mem.cap + s->mem.cap / 2), s->total,
@@ -257,6 +270,8 @@ void commit_staged(rrg_store* s, uint64_t count, uint32_t thr, uint64_t rows_big
   s->dense_members += big_members + dc[1];
   s->dense_max = std::max<uint32_t>(s->dense_max, std::max<uint32_t>(big_max,
                                                                      static_cast<uint32_t>(dc[2])));
+  s->live = s->nsets;  // finalize revives every set (rrr_store.hpp:49-59)
+  s->sel_mode = 0;
 }
 
 // bdix[0, count) = kNoRow (every slot of a new batch starts as a list set)
@@ -567,6 +582,8 @@ rrg_status rrg_store_clear(rrg_store* s) {
     s->max_len = 0;
     s->ndense = s->dense_members = 0;
     s->dense_max = 0;
+    s->live = 0;
+    s->sel_mode = 0;
     s->counter_complete = true;
     return RRG_OK;
   });
@@ -580,6 +597,58 @@ rrg_status rrg_store_dense_info(const rrg_store* s, uint64_t* dense_sets,
   if (dense_members) *dense_members = s->dense_members;
   if (dense_bytes) *dense_bytes = s->ndense * s->dwords * 4ull;
   if (rebuild_rounds) *rebuild_rounds = s->last_rebuilds;
+  return RRG_OK;
+}
+
+rrg_status rrg_store_live_count(const rrg_store* s, uint64_t* live) {
+  if (!s || !live) return invalid("null argument");
+  *live = s->live;
+  return RRG_OK;
+}
+
+rrg_status rrg_store_live_flags(const rrg_store* s, uint64_t first, uint64_t count,
+                                uint8_t* out) {
+  if (!s || (count && !out)) return invalid("null argument");
+  if (count > s->nsets || first > s->nsets - count) return invalid("live_flags: range out of bounds");
+  if (!count) return RRG_OK;
+  if (s->sel_mode == 0) {
+    std::fill(out, out + count, uint8_t{1});
+    return RRG_OK;
+  }
+  return guarded([&]() -> rrg_status {
+    rrg_graph* g = s->g;
+    auto* ms = const_cast<rrg_store*>(s);  // scratch only
+    ms->xlen.reserve_discard((count + 3) / 4 + 1);
+    launch_live_flags(s->off.ptr, s->dix.ptr, s->inv.ptr, s->covered.ptr, s->dcov.ptr,
+                      s->sel_mode == 1, first, count,
+                      reinterpret_cast<uint8_t*>(ms->xlen.ptr), g->stream);
+    d2h(out, reinterpret_cast<const uint8_t*>(ms->xlen.ptr), count, g->stream);
+    sync(g);
+    return RRG_OK;
+  });
+}
+
+rrg_status rrg_store_set_counter(rrg_store* s, const uint64_t* counts) {
+  if (!s || !counts) return invalid("null argument");
+  rrg_graph* g = s->g;
+  std::vector<uint32_t> c32(g->n);
+  for (uint32_t v = 0; v < g->n; ++v) {
+    if (counts[v] > UINT32_MAX) return invalid("set_counter: count exceeds 2^32 - 1");
+    c32[v] = static_cast<uint32_t>(counts[v]);
+  }
+  return guarded([&]() -> rrg_status {
+    if (g->n)
+      RRG_CUDA(cudaMemcpyAsync(s->counter.ptr, c32.data(), 4ull * g->n, cudaMemcpyHostToDevice,
+                               g->stream));
+    sync(g);
+    s->counter_complete = true;  // the caller's tally is the prebuilt counter
+    return RRG_OK;
+  });
+}
+
+rrg_status rrg_store_set_member_limit(rrg_store* s, uint64_t max_members) {
+  if (!s) return invalid("null store");
+  s->member_limit = max_members;
   return RRG_OK;
 }
 
@@ -626,8 +695,21 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
     float sample_ms = 0.0f;
     const auto t0 = std::chrono::steady_clock::now();
     rrg_batch_stats acc{};
+    // The fused counter is restored to its value before a chunk that fails
+    // (device allocation or the store's member limit): the store then holds
+    // exactly the sets counted, *sets_generated of them (BatchOutOfMemory,
+    // sampling.hpp:148-154, :190-198).
+    bool snap = false;
+    try {
     for (uint64_t done = 0; done < count;) {
       uint64_t c = std::min(kChunk, count - done);
+      if (s->member_limit) c = std::min<uint64_t>(c, 4096);  // partial progress before the limit
+      if (fused) {
+        s->csnap.reserve_discard(g->n ? g->n : 1);
+        RRG_CUDA(cudaMemcpyAsync(s->csnap.ptr, s->counter.ptr, 4ull * g->n,
+                                 cudaMemcpyDeviceToDevice, st));
+        snap = true;
+      }
       // IC execution mode. Auto mode measures a pilot chunk on a new graph first
       // (block schedule: bounded latency whatever the set sizes); sub-batches
       // append in slot order, so splitting changes nothing. Then: hub-dominated
@@ -889,6 +971,13 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       done += c;
       if (sets_generated) *sets_generated = done;
     }
+    } catch (...) {
+      if (snap) {
+        cudaMemcpyAsync(s->counter.ptr, s->csnap.ptr, 4ull * g->n, cudaMemcpyDeviceToDevice, st);
+        cudaStreamSynchronize(st);
+      }
+      throw;
+    }
     acc.sample_ms = sample_ms;
     acc.total_ms = static_cast<float>(
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
@@ -1024,6 +1113,8 @@ rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double adaptive_threshold,
     }
     if (covered_total) *covered_total = covered;
     if (rounds_done) *rounds_done = status[0];
+    s->live = s->nsets - covered;  // the store stays tombstoned (imm.hpp:194-195)
+    s->sel_mode = scan ? 1 : 2;
     if (round_counters && status[0]) {
       std::vector<uint32_t> snap(static_cast<uint64_t>(status[0]) * n);
       d2h(snap.data(), s->snap.ptr, snap.size(), st);
@@ -1177,6 +1268,8 @@ rrg_status rrg_store_append_from(rrg_store* dst, const rrg_store* src, uint64_t 
     dst->nsets += count;
     dst->total += added;
     dst->max_len = mx;
+    dst->live = dst->nsets;  // finalize revives every set
+    dst->sel_mode = 0;
     return RRG_OK;
   });
 }

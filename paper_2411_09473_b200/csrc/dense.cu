@@ -191,6 +191,21 @@ __global__ void k_gather_rows(const uint32_t* src, uint32_t dwords, const uint32
   }
 }
 
+__global__ void k_live_flags(const uint64_t* off, const uint32_t* dix, const uint32_t* wmem,
+                             const uint32_t* covered, const uint32_t* dcov, bool scan,
+                             uint64_t first, uint64_t count, uint8_t* out) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t s = first + i;
+    const uint32_t r = dix[s];
+    bool live;
+    if (r != kNoRow) live = dcov[r] == 0u;
+    else if (scan) live = wmem[off[s]] != 0xffffffffu;  // covered sets are blanked
+    else live = covered[s] == 0u;
+    out[i] = live ? 1 : 0;
+  }
+}
+
 int grid_items(uint64_t items, int block) {
   const uint64_t b = (items + block - 1) / block;
   return static_cast<int>(b < 1 ? 1 : (b > 65535 ? 65535 : b));
@@ -251,6 +266,15 @@ void launch_materialize(const uint64_t* off, const uint32_t* mem, const uint32_t
   if (!count) return;
   k_materialize<<<grid_items(count * 32, 256), 256, 0, s>>>(off, mem, dix, dbits, dwords, droot,
                                                            first, count, xoff, xmem);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_live_flags(const uint64_t* off, const uint32_t* dix, const uint32_t* wmem,
+                       const uint32_t* covered, const uint32_t* dcov, bool scan, uint64_t first,
+                       uint64_t count, uint8_t* out, cudaStream_t s) {
+  k_live_flags<<<grid_items(count, 256), 256, 0, s>>>(off, dix, wmem, covered, dcov, scan, first,
+                                                      count, out);
   RRG_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -219,6 +219,10 @@ struct rrg_store {
   rrgpu::DevBuf<uint64_t> xoff;        // export: materialized offsets
   rrgpu::DevBuf<uint32_t> xmem;        // export: materialized members
   uint64_t last_rebuilds = 0;          // rounds of the last select_seeds that rebuilt
+  uint64_t live = 0;                   // RRRStore::live_count (rrr_store.hpp:84)
+  int sel_mode = 0;                    // liveness held by: 0 none (all live), 1 scan copy, 2 covered[]
+  uint64_t member_limit = 0;           // 0: none; else RRG_ENOMEM past it (tests, budgets)
+  rrgpu::DevBuf<uint32_t> csnap;       // fused counter before the current chunk
   uint64_t members() const { return total + dense_members; }
 };
 
@@ -350,6 +354,11 @@ void launch_materialize(const uint64_t* off, const uint32_t* mem, const uint32_t
                         const uint32_t* dbits, uint32_t dwords, const uint32_t* droot,
                         uint64_t first, uint64_t count, const uint64_t* xoff, uint32_t* xmem,
                         cudaStream_t s);
+// is_live per set of [first, first + count) after a selection: rows by dcov,
+// list sets by the blanked scan copy (scan) or covered[] (index)
+void launch_live_flags(const uint64_t* off, const uint32_t* dix, const uint32_t* wmem,
+                       const uint32_t* covered, const uint32_t* dcov, bool scan, uint64_t first,
+                       uint64_t count, uint8_t* out, cudaStream_t s);
 // fraction_covered over rows: rows holding a flagged vertex -> hits
 void launch_dense_fraction(const uint32_t* dbits, uint32_t dwords, uint64_t nrows,
                            const uint32_t* seeds, uint32_t nseeds, unsigned long long* hits,

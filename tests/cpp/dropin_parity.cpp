@@ -103,6 +103,40 @@ int main() {
     const rrgpu::SeedSet gs = rrgpu::select_seeds(gstore, g.num_vertices, c.k, 0.25, true);
     expect(rs.seeds == gs.seeds && rs.marginal_counts == gs.marginal_counts, "select_seeds", id);
 
+    expect(rstore.live_count() == gstore.live_count(), "live_count after select_seeds", id);
+    bool same_live = true;
+    for (uint64_t j = 0; j < rstore.size(); j += 7) same_live &= rstore.is_live(j) == gstore.is_live(j);
+    expect(same_live, "is_live after select_seeds", id);
+
+    // --- the reference's own signatures: WorkPool&, Counter*, SelectionStats --
+    {
+      rrgpu::WorkPool gpool(4);
+      rrgpu::RRRStore gs2(dg);
+      rrgpu::Counter gcnt(g.num_vertices);
+      rrgpu::generate_batch(dg, gc.model, 9, 1000, gpool, gs2, &gcnt);
+      rrgpu::generate_batch_fused(dg, gc.model, 9, 2000, gcnt, gpool, gs2);
+      bool same_cnt = true;
+      for (uint32_t v = 0; v < g.num_vertices; ++v) same_cnt &= counter.get(v) == gcnt.get(v);
+      expect(same_cnt, "Counter* overload of generate_batch", id);
+      rrflow::SelectionStats rstats;
+      rstats.capture_round_counters = true;
+      const rrflow::SeedSet rs2 = rrflow::select_seeds(rstore, g.num_vertices, c.k, pool, 0.25,
+                                                       &counter, &rstats);
+      rrgpu::SelectionStats gstats;
+      gstats.capture_round_counters = true;
+      const rrgpu::SeedSet gs3 = rrgpu::select_seeds(gs2, g.num_vertices, c.k, gpool, 0.25,
+                                                     &gcnt, &gstats);
+      expect(rs2.seeds == gs3.seeds && rs2.marginal_counts == gs3.marginal_counts,
+             "select_seeds (WorkPool&, prebuilt Counter*)", id);
+      expect(rstats.round_counters == gstats.round_counters, "SelectionStats round counters", id);
+      // prebuilt == nullptr: build_counter over the store
+      rrgpu::RRRStore gs4(dg);
+      rrgpu::generate_batch(dg, gc.model, 9, 3000, gpool, gs4, nullptr);
+      const rrgpu::SeedSet gs5 = rrgpu::select_seeds(gs4, g.num_vertices, c.k, gpool);
+      expect(gs5.seeds == rs2.seeds && gs5.marginal_counts == rs2.marginal_counts,
+             "select_seeds recount (unfused store)", id);
+    }
+
     // --- sampling_phase (imm.hpp:169-209) and the baseline strategy ----------
     rrflow::WorkPool pool1(1);
     const rrflow::SamplingPhaseResult rp = rrflow::sampling_phase(g, rc, pool1);
@@ -135,6 +169,35 @@ int main() {
       threw = true;
     }
     expect(threw, "k > n throws std::invalid_argument", 0);
+  }
+  // BatchOutOfMemory{sets_generated} (sampling.hpp:148-154): a store budget hit
+  // mid-batch keeps the sets made so far, their counts, and reports how many
+  {
+    rrflow::Graph g = rrflow::synth_graph(rrflow::SynthKind::erdos_renyi, 3000, 0.002, 11);
+    rrflow::generate_ic_weights(g, 12);
+    rrgpu::Graph dg(g.num_vertices, g.reverse_offsets, g.reverse_sources, g.reverse_weights);
+    rrgpu::WorkPool gpool(1);
+    rrgpu::RRRStore st(dg);
+    rrg_store_set_member_limit(st.handle(), 20000);
+    rrgpu::Counter cnt(g.num_vertices);
+    uint64_t made = UINT64_MAX;
+    try {
+      rrgpu::generate_batch(dg, rrgpu::DiffusionModel::IC, 3, 100000, gpool, st, &cnt);
+    } catch (const rrgpu::BatchOutOfMemory& e) {
+      made = e.sets_generated;
+    }
+    expect(made != UINT64_MAX && made > 0 && made < 100000 && made == st.size(),
+           "BatchOutOfMemory carries sets_generated == store size", 0);
+    rrflow::WorkPool pool(2);
+    rrflow::RRRStore rs(g.num_vertices, pool.workers());
+    rrflow::Counter rc(g.num_vertices);
+    rrflow::generate_batch(g, rrflow::DiffusionModel::IC, 3, made, pool, rs, &rc);
+    bool same = true;
+    for (uint32_t v = 0; v < g.num_vertices; ++v) same &= rc.get(v) == cnt.get(v);
+    const std::vector<uint64_t> dc = st.counter();
+    for (uint32_t v = 0; v < g.num_vertices; ++v) same &= rc.get(v) == dc[v];
+    expect(same && st.total_member_count() <= 20000,
+           "after BatchOutOfMemory: the kept sets and counts are the reference's first sets", 0);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL PASS", failures);
   return failures ? 1 : 0;

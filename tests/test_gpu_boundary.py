@@ -1,0 +1,79 @@
+"""The rest of the reference's store / selection surface through the C ABI:
+RRRStore::live_count / is_live after a selection (rrr_store.hpp:62, :84; the
+store stays tombstoned, imm.hpp:194-195), a caller-held prebuilt Counter
+(selection.hpp:209-218), SelectionStats round counters (:45-49, :237-239) and
+BatchOutOfMemory{sets_generated} (sampling.hpp:148-154)."""
+import numpy as np
+import pytest
+
+import paper_2411_09473_b200 as P
+from paper_2411_09473_b200 import graphs
+
+pytestmark = pytest.mark.gpu
+
+IC = 0
+
+
+def small(name="cfg1", n=1 << 11, m=1 << 15):
+    return graphs.generate(graphs.scaled(graphs.CONFIGS[name], n, m))
+
+
+@pytest.mark.parametrize("index", [False, True])
+def test_live_count_and_flags_after_selection(cuda, oracle, monkeypatch, index):
+    if index:
+        monkeypatch.setenv("RRGPU_SELECT_INDEX", "1")
+    arrays = small()
+    n = arrays[0].size - 1
+    g = P.Graph(*arrays)
+    st = P.RRRStore(g)
+    P.generate_batch(g, IC, 3, 3000, st)
+    assert st.live_count() == 3000 and st.live_flags().all()
+    sel = P.select_seeds(st, n, 15)
+    off, mem = st.export()
+    covered = np.array([bool(np.isin(sel.seeds, mem[off[i]:off[i + 1]]).any()) for i in range(3000)])
+    assert st.live_count() == 3000 - sum(sel.marginal_counts) == int((~covered).sum())
+    assert (st.live_flags() == ~covered).all()
+    assert (st.live_flags(100, 50) == ~covered[100:150]).all()
+    P.generate_batch(g, IC, 3, 10, st)  # an append revives every set (finalize)
+    assert st.live_count() == 3010 and st.live_flags().all()
+
+
+def test_prebuilt_counter_and_stats(cuda, oracle):
+    arrays = small("cfg2")
+    n = arrays[0].size - 1
+    g = P.Graph(*arrays)
+    st = P.RRRStore(g)
+    P.generate_batch(g, 1, 5, 2500, st, fused=False)
+    off, mem = st.export()
+    tally = np.bincount(mem, minlength=n).astype(np.uint64)
+    stats = P.SelectionStats(capture_round_counters=True)
+    s = P.select_seeds(st, n, 12, prebuilt=tally, stats=stats)
+    seeds, marg, rc = oracle.select(n, off, mem, 12, capture=True)
+    assert s.seeds == seeds and s.marginal_counts == marg
+    assert (stats.round_counters == rc).all()
+    # a different starting tally changes the greedy exactly like the reference's
+    skew = tally.copy()
+    skew[7] += 100000
+    s2 = P.select_seeds(st, n, 3, prebuilt=skew)
+    assert s2.seeds[0] == 7
+
+
+def test_batch_out_of_memory_keeps_a_consistent_store(cuda, oracle):
+    arrays = small()
+    n = arrays[0].size - 1
+    g = P.Graph(*arrays)
+    st = P.RRRStore(g)
+    P.generate_batch(g, IC, 1, 500, st)
+    st.set_member_limit(st.total_member_count() + 30000)
+    with pytest.raises(P.RRGOutOfMemory) as e:
+        P.generate_batch(g, IC, 1, 200000, st)
+    made = e.value.sets_generated
+    assert 0 < made < 200000 and st.size() == 500 + made
+    assert st.total_member_count() <= 500 + 30000 + st.total_member_count()
+    ref = oracle.graph(*arrays).sample(IC, 1, 0, 500 + made, workers=4)
+    assert (st.counter() == ref.counter).all()
+    off, mem = st.export()
+    assert (np.diff(off.astype(np.int64)) == np.diff(ref.offsets.astype(np.int64))).all()
+    st.set_member_limit(0)
+    P.generate_batch(g, IC, 1, 100, st)  # the store keeps working past the failure
+    assert st.size() == 600 + made
