@@ -41,6 +41,8 @@ typedef struct rrg_store rrg_store; /* RRRStore + fused Counter (rrr_store.hpp:2
 rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* rev_offsets,
                             const uint32_t* rev_sources, const float* rev_weights,
                             rrg_graph** out);
+/* Frees the graph; while stores of it are alive it is only marked, and the last
+ * rrg_store_destroy frees it (destruction order is the caller's choice). */
 void rrg_graph_destroy(rrg_graph* g);
 /* Builds the per-model device layout up front (otherwise done on first use):
  * IC -> interleaved {source, weight} records; LT -> sequential fp64 CDF (K0). */

@@ -171,6 +171,21 @@ uint32_t big_workers(rrg_graph* g, uint64_t n_items) {
   return static_cast<uint32_t>(std::max<uint64_t>(1, w));
 }
 
+void ensure_giant_scratch(rrg_graph* g, uint32_t ctas) {
+  GiantScratch& gs = g->giant;
+  if (gs.ctas >= ctas) return;
+  gs.lists.release();
+  gs.tabs.release();
+  gs.tags.release();
+  gs.lists.reserve_discard(static_cast<uint64_t>(ctas) * kGiantCap);
+  gs.tabs.reserve_discard(static_cast<uint64_t>(ctas) * 2 * kGiantCap);
+  gs.tags.reserve_discard(ctas);
+  RRG_CUDA(cudaMemsetAsync(gs.tabs.ptr, 0, static_cast<uint64_t>(ctas) * 2 * kGiantCap * 8,
+                           g->stream));
+  RRG_CUDA(cudaMemsetAsync(gs.tags.ptr, 0, ctas * 4ull, g->stream));
+  gs.ctas = ctas;
+}
+
 void ensure_big_scratch(rrg_graph* g, uint32_t workers) {
   BigScratch& b = g->big;
   if (b.workers >= workers) return;
@@ -450,13 +465,26 @@ rrg_status rrg_graph_export_transpose(const rrg_graph* g, uint64_t* roff, uint32
   });
 }
 
-void rrg_graph_destroy(rrg_graph* g) {
-  if (!g) return;
+namespace {
+void graph_free(rrg_graph* g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
   delete g;
+}
+}  // namespace
+
+// A graph outlives its stores: destroying it while stores remain (a caller's
+// garbage collector may run the two in any order) only marks it, and the last
+// store's destroy frees it.
+void rrg_graph_destroy(rrg_graph* g) {
+  if (!g) return;
+  if (g->nstores > 0) {
+    g->destroyed = true;
+    return;
+  }
+  graph_free(g);
 }
 
 rrg_status rrg_graph_prepare(rrg_graph* g, rrg_model model) {
@@ -561,14 +589,17 @@ rrg_status rrg_store_create(rrg_graph* g, rrg_store** out) {
     delete s;
     return st;
   }
+  ++g->nstores;
   *out = s;
   return RRG_OK;
 }
 
 void rrg_store_destroy(rrg_store* s) {
   if (!s) return;
-  cudaStreamSynchronize(s->g->stream);
+  rrg_graph* g = s->g;
+  cudaStreamSynchronize(g->stream);
   delete s;
+  if (--g->nstores == 0 && g->destroyed) graph_free(g);
 }
 
 rrg_status rrg_store_clear(rrg_store* s) {
@@ -703,7 +734,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
     try {
     for (uint64_t done = 0; done < count;) {
       uint64_t c = std::min(kChunk, count - done);
-      if (s->member_limit) c = std::min<uint64_t>(c, 4096);  // partial progress before the limit
+      if (s->member_limit) c = std::min<uint64_t>(c, 1024);  // partial progress before the limit
       if (fused) {
         s->csnap.reserve_discard(g->n ? g->n : 1);
         RRG_CUDA(cudaMemcpyAsync(s->csnap.ptr, s->counter.ptr, 4ull * g->n,
@@ -822,7 +853,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
 
       // One launch of `kind` over `list` (nullptr: the range [0, n_items)). The
       // per-launch counters reset here; the deferral list accumulates over a pass.
-      enum Kind { kMain, kMainWarp, kCta, kBig, kFast, kFastBig, kFastLane };
+      enum Kind { kMain, kMainWarp, kCta, kBig, kFast, kFastBig, kFastLane, kCtaGiant };
       auto launch = [&](Kind kind, const uint32_t* list, uint64_t n_items, uint32_t* restage_out) {
         ctl.next = 0;
         ctl.restage_members = 0;
@@ -853,12 +884,21 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
           launch_big(model, p, list, static_cast<uint32_t>(n_items), g->big.bitmaps.ptr,
                      g->big.lists.ptr, workers, st);
         } else {
-          const int sched = kind == kMainWarp ? kSchedWarp : kind == kCta ? kSchedCta : kSchedLane;
+          const int sched = kind == kMainWarp ? kSchedWarp : kind == kCta ? kSchedCta
+                            : kind == kCtaGiant ? kSchedCtaGiant : kSchedLane;
           p.list = list;
           p.count = n_items;
           const uint64_t per_block = sched == kSchedLane ? block : sched == kSchedWarp ? block / 32 : 1;
           uint64_t grid_cap = full_grid;
           if (sched == kSchedCta) grid_cap = g->scratch.lanes / block;
+          if (sched == kSchedCtaGiant) {
+            grid_cap = std::min<uint64_t>(g->scratch.lanes / block, n_items);
+            ensure_giant_scratch(g, static_cast<uint32_t>(grid_cap));
+            p.glists = g->giant.lists.ptr;
+            p.gtabs = g->giant.tabs.ptr;
+            p.gtags = g->giant.tags.ptr;
+            p.gctas = g->giant.ctas;
+          }
           const uint64_t grid_need = (n_items + per_block - 1) / per_block;
           launch_sampler(model, p,
                          static_cast<int>(std::max<uint64_t>(1, std::min(grid_cap, grid_need))),
@@ -933,29 +973,40 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
           pass(kFastBig, dlist, ndef, dspare);
           ndef = 0;
         }
-      } else if (model == RRG_IC) {
+      }
+      // the giant / big-set passes get the largest sets of the batch: reserve a
+      // row for each when they are dense-sized (bounded by a quarter of the free
+      // memory; a slot that finds no row is re-run after the pool grows)
+      auto reserve_rows_for = [&](uint64_t nsets_big) {
+        if (dense_thr == kNoDense || dense_thr > static_cast<uint32_t>(block) * kMemCap) return;
+        size_t free_b = 0, total_b = 0;
+        RRG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const uint64_t fit = free_b / 4 / (static_cast<uint64_t>(s->dwords) * 4 + 16);
+        const uint64_t want = std::min<uint64_t>(nsets_big, fit);
+        if (drow_avail - ctl.ndense < want) {
+          ensure_rows(s, s->ndense + ctl.ndense + want, s->ndense + ctl.ndense);
+          drow_avail = rows_cap(s) - s->ndense;
+          set_rows();
+        }
+      };
+      if (!ic_fast && model == RRG_IC) {
         if (ndef && main_kind != kCta) {
           acc.deferred += ndef;
           ndef = pass(kCta, dlist, ndef, dspare);
           std::swap(dlist, dspare);
         }
+        // sets past the block scratch (256K members): the same block schedule
+        // over a private 1M-member scratch per block
+        if (ndef && g->n > static_cast<uint32_t>(block) * kMemCap) {
+          acc.deferred += ndef;
+          reserve_rows_for(ndef);
+          ndef = pass(kCtaGiant, dlist, ndef, dspare);
+          std::swap(dlist, dspare);
+        }
       }
       if (ndef) {
         acc.deferred += ndef;
-        // the big-set path's sets are the largest of the batch: reserve a row for
-        // each when they are dense-sized (bounded by a quarter of the free memory;
-        // a slot that finds no row is re-run after the pool grows)
-        if (dense_thr != kNoDense && dense_thr <= static_cast<uint32_t>(block) * kMemCap) {
-          size_t free_b = 0, total_b = 0;
-          RRG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-          const uint64_t fit = free_b / 4 / (static_cast<uint64_t>(s->dwords) * 4 + 16);
-          const uint64_t want = std::min<uint64_t>(ndef, fit);
-          if (drow_avail - ctl.ndense < want) {
-            ensure_rows(s, s->ndense + ctl.ndense + want, s->ndense + ctl.ndense);
-            drow_avail = rows_cap(s) - s->ndense;
-            set_rows();
-          }
-        }
+        reserve_rows_for(ndef);
         pass(kBig, dlist, ndef, s->bigre.ptr);
       }
       acc.edges_inspected += ctl.inspected;

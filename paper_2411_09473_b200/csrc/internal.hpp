@@ -96,6 +96,15 @@ struct LaneScratch {
   DevBuf<uint32_t> wtags;
 };
 
+// Giant CTA schedule scratch (sample_ic.cu k_sample_ic_cta<true>): per block a
+// list of kGiantCap members, a tagged table of 2 kGiantCap entries, a tag.
+struct GiantScratch {
+  uint32_t ctas = 0;
+  DevBuf<uint32_t> lists;
+  DevBuf<uint64_t> tabs;
+  DevBuf<uint32_t> tags;
+};
+
 // Big-set path scratch: one n-bit map and one n-entry list per worker warp.
 struct BigScratch {
   uint32_t workers = 0;
@@ -152,8 +161,11 @@ struct rrg_graph {
   uint32_t ic_inner = 8;         // IC: edge steps per flat-loop iteration
   rrgpu::LaneScratch scratch;
   rrgpu::BigScratch big;
+  rrgpu::GiantScratch giant;
   rrgpu::DevBuf<rrgpu::SampleCtl> ctl;
   rrg_batch_stats last{};
+  int nstores = 0;               // stores alive on this graph
+  bool destroyed = false;        // rrg_graph_destroy ran while stores were alive
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -284,6 +296,11 @@ struct SampleParams {
   uint64_t drow_base;       // first row of this batch
   uint64_t drow_avail;      // rows allocated after drow_base
   uint64_t set_base;        // store index of batch slot 0
+  // giant CTA schedule: per block kGiantCap list entries, 2 kGiantCap table entries
+  uint32_t* glists;
+  uint64_t* gtabs;
+  uint32_t* gtags;
+  uint32_t gctas;
 };
 
 // graph_dev.cu: device transpose (+ normalize_lt_weights) of an edge list on the
@@ -309,7 +326,8 @@ int sampler_block();
 int sampler_blocks_per_sm(int model, uint32_t ic_inner, int lt_mode = 1);
 // IC schedules: lane per sample; warp per sample over its 32 lanes' scratch
 // (sets up to 32K members); CTA per sample over its 256 lanes' scratch (256K).
-enum Schedule : int { kSchedLane = 0, kSchedWarp = 1, kSchedCta = 2 };
+enum Schedule : int { kSchedLane = 0, kSchedWarp = 1, kSchedCta = 2, kSchedCtaGiant = 3 };
+constexpr uint32_t kGiantCap = 1u << 20;  // members per block of the giant CTA schedule
 void launch_sampler(int model, const SampleParams& p, int grid, uint32_t ic_inner, int schedule,
                     cudaStream_t s);
 // per-model halves of the two above (sample_ic.cu, sample_lt.cu)

@@ -865,8 +865,15 @@ __device__ __forceinline__ void cta_tab_insert(uint64_t* tab, uint32_t tag, uint
   do {            \
   } while (0)
 #endif
+// kGiant: the same schedule for the sets the block scratch (256K members) could
+// not hold -- the giant-component sets of supercritical graphs (cfg3c: ~1/3 of
+// the sets, ~500K members each). Per block a private list of kGiantCap members
+// and a table of 2 kGiantCap entries (own tag range); a set of >= dense_thr
+// members is written straight into a row of the dense arm (rrr_set.hpp:82-83).
+// Sets past kGiantCap go on to the big-set path.
+template <bool kGiant>
 __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(const SampleParams p) {
-  constexpr uint32_t kCap = kBlock * kMemCap;
+  constexpr uint32_t kCap = kGiant ? kGiantCap : kBlock * kMemCap;
   extern __shared__ __align__(16) unsigned char k_dsm[];
   CtaSmem& cs = *reinterpret_cast<CtaSmem*>(k_dsm);
   const int tid = threadIdx.x;
@@ -875,16 +882,20 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
   CtaWarpFields& ws = cs.w[wl];
   const uint64_t region = static_cast<uint64_t>(blockIdx.x) * kBlock;
   if (region + kBlock > p.lanes) return;  // uniform per block
-  uint32_t* mem = p.lists + region * kMemCap;
-  uint64_t* tab = p.tabs + region * kTabCap;
+  if (kGiant && blockIdx.x >= p.gctas) return;
+  uint32_t* mem = kGiant ? p.glists + static_cast<uint64_t>(blockIdx.x) * kGiantCap
+                         : p.lists + region * kMemCap;
+  uint64_t* tab = kGiant ? p.gtabs + static_cast<uint64_t>(blockIdx.x) * (2ull * kGiantCap)
+                         : p.tabs + region * kTabCap;
   // general windows: high word of the draw at each stream rank (global: kept
   // out of shared memory so two blocks still leave L1 its share)
   uint32_t* xhi = p.xhi + static_cast<size_t>(blockIdx.x) * kCtaWin;
   uint32_t* sf = cs.filt;
   for (uint32_t t = tid; t < kCtaFilterWords; t += kBlock) sf[t] = 0;
-  // same 256-lane regions and tag range as the 256-lane warp layout
+  // same 256-lane regions and tag range as the 256-lane warp layout; the giant
+  // tables are private to the block and count their own tags
   const uint64_t tslot = region / 32;
-  uint32_t tag = 0xC0000000u | (p.wtags[tslot] & 0x3fffffffu);
+  uint32_t tag = kGiant ? p.gtags[blockIdx.x] : 0xC0000000u | (p.wtags[tslot] & 0x3fffffffu);
   uint64_t insp = 0;
   const uint32_t wbase = kWin * wl;  // this warp's first window position
 #ifdef RRG_CTA_PHASES
@@ -1677,6 +1688,37 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       if (tid == 0) defer_slot(p, idx);
       continue;
     }
+    if (kGiant && nmem >= p.dense_thr) {
+      // a row of the dense arm: zeroed, the members OR-ed in, counted
+      if (tid == 0) cs.next = atomicAdd(&p.ctl->ndense, 1ull);
+      __syncthreads();
+      const unsigned long long row = cs.next;
+      if (row >= p.drow_avail) {
+        if (tid == 0) restage_slot(p, idx, 0);  // the row pool grows, then a re-run
+        continue;
+      }
+      const uint64_t grow = p.drow_base + row;
+      uint32_t* dst = p.dbits + grow * p.dwords;
+      for (uint32_t t = tid; t < p.dwords; t += kBlock) dst[t] = 0u;
+      __syncthreads();
+      for (uint32_t t = tid; t < nmem; t += kBlock) {
+        const uint32_t v = mem[t];
+        atomicOr(dst + (v >> 5), 1u << (v & 31));
+        if (p.counter) atomicAdd(p.counter + v, 1u);
+      }
+      if (tid == 0) {
+        p.dlen[grow] = nmem;
+        p.droot[grow] = mem[0];
+        p.dslot[grow] = static_cast<uint32_t>(p.set_base + idx);
+        p.bdix[idx] = static_cast<uint32_t>(grow);
+        p.slot_start[idx] = 0;
+        p.slot_len[idx] = 0;  // empty list range
+        atomicAdd(&p.ctl->dense_members, (unsigned long long)nmem);
+        atomicMax(&p.ctl->dense_max, nmem);
+      }
+      insp += sinsp;
+      continue;
+    }
     if (tid == 0) cs.next = atomicAdd(&p.ctl->cursor, (unsigned long long)nmem);
     __syncthreads();
     const unsigned long long pos = cs.next;
@@ -1715,7 +1757,10 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
              ph_[12] * 1e-6, ph_[13] * 1e-6, ph_[14] * 1e-6, ph_[1] * 1e-6);
   }
 #endif
-  if (tid == 0) p.wtags[tslot] = tag;
+  if (tid == 0) {
+    if (kGiant) p.gtags[blockIdx.x] = tag;
+    else p.wtags[tslot] = tag;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -2050,12 +2095,18 @@ void launch_ic_sampler(const SampleParams& p, int grid, uint32_t ic_inner, int s
       RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_warp<32>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kWarpKernelDynSmem)));
-      RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_cta<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kCtaKernelDynSmem)));
+      RRG_CUDA(cudaFuncSetAttribute(k_sample_ic_cta<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kCtaKernelDynSmem)));
       attr_set = true;
     }
     if (schedule == kSchedWarp) k_sample_ic_warp<32><<<grid, kBlock, kWarpKernelDynSmem, s>>>(p);
-    else k_sample_ic_cta<<<grid, kBlock, kCtaKernelDynSmem, s>>>(p);
+    else if (schedule == kSchedCtaGiant)
+      k_sample_ic_cta<true><<<grid, kBlock, kCtaKernelDynSmem, s>>>(p);
+    else k_sample_ic_cta<false><<<grid, kBlock, kCtaKernelDynSmem, s>>>(p);
   } else {
     k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
   }

@@ -177,8 +177,11 @@ int main() {
     rrflow::generate_ic_weights(g, 12);
     rrgpu::Graph dg(g.num_vertices, g.reverse_offsets, g.reverse_sources, g.reverse_weights);
     rrgpu::WorkPool gpool(1);
+    rrgpu::RRRStore probe(dg);
+    rrgpu::generate_batch(dg, rrgpu::DiffusionModel::IC, 3, 1000, probe, true);
+    const uint64_t limit = probe.total_member_count() * 11 / 2;  // ~5 chunks of 1024 sets fit
     rrgpu::RRRStore st(dg);
-    rrg_store_set_member_limit(st.handle(), 20000);
+    rrg_store_set_member_limit(st.handle(), limit);
     rrgpu::Counter cnt(g.num_vertices);
     uint64_t made = UINT64_MAX;
     try {
@@ -196,7 +199,7 @@ int main() {
     for (uint32_t v = 0; v < g.num_vertices; ++v) same &= rc.get(v) == cnt.get(v);
     const std::vector<uint64_t> dc = st.counter();
     for (uint32_t v = 0; v < g.num_vertices; ++v) same &= rc.get(v) == dc[v];
-    expect(same && st.total_member_count() <= 20000,
+    expect(same && st.total_member_count() <= limit,
            "after BatchOutOfMemory: the kept sets and counts are the reference's first sets", 0);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL PASS", failures);

@@ -64,12 +64,14 @@ def test_batch_out_of_memory_keeps_a_consistent_store(cuda, oracle):
     g = P.Graph(*arrays)
     st = P.RRRStore(g)
     P.generate_batch(g, IC, 1, 500, st)
-    st.set_member_limit(st.total_member_count() + 30000)
+    mean = st.total_member_count() / 500
+    limit = st.total_member_count() + int(5.5 * 1024 * mean)  # ~5 chunks of 1024 sets fit
+    st.set_member_limit(limit)
     with pytest.raises(P.RRGOutOfMemory) as e:
         P.generate_batch(g, IC, 1, 200000, st)
     made = e.value.sets_generated
     assert 0 < made < 200000 and st.size() == 500 + made
-    assert st.total_member_count() <= 500 + 30000 + st.total_member_count()
+    assert st.total_member_count() <= limit
     ref = oracle.graph(*arrays).sample(IC, 1, 0, 500 + made, workers=4)
     assert (st.counter() == ref.counter).all()
     off, mem = st.export()
@@ -77,3 +79,15 @@ def test_batch_out_of_memory_keeps_a_consistent_store(cuda, oracle):
     st.set_member_limit(0)
     P.generate_batch(g, IC, 1, 100, st)  # the store keeps working past the failure
     assert st.size() == 600 + made
+
+
+def test_graph_destroyed_before_its_store(cuda):
+    """A caller's garbage collector may finalize a graph before its stores (e.g.
+    both in a reference cycle): the graph stays alive until its last store goes."""
+    arrays = small()
+    g = P.Graph(*arrays)
+    st = P.RRRStore(g)
+    P.generate_batch(g, IC, 1, 100, st)
+    g.close()
+    assert st.size() == 100 and st.total_member_count() > 0
+    st.close()

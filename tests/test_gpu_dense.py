@@ -215,3 +215,26 @@ def test_imm_cfg3_correlated_full_size(cuda):
     assert res.sets_generated == ref["sets_generated"]
     assert res.mean_set_size == ref["mean_set_size"]
     assert res.max_set_size == ref["max_set_size"]
+
+
+def test_cfg3c_giant_sets_per_slot(cuda, oracle):
+    """Full-size cfg3c: sets of ~500K members run the giant block schedule
+    (private 1M-member scratch per block) and land in rows directly; the 16
+    largest and 16 random slots of a batch equal the reference's."""
+    cfg = graphs.CONFIGS["cfg3c"]
+    arrays = graphs.generate(cfg)
+    n = arrays[0].size - 1
+    g = P.Graph(*arrays)
+    st = P.RRRStore(g)
+    P.generate_batch(g, IC, 1, 512, st)
+    stats = g.last_batch_stats()
+    off, mem = st.export()
+    sizes = np.diff(off.astype(np.int64))
+    assert sizes.max() > 256 * 1024 and stats.deferred > 0
+    assert (np.bincount(mem, minlength=n).astype(np.uint64) == st.counter()).all()
+    og = oracle.graph(*arrays)
+    rng = np.random.default_rng(3)
+    picks = set(np.argsort(sizes, kind="stable")[-16:].tolist()) | set(rng.choice(512, 16, replace=False).tolist())
+    for s in sorted(int(x) for x in picks):
+        ref = og.sample(IC, 1, s, 1)
+        assert_sets_equal(off[s:s + 2] - off[s], mem[off[s]:off[s + 1]], ref, first_slot=s)
