@@ -957,23 +957,6 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       // for large batches (throughput), warp for small ones (latency of the
       // largest sets: cfg5 32K sets 5.1 ms per warp vs 9.2 ms per lane)
       const bool fast_lane = ic_fast && (g->ic_mode == 1 || (g->ic_mode == 0 && c >= (1u << 17)));
-      const Kind main_kind = fast_lane ? kFastLane : ic_fast ? kFast
-                             : ic_cta ? kCta : ic_warp ? kMainWarp : kMain;
-      uint64_t ndef = pass(main_kind, nullptr, c, s->deferred.ptr);
-      uint32_t* dlist = s->deferred.ptr;
-      uint32_t* dspare = s->deferred2.ptr;
-      if (ic_fast) {
-        if (ndef && fast_lane) {
-          acc.deferred += ndef;
-          ndef = pass(kFast, dlist, ndef, dspare);
-          std::swap(dlist, dspare);
-        }
-        if (ndef) {
-          acc.deferred += ndef;
-          pass(kFastBig, dlist, ndef, dspare);
-          ndef = 0;
-        }
-      }
       // the giant / big-set passes get the largest sets of the batch: reserve a
       // row for each when they are dense-sized (bounded by a quarter of the free
       // memory; a slot that finds no row is re-run after the pool grows)
@@ -989,15 +972,40 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
           set_rows();
         }
       };
+      // giant-component graphs (auto mode: a block pass deferred >= 5 % of its
+      // sets past the 256K-member block scratch) run the block schedule over the
+      // giant scratch from the start: no set is run twice
+      const bool giant_main = ic_cta && g->ic_giant && g->ic_mode == 0;
+      const Kind main_kind = fast_lane ? kFastLane : ic_fast ? kFast
+                             : giant_main ? kCtaGiant
+                             : ic_cta ? kCta : ic_warp ? kMainWarp : kMain;
+      if (giant_main) reserve_rows_for(c / 2);
+      uint64_t ndef = pass(main_kind, nullptr, c, s->deferred.ptr);
+      if (main_kind == kCta && g->n > static_cast<uint32_t>(block) * kMemCap && ndef * 20 >= c)
+        g->ic_giant = true;
+      uint32_t* dlist = s->deferred.ptr;
+      uint32_t* dspare = s->deferred2.ptr;
+      if (ic_fast) {
+        if (ndef && fast_lane) {
+          acc.deferred += ndef;
+          ndef = pass(kFast, dlist, ndef, dspare);
+          std::swap(dlist, dspare);
+        }
+        if (ndef) {
+          acc.deferred += ndef;
+          pass(kFastBig, dlist, ndef, dspare);
+          ndef = 0;
+        }
+      }
       if (!ic_fast && model == RRG_IC) {
-        if (ndef && main_kind != kCta) {
+        if (ndef && main_kind != kCta && main_kind != kCtaGiant) {
           acc.deferred += ndef;
           ndef = pass(kCta, dlist, ndef, dspare);
           std::swap(dlist, dspare);
         }
         // sets past the block scratch (256K members): the same block schedule
         // over a private 1M-member scratch per block
-        if (ndef && g->n > static_cast<uint32_t>(block) * kMemCap) {
+        if (ndef && main_kind != kCtaGiant && g->n > static_cast<uint32_t>(block) * kMemCap) {
           acc.deferred += ndef;
           reserve_rows_for(ndef);
           ndef = pass(kCtaGiant, dlist, ndef, dspare);

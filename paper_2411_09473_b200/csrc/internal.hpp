@@ -146,6 +146,7 @@ struct rrg_graph {
   int ic_rng = 0;                // IC: 0 the reference's stream (exact), 1 fast (statistical)
   uint32_t ic_coop_min = 256;    // IC: in-lists at least this long expand warp-cooperatively
   int ic_mode = 0;               // IC: 0 auto, 1 lane, 2 warp, 3 block per sample
+  bool ic_giant = false;         // IC auto: run the block schedule over the giant scratch
   double ic_mean_insp = -1.0;    // IC: running mean of inspected in-edges per set
   double ic_hub_insp = 1e5;       // auto: warp per sample from this mean on (cfg5 ~1M)
   double ic_cta_max_edges = 1.5e8;  // auto: block per sample up to this many expected
