@@ -78,6 +78,8 @@ def parse():
     ap.add_argument("--no-imm", action="store_true")
     ap.add_argument("--no-graph-prep", action="store_true",
                     help="skip the edge-list -> transpose comparison (device vs reference)")
+    ap.add_argument("--sharded-imm", type=int, default=1,
+                    help="time run_imm_sharded over all ranks (NCCL exchange); 0 = skip")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the IC sampling blocks (cfg1, cfg5) and the five-config IMM table")
     ap.add_argument("--ic-sets", default="cfg1:1048576,cfg5:32768",
@@ -794,6 +796,46 @@ def run_ours(args, rank, world, local):
                 "theta_match": (r.theta, r.theta_prime, r.lower_bound) ==
                                (rr["theta"], rr["theta_prime"], rr["lower_bound"]),
                 "influence_estimate": n * sum(r.seeds.marginal_counts) / r.sets_generated}
+    # ---- multi-GPU IMM through the drop-in (rrg_run_imm_sharded) -------------
+    # every rank samples its shard of each top-up; the shards' device buffers go
+    # over NCCL; wall time = max over ranks; the result must equal single-GPU
+    # run_imm (rank 0 checks)
+    if not args.no_imm and args.sharded_imm:
+        from paper_2411_09473_b200 import parallel as PP
+        try:
+            store.close()
+        except Exception:
+            pass
+        icfg = P.ImmConfig(k=cfg.k, epsilon=cfg.epsilon, model=model)
+        if dist:
+            group = dist.new_group(backend="gloo")  # the 128-byte id travels over gloo
+            uid = PP.share_unique_id(P.nccl_unique_id, group)
+        else:
+            uid = P.nccl_unique_id()
+        comm = P.NcclComm(uid, world, rank)
+        P.run_imm_sharded(g, icfg, comm)  # warm-up
+        walls = []
+        for _ in range(3):
+            barrier()
+            t0 = time.perf_counter()
+            rs = P.run_imm_sharded(g, icfg, comm)
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+        comm.close()
+        wt = torch.tensor([statistics.median(walls)], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        single = P.run_imm(g, icfg) if rank == 0 else None
+        line["imm_sharded"] = {
+            "workload": args.workload, "ranks": world, "k": cfg.k, "epsilon": cfg.epsilon,
+            "wall_s": float(wt.item()),
+            "wall_note": "median of 3 after a warm-up, max over ranks; graph resident",
+            "exchange": "per top-up: ncclAllGather of shard sizes + ncclBroadcast of each "
+                        "rank's device buffers (lists, offsets, rows), appended in slot order",
+            "equals_single_gpu": (rs.seeds.seeds == single.seeds.seeds and
+                                  rs.seeds.marginal_counts == single.seeds.marginal_counts and
+                                  rs.theta == single.theta) if single else None}
+
     # ---- IC sampling blocks and the five-config IMM table (rank 0, N=1) ------
     if rank == 0 and world == 1 and not args.no_extra:
         orc_x = None

@@ -223,6 +223,24 @@ rrg_status rrg_sampling_phase(rrg_graph* g, const rrg_imm_config* cfg, rrg_store
                               double* lower_bound, uint64_t* theta_prime,
                               rrg_imm_result* timings);
 
+/* ---- multi-GPU IMM ----------------------------------------
+ * One process per GPU sharing an NCCL communicator (NCCL is loaded at first use:
+ * libnccl.so.2). rrg_nccl_unique_id on one rank, the 128 bytes passed to every
+ * rank (e.g. over torch.distributed), rrg_nccl_comm_create on each with the
+ * rank's device current. rrg_run_imm_sharded: every top-up's new slots are split
+ * into nranks contiguous shards, rank r samples shard r with no communication
+ * (slot j depends only on (run_seed, j), sampling.hpp:179), the shards' device
+ * buffers are broadcast over NCCL and appended in slot order on every rank; the
+ * selection runs replicated. Every rank returns the result of rrg_run_imm.
+ * nccl_comm == NULL with sim_ranks >= 1: the same shard split and ordered
+ * assembly in one process (no transport; parity of the sharding). */
+rrg_status rrg_nccl_unique_id(uint8_t* id /* [128] */);
+rrg_status rrg_nccl_comm_create(const uint8_t* id, int nranks, int rank, void** comm);
+void rrg_nccl_comm_destroy(void* comm);
+rrg_status rrg_run_imm_sharded(rrg_graph* g, const rrg_imm_config* cfg, void* nccl_comm,
+                               int sim_ranks, uint32_t* seeds, uint64_t* marginals,
+                               rrg_imm_result* out);
+
 /* ---- parity / interop --------------------------------------------------- */
 /* Copies sets [first, first+count) to the host: offsets u64[count+1] (relative to
  * the first set), members in visit order (root first, sampling.hpp:93-94). */

@@ -30,7 +30,8 @@ __all__ = [
     "DiffusionModel", "Graph", "RRRStore", "SeedSet", "ImmConfig", "ImmResult",
     "generate_batch", "generate_batch_fused", "select_seeds", "fraction_covered",
     "run_imm", "build_graph", "normalize_lt_weights", "RRGError", "RRGOutOfMemory",
-    "version", "BatchStats", "SelectionStats",
+    "version", "BatchStats", "SelectionStats", "run_imm_sharded", "NcclComm",
+    "nccl_unique_id",
 ]
 
 kDefaultDensityDivisor = 64  # rrr_set.hpp:13
@@ -500,13 +501,65 @@ def sampling_phase(g: Graph, cfg: ImmConfig) -> SamplingPhaseResult:
 
 def run_imm(g: Graph, cfg: ImmConfig) -> ImmResult:
     """imm.hpp:214-251, driven by the C++17 driver in csrc/imm.cpp."""
+    return _run_imm(g, cfg, None, 0)
+
+
+def run_imm_sharded(g: Graph, cfg: ImmConfig, comm: Optional["NcclComm"] = None,
+                    sim_ranks: int = 0) -> ImmResult:
+    """Multi-GPU run_imm: every rank of `comm` samples its shard
+    of each top-up, the shards are exchanged over NCCL from device memory, and
+    every rank returns run_imm's result. comm=None with sim_ranks >= 1 runs the
+    same shard split in one process."""
+    return _run_imm(g, cfg, comm, sim_ranks)
+
+
+class NcclComm:
+    """An NCCL communicator for rrg_run_imm_sharded: one per rank, created with
+    this process's GPU current (torch.cuda.set_device) from the 128-byte id of
+    nccl_unique_id() on rank 0, passed to all ranks."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(lib.rrg_nccl_comm_create(buf, int(nranks), int(rank), C.byref(h)))
+        self._h = h
+        self.nranks, self.rank = nranks, rank
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.rrg_nccl_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib.rrg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def _run_imm(g: Graph, cfg: ImmConfig, comm, sim_ranks: int) -> ImmResult:
     c = _imm_config(cfg)
     k = max(int(cfg.k), 1)
     seeds = np.zeros(k, dtype=np.uint32)
     marg = np.zeros(k, dtype=np.uint64)
     r = _lib.ImmResultC()
-    check(lib.rrg_run_imm(g.handle, C.byref(c), ptr(seeds, C.c_uint32), ptr(marg, C.c_uint64),
-                          C.byref(r)))
+    if comm is None and sim_ranks == 0:
+        check(lib.rrg_run_imm(g.handle, C.byref(c), ptr(seeds, C.c_uint32),
+                              ptr(marg, C.c_uint64), C.byref(r)))
+    else:
+        check(lib.rrg_run_imm_sharded(g.handle, C.byref(c), comm.handle if comm else None,
+                                      int(sim_ranks), ptr(seeds, C.c_uint32),
+                                      ptr(marg, C.c_uint64), C.byref(r)))
     return ImmResult(
         seeds=SeedSet([int(x) for x in seeds], [int(x) for x in marg]),
         theta=r.theta, theta_prime=r.theta_prime, lower_bound=r.lower_bound,

@@ -77,6 +77,11 @@ SIGNATURES = [
     ("rrg_store_destroy", None, [vp]),
     ("rrg_store_clear", C.c_int, [vp]),
     ("rrg_store_dense_info", C.c_int, [vp, u64p, u64p, u64p, u64p]),
+    ("rrg_nccl_unique_id", C.c_int, [u8p]),
+    ("rrg_nccl_comm_create", C.c_int, [u8p, C.c_int, C.c_int, C.POINTER(vp)]),
+    ("rrg_nccl_comm_destroy", None, [vp]),
+    ("rrg_run_imm_sharded", C.c_int, [vp, C.POINTER(ImmConfigC), vp, C.c_int, u32p, u64p,
+                                      C.POINTER(ImmResultC)]),
     ("rrg_store_live_count", C.c_int, [vp, u64p]),
     ("rrg_store_live_flags", C.c_int, [vp, C.c_uint64, C.c_uint64, u8p]),
     ("rrg_store_set_counter", C.c_int, [vp, u64p]),

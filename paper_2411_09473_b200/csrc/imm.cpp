@@ -14,6 +14,9 @@
 
 namespace rrgpu {
 void set_error(const std::string& msg);
+// shard.cu (multi-GPU): NCCL exchange of this rank's shard + ordered append
+rrg_status exchange_and_append(rrg_store* side, rrg_store* dst, void* comm);
+void nccl_comm_shape(void* comm, int* nranks, int* rank);
 }
 
 namespace {
@@ -122,10 +125,11 @@ rrg_status validate(rrg_graph* g, const rrg_imm_config* cfg) {
 // selections, timed like ImmTimings (imm.hpp:38-42).
 class Driver {
  public:
-  Driver(rrg_graph* g, const rrg_imm_config* cfg, rrg_store* store)
+  Driver(rrg_graph* g, const rrg_imm_config* cfg, rrg_store* store, void* comm = nullptr,
+         int sim_ranks = 0)
       : g_(g), cfg_(cfg), store_(store), n_(rrg_graph_num_vertices(g)),
         ell_(effective_ell(cfg->ell, n_)), fused_(cfg->strategy == RRG_STRATEGY_FUSED),
-        trial_seeds_(cfg->k), trial_marg_(cfg->k) {}
+        comm_(comm), sim_ranks_(sim_ranks), trial_seeds_(cfg->k), trial_marg_(cfg->k) {}
 
   double ell() const { return ell_; }
   uint64_t size() const { return size_; }
@@ -137,8 +141,37 @@ class Driver {
   // store ends up with exactly the reference's sets. Small batches are bound by
   // the latency of their largest set, so one batch covering the next rounds
   // costs about what one round's batch does.
+  // Multi-GPU top-up: the new slots [size, target) split into
+  // contiguous shards, rank r samples shard r (no communication), the shards are
+  // exchanged over NCCL and appended in rank (= slot) order on every rank.
+  // comm == nullptr with sim_ranks >= 1: the same split and ordered assembly in
+  // one process (parity of the shard arithmetic without a second GPU).
+  rrg_status top_up_sharded(uint64_t target) {
+    const auto t = std::chrono::steady_clock::now();
+    const uint64_t count = target - size_;
+    int nranks = sim_ranks_, rank = 0;
+    if (comm_) rrgpu::nccl_comm_shape(comm_, &nranks, &rank);
+    rrg_status s = RRG_OK;
+    if (!ahead_.s) s = rrg_store_create(g_, &ahead_.s);
+    for (int r = comm_ ? rank : 0; s == RRG_OK && r < (comm_ ? rank + 1 : nranks); ++r) {
+      const uint64_t a = count * static_cast<uint64_t>(r) / nranks;
+      const uint64_t b = count * static_cast<uint64_t>(r + 1) / nranks;
+      s = rrg_store_clear(ahead_.s);
+      uint64_t made = 0;
+      if (s == RRG_OK && b > a)
+        s = rrg_generate_slots(g_, static_cast<rrg_model>(cfg_->model), cfg_->rng_seed,
+                               size_ + a, b - a, ahead_.s, fused_ ? 1 : 0, 64, &made);
+      if (s == RRG_OK && !comm_) s = rrg_store_append_from(store_, ahead_.s, 0, b - a);
+    }
+    if (s == RRG_OK && comm_) s = rrgpu::exchange_and_append(ahead_.s, store_, comm_);
+    if (s == RRG_OK) size_ = target;
+    t_generate += seconds_since(t);
+    return s;
+  }
+
   rrg_status top_up(uint64_t target, uint64_t ahead) {
     if (target <= size_) return RRG_OK;
+    if (comm_ || sim_ranks_ > 0) return top_up_sharded(target);
     const auto t = std::chrono::steady_clock::now();
     rrg_status s = RRG_OK;
     const bool covered = ahead_count_ && ahead_first_ <= size_ && target <= ahead_first_ + ahead_count_;
@@ -232,6 +265,8 @@ class Driver {
   uint32_t n_;
   double ell_;
   bool fused_;
+  void* comm_ = nullptr;  // NCCL communicator (multi-GPU), or null
+  int sim_ranks_ = 0;     // > 0: shards simulated in-process
   StoreGuard ahead_;
   uint64_t ahead_first_ = 0, ahead_count_ = 0;
   uint64_t size_ = 0;
@@ -278,9 +313,15 @@ rrg_status rrg_sampling_phase(rrg_graph* g, const rrg_imm_config* cfg, rrg_store
   return RRG_OK;
 }
 
-// run_imm (imm.hpp:214-251)
-rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
-                       uint64_t* marginals, rrg_imm_result* out) {
+}  // extern "C"
+
+namespace {
+
+// run_imm (imm.hpp:214-251) on one GPU (comm == nullptr, sim_ranks == 0), N
+// GPUs (an NCCL communicator: every rank returns the same result) or shards
+// simulated in one process (sim_ranks >= 1).
+rrg_status run_imm_impl(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
+                        uint64_t* marginals, rrg_imm_result* out, void* comm, int sim_ranks) {
   const auto t_total = std::chrono::steady_clock::now();
   if (!g || !cfg || !seeds || !marginals || !out) {
     rrgpu::set_error("run_imm: null argument");
@@ -293,7 +334,7 @@ rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
   StoreGuard store;
   st = rrg_store_create(g, &store.s);
   if (st != RRG_OK) return st;
-  Driver d(g, cfg, store.s);
+  Driver d(g, cfg, store.s, comm, sim_ranks);
   st = d.sampling_phase(&out->lower_bound);
   if (st != RRG_OK) return st;
   out->theta_prime = d.size();
@@ -319,6 +360,30 @@ rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
   out->t_select = d.t_select;
   out->t_total = seconds_since(t_total);
   return RRG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rrg_status rrg_run_imm(rrg_graph* g, const rrg_imm_config* cfg, uint32_t* seeds,
+                       uint64_t* marginals, rrg_imm_result* out) {
+  return run_imm_impl(g, cfg, seeds, marginals, out, nullptr, 0);
+}
+
+rrg_status rrg_run_imm_sharded(rrg_graph* g, const rrg_imm_config* cfg, void* nccl_comm,
+                               int sim_ranks, uint32_t* seeds, uint64_t* marginals,
+                               rrg_imm_result* out) {
+  if (!nccl_comm && sim_ranks < 1) {
+    rrgpu::set_error("run_imm_sharded: need an NCCL communicator or sim_ranks >= 1");
+    return RRG_EINVAL;
+  }
+  try {
+    return run_imm_impl(g, cfg, seeds, marginals, out, nccl_comm, nccl_comm ? 0 : sim_ranks);
+  } catch (const std::exception& e) {  // NCCL loading / communicator errors
+    rrgpu::set_error(e.what());
+    return RRG_ECUDA;
+  }
 }
 
 }  // extern "C"

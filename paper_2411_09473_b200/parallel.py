@@ -206,3 +206,27 @@ def sharded_imm(n: int, k: int, epsilon: float, ell: float,
     seeds, marg = select_fn(off, mem, merged)
     del local_off, local_mem
     return ShardedImmResult(list(seeds), list(marg), theta, theta_prime, lb, size)
+
+
+def share_unique_id(make_id: Callable[[], bytes], group=None) -> bytes:
+    """Rank 0's NCCL unique id (128 bytes), handed to every rank over the
+    torch.distributed group (gloo or nccl)."""
+    import torch.distributed as dist
+    obj = [make_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+def run_imm_distributed(g, cfg, group=None):
+    """run_imm over every rank of `group`, one GPU each (the current device):
+    rrg_run_imm_sharded with an NCCL communicator of the group's ranks -- each
+    top-up's shards sampled locally and exchanged as device buffers over NCCL;
+    every rank returns the same ImmResult as single-GPU run_imm."""
+    import torch.distributed as dist
+    from . import NcclComm, nccl_unique_id, run_imm_sharded
+    uid = share_unique_id(nccl_unique_id, group)
+    comm = NcclComm(uid, dist.get_world_size(group), dist.get_rank(group))
+    try:
+        return run_imm_sharded(g, cfg, comm)
+    finally:
+        comm.close()

@@ -92,3 +92,38 @@ def test_sharded_imm_world2_equals_single_process(port, model, name):
         assert theta == ref["theta"] and theta_p == ref["theta_prime"]
         assert lb == ref["lower_bound"]
         assert sets == ref["sets_generated"]
+
+
+def _uid_worker(rank, world, port_no, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    calls = []
+
+    def make_id():
+        calls.append(rank)
+        return bytes(range(128))[::-1]
+
+    uid = parallel.share_unique_id(make_id)
+    q.put((rank, uid, calls))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_unique_id_reaches_every_rank():
+    """rrg_run_imm_sharded's communicator setup: only rank 0 makes the 128-byte
+    NCCL id, every rank receives the same bytes (world size 3, gloo)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = free_port()
+    procs = [ctx.Process(target=_uid_worker, args=(r, 3, port_no, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = bytes(range(128))[::-1]
+    assert all(uid == want for _, uid, _ in results)
+    assert [calls for _, _, calls in results] == [[0], [], []]
