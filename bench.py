@@ -258,7 +258,7 @@ def run_reference(args, rank):
         "e2e": {"value": value, "unit": "sets/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def graph_prep(P, orc, roff, rsrc, rw, model):
@@ -857,20 +857,51 @@ def run_ours(args, rank, world, local):
         for name in filter(None, args.imm_configs.split(",")):
             line["imm_all"][name] = imm_block(P, name, orc_x, cores)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+class StdoutToStderr:
+    """Native libraries (NCCL's version banner, CUDA) may print to fd 1; the
+    contract is ONE JSON line on stdout, so fd 1 points at stderr until the
+    line is printed."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def restore(self):
+        if self.saved is not None:
+            sys.stdout.flush()
+            os.dup2(self.saved, 1)
+            os.close(self.saved)
+            self.saved = None
+
+    def __exit__(self, *exc):
+        self.restore()
+
+
+QUIET = StdoutToStderr()
+
+
+def emit(line):
+    QUIET.restore()
+    print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
     args.ic_cpu_sets = {"cfg1": 1 << 16, "cfg3": 1 << 16, "cfg5": 2048}
     rank, world, local = dist_env()
-    if args.impl == "reference":
-        run_reference(args, rank)
-        return
-    run_ours(args, rank, world, local)
+    with QUIET:
+        if args.impl == "reference":
+            run_reference(args, rank)
+            return
+        run_ours(args, rank, world, local)
 
 
 if __name__ == "__main__":

@@ -510,7 +510,7 @@ def run_imm_sharded(g: Graph, cfg: ImmConfig, comm: Optional["NcclComm"] = None,
     of each top-up, the shards are exchanged over NCCL from device memory, and
     every rank returns run_imm's result. comm=None with sim_ranks >= 1 runs the
     same shard split in one process."""
-    return _run_imm(g, cfg, comm, sim_ranks)
+    return _run_imm(g, cfg, comm, sim_ranks, sharded=True)
 
 
 class NcclComm:
@@ -547,13 +547,13 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def _run_imm(g: Graph, cfg: ImmConfig, comm, sim_ranks: int) -> ImmResult:
+def _run_imm(g: Graph, cfg: ImmConfig, comm, sim_ranks: int, sharded: bool = False) -> ImmResult:
     c = _imm_config(cfg)
     k = max(int(cfg.k), 1)
     seeds = np.zeros(k, dtype=np.uint32)
     marg = np.zeros(k, dtype=np.uint64)
     r = _lib.ImmResultC()
-    if comm is None and sim_ranks == 0:
+    if not sharded:
         check(lib.rrg_run_imm(g.handle, C.byref(c), ptr(seeds, C.c_uint32),
                               ptr(marg, C.c_uint64), C.byref(r)))
     else:

@@ -212,7 +212,10 @@ void sync(rrg_graph* g) { RRG_CUDA(cudaStreamSynchronize(g->stream)); }
 void ensure_rows(rrg_store* s, uint64_t need, uint64_t keep = UINT64_MAX) {
   rrg_graph* g = s->g;
   if (keep == UINT64_MAX) keep = s->ndense;
-  if (need * s->dwords <= s->dbits.cap && need <= s->dlen.cap) return;
+  // (the caching allocator may grant any of the four more than asked: check each)
+  if (need * s->dwords <= s->dbits.cap && need <= s->dlen.cap && need <= s->droot.cap &&
+      need <= s->dslot.cap)
+    return;
   const uint64_t rows = std::max<uint64_t>(need, std::max<uint64_t>(16, s->dlen.cap + s->dlen.cap / 2));
   s->dbits.reserve_keep(rows * s->dwords, keep * s->dwords, g->stream);
   s->dlen.reserve_keep(rows, keep, g->stream);
@@ -221,7 +224,9 @@ void ensure_rows(rrg_store* s, uint64_t need, uint64_t keep = UINT64_MAX) {
 }
 
 uint64_t rows_cap(const rrg_store* s) {
-  return s->dwords ? std::min<uint64_t>(s->dbits.cap / s->dwords, s->dlen.cap) : 0;
+  if (!s->dwords) return 0;
+  return std::min<uint64_t>(std::min<uint64_t>(s->dbits.cap / s->dwords, s->dlen.cap),
+                            std::min<uint64_t>(s->droot.cap, s->dslot.cap));
 }
 
 // Appends `count` already-staged sets (slot_len/slot_start in the store's staging
