@@ -191,6 +191,26 @@ constexpr uint32_t kGuidePivot = 0x3fffffffu;
 
 __device__ __forceinline__ uint32_t vhash(uint32_t v) { return v * 0x9E3779B1u; }
 
+// RRG_CHECKED builds (librrgpu_checked.so, tests/test_gpu_checked.py): bounds
+// checks at the buffer writes that matter -- member ids < n, list positions
+// within their scratch, staging / row / export positions within their buffers
+// -- trap with a code instead of corrupting memory. compute-sanitizer is not
+// available on the GPU pool; this build is what the parity fixtures run under.
+#ifdef RRG_CHECKED
+#define RRG_DCHECK(cond, code)                                                      \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("rrgpu check %d failed: blk %d thr %d at %s:%d\n", (code), blockIdx.x,   \
+             threadIdx.x, __FILE__, __LINE__);                                      \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define RRG_DCHECK(cond, code) \
+  do {                         \
+  } while (0)
+#endif
+
 // RRG_PROBE_GUARD (debug builds): a probe chain longer than the table traps
 // with a code naming the loop, instead of spinning forever.
 #ifdef RRG_PROBE_GUARD

@@ -54,6 +54,7 @@ __global__ void k_densify(const uint32_t* dreq, uint64_t nreq, const uint32_t* s
     const uint32_t* from = stage + slot_start[i];
     for (uint32_t t = lane; t < len; t += 32) {
       const uint32_t v = from[t];
+      RRG_DCHECK(v < dwords * 32u, 9);
       atomicOr(dst + (v >> 5), 1u << (v & 31));
     }
     __syncwarp();
@@ -155,6 +156,7 @@ __global__ void k_materialize(const uint64_t* off, const uint32_t* mem, const ui
       while (x) {
         const int b = __ffs(x) - 1;
         x &= x - 1;
+        RRG_DCHECK(at < xoff[i + 1], 10);
         xmem[at++] = w * 32 + b;
       }
       pos += __shfl_sync(kFull, incl, 31);

@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
     } else {
       for (uint32_t i = lane; i < nmem; i += 32) {
         const uint32_t v = mem[i];
+        RRG_DCHECK(v < p.n && nmem <= p.n, 8);
         p.stage[pos + i] = v;
         if (p.counter) atomicAdd(p.counter + v, 1u);
       }

@@ -1703,6 +1703,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       __syncthreads();
       for (uint32_t t = tid; t < nmem; t += kBlock) {
         const uint32_t v = mem[t];
+        RRG_DCHECK(v < p.n, 7);
         atomicOr(dst + (v >> 5), 1u << (v & 31));
         if (p.counter) atomicAdd(p.counter + v, 1u);
       }
@@ -1728,6 +1729,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
     }
     for (uint32_t t = tid; t < nmem; t += kBlock) {
       const uint32_t v = mem[t];
+      RRG_DCHECK(v < p.n && nmem <= kCap, 6);
       p.stage[pos + t] = v;
       if (p.counter) atomicAdd(p.counter + v, 1u);
     }

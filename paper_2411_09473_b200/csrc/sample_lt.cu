@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
       defer_slot(p, idx);
       active = false;
     } else {  // v is in the table already (tab_find_or_insert)
+      RRG_DCHECK(nmem < kMemCap && v < p.n, 5);
       mem[nmem++] = v;
       if (2 * nmem > (1u << lg)) {  // grow: re-insert under a fresh tag
         ++lg;
@@ -374,6 +375,7 @@ __device__ __forceinline__ bool warp_emit_pending(const SampleParams& p, bool pe
       for (uint32_t k = 0; k < 4; ++k) {
         const uint32_t i = t + 32 * k + lane;
         if (i < nL) {
+          RRG_DCHECK(v[k] < p.n && pos + i < p.stage_cap, 3);
           out[i] = v[k];
           if (p.counter) atomicAdd(p.counter + v[k], 1u);
         }
@@ -450,6 +452,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_sample_lt_guide(const Sa
           lfilt_bits<kFiltLog>(vL, w1, b1, w2, b2);
           filt[w1 * kBlock] |= 1u << b1;
           filt[w2 * kBlock] |= 1u << b2;
+          RRG_DCHECK(nmem < kMemCap && vL < p.n, 4);
           mem[nmem++] = vL;
           offu = offc;
           degu = degc;
@@ -537,6 +540,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_sample_lt_guide(const Sa
       defer_slot(p, idx);
       active = false;
     } else {
+      RRG_DCHECK(nmem < kMemCap && v < p.n, 5);
       mem[nmem++] = v;
       rebuild = !big && nmem == kLtFiltMax;
       offu = offv;

@@ -44,12 +44,14 @@ __device__ __forceinline__ bool emit_set(const SampleParams& p, uint32_t idx, co
     for (int q = 0; q < 8; ++q) v[q] = mem[t + q];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
+      RRG_DCHECK(v[q] < p.n, 1);
       out[t + q] = v[q];
       if (p.counter) atomicAdd(p.counter + v[q], 1u);
     }
   }
   for (; t < nmem; ++t) {
     const uint32_t v = mem[t];
+    RRG_DCHECK(v < p.n, 1);
     out[t] = v;
     if (p.counter) atomicAdd(p.counter + v, 1u);
   }
@@ -125,6 +127,7 @@ __device__ __forceinline__ bool fetch_slot_q(const SampleParams& p, bool need, b
 // table by rehash when the load would exceed 1/2.
 __device__ __forceinline__ void lane_insert(uint32_t* mem, uint64_t* tab, uint32_t& tag,
                                             uint32_t& lg, uint32_t& nmem, uint32_t v) {
+  RRG_DCHECK(nmem < kMemCap, 2);
   mem[nmem++] = v;
   if (2 * nmem > (1u << lg)) {
     ++lg;

@@ -93,6 +93,7 @@ __device__ __forceinline__ void warp_cover(const SelectParams& p, uint64_t s) {
   const uint64_t b = p.off[s], e = p.off[s + 1];
   for (uint64_t j = b + lane; j < e; j += 32) {
     const uint32_t u = p.mem[j];
+    RRG_DCHECK(u < p.n, 11);
     atomicSub(p.cnt + u, 1u);
     p.dirty[u >> kSelTileLog] = 1u;
   }

@@ -137,6 +137,7 @@ __global__ void k_compact(const uint32_t* stage, const uint64_t* slot_start,
     const uint32_t* from = stage + slot_start[i];
     const uint64_t dst = base_total + scan[i];
     for (uint32_t t = lane; t < len; t += 32) mem_out[dst + t] = from[t];
+    RRG_DCHECK(len < (1u << 31), 12);
     if (lane == 0) off_out[i + 1] = dst + len;
     mx = max(mx, len);
   }
