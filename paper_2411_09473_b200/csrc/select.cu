@@ -360,9 +360,220 @@ __global__ void __launch_bounds__(kSelBlock, 1) k_select(const SelectParams p) {
   if (tid == 0) p.status[0] = p.k;
 }
 
+// ---------------------------------------------------------------------------
+// Cluster-resident variant (stores scanned per round, no dense rows, no counter
+// snapshots): ONE cluster of kClCtas blocks runs all k rounds. Every block keeps
+// a full replica of the tile maxima in shared memory, so the argmax of a round
+// is a block-local reduction (no global round trip, same key in every block).
+// The scan-mode cover is the grid kernel's; a decremented vertex flags its tile
+// in the OWNER block's shared bitmap (tile t belongs to block t % kClCtas,
+// a distributed-shared-memory atomic), and after the cluster barrier each block
+// re-reduces its flagged tiles and writes the new maxima into all kClCtas
+// replicas (DSMEM stores) before the second barrier. Two cluster barriers
+// (~0.2 us each) per round instead of two grid barriers across 148 SMs.
+// ---------------------------------------------------------------------------
+constexpr int kClBlock = 1024;
+constexpr int kClCtas = 16;
+
+__device__ __forceinline__ unsigned long long cl_block_max(unsigned long long x,
+                                                           unsigned long long* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) x = umax64(x, __shfl_xor_sync(kFull, x, o));
+  __syncthreads();
+  if (lane == 0) red[wid] = x;
+  __syncthreads();
+  x = lane < kClBlock / 32 ? red[lane] : 0ull;
+  for (int o = 16; o; o >>= 1) x = umax64(x, __shfl_xor_sync(kFull, x, o));
+  return x;
+}
+
+__global__ void __launch_bounds__(kClBlock, 1) k_select_cluster(const SelectParams p) {
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned crank = cl.block_rank();
+  const uint32_t ntiles = (p.n + kSelTile - 1) >> kSelTileLog;
+  extern __shared__ unsigned long long cl_smem[];
+  unsigned long long* tmax = cl_smem;                                      // [ntiles]
+  unsigned long long* red = tmax + ntiles;                                 // [32]
+  uint32_t* dirty = reinterpret_cast<uint32_t*>(red + kClBlock / 32);      // [ntiles/32 + 1]
+  const uint32_t dwords_t = (ntiles >> 5) + 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t tid = static_cast<uint64_t>(crank) * kClBlock + threadIdx.x;
+  const uint64_t nthreads = static_cast<uint64_t>(kClCtas) * kClBlock;
+  const uint64_t gwarp = tid >> 5, nwarps = nthreads >> 5;
+  for (uint32_t i = threadIdx.x; i < dwords_t; i += kClBlock) dirty[i] = 0u;
+  // initial maxima: warp per tile across the cluster, broadcast to every replica
+  for (uint64_t t = gwarp; t < ntiles; t += nwarps) {
+    const unsigned long long m = tile_max_warp(p, static_cast<uint32_t>(t));
+    if (lane < kClCtas) cl.map_shared_rank(tmax, lane)[t] = m;
+  }
+  cl.sync();
+
+  auto flag_tile = [&](uint32_t u) {
+    const uint32_t t = u >> kSelTileLog;
+    uint32_t* d = cl.map_shared_rank(dirty, t % kClCtas);
+    atomicOr(d + ((t / kClCtas) >> 5), 1u << ((t / kClCtas) & 31));
+  };
+
+  unsigned long long covered_sum = 0;
+  for (uint32_t r = 0; r < p.k; ++r) {
+    // ---- A: argmax over the local replica --------------------------------------
+    unsigned long long best = 0;
+    for (uint32_t t = threadIdx.x; t < ntiles; t += kClBlock) best = umax64(best, tmax[t]);
+    const unsigned long long key = cl_block_max(best, red);
+    const uint32_t top = static_cast<uint32_t>(key >> 32);
+    const uint32_t v = 0xffffffffu - static_cast<uint32_t>(key);
+    if (top == 0) {
+      if (tid == 0) {  // exhaustion (selection.hpp:61-72)
+        uint32_t filled = r;
+        for (uint32_t u = 0; u < p.n && filled < p.k; ++u) {
+          if (!p.selected[u]) {
+            p.selected[u] = 1;
+            p.seeds[filled] = u;
+            p.marg[filled] = 0;
+            ++filled;
+          }
+        }
+        p.status[0] = r;
+      }
+      cl.sync();  // no block leaves while others may still write its shared memory
+      return;
+    }
+    const unsigned long long live = p.nsets - covered_sum;
+    const bool rebuild = live > 0 && static_cast<double>(top) / static_cast<double>(live) >
+                                         p.adaptive_threshold;
+
+    // ---- B: scan-mode cover (see k_select) ----------------------------------
+    unsigned long long killed = 0;
+    const uint64_t nchunk = (p.total + 255) / 256;
+    for (uint64_t c = gwarp; c < nchunk; c += nwarps) {
+      const uint64_t base = c * 256 + static_cast<uint64_t>(lane) * 8;
+      uint32_t q[8];
+      if (base + 8 <= p.total) {
+        const uint4 a = *reinterpret_cast<const uint4*>(p.wmem + base);
+        const uint4 b = *reinterpret_cast<const uint4*>(p.wmem + base + 4);
+        q[0] = a.x; q[1] = a.y; q[2] = a.z; q[3] = a.w;
+        q[4] = b.x; q[5] = b.y; q[6] = b.z; q[7] = b.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = base + j < p.total ? p.wmem[base + j] : kBlank;
+      }
+      uint32_t hits = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) hits |= (q[j] == v ? 1u : 0u) << j;
+      killed += __popc(hits);
+      while (__any_sync(kFull, hits != 0)) {
+        const uint64_t w = hits ? p.span[base + (__ffs(hits) - 1)] : 0ull;
+        unsigned hm = __ballot_sync(kFull, hits != 0);
+        if (hits) hits &= hits - 1;
+        while (hm) {
+          const int L = __ffs(hm) - 1;
+          hm &= hm - 1;
+          const uint64_t wL = __shfl_sync(kFull, w, L);
+          const uint64_t sb = wL >> 32, se = sb + (wL & 0xffffffffull);
+          for (uint64_t t = sb + lane; t < se; t += 32) {
+            const uint32_t u = p.wmem[t];
+            if (!rebuild) {
+              atomicSub(p.cnt + u, 1u);
+              flag_tile(u);
+            }
+            p.wmem[t] = kBlank;
+          }
+        }
+      }
+    }
+    for (int o = 16; o; o >>= 1) killed += __shfl_xor_sync(kFull, killed, o);
+    if (lane == 0 && killed) atomicAdd(p.marg + r, killed);
+    if (tid == 0) {
+      p.keys[r] = key;
+      p.seeds[r] = v;
+      p.selected[v] = 1;
+      if (rebuild) atomicAdd(p.rebuilds, 1ull);
+    }
+    cl.sync();
+    covered_sum += p.marg[r];
+
+    if (rebuild) {  // rebuild_update: zero, recount the surviving sets
+      for (uint64_t u = tid; u < p.n; u += nthreads) p.cnt[u] = 0u;
+      cl.sync();
+      for (uint64_t t = tid; t < p.total; t += nthreads) {
+        const uint32_t u = p.wmem[t];
+        if (u != kBlank) atomicAdd(p.cnt + u, 1u);
+      }
+      cl.sync();
+    }
+
+    // ---- C: re-reduce this block's flagged tiles, broadcast the maxima ---------
+    const uint32_t owned = ntiles > crank ? (ntiles - crank + kClCtas - 1) / kClCtas : 0;
+    for (uint32_t j = wid; j < owned; j += kClBlock / 32) {
+      const bool d = rebuild || ((dirty[j >> 5] >> (j & 31)) & 1u);
+      if (!d) continue;  // uniform in the warp
+      const uint32_t t = j * kClCtas + crank;
+      const unsigned long long m = tile_max_warp(p, t);
+      if (lane < kClCtas) cl.map_shared_rank(tmax, lane)[t] = m;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < dwords_t; i += kClBlock) dirty[i] = 0u;
+    cl.sync();
+  }
+  if (tid == 0) p.status[0] = p.k;
+}
+
 }  // namespace
 
+// The cluster-resident selection when the store qualifies (scan mode, no dense
+// rows, no per-round snapshots, tile maxima within shared memory) and the
+// device can place a 16-block cluster; false otherwise (caller uses the grid).
+// Measured (profiles/r2/sel_r2n.log, k = 50 over 8,192 sets): cfg2 (238K members)
+// 0.42 vs 0.57 ms, cfg1 (114K) 0.39 vs 0.50, cfg3 (75K) 0.65 vs 0.75; cfg4
+// (667K members, 2,367 tiles) 0.92 vs 0.65 -- 16 SMs re-scan a large store
+// slower than 148 -- so the cluster takes stores of up to 2^19 members.
+constexpr uint64_t kClMaxMembers = 1ull << 19;
+
+bool launch_select_cluster(const SelectParams& p, cudaStream_t s) {
+  if (!p.scan || p.nd || p.snap) return false;
+  bool force = false;
+  if (const char* e = std::getenv("RRGPU_SELECT_CLUSTER")) {  // tests / tuning: 0 off, 1 always
+    if (*e == '0') return false;
+    force = *e == '1';
+  }
+  if (!force && p.total > kClMaxMembers) return false;
+  const uint32_t ntiles = (p.n + kSelTile - 1) >> kSelTileLog;
+  const size_t smem = static_cast<size_t>(ntiles) * 8 + (kClBlock / 32) * 8 + ((ntiles >> 5) + 1) * 4;
+  if (smem > 200 * 1024) return false;
+  static int ok = -1;
+  if (ok < 0) {
+    ok = cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                 cudaSuccess &&
+         cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              200 * 1024) == cudaSuccess;
+    cudaGetLastError();
+  }
+  if (!ok) return false;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kClCtas);
+  cfg.blockDim = dim3(kClBlock);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kClCtas;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, k_select_cluster, &cfg) != cudaSuccess ||
+      clusters < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  RRG_CUDA(cudaLaunchKernelEx(&cfg, k_select_cluster, p));
+  count_launch();
+  return true;
+}
+
 void launch_select(const SelectParams& p, int num_sms, cudaStream_t s) {
+  if (launch_select_cluster(p, s)) return;
   const void* fn = p.scan ? reinterpret_cast<const void*>(k_select<true>)
                           : reinterpret_cast<const void*>(k_select<false>);
   int per_sm = 0;

@@ -161,3 +161,28 @@ def test_coverage_of_prefixes_nondecreasing(cuda):
         f = P.fraction_covered(st, s.seeds[:L])
         assert f >= prev
         prev = f
+
+
+@pytest.mark.parametrize("cluster", ["0", "1"])
+@pytest.mark.parametrize("threshold", [0.0, 0.25, 2.0])
+@pytest.mark.parametrize("name", ["cfg1", "cfg4"])
+def test_cluster_and_grid_selection_equal_reference(cuda, oracle, monkeypatch, cluster,
+                                                    threshold, name):
+    """The cluster-resident selection (one 16-block cluster, tile maxima replicated
+    in shared memory, DSMEM tile flags) and the cooperative-grid one give the
+    reference's seeds, marginals and covered count, with and without rebuilds."""
+    from paper_2411_09473_b200 import graphs
+    monkeypatch.setenv("RRGPU_SELECT_CLUSTER", cluster)
+    cfg = graphs.scaled(graphs.CONFIGS[name], 1 << 13 if name == "cfg1" else 40000,
+                        1 << 17 if name == "cfg1" else 600000)
+    arrays = graphs.generate(cfg)
+    n = arrays[0].size - 1
+    g = P.Graph(*arrays)
+    st = P.RRRStore(g)
+    P.generate_batch(g, cfg.model, 3, 6000, st, density_divisor=0)  # list sets only
+    off, mem = st.export()
+    seeds, marg = oracle.select(n, off, mem, 40, threshold=threshold)
+    for _ in range(2):  # the store is revived by every selection
+        s = P.select_seeds(st, n, 40, adaptive_threshold=threshold)
+        assert s.seeds == seeds and s.marginal_counts == marg
+        assert st.live_count() == 6000 - sum(marg)
