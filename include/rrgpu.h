@@ -86,8 +86,10 @@ typedef enum {
                         sets bit-identical; 1 FAST: counter-based per-edge draws with
                         geometric skipping over equal-weight in-lists -- same set
                         distribution, statistical parity only */,
-  RRG_OPT_LT_GUIDE_MULT = 8 /* LT guide buckets per in-edge, 1..16 (default 4; table =
+  RRG_OPT_LT_GUIDE_MULT = 8, /* LT guide buckets per in-edge, 1..16 (default 4; table =
                                32 B x mult x m; larger = fewer multi-entry buckets) */
+  RRG_OPT_IC_WARP_BUDGET = 9 /* IC warp schedule: 512-edge windows a set may take before it
+                                is handed to the block schedule (0 = no budget) */
 } rrg_option;
 rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value);
 

@@ -162,7 +162,7 @@ class Graph:
     def set_option(self, opt: str, value: int) -> None:
         code = {"lt_scan": 0, "lt_coop_min": 1, "ic_inner": 2, "ic_coop_min": 3,
                 "lt_kary": 4, "ic_mode": 5, "ic_warp_min_insp": 6, "ic_rng": 7,
-                "lt_guide_mult": 8}[opt]
+                "lt_guide_mult": 8, "ic_warp_budget": 9}[opt]
         check(lib.rrg_graph_set_option(self._h, code, int(value)))
 
     def last_batch_stats(self) -> "BatchStats":

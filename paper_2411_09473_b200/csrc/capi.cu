@@ -561,6 +561,10 @@ rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value) {
       if (value != 0 && value != 1) return invalid("ic_rng must be 0 (exact) or 1 (fast)");
       g->ic_rng = static_cast<int>(value);
       return RRG_OK;
+    case RRG_OPT_IC_WARP_BUDGET:
+      if (value < 0) return invalid("ic_warp_budget must be >= 0");
+      g->ic_warp_budget = static_cast<uint32_t>(std::min<int64_t>(value, UINT32_MAX));
+      return RRG_OK;
     case RRG_OPT_IC_COOP_MIN:
       if (value < 1) return invalid("ic_coop_min must be >= 1");
       g->ic_coop_min = static_cast<uint32_t>(std::min<int64_t>(value, UINT32_MAX));
@@ -839,6 +843,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.dupfree = g->dupfree.ptr;
       p.uniformw = g->uniformw.ptr;
       p.ic_coop_min = g->ic_coop_min;
+      p.warp_win_budget = 0;
       // dense arm: the big-set path writes rows from s->ndense on
       uint64_t drow_avail = rows_cap(s) - s->ndense;
       p.dense_thr = dense_thr;
@@ -889,6 +894,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
           launch_big(model, p, list, static_cast<uint32_t>(n_items), g->big.bitmaps.ptr,
                      g->big.lists.ptr, workers, st);
         } else {
+          p.warp_win_budget = kind == kMainWarp ? g->ic_warp_budget : 0;
           const int sched = kind == kMainWarp ? kSchedWarp : kind == kCta ? kSchedCta
                             : kind == kCtaGiant ? kSchedCtaGiant : kSchedLane;
           p.list = list;

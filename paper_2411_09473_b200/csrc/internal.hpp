@@ -147,6 +147,7 @@ struct rrg_graph {
   uint32_t ic_coop_min = 256;    // IC: in-lists at least this long expand warp-cooperatively
   int ic_mode = 0;               // IC: 0 auto, 1 lane, 2 warp, 3 block per sample
   bool ic_giant = false;         // IC auto: run the block schedule over the giant scratch
+  uint32_t ic_warp_budget = 0;   // IC: warp-schedule windows per set before the block pass (0: off)
   double ic_mean_insp = -1.0;    // IC: running mean of inspected in-edges per set
   double ic_hub_insp = 1e5;       // auto: warp per sample from this mean on (cfg5 ~1M)
   double ic_cta_max_edges = 1.5e8;  // auto: block per sample up to this many expected
@@ -286,6 +287,7 @@ struct SampleParams {
   const uint8_t* dupfree;   // per vertex: in-list sources strictly increasing
   const uint8_t* uniformw;  // IC fast mode: per vertex, all in-weights equal
   uint32_t ic_coop_min;     // in-lists at least this long go warp-cooperative
+  uint32_t warp_win_budget; // IC warp schedule: windows per set before deferring it (0: none)
   // dense arm: the big-set path writes sets of >= dense_thr members as rows
   uint32_t dense_thr;       // kNoDense: never
   uint32_t dwords;

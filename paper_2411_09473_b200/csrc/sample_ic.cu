@@ -359,11 +359,17 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
     bool ok = true;
     uint32_t qi = 0;             // queue position of the in-list being consumed
     uint32_t qj = p.off[root];   // its next in-edge
+    uint32_t wspent = 0;         // windows spent on this set (edge budget, p.warp_win_budget)
     while (qi < s.nmem && ok) {
+      if (p.warp_win_budget && ++wspent > p.warp_win_budget) {
+        ok = false;  // a large set: handed to the block schedule (deferred pass)
+        break;
+      }
       {  // a long duplicate-free in-list at the head: 1024-edge windows of one list
         const uint32_t u = mem[qi];
         const uint32_t je = p.off[u + 1];
         if (je - qj >= p.ic_coop_min && p.dupfree[u]) {
+          wspent += (je - qj) / kWin;
           ok = coop_expand<kVisSmem>(p, qj, je, mem, tab, nullptr, s, wsm.u.coop, kRegionMemCap,
                                      sf);
           ++qi;
