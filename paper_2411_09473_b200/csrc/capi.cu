@@ -175,13 +175,13 @@ void ensure_giant_scratch(rrg_graph* g, uint32_t ctas) {
   GiantScratch& gs = g->giant;
   if (gs.ctas >= ctas) return;
   gs.lists.release();
-  gs.tabs.release();
+  gs.bits.release();
   gs.tags.release();
+  const uint64_t words = (static_cast<uint64_t>(g->n) + 31) / 32;
   gs.lists.reserve_discard(static_cast<uint64_t>(ctas) * kGiantCap);
-  gs.tabs.reserve_discard(static_cast<uint64_t>(ctas) * 2 * kGiantCap);
+  gs.bits.reserve_discard(static_cast<uint64_t>(ctas) * words);
   gs.tags.reserve_discard(ctas);
-  RRG_CUDA(cudaMemsetAsync(gs.tabs.ptr, 0, static_cast<uint64_t>(ctas) * 2 * kGiantCap * 8,
-                           g->stream));
+  RRG_CUDA(cudaMemsetAsync(gs.bits.ptr, 0, static_cast<uint64_t>(ctas) * words * 4, g->stream));
   RRG_CUDA(cudaMemsetAsync(gs.tags.ptr, 0, ctas * 4ull, g->stream));
   gs.ctas = ctas;
 }
@@ -906,7 +906,8 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
             grid_cap = std::min<uint64_t>(g->scratch.lanes / block, n_items);
             ensure_giant_scratch(g, static_cast<uint32_t>(grid_cap));
             p.glists = g->giant.lists.ptr;
-            p.gtabs = g->giant.tabs.ptr;
+            p.gbits = g->giant.bits.ptr;
+            p.gwords = (static_cast<uint64_t>(g->n) + 31) / 32;
             p.gtags = g->giant.tags.ptr;
             p.gctas = g->giant.ctas;
           }

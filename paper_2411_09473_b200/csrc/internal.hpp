@@ -97,11 +97,11 @@ struct LaneScratch {
 };
 
 // Giant CTA schedule scratch (sample_ic.cu k_sample_ic_cta<true>): per block a
-// list of kGiantCap members, a tagged table of 2 kGiantCap entries, a tag.
+// list of kGiantCap members and an n-bit visited map.
 struct GiantScratch {
   uint32_t ctas = 0;
   DevBuf<uint32_t> lists;
-  DevBuf<uint64_t> tabs;
+  DevBuf<uint32_t> bits;  // per block: an n-bit visited map, zero between sets
   DevBuf<uint32_t> tags;
 };
 
@@ -301,7 +301,8 @@ struct SampleParams {
   uint64_t set_base;        // store index of batch slot 0
   // giant CTA schedule: per block kGiantCap list entries, 2 kGiantCap table entries
   uint32_t* glists;
-  uint64_t* gtabs;
+  uint32_t* gbits;          // per block: an n-bit visited map (gwords words)
+  uint64_t gwords;
   uint32_t* gtags;
   uint32_t gctas;
 };

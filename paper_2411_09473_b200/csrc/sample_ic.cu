@@ -871,6 +871,49 @@ __device__ __forceinline__ void cta_tab_insert(uint64_t* tab, uint32_t tag, uint
   do {            \
   } while (0)
 #endif
+// Visited-set primitives of the block schedule: the tagged hash table + the
+// shared-memory filter in front of it, or -- giant variant -- an n-bit map per
+// block (L2-resident: 204 KB per block at n = 1.6M) with no filter: a giant set
+// saturates any filter, and a 2M-entry hash table per block sends every probe
+// to DRAM (ncu: 1.36 TB read for 2,048 cfg3c sets with tables).
+template <bool kGiant, int K>
+__device__ __forceinline__ uint32_t cta_contains(const uint64_t* tab, const uint32_t* gbits,
+                                                 uint32_t tag, uint32_t lg,
+                                                 const uint32_t (&vs)[K], uint32_t maybe) {
+  if (!kGiant) return tab_contains_batch<K>(tab, tag, lg, vs, maybe);
+  uint32_t w[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) w[q] = ((maybe >> q) & 1u) ? gbits[vs[q] >> 5] : 0u;
+  uint32_t found = 0;
+#pragma unroll
+  for (int q = 0; q < K; ++q) found |= ((w[q] >> (vs[q] & 31)) & 1u) << q;
+  return found;
+}
+
+template <bool kGiant>
+__device__ __forceinline__ void cta_insert_range(uint64_t* tab, uint32_t* gbits, uint32_t tag,
+                                                 uint32_t lg, const uint32_t* mem, uint32_t lo,
+                                                 uint32_t hi) {
+  if (!kGiant) {
+    cta_tab_insert(tab, tag, lg, mem, lo, hi);
+    return;
+  }
+  for (uint32_t i = lo + threadIdx.x; i < hi; i += kBlock) {
+    const uint32_t v = mem[i];
+    atomicOr(gbits + (v >> 5), 1u << (v & 31));
+  }
+}
+
+template <bool kGiant>
+__device__ __forceinline__ bool cta_filter_maybe(const uint32_t* sf, uint32_t v) {
+  return kGiant ? true : cfilt_maybe(sf, v);
+}
+
+template <bool kGiant>
+__device__ __forceinline__ void cta_filter_add(uint32_t* sf, uint32_t v) {
+  if (!kGiant) cfilt_add(sf, v);
+}
+
 // kGiant: the same schedule for the sets the block scratch (256K members) could
 // not hold -- the giant-component sets of supercritical graphs (cfg3c: ~1/3 of
 // the sets, ~500K members each). Per block a private list of kGiantCap members
@@ -891,8 +934,8 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
   if (kGiant && blockIdx.x >= p.gctas) return;
   uint32_t* mem = kGiant ? p.glists + static_cast<uint64_t>(blockIdx.x) * kGiantCap
                          : p.lists + region * kMemCap;
-  uint64_t* tab = kGiant ? p.gtabs + static_cast<uint64_t>(blockIdx.x) * (2ull * kGiantCap)
-                         : p.tabs + region * kTabCap;
+  uint64_t* tab = kGiant ? nullptr : p.tabs + region * kTabCap;
+  uint32_t* gbits = kGiant ? p.gbits + static_cast<uint64_t>(blockIdx.x) * p.gwords : nullptr;
   // general windows: high word of the draw at each stream rank (global: kept
   // out of shared memory so two blocks still leave L1 its share)
   uint32_t* xhi = p.xhi + static_cast<size_t>(blockIdx.x) * kCtaWin;
@@ -920,8 +963,9 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
     uint32_t stag = ++tag, lg = kTabLog0, nmem = 1;
     if (tid == 0) {
       mem[0] = root;
-      tab_insert(tab, stag, lg, root);
-      cfilt_add(sf, root);
+      if (kGiant) atomicOr(gbits + (root >> 5), 1u << (root & 31));
+      else tab_insert(tab, stag, lg, root);
+      cta_filter_add<kGiant>(sf, root);
     }
     __syncthreads();
     RRG_PH(0);
@@ -967,8 +1011,8 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               }
 #pragma unroll
               for (int q = 0; q < 16; ++q)
-                maybe |= (32 * (16 * part + q) + lane < wend && cfilt_maybe(sf, vv[q]) ? 1u : 0u) << q;
-              const uint32_t seen = tab_contains_batch<16>(tab, stag, lg, vv, maybe);
+                maybe |= (32 * (16 * part + q) + lane < wend && cta_filter_maybe<kGiant>(sf, vv[q]) ? 1u : 0u) << q;
+              const uint32_t seen = cta_contains<kGiant, 16>(tab, gbits, stag, lg, vv, maybe);
 #pragma unroll
               for (int q = 0; q < 16; ++q) {
                 const int c = 16 * part + q;
@@ -1121,7 +1165,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             } else {
               uint32_t lg2 = lg;
               while (2 * (nmem + A) > (1u << lg2)) ++lg2;
-              if (lg2 != lg) {  // grow: re-insert the members under a fresh tag
+              if (!kGiant && lg2 != lg) {  // grow: re-insert the members under a fresh tag
                 lg = lg2;
                 ++stag;
                 cta_tab_insert(tab, stag, lg, mem, 0, nmem);
@@ -1140,14 +1184,14 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
                     if ((am >> lane) & 1u) {
                       const uint32_t v = __ldg(p.src + qj + t * kLxWin + 32 * (32 * i + c) + lane);
                       mem[base + __popc(am & lanemask_lt())] = v;
-                      cfilt_add(sf, v);
+                      cta_filter_add<kGiant>(sf, v);
                     }
                     base += __popc(am);
                   }
                 }
               }
               __syncthreads();  // the appended members are visible block-wide
-              cta_tab_insert(tab, stag, lg, mem, nmem, nmem + A);
+              cta_insert_range<kGiant>(tab, gbits, stag, lg, mem, nmem, nmem + A);
               nmem += A;
             }
           }
@@ -1183,9 +1227,9 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
 #pragma unroll
             for (int q4 = 0; q4 < kClassifyBatch; ++q4) {
               vv[q4] = r[q4].x;
-              maybe |= (32 * (c0 + q4) + lane < wend && cfilt_maybe(sf, vv[q4]) ? 1u : 0u) << q4;
+              maybe |= (32 * (c0 + q4) + lane < wend && cta_filter_maybe<kGiant>(sf, vv[q4]) ? 1u : 0u) << q4;
             }
-            const uint32_t seen = tab_contains_batch<kClassifyBatch>(tab, stag, lg, vv, maybe);
+            const uint32_t seen = cta_contains<kGiant, kClassifyBatch>(tab, gbits, stag, lg, vv, maybe);
 #pragma unroll
             for (int q4 = 0; q4 < kClassifyBatch; ++q4) {
               const uint32_t c = c0 + q4;
@@ -1278,7 +1322,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             } else {
               uint32_t lg2 = lg;
               while (2 * (nmem + A) > (1u << lg2)) ++lg2;
-              if (lg2 != lg) {  // grow: re-insert the members under a fresh tag
+              if (!kGiant && lg2 != lg) {  // grow: re-insert the members under a fresh tag
                 lg = lg2;
                 ++stag;
                 cta_tab_insert(tab, stag, lg, mem, 0, nmem);
@@ -1293,12 +1337,12 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
                 if ((am >> lane) & 1u) {
                   const uint32_t v = ws.src[32 * c + lane];
                   mem[base + __popc(am & lanemask_lt())] = v;
-                  cfilt_add(sf, v);
+                  cta_filter_add<kGiant>(sf, v);
                 }
                 base += __popc(am);
               }
               __syncthreads();  // the appended members are visible block-wide
-              cta_tab_insert(tab, stag, lg, mem, nmem, nmem + A);
+              cta_insert_range<kGiant>(tab, gbits, stag, lg, mem, nmem, nmem + A);
               nmem += A;
             }
           }
@@ -1381,9 +1425,9 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           vv[q4] = r[q4].x;
-          maybe |= (32 * (c0 + q4) + lane < wend && cfilt_maybe(sf, vv[q4]) ? 1u : 0u) << q4;
+          maybe |= (32 * (c0 + q4) + lane < wend && cta_filter_maybe<kGiant>(sf, vv[q4]) ? 1u : 0u) << q4;
         }
-        const uint32_t seen = tab_contains_batch<4>(tab, stag, lg, vv, maybe);
+        const uint32_t seen = cta_contains<kGiant, 4>(tab, gbits, stag, lg, vv, maybe);
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const uint32_t c = c0 + q4;
@@ -1637,7 +1681,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
           } else {
             uint32_t lg2 = lg;
             while (2 * (nmem + A) > (1u << lg2)) ++lg2;
-            if (lg2 != lg) {  // grow: re-insert the members under a fresh tag
+            if (!kGiant && lg2 != lg) {  // grow: re-insert the members under a fresh tag
               lg = lg2;
               ++stag;
               cta_tab_insert(tab, stag, lg, mem, 0, nmem);
@@ -1652,12 +1696,12 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               if ((am >> lane) & 1u) {
                 const uint32_t v = ws.src[32 * c + lane];
                 mem[base + __popc(am & lanemask_lt())] = v;
-                cfilt_add(sf, v);
+                cta_filter_add<kGiant>(sf, v);
               }
               base += __popc(am);
             }
             __syncthreads();  // the appended members are visible block-wide
-            cta_tab_insert(tab, stag, lg, mem, nmem, nmem + A);
+            cta_insert_range<kGiant>(tab, gbits, stag, lg, mem, nmem, nmem + A);
             nmem += A;
           }
         }
@@ -1690,6 +1734,10 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       for (uint32_t t = tid; t < nmem; t += kBlock) sinsp += p.off[mem[t] + 1] - p.off[mem[t]];
     tag = stag;
     for (uint32_t t = tid; t < kCtaFilterWords; t += kBlock) sf[t] = 0;  // filter per sample
+    if (kGiant) {  // the block's n-bit map back to zero: exactly mem[0, nmem) is set
+      __syncthreads();
+      for (uint32_t t = tid; t < nmem; t += kBlock) gbits[mem[t] >> 5] = 0u;
+    }
     if (!ok) {
       if (tid == 0) defer_slot(p, idx);
       continue;
