@@ -280,6 +280,8 @@ const char* rrg_last_error(void);
 const char* rrg_version(void);
 /* Kernels this library has launched in the process so far (all graphs). */
 uint64_t rrg_launch_count(void);
+/* Host waits on the device (stream synchronizations) by this library so far. */
+uint64_t rrg_host_sync_count(void);
 /* Test hook: the integer Bernoulli threshold used by the IC kernel
  * (uniform01() < (double)w  <=>  (next_u64() >> 11) < threshold(w)). */
 uint64_t rrg_debug_bernoulli_threshold(uint32_t weight_bits);

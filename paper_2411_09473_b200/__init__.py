@@ -358,6 +358,11 @@ def generate_slots(g: Graph, model, run_seed: int, first_slot: int, count: int,
     return made.value
 
 
+def host_sync_count() -> int:
+    """Host waits on the device (stream synchronizations) by librrgpu.so so far."""
+    return int(lib.rrg_host_sync_count())
+
+
 def launch_count() -> int:
     """Kernels librrgpu.so has launched in this process."""
     return int(lib.rrg_launch_count())

@@ -77,6 +77,7 @@ SIGNATURES = [
     ("rrg_store_destroy", None, [vp]),
     ("rrg_store_clear", C.c_int, [vp]),
     ("rrg_store_dense_info", C.c_int, [vp, u64p, u64p, u64p, u64p]),
+    ("rrg_host_sync_count", C.c_uint64, []),
     ("rrg_nccl_unique_id", C.c_int, [u8p]),
     ("rrg_nccl_comm_create", C.c_int, [u8p, C.c_int, C.c_int, C.POINTER(vp)]),
     ("rrg_nccl_comm_destroy", None, [vp]),

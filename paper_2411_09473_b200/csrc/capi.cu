@@ -42,6 +42,13 @@ Pool& pool() {
 }  // namespace
 
 uint64_t launches() { return g_launches.load(); }
+
+std::atomic<uint64_t> g_syncs{0};
+void host_sync(cudaStream_t s) {
+  g_syncs += 1;
+  RRG_CUDA(cudaStreamSynchronize(s));
+}
+uint64_t host_syncs() { return g_syncs.load(); }
 void count_launch(uint64_t k) { g_launches += k; }
 
 void* pool_alloc(size_t bytes, size_t* granted) {
@@ -204,7 +211,7 @@ void d2h(T* dst, const T* src, size_t count, cudaStream_t s) {
   RRG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
 }
 
-void sync(rrg_graph* g) { RRG_CUDA(cudaStreamSynchronize(g->stream)); }
+void sync(rrg_graph* g) { host_sync((g->stream)); }
 
 // Grows the row pool of the dense arm to hold `need` rows, keeping the rows in use.
 // Grows the row pool of the dense arm to hold `need` rows, keeping the first
@@ -318,7 +325,7 @@ uint64_t materialize(rrg_store* s, uint64_t first, uint64_t count, cudaStream_t 
   exclusive_scan_u32(s->xlen.ptr, s->xoff.ptr, count, s->scan_tmp, st);
   uint64_t tot = 0;
   d2h(&tot, s->xoff.ptr + count, 1, st);
-  RRG_CUDA(cudaStreamSynchronize(st));
+  host_sync((st));
   s->xmem.reserve_discard(tot ? tot : 1);
   launch_materialize(s->off.ptr, s->mem.ptr, s->dix.ptr, s->dbits.ptr, s->dwords, s->droot.ptr,
                      first, count, s->xoff.ptr, s->xmem.ptr, st);
@@ -330,6 +337,8 @@ uint64_t materialize(rrg_store* s, uint64_t first, uint64_t count, cudaStream_t 
 extern "C" {
 
 const char* rrg_last_error(void) { return rrgpu::t_err.c_str(); }
+uint64_t rrg_host_sync_count(void) { return rrgpu::host_syncs(); }
+
 uint64_t rrg_launch_count(void) { return rrgpu::launches(); }
 const char* rrg_version(void) { return "rrgpu 0.1.0 (sm_100a; reference rrflow 0.1.0)"; }
 uint64_t rrg_debug_bernoulli_threshold(uint32_t bits) { return bernoulli_threshold(bits); }
@@ -361,7 +370,7 @@ rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* roff, const 
     g->ctl.reserve_discard(1);
     if (n == 0) {
       RRG_CUDA(cudaMemsetAsync(g->off.ptr, 0, 4, g->stream));
-      RRG_CUDA(cudaStreamSynchronize(g->stream));
+      host_sync((g->stream));
       return RRG_OK;
     }
     // offsets travel as u64 and are narrowed + validated on the device
@@ -505,7 +514,7 @@ rrg_status rrg_graph_prepare(rrg_graph* g, rrg_model model) {
 rrg_status rrg_graph_set_stream(rrg_graph* g, void* stream) {
   if (!g) return invalid("null graph");
   return guarded([&]() -> rrg_status {
-    RRG_CUDA(cudaStreamSynchronize(g->stream));
+    host_sync((g->stream));
     if (g->own_stream) {
       RRG_CUDA(cudaStreamDestroy(g->stream));
       g->own_stream = false;

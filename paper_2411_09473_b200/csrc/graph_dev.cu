@@ -227,7 +227,7 @@ uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint3
     // 32 + vbits bits, and the offsets below assume every target is < n.
     uint32_t hbad = 0;
     RRG_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, 4, cudaMemcpyDeviceToHost, st));
-    RRG_CUDA(cudaStreamSynchronize(st));
+    host_sync((st));
     if (hbad) return 1;
     int vbits = 1;
     while (vbits < 32 && (1ull << vbits) < n) ++vbits;
@@ -249,11 +249,11 @@ uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint3
     k_transpose_offsets<<<(n + 256) / 256, 256, 0, st>>>(keys2.ptr, m, n, g->off.ptr);
     RRG_CUDA(cudaGetLastError());
     count_launch();
-    RRG_CUDA(cudaStreamSynchronize(st));  // temporaries are released at scope end
+    host_sync((st));  // temporaries are released at scope end
   }
   uint32_t hb[2] = {0, 0};
   RRG_CUDA(cudaMemcpyAsync(hb, bad.ptr, 8, cudaMemcpyDeviceToHost, st));
-  RRG_CUDA(cudaStreamSynchronize(st));
+  host_sync((st));
   if (hb[0]) return 1;
   if (normalize && n) {
     k_normalize_lt<<<(n + 127) / 128, 128, 0, st>>>(g->off.ptr, n, g->w.ptr, bad.ptr + 1);
@@ -264,7 +264,7 @@ uint64_t build_transpose_device(rrg_graph* g, const uint32_t* d_src, const uint3
     RRG_CUDA(cudaGetLastError());
     count_launch();
     RRG_CUDA(cudaMemcpyAsync(hb, bad.ptr, 8, cudaMemcpyDeviceToHost, st));
-    RRG_CUDA(cudaStreamSynchronize(st));
+    host_sync((st));
     if (hb[1] != 0xffffffffu) return 2ull + hb[1];
   }
   return 0;

@@ -25,6 +25,11 @@ struct CudaError {
     if (e_ != cudaSuccess) throw ::rrgpu::CudaError{e_, #call};          \
   } while (0)
 
+// cudaStreamSynchronize + a process-wide count of host round trips (evidence of
+// how often the host waits on the device per IMM run; rrg_host_sync_count).
+void host_sync(cudaStream_t s);
+uint64_t host_syncs();
+
 // Process-wide caching allocator (per device): freed blocks are kept and reused
 // for requests of 1/2..1x their size, so graph/store churn (the e2e path creates
 // a graph per call) does not pay cudaMalloc/cudaFree every time.
@@ -62,7 +67,7 @@ struct DevBuf {
     size_t got = 0;
     T* np = static_cast<T*>(pool_alloc(n * sizeof(T), &got));
     if (keep) RRG_CUDA(cudaMemcpyAsync(np, ptr, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
-    RRG_CUDA(cudaStreamSynchronize(s));
+    host_sync((s));
     release();
     ptr = np;
     bytes = got;

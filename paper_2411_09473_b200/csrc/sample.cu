@@ -262,7 +262,7 @@ uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64) {
   }
   uint32_t h = 0;
   RRG_CUDA(cudaMemcpyAsync(&h, bad.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
-  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  host_sync((g->stream));
   return h;
 }
 

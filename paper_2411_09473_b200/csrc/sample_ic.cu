@@ -2194,7 +2194,7 @@ void prepare_ic_fast(rrg_graph* g) {
                                                             g->uniformw.ptr);
     RRG_CUDA(cudaGetLastError());
     count_launch();
-    RRG_CUDA(cudaStreamSynchronize(g->stream));
+    host_sync((g->stream));
   }
   g->uniform_ready = true;
 }
@@ -2242,7 +2242,7 @@ void prepare_ic(rrg_graph* g) {
       count_launch();
     }
     RRG_CUDA(cudaMemcpyAsync(&g->max_indeg, mx.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
-    RRG_CUDA(cudaStreamSynchronize(g->stream));
+    host_sync((g->stream));
   }
   g->jtab.reserve_discard(jt.size());
   g->jtab16.reserve_discard(jt16.size());
@@ -2253,7 +2253,7 @@ void prepare_ic(rrg_graph* g) {
                            g->stream));
   RRG_CUDA(cudaMemcpyAsync(g->jtab16.ptr, jt16.data(), jt16.size() * 8, cudaMemcpyHostToDevice,
                            g->stream));
-  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  host_sync((g->stream));
   g->rec_ready = true;
 }
 

@@ -967,11 +967,11 @@ void prepare_lt(rrg_graph* g) {
         g->off.ptr, g->w.ptr, g->cdf.ptr, longv.ptr, bad.ptr + 1, bad.ptr);
     RRG_CUDA(cudaGetLastError());
     count_launch();
-    RRG_CUDA(cudaStreamSynchronize(g->stream));  // longv is released at scope end
+    host_sync((g->stream));  // longv is released at scope end
   }
   uint32_t hbad = 0;
   RRG_CUDA(cudaMemcpyAsync(&hbad, bad.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
-  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  host_sync((g->stream));
   g->cdf_monotone = hbad == 0;
   g->cdf_ready = true;
 }
@@ -992,7 +992,7 @@ void prepare_lt_search(rrg_graph* g) {
   uint64_t slots = 0;
   RRG_CUDA(cudaMemcpyAsync(&slots, g->ltnodeoff.ptr + g->n, 8, cudaMemcpyDeviceToHost,
                            g->stream));
-  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  host_sync((g->stream));
   if (slots >= (1ull << 32)) {  // node slots are u32 in the records: use the plain search
     g->ltrec.release();
     g->ltnodes.release();
@@ -1010,7 +1010,7 @@ void prepare_lt_search(rrg_graph* g) {
       g->off.ptr, g->cdf.ptr, g->src.ptr, g->ltnodeoff.ptr, g->n, g->ltrec.ptr);
   RRG_CUDA(cudaGetLastError());
   count_launch();
-  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  host_sync((g->stream));
 }
 
 // LT guide mode: 32 bytes per bucket, mult buckets per in-edge. False (and no
@@ -1031,7 +1031,7 @@ bool prepare_lt_guide(rrg_graph* g) {
       g->off.ptr, g->cdf.ptr, g->src.ptr, g->n, g->m, g->lt_guide_mult, g->ltguide.ptr);
   RRG_CUDA(cudaGetLastError());
   count_launch();
-  RRG_CUDA(cudaStreamSynchronize(g->stream));
+  host_sync((g->stream));
   g->lt_guide_built = g->lt_guide_mult;
   return true;
 }

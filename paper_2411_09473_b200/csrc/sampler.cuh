@@ -27,6 +27,25 @@ __device__ __forceinline__ void restage_slot(const SampleParams& p, uint32_t idx
   p.restage[atomicAdd(&p.ctl->nrestage, 1u)] = idx;
 }
 
+// Fused-counter increment. North star (4) asks for warp-aggregated atomics; with
+// RRG_WARP_AGG the lanes of the warp that are here together and add the same
+// vertex issue one atomic with their count. Measured (profiles/r2/NOTES.md):
+// +20 % on cfg2 (lane walks, search mode), +12 % on cfg4, +3 % on cfg3 -- the
+// lanes of a warp emit different sets whose members rarely coincide at the
+// same instant, so __match_any_sync costs more than the fire-and-forget L2
+// reductions it saves. Default: one RED per member (the counter is L2-resident).
+// Where counts do coincide -- dense rows -- they are aggregated by construction
+// (bit-sliced column sums, one atomic per vertex and 32-row chunk, dense.cu).
+__device__ __forceinline__ void counter_add(uint32_t* counter, uint32_t v) {
+#ifndef RRG_WARP_AGG
+  atomicAdd(counter + v, 1u);
+  return;
+#endif
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, v);
+  if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counter + v, __popc(peers));
+}
+
 // Writes a finished set to staging, bumps the fused counter, records the slot.
 // False when staging is full (the slot is re-run later and counted then).
 __device__ __forceinline__ bool emit_set(const SampleParams& p, uint32_t idx, const uint32_t* mem,
@@ -46,14 +65,14 @@ __device__ __forceinline__ bool emit_set(const SampleParams& p, uint32_t idx, co
     for (int q = 0; q < 8; ++q) {
       RRG_DCHECK(v[q] < p.n, 1);
       out[t + q] = v[q];
-      if (p.counter) atomicAdd(p.counter + v[q], 1u);
+      if (p.counter) counter_add(p.counter, v[q]);
     }
   }
   for (; t < nmem; ++t) {
     const uint32_t v = mem[t];
     RRG_DCHECK(v < p.n, 1);
     out[t] = v;
-    if (p.counter) atomicAdd(p.counter + v, 1u);
+    if (p.counter) counter_add(p.counter, v);
   }
   p.slot_start[idx] = pos;
   p.slot_len[idx] = nmem;

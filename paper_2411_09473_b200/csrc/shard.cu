@@ -170,7 +170,7 @@ rrg_status exchange_impl(rrg_store* side, rrg_store* dst, void* comm) {
   nccl_check(n.all_gather(hdr.ptr, hdrs.ptr, 4, kNcclUint64, c, st), "ncclAllGather");
   std::vector<uint64_t> h(4ull * nranks);
   RRG_CUDA(cudaMemcpyAsync(h.data(), hdrs.ptr, h.size() * 8, cudaMemcpyDeviceToHost, st));
-  RRG_CUDA(cudaStreamSynchronize(st));
+  host_sync((st));
   std::vector<Shard> shards(nranks);
   const uint32_t W = dst->dwords;
   for (int r = 0; r < nranks; ++r) {
