@@ -407,9 +407,11 @@ def imm_block(P, name, orc, cores, reps=3):
     P.run_imm(g, icfg)
     walls = []
     for _ in range(reps):
+        s0, l0 = P.host_sync_count(), P.launch_count()
         t0 = time.perf_counter()
         r = P.run_imm(g, icfg)
         walls.append(time.perf_counter() - t0)
+        syncs, launches = P.host_sync_count() - s0, P.launch_count() - l0
     g.close()
     t0 = time.perf_counter()
     ge = P.Graph(*arrays)
@@ -421,7 +423,8 @@ def imm_block(P, name, orc, cores, reps=3):
            "gpu_wall_s_note": f"median of {reps} after one warm-up, graph resident",
            "gpu_e2e_wall_s": t_e2e, "gpu_e2e_note": "from host arrays: upload + K0 + IMM",
            "gpu_timings": r.timings, "theta": r.theta, "theta_prime": r.theta_prime,
-           "sets_generated": r.sets_generated,
+           "sets_generated": r.sets_generated, "host_syncs_per_imm": syncs,
+           "gpu_launches_per_imm": launches,
            "influence_estimate": n * sum(r.seeds.marginal_counts) / r.sets_generated,
            "e2e_same_seeds": re_.seeds.seeds == r.seeds.seeds}
     golden = os.path.join(ROOT, "tests", "golden", f"imm_full_{name}.json")

@@ -1,0 +1,31 @@
+"""Where the time of run_imm from host arrays goes (graph upload, K0 layouts,
+IMM) on one config, pinned host arrays, per LT scan mode."""
+import sys
+import time
+
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+import paper_2411_09473_b200 as P  # noqa: E402
+from paper_2411_09473_b200 import graphs  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
+cfg = graphs.CONFIGS[name]
+host = [torch.from_numpy(a).pin_memory().numpy() for a in graphs.generate(cfg)]
+icfg = P.ImmConfig(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model)
+P.run_imm(P.Graph(*host), icfg)  # warm-up: allocator, module load
+for scan in (2, 1):
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g = P.Graph(*host)
+        t1 = time.perf_counter()
+        g.set_option("lt_scan", scan)
+        g.prepare(cfg.model)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        r = P.run_imm(g, icfg)
+        t3 = time.perf_counter()
+        g.close()
+        print(f"{name} lt_scan {scan}: upload {1e3*(t1-t0):.1f} ms  K0 {1e3*(t2-t1):.1f} ms  "
+              f"imm {1e3*(t3-t2):.1f} ms  total {1e3*(t3-t0):.1f} ms  seeds[:3] {r.seeds.seeds[:3]}",
+              flush=True)
