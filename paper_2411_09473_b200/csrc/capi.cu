@@ -241,12 +241,16 @@ uint64_t rows_cap(const rrg_store* s) {
 // slot-ordered buffer: staged lists of >= thr members become rows of the dense
 // arm (make_repr, rrr_set.hpp:82-83), then K3 scan + compaction of the lists.
 // rows_big rows from s->ndense on were written by the big-set path.
+// list_max: the batch's longest staged list when the sampler reported it (then
+// no list can become a row below thr and the store's maximum needs no read-back),
+// UINT32_MAX when unknown (imports).
 void commit_staged(rrg_store* s, uint64_t count, uint32_t thr, uint64_t rows_big = 0,
-                   uint64_t big_members = 0, uint32_t big_max = 0) {
+                   uint64_t big_members = 0, uint32_t big_max = 0,
+                   uint32_t list_max = UINT32_MAX) {
   rrg_graph* g = s->g;
   uint64_t nreq = 0;
   unsigned long long dc[3] = {0, 0, 0};
-  if (thr != kNoDense && count) {
+  if (thr != kNoDense && count && list_max >= thr) {
     s->dreq.reserve_discard(count);
     s->dctl.reserve_discard(3);
     RRG_CUDA(cudaMemsetAsync(s->dctl.ptr, 0, 3 * sizeof(unsigned long long), g->stream));
@@ -287,12 +291,14 @@ void commit_staged(rrg_store* s, uint64_t count, uint32_t thr, uint64_t rows_big
                              cudaMemcpyDeviceToDevice, g->stream));
   launch_compact(s->stage.ptr, s->slot_start.ptr, s->slot_len.ptr, s->scan.ptr, s->total, count,
                  s->mem.ptr, s->off.ptr + s->nsets, s->maxlen_dev.ptr, g->stream);
-  uint32_t mx = 0;
-  d2h(&mx, s->maxlen_dev.ptr, 1, g->stream);
-  sync(g);
+  uint32_t mx = list_max;
+  if (list_max == UINT32_MAX) {  // not reported: read the compaction's maximum back
+    d2h(&mx, s->maxlen_dev.ptr, 1, g->stream);
+    sync(g);
+  }
   s->nsets += count;
   s->total += added;
-  s->max_len = mx;
+  s->max_len = std::max(s->max_len, mx);
   s->ndense += rows_big + nreq;
   s->dense_members += big_members + dc[1];
   s->dense_max = std::max<uint32_t>(s->dense_max, std::max<uint32_t>(big_max,
@@ -1045,7 +1051,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       }
       acc.entries_read += ctl.entries;
       const uint64_t before = s->members();
-      commit_staged(s, c, dense_thr, ctl.ndense, ctl.dense_members, ctl.dense_max);
+      commit_staged(s, c, dense_thr, ctl.ndense, ctl.dense_members, ctl.dense_max, ctl.max_len);
       acc.members += s->members() - before;
       acc.sets += c;
       done += c;

@@ -455,6 +455,7 @@ struct SampleCtl {
   unsigned long long repairs;     // IC block schedule: conflicts repaired inside a window
   unsigned int ndeferred;         // slots handed to the big-set path (set > kMemCap)
   unsigned int nrestage;          // slots to re-run once staging has grown
+  unsigned int max_len;           // largest set written to staging (note_len)
   unsigned long long ndense;      // big-set path: rows requested (dense arm)
   unsigned long long dense_members;  // big-set path: members of the rows written
   unsigned int dense_max;         // big-set path: largest row written

@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_big(const SampleParams p, con
       if (lane == 0) {
         p.slot_start[idx] = pos;
         p.slot_len[idx] = nmem;
+        note_len(p, nmem);
         insp += sinsp;
       }
     }

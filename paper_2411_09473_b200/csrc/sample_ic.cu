@@ -625,6 +625,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
     if (lane == 0) {
       p.slot_start[idx] = pos;
       p.slot_len[idx] = s.nmem;
+      note_len(p, s.nmem);
     }
     insp += sinsp;
     __syncwarp();
@@ -1790,6 +1791,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
     if (tid == 0) {
       p.slot_start[idx] = pos;
       p.slot_len[idx] = nmem;
+      note_len(p, nmem);
     }
     insp += sinsp;
   }
@@ -1989,6 +1991,7 @@ __global__ void __launch_bounds__(kBlock) k_sample_ic_fast(const SampleParams p,
         if (lane == 0) {
           p.slot_start[idx] = spos;
           p.slot_len[idx] = nmem;
+          note_len(p, nmem);
         }
         insp += sinsp;
       }

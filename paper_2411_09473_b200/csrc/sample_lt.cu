@@ -384,6 +384,7 @@ __device__ __forceinline__ bool warp_emit_pending(const SampleParams& p, bool pe
     if (lane == L) {
       p.slot_start[iL] = pos;
       p.slot_len[iL] = nL;
+      note_len(p, nL);
       mine = true;
     }
   }

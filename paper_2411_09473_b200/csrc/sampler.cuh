@@ -46,6 +46,13 @@ __device__ __forceinline__ void counter_add(uint32_t* counter, uint32_t v) {
   if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counter + v, __popc(peers));
 }
 
+// Records a staged set's length in the batch maximum: an atomic only when the
+// set beats the maximum seen so far (a few per batch), so the host learns the
+// batch's longest list without reading the store back.
+__device__ __forceinline__ void note_len(const SampleParams& p, uint32_t n) {
+  if (n > *reinterpret_cast<volatile unsigned*>(&p.ctl->max_len)) atomicMax(&p.ctl->max_len, n);
+}
+
 // Writes a finished set to staging, bumps the fused counter, records the slot.
 // False when staging is full (the slot is re-run later and counted then).
 __device__ __forceinline__ bool emit_set(const SampleParams& p, uint32_t idx, const uint32_t* mem,
@@ -76,6 +83,7 @@ __device__ __forceinline__ bool emit_set(const SampleParams& p, uint32_t idx, co
   }
   p.slot_start[idx] = pos;
   p.slot_len[idx] = nmem;
+  note_len(p, nmem);
   return true;
 }
 
