@@ -394,13 +394,21 @@ __global__ void __launch_bounds__(kClBlock, 1) k_select_cluster(const SelectPara
   extern __shared__ unsigned long long cl_smem[];
   unsigned long long* tmax = cl_smem;                                      // [ntiles]
   unsigned long long* red = tmax + ntiles;                                 // [32]
-  uint32_t* dirty = reinterpret_cast<uint32_t*>(red + kClBlock / 32);      // [ntiles/32 + 1]
-  const uint32_t dwords_t = (ntiles >> 5) + 1;
+  // block b owns the contiguous tiles [b tpc, (b + 1) tpc): its dirty bitmap is
+  // indexed by the tile's offset in that range; `touch` collects, per block, the
+  // tiles its own decrements hit (local shared atomics), sent to the owners
+  // one word at a time after the cover
+  const uint32_t tpc = (ntiles + kClCtas - 1) / kClCtas;
+  uint32_t* dirty = reinterpret_cast<uint32_t*>(red + kClBlock / 32);      // [tpc/32 + 1]
+  const uint32_t dwords_t = (tpc >> 5) + 1;
+  uint32_t* touch = dirty + dwords_t;                                      // [ntiles/32 + 1]
+  const uint32_t twords = (ntiles >> 5) + 1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t tid = static_cast<uint64_t>(crank) * kClBlock + threadIdx.x;
   const uint64_t nthreads = static_cast<uint64_t>(kClCtas) * kClBlock;
   const uint64_t gwarp = tid >> 5, nwarps = nthreads >> 5;
   for (uint32_t i = threadIdx.x; i < dwords_t; i += kClBlock) dirty[i] = 0u;
+  for (uint32_t i = threadIdx.x; i < twords; i += kClBlock) touch[i] = 0u;
   // initial maxima: warp per tile across the cluster, broadcast to every replica
   for (uint64_t t = gwarp; t < ntiles; t += nwarps) {
     const unsigned long long m = tile_max_warp(p, static_cast<uint32_t>(t));
@@ -410,8 +418,7 @@ __global__ void __launch_bounds__(kClBlock, 1) k_select_cluster(const SelectPara
 
   auto flag_tile = [&](uint32_t u) {
     const uint32_t t = u >> kSelTileLog;
-    uint32_t* d = cl.map_shared_rank(dirty, t % kClCtas);
-    atomicOr(d + ((t / kClCtas) >> 5), 1u << ((t / kClCtas) & 31));
+    atomicOr(touch + (t >> 5), 1u << (t & 31));
   };
 
   unsigned long long covered_sum = 0;
@@ -489,6 +496,16 @@ __global__ void __launch_bounds__(kClBlock, 1) k_select_cluster(const SelectPara
       p.selected[v] = 1;
       if (rebuild) atomicAdd(p.rebuilds, 1ull);
     }
+    __syncthreads();
+    // this block's touched tiles -> their owners' dirty bitmaps (DSMEM): thread
+    // per tile, one remote atomic per touched tile
+    for (uint32_t t = threadIdx.x; t < ntiles; t += kClBlock) {
+      if (!((touch[t >> 5] >> (t & 31)) & 1u)) continue;
+      const uint32_t owner = t / tpc, jo = t - owner * tpc;
+      atomicOr(cl.map_shared_rank(dirty, owner) + (jo >> 5), 1u << (jo & 31));
+    }
+    __syncthreads();
+    for (uint32_t i2 = threadIdx.x; i2 < twords; i2 += kClBlock) touch[i2] = 0u;
     cl.sync();
     covered_sum += p.marg[r];
 
@@ -503,11 +520,12 @@ __global__ void __launch_bounds__(kClBlock, 1) k_select_cluster(const SelectPara
     }
 
     // ---- C: re-reduce this block's flagged tiles, broadcast the maxima ---------
-    const uint32_t owned = ntiles > crank ? (ntiles - crank + kClCtas - 1) / kClCtas : 0;
+    const uint32_t t0 = crank * tpc;
+    const uint32_t owned = ntiles > t0 ? min(tpc, ntiles - t0) : 0;
     for (uint32_t j = wid; j < owned; j += kClBlock / 32) {
       const bool d = rebuild || ((dirty[j >> 5] >> (j & 31)) & 1u);
       if (!d) continue;  // uniform in the warp
-      const uint32_t t = j * kClCtas + crank;
+      const uint32_t t = t0 + j;
       const unsigned long long m = tile_max_warp(p, t);
       if (lane < kClCtas) cl.map_shared_rank(tmax, lane)[t] = m;
     }
@@ -538,7 +556,9 @@ bool launch_select_cluster(const SelectParams& p, cudaStream_t s) {
   }
   if (!force && p.total > kClMaxMembers) return false;
   const uint32_t ntiles = (p.n + kSelTile - 1) >> kSelTileLog;
-  const size_t smem = static_cast<size_t>(ntiles) * 8 + (kClBlock / 32) * 8 + ((ntiles >> 5) + 1) * 4;
+  const uint32_t tpc = (ntiles + kClCtas - 1) / kClCtas;
+  const size_t smem = static_cast<size_t>(ntiles) * 8 + (kClBlock / 32) * 8 +
+                      ((tpc >> 5) + 1) * 4 + ((ntiles >> 5) + 1) * 4;
   if (smem > 200 * 1024) return false;
   static int ok = -1;
   if (ok < 0) {
