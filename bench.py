@@ -719,6 +719,18 @@ def run_ours(args, rank, world, local):
             "frac": (got / ceil) if ceil else None,
             "peak_source": "measured live: tools/gather/gather_probe.cu (8 GB table, "
                            "1-8 x 256 chains per SM, best)"}
+        # the kernel's DRAM traffic rate (ncu bytes per launch / live kernel time)
+        # against the DRAM rate of the gather probe at its ceiling (2.96 DRAM
+        # sectors per random 32-B load, profiles/r1/NOTES.md): how close the walk
+        # is to the random-access limit of HBM, whatever the bytes are for
+        if traffic and ceil:
+            rate = traffic / (per_launch_ms / 1e3) / 1e9
+            cap = ceil * 2.96 * 32 / 1e9
+            line["roofline"]["dram_random_access"] = {
+                "achieved": rate, "peak": cap, "unit": "GB/s of DRAM traffic",
+                "frac": rate / cap,
+                "note": "ncu DRAM bytes (read + write) per launch / sampler event time vs "
+                        "the gather probe's rate x 2.96 sectors x 32 B per gather"}
     if small_block is not None:
         sb = small_block
         line["small_batch"] = {
