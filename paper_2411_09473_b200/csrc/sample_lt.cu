@@ -289,17 +289,41 @@ __device__ __forceinline__ void lt_guide_resolve(const SampleParams& p, const ui
   }
 }
 
+#ifndef RRG_GUIDE_EVICT_FIRST
+#define RRG_GUIDE_EVICT_FIRST 1
+#endif
+// L2 policy of the bucket-entry loads: evict first. The 8.8 GB table has no
+// reuse worth keeping (a walk's buckets are uniformly likely), so its lines
+// should not push the walks' member lists, hash tables and the fused counter
+// out of L2 -- the kernel runs at the random-access DRAM ceiling, so every
+// DRAM byte it does not move is time (profiles/r2/NOTES.md).
+__device__ __forceinline__ uint64_t lt_guide_policy() {
+  uint64_t pol = 0;
+#if RRG_GUIDE_EVICT_FIRST
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+
 __device__ __forceinline__ void lt_guide_fetch(const SampleParams& p, uint32_t offu, uint32_t degu,
-                                               uint64_t x, uint4& e0, uint4& e1) {
+                                               uint64_t x, uint4& e0, uint4& e1, uint64_t pol) {
   if (!degu) return;
   const uint64_t G = static_cast<uint64_t>(degu) * p.lt_guide_mult;
   const uint64_t gi = static_cast<uint64_t>(offu) * p.lt_guide_mult + __umul64hi(x & ~0x7ffull, G);
   // one 256-bit load (sm_100: LDG.256), not allocated in L1: the entry is one
   // 32-byte sector and is never re-read by this SM
+#if RRG_GUIDE_EVICT_FIRST
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(e0.x), "=r"(e0.y), "=r"(e0.z), "=r"(e0.w), "=r"(e1.x), "=r"(e1.y),
+                 "=r"(e1.z), "=r"(e1.w)
+               : "l"(p.ltguide + 2 * gi), "l"(pol));
+#else
+  (void)pol;
   asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(e0.x), "=r"(e0.y), "=r"(e0.z), "=r"(e0.w), "=r"(e1.x), "=r"(e1.y),
                  "=r"(e1.z), "=r"(e1.w)
                : "l"(p.ltguide + 2 * gi));
+#endif
 }
 
 // Visited set of a guide-mode walk while it is short: a 2048-bit filter per lane
@@ -422,6 +446,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_sample_lt_guide(const Sa
   uint4 e0 = make_uint4(0, 0, 0, 0), e1 = make_uint4(0, 0, 0, 0);
   uint64_t insp = 0, sinsp = 0, ent = 0;
   uint64_t wq_next = 0, wq_end = 0, sc_next = 0, sc_end = 0;  // warp-uniform queues
+  const uint64_t gpol = lt_guide_policy();
 
   for (;;) {
     // (1) filter hits: the warp scans each such lane's members (<= kLtFiltMax,
@@ -489,7 +514,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_sample_lt_guide(const Sa
       offu = __ldg(p.off + u);
       degu = __ldg(p.off + u + 1) - offu;
       x = rng.next();  // the first step's draw (sampling.hpp:127)
-      lt_guide_fetch(p, offu, degu, x, e0, e1);
+      lt_guide_fetch(p, offu, degu, x, e0, e1, gpol);
       xn = rng.next();
 #pragma unroll
       for (uint32_t w = 0; w < kLtFiltWords; ++w) filt[w * kBlock] = 0u;
@@ -514,7 +539,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_sample_lt_guide(const Sa
     sinsp += pick < degu ? pick + 1 : degu;  // reference trip count (sampling.hpp:130-136)
     bool stop = v == kGuideNone;
     if (!stop) {
-      lt_guide_fetch(p, offv, degv, xn, e0, e1);  // next step's entry, in flight now
+      lt_guide_fetch(p, offv, degv, xn, e0, e1, gpol);  // next step's entry, in flight now
       x = xn;
       xn = rng.next();
       if (big) {
