@@ -400,6 +400,8 @@ def imm_block(P, name, orc, cores, reps=3):
     for seeds, marginals, theta / theta' / LB."""
     cfg, arrays = graph_arrays(name)
     n = arrays[0].size - 1
+    import torch
+    host = [torch.from_numpy(a).pin_memory().numpy() for a in arrays]  # pinned, as in e2e
     if name in SLOW_REFERENCE:
         reps = 1  # seconds per run
     icfg = P.ImmConfig(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model)
@@ -416,7 +418,7 @@ def imm_block(P, name, orc, cores, reps=3):
     e2e = []
     for _ in range(1 if name in SLOW_REFERENCE else 3):
         t0 = time.perf_counter()
-        ge = P.Graph(*arrays)
+        ge = P.Graph(*host)
         re_ = P.run_imm(ge, icfg)
         e2e.append(time.perf_counter() - t0)
         ge.close()
@@ -425,7 +427,7 @@ def imm_block(P, name, orc, cores, reps=3):
            "epsilon": cfg.epsilon, "gpu_wall_s": statistics.median(walls),
            "gpu_wall_s_note": f"median of {reps} after one warm-up, graph resident",
            "gpu_e2e_wall_s": t_e2e,
-           "gpu_e2e_note": "from host arrays: upload + K0 + IMM, median of 3 (cfg3c: 1)",
+           "gpu_e2e_note": "from pinned host arrays: upload + K0 + IMM, median of 3 (cfg3c: 1)",
            "gpu_timings": r.timings, "theta": r.theta, "theta_prime": r.theta_prime,
            "sets_generated": r.sets_generated, "host_syncs_per_imm": syncs,
            "gpu_launches_per_imm": launches,
@@ -719,18 +721,17 @@ def run_ours(args, rank, world, local):
             "frac": (got / ceil) if ceil else None,
             "peak_source": "measured live: tools/gather/gather_probe.cu (8 GB table, "
                            "1-8 x 256 chains per SM, best)"}
-        # the kernel's DRAM traffic rate (ncu bytes per launch / live kernel time)
-        # against the DRAM rate of the gather probe at its ceiling (2.96 DRAM
-        # sectors per random 32-B load, profiles/r1/NOTES.md): how close the walk
-        # is to the random-access limit of HBM, whatever the bytes are for
-        if traffic and ceil:
+        # the kernel's DRAM traffic rate (ncu bytes per launch / live kernel time):
+        # what the random-access stream sustains, whatever the bytes are for
+        if traffic:
             rate = traffic / (per_launch_ms / 1e3) / 1e9
-            cap = ceil * 2.96 * 32 / 1e9
-            line["roofline"]["dram_random_access"] = {
-                "achieved": rate, "peak": cap, "unit": "GB/s of DRAM traffic",
-                "frac": rate / cap,
-                "note": "ncu DRAM bytes (read + write) per launch / sampler event time vs "
-                        "the gather probe's rate x 2.96 sectors x 32 B per gather"}
+            line["roofline"]["dram_traffic"] = {
+                "achieved": rate, "peak": peak, "unit": "GB/s of DRAM traffic",
+                "frac": rate / peak,
+                "note": "ncu DRAM bytes (read + write) per launch / sampler event time, "
+                        "against the measured streaming HBM peak: the walk's accesses are "
+                        "random 32-B loads (~3 DRAM sectors each), so this is the share of "
+                        "HBM the random-access stream sustains"}
     if small_block is not None:
         sb = small_block
         line["small_batch"] = {
