@@ -289,10 +289,18 @@ class RRRStore:
         """Enqueues the D2H copies of the whole store (offsets, members, counter) on
         the CUDA stream handle `stream` and returns the member count without
         waiting; synchronize the stream before reading the buffers or touching
-        the store again."""
+        the store again. u32 `offsets` / `counts` arrays select the compact
+        32-bit export (fewer bytes over PCIe)."""
         total = self.total_member_count()
         if offsets.size < self.size() + 1 or members.size < total:
             raise ValueError("export buffers too small")
+        if offsets.dtype == np.uint32:  # compact: u32 offsets and counts
+            if counts is not None and counts.dtype != np.uint32:
+                raise ValueError("export_all_async: u32 offsets need u32 counts")
+            check(lib.rrg_store_export_all_async32(
+                self._h, ptr(offsets, C.c_uint32), ptr(members, C.c_uint32),
+                ptr(counts, C.c_uint32) if counts is not None else None, C.c_void_p(stream)))
+            return total
         check(lib.rrg_store_export_all_async(
             self._h, ptr(offsets, C.c_uint64), ptr(members, C.c_uint32),
             ptr(counts, C.c_uint64) if counts is not None else None, C.c_void_p(stream)))

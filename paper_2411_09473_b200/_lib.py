@@ -106,6 +106,7 @@ SIGNATURES = [
     ("rrg_store_append_from", C.c_int, [vp, vp, C.c_uint64, C.c_uint64]),
     ("rrg_store_counter", C.c_int, [vp, u64p]),
     ("rrg_store_export_all_async", C.c_int, [vp, u64p, u32p, u64p, vp]),
+    ("rrg_store_export_all_async32", C.c_int, [vp, u32p, u32p, u32p, vp]),
     ("rrg_build_transpose", C.c_int,
      [C.c_uint32, C.c_uint64, u32p, u32p, f32p, u64p, u32p, f32p]),
     ("rrg_normalize_lt_weights", C.c_int, [C.c_uint32, u64p, f32p]),

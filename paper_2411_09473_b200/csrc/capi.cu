@@ -1434,6 +1434,37 @@ rrg_status rrg_store_export_all_async(const rrg_store* s, uint64_t* offsets, uin
   });
 }
 
+rrg_status rrg_store_export_all_async32(const rrg_store* s, uint32_t* offsets, uint32_t* members,
+                                        uint32_t* counts, void* stream) {
+  if (!s || !offsets || (s->members() && !members)) return invalid("null argument");
+  if (s->members() >= (1ull << 32)) return invalid("export32: store exceeds 2^32 - 1 members");
+  return guarded([&]() -> rrg_status {
+    rrg_graph* g = s->g;
+    const cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    auto* ms = const_cast<rrg_store*>(s);  // scratch only; the store's sets are unchanged
+    const uint64_t* off_src = s->off.ptr;
+    const uint32_t* mem_src = s->mem.ptr;
+    if (s->ndense) {
+      materialize(ms, 0, s->nsets, g->stream);
+      off_src = s->xoff.ptr;
+      mem_src = s->xmem.ptr;
+    }
+    ms->narrow.reserve_discard(s->nsets + 1);
+    launch_narrow(off_src, ms->narrow.ptr, s->nsets + 1, g->stream);
+    RRG_CUDA(cudaEventRecord(g->ev1, g->stream));
+    RRG_CUDA(cudaStreamWaitEvent(cs, g->ev1, 0));
+    RRG_CUDA(cudaMemcpyAsync(offsets, ms->narrow.ptr, (s->nsets + 1) * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, cs));
+    if (s->members())
+      RRG_CUDA(cudaMemcpyAsync(members, mem_src, s->members() * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, cs));
+    if (counts && g->n)
+      RRG_CUDA(cudaMemcpyAsync(counts, s->counter.ptr, g->n * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, cs));
+    return RRG_OK;
+  });
+}
+
 rrg_status rrg_store_counter(const rrg_store* s, uint64_t* counts) {
   if (!s || !counts) return invalid("null argument");
   return guarded([&]() -> rrg_status {

@@ -213,6 +213,7 @@ struct rrg_store {
   rrgpu::DevBuf<uint32_t> tdirty;          // selection: per-tile dirty flags
   rrgpu::DevBuf<uint64_t> span;            // selection (scan mode): member -> set span
   rrgpu::DevBuf<uint64_t> wide;  // u64 staging of counter exports
+  rrgpu::DevBuf<uint32_t> narrow;  // u32 offsets of compact exports
   // ---- dense arm (rrr_set.hpp:10-13, :73-90; pack_sketch, sampling.hpp:68-84) ----
   // A set of >= n / density_divisor members is a row of the n-bit map pool
   // instead of a list: its list range in mem/off is EMPTY (a list set always
@@ -411,6 +412,7 @@ void launch_invert(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
 void launch_fraction(const uint64_t* off, const uint32_t* mem, uint64_t nsets,
                      const uint8_t* in_seed_set, unsigned long long* hits, cudaStream_t s);
 void launch_widen(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t s);
+void launch_narrow(const uint64_t* in, uint32_t* out, uint64_t n, cudaStream_t s);
 void launch_rebase(const uint64_t* in, uint64_t count, uint64_t base, uint64_t* out,
                    uint32_t* maxlen, cudaStream_t s);
 

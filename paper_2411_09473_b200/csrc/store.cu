@@ -276,6 +276,12 @@ __global__ void k_widen(const uint32_t* in, uint64_t* out, uint64_t n) {
     out[i] = in[i];
 }
 
+__global__ void k_narrow(const uint64_t* in, uint32_t* out, uint64_t n) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<uint32_t>(in[i]);
+}
+
 int grid_for(uint64_t warps_needed) {
   const uint64_t blocks = (warps_needed * 32 + 255) / 256;
   return static_cast<int>(blocks < 1 ? 1 : (blocks > 65535 ? 65535 : blocks));
@@ -339,6 +345,13 @@ void launch_rebase(const uint64_t* in, uint64_t count, uint64_t base, uint64_t* 
   if (!count) return;
   const uint64_t blocks = std::min<uint64_t>((count + 255) / 256, 4096);
   k_rebase<<<static_cast<unsigned>(blocks), 256, 0, s>>>(in, count, base, out, maxlen);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_narrow(const uint64_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
+  if (!n) return;
+  k_narrow<<<1184, 256, 0, s>>>(in, out, n);
   RRG_CUDA(cudaGetLastError());
   count_launch();
 }

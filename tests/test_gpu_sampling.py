@@ -223,6 +223,13 @@ def test_export_all_async_equals_sync_export(cuda):
     assert st.export_all_async(o, m, c, s.cuda_stream) == mem.size
     s.synchronize()
     assert (o == off).all() and (m == mem).all() and (c == st.counter()).all()
+    # the compact 32-bit variant (u32 offsets and counts)
+    o32 = torch.empty(st.size() + 1, dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+    c32 = torch.empty(g.num_vertices, dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+    m.fill(0)
+    assert st.export_all_async(o32, m, c32, s.cuda_stream) == mem.size
+    s.synchronize()
+    assert (o32 == off).all() and (m == mem).all() and (c32 == st.counter()).all()
 
 
 @pytest.mark.parametrize("coop_min", [2, 7, 64, 1 << 30])
