@@ -1107,6 +1107,7 @@ rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double adaptive_threshold,
     const char* force_index = std::getenv("RRGPU_SELECT_INDEX");  // tests: the index path
     const bool scan = s->total <= kScanMaxMembers &&
                       !(force_index && *force_index && *force_index != '0');
+
     if (scan) {
       s->inv.reserve_discard(s->total ? s->total : 1);  // the blanked working copy
       s->span.reserve_discard(s->total ? s->total : 1);

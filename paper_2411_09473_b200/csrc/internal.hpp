@@ -452,5 +452,8 @@ struct SelectParams {
 };
 constexpr uint32_t kSelTileLog = 11;  // 2048 vertices per argmax tile
 void launch_select(const SelectParams& p, int num_sms, cudaStream_t s);
+// whether the cluster-resident selection may run this store (no dense rows, no
+// per-round snapshots, not disabled by RRGPU_SELECT_CLUSTER=0)
+bool select_cluster_eligible(const SelectParams& p);
 
 }  // namespace rrgpu

@@ -449,9 +449,26 @@ __global__ void __launch_bounds__(kClBlock, 1) k_select_cluster(const SelectPara
     const bool rebuild = live > 0 && static_cast<double>(top) / static_cast<double>(live) >
                                          p.adaptive_threshold;
 
-    // ---- B: scan-mode cover (see k_select) ----------------------------------
+    // ---- B: cover (scan mode as in k_select; index mode: warp per set of inv[v]) --
     unsigned long long killed = 0;
-    const uint64_t nchunk = (p.total + 255) / 256;
+    if (!p.scan) {
+      const uint64_t ib = p.ioff[v], ie = p.ioff[v + 1];
+      for (uint64_t t = ib + gwarp; t < ie; t += nwarps) {
+        const uint32_t sid = p.inv[t];
+        uint32_t was = 0;
+        if (lane == 0) was = atomicExch(p.covered + sid, 1u);
+        was = __shfl_sync(kFull, was, 0);
+        if (was) continue;
+        killed += lane == 0;
+        if (rebuild) continue;
+        for (uint64_t j = p.off[sid] + lane; j < p.off[sid + 1]; j += 32) {
+          const uint32_t u = p.mem[j];
+          atomicSub(p.cnt + u, 1u);
+          flag_tile(u);
+        }
+      }
+    }
+    const uint64_t nchunk = p.scan ? (p.total + 255) / 256 : 0;
     for (uint64_t c = gwarp; c < nchunk; c += nwarps) {
       const uint64_t base = c * 256 + static_cast<uint64_t>(lane) * 8;
       uint32_t q[8];
@@ -512,9 +529,17 @@ __global__ void __launch_bounds__(kClBlock, 1) k_select_cluster(const SelectPara
     if (rebuild) {  // rebuild_update: zero, recount the surviving sets
       for (uint64_t u = tid; u < p.n; u += nthreads) p.cnt[u] = 0u;
       cl.sync();
-      for (uint64_t t = tid; t < p.total; t += nthreads) {
-        const uint32_t u = p.wmem[t];
-        if (u != kBlank) atomicAdd(p.cnt + u, 1u);
+      if (p.scan) {
+        for (uint64_t t = tid; t < p.total; t += nthreads) {
+          const uint32_t u = p.wmem[t];
+          if (u != kBlank) atomicAdd(p.cnt + u, 1u);
+        }
+      } else {
+        for (uint64_t sid = gwarp; sid < p.nsets; sid += nwarps) {
+          if (p.covered[sid]) continue;
+          for (uint64_t j = p.off[sid] + lane; j < p.off[sid + 1]; j += 32)
+            atomicAdd(p.cnt + p.mem[j], 1u);
+        }
       }
       cl.sync();
     }
@@ -547,14 +572,20 @@ __global__ void __launch_bounds__(kClBlock, 1) k_select_cluster(const SelectPara
 // slower than 148 -- so the cluster takes stores of up to 2^19 members.
 constexpr uint64_t kClMaxMembers = 1ull << 19;
 
-bool launch_select_cluster(const SelectParams& p, cudaStream_t s) {
-  if (!p.scan || p.nd || p.snap) return false;
-  bool force = false;
-  if (const char* e = std::getenv("RRGPU_SELECT_CLUSTER")) {  // tests / tuning: 0 off, 1 always
+bool select_cluster_eligible(const SelectParams& p) {
+  if (p.nd || p.snap) return false;
+  if (const char* e = std::getenv("RRGPU_SELECT_CLUSTER"))  // tests / tuning: 0 off
     if (*e == '0') return false;
-    force = *e == '1';
-  }
-  if (!force && p.total > kClMaxMembers) return false;
+  return true;
+}
+
+bool launch_select_cluster(const SelectParams& p, cudaStream_t s) {
+  if (!select_cluster_eligible(p)) return false;
+  bool force = false;
+  if (const char* e = std::getenv("RRGPU_SELECT_CLUSTER")) force = *e == '1';
+  // scan mode re-reads the whole store every round: 16 SMs only for small stores;
+  // index mode touches only the seed's sets (capi picks it for larger stores)
+  if (p.scan && !force && p.total > kClMaxMembers) return false;
   const uint32_t ntiles = (p.n + kSelTile - 1) >> kSelTileLog;
   const uint32_t tpc = (ntiles + kClCtas - 1) / kClCtas;
   const size_t smem = static_cast<size_t>(ntiles) * 8 + (kClBlock / 32) * 8 +
