@@ -214,6 +214,18 @@ void d2h(T* dst, const T* src, size_t count, cudaStream_t s) {
 void sync(rrg_graph* g) { host_sync((g->stream)); }
 
 // Grows the row pool of the dense arm to hold `need` rows, keeping the rows in use.
+}  // namespace
+
+namespace rrgpu {
+// The IMM driver's side stores keep their offsets on the host (csrc/imm.cpp).
+void store_keep_host_offsets(rrg_store* s, bool on) {
+  s->keep_hoff = on;
+  if (on && s->hoff.size() != s->nsets + 1) s->hoff.clear();  // valid again after a clear
+}
+}  // namespace rrgpu
+
+namespace {
+
 // Grows the row pool of the dense arm to hold `need` rows, keeping the first
 // `keep` (default: the rows in use).
 void ensure_rows(rrg_store* s, uint64_t need, uint64_t keep = UINT64_MAX) {
@@ -269,8 +281,16 @@ void commit_staged(rrg_store* s, uint64_t count, uint32_t thr, uint64_t rows_big
   s->scan.reserve_discard(count + 1);
   exclusive_scan_u32(s->slot_len.ptr, s->scan.ptr, count, s->scan_tmp, g->stream);
   uint64_t added = 0;
-  d2h(&added, s->scan.ptr + count, 1, g->stream);
+  std::vector<uint64_t> scan_h;
+  const bool mirror = s->keep_hoff && s->hoff.size() == s->nsets + 1;
+  if (mirror) {  // the whole scan in the same round trip: the host offsets
+    scan_h.resize(count + 1);
+    d2h(scan_h.data(), s->scan.ptr, count + 1, g->stream);
+  } else {
+    d2h(&added, s->scan.ptr + count, 1, g->stream);
+  }
   sync(g);
+  if (mirror) added = scan_h[count];
   if (s->member_limit &&
       s->members() + added + big_members + dc[1] > s->member_limit)
     throw OutOfMemory("store member limit reached (" + std::to_string(s->member_limit) +
@@ -295,6 +315,11 @@ void commit_staged(rrg_store* s, uint64_t count, uint32_t thr, uint64_t rows_big
   if (list_max == UINT32_MAX) {  // not reported: read the compaction's maximum back
     d2h(&mx, s->maxlen_dev.ptr, 1, g->stream);
     sync(g);
+  }
+  if (mirror) {
+    for (uint64_t i = 1; i <= count; ++i) s->hoff.push_back(s->total + scan_h[i]);
+  } else if (s->keep_hoff) {
+    s->hoff.clear();  // unknown: invalid until the next clear
   }
   s->nsets += count;
   s->total += added;
@@ -639,6 +664,7 @@ rrg_status rrg_store_clear(rrg_store* s) {
     s->dense_max = 0;
     s->live = 0;
     s->sel_mode = 0;
+    s->hoff.assign(1, 0);
     s->counter_complete = true;
     return RRG_OK;
   });
@@ -1286,9 +1312,19 @@ rrg_status rrg_store_append_from(rrg_store* dst, const rrg_store* src, uint64_t 
     rrg_graph* g = dst->g;
     const cudaStream_t st = g->stream;
     uint64_t ends[2] = {0, 0};
-    d2h(ends, src->off.ptr + first, 1, st);
-    d2h(ends + 1, src->off.ptr + first + count, 1, st);
-    sync(g);
+    const bool mirror = src->keep_hoff && src->hoff.size() == src->nsets + 1;
+    uint32_t mirror_max = 0;
+    if (mirror) {  // the source's offsets are on the host: no round trip
+      ends[0] = src->hoff[first];
+      ends[1] = src->hoff[first + count];
+      for (uint64_t i = first; i < first + count; ++i)
+        mirror_max = std::max<uint32_t>(mirror_max,
+                                        static_cast<uint32_t>(src->hoff[i + 1] - src->hoff[i]));
+    } else {
+      d2h(ends, src->off.ptr + first, 1, st);
+      d2h(ends + 1, src->off.ptr + first + count, 1, st);
+      sync(g);
+    }
     const uint64_t added = ends[1] - ends[0];
     if (dst->total + added > dst->mem.cap)
       dst->mem.reserve_keep(std::max<uint64_t>(dst->total + added, dst->mem.cap + dst->mem.cap / 2),
@@ -1349,12 +1385,22 @@ rrg_status rrg_store_append_from(rrg_store* dst, const rrg_store* src, uint64_t 
     launch_recount(dst->off.ptr + dst->nsets, dst->mem.ptr, count, dst->counter.ptr, st);
     launch_dense_colsum(dst->dbits.ptr, dst->dwords, g->n, nullptr, rows0, dst->ndense - rows0,
                         dst->counter.ptr, +1, st);
-    uint32_t mx = 0;
-    d2h(&mx, dst->maxlen_dev.ptr, 1, st);
-    sync(g);
+    uint32_t mx = mirror_max;
+    if (!mirror) {
+      d2h(&mx, dst->maxlen_dev.ptr, 1, st);
+      sync(g);
+    }
+    if (dst->keep_hoff) {
+      if (mirror && dst->hoff.size() == dst->nsets + 1) {
+        for (uint64_t i = 1; i <= count; ++i)
+          dst->hoff.push_back(dst->total + (src->hoff[first + i] - ends[0]));
+      } else {
+        dst->hoff.clear();  // unknown: invalid until the next clear
+      }
+    }
     dst->nsets += count;
     dst->total += added;
-    dst->max_len = mx;
+    dst->max_len = std::max(dst->max_len, mx);
     dst->live = dst->nsets;  // finalize revives every set
     dst->sel_mode = 0;
     return RRG_OK;

@@ -17,6 +17,7 @@ void set_error(const std::string& msg);
 // shard.cu (multi-GPU): NCCL exchange of this rank's shard + ordered append
 rrg_status exchange_and_append(rrg_store* side, rrg_store* dst, void* comm);
 void nccl_comm_shape(void* comm, int* nranks, int* rank);
+void store_keep_host_offsets(rrg_store* s, bool on);  // capi.cu
 }
 
 namespace {
@@ -179,6 +180,7 @@ class Driver {
       if (!ahead_.s) {
         s = rrg_store_create(g_, &ahead_.s);
         if (s != RRG_OK) return s;
+        rrgpu::store_keep_host_offsets(ahead_.s, true);  // appends need no read-back
       } else {
         rrg_store_clear(ahead_.s);
       }

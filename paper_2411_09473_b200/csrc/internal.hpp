@@ -239,6 +239,10 @@ struct rrg_store {
   rrgpu::DevBuf<uint64_t> xoff;        // export: materialized offsets
   rrgpu::DevBuf<uint32_t> xmem;        // export: materialized members
   uint64_t last_rebuilds = 0;          // rounds of the last select_seeds that rebuilt
+  // host copy of the offsets (side stores the IMM driver appends from): filled
+  // from the commit's scan, so appends need no device read-back
+  bool keep_hoff = false;
+  std::vector<uint64_t> hoff{0};
   uint64_t live = 0;                   // RRRStore::live_count (rrr_store.hpp:84)
   int sel_mode = 0;                    // liveness held by: 0 none (all live), 1 scan copy, 2 covered[]
   uint64_t member_limit = 0;           // 0: none; else RRG_ENOMEM past it (tests, budgets)
