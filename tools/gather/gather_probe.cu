@@ -89,6 +89,12 @@ int main(int argc, char** argv) {
   const double gb = argc > 1 ? atof(argv[1]) : 8.0;
   const int steps = argc > 2 ? atoi(argv[2]) : 256;
   const uint64_t n = (uint64_t)(gb * (1ull << 30)) / 32;
+  if (argc > 3) {  // L2 fetch granularity hint in bytes (32 / 64 / 128)
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(argv[3]));
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+    printf("{\"l2_fetch_granularity\": %zu}\n", got);
+  }
   uint4* t;
   unsigned long long* sink;
   cudaMalloc(&t, n * 32);

@@ -19,7 +19,19 @@ ap.add_argument("--lt-kary", type=int, default=0)
 ap.add_argument("--ic-mode", type=int, default=0)
 ap.add_argument("--lt-guide-mult", type=int, default=0)
 ap.add_argument("--ic-rng", type=int, default=0, help="1 = fast statistical IC sampling")
+ap.add_argument("--l2-fetch", type=int, default=0,
+                help="cudaLimitMaxL2FetchGranularity hint in bytes (32 / 64 / 128); 0 = leave")
+ap.add_argument("--reps", type=int, default=1)
 a = ap.parse_args()
+if a.l2_fetch:
+    import ctypes
+    import torch
+    torch.cuda.init()
+    rt = ctypes.CDLL("libcudart.so.12")
+    got = ctypes.c_size_t(0)
+    rc = rt.cudaDeviceSetLimit(5, ctypes.c_size_t(a.l2_fetch))  # cudaLimitMaxL2FetchGranularity
+    rt.cudaDeviceGetLimit(ctypes.byref(got), 5)
+    print(f"l2 fetch granularity: set rc {rc}, now {got.value}")
 cfg = graphs.CONFIGS[a.workload]
 if a.n:
     cfg = graphs.scaled(cfg, a.n, a.m)
@@ -39,6 +51,10 @@ g.set_option("ic_mode", a.ic_mode)
 g.set_option("ic_rng", a.ic_rng)
 st = P.RRRStore(g)
 P.generate_batch(g, cfg.model, 99, a.sets, st)
+for _ in range(a.reps - 1):
+    st.clear()
+    P.generate_batch(g, cfg.model, 1, a.sets, st)
+    print(f"rep sample {g.last_batch_stats().sample_ms:.3f} ms")
 st.clear()
 t = time.time()
 P.generate_batch(g, cfg.model, 1, a.sets, st)
