@@ -222,6 +222,9 @@ void store_keep_host_offsets(rrg_store* s, bool on) {
   s->keep_hoff = on;
   if (on && s->hoff.size() != s->nsets + 1) s->hoff.clear();  // valid again after a clear
 }
+// IC: running mean of inspected in-edges per set on this graph (< 0: no batch
+// sampled yet) -- the IMM driver's estimate of what sampling ahead costs.
+double graph_ic_mean_inspected(const rrg_graph* g) { return g->ic_mean_insp; }
 }  // namespace rrgpu
 
 namespace {

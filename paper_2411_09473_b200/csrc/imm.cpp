@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -18,7 +19,12 @@ void set_error(const std::string& msg);
 rrg_status exchange_and_append(rrg_store* side, rrg_store* dst, void* comm);
 void nccl_comm_shape(void* comm, int* nranks, int* rank);
 void store_keep_host_offsets(rrg_store* s, bool on);  // capi.cu
+double graph_ic_mean_inspected(const rrg_graph* g);   // capi.cu
 }
+
+#ifndef RRG_IMM_FREE_EDGES
+#define RRG_IMM_FREE_EDGES 67108864.0  // 2^26 inspected edges: ~1.5 ms of IC sampler throughput
+#endif
 
 namespace {
 
@@ -207,10 +213,46 @@ class Driver {
     // batches are bound by their largest sets, so 69K sets cost about what 23K do
     // (IMM cfg3 28.5 -> 24.0 ms; the other configs unchanged)
     constexpr uint64_t kAheadMax = 1ull << 17;
+    // IC batches of few inspected edges in total are bound by the latency of
+    // their largest set, not by the work (cfg3: 92,504 sets are 10M inspected
+    // edges, 0.2 ms of sampler throughput, behind one 10 ms set): while the
+    // slots up to a later round's target stay under kFreeEdges of estimated work
+    // (mean inspected edges per set of this graph's earlier batches), sample
+    // them in the same batch, however many rounds ahead that is.
+    static const double kFreeEdges = [] {
+      const char* e = std::getenv("RRGPU_IMM_FREE_EDGES");  // tuning
+      return e ? std::atof(e) : RRG_IMM_FREE_EDGES;
+    }();
+    // off by default: measured cfg1 11.4 -> 10.0 ms (the final batch disappears)
+    // but cfg3 19.7 -> 24.3 ms (30 % more slots, one more giant set in the tail,
+    // and that run needs no final top-up): profiles/r2/NOTES.md
+    static const bool kFinal = [] {
+      const char* e = std::getenv("RRGPU_IMM_SPEC_FINAL");  // tuning
+      return e && *e == '1';
+    }();
+    const double mean = cfg_->model == RRG_IC ? rrgpu::graph_ic_mean_inspected(g_) : -1.0;
+    auto free_to = [&](uint64_t from, uint64_t to) {
+      return mean >= 0.0 && to > from && static_cast<double>(to - from) * mean <= kFreeEdges;
+    };
     uint64_t best = 0;
-    for (unsigned j = i + 1; j <= std::min(rounds_total, i + 2); ++j) {
+    unsigned jlast = 0;
+    for (unsigned j = i + 1; j <= rounds_total; ++j) {
       const uint64_t tj = theta_for_round(n_, cfg_->k, cfg_->epsilon, ell_, j);
-      if (tj > size_ && tj - size_ <= kAheadMax) best = std::max(best, tj);
+      if (tj <= size_) continue;
+      if (tj - size_ > kAheadMax) break;
+      if (j <= i + 2 || free_to(size_, tj)) {
+        best = std::max(best, tj);
+        jlast = j;
+      }
+    }
+    // The final top-up (imm.hpp:227-231): a trigger at round j gives LB >= x_j,
+    // so theta <= set_theta(x_j). While those extra slots are free too, the batch
+    // covers them and the final top-up finds its sets already sampled.
+    if (kFinal && mean >= 0.0) {
+      const unsigned j = std::max(jlast, i);
+      const uint64_t have = std::max(best, theta_for_round(n_, cfg_->k, cfg_->epsilon, ell_, i));
+      const uint64_t fj = set_theta(n_, cfg_->k, cfg_->epsilon, ell_, round_target(n_, j));
+      if (fj > have && fj - size_ <= kAheadMax && free_to(have, fj)) best = fj;
     }
     return best;
   }
