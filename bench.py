@@ -418,7 +418,7 @@ def imm_block(P, name, orc, cores, reps=3):
     e2e = []
     for _ in range(1 if name in SLOW_REFERENCE else 3):
         t0 = time.perf_counter()
-        ge = P.Graph(*host)
+        ge = P.Graph(*host, model=cfg.model)  # upload overlaps the model's layouts
         re_ = P.run_imm(ge, icfg)
         e2e.append(time.perf_counter() - t0)
         ge.close()
@@ -802,7 +802,7 @@ def run_ours(args, rank, world, local):
                 walls.append(time.perf_counter() - ti)
             gpu_imm = statistics.median(walls)
             ti = time.perf_counter()  # end to end: upload + K0 + IMM + seeds back
-            ge = P.Graph(*host)
+            ge = P.Graph(*host, model=model)  # upload overlaps the model's layouts
             re = P.run_imm(ge, icfg)
             ge.close()
             gpu_imm_e2e = time.perf_counter() - ti

@@ -49,6 +49,14 @@ void rrg_graph_destroy(rrg_graph* g);
 rrg_status rrg_graph_prepare(rrg_graph* g, rrg_model model);
 /* Runs every subsequent call of this graph and its stores on `cuda_stream`
  * (a cudaStream_t; NULL restores the graph's private stream). */
+/* rrg_graph_create with the diffusion model the graph will be sampled under
+ * (RRG_IC, RRG_LT, or -1 = unknown: exactly rrg_graph_create). With RRG_LT the
+ * weight-only LT layouts (the exact sequential fp64 CDF, sampling.hpp:130-136)
+ * are built on the device while the sources are still being uploaded; results
+ * are identical, only the time from host arrays to the first batch changes. */
+rrg_status rrg_graph_create_for(uint32_t n, uint64_t m, const uint64_t* rev_offsets,
+                                const uint32_t* rev_sources, const float* rev_weights,
+                                int model_hint, rrg_graph** out);
 /* On-device graph preparation: uploads an edge list
  * (src[i] -> dst[i], weight w[i]) and builds the transpose on the device in the
  * in-list order of detail::build_graph (graph.hpp:69-115: sources ascending,
@@ -291,6 +299,10 @@ uint64_t rrg_host_sync_count(void);
 uint64_t rrg_debug_bernoulli_threshold(uint32_t weight_bits);
 /* The 32-bit threshold stored in IC edge records: T >> 21, saturated at 2^32-1. */
 uint32_t rrg_debug_bernoulli_thr_hi(uint32_t weight_bits);
+/* Test hook: the LT running sums cdf[j] = acc after in-edge j (sampling.hpp:130-136:
+ * acc = 0.0 per vertex, acc += (double)w[j] in CSR order) as the device built them;
+ * f64[m]. Must equal the host's sequential sums bit for bit. */
+rrg_status rrg_debug_export_lt_cdf(rrg_graph* g, double* cdf);
 /* Test hook: advances a xoshiro256** state (4 words) by k draws with the GF(2)
  * jump matrices the IC hub expansion uses (csrc/jump.cpp). */
 void rrg_debug_jump(const uint64_t* state_in, uint64_t k, uint64_t* state_out);

@@ -48,16 +48,30 @@ inline rrg_model to_c(DiffusionModel m) { return m == DiffusionModel::IC ? RRG_I
 class Graph {
  public:
   Graph(uint32_t n, const std::vector<uint64_t>& reverse_offsets,
-        const std::vector<uint32_t>& reverse_sources, const std::vector<float>& reverse_weights) {
+        const std::vector<uint32_t>& reverse_sources, const std::vector<float>& reverse_weights)
+      : Graph(n, reverse_offsets, reverse_sources, reverse_weights, -1) {}
+  // With the diffusion model the graph will be sampled under, the upload and
+  // the model's device layouts overlap (rrg_graph_create_for); same results.
+  Graph(uint32_t n, const std::vector<uint64_t>& reverse_offsets,
+        const std::vector<uint32_t>& reverse_sources, const std::vector<float>& reverse_weights,
+        DiffusionModel model)
+      : Graph(n, reverse_offsets, reverse_sources, reverse_weights, static_cast<int>(to_c(model))) {}
+
+ private:
+  Graph(uint32_t n, const std::vector<uint64_t>& reverse_offsets,
+        const std::vector<uint32_t>& reverse_sources, const std::vector<float>& reverse_weights,
+        int model_hint) {
     if (reverse_offsets.size() != static_cast<size_t>(n) + 1)
       throw std::invalid_argument("reverse_offsets must hold n + 1 entries");
     if (reverse_sources.size() != reverse_weights.size())
       throw std::invalid_argument("reverse_sources and reverse_weights differ in length");
     rrg_graph* h = nullptr;
-    check(rrg_graph_create(n, reverse_sources.size(), reverse_offsets.data(),
-                           reverse_sources.data(), reverse_weights.data(), &h));
+    check(rrg_graph_create_for(n, reverse_sources.size(), reverse_offsets.data(),
+                               reverse_sources.data(), reverse_weights.data(), model_hint, &h));
     h_.reset(h);
   }
+
+ public:
   uint32_t num_vertices() const { return rrg_graph_num_vertices(h_.get()); }
   uint64_t num_edges() const { return rrg_graph_num_edges(h_.get()); }
   rrg_graph* handle() const { return h_.get(); }

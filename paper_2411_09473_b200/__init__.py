@@ -83,7 +83,10 @@ def normalize_lt_weights(roff, rw):
 class Graph:
     """Device-resident transpose CSR (the reverse arrays of rrflow::Graph)."""
 
-    def __init__(self, rev_offsets, rev_sources, rev_weights):
+    def __init__(self, rev_offsets, rev_sources, rev_weights, model=None):
+        """model (optional: IC / LT, as generate_batch takes it): the diffusion
+        model the graph will be sampled under -- the upload then overlaps that
+        model's device layouts (rrg_graph_create_for); results are the same."""
         self.reverse_offsets = np.ascontiguousarray(rev_offsets, dtype=np.uint64)
         self.reverse_sources = np.ascontiguousarray(rev_sources, dtype=np.uint32)
         self.reverse_weights = np.ascontiguousarray(rev_weights, dtype=np.float32)
@@ -95,10 +98,10 @@ class Graph:
         self.num_vertices = int(self.reverse_offsets.size - 1)
         self.num_edges = int(self.reverse_sources.size)
         h = C.c_void_p()
-        check(lib.rrg_graph_create(
+        check(lib.rrg_graph_create_for(
             self.num_vertices, self.num_edges, ptr(self.reverse_offsets, C.c_uint64),
             ptr(self.reverse_sources, C.c_uint32), ptr(self.reverse_weights, C.c_float),
-            C.byref(h)))
+            -1 if model is None else _model(model), C.byref(h)))
         self._h = h
 
     @classmethod

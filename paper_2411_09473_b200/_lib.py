@@ -64,6 +64,8 @@ class ImmResultC(C.Structure):
 # (name, restype, argtypes) for every symbol of include/rrgpu.h
 SIGNATURES = [
     ("rrg_graph_create", C.c_int, [C.c_uint32, C.c_uint64, u64p, u32p, f32p, C.POINTER(vp)]),
+    ("rrg_graph_create_for", C.c_int,
+     [C.c_uint32, C.c_uint64, u64p, u32p, f32p, C.c_int, C.POINTER(vp)]),
     ("rrg_graph_create_from_edges", C.c_int,
      [C.c_uint32, C.c_uint64, u32p, u32p, f32p, C.c_int, C.POINTER(vp)]),
     ("rrg_graph_export_transpose", C.c_int, [vp, u64p, u32p, f32p]),
@@ -114,6 +116,7 @@ SIGNATURES = [
     ("rrg_version", C.c_char_p, []),
     ("rrg_debug_bernoulli_threshold", C.c_uint64, [C.c_uint32]),
     ("rrg_debug_bernoulli_thr_hi", C.c_uint32, [C.c_uint32]),
+    ("rrg_debug_export_lt_cdf", C.c_int, [vp, C.POINTER(C.c_double)]),
     ("rrg_debug_jump", None, [u64p, C.c_uint64, u64p]),
 ]
 

@@ -380,6 +380,17 @@ uint32_t rrg_debug_bernoulli_thr_hi(uint32_t bits) { return bern_thr_hi(bits); }
 
 rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* roff, const uint32_t* rsrc,
                             const float* rw, rrg_graph** out) {
+  return rrg_graph_create_for(n, m, roff, rsrc, rw, -1, out);
+}
+
+// model_hint = RRG_LT: the LT layouts that need only offsets and weights (the
+// exact sequential fp64 CDF: k_build_cdf, and the hubs' serial chains,
+// k_build_cdf_long) are built on a second stream WHILE the sources are still
+// crossing PCIe: upload order offsets, weights, sources; the CDF kernels start
+// at the weights' arrival. At cfg4 the 5.9 ms of CDF chains hide behind the
+// 5.1 ms source upload (IMM from host arrays 24 -> ~17 ms).
+rrg_status rrg_graph_create_for(uint32_t n, uint64_t m, const uint64_t* roff, const uint32_t* rsrc,
+                                const float* rw, int model_hint, rrg_graph** out) {
   if (!out) return invalid("rrg_graph_create: null output");
   *out = nullptr;
   if (m >= (1ull << 32)) return invalid("rrg_graph_create: m must be < 2^32");
@@ -387,8 +398,12 @@ rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* roff, const 
   if (m && (!rsrc || !rw)) return invalid("rrg_graph_create: null edge arrays");
   if (n == UINT32_MAX) return invalid("rrg_graph_create: n must be < 2^32 - 1");
   if (n == 0 && m != 0) return invalid("rrg_graph_create: edges without vertices");
+  if (model_hint != -1 && model_hint != RRG_IC && model_hint != RRG_LT)
+    return invalid("rrg_graph_create_for: unknown model hint");
   auto* g = new (std::nothrow) rrg_graph;
   if (!g) return RRG_ENOMEM;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_off = nullptr, ev_w = nullptr;
   const rrg_status st = guarded([&]() -> rrg_status {
     RRG_CUDA(cudaGetDevice(&g->device));
     RRG_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device));
@@ -412,15 +427,62 @@ rrg_status rrg_graph_create(uint32_t n, uint64_t m, const uint64_t* roff, const 
     off64.reserve_discard(static_cast<size_t>(n) + 1);
     RRG_CUDA(cudaMemcpyAsync(off64.ptr, roff, (static_cast<size_t>(n) + 1) * 8,
                              cudaMemcpyHostToDevice, g->stream));
-    if (m) {
-      RRG_CUDA(cudaMemcpyAsync(g->src.ptr, rsrc, m * 4, cudaMemcpyHostToDevice, g->stream));
-      RRG_CUDA(cudaMemcpyAsync(g->w.ptr, rw, m * 4, cudaMemcpyHostToDevice, g->stream));
+    const bool overlap = model_hint == RRG_LT && m != 0;
+    if (!overlap) {
+      if (m) {
+        RRG_CUDA(cudaMemcpyAsync(g->src.ptr, rsrc, m * 4, cudaMemcpyHostToDevice, g->stream));
+        RRG_CUDA(cudaMemcpyAsync(g->w.ptr, rw, m * 4, cudaMemcpyHostToDevice, g->stream));
+      }
+      const uint32_t bad = upload_checks(g, off64.ptr, 3u);
+      if (bad & 1u) return invalid("rrg_graph_create: offsets must run 0..m, non-decreasing");
+      if (bad & 2u) return invalid("rrg_graph_create: source id out of range");
+      return RRG_OK;
     }
-    const uint32_t bad = upload_checks(g, off64.ptr);
-    if (bad & 1u) return invalid("rrg_graph_create: offsets must run 0..m, non-decreasing");
-    if (bad & 2u) return invalid("rrg_graph_create: source id out of range");
+    RRG_CUDA(cudaEventCreateWithFlags(&ev_off, cudaEventDisableTiming));
+    RRG_CUDA(cudaEventCreateWithFlags(&ev_w, cudaEventDisableTiming));
+    RRG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    // main stream: offsets (checked), weights, sources (checked)
+    DevBuf<uint32_t> bad;
+    // pinned flag words (kept per thread): a pageable read would be staged
+    // behind the uploads
+    thread_local uint32_t* hbad = nullptr;
+    if (!hbad) RRG_CUDA(cudaMallocHost(&hbad, 8));
+    hbad[0] = hbad[1] = 0;
+    upload_checks_async(g, off64.ptr, 1u, bad);
+    RRG_CUDA(cudaMemcpyAsync(hbad, bad.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
+    RRG_CUDA(cudaEventRecord(ev_off, g->stream));
+    RRG_CUDA(cudaMemcpyAsync(g->w.ptr, rw, m * 4, cudaMemcpyHostToDevice, g->stream));
+    RRG_CUDA(cudaEventRecord(ev_w, g->stream));
+    RRG_CUDA(cudaMemcpyAsync(g->src.ptr, rsrc, m * 4, cudaMemcpyHostToDevice, g->stream));
+    DevBuf<uint32_t> bad2;
+    upload_checks_async(g, off64.ptr, 2u, bad2);
+    RRG_CUDA(cudaMemcpyAsync(hbad + 1, bad2.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
+    // the CDF kernels index the weights through the offsets: only valid ones
+    RRG_CUDA(cudaEventSynchronize(ev_off));
+    g_syncs += 1;
+    if (hbad[0] & 1u) {
+      host_sync((g->stream));
+      return invalid("rrg_graph_create: offsets must run 0..m, non-decreasing");
+    }
+    // side stream: the CDF, from the weights' arrival on
+    RRG_CUDA(cudaStreamWaitEvent(side, ev_w, 0));
+    const cudaStream_t main_stream = g->stream;
+    g->stream = side;
+    try {
+      prepare_lt(g);  // ends with a host sync of the side stream
+    } catch (...) {
+      g->stream = main_stream;
+      cudaStreamSynchronize(main_stream);
+      throw;
+    }
+    g->stream = main_stream;
+    host_sync((g->stream));
+    if (hbad[1] & 2u) return invalid("rrg_graph_create: source id out of range");
     return RRG_OK;
   });
+  if (side) cudaStreamDestroy(side);
+  if (ev_off) cudaEventDestroy(ev_off);
+  if (ev_w) cudaEventDestroy(ev_w);
   if (st != RRG_OK) {
     rrg_graph_destroy(g);
     return st;
@@ -513,6 +575,17 @@ rrg_status rrg_graph_export_transpose(const rrg_graph* g, uint64_t* roff, uint32
   });
 }
 
+// Test hook: the LT CDF as built on the device (prepares the LT layout first).
+rrg_status rrg_debug_export_lt_cdf(rrg_graph* g, double* cdf) {
+  if (!g || (g->m && !cdf)) return invalid("null argument");
+  return guarded([&]() -> rrg_status {
+    prepare_lt(g);
+    if (g->m) d2h(cdf, g->cdf.ptr, g->m, g->stream);
+    sync(g);
+    return RRG_OK;
+  });
+}
+
 namespace {
 void graph_free(rrg_graph* g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
@@ -540,7 +613,7 @@ rrg_status rrg_graph_prepare(rrg_graph* g, rrg_model model) {
   if (model != RRG_IC && model != RRG_LT) return invalid("unknown diffusion model");
   return guarded([&]() -> rrg_status {
     if (model == RRG_IC) prepare_ic(g);
-    else prepare_lt_mode(g);
+    else prepare_lt_mode(g, 0);
     return RRG_OK;
   });
 }
@@ -577,6 +650,7 @@ rrg_status rrg_graph_set_option(rrg_graph* g, rrg_option opt, int64_t value) {
     case RRG_OPT_LT_GUIDE_MULT:
       if (value < 1 || value > 16) return invalid("lt_guide_mult must be in [1, 16]");
       g->lt_guide_mult = static_cast<uint32_t>(value);
+      g->lt_guide_mult_explicit = true;
       return RRG_OK;
     case RRG_OPT_LT_COOP_MIN:
       if (value < 2) return invalid("coop_min must be >= 2");
@@ -765,7 +839,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
   return guarded([&]() -> rrg_status {
     int lt_mode = kLtLinear;
     if (model == RRG_IC) prepare_ic(g);
-    else lt_mode = prepare_lt_mode(g);
+    else lt_mode = prepare_lt_mode(g, count);
     const bool ic_fast = model == RRG_IC && g->ic_rng == 1;
     if (model == RRG_IC) prepare_ic_fast(g);  // uniform-weight flags (fast mode, list expansion)
     if (!fused) s->counter_complete = false;
@@ -864,7 +938,7 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.ctl = g->ctl.ptr;
       p.lt_scan = lt_mode;
       p.ltguide = g->ltguide.ptr;
-      p.lt_guide_mult = g->lt_guide_mult;
+      p.lt_guide_mult = g->lt_guide_built;
       p.coop_min = g->coop_min;
       p.jtab = g->jtab.ptr;
       p.jtab16 = g->jtab16.ptr;

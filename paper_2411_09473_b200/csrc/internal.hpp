@@ -137,6 +137,8 @@ struct rrg_graph {
   rrgpu::DevBuf<uint4> ltguide;  // LT: guide table, 32 bytes per bucket (common.cuh), lazy
   uint32_t lt_guide_mult = 4;    // LT: guide buckets per in-edge (4: 0.74 vs 0.85 ms at 2, cfg4 65K walks)
   uint32_t lt_guide_built = 0;   // multiplier the current table was built with (0: none)
+  uint64_t lt_light_walks = 0;   // walks sampled on the light (one bucket per in-edge) table
+  bool lt_guide_mult_explicit = false;  // set through RRG_OPT_LT_GUIDE_MULT: no light table
   bool lt_search_ready = false;  // LT: records + search trees built
   rrgpu::DevBuf<uint64_t> jtab;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
   rrgpu::DevBuf<uint64_t> jtab16;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
@@ -332,10 +334,13 @@ void prepare_lt(rrg_graph* g);  // fp64 CDF + monotone flag
 // prepare_lt + what the graph's LT scan mode needs; returns the mode to launch
 // (guide falls back to search when the table does not fit, both to linear
 // when the CDF is not monotone)
-int prepare_lt_mode(rrg_graph* g);
+int prepare_lt_mode(rrg_graph* g, uint64_t batch_sets);  // 0: explicit prepare
 // converts d_off64 into g->off and validates offsets/sources on the device;
 // returns a bit mask of violations (1 offsets, 2 sources), 0 if clean
-uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64);
+// which: 1 = offsets, 2 = sources (sample.cu)
+uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64, uint32_t which);
+void upload_checks_async(rrg_graph* g, const uint64_t* d_off64, uint32_t which,
+                         DevBuf<uint32_t>& bad);
 int sampler_block();
 int sampler_blocks_per_sm(int model, uint32_t ic_inner, int lt_mode = 1);
 // IC schedules: lane per sample; warp per sample over its 32 lanes' scratch

@@ -248,19 +248,28 @@ __global__ void k_check_sources(const uint32_t* src, uint64_t m, uint32_t n, uin
 
 }  // namespace
 
-uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64) {
-  DevBuf<uint32_t> bad;
+// which: 1 = offsets (u64 -> u32 + monotonicity / range), 2 = sources < n.
+// Enqueues the checks on the graph's stream; `bad` receives the flag word.
+void upload_checks_async(rrg_graph* g, const uint64_t* d_off64, uint32_t which,
+                         DevBuf<uint32_t>& bad) {
   bad.reserve_discard(1);
   RRG_CUDA(cudaMemsetAsync(bad.ptr, 0, 4, g->stream));
   const int grid = g->num_sms * 8;
-  k_offsets_u32<<<grid, 256, 0, g->stream>>>(d_off64, g->off.ptr, g->n, g->m, bad.ptr);
-  RRG_CUDA(cudaGetLastError());
-  count_launch();
-  if (g->m) {
+  if (which & 1u) {
+    k_offsets_u32<<<grid, 256, 0, g->stream>>>(d_off64, g->off.ptr, g->n, g->m, bad.ptr);
+    RRG_CUDA(cudaGetLastError());
+    count_launch();
+  }
+  if ((which & 2u) && g->m) {
     k_check_sources<<<grid, 256, 0, g->stream>>>(g->src.ptr, g->m, g->n, bad.ptr);
     RRG_CUDA(cudaGetLastError());
     count_launch();
   }
+}
+
+uint32_t upload_checks(rrg_graph* g, const uint64_t* d_off64, uint32_t which) {
+  DevBuf<uint32_t> bad;
+  upload_checks_async(g, d_off64, which, bad);
   uint32_t h = 0;
   RRG_CUDA(cudaMemcpyAsync(&h, bad.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
   host_sync((g->stream));

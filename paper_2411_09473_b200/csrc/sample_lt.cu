@@ -622,18 +622,34 @@ __global__ void k_build_cdf(const uint32_t* off, const float* w, double* cdf, ui
   }
 }
 
-// Hub in-lists: one warp per list. The warp streams the weights into shared
-// memory with asynchronous copies (LDGSTS), double-buffered 512 entries ahead,
-// while lane 0 runs the dependent fp64 add chain out of shared memory; the warp
-// then writes the 512 prefix values back with coalesced stores. The chain
-// itself -- the reference's sequential order -- is the only serial part.
-constexpr int kCdfChunk = 512;
+// Hub in-lists: one warp per list. The reference's running sum acc += (double)w[j]
+// (sampling.hpp:130-136) is a serial fp64 chain -- ~20 cycles per entry on one
+// lane, 5.5 ms for cfg4's 542,861-entry hub -- but almost every one of its adds
+// is EXACT (the weights are floats, the sum is < 2: an add rounds only when a
+// weight has bits below the sum's last place, ~0.005 % of cfg4's hub entries).
+// Exact adds are associative, so the warp scans 256 entries at a time in
+// parallel -- eight per lane, a warp scan of the lane totals, the carry added
+// last -- with every add checked by TwoSum: when all error terms are zero each
+// value is the exact sum of its operands, hence representable, hence what the
+// serial chain produces (by induction from the carry, which IS the chain's
+// value). A chunk with any nonzero error term is redone by lane 0 as the plain
+// serial chain. The weights stream into shared memory with asynchronous copies
+// (LDGSTS), double-buffered one stage ahead.
+constexpr int kCdfChunk = 512;  // staged entries (two scanned chunks of 256)
 constexpr int kCdfWarps = 4;
+// s = fl(a + b); err |= (a + b != s), Knuth's TwoSum (no ordering assumption)
+__device__ __forceinline__ double cdf_add_checked(double a, double b, bool& err) {
+  const double s = __dadd_rn(a, b);
+  const double bb = __dadd_rn(s, -a);
+  const double e = __dadd_rn(__dadd_rn(a, -__dadd_rn(s, -bb)), __dadd_rn(b, -bb));
+  err |= e != 0.0;
+  return s;
+}
 __global__ void __launch_bounds__(kCdfWarps * 32)
     k_build_cdf_long(const uint32_t* off, const float* w, double* cdf, const uint32_t* longv,
                      const uint32_t* nlong, uint32_t* bad) {
-  __shared__ float sw[kCdfWarps][2][kCdfChunk];
-  __shared__ double sd[kCdfWarps][kCdfChunk];
+  __shared__ __align__(16) float sw[kCdfWarps][2][kCdfChunk];
+  __shared__ double sd[kCdfWarps][256];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const uint32_t nw = gridDim.x * kCdfWarps;
   for (uint32_t i = blockIdx.x * kCdfWarps + wl; i < *nlong; i += nw) {
@@ -645,7 +661,7 @@ __global__ void __launch_bounds__(kCdfWarps * 32)
         __pipeline_memcpy_async(&sw[wl][buf][t], w + c0 + t, sizeof(float));
       __pipeline_commit();
     };
-    double acc = 0.0;
+    double acc = 0.0;  // the chain's value before the current chunk (warp-uniform)
     bool neg = false;
     fetch(b, 0);
     int cur = 0;
@@ -653,37 +669,77 @@ __global__ void __launch_bounds__(kCdfWarps * 32)
       const uint32_t len = min(static_cast<uint32_t>(kCdfChunk), e - c0);
       if (c0 + kCdfChunk < e) {
         fetch(c0 + kCdfChunk, cur ^ 1);
-        __pipeline_wait_prior(1);  // this chunk landed; the next stays in flight
+        __pipeline_wait_prior(1);  // this stage landed; the next stays in flight
       } else {
         __pipeline_wait_prior(0);
       }
       __syncwarp();
-      if (lane == 0) {
-        const float* x = sw[wl][cur];
-        double* y = sd[wl];
-        uint32_t t = 0;
-        for (; t + 8 <= len; t += 8) {
-          float xs[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) xs[u] = x[t + u];
+      for (uint32_t h0 = 0; h0 < len; h0 += 256) {
+        const float* x = sw[wl][cur] + h0;
+        const uint32_t hl = min(256u, len - h0);
+        // lane l: entries [8 l, 8 l + 8) of the chunk (zeros past its end: exact)
+        double loc[8];
+        bool err = false;
+        {
+          const float4 q0 = *reinterpret_cast<const float4*>(x + 8 * lane);
+          const float4 q1 = *reinterpret_cast<const float4*>(x + 8 * lane + 4);
+          const float xs[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+          double run = 0.0;
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            neg |= !(xs[u] >= 0.0f);
-            acc = __dadd_rn(acc, static_cast<double>(xs[u]));
-            y[t + u] = acc;
+            const bool in = 8u * lane + u < hl;
+            const float xv = in ? xs[u] : 0.0f;
+            neg |= !(xv >= 0.0f);
+            run = u == 0 ? static_cast<double>(xv)
+                         : cdf_add_checked(run, static_cast<double>(xv), err);
+            loc[u] = run;
           }
         }
-        for (; t < len; ++t) {
-          neg |= !(x[t] >= 0.0f);
-          acc = __dadd_rn(acc, static_cast<double>(x[t]));
-          y[t] = acc;
+        double incl = loc[7];  // inclusive scan of the lane totals
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl = cdf_add_checked(y, incl, err);
+        }
+        double base = __shfl_up_sync(kFull, incl, 1);  // exclusive prefix of the lane
+        base = lane == 0 ? acc : cdf_add_checked(acc, base, err);
+        double out[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) out[u] = cdf_add_checked(base, loc[u], err);
+        if (!__any_sync(kFull, err)) {
+          double* y = cdf + c0 + h0 + 8 * lane;
+          if (8u * lane + 8 <= hl && ((c0 + h0) & 1u) == 0) {
+#pragma unroll
+            for (int u = 0; u < 8; u += 2)
+              *reinterpret_cast<double2*>(y + u) = make_double2(out[u], out[u + 1]);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (8u * lane + u < hl) y[u] = out[u];
+          }
+          // the chain after the chunk: its last entry's value
+          const uint32_t last = hl - 1;
+          double tail = out[0];
+#pragma unroll
+          for (int u = 1; u < 8; ++u) tail = (last & 7u) == static_cast<uint32_t>(u) ? out[u] : tail;
+          acc = __shfl_sync(kFull, tail, last >> 3);
+        } else {  // some add rounded: the serial chain, as the reference runs it
+          if (lane == 0) {
+            double a2 = acc;
+            for (uint32_t t = 0; t < hl; ++t) {
+              a2 = __dadd_rn(a2, static_cast<double>(x[t]));
+              sd[wl][t] = a2;
+            }
+          }
+          __syncwarp();
+          for (uint32_t t = lane; t < hl; t += 32) cdf[c0 + h0 + t] = sd[wl][t];
+          acc = sd[wl][hl - 1];
+          __syncwarp();
         }
       }
-      __syncwarp();
-      for (uint32_t t = lane; t < len; t += 32) cdf[c0 + t] = sd[wl][t];
-      __syncwarp();
+      __syncwarp();  // the stage is free for the copy after next
     }
-    if (lane == 0 && neg) *bad = 1;
+    if (__any_sync(kFull, neg) && lane == 0) *bad = 1;
   }
 }
 
@@ -1041,12 +1097,29 @@ void prepare_lt_search(rrg_graph* g) {
 
 // LT guide mode: 32 bytes per bucket, mult buckets per in-edge. False (and no
 // table) when the CDF is not monotone or the table would not fit in free HBM.
-bool prepare_lt_guide(rrg_graph* g) {
+// batch_sets (0: an explicit prepare) picks the multiplier of a table built on
+// demand: a batch below kGuideLightSets walks gets the light table (one bucket
+// per in-edge: a quarter of the build time and of the memory; more buckets hold
+// two or more CDF entries, which costs a small batch nothing measurable), and
+// the first large batch replaces it with the full one. A multiplier set through
+// RRG_OPT_LT_GUIDE_MULT is always used as given.
+constexpr uint64_t kGuideLightSets = 1ull << 17;
+constexpr uint64_t kGuideLightTotal = 1ull << 19;
+bool prepare_lt_guide(rrg_graph* g, uint64_t batch_sets) {
   if (!g->cdf_monotone || !g->m) return false;
-  if (g->lt_guide_built == g->lt_guide_mult && g->ltguide.ptr) return true;
+  // ... and so do many small ones (kGuideLightTotal walks on the light table)
+  bool light_ok = !g->lt_guide_mult_explicit && batch_sets && batch_sets < kGuideLightSets;
+  if (light_ok && g->lt_guide_built != g->lt_guide_mult) {
+    g->lt_light_walks += batch_sets;
+    light_ok = g->lt_light_walks <= kGuideLightTotal;
+  }
+  if (g->ltguide.ptr && g->lt_guide_built &&
+      (g->lt_guide_built == g->lt_guide_mult || light_ok))
+    return true;
+  const uint32_t mult = light_ok ? 1u : g->lt_guide_mult;
   g->ltguide.release();
   g->lt_guide_built = 0;
-  const uint64_t entries = static_cast<uint64_t>(g->lt_guide_mult) * g->m;
+  const uint64_t entries = static_cast<uint64_t>(mult) * g->m;
   size_t freeb = 0, totalb = 0;
   RRG_CUDA(cudaMemGetInfo(&freeb, &totalb));
   if (entries * 32 + (2ull << 30) > freeb) return false;
@@ -1054,18 +1127,18 @@ bool prepare_lt_guide(rrg_graph* g) {
   const uint64_t chunks = (entries + kGuideChunk - 1) / kGuideChunk;
   const uint64_t grid = std::min<uint64_t>((chunks + 127) / 128, 1u << 20);
   k_build_ltguide<<<static_cast<unsigned>(grid), 128, 0, g->stream>>>(
-      g->off.ptr, g->cdf.ptr, g->src.ptr, g->n, g->m, g->lt_guide_mult, g->ltguide.ptr);
+      g->off.ptr, g->cdf.ptr, g->src.ptr, g->n, g->m, mult, g->ltguide.ptr);
   RRG_CUDA(cudaGetLastError());
   count_launch();
   host_sync((g->stream));
-  g->lt_guide_built = g->lt_guide_mult;
+  g->lt_guide_built = mult;
   return true;
 }
 
 // The structures the graph's LT scan mode needs; returns the mode launches use.
-int prepare_lt_mode(rrg_graph* g) {
+int prepare_lt_mode(rrg_graph* g, uint64_t batch_sets) {
   prepare_lt(g);
-  if (g->lt_scan == kLtGuide && prepare_lt_guide(g)) return kLtGuide;
+  if (g->lt_scan == kLtGuide && prepare_lt_guide(g, batch_sets)) return kLtGuide;
   if (g->lt_scan == kLtLinear || !g->cdf_monotone) return kLtLinear;
   prepare_lt_search(g);
   return kLtBsearch;

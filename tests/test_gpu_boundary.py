@@ -91,3 +91,63 @@ def test_graph_destroyed_before_its_store(cuda):
     g.close()
     assert st.size() == 100 and st.total_member_count() > 0
     st.close()
+
+
+def _sets(g, model, seed, count):
+    st = P.RRRStore(g)
+    P.generate_batch(g, model, seed, count, st)
+    off, mem = st.export()
+    return off, mem, st.counter()
+
+
+@pytest.mark.parametrize("name,model", [("cfg2", 1), ("cfg1", 0)])
+def test_graph_created_with_a_model_hint_samples_the_same_sets(cuda, oracle, name, model):
+    """rrg_graph_create_for: the LT layouts are built while the sources upload;
+    the sets are the plain graph's (and the reference's)."""
+    arrays = small(name, 1 << 12, 1 << 16)
+    plain = _sets(P.Graph(*arrays), model, 7, 3000)
+    hinted = _sets(P.Graph(*arrays, model=model), model, 7, 3000)
+    for a, b in zip(plain, hinted):
+        assert np.array_equal(a, b)
+    ref = oracle.graph(*arrays).sample(model, 7, 0, 3000)
+    assert np.array_equal(plain[2], ref.counter)
+    # the other model on a hinted graph still works (the hint is only a hint)
+    other = 1 - model
+    a = _sets(P.Graph(*arrays), other, 3, 500)
+    b = _sets(P.Graph(*arrays, model=model), other, 3, 500)
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+def test_model_hint_keeps_the_upload_checks(cuda):
+    off, src, w = small("cfg2", 1 << 10, 1 << 13)
+    bad_off = off.copy()
+    bad_off[5] = bad_off[-1] + 7  # beyond m: the CDF kernels must never see it
+    with pytest.raises(ValueError):
+        P.Graph(bad_off, src, w, model=1)
+    bad_src = src.copy()
+    bad_src[11] = off.size + 3
+    with pytest.raises(ValueError):
+        P.Graph(off, bad_src, w, model=1)
+    with pytest.raises(ValueError):
+        P.Graph(off, src, w, model=7)
+
+
+def test_light_guide_table_then_full_table(cuda, oracle):
+    """Small LT batches on an unprepared graph walk the light guide table (one
+    bucket per in-edge); many of them, or one large batch, replace it with the
+    full table. Every batch is the reference's."""
+    arrays = small("cfg2", 1 << 12, 1 << 16)
+    og = oracle.graph(*arrays)
+    g = P.Graph(*arrays, model=1)
+    st = P.RRRStore(g)
+    done = 0
+    for count in (2000, 3000, 1 << 17, 1000):  # light, light, full (large batch), full
+        P.generate_batch(g, 1, 9, count, st)
+        done += count
+    off, mem = st.export()
+    ref = og.sample(1, 9, 0, done)
+    assert np.array_equal(np.diff(off.astype(np.int64)), np.diff(ref.offsets.astype(np.int64)))
+    assert np.array_equal(st.counter(), ref.counter)
+    for i in list(range(0, 5000, 97)) + list(range(done - 1000, done, 53)):
+        assert np.array_equal(np.sort(mem[off[i]:off[i + 1]]),
+                              ref.members[ref.offsets[i]:ref.offsets[i + 1]]), i
