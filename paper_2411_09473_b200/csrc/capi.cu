@@ -470,6 +470,7 @@ rrg_status rrg_graph_create_for(uint32_t n, uint64_t m, const uint64_t* roff, co
     g->stream = side;
     try {
       prepare_lt(g);  // ends with a host sync of the side stream
+      if (g->cdf_monotone) prepare_lt_lite(g);  // CDF only: also before the sources land
     } catch (...) {
       g->stream = main_stream;
       cudaStreamSynchronize(main_stream);
@@ -613,7 +614,10 @@ rrg_status rrg_graph_prepare(rrg_graph* g, rrg_model model) {
   if (model != RRG_IC && model != RRG_LT) return invalid("unknown diffusion model");
   return guarded([&]() -> rrg_status {
     if (model == RRG_IC) prepare_ic(g);
-    else prepare_lt_mode(g, 0);
+    else {
+      bool lite = false;
+      prepare_lt_mode(g, 0, &lite);
+    }
     return RRG_OK;
   });
 }
@@ -838,8 +842,9 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
   if (count == 0) return RRG_OK;
   return guarded([&]() -> rrg_status {
     int lt_mode = kLtLinear;
+    bool lt_lite = false;
     if (model == RRG_IC) prepare_ic(g);
-    else lt_mode = prepare_lt_mode(g, count);
+    else lt_mode = prepare_lt_mode(g, count, &lt_lite);
     const bool ic_fast = model == RRG_IC && g->ic_rng == 1;
     if (model == RRG_IC) prepare_ic_fast(g);  // uniform-weight flags (fast mode, list expansion)
     if (!fused) s->counter_complete = false;
@@ -937,14 +942,15 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
       p.counter = fused ? s->counter.ptr : nullptr;
       p.ctl = g->ctl.ptr;
       p.lt_scan = lt_mode;
-      p.ltguide = g->ltguide.ptr;
-      p.lt_guide_mult = g->lt_guide_built;
+      p.ltguide = lt_lite ? nullptr : g->ltguide.ptr;
+      p.ltlite = lt_lite ? g->ltlite.ptr : nullptr;
+      p.lt_guide_mult = lt_lite ? lt_lite_mult() : g->lt_guide_built;
       p.coop_min = g->coop_min;
-      p.jtab = g->jtab.ptr;
-      p.jtab16 = g->jtab16.ptr;
-      p.jtab256 = g->jtab256.ptr;
-      p.jtabhi = g->jtabhi.ptr;
-      p.jtab64 = g->jtab64.ptr;
+      p.jtab = g->jtab;
+      p.jtab16 = g->jtab16;
+      p.jtab256 = g->jtab256;
+      p.jtabhi = g->jtabhi;
+      p.jtab64 = g->jtab64;
       p.lx = nullptr;
       p.lx_wmax = 0;
       if (model == RRG_IC && !ic_fast && g->max_indeg >= kListMin &&

@@ -135,16 +135,17 @@ struct rrg_graph {
   rrgpu::DevBuf<uint64_t> ltnodeoff;  // LT: first search-tree slot per vertex (u64[n+1])
   rrgpu::DevBuf<uint32_t> ltnodes;    // LT: search-tree nodes, 32 floats (31 pivots) each
   rrgpu::DevBuf<uint4> ltguide;  // LT: guide table, 32 bytes per bucket (common.cuh), lazy
+  rrgpu::DevBuf<uint2> ltlite;   // LT: lite guide table, 8 bytes per bucket (small batches before the full table)
   uint32_t lt_guide_mult = 4;    // LT: guide buckets per in-edge (4: 0.74 vs 0.85 ms at 2, cfg4 65K walks)
   uint32_t lt_guide_built = 0;   // multiplier the current table was built with (0: none)
-  uint64_t lt_light_walks = 0;   // walks sampled on the light (one bucket per in-edge) table
+  uint64_t lt_light_walks = 0;   // walks sampled on the lite guide table so far
   bool lt_guide_mult_explicit = false;  // set through RRG_OPT_LT_GUIDE_MULT: no light table
   bool lt_search_ready = false;  // LT: records + search trees built
-  rrgpu::DevBuf<uint64_t> jtab;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
-  rrgpu::DevBuf<uint64_t> jtab16;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
-  rrgpu::DevBuf<uint64_t> jtab256;  // IC: byte tables of T^(256 a), a = 1..15 (3.75 MB)
-  rrgpu::DevBuf<uint64_t> jtabhi;   // IC: byte tables of T^(16^k a), k = 3, 4, 5, a = 1..15 (11.25 MB)
-  rrgpu::DevBuf<uint64_t> jtab64;   // IC: byte tables of T^(kLxPer l), l = 1..31 (list expansion)
+  const uint64_t* jtab = nullptr;  // IC: byte tables of T^(32 l), l = 1..31 (7.75 MB)
+  const uint64_t* jtab16 = nullptr;  // IC: byte tables of T^(16 l), l = 1..31 (7.75 MB)
+  const uint64_t* jtab256 = nullptr;  // IC: byte tables of T^(256 a), a = 1..15 (3.75 MB)
+  const uint64_t* jtabhi = nullptr;   // IC: byte tables of T^(16^k a), k = 3, 4, 5, a = 1..15 (11.25 MB)
+  const uint64_t* jtab64 = nullptr;   // IC: byte tables of T^(kLxPer l), l = 1..31 (list expansion)
   uint32_t max_indeg = 0;           // IC: largest in-list (list-expansion scratch sizing)
   rrgpu::DevBuf<uint32_t> lx;       // IC: per-CTA list-expansion scratch (masks, counts)
   rrgpu::DevBuf<uint8_t> dupfree;  // IC: per-vertex strictly-increasing-sources flag
@@ -265,6 +266,7 @@ struct SampleParams {
   const uint4* ltrec;    // LT vertex records (search mode), 4 x uint4 per vertex
   const uint32_t* ltnodes;  // LT search-tree nodes (32 floats each)
   const uint4* ltguide;     // LT guide table (guide mode), 2 x uint4 per bucket
+  const uint2* ltlite;      // LT lite guide table (set INSTEAD of ltguide), 8 bytes per bucket
   uint32_t lt_guide_mult;   // LT guide buckets per in-edge
   uint64_t run_seed;
   uint64_t base_slot;
@@ -334,7 +336,11 @@ void prepare_lt(rrg_graph* g);  // fp64 CDF + monotone flag
 // prepare_lt + what the graph's LT scan mode needs; returns the mode to launch
 // (guide falls back to search when the table does not fit, both to linear
 // when the CDF is not monotone)
-int prepare_lt_mode(rrg_graph* g, uint64_t batch_sets);  // 0: explicit prepare
+// batch_sets 0: explicit prepare (full structures). *lite: launches use the lite
+// guide table (g->ltlite, kGuideLiteMult buckets per in-edge) instead of the full one.
+int prepare_lt_mode(rrg_graph* g, uint64_t batch_sets, bool* lite);
+bool prepare_lt_lite(rrg_graph* g);  // the lite guide table (needs the CDF only)
+uint32_t lt_lite_mult();
 // converts d_off64 into g->off and validates offsets/sources on the device;
 // returns a bit mask of violations (1 offsets, 2 sources), 0 if clean
 // which: 1 = offsets, 2 = sources (sample.cu)

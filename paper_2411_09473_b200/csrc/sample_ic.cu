@@ -3,6 +3,9 @@
 // the opt-in fast mode, and the IC K0 layouts (edge records, duplicate-free and
 // uniform-weight flags, GF(2) jump tables, largest in-degree). See sample.cu
 // for the execution model shared by all samplers.
+#include <map>
+#include <mutex>
+
 #include "sampler.cuh"
 
 namespace rrgpu {
@@ -2189,6 +2192,38 @@ void launch_fast(const SampleParams& p, int grid, bool bitmap, uint32_t* bitmaps
   count_launch();
 }
 
+// The GF(2) jump tables are constants of xoshiro256** (csrc/jump.cpp), ~39 MB:
+// built on the host and uploaded ONCE per device and process, shared by every
+// graph (they used to be re-uploaded from pageable memory by each graph's first
+// IC batch: ~4 ms of every IMM run from host arrays). Never freed.
+struct JumpTables {
+  DevBuf<uint64_t> t32, t16, t256, thi, t64;
+};
+const JumpTables& jump_tables(int device, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<int, JumpTables*> per_device;
+  std::lock_guard<std::mutex> lock(mu);
+  JumpTables*& jt = per_device[device];
+  if (jt) return *jt;
+  jt = new JumpTables;
+  auto up = [&](DevBuf<uint64_t>& d, const std::vector<uint64_t>& h) {
+    d.reserve_discard(h.size());
+    RRG_CUDA(cudaMemcpyAsync(d.ptr, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+  };
+  up(jt->t32, segment_tables(32, 31));
+  up(jt->t16, segment_tables(16, 31));
+  up(jt->t256, segment_tables(256, 15));
+  up(jt->t64, segment_tables(kLxPer, 31));  // list-expansion lanes
+  std::vector<uint64_t> hi;  // T^(4096 a), T^(65536 a), T^(2^20 a)
+  for (uint64_t seg : {4096ull, 65536ull, 1048576ull}) {
+    const std::vector<uint64_t> t = segment_tables(seg, 15);
+    hi.insert(hi.end(), t.begin(), t.end());
+  }
+  up(jt->thi, hi);
+  host_sync(st);  // pageable sources: the copies are done when this returns
+  return *jt;
+}
+
 void prepare_ic_fast(rrg_graph* g) {
   if (g->uniform_ready) return;
   g->uniformw.reserve_discard(g->n ? g->n : 1);
@@ -2217,24 +2252,6 @@ void prepare_ic(rrg_graph* g) {
     RRG_CUDA(cudaGetLastError());
     count_launch();
   }
-  static const std::vector<uint64_t> jt = segment_tables(32, 31);  // host, built once
-  static const std::vector<uint64_t> jt16 = segment_tables(16, 31);
-  static const std::vector<uint64_t> jt256 = segment_tables(256, 15);
-  static const std::vector<uint64_t> jt64 = segment_tables(kLxPer, 31);  // list-expansion lanes
-  g->jtab64.reserve_discard(jt64.size());
-  RRG_CUDA(cudaMemcpyAsync(g->jtab64.ptr, jt64.data(), jt64.size() * 8, cudaMemcpyHostToDevice,
-                           g->stream));
-  static const std::vector<uint64_t> jthi = [] {  // T^(4096 a), T^(65536 a), T^(2^20 a)
-    std::vector<uint64_t> v;
-    for (uint64_t seg : {4096ull, 65536ull, 1048576ull}) {
-      const std::vector<uint64_t> t = segment_tables(seg, 15);
-      v.insert(v.end(), t.begin(), t.end());
-    }
-    return v;
-  }();
-  g->jtabhi.reserve_discard(jthi.size());
-  RRG_CUDA(cudaMemcpyAsync(g->jtabhi.ptr, jthi.data(), jthi.size() * 8, cudaMemcpyHostToDevice,
-                           g->stream));
   {  // largest in-list: sizes the list-expansion scratch
     DevBuf<uint32_t> mx;
     mx.reserve_discard(1);
@@ -2247,16 +2264,12 @@ void prepare_ic(rrg_graph* g) {
     RRG_CUDA(cudaMemcpyAsync(&g->max_indeg, mx.ptr, 4, cudaMemcpyDeviceToHost, g->stream));
     host_sync((g->stream));
   }
-  g->jtab.reserve_discard(jt.size());
-  g->jtab16.reserve_discard(jt16.size());
-  g->jtab256.reserve_discard(jt256.size());
-  RRG_CUDA(cudaMemcpyAsync(g->jtab256.ptr, jt256.data(), jt256.size() * 8, cudaMemcpyHostToDevice,
-                           g->stream));
-  RRG_CUDA(cudaMemcpyAsync(g->jtab.ptr, jt.data(), jt.size() * 8, cudaMemcpyHostToDevice,
-                           g->stream));
-  RRG_CUDA(cudaMemcpyAsync(g->jtab16.ptr, jt16.data(), jt16.size() * 8, cudaMemcpyHostToDevice,
-                           g->stream));
-  host_sync((g->stream));
+  const JumpTables& jt = jump_tables(g->device, g->stream);
+  g->jtab = jt.t32.ptr;
+  g->jtab16 = jt.t16.ptr;
+  g->jtab256 = jt.t256.ptr;
+  g->jtabhi = jt.thi.ptr;
+  g->jtab64 = jt.t64.ptr;
   g->rec_ready = true;
 }
 

@@ -235,6 +235,10 @@ __global__ void __launch_bounds__(kBlock) k_sample_lt(const SampleParams p) {
 // Guide-mode LT step resolution (common.cuh, "LT guide table"): the bucket
 // entry (e0, e1) of vertex u for draw x gives the chosen index `pick` (local;
 // deg_u = none) and what the next step needs of the chosen source.
+// kLite: the entry is {A_g, pivot | flags (span in the pivot bits when kGuideSearch)}
+// only (ltlite, 8 bytes: built from the CDF alone, before the sources are on
+// the device); the chosen source and its offsets are three dependent loads.
+template <bool kLite>
 __device__ __forceinline__ void lt_guide_resolve(const SampleParams& p, const uint4 e0,
                                                  const uint4 e1, uint64_t x, uint32_t offu,
                                                  uint32_t degu, uint32_t& pick, uint32_t& v,
@@ -243,43 +247,48 @@ __device__ __forceinline__ void lt_guide_resolve(const SampleParams& p, const ui
   const uint32_t pw = e0.y;
   if (pw & kGuideSpan0) {  // no CDF entry inside the bucket: index A_g whatever the draw
     pick = A;
-    v = e0.z;
-    offv = e0.w;
-    degv = e1.x;
-    return;
-  }
-  const double d = __ull2double_rn(x >> 11) * 0x1.0p-53;  // uniform01(), exact
-  const uint32_t dbits = __float_as_uint(__double2float_rd(d));
-  if (!(pw & kGuideSearch)) {  // one entry: pick A_g + [cdf[A_g] <= d]
-    const uint32_t f = pw & kGuidePivot;
-    const bool le = f < dbits || (f == dbits && __ldg(p.cdf + offu + A) <= d);
-    if (le) {
-      pick = A + 1;
-      v = e1.y;
-      offv = e1.z;
-      degv = e1.w;
-    } else {
-      pick = A;
+    if (!kLite) {
       v = e0.z;
       offv = e0.w;
       degv = e1.x;
+      return;
     }
-    return;
-  }
-  // span >= 2 (rare): count cdf[A_g, A_g + span) <= d, eight loads in flight
-  const uint32_t span = e1.y;
-  const double* c = p.cdf + offu + A;
-  uint32_t cnt = 0;
-  for (uint32_t t = 0; t < span; t += 8) {
-    double q[8];
+  } else {
+    const double d = __ull2double_rn(x >> 11) * 0x1.0p-53;  // uniform01(), exact
+    const uint32_t dbits = __float_as_uint(__double2float_rd(d));
+    if (!(pw & kGuideSearch)) {  // one entry: pick A_g + [cdf[A_g] <= d]
+      const uint32_t f = pw & kGuidePivot;
+      const bool le = f < dbits || (f == dbits && __ldg(p.cdf + offu + A) <= d);
+      pick = le ? A + 1 : A;
+      if (!kLite) {
+        if (le) {
+          v = e1.y;
+          offv = e1.z;
+          degv = e1.w;
+        } else {
+          v = e0.z;
+          offv = e0.w;
+          degv = e1.x;
+        }
+        return;
+      }
+    } else {
+      // span >= 2 (rare): count cdf[A_g, A_g + span) <= d, eight loads in flight
+      const uint32_t span = kLite ? (pw & kGuidePivot) : e1.y;
+      const double* c = p.cdf + offu + A;
+      uint32_t cnt = 0;
+      for (uint32_t t = 0; t < span; t += 8) {
+        double q[8];
 #pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) q[k] = t + k < span ? __ldg(c + t + k) : 2.0;
+        for (uint32_t k = 0; k < 8; ++k) q[k] = t + k < span ? __ldg(c + t + k) : 2.0;
 #pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) cnt += q[k] <= d ? 1u : 0u;
-    if (cnt < t + 8) break;  // the entries are sorted: the first one > d ends the count
+        for (uint32_t k = 0; k < 8; ++k) cnt += q[k] <= d ? 1u : 0u;
+        if (cnt < t + 8) break;  // the entries are sorted: the first one > d ends the count
+      }
+      ent += span;
+      pick = A + cnt;
+    }
   }
-  ent += span;
-  pick = A + cnt;
   if (pick < degu) {
     v = __ldg(p.src + offu + pick);
     offv = __ldg(p.off + v);
@@ -305,11 +314,20 @@ __device__ __forceinline__ uint64_t lt_guide_policy() {
   return pol;
 }
 
+template <bool kLite>
 __device__ __forceinline__ void lt_guide_fetch(const SampleParams& p, uint32_t offu, uint32_t degu,
                                                uint64_t x, uint4& e0, uint4& e1, uint64_t pol) {
   if (!degu) return;
   const uint64_t G = static_cast<uint64_t>(degu) * p.lt_guide_mult;
   const uint64_t gi = static_cast<uint64_t>(offu) * p.lt_guide_mult + __umul64hi(x & ~0x7ffull, G);
+  if (kLite) {
+    const uint2 q = __ldg(p.ltlite + gi);
+    e0.x = q.x;
+    e0.y = q.y;
+    (void)e1;
+    (void)pol;
+    return;
+  }
   // one 256-bit load (sm_100: LDG.256), not allocated in L1: the entry is one
   // 32-byte sector and is never re-read by this SM
 #if RRG_GUIDE_EVICT_FIRST
@@ -421,7 +439,7 @@ __device__ __forceinline__ bool warp_emit_pending(const SampleParams& p, bool pe
 // while it is in flight, and the chosen source's visited test runs against the
 // shared-memory filter. Same index as the reference's linear scan
 // (sampling.hpp:127-137), same draws in the same order.
-template <int kFiltLog, uint32_t kLtFiltMax, int kMinBlocks>
+template <int kFiltLog, uint32_t kLtFiltMax, int kMinBlocks, bool kLite = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) k_sample_lt_guide(const SampleParams p) {
   constexpr uint32_t kLtFiltWords = 1u << kFiltLog;
   extern __shared__ uint32_t filt_all[];  // kLtFiltWords * kBlock words
@@ -514,7 +532,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_sample_lt_guide(const Sa
       offu = __ldg(p.off + u);
       degu = __ldg(p.off + u + 1) - offu;
       x = rng.next();  // the first step's draw (sampling.hpp:127)
-      lt_guide_fetch(p, offu, degu, x, e0, e1, gpol);
+      lt_guide_fetch<kLite>(p, offu, degu, x, e0, e1, gpol);
       xn = rng.next();
 #pragma unroll
       for (uint32_t w = 0; w < kLtFiltWords; ++w) filt[w * kBlock] = 0u;
@@ -533,13 +551,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_sample_lt_guide(const Sa
 
     uint32_t pick = degu, v = kGuideNone, offv = 0, degv = 0;
     if (degu) {
-      lt_guide_resolve(p, e0, e1, x, offu, degu, pick, v, offv, degv, ent);
-      ent += 4;  // the 32-byte bucket entry (in 8-byte units)
+      lt_guide_resolve<kLite>(p, e0, e1, x, offu, degu, pick, v, offv, degv, ent);
+      ent += kLite ? 3 : 4;  // the 32-byte bucket entry (in 8-byte units); lite: 8 + 3 x 4 bytes
     }
     sinsp += pick < degu ? pick + 1 : degu;  // reference trip count (sampling.hpp:130-136)
     bool stop = v == kGuideNone;
     if (!stop) {
-      lt_guide_fetch(p, offv, degv, xn, e0, e1, gpol);  // next step's entry, in flight now
+      lt_guide_fetch<kLite>(p, offv, degv, xn, e0, e1, gpol);  // next step's entry, in flight now
       x = xn;
       xn = rng.next();
       if (big) {
@@ -876,8 +894,12 @@ __device__ __forceinline__ void guide_cand(const uint32_t* off, const uint32_t* 
   }
 }
 
+// kLite: 8-byte entries {A_g, pivot | flags; the span in the pivot bits when
+// kGuideSearch} into `lite` -- no candidate infos, so neither the sources nor
+// their offsets are read: the table can be built while the sources upload.
+template <bool kLite>
 __global__ void k_build_ltguide(const uint32_t* off, const double* cdf, const uint32_t* src,
-                                uint32_t n, uint64_t m, uint32_t mult, uint4* guide) {
+                                uint32_t n, uint64_t m, uint32_t mult, uint4* guide, uint2* lite) {
   const uint64_t total = static_cast<uint64_t>(mult) * m;
   const uint64_t nchunks = (total + kGuideChunk - 1) / kGuideChunk;
   const uint64_t two53 = 1ull << 53;
@@ -940,6 +962,14 @@ __global__ void k_build_ltguide(const uint32_t* off, const double* cdf, const ui
       e0.x = A;
       e0.y = (A < deg ? lt_fdown(__ldg(cdf + b + A)) : 0u) |
              (span == 0 ? kGuideSpan0 : span >= 2 ? kGuideSearch : 0u);
+      if (kLite) {
+        if (span >= 2) e0.y = kGuideSearch | span;  // span <= deg < 2^30 (checked by the host)
+        lite[i] = make_uint2(e0.x, e0.y);
+        A = A1;
+        Q = Q1;
+        R = R1;
+        continue;
+      }
       // candidate infos, reused while consecutive buckets share A (about mult
       // buckets per CDF entry): the source's offsets are random L2 reads
       if (u != cu || A != cA) {
@@ -994,23 +1024,26 @@ int lt_filter_variant() {
   }();
   return v;
 }
-LtGuideFn lt_guide_kernel() {
+LtGuideFn lt_guide_kernel(bool lite) {
   static bool attr = false;
   if (!attr) {
     RRG_CUDA(cudaFuncSetAttribute(k_sample_lt_guide<6, 384, 3>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    RRG_CUDA(cudaFuncSetAttribute(k_sample_lt_guide<6, 384, 3, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr = true;
   }
+  if (lite) return k_sample_lt_guide<6, 384, 3, true>;
   return lt_filter_variant() ? k_sample_lt_guide<6, 384, 3> : k_sample_lt_guide<5, 128, 4>;
 }
-size_t lt_guide_smem() { return (lt_filter_variant() ? 64u : 32u) * kBlock * 4u; }
+size_t lt_guide_smem(bool lite) { return (lite || lt_filter_variant() ? 64u : 32u) * kBlock * 4u; }
 
 
 int lt_blocks_per_sm(int lt_mode) {
   int b = 0;
   if (lt_mode == kLtGuide)
-    RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, lt_guide_kernel(), kBlock,
-                                                           lt_guide_smem()));
+    RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, lt_guide_kernel(false), kBlock,
+                                                           lt_guide_smem(false)));
   else
     RRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_lt<16>, kBlock, 0));
   return b;
@@ -1018,7 +1051,8 @@ int lt_blocks_per_sm(int lt_mode) {
 
 void launch_lt_sampler(const SampleParams& p, int grid, cudaStream_t s) {
   if (p.lt_scan == kLtGuide) {
-    lt_guide_kernel()<<<grid, kBlock, lt_guide_smem(), s>>>(p);
+    const bool lite = p.ltlite != nullptr;  // the host passes exactly one of the two tables
+    lt_guide_kernel(lite)<<<grid, kBlock, lt_guide_smem(lite), s>>>(p);
   } else {
     switch (p.lt_kary) {
       case 2: k_sample_lt<2><<<grid, kBlock, 0, s>>>(p); break;
@@ -1095,50 +1129,77 @@ void prepare_lt_search(rrg_graph* g) {
   host_sync((g->stream));
 }
 
+// The lite guide table: 8 bytes per bucket, kGuideLiteMult buckets per in-edge,
+// built from the offsets and the CDF alone (no candidate infos). It serves the
+// small batches of a graph that has no full table yet: an IMM run from host
+// arrays samples a few thousand walks, for which the full table's build (cfg4:
+// 4.5 ms, 8.8 GB) costs more than it saves; with a model hint the lite table is
+// built while the sources are still uploading (rrg_graph_create_for).
+constexpr uint32_t kGuideLiteMult = 2;
+bool prepare_lt_lite(rrg_graph* g) {
+  if (!g->cdf_monotone || !g->m) return false;
+  if (g->ltlite.ptr) return true;
+  if (g->m >= (1ull << 30)) return false;  // a span (<= an in-degree) must fit the 30 pivot bits
+  const uint64_t entries = static_cast<uint64_t>(kGuideLiteMult) * g->m;
+  size_t freeb = 0, totalb = 0;
+  RRG_CUDA(cudaMemGetInfo(&freeb, &totalb));
+  if (entries * 8 + (2ull << 30) > freeb) return false;
+  g->ltlite.reserve_discard(entries);
+  const uint64_t chunks = (entries + kGuideChunk - 1) / kGuideChunk;
+  const uint64_t grid = std::min<uint64_t>((chunks + 127) / 128, 1u << 20);
+  k_build_ltguide<true><<<static_cast<unsigned>(grid), 128, 0, g->stream>>>(
+      g->off.ptr, g->cdf.ptr, nullptr, g->n, g->m, kGuideLiteMult, nullptr, g->ltlite.ptr);
+  RRG_CUDA(cudaGetLastError());
+  count_launch();
+  host_sync((g->stream));
+  return true;
+}
+
 // LT guide mode: 32 bytes per bucket, mult buckets per in-edge. False (and no
 // table) when the CDF is not monotone or the table would not fit in free HBM.
-// batch_sets (0: an explicit prepare) picks the multiplier of a table built on
-// demand: a batch below kGuideLightSets walks gets the light table (one bucket
-// per in-edge: a quarter of the build time and of the memory; more buckets hold
-// two or more CDF entries, which costs a small batch nothing measurable), and
-// the first large batch replaces it with the full one. A multiplier set through
-// RRG_OPT_LT_GUIDE_MULT is always used as given.
+// batch_sets (0: an explicit prepare) decides what a graph WITHOUT a full table
+// does: a batch below kGuideLightSets walks runs on the lite table (*lite =
+// true), and the first large batch -- or kGuideLightTotal walks of small ones
+// -- builds the full table and drops the lite one. A multiplier set through
+// RRG_OPT_LT_GUIDE_MULT always means the full table.
 constexpr uint64_t kGuideLightSets = 1ull << 17;
 constexpr uint64_t kGuideLightTotal = 1ull << 19;
-bool prepare_lt_guide(rrg_graph* g, uint64_t batch_sets) {
+bool prepare_lt_guide(rrg_graph* g, uint64_t batch_sets, bool* lite) {
+  *lite = false;
   if (!g->cdf_monotone || !g->m) return false;
-  // ... and so do many small ones (kGuideLightTotal walks on the light table)
-  bool light_ok = !g->lt_guide_mult_explicit && batch_sets && batch_sets < kGuideLightSets;
-  if (light_ok && g->lt_guide_built != g->lt_guide_mult) {
+  if (g->lt_guide_built == g->lt_guide_mult && g->ltguide.ptr) return true;
+  if (!g->lt_guide_mult_explicit && batch_sets && batch_sets < kGuideLightSets &&
+      g->lt_light_walks + batch_sets <= kGuideLightTotal && prepare_lt_lite(g)) {
     g->lt_light_walks += batch_sets;
-    light_ok = g->lt_light_walks <= kGuideLightTotal;
-  }
-  if (g->ltguide.ptr && g->lt_guide_built &&
-      (g->lt_guide_built == g->lt_guide_mult || light_ok))
+    *lite = true;
     return true;
-  const uint32_t mult = light_ok ? 1u : g->lt_guide_mult;
+  }
+  g->ltlite.release();
   g->ltguide.release();
   g->lt_guide_built = 0;
-  const uint64_t entries = static_cast<uint64_t>(mult) * g->m;
+  const uint64_t entries = static_cast<uint64_t>(g->lt_guide_mult) * g->m;
   size_t freeb = 0, totalb = 0;
   RRG_CUDA(cudaMemGetInfo(&freeb, &totalb));
   if (entries * 32 + (2ull << 30) > freeb) return false;
   g->ltguide.reserve_discard(2 * entries);
   const uint64_t chunks = (entries + kGuideChunk - 1) / kGuideChunk;
   const uint64_t grid = std::min<uint64_t>((chunks + 127) / 128, 1u << 20);
-  k_build_ltguide<<<static_cast<unsigned>(grid), 128, 0, g->stream>>>(
-      g->off.ptr, g->cdf.ptr, g->src.ptr, g->n, g->m, mult, g->ltguide.ptr);
+  k_build_ltguide<false><<<static_cast<unsigned>(grid), 128, 0, g->stream>>>(
+      g->off.ptr, g->cdf.ptr, g->src.ptr, g->n, g->m, g->lt_guide_mult, g->ltguide.ptr, nullptr);
   RRG_CUDA(cudaGetLastError());
   count_launch();
   host_sync((g->stream));
-  g->lt_guide_built = mult;
+  g->lt_guide_built = g->lt_guide_mult;
   return true;
 }
 
+uint32_t lt_lite_mult() { return kGuideLiteMult; }
+
 // The structures the graph's LT scan mode needs; returns the mode launches use.
-int prepare_lt_mode(rrg_graph* g, uint64_t batch_sets) {
+int prepare_lt_mode(rrg_graph* g, uint64_t batch_sets, bool* lite) {
+  *lite = false;
   prepare_lt(g);
-  if (g->lt_scan == kLtGuide && prepare_lt_guide(g, batch_sets)) return kLtGuide;
+  if (g->lt_scan == kLtGuide && prepare_lt_guide(g, batch_sets, lite)) return kLtGuide;
   if (g->lt_scan == kLtLinear || !g->cdf_monotone) return kLtLinear;
   prepare_lt_search(g);
   return kLtBsearch;

@@ -569,8 +569,10 @@ __global__ void __launch_bounds__(kClBlock, 1) k_select_cluster(const SelectPara
 // Measured (profiles/r2/sel_r2n.log, k = 50 over 8,192 sets): cfg2 (238K members)
 // 0.42 vs 0.57 ms, cfg1 (114K) 0.39 vs 0.50, cfg3 (75K) 0.65 vs 0.75; cfg4
 // (667K members, 2,367 tiles) 0.92 vs 0.65 -- 16 SMs re-scan a large store
-// slower than 148 -- so the cluster takes stores of up to 2^19 members.
-constexpr uint64_t kClMaxMembers = 1ull << 19;
+// slower than 148; cfg4's first IMM selection (6,331 sets, ~500K members) 0.80
+// vs ~0.50 ms -- the two cost lines cross near 390K members, so the cluster
+// takes stores of up to 3 x 2^17 members.
+constexpr uint64_t kClMaxMembers = 3ull << 17;
 
 bool select_cluster_eligible(const SelectParams& p) {
   if (p.nd || p.snap) return false;

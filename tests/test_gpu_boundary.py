@@ -132,16 +132,18 @@ def test_model_hint_keeps_the_upload_checks(cuda):
         P.Graph(off, src, w, model=7)
 
 
-def test_light_guide_table_then_full_table(cuda, oracle):
-    """Small LT batches on an unprepared graph walk the light guide table (one
-    bucket per in-edge); many of them, or one large batch, replace it with the
-    full table. Every batch is the reference's."""
+@pytest.mark.parametrize("hint", [None, 1])
+def test_lite_guide_table_then_full_table(cuda, oracle, hint):
+    """Small LT batches on an unprepared graph walk the lite guide table (8-byte
+    entries built from the CDF alone -- with a model hint, while the sources
+    upload); a large batch replaces it with the full table. Every batch is the
+    reference's."""
     arrays = small("cfg2", 1 << 12, 1 << 16)
     og = oracle.graph(*arrays)
-    g = P.Graph(*arrays, model=1)
+    g = P.Graph(*arrays, model=hint)
     st = P.RRRStore(g)
     done = 0
-    for count in (2000, 3000, 1 << 17, 1000):  # light, light, full (large batch), full
+    for count in (2000, 3000, 1 << 17, 1000):  # lite, lite, full (large batch), full
         P.generate_batch(g, 1, 9, count, st)
         done += count
     off, mem = st.export()
