@@ -395,9 +395,12 @@ __device__ __forceinline__ void ld_u64x4(const uint64_t* p, uint64_t& a, uint64_
                : "l"(p));
 }
 
+#ifndef RRG_JUMP_CALL
+#define RRG_JUMP_CALL 1
+#endif
 // Same product with byte tables (jump.cpp segment_tables): 32 independent
 // 32-byte loads (one LDG.256 each), 16 in flight at a time, then XORs.
-__device__ __forceinline__ void gf2_jump_tables(const uint64_t* __restrict__ T, uint64_t& a,
+__device__ __forceinline__ void gf2_jump_tables_inl(const uint64_t* __restrict__ T, uint64_t& a,
                                                 uint64_t& b, uint64_t& c, uint64_t& d) {
   const uint64_t in[4] = {a, b, c, d};
   uint64_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
@@ -422,6 +425,30 @@ __device__ __forceinline__ void gf2_jump_tables(const uint64_t* __restrict__ T, 
   b = o1;
   c = o2;
   d = o3;
+}
+
+// RRG_JUMP_CALL: the product as a real function call (one copy of its ~10 KB of
+// code per kernel instead of one per call site; the block schedule's code was
+// 282 KB, far past the instruction caches).
+struct JumpState {
+  uint64_t a, b, c, d;
+};
+static __device__ __noinline__ JumpState gf2_jump_call(const uint64_t* __restrict__ T, uint64_t a,
+                                                uint64_t b, uint64_t c, uint64_t d) {
+  gf2_jump_tables_inl(T, a, b, c, d);
+  return JumpState{a, b, c, d};
+}
+__device__ __forceinline__ void gf2_jump_tables(const uint64_t* __restrict__ T, uint64_t& a,
+                                                uint64_t& b, uint64_t& c, uint64_t& d) {
+#if RRG_JUMP_CALL
+  const JumpState r = gf2_jump_call(T, a, b, c, d);
+  a = r.a;
+  b = r.b;
+  c = r.c;
+  d = r.d;
+#else
+  gf2_jump_tables_inl(T, a, b, c, d);
+#endif
 }
 
 // 128-bit register filter in front of the table: a clear bit proves absence.

@@ -776,9 +776,20 @@ __device__ __forceinline__ void cfilt_add(uint32_t* sf, uint32_t v) {
 
 // Warp-cooperative jump: every lane holds the same state; lane i looks up byte
 // i of it in the byte tables (one 32-byte load) and the warp XOR-reduces.
-__device__ __forceinline__ void warp_jump(const uint64_t* __restrict__ T, Xoshiro& st) {
+#ifndef RRG_WARP_JUMP_CALL
+#define RRG_WARP_JUMP_CALL 1
+#endif
+#if RRG_WARP_JUMP_CALL
+// a real call: 22 inlined copies (40 shuffles each) were ~75 KB of the block
+// schedule's 282 KB of code
+#define RRG_WJ_INLINE __noinline__
+#else
+#define RRG_WJ_INLINE __forceinline__
+#endif
+__device__ RRG_WJ_INLINE Xoshiro warp_jump_fn(const uint64_t* __restrict__ T, uint64_t a, uint64_t b,
+                                              uint64_t c, uint64_t d) {
   const int lane = threadIdx.x & 31;
-  const uint64_t wv = lane < 8 ? st.a : lane < 16 ? st.b : lane < 24 ? st.c : st.d;
+  const uint64_t wv = lane < 8 ? a : lane < 16 ? b : lane < 24 ? c : d;
   const uint32_t byte = static_cast<uint32_t>(wv >> (8 * (lane & 7))) & 255u;
   const ulonglong2* e = reinterpret_cast<const ulonglong2*>(T + (static_cast<size_t>(lane) * 256 + byte) * 4);
   ulonglong2 x = __ldg(e), y = __ldg(e + 1);
@@ -788,7 +799,10 @@ __device__ __forceinline__ void warp_jump(const uint64_t* __restrict__ T, Xoshir
     y.x ^= __shfl_xor_sync(kFull, y.x, o);
     y.y ^= __shfl_xor_sync(kFull, y.y, o);
   }
-  st = Xoshiro{x.x, x.y, y.x, y.y};
+  return Xoshiro{x.x, x.y, y.x, y.y};
+}
+__device__ __forceinline__ void warp_jump(const uint64_t* __restrict__ T, Xoshiro& st) {
+  st = warp_jump_fn(T, st.a, st.b, st.c, st.d);
 }
 // T^P st for P < 4096, warp-uniform.
 __device__ __forceinline__ Xoshiro warp_advance(const SampleParams& p, Xoshiro st, uint32_t P) {
