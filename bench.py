@@ -416,18 +416,22 @@ def imm_block(P, name, orc, cores, reps=3):
         syncs, launches = P.host_sync_count() - s0, P.launch_count() - l0
     g.close()
     e2e = []
-    for _ in range(1 if name in SLOW_REFERENCE else 3):
+    # one untimed pass first (as for the resident figure): the library's caching
+    # allocator then holds blocks of this graph's sizes (the first graph of a new
+    # size pays cudaMalloc: 33 vs 14 ms at cfg4)
+    for it in range(1 if name in SLOW_REFERENCE else 4):
         t0 = time.perf_counter()
         ge = P.Graph(*host, model=cfg.model)  # upload overlaps the model's layouts
         re_ = P.run_imm(ge, icfg)
-        e2e.append(time.perf_counter() - t0)
+        if it or name in SLOW_REFERENCE:
+            e2e.append(time.perf_counter() - t0)
         ge.close()
     t_e2e = statistics.median(e2e)
     out = {"workload": workload_desc(cfg, n, arrays[1].size), "k": cfg.k,
            "epsilon": cfg.epsilon, "gpu_wall_s": statistics.median(walls),
            "gpu_wall_s_note": f"median of {reps} after one warm-up, graph resident",
-           "gpu_e2e_wall_s": t_e2e,
-           "gpu_e2e_note": "from pinned host arrays: upload + K0 + IMM, median of 3 (cfg3c: 1)",
+           "gpu_e2e_wall_s": t_e2e, "gpu_e2e_runs_s": e2e,
+           "gpu_e2e_note": "from pinned host arrays (graph created with the model hint): upload + K0 + IMM, median of 3 after one warm-up (cfg3c: 1 run)",
            "gpu_timings": r.timings, "theta": r.theta, "theta_prime": r.theta_prime,
            "sets_generated": r.sets_generated, "host_syncs_per_imm": syncs,
            "gpu_launches_per_imm": launches,
@@ -801,11 +805,15 @@ def run_ours(args, rank, world, local):
                 r = P.run_imm(g, icfg)
                 walls.append(time.perf_counter() - ti)
             gpu_imm = statistics.median(walls)
-            ti = time.perf_counter()  # end to end: upload + K0 + IMM + seeds back
-            ge = P.Graph(*host, model=model)  # upload overlaps the model's layouts
-            re = P.run_imm(ge, icfg)
-            ge.close()
-            gpu_imm_e2e = time.perf_counter() - ti
+            e2e_runs = []  # end to end: upload + K0 + IMM + seeds back
+            for it in range(4):  # one untimed pass (allocator), then the median of 3
+                ti = time.perf_counter()
+                ge = P.Graph(*host, model=model)  # upload overlaps the model's layouts
+                re = P.run_imm(ge, icfg)
+                ge.close()
+                if it:
+                    e2e_runs.append(time.perf_counter() - ti)
+            gpu_imm_e2e = statistics.median(e2e_runs)
             assert re.seeds.seeds == r.seeds.seeds
             ti = time.perf_counter()
             rr = og.imm(k=cfg.k, epsilon=cfg.epsilon, model=model, workers=cores)
@@ -813,7 +821,9 @@ def run_ours(args, rank, world, local):
             line["imm"] = {
                 "k": cfg.k, "epsilon": cfg.epsilon, "gpu_wall_s": gpu_imm,
                 "gpu_wall_s_note": "median of 3 after one warm-up, graph resident",
-                "gpu_e2e_wall_s": gpu_imm_e2e,
+                "gpu_e2e_wall_s": gpu_imm_e2e, "gpu_e2e_runs_s": e2e_runs,
+                "gpu_e2e_note": "from pinned host arrays (graph created with the model hint): "
+                                "upload + K0 + IMM, median of 3 after one warm-up",
                 "gpu_timings": r.timings, "cpu_reference_wall_s": cpu_imm, "cpu_cores": cores,
                 "theta": r.theta, "theta_prime": r.theta_prime,
                 "seeds_match": r.seeds.seeds == rr["seeds"],

@@ -208,7 +208,7 @@ constexpr int kVisLane = 0, kVisBitmap = 1, kVisSmem = 2;
 // the in-list per load per warp): the classification is one dependent round
 // trip per kClassifyBatch chunks
 #ifndef RRG_CLASSIFY_BATCH
-#define RRG_CLASSIFY_BATCH 8
+#define RRG_CLASSIFY_BATCH 2
 #endif
 constexpr int kClassifyBatch = RRG_CLASSIFY_BATCH;
 constexpr uint32_t kSmemFilterWords = 1024;  // 32K bits per warp
@@ -233,8 +233,11 @@ __device__ __noinline__ uint32_t win_edge(const uint32_t* lstart, const uint32_t
   return lstart[t] + (e - lpre[t]);
 }
 
+#ifndef RRG_COOP_INLINE
+#define RRG_COOP_INLINE
+#endif
 template <int kVis>
-__device__ bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uint32_t* mem,
+__device__ RRG_COOP_INLINE bool coop_expand(const SampleParams& p, uint32_t jb, uint32_t je, uint32_t* mem,
                             uint64_t* tab, uint32_t* vis, CoopState& s, CoopSmem& sm,
                             uint32_t memcap = kMemCap, uint32_t* sfilt = nullptr) {
   constexpr bool kBitmap = kVis == kVisBitmap;
