@@ -102,17 +102,36 @@ __global__ void k_normalize_lt(const uint32_t* off, uint32_t n, float* w, uint32
   }
 }
 
+// s = fl(a + b); err |= (a + b != s): Knuth's TwoSum, no ordering assumption.
+__device__ __forceinline__ double norm_add_checked(double a, double b, bool& err) {
+  const double s = __dadd_rn(a, b);
+  const double bb = __dadd_rn(s, -a);
+  const double e = __dadd_rn(__dadd_rn(a, -__dadd_rn(s, -bb)), __dadd_rn(b, -bb));
+  err |= e != 0.0;
+  return s;
+}
+
 // Sum over w[b, e) in list order of x (scale == 0) or of float(x * scale),
 // both widened to fp64; returns the sum in every lane. *neg is set when an
 // addend is negative (first pass only, like the reference's check).
+// The reference's running sum is a serial fp64 chain, but almost all of its adds
+// are exact (float addends, a sum of order 1), and exact adds are associative: a
+// chunk of 256 addends is scanned in parallel -- eight consecutive addends per
+// lane, a warp scan of the lane totals, the running sum added last -- with every
+// add checked by TwoSum. When all error terms are zero EVERY prefix of the chunk
+// came out exact, hence representable, hence what the serial chain holds at that
+// point (by induction from the running sum): the chunk's last prefix is the
+// chain's value. Checking only a reduction tree would not do -- a prefix can
+// need rounding while the total does not. A chunk with a nonzero error term is
+// added by lane 0 in list order (the plain chain).
 __device__ double warp_list_sum(const float* w, uint32_t b, uint32_t e, double scale,
                                 double* sm, bool* neg) {
   const uint32_t lane = threadIdx.x & 31;
   float r[kNormChunk / 32];
-  auto load = [&](uint32_t c) {
+  auto load = [&](uint32_t c) {  // lane l: addends [8 l, 8 l + 8) of the chunk
 #pragma unroll
     for (uint32_t k = 0; k < kNormChunk / 32; ++k) {
-      const uint32_t i = c + k * 32 + lane;
+      const uint32_t i = c + 8 * lane + k;
       r[k] = i < e ? w[i] : 0.0f;
     }
   };
@@ -120,29 +139,51 @@ __device__ double warp_list_sum(const float* w, uint32_t b, uint32_t e, double s
   bool anyneg = false;
   load(b);
   for (uint32_t c = b; c < e; c += kNormChunk) {
-    bool mine = false;
+    bool mine = false, err = false;
+    double x[kNormChunk / 32], run = 0.0;
 #pragma unroll
     for (uint32_t k = 0; k < kNormChunk / 32; ++k) {
       mine |= r[k] < 0.0f;
-      sm[k * 32 + lane] = scale == 0.0
+      x[k] = scale == 0.0
           ? static_cast<double>(r[k])
           : static_cast<double>(__double2float_rn(__dmul_rn(static_cast<double>(r[k]), scale)));
+      run = k == 0 ? x[0] : norm_add_checked(run, x[k], err);  // prefixes inside the lane
     }
     if (__any_sync(0xffffffffu, mine)) {
       anyneg = true;
       break;
     }
-    __syncwarp();
     if (c + kNormChunk < e) load(c + kNormChunk);
-    if (lane == 0) {
-      const uint32_t cnt = e - c < kNormChunk ? e - c : kNormChunk;
-#pragma unroll 8
-      for (uint32_t i = 0; i < cnt; ++i) sum = __dadd_rn(sum, sm[i]);
+    double incl = run;  // inclusive scan of the lane totals: the prefixes at lane ends
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= static_cast<uint32_t>(o)) incl = norm_add_checked(y, incl, err);
     }
-    __syncwarp();
+    double base = __shfl_up_sync(0xffffffffu, incl, 1);
+    base = lane == 0 ? sum : norm_add_checked(sum, base, err);
+    // every prefix of the chunk: running sum + lanes before + inside the lane
+    double pre = base;
+#pragma unroll
+    for (uint32_t k = 0; k < kNormChunk / 32; ++k) pre = norm_add_checked(pre, x[k], err);
+    // (pre re-adds the lane's addends onto base one by one: each step IS a prefix)
+    if (!__any_sync(0xffffffffu, err)) {
+      sum = __shfl_sync(0xffffffffu, pre, 31);
+    } else {  // some add rounded: the plain chain over this chunk
+#pragma unroll
+      for (uint32_t k = 0; k < kNormChunk / 32; ++k) sm[8 * lane + k] = x[k];
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t cnt = e - c < kNormChunk ? e - c : kNormChunk;
+#pragma unroll 8
+        for (uint32_t i = 0; i < cnt; ++i) sum = __dadd_rn(sum, sm[i]);
+      }
+      sum = __shfl_sync(0xffffffffu, sum, 0);
+      __syncwarp();
+    }
   }
   *neg = anyneg;
-  return __shfl_sync(0xffffffffu, sum, 0);
+  return sum;
 }
 
 __global__ void __launch_bounds__(kNormWarps * 32)

@@ -71,6 +71,38 @@ def test_device_normalize_hub_lists(cuda, oracle, whi):
     assert same_bits(g.reverse_weights, rw_n)
 
 
+def test_device_normalize_hub_lists_with_rounding_adds(cuda, oracle):
+    """Hub in-lists whose running sums ROUND (weights spanning 40 binades, tiny
+    weights among ordinary ones, sums far above 1 so the deflation loop runs):
+    the checked parallel scan of k_normalize_lt_hubs must fall back to the serial
+    chain exactly where the reference's adds are inexact."""
+    rng = np.random.default_rng(99)
+    n = 64
+    dsts, ws = [], []
+    for v in range(n):
+        deg = int(rng.integers(300, 6000))
+        kind = v % 4
+        if kind == 0:
+            w = rng.random(deg) * 2.0 ** rng.integers(-45, -5, deg)
+        elif kind == 1:
+            w = rng.random(deg) / deg * 3.0           # sums ~1.5: deflated
+            w[rng.integers(0, deg, 8)] = 1e-30
+        elif kind == 2:
+            w = rng.random(deg) * 5.0                 # sums in the thousands
+        else:
+            w = np.full(deg, 1.0 / deg) * (1 + 1e-3)  # equal weights just above 1
+        dsts.append(np.full(deg, v, np.uint32))
+        ws.append(w.astype(np.float32))
+    dst = np.concatenate(dsts)
+    w = np.concatenate(ws)
+    src = rng.integers(0, 1 << 20, dst.size).astype(np.uint32) % 100000 + n  # no self-loops
+    nn = 100000 + n
+    roff, rsrc, rw = oracle.build_graph(nn, src, dst, w)
+    rw_n = oracle.normalize_lt(roff, rw.copy())
+    g = P.Graph.from_edge_arrays(nn, src, dst, w, normalize_lt=True)
+    assert same_bits(g.reverse_weights, rw_n)
+
+
 def test_device_normalize_negative_on_hub(cuda):
     src, dst, w = edge_list(5, 100, 50000, hub=3000)
     w[np.flatnonzero(dst == 33)[-1]] = -0.25  # inside the hub list of vertex 33
