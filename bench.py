@@ -406,6 +406,7 @@ def imm_block(P, name, orc, cores, reps=3):
         reps = 1  # seconds per run
     icfg = P.ImmConfig(k=cfg.k, epsilon=cfg.epsilon, model=cfg.model)
     g = P.Graph(*arrays)
+    g.prepare(cfg.model)  # resident = uploaded and K0 done (LT: CDF + the full guide table)
     P.run_imm(g, icfg)
     walls = []
     for _ in range(reps):
@@ -739,8 +740,11 @@ def run_ours(args, rank, world, local):
                 "frac": rate / peak,
                 "note": "ncu DRAM bytes (read + write) per launch / sampler event time, "
                         "against the measured streaming HBM peak: the walk's accesses are "
-                        "random 32-B loads (~3 DRAM sectors each), so this is the share of "
-                        "HBM the random-access stream sustains"}
+                        "random 32-B loads, each an L2 miss that fetches a 128-B line (117 B "
+                        "of DRAM reads per gather whatever the load width, "
+                        "tools/gather/width_probe.cu), so this is the share of HBM the "
+                        "random-access stream sustains; the ceiling counts missing "
+                        "requests (~36.7 G/s), not bytes"}
     if small_block is not None:
         sb = small_block
         line["small_batch"] = {
