@@ -638,7 +638,9 @@ def run_ours(args, rank, world, local):
             barrier()
             t0 = time.perf_counter()
             if cold:
-                ge = P.Graph(*host)  # H2D of the transpose arrays from pinned memory
+                # H2D of the transpose arrays from pinned memory; with the model
+                # known, the weight-only layouts are built while the sources upload
+                ge = P.Graph(*host, model=model)
                 ge.set_option("lt_scan", SCAN[args.lt_scan])
                 se = P.RRRStore(ge)
             else:
