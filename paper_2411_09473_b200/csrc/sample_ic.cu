@@ -651,8 +651,22 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_warp(co
 // 16 b + c), and the accepted-source map is CTA-wide, so the conflict cut is
 // the reference's across warps. The visited filter is 256K bits.
 // ---------------------------------------------------------------------------
-constexpr int kCtaWarps = kBlock / 32;
-constexpr uint32_t kCtaWin = kCtaWarps * kWin;  // 4096 in-edges
+// Threads per block of this schedule: 256 (8 warps, 512 window positions each,
+// two blocks per SM) or 512 (16 warps, 256 positions each, one block per SM; the
+// block still owns the scratch of 256 lane regions). Measured (profiles/r2/
+// NOTES.md): 512 threads run ONE set 1.2-1.3x faster (cfg3's 35,624-member set
+// 10.1 -> 7.6 ms) but halve the sets in flight, and IMM-sized batches lose more
+// than their tail gains (cfg1 IMM 11.4 -> 13.7 ms, cfg3 19.6 -> 20.9 ms, cfg3c
+// 4.1 -> 5.2 s): 256 stays the default.
+#ifndef RRG_CTA_THREADS
+#define RRG_CTA_THREADS 256
+#endif
+constexpr int kCtaThreads = RRG_CTA_THREADS;
+constexpr int kCtaWarps = kCtaThreads / 32;
+constexpr uint32_t kCtaWin = 4096;                       // in-edges per window
+constexpr uint32_t kCtaSlice = kCtaWin / kCtaWarps;      // window positions per warp
+constexpr uint32_t kCtaSliceChunks = kCtaSlice / 32;
+static_assert(kCtaThreads == 256 || kCtaThreads == 512, "8 or 16 warps per block");
 constexpr int kCtaAmapLog = 11;                 // 2048 slots; a full map cuts the window
 #ifndef RRG_CTA_FILT_LOG
 #define RRG_CTA_FILT_LOG 18
@@ -665,15 +679,15 @@ constexpr int kLxCpl = RRG_LX_CPL;            // list expansion: 32-edge chunks 
 constexpr uint32_t kLxPer = 32u * kLxCpl;     // draws per lane per sub-window
 constexpr uint32_t kLxWords = 32u * kLxCpl;   // mask words (chunks) per sub-window
 struct CtaWarpFields {
-  uint32_t mask[kWinChunks];
-  uint32_t pre[kWinChunks];
-  uint32_t acc[kWinChunks];
+  uint32_t mask[kCtaSliceChunks];
+  uint32_t pre[kCtaSliceChunks];
+  uint32_t acc[kCtaSliceChunks];
   union {
     struct {
-      uint32_t thr[kWin];
-      uint32_t src[kWin];
+      uint32_t thr[kCtaSlice];
+      uint32_t src[kCtaSlice];
     };
-    uint32_t lxthr[2 * kWin];  // list expansion: the sub-window's thresholds (unequal weights)
+    uint32_t lxthr[kLxWin];  // list expansion: the sub-window's thresholds (unequal weights)
   };
   uint32_t lxmask[kLxWords], lxpre[kLxWords], lxacc[kLxWords];  // list expansion: per chunk
   unsigned long long st[4];  // list expansion: the warp's stream state after a sub-window
@@ -682,8 +696,8 @@ struct CtaSmem {
   CtaWarpFields w[kCtaWarps];
   unsigned long long amap[1u << kCtaAmapLog];
   uint32_t filt[kCtaFilterWords];
-  uint32_t lstart[kBlock];
-  uint32_t lpre[kBlock];
+  uint32_t lstart[kCtaThreads];
+  uint32_t lpre[kCtaThreads];
   unsigned long long st[4];
   unsigned long long next;
   uint32_t wsum[kCtaWarps];
@@ -756,7 +770,8 @@ __device__ __forceinline__ void warp_first_conflict(const unsigned long long* am
   }
 }
 constexpr size_t kCtaKernelDynSmem = sizeof(CtaSmem);
-static_assert(kCtaKernelDynSmem <= 97 * 1024, "two blocks per SM within the 196 KB carveout");
+static_assert(kCtaKernelDynSmem <= (kCtaThreads > 256 ? 200 : 97) * 1024,
+              "one 512-thread block, or two 256-thread blocks, per SM within the shared-memory carveout");
 constexpr uint32_t kMaxRepairs = 64;  // repairs per window before falling back to a cut
 #ifndef RRG_REPAIR_MIN
 #define RRG_REPAIR_MIN 1024
@@ -828,7 +843,7 @@ __device__ __forceinline__ Xoshiro warp_advance_far(const SampleParams& p, Xoshi
 // which is also returned. Thread t scans a contiguous run of the entries.
 __device__ __forceinline__ uint32_t block_exscan_global(uint32_t* x, uint32_t W, uint32_t* wsum) {
   const int tid = threadIdx.x, lane = tid & 31, wl = tid >> 5;
-  const uint32_t per = (W + kBlock - 1) / kBlock;
+  const uint32_t per = (W + kCtaThreads - 1) / kCtaThreads;
   const uint32_t lo = min(W, per * tid), hi = min(W, lo + per);
   uint32_t sum = 0;
   for (uint32_t i = lo; i < hi; ++i) sum += x[i];
@@ -840,7 +855,7 @@ __device__ __forceinline__ uint32_t block_exscan_global(uint32_t* x, uint32_t W,
   if (lane == 31) wsum[wl] = incl;
   __syncthreads();
   uint32_t base = 0, total = 0;
-  for (int w = 0; w < kBlock / 32; ++w) {
+  for (int w = 0; w < kCtaThreads / 32; ++w) {
     const uint32_t v = wsum[w];
     if (w < wl) base += v;
     total += v;
@@ -861,11 +876,11 @@ __device__ __forceinline__ uint32_t block_exscan_global(uint32_t* x, uint32_t W,
 // chunk, the grows one per member).
 __device__ __forceinline__ void cta_tab_insert(uint64_t* tab, uint32_t tag, uint32_t lg,
                                                const uint32_t* mem, uint32_t lo, uint32_t hi) {
-  for (uint32_t b = lo + threadIdx.x; b < hi; b += 4 * kBlock) {
+  for (uint32_t b = lo + threadIdx.x; b < hi; b += 4 * kCtaThreads) {
     uint32_t vs[4], pend = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint32_t i = b + q * kBlock;
+      const uint32_t i = b + q * kCtaThreads;
       vs[q] = i < hi ? mem[i] : 0u;
       pend |= (i < hi ? 1u : 0u) << q;
     }
@@ -916,7 +931,7 @@ __device__ __forceinline__ void cta_insert_range(uint64_t* tab, uint32_t* gbits,
     cta_tab_insert(tab, tag, lg, mem, lo, hi);
     return;
   }
-  for (uint32_t i = lo + threadIdx.x; i < hi; i += kBlock) {
+  for (uint32_t i = lo + threadIdx.x; i < hi; i += kCtaThreads) {
     const uint32_t v = mem[i];
     atomicOr(gbits + (v >> 5), 1u << (v & 31));
   }
@@ -939,7 +954,8 @@ __device__ __forceinline__ void cta_filter_add(uint32_t* sf, uint32_t v) {
 // members is written straight into a row of the dense arm (rrr_set.hpp:82-83).
 // Sets past kGiantCap go on to the big-set path.
 template <bool kGiant>
-__global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(const SampleParams p) {
+__global__ void __launch_bounds__(kCtaThreads, kCtaThreads > 256 ? 1 : RRG_IC_MIN_BLOCKS)
+    k_sample_ic_cta(const SampleParams p) {
   constexpr uint32_t kCap = kGiant ? kGiantCap : kBlock * kMemCap;
   extern __shared__ __align__(16) unsigned char k_dsm[];
   CtaSmem& cs = *reinterpret_cast<CtaSmem*>(k_dsm);
@@ -958,13 +974,13 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
   // out of shared memory so two blocks still leave L1 its share)
   uint32_t* xhi = p.xhi + static_cast<size_t>(blockIdx.x) * kCtaWin;
   uint32_t* sf = cs.filt;
-  for (uint32_t t = tid; t < kCtaFilterWords; t += kBlock) sf[t] = 0;
+  for (uint32_t t = tid; t < kCtaFilterWords; t += kCtaThreads) sf[t] = 0;
   // same 256-lane regions and tag range as the 256-lane warp layout; the giant
   // tables are private to the block and count their own tags
   const uint64_t tslot = region / 32;
   uint32_t tag = kGiant ? p.gtags[blockIdx.x] : 0xC0000000u | (p.wtags[tslot] & 0x3fffffffu);
   uint64_t insp = 0;
-  const uint32_t wbase = kWin * wl;  // this warp's first window position
+  const uint32_t wbase = kCtaSlice * wl;  // this warp's first window position
 #ifdef RRG_CTA_PHASES
   long long ph_[16] = {0}, ph_t_ = clock64();
 #endif
@@ -1005,7 +1021,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
         const uint32_t L = fe - qj;
         const bool uni = p.uniformw != nullptr && p.uniformw[fv];  // one threshold (WC)
         if (L >= kListMin && L < (1u << 24) && p.dupfree[fv] &&
-            (uni || kLxWin <= 2 * kWin)) {  // uniform across the block
+            (uni || kLxWin <= sizeof(ws.lxthr) / 4)) {  // uniform across the block
           const uint32_t W = (L + kLxWin - 1) / kLxWin;
           uint32_t* xm = p.lx + static_cast<size_t>(blockIdx.x) * (p.lx_wmax * (2ull * kLxWords + 2) + 2);
           uint32_t* xa = xm + static_cast<uint64_t>(kLxWords) * p.lx_wmax;
@@ -1231,7 +1247,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
         const uint32_t fe = p.off[fv + 1];
         if (fe - qj >= kCtaFastMin && p.dupfree[fv]) {  // uniform across the block
           const uint32_t E = min(fe - qj, kCtaWin);
-          const uint32_t wend = wbase < E ? min(kWin, E - wbase) : 0u;
+          const uint32_t wend = wbase < E ? min(kCtaSlice, E - wbase) : 0u;
           const uint32_t nch = (wend + 31) >> 5;
           uint32_t mymask = 0;
           for (uint32_t c0 = 0; c0 < nch; c0 += kClassifyBatch) {
@@ -1270,7 +1286,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             if (lane >= o) ui += y;
           }
           const uint32_t Uw = __shfl_sync(kFull, ui, 31);
-          if (lane < static_cast<int>(kWinChunks)) {
+          if (lane < static_cast<int>(kCtaSliceChunks)) {
             ws.mask[lane] = mymask;
             ws.pre[lane] = ui - cnt;
             ws.acc[lane] = 0;
@@ -1291,7 +1307,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               if (lane) gf2_jump_tables(p.jtab16 + static_cast<size_t>(lane - 1) * kJumpTableWords,
                                         st.a, st.b, st.c, st.d);
               uint32_t c = 0;
-              for (uint32_t step = 8; step; step >>= 1)
+              for (uint32_t step = kCtaSliceChunks / 2; step; step >>= 1)
                 if (c + step < nch && ws.pre[c + step] <= r0) c += step;
               uint32_t m = ws.mask[c];
               for (uint32_t k2 = r0 - ws.pre[c]; k2; --k2) m &= m - 1;
@@ -1392,7 +1408,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
         if (lane >= o) incl += y;
       }
       if (lane == 31) cs.wsum[wl] = incl;
-      for (uint32_t t = tid; t < (1u << kCtaAmapLog); t += kBlock) cs.amap[t] = ~0ull;
+      for (uint32_t t = tid; t < (1u << kCtaAmapLog); t += kCtaThreads) cs.amap[t] = ~0ull;
       __syncthreads();
       if (tid == 0) {  // after the barrier: every thread has read the previous window's
         cs.cut = 0xffffffffu;
@@ -1413,12 +1429,12 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       uint32_t ecur = min(kCtaWin, total);
       // ---- 1. warp wl classifies positions [wbase, wbase + 512) (status at window start)
       uint32_t mymask = 0;
-      const uint32_t wend = wbase < ecur ? min(kWin, ecur - wbase) : 0u;
+      const uint32_t wend = wbase < ecur ? min(kCtaSlice, ecur - wbase) : 0u;
       // lists holding this warp's first and last position (warp-uniform); the
       // per-edge search then only spans [tlo, thi] -- usually one list
       uint32_t tlo = 0, thi = 0;
       if (wend) {
-        for (uint32_t step = kBlock / 2; step; step >>= 1) {
+        for (uint32_t step = kCtaThreads / 2; step; step >>= 1) {
           if (cs.lpre[tlo + step] <= wbase) tlo += step;
           if (cs.lpre[thi + step] <= wbase + wend - 1) thi += step;
         }
@@ -1468,7 +1484,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
         if (lane >= o) ui += y;
       }
       const uint32_t Uw = __shfl_sync(kFull, ui, 31);
-      if (lane < static_cast<int>(kWinChunks)) {
+      if (lane < static_cast<int>(kCtaSliceChunks)) {
         ws.mask[lane] = mymask;
         ws.pre[lane] = ui - cnt;
         ws.acc[lane] = 0;
@@ -1495,7 +1511,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
             if (lane) gf2_jump_tables(p.jtab16 + static_cast<size_t>(lane - 1) * kJumpTableWords,
                                       st.a, st.b, st.c, st.d);
             uint32_t c = 0;
-            for (uint32_t step = 8; step; step >>= 1)
+            for (uint32_t step = kCtaSliceChunks / 2; step; step >>= 1)
               if (c + step < nch && ws.pre[c + step] <= r0) c += step;
             uint32_t m = ws.mask[c];
             for (uint32_t k2 = r0 - ws.pre[c]; k2; --k2) m &= m - 1;
@@ -1513,7 +1529,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               const uint64_t x = st.next();
               const uint32_t kh = static_cast<uint32_t>(x >> 32), th = ws.thr[32 * c + bit];
               if (kh < th ||
-                  (kh == th && bern_tie(x, p.w, win_edge(cs.lstart, cs.lpre, kBlock, wbase + 32 * c + bit))))
+                  (kh == th && bern_tie(x, p.w, win_edge(cs.lstart, cs.lpre, kCtaThreads, wbase + 32 * c + bit))))
                 acc |= 1u << bit;
               xhi[Pw + r0 + done] = kh;
               ++done;
@@ -1589,7 +1605,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
               const uint32_t y = __shfl_up_sync(kFull, ui2, o);
               if (lane >= o) ui2 += y;
             }
-            if (lane < static_cast<int>(kWinChunks)) ws.pre[lane] = ui2 - cnt2;
+            if (lane < static_cast<int>(kCtaSliceChunks)) ws.pre[lane] = ui2 - cnt2;
             if (lane == 31) cs.wU[wl] = ui2;
             __syncthreads();
             Pw = 0;
@@ -1657,7 +1673,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
           }
           if (cpos < ecur) {
             cut = true;
-            const uint32_t cw = cpos / kWin, cl = cpos % kWin, cc = cl >> 5, cb = cl & 31;
+            const uint32_t cw = cpos / kCtaSlice, cl = cpos % kCtaSlice, cc = cl >> 5, cb = cl & 31;
             if (wl == static_cast<int>(cw)) {
               // the stream resumes after the draws of the edges before the cut
               const uint32_t Rl = ws.pre[cc] + __popc(ws.mask[cc] & ((1u << cb) - 1u));
@@ -1740,7 +1756,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
         qi = cs.adv_qi;
         qj = cs.adv_qj;
       } else {
-        qi += min(static_cast<uint32_t>(kBlock), nq - qi);
+        qi += min(static_cast<uint32_t>(kCtaThreads), nq - qi);
         if (qi < nmem) qj = p.off[mem[qi]];
       }
     }
@@ -1749,12 +1765,12 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
     // inspected in-edges of the set = sum of its members' in-degrees
     uint64_t sinsp = 0;
     if (ok)
-      for (uint32_t t = tid; t < nmem; t += kBlock) sinsp += p.off[mem[t] + 1] - p.off[mem[t]];
+      for (uint32_t t = tid; t < nmem; t += kCtaThreads) sinsp += p.off[mem[t] + 1] - p.off[mem[t]];
     tag = stag;
-    for (uint32_t t = tid; t < kCtaFilterWords; t += kBlock) sf[t] = 0;  // filter per sample
+    for (uint32_t t = tid; t < kCtaFilterWords; t += kCtaThreads) sf[t] = 0;  // filter per sample
     if (kGiant) {  // the block's n-bit map back to zero: exactly mem[0, nmem) is set
       __syncthreads();
-      for (uint32_t t = tid; t < nmem; t += kBlock) gbits[mem[t] >> 5] = 0u;
+      for (uint32_t t = tid; t < nmem; t += kCtaThreads) gbits[mem[t] >> 5] = 0u;
     }
     if (!ok) {
       if (tid == 0) defer_slot(p, idx);
@@ -1771,9 +1787,9 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       }
       const uint64_t grow = p.drow_base + row;
       uint32_t* dst = p.dbits + grow * p.dwords;
-      for (uint32_t t = tid; t < p.dwords; t += kBlock) dst[t] = 0u;
+      for (uint32_t t = tid; t < p.dwords; t += kCtaThreads) dst[t] = 0u;
       __syncthreads();
-      for (uint32_t t = tid; t < nmem; t += kBlock) {
+      for (uint32_t t = tid; t < nmem; t += kCtaThreads) {
         const uint32_t v = mem[t];
         RRG_DCHECK(v < p.n, 7);
         atomicOr(dst + (v >> 5), 1u << (v & 31));
@@ -1799,7 +1815,7 @@ __global__ void __launch_bounds__(kBlock, RRG_IC_MIN_BLOCKS) k_sample_ic_cta(con
       if (tid == 0) restage_slot(p, idx, nmem);
       continue;
     }
-    for (uint32_t t = tid; t < nmem; t += kBlock) {
+    for (uint32_t t = tid; t < nmem; t += kCtaThreads) {
       const uint32_t v = mem[t];
       RRG_DCHECK(v < p.n && nmem <= kCap, 6);
       p.stage[pos + t] = v;
@@ -2181,8 +2197,8 @@ void launch_ic_sampler(const SampleParams& p, int grid, uint32_t ic_inner, int s
     }
     if (schedule == kSchedWarp) k_sample_ic_warp<32><<<grid, kBlock, kWarpKernelDynSmem, s>>>(p);
     else if (schedule == kSchedCtaGiant)
-      k_sample_ic_cta<true><<<grid, kBlock, kCtaKernelDynSmem, s>>>(p);
-    else k_sample_ic_cta<false><<<grid, kBlock, kCtaKernelDynSmem, s>>>(p);
+      k_sample_ic_cta<true><<<grid, kCtaThreads, kCtaKernelDynSmem, s>>>(p);
+    else k_sample_ic_cta<false><<<grid, kCtaThreads, kCtaKernelDynSmem, s>>>(p);
   } else {
     k_sample_ic<<<grid, kBlock, 0, s>>>(p, ic_inner);
   }
