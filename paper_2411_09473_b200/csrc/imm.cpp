@@ -223,12 +223,14 @@ class Driver {
       const char* e = std::getenv("RRGPU_IMM_FREE_EDGES");  // tuning
       return e ? std::atof(e) : RRG_IMM_FREE_EDGES;
     }();
-    // off by default: measured cfg1 11.4 -> 10.0 ms (the final batch disappears)
-    // but cfg3 19.7 -> 24.3 ms (30 % more slots, one more giant set in the tail,
-    // and that run needs no final top-up): profiles/r2/NOTES.md
+    // The final top-up's slots are added only when they are few (kFinalMaxSets):
+    // measured cfg1 11.4 -> 10.0 ms (5,268 extra slots, the final batch disappears)
+    // but cfg3 19.7 -> 24.3 ms with 27,966 extra slots (one more giant set in the
+    // tail, for a top-up that run never needs): profiles/r2/NOTES.md
+    constexpr uint64_t kFinalMaxSets = 1ull << 13;
     static const bool kFinal = [] {
-      const char* e = std::getenv("RRGPU_IMM_SPEC_FINAL");  // tuning
-      return e && *e == '1';
+      const char* e = std::getenv("RRGPU_IMM_SPEC_FINAL");  // tuning: 0 off
+      return !e || *e != '0';
     }();
     const double mean = cfg_->model == RRG_IC ? rrgpu::graph_ic_mean_inspected(g_) : -1.0;
     auto free_to = [&](uint64_t from, uint64_t to) {
@@ -252,7 +254,8 @@ class Driver {
       const unsigned j = std::max(jlast, i);
       const uint64_t have = std::max(best, theta_for_round(n_, cfg_->k, cfg_->epsilon, ell_, i));
       const uint64_t fj = set_theta(n_, cfg_->k, cfg_->epsilon, ell_, round_target(n_, j));
-      if (fj > have && fj - size_ <= kAheadMax && free_to(have, fj)) best = fj;
+      if (fj > have && fj - have <= kFinalMaxSets && fj - size_ <= kAheadMax && free_to(have, fj))
+        best = fj;
     }
     return best;
   }
