@@ -124,3 +124,40 @@ def test_unknown_strategy_rejected(cuda):
         P.run_imm(g, P.ImmConfig(k=1, strategy=7))
     with pytest.raises(ValueError):
         P.parse_strategy("nope")
+
+
+_SPEC_CHILD = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import paper_2411_09473_b200 as P
+from paper_2411_09473_b200 import graphs
+out = {}
+for name, n, m, k in (("cfg1", 1 << 12, 1 << 16, 20), ("cfg3", 30000, 500000, 10)):
+    cfg = graphs.scaled(graphs.CONFIGS[name], n, m)
+    g = P.Graph(*graphs.generate(cfg))
+    icfg = P.ImmConfig(k=k, epsilon=0.5, model=cfg.model, rng_seed=1)
+    P.run_imm(g, icfg)       # the first run measures the graph's mean inspected edges,
+    r = P.run_imm(g, icfg)   # the second one speculates with it
+    out[name] = [r.seeds.seeds, r.seeds.marginal_counts, r.theta, r.theta_prime,
+                 r.lower_bound, r.sets_generated, r.max_set_size, r.mean_set_size]
+print(json.dumps(out))
+"""
+
+
+def test_speculation_settings_never_change_the_result(cuda):
+    """The driver samples later rounds' (and the final top-up's) slots ahead when
+    they look cheap; the main store only ever receives the reference's slots, so
+    every setting of the two tuning variables must give the same ImmResult."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    results = []
+    for free, final in (("0", "0"), ("1e15", "1"), ("67108864", "1"), ("1e15", "0")):
+        env = dict(os.environ, RRGPU_IMM_FREE_EDGES=free, RRGPU_IMM_SPEC_FINAL=final)
+        p = subprocess.run([sys.executable, "-c", _SPEC_CHILD, root], env=env, check=True,
+                           capture_output=True, text=True, timeout=300)
+        results.append(json.loads(p.stdout.strip().splitlines()[-1]))
+    for r in results[1:]:
+        assert r == results[0]
