@@ -1051,11 +1051,12 @@ rrg_status rrg_generate_slots(rrg_graph* g, rrg_model model, uint64_t run_seed,
         sample_ms += ms;
         if (debug_enabled())
           std::fprintf(stderr, "[rrgpu] launch kind=%d model=%d items=%llu ms=%.3f deferred=%u "
-                               "restage=%u cursor=%llu cap=%zu windows=%llu cuts=%llu repairs=%llu\n",
+                               "restage=%u cursor=%llu cap=%zu windows=%llu cuts=%llu repairs=%llu "
+                               "blocks/SM=%d\n",
                        static_cast<int>(kind), static_cast<int>(model),
                        static_cast<unsigned long long>(n_items), ms, ctl.ndeferred, ctl.nrestage,
                        static_cast<unsigned long long>(ctl.cursor), s->stage.cap, ctl.windows,
-                       ctl.cuts, ctl.repairs);
+                       ctl.cuts, ctl.repairs, per_sm);
       };
       auto grow_staging = [&]() {
         const uint64_t ncap = std::max<uint64_t>(
