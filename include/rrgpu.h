@@ -53,7 +53,9 @@ rrg_status rrg_graph_prepare(rrg_graph* g, rrg_model model);
  * (RRG_IC, RRG_LT, or -1 = unknown: exactly rrg_graph_create). With RRG_LT the
  * weight-only LT layouts (the exact sequential fp64 CDF, sampling.hpp:130-136)
  * are built on the device while the sources are still being uploaded; results
- * are identical, only the time from host arrays to the first batch changes. */
+ * are identical, only the time from host arrays to the first batch changes (and
+ * the LT layouts -- 8 B per in-edge of CDF, 16 B of lite guide table -- are
+ * resident from creation on, also if the graph is then only sampled under IC). */
 rrg_status rrg_graph_create_for(uint32_t n, uint64_t m, const uint64_t* rev_offsets,
                                 const uint32_t* rev_sources, const float* rev_weights,
                                 int model_hint, rrg_graph** out);
