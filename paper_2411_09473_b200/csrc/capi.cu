@@ -1188,10 +1188,45 @@ rrg_status rrg_last_batch_stats(const rrg_graph* g, rrg_batch_stats* out) {
   return RRG_OK;
 }
 
+}  // extern "C"
+
+namespace {
+rrg_status select_seeds_impl(rrg_store* s, uint32_t k, double adaptive_threshold,
+                             int use_prebuilt, uint32_t* seeds, uint64_t* marginals,
+                             uint64_t* round_counters, uint32_t* rounds_done,
+                             uint64_t* covered_total, uint64_t need, bool* aborted);
+}
+
+extern "C" {
+
 rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double adaptive_threshold,
                             int use_prebuilt, uint32_t* seeds, uint64_t* marginals,
                             uint64_t* round_counters, uint32_t* rounds_done,
                             uint64_t* covered_total) {
+  return select_seeds_impl(s, k, adaptive_threshold, use_prebuilt, seeds, marginals,
+                           round_counters, rounds_done, covered_total, 0, nullptr);
+}
+
+}  // extern "C"
+
+namespace rrgpu {
+// select_seeds for the IMM driver's trial rounds (csrc/imm.cpp): stops as soon as
+// the coverage provably cannot reach `need` sets (*aborted = true; seeds and
+// marginals then hold only the rounds done). need == 0: rrg_select_seeds.
+rrg_status select_seeds_until(rrg_store* s, uint32_t k, double adaptive_threshold,
+                              int use_prebuilt, uint32_t* seeds, uint64_t* marginals,
+                              uint64_t* covered_total, uint64_t need, bool* aborted) {
+  return select_seeds_impl(s, k, adaptive_threshold, use_prebuilt, seeds, marginals, nullptr,
+                           nullptr, covered_total, need, aborted);
+}
+}  // namespace rrgpu
+
+namespace {
+rrg_status select_seeds_impl(rrg_store* s, uint32_t k, double adaptive_threshold,
+                             int use_prebuilt, uint32_t* seeds, uint64_t* marginals,
+                             uint64_t* round_counters, uint32_t* rounds_done,
+                             uint64_t* covered_total, uint64_t need, bool* aborted) {
+  if (aborted) *aborted = false;
   if (!s) return invalid("null store");
   rrg_graph* g = s->g;
   if (k < 1) return invalid("select_seeds: k must be >= 1");
@@ -1289,6 +1324,7 @@ rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double adaptive_threshold,
     p.dkn = s->dkn.ptr;
     p.adaptive_threshold = adaptive_threshold;
     p.rebuilds = s->dctl.ptr;
+    p.need = round_counters ? 0 : need;
     launch_select(p, g->num_sms, st);
     uint32_t status[2] = {0, 0};
     std::vector<unsigned long long> marg(k);
@@ -1309,6 +1345,10 @@ rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double adaptive_threshold,
       covered += marg[r];
     }
     if (covered_total) *covered_total = covered;
+    if (status[0] & kSelAborted) {
+      status[0] &= ~kSelAborted;
+      if (aborted) *aborted = true;
+    }
     if (rounds_done) *rounds_done = status[0];
     s->live = s->nsets - covered;  // the store stays tombstoned (imm.hpp:194-195)
     s->sel_mode = scan ? 1 : 2;
@@ -1321,6 +1361,9 @@ rrg_status rrg_select_seeds(rrg_store* s, uint32_t k, double adaptive_threshold,
     return RRG_OK;
   });
 }
+}  // namespace
+
+extern "C" {
 
 rrg_status rrg_fraction_covered(rrg_store* s, const uint32_t* seeds, uint32_t nseeds,
                                 double* out) {

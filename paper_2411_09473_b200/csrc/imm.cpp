@@ -20,6 +20,10 @@ rrg_status exchange_and_append(rrg_store* side, rrg_store* dst, void* comm);
 void nccl_comm_shape(void* comm, int* nranks, int* rank);
 void store_keep_host_offsets(rrg_store* s, bool on);  // capi.cu
 double graph_ic_mean_inspected(const rrg_graph* g);   // capi.cu
+// select_seeds that stops once the coverage provably cannot reach `need` sets
+rrg_status select_seeds_until(rrg_store* s, uint32_t k, double adaptive_threshold,
+                              int use_prebuilt, uint32_t* seeds, uint64_t* marginals,
+                              uint64_t* covered_total, uint64_t need, bool* aborted);  // capi.cu
 }
 
 #ifndef RRG_IMM_FREE_EDGES
@@ -87,6 +91,15 @@ uint64_t set_theta(uint64_t n, uint64_t k, double epsilon, double ell, double lo
   const double theta = std::ceil(lambda_star(n, k, epsilon, ell) / lower_bound);
   if (!(theta >= 1.0)) return 1;
   return static_cast<uint64_t>(theta);
+}
+
+// RRGPU_IMM_EARLY_EXIT=0 runs every trial selection to the end (tests, A/B)
+bool early_exit_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RRGPU_IMM_EARLY_EXIT");
+    return !e || *e != '0';
+  }();
+  return on;
 }
 
 double seconds_since(std::chrono::steady_clock::time_point t) {
@@ -261,13 +274,19 @@ class Driver {
   }
 
   // run_selection (imm.hpp:147-153): the fused strategy uses the fused counter,
-  // the baseline strategy recounts (build_counter) -- same seeds either way
-  rrg_status select(uint32_t* sd, uint64_t* mg, uint64_t* covered) {
+  // the baseline strategy recounts (build_counter) -- same seeds either way.
+  // need > 0 (trial rounds that have a successor): the selection may stop once
+  // its coverage provably stays below `need` sets (*aborted); such a round fails
+  // the trigger test whatever its seeds are, and nothing else of it is used.
+  rrg_status select(uint32_t* sd, uint64_t* mg, uint64_t* covered, uint64_t need = 0,
+                    bool* aborted = nullptr) {
     const auto t = std::chrono::steady_clock::now();
-    const rrg_status s = rrg_select_seeds(store_, cfg_->k, cfg_->adaptive_threshold,
-                                          fused_ ? 1 : 0, sd, mg, nullptr, nullptr, covered);
+    bool ab = false;
+    const rrg_status s = rrgpu::select_seeds_until(store_, cfg_->k, cfg_->adaptive_threshold,
+                                                   fused_ ? 1 : 0, sd, mg, covered, need, &ab);
     t_select += seconds_since(t);
-    if (s == RRG_OK && sd == trial_seeds_.data()) trial_size_ = size_;
+    if (aborted) *aborted = ab;
+    if (s == RRG_OK && !ab && sd == trial_seeds_.data()) trial_size_ = size_;
     return s;
   }
 
@@ -293,11 +312,28 @@ class Driver {
       rrg_status st = top_up(theta_for_round(n_, cfg_->k, cfg_->epsilon, ell_, i), ahead_for(i, rounds));
       if (st != RRG_OK) return st;
       uint64_t covered = 0;
-      st = select(trial_seeds_.data(), trial_marg_.data(), &covered);
+      // the smallest covered count that passes the round's test below (the
+      // expression is monotone in the count): a selection that cannot reach it
+      // is cut short. The last round always runs to the end (its estimate is
+      // the lower bound when no round triggers).
+      const double target = (1.0 + eps_prime) * round_target(n_, i);
+      auto spread_of = [&](uint64_t c) {
+        return static_cast<double>(n_) * (static_cast<double>(c) / static_cast<double>(size_));
+      };
+      uint64_t need = 0;
+      if (i < rounds && early_exit_enabled()) {
+        const double guess = std::ceil(target * static_cast<double>(size_) / static_cast<double>(n_));
+        need = guess >= 1.0 ? (guess < 1.8e19 ? static_cast<uint64_t>(guess) : UINT64_MAX) : 1;
+        while (need > 1 && spread_of(need - 1) >= target) --need;
+        while (need < UINT64_MAX && spread_of(need) < target) ++need;
+      }
+      bool aborted = false;
+      st = select(trial_seeds_.data(), trial_marg_.data(), &covered, need, &aborted);
       if (st != RRG_OK) return st;
+      if (aborted) continue;  // covered < need: the test below fails
       const double fraction = static_cast<double>(covered) / static_cast<double>(size_);
       estimated_spread = static_cast<double>(n_) * fraction;
-      if (estimated_spread >= (1.0 + eps_prime) * round_target(n_, i)) {
+      if (estimated_spread >= target) {
         triggered = true;
         break;
       }

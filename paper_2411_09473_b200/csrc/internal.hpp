@@ -464,7 +464,14 @@ struct SelectParams {
   uint32_t* dkn;               // per round: rows killed
   double adaptive_threshold;   // rebuild_update when top_count / live exceeds it
   unsigned long long* rebuilds;  // rounds that rebuilt (stats)
+  // Early exit for the IMM driver's trial selections: when, at the start of a
+  // round r, covered so far + (k - r) x the round's top count cannot reach
+  // `need` sets, the selection stops (status[0] = r | kSelAborted). Every later
+  // marginal is at most this round's top count (counts only fall), so the final
+  // coverage provably stays below `need`. 0: run all k rounds.
+  unsigned long long need;
 };
+constexpr uint32_t kSelAborted = 0x80000000u;
 constexpr uint32_t kSelTileLog = 11;  // 2048 vertices per argmax tile
 void launch_select(const SelectParams& p, int num_sms, cudaStream_t s);
 // whether the cluster-resident selection may run this store (no dense rows, no

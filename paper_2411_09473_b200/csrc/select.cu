@@ -184,6 +184,10 @@ __global__ void __launch_bounds__(kSelBlock, 1) k_select(const SelectParams p) {
       }
       return;  // uniform: every block computed the same key
     }
+    if (p.need && covered_sum + static_cast<unsigned long long>(p.k - r) * top < p.need) {
+      if (tid == 0) p.status[0] = r | kSelAborted;  // the coverage cannot reach `need`
+      return;  // uniform: same key and covered_sum in every block
+    }
 
     // rebuild_update vs decrement_update (selection.hpp:226-231): the same rule,
     // the same counts either way (test_selection.cpp:116-137)
@@ -443,6 +447,11 @@ __global__ void __launch_bounds__(kClBlock, 1) k_select_cluster(const SelectPara
         p.status[0] = r;
       }
       cl.sync();  // no block leaves while others may still write its shared memory
+      return;
+    }
+    if (p.need && covered_sum + static_cast<unsigned long long>(p.k - r) * top < p.need) {
+      if (tid == 0) p.status[0] = r | kSelAborted;  // the coverage cannot reach `need`
+      cl.sync();
       return;
     }
     const unsigned long long live = p.nsets - covered_sum;

@@ -147,15 +147,19 @@ print(json.dumps(out))
 def test_speculation_settings_never_change_the_result(cuda):
     """The driver samples later rounds' (and the final top-up's) slots ahead when
     they look cheap; the main store only ever receives the reference's slots, so
-    every setting of the two tuning variables must give the same ImmResult."""
+    every setting of the tuning variables must give the same ImmResult -- also
+    with the trial selections cut short once they provably cannot trigger
+    (RRGPU_IMM_EARLY_EXIT)."""
     import json
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     results = []
-    for free, final in (("0", "0"), ("1e15", "1"), ("67108864", "1"), ("1e15", "0")):
-        env = dict(os.environ, RRGPU_IMM_FREE_EDGES=free, RRGPU_IMM_SPEC_FINAL=final)
+    for free, final, early in (("0", "0", "0"), ("1e15", "1", "1"), ("67108864", "1", "1"),
+                               ("1e15", "0", "0"), ("0", "0", "1")):
+        env = dict(os.environ, RRGPU_IMM_FREE_EDGES=free, RRGPU_IMM_SPEC_FINAL=final,
+                   RRGPU_IMM_EARLY_EXIT=early)
         p = subprocess.run([sys.executable, "-c", _SPEC_CHILD, root], env=env, check=True,
                            capture_output=True, text=True, timeout=300)
         results.append(json.loads(p.stdout.strip().splitlines()[-1]))
