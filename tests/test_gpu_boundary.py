@@ -153,3 +153,33 @@ def test_lite_guide_table_then_full_table(cuda, oracle, hint):
     for i in list(range(0, 5000, 97)) + list(range(done - 1000, done, 53)):
         assert np.array_equal(np.sort(mem[off[i]:off[i + 1]]),
                               ref.members[ref.offsets[i]:ref.offsets[i + 1]]), i
+
+
+def test_model_hint_edge_cases(cuda, oracle):
+    """rrg_graph_create_for on degenerate inputs: no vertices, no edges, and an
+    LT graph whose CDF is not monotone (a negative weight: no lite table, the
+    linear scan samples it) -- same behaviour as the plain constructor."""
+    g0 = P.Graph(np.zeros(1, np.uint64), np.zeros(0, np.uint32), np.zeros(0, np.float32), model=1)
+    assert g0.num_vertices == 0
+    with pytest.raises(ValueError):
+        P.generate_batch(g0, 1, 1, 4, P.RRRStore(g0))  # empty graph (sampling.hpp:165)
+    g1 = P.Graph(np.zeros(6, np.uint64), np.zeros(0, np.uint32), np.zeros(0, np.float32), model=1)
+    st = P.RRRStore(g1)
+    P.generate_batch(g1, 1, 3, 50, st)
+    off, mem = st.export()
+    assert (np.diff(off.astype(np.int64)) == 1).all()  # isolated roots (test_sampling.cpp:44-50)
+    rng = np.random.default_rng(5)
+    n, m = 1500, 20000
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    keep = src != dst
+    pairs = np.unique(np.stack([src[keep], dst[keep]]), axis=1)
+    w = rng.uniform(0.0, 0.1, pairs.shape[1]).astype(np.float32)
+    w[::53] = -0.02
+    arrays = P.build_graph(n, pairs[0], pairs[1], w)
+    a = _sets(P.Graph(*arrays), 1, 11, 2000)
+    b = _sets(P.Graph(*arrays, model=1), 1, 11, 2000)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    ref = oracle.graph(*arrays).sample(1, 11, 0, 2000, workers=2)
+    assert np.array_equal(a[2], ref.counter)
