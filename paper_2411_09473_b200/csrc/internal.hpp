@@ -158,8 +158,11 @@ struct rrg_graph {
   uint32_t ic_warp_budget = 0;   // IC: warp-schedule windows per set before the block pass (0: off)
   double ic_mean_insp = -1.0;    // IC: running mean of inspected in-edges per set
   double ic_hub_insp = 1e5;       // auto: warp per sample from this mean on (cfg5 ~1M)
-  double ic_cta_max_edges = 1.5e8;  // auto: block per sample up to this many expected
-                                    // inspected edges per batch (cfg1 IMM, cfg3 65K)
+  double ic_cta_max_edges = 1.0e8;  // auto: block per sample up to this many expected
+                                    // inspected edges per batch (cfg1: the block schedule
+                                    // wins up to ~18K sets = 1e8 edges -- 16,631 sets 6.65 vs
+                                    // 7.2 ms -- the warp schedule beyond -- 21,899 sets 7.5
+                                    // vs 8.0 ms, 66,523 sets 12.9 vs 20.5 ms)
   double ic_warp_min_insp = 1024.0;  // auto: warp per sample from this mean on (cfg1 5.5K
                                      // and cfg5 986K run faster per warp; cfg3 237 per lane)
   bool rec_ready = false;
