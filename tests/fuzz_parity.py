@@ -3,22 +3,31 @@ the port): random graphs (sizes, degree skew, weight scales incl. hub in-lists
 past the warp-per-list thresholds), both models, random seeds / k / batch sizes,
 plain and model-hinted graph creation, device-built graphs (LT normalization),
 generate_batch + select_seeds + run_imm. Prints one line per case; exits non-zero
-at the first mismatch.   usage: python tools/fuzz_parity.py [seconds=240] [seed=1]"""
+at the first mismatch. tests/test_gpu_fuzz.py runs a bounded number of cases;
+longer sweeps: python tests/fuzz_parity.py [seconds=240] [seed=1]"""
 import sys
 import time
 
-sys.path.insert(0, ".")
+import os  # noqa: E402
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import paper_2411_09473_b200 as P  # noqa: E402
 from oracle import Oracle, available  # noqa: E402
 
-budget = float(sys.argv[1]) if len(sys.argv) > 1 else 240.0
-rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
-orc = Oracle("reference" if available("reference") else "port")
-t_end = time.time() + budget
-case = 0
-while time.time() < t_end:
-    case += 1
+
+def run(budget=240.0, seed=1, max_cases=None, verbose=True):
+    rng = np.random.default_rng(seed)
+    orc = Oracle("reference" if available("reference") else "port")
+    t_end = time.time() + budget
+    case = 0
+    while time.time() < t_end and (max_cases is None or case < max_cases):
+        case += 1
+        one_case(rng, orc, case, verbose)
+    return case, orc.kind
+
+
+def one_case(rng, orc, case, verbose):
     n = int(rng.choice([50, 400, 3000, 20000]))
     m = int(n * rng.choice([2, 8, 30]))
     hubs = int(rng.integers(0, 4))
@@ -77,9 +86,14 @@ while time.time() < t_end:
     assert r.seeds.seeds == rr["seeds"] and r.seeds.marginal_counts == rr["marginals"], "imm seeds"
     assert (r.theta, r.theta_prime, r.lower_bound, r.sets_generated) == \
         (rr["theta"], rr["theta_prime"], rr["lower_bound"], rr["sets_generated"]), "imm theta"
-    print(f"case {case}: n {n} m {src.size} hubs {hubs} model {model} scale {scale} "
-          f"{'device-built ' if device_built else ''}count {count} k {k} eps {eps} "
-          f"theta {r.theta} ok", flush=True)
+    if verbose:
+        print(f"case {case}: n {n} m {src.size} hubs {hubs} model {model} scale {scale} "
+              f"{'device-built ' if device_built else ''}count {count} k {k} eps {eps} "
+              f"theta {r.theta} ok", flush=True)
     st.close()
     g.close()
-print(f"{case} cases ok ({orc.kind} checker)")
+
+if __name__ == "__main__":
+    n_cases, kind = run(float(sys.argv[1]) if len(sys.argv) > 1 else 240.0,
+                        int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+    print(f"{n_cases} cases ok ({kind} checker)")
