@@ -189,26 +189,60 @@ class Driver {
     return s;
   }
 
+  rrg_status ensure_ahead() {
+    if (ahead_.s) return RRG_OK;
+    const rrg_status s = rrg_store_create(g_, &ahead_.s);
+    if (s == RRG_OK) rrgpu::store_keep_host_offsets(ahead_.s, true);  // appends need no read-back
+    return s;
+  }
+
+  // A graph that has not sampled IC yet has no mean-inspected-edges estimate, so
+  // its first top-up could not tell which later rounds are free to sample along
+  // (ahead_for). Its first slots go out as a small pilot batch -- the sampler
+  // splits a fresh graph's first batch at 2,048 sets anyway, to choose its
+  // schedule -- and the first top-up then extends the side store knowing the
+  // mean: cfg3 from host arrays samples 2,048 + 90,456 sets instead of 2,048 +
+  // 21,078 + 69,378.
+  rrg_status prime() {
+    if (cfg_->model != RRG_IC || comm_ || sim_ranks_ > 0) return RRG_OK;
+    if (rrgpu::graph_ic_mean_inspected(g_) >= 0.0) return RRG_OK;
+    const auto t = std::chrono::steady_clock::now();
+    rrg_status s = ensure_ahead();
+    if (s != RRG_OK) return s;
+    const uint64_t pilot =
+        std::min<uint64_t>(2048, theta_for_round(n_, cfg_->k, cfg_->epsilon, ell_, 1));
+    uint64_t made = 0;
+    s = rrg_generate_slots(g_, static_cast<rrg_model>(cfg_->model), cfg_->rng_seed, 0, pilot,
+                           ahead_.s, fused_ ? 1 : 0, 64, &made);
+    ahead_first_ = 0;
+    ahead_count_ = made;
+    t_generate += seconds_since(t);
+    return s;
+  }
+
   rrg_status top_up(uint64_t target, uint64_t ahead) {
     if (target <= size_) return RRG_OK;
     if (comm_ || sim_ranks_ > 0) return top_up_sharded(target);
     const auto t = std::chrono::steady_clock::now();
     rrg_status s = RRG_OK;
-    const bool covered = ahead_count_ && ahead_first_ <= size_ && target <= ahead_first_ + ahead_count_;
+    const uint64_t have_end = ahead_first_ + ahead_count_;
+    const bool covered = ahead_count_ && ahead_first_ <= size_ && target <= have_end;
     if (!covered) {
-      if (!ahead_.s) {
-        s = rrg_store_create(g_, &ahead_.s);
-        if (s != RRG_OK) return s;
-        rrgpu::store_keep_host_offsets(ahead_.s, true);  // appends need no read-back
-      } else {
+      s = ensure_ahead();
+      if (s != RRG_OK) return s;
+      // the side store is extended when it still holds uncommitted slots from
+      // size_ on (the pilot batch of a fresh graph), else restarted at size_
+      const bool extend = ahead_count_ && ahead_first_ <= size_ && size_ < have_end;
+      if (!extend) {
         rrg_store_clear(ahead_.s);
+        ahead_first_ = size_;
+        ahead_count_ = 0;
       }
-      const uint64_t want = std::max(target, ahead) - size_;
+      const uint64_t from = ahead_first_ + ahead_count_;
       uint64_t made = 0;
-      s = rrg_generate_slots(g_, static_cast<rrg_model>(cfg_->model), cfg_->rng_seed, size_, want,
-                             ahead_.s, fused_ ? 1 : 0, 64, &made);
-      ahead_first_ = size_;
-      ahead_count_ = made;
+      s = rrg_generate_slots(g_, static_cast<rrg_model>(cfg_->model), cfg_->rng_seed, from,
+                             std::max(target, ahead) - from, ahead_.s, fused_ ? 1 : 0, 64, &made);
+      ahead_count_ += made;
       if (s != RRG_OK) {
         t_generate += seconds_since(t);
         return s;
@@ -308,6 +342,8 @@ class Driver {
     const unsigned rounds = sampling_rounds(n_);
     double estimated_spread = 0.0;
     bool triggered = false;
+    const rrg_status primed = prime();
+    if (primed != RRG_OK) return primed;
     for (unsigned i = 1; i <= rounds; ++i) {
       rrg_status st = top_up(theta_for_round(n_, cfg_->k, cfg_->epsilon, ell_, i), ahead_for(i, rounds));
       if (st != RRG_OK) return st;
