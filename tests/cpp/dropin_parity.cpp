@@ -70,6 +70,15 @@ int main() {
     gc.rng_seed = 5;
     const rrgpu::ImmResult got = rrgpu::run_imm(dg, gc);
 
+    {  // the same graph created with the model hint (rrg_graph_create_for): same result
+      rrgpu::Graph dh(g.num_vertices, g.reverse_offsets, g.reverse_sources, g.reverse_weights,
+                      to_gpu(c.model));
+      const rrgpu::ImmResult hinted = rrgpu::run_imm(dh, gc);
+      expect(hinted.seeds.seeds == got.seeds.seeds &&
+                 hinted.seeds.marginal_counts == got.seeds.marginal_counts &&
+                 hinted.theta == got.theta && hinted.lower_bound == got.lower_bound,
+             "run_imm on a model-hinted graph", id);
+    }
     expect(ref.seeds.seeds == got.seeds.seeds, "run_imm seeds", id);
     expect(ref.seeds.marginal_counts == got.seeds.marginal_counts, "run_imm marginals", id);
     expect(ref.theta == got.theta && ref.theta_prime == got.theta_prime, "theta, theta'", id);
